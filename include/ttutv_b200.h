@@ -1,0 +1,152 @@
+/*
+ * ttutv_b200.h -- C-ABI of the B200-native TT-UTV engine.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no C++ or
+ * torch types. The C++ API in include/ttutv_b200/ttutv.hpp (namespace ttutv, the same
+ * names and signatures as the reference's include/ttutv/*.hpp) is a thin layer over
+ * these entry points, and any FFI (ctypes, cgo, JNI) can bind them directly
+ * (see INTEGRATION.md).
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/proj):
+ *   ttg_decompose          <- decompose()                 include/ttutv/tt_decomp.hpp:100
+ *                             and the seven named sweeps   include/ttutv/tt_decomp.hpp:69-97
+ *   ttg_verify_bound       <- verify_bound()              include/ttutv/tt_decomp.hpp:105
+ *   ttg_qr_col_pivot       <- qr_col_pivot()              include/ttutv/factor.hpp:19
+ *   ttg_svd                <- svd()                       include/ttutv/factor.hpp:35
+ *   ttg_utv                <- ulv() / urv()               include/ttutv/factor.hpp:56-57
+ *   ttg_truncate           <- truncate_fixed_rank/tol()   include/ttutv/factor.hpp:73-82
+ *   ttg_reconstruct        <- reconstruct()               include/ttutv/tt.hpp:60
+ *   ttg_frobenius_norm     <- frobenius_norm()            include/ttutv/tensor_ops.hpp:26
+ *   ttg_rse                <- rse()                       include/ttutv/tensor_ops.hpp:30
+ *
+ * Storage conventions are the reference's: matrices are column-major
+ * ((i,j) -> data[i + j*rows], include/ttutv/matrix.hpp:36), tensors are flat with the
+ * first index fastest (include/ttutv/dense_tensor.hpp:13-15), cores are
+ * (r_{k-1}, I_k, r_k) tensors in the same order, perms are 0-based int64 source columns.
+ *
+ * Error convention: every call returns a ttg_status. Codes 1..6 correspond 1:1 to the
+ * reference exception classes (include/ttutv/errors.hpp:10-54); the message is available
+ * from ttg_last_error() on the calling thread. The C++ layer rethrows the matching class.
+ *
+ * Threading: calls are reentrant; each host thread gets its own CUDA stream on the
+ * current device. Results are bitwise deterministic for a given input and device.
+ */
+#ifndef TTUTV_B200_H
+#define TTUTV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ttg_status {
+    TTG_OK = 0,
+    TTG_ERR_ARGUMENT = 1,  /* ttutv::ArgumentError  */
+    TTG_ERR_INDEX = 2,     /* ttutv::IndexError     */
+    TTG_ERR_PARSE = 3,     /* ttutv::ParseError     */
+    TTG_ERR_NUMERICAL = 4, /* ttutv::NumericalError */
+    TTG_ERR_RESOURCE = 5,  /* ttutv::ResourceError  */
+    TTG_ERR_INVARIANT = 6, /* ttutv::InvariantError */
+    TTG_ERR_INTERNAL = 7,  /* any other ttutv::Error */
+    TTG_ERR_CUDA = 8       /* CUDA runtime failure (no reference analogue; maps to Error) */
+} ttg_status;
+
+enum { TTG_METHOD_SVD = 0, TTG_METHOD_ULV = 1, TTG_METHOD_URV = 2 };
+enum { TTG_SWEEP_L2R = 0, TTG_SWEEP_R2L = 1 };
+enum { TTG_RETAIN_L11_ONLY = 0, TTG_RETAIN_FULL_COLUMN = 1 };
+enum { TTG_BOUND_RSS = 0, TTG_BOUND_PLAIN_SUM = 1 };
+/* QLP policy. EARLY_EXIT (default) stops each pivoted pass as soon as the kept block is
+ * provably the one the full factorisation would produce;
+ * FULL runs all p = min(m,n) steps of both passes exactly as the reference does. */
+enum { TTG_QLP_EARLY_EXIT = 0, TTG_QLP_FULL = 1 };
+
+/* Mirrors DecompConfig + FixedRank/FixedTol (tt_decomp.hpp:24-45). */
+typedef struct ttg_config {
+    int method;            /* TTG_METHOD_* */
+    int sweep;             /* TTG_SWEEP_*  */
+    int fixed_rank;        /* nonzero: ranks[0..d] used; zero: eps + weights */
+    const int64_t* ranks;  /* rank chain (r_0..r_d) when fixed_rank */
+    int nranks;            /* its length; validated against d+1 like FixedRank */
+    double eps;            /* relative tolerance when !fixed_rank */
+    const double* weights; /* may be NULL when nweights == 0 (equal split) */
+    int nweights;
+    int refine_passes;     /* default 1 */
+    int retain;            /* TTG_RETAIN_*, right-to-left ULV only */
+    int debug_checks;
+    int qlp_policy;        /* TTG_QLP_* */
+} ttg_config;
+
+typedef struct ttg_result ttg_result; /* opaque; owns device and host buffers */
+
+/* ---- library / device ------------------------------------------------------- */
+const char* ttg_last_error(void);
+int ttg_abi_version(void);
+int ttg_device_count(void);
+ttg_status ttg_set_device(int device);
+/* Number of CUDA kernels this thread has launched (monotone counter; for bench/tests). */
+int64_t ttg_kernel_launches(void);
+ttg_status ttg_synchronize(void);
+
+/* ---- tensor-train sweeps ---------------------------------------------------- */
+/* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`
+ * is a host pointer (copied in, timed in the report) or a device pointer (read in place). */
+ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_config* cfg,
+                         int a_on_device, ttg_result** out);
+void ttg_result_free(ttg_result* res);
+int ttg_result_order(const ttg_result* res);
+void ttg_result_core_dims(const ttg_result* res, int k, int64_t dims3[3]); /* k is 0-based */
+ttg_status ttg_result_core_copy(const ttg_result* res, int k, double* host_out);
+const double* ttg_result_core_device(const ttg_result* res, int k);
+/* step_errors: d-1 (unfolding order); ranks_chosen: d+1; ranks_requested: d+1 or 0.
+ * Returns the number of ranks_requested entries written (0 for tolerance mode). */
+int ttg_result_report(const ttg_result* res, double* step_errors, int64_t* ranks_chosen,
+                      int64_t* ranks_requested, double* bound, int* bound_kind,
+                      double* input_norm, double* wall_time_ms);
+int ttg_result_warning_count(const ttg_result* res);
+const char* ttg_result_warning(const ttg_result* res, int i);
+/* Per-cut diagnostics (cut = 0..d-2 in unfolding order):
+ *   diag: |T_ii| of the kept block, i < r (the "per-unfolding diagonal estimates"),
+ *   info[0] pivoted steps run in pass 1, info[1] p = min(m,n), info[2] rank kept,
+ *   info[3] early-exit extensions, info[4..5] m, n of the cut matrix.
+ * Returns the number of diag entries written (<= max). */
+int ttg_result_cut_diag(const ttg_result* res, int cut, double* diag, int max, int64_t info[6]);
+
+/* achieved = |A - reconstruct(tt)|_F computed on device (reconstruct fused with the
+ * difference norm). Throws (returns) TTG_ERR_INVARIANT when achieved exceeds
+ * bound + slack_rel * |A|_F, like verify_bound (tt_decomp.cpp:445-462). */
+ttg_status ttg_verify_bound(const double* a, int a_on_device, const ttg_result* res,
+                            double slack_rel, double* achieved);
+/* |A - reconstruct(tt)|_F / |A|_F on device (no element cap: Â is never materialised). */
+ttg_status ttg_result_rse(const ttg_result* res, const double* a, int a_on_device, double* rse);
+
+/* ---- factor level (host buffers, column-major) ------------------------------ */
+/* q: m x p, r: p x n, perm: n. Any of the outputs may be NULL. */
+ttg_status ttg_qr_col_pivot(const double* a, int64_t m, int64_t n, double* q, double* r,
+                            int64_t* perm);
+/* lower != 0: ULV (t lower-triangular), else URV. u: m x p, t: p x p, v: n x p. */
+ttg_status ttg_utv(const double* a, int64_t m, int64_t n, int lower, int refine_passes,
+                   double* u, double* t, double* v);
+/* Economy SVD (one-sided Jacobi on the p x p triangle of a pivoted QR). u: m x p, s: p,
+ * v: n x p. max_sweeps / pair_tol as SvdOptions (factor.hpp:30-33). */
+ttg_status ttg_svd(const double* a, int64_t m, int64_t n, int max_sweeps, double pair_tol,
+                   double* u, double* s, double* v);
+/* kind: 0 svd (t is diag(s) given as the p-vector s), 1 ulv, 2 urv.
+ * rank > 0: fixed rank; rank == 0: tolerance eps. Outputs u1 m x r, t11 r x r, v1 n x r
+ * (caller sizes them for r = p). */
+ttg_status ttg_truncate(int kind, const double* u, const double* t, const double* v, int64_t m,
+                        int64_t n, int64_t p, int64_t rank, double eps, int64_t* rank_out,
+                        double* residual, double* u1, double* t11, double* v1);
+
+/* ---- tensor ops ------------------------------------------------------------- */
+/* cores: concatenated (r_{k-1}, I_k, r_k) blocks; ranks: d+1; dims: d. out: prod(dims). */
+ttg_status ttg_reconstruct(const double* cores, const int64_t* dims, const int64_t* ranks, int d,
+                           int64_t element_cap, double* out);
+ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, double* out);
+ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTUTV_B200_H */

@@ -1,0 +1,284 @@
+// TEST INFRASTRUCTURE ONLY (oracle/). Never linked into the product.
+//
+// A C-ABI veneer over the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src by oracle/build_ref.sh into oracle/_ref/). It lets
+// the Python test-suite, the golden-fixture generator and bench.py's
+// `--impl reference` arm drive the reference's own public API
+// (include/ttutv/{tt_decomp,factor,generators,tt,tensor_ops,kernels}.hpp)
+// through ctypes. Only plain pointers and sizes cross this boundary.
+//
+// Error convention: every entry point returns 0 on success or the code of the
+// reference exception class (same numbering as include/ttutv_b200.h):
+//   1 ArgumentError 2 IndexError 3 ParseError 4 NumericalError
+//   5 ResourceError 6 InvariantError 7 other ttutv::Error / std::exception
+// and the message is available from ref_last_error().
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ttutv/errors.hpp"
+#include "ttutv/factor.hpp"
+#include "ttutv/generators.hpp"
+#include "ttutv/kernels.hpp"
+#include "ttutv/tensor_ops.hpp"
+#include "ttutv/tt.hpp"
+#include "ttutv/tt_decomp.hpp"
+
+namespace {
+
+thread_local std::string g_msg;
+
+template <class F>
+int guarded(F&& body) {
+    try {
+        body();
+        g_msg.clear();
+        return 0;
+    } catch (const ttutv::ArgumentError& e) {
+        g_msg = e.what();
+        return 1;
+    } catch (const ttutv::IndexError& e) {
+        g_msg = e.what();
+        return 2;
+    } catch (const ttutv::ParseError& e) {
+        g_msg = e.what();
+        return 3;
+    } catch (const ttutv::NumericalError& e) {
+        g_msg = e.what();
+        return 4;
+    } catch (const ttutv::ResourceError& e) {
+        g_msg = e.what();
+        return 5;
+    } catch (const ttutv::InvariantError& e) {
+        g_msg = e.what();
+        return 6;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return 7;
+    }
+}
+
+ttutv::Shape shape_of(const int64_t* dims, int d) {
+    return ttutv::Shape(std::vector<std::int64_t>(dims, dims + d));
+}
+
+ttutv::DenseTensor tensor_of(const double* a, const int64_t* dims, int d) {
+    ttutv::Shape s = shape_of(dims, d);
+    std::vector<double> buf(a, a + s.element_count());
+    return ttutv::DenseTensor(std::move(s), std::move(buf));
+}
+
+ttutv::Matrix matrix_of(const double* a, int64_t m, int64_t n) {
+    return ttutv::Matrix(m, n, std::vector<double>(a, a + m * n));
+}
+
+void put(const ttutv::Matrix& x, double* out) {
+    if (out) std::memcpy(out, x.data(), sizeof(double) * static_cast<size_t>(x.size()));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_msg.c_str(); }
+
+void ref_set_parallel(int enabled) { ttutv::kernels::set_parallel_enabled(enabled != 0); }
+
+// ---- decompositions -------------------------------------------------------
+
+// method: 0 svd, 1 ulv, 2 urv; sweep: 0 l2r, 1 r2l; retain: 0 l11_only, 1 full_column
+// fixed_rank != 0 -> ranks[0..d] used; else eps + weights (nweights may be 0).
+int ref_decompose(const double* a, const int64_t* dims, int d, int method, int sweep,
+                  int fixed_rank, const int64_t* ranks, double eps, const double* weights,
+                  int nweights, int refine, int retain, int debug_checks, void** handle) {
+    *handle = nullptr;
+    return guarded([&] {
+        ttutv::DecompConfig cfg;
+        cfg.method = static_cast<ttutv::Method>(method);
+        cfg.sweep = static_cast<ttutv::Sweep>(sweep);
+        cfg.refine_passes = refine;
+        cfg.retain = static_cast<ttutv::Retain>(retain);
+        cfg.debug_checks = debug_checks != 0;
+        if (fixed_rank)
+            cfg.mode = ttutv::FixedRank{std::vector<std::int64_t>(ranks, ranks + d + 1)};
+        else
+            cfg.mode = ttutv::FixedTol{eps, std::vector<double>(weights, weights + nweights)};
+        auto* res = new ttutv::DecompResult(ttutv::decompose(tensor_of(a, dims, d), cfg));
+        *handle = res;
+    });
+}
+
+void ref_result_free(void* h) { delete static_cast<ttutv::DecompResult*>(h); }
+
+int ref_result_order(void* h) {
+    return static_cast<int>(static_cast<ttutv::DecompResult*>(h)->tt.order());
+}
+
+void ref_result_core_dims(void* h, int k, int64_t* out3) {
+    const auto& c = static_cast<ttutv::DecompResult*>(h)->tt.cores()[static_cast<size_t>(k)];
+    out3[0] = c.rank_left();
+    out3[1] = c.mode_dim();
+    out3[2] = c.rank_right();
+}
+
+void ref_result_core_copy(void* h, int k, double* out) {
+    const auto& c = static_cast<ttutv::DecompResult*>(h)->tt.cores()[static_cast<size_t>(k)];
+    std::memcpy(out, c.data.data(), sizeof(double) * static_cast<size_t>(c.data.element_count()));
+}
+
+// step_errors: d-1 entries; ranks_chosen: d+1; returns number of warnings.
+int ref_result_report(void* h, double* step_errors, int64_t* ranks_chosen, double* bound,
+                      int* bound_kind, double* input_norm, double* wall_ms) {
+    const auto& r = static_cast<ttutv::DecompResult*>(h)->report;
+    for (size_t i = 0; i < r.step_errors.size(); ++i) step_errors[i] = r.step_errors[i];
+    for (size_t i = 0; i < r.ranks_chosen.size(); ++i) ranks_chosen[i] = r.ranks_chosen[i];
+    *bound = r.bound;
+    *bound_kind = r.bound_kind == ttutv::BoundKind::root_sum_square ? 0 : 1;
+    *input_norm = r.input_norm;
+    *wall_ms = r.wall_time_ms;
+    return static_cast<int>(r.warnings.size());
+}
+
+const char* ref_result_warning(void* h, int i) {
+    return static_cast<ttutv::DecompResult*>(h)->report.warnings[static_cast<size_t>(i)].c_str();
+}
+
+// RSE of the train in `h` against the dense tensor a (reference reconstruct + rse).
+int ref_result_rse(void* h, const double* a, const int64_t* dims, int d, int64_t cap,
+                   double* out) {
+    return guarded([&] {
+        const auto* res = static_cast<ttutv::DecompResult*>(h);
+        *out = ttutv::rse(ttutv::reconstruct(res->tt, cap), tensor_of(a, dims, d));
+    });
+}
+
+int ref_result_reconstruct(void* h, int64_t cap, double* out) {
+    return guarded([&] {
+        const auto* res = static_cast<ttutv::DecompResult*>(h);
+        ttutv::DenseTensor x = ttutv::reconstruct(res->tt, cap);
+        std::memcpy(out, x.data(), sizeof(double) * static_cast<size_t>(x.element_count()));
+    });
+}
+
+// ---- factorizations -------------------------------------------------------
+
+int ref_qr_col_pivot(const double* a, int64_t m, int64_t n, double* q, double* r,
+                     int64_t* perm) {
+    return guarded([&] {
+        ttutv::QrPivotResult f = ttutv::qr_col_pivot(matrix_of(a, m, n));
+        put(f.q, q);
+        put(f.r, r);
+        if (perm) std::memcpy(perm, f.perm.data(), sizeof(int64_t) * f.perm.size());
+    });
+}
+
+// lower != 0 -> ulv (t lower), else urv (t upper). u: m x p, t: p x p, v: n x p.
+int ref_utv(const double* a, int64_t m, int64_t n, int lower, int refine, double* u, double* t,
+            double* v) {
+    return guarded([&] {
+        if (lower) {
+            ttutv::UlvFactors f = ttutv::ulv(matrix_of(a, m, n), refine);
+            put(f.u, u);
+            put(f.l, t);
+            put(f.v, v);
+        } else {
+            ttutv::UrvFactors f = ttutv::urv(matrix_of(a, m, n), refine);
+            put(f.u, u);
+            put(f.r, t);
+            put(f.v, v);
+        }
+    });
+}
+
+// u: m x p, s: p, v: n x p
+int ref_svd(const double* a, int64_t m, int64_t n, double* u, double* s, double* v) {
+    return guarded([&] {
+        ttutv::SvdResult f = ttutv::svd(matrix_of(a, m, n));
+        put(f.u, u);
+        put(f.v, v);
+        std::memcpy(s, f.s.data(), sizeof(double) * f.s.size());
+    });
+}
+
+// kind: 0 svd (t = diag s as p x p), 1 ulv, 2 urv. Truncation from full factors.
+// fixed: rank >= 1 used; else eps. Outputs u1 (m x r), t11 (r x r), v1 (n x r).
+int ref_truncate(int kind, const double* u, const double* t, const double* v, int64_t m,
+                 int64_t n, int64_t p, int64_t rank, double eps, int64_t* rank_out,
+                 double* residual, double* u1, double* t11, double* v1) {
+    return guarded([&] {
+        ttutv::TruncatedFactorization tf;
+        ttutv::Matrix U = matrix_of(u, m, p), V = matrix_of(v, n, p);
+        if (kind == 0) {
+            ttutv::SvdResult f{U, {}, V};
+            for (int64_t i = 0; i < p; ++i) f.s.push_back(t[i + i * p]);
+            tf = rank > 0 ? ttutv::truncate_fixed_rank(f, rank) : ttutv::truncate_fixed_tol(f, eps);
+        } else if (kind == 1) {
+            ttutv::UlvFactors f{U, matrix_of(t, p, p), V};
+            tf = rank > 0 ? ttutv::truncate_fixed_rank(f, rank) : ttutv::truncate_fixed_tol(f, eps);
+        } else {
+            ttutv::UrvFactors f{U, matrix_of(t, p, p), V};
+            tf = rank > 0 ? ttutv::truncate_fixed_rank(f, rank) : ttutv::truncate_fixed_tol(f, eps);
+        }
+        *rank_out = tf.rank;
+        *residual = tf.residual_norm;
+        put(tf.u1, u1);
+        put(tf.t11, t11);
+        put(tf.v1, v1);
+    });
+}
+
+// ---- generators and tensor ops -------------------------------------------
+
+int ref_gen_gaussian(const int64_t* dims, int d, uint64_t seed, double* out) {
+    return guarded([&] {
+        ttutv::DenseTensor x = ttutv::gen_gaussian(shape_of(dims, d), seed);
+        std::memcpy(out, x.data(), sizeof(double) * static_cast<size_t>(x.element_count()));
+    });
+}
+
+int ref_gen_hilbert(const int64_t* dims, int d, double* out) {
+    return guarded([&] {
+        ttutv::DenseTensor x = ttutv::gen_hilbert(shape_of(dims, d));
+        std::memcpy(out, x.data(), sizeof(double) * static_cast<size_t>(x.element_count()));
+    });
+}
+
+// Dense reconstruction of gen_planted_tt(shape, ranks, seed).
+int ref_gen_planted_dense(const int64_t* dims, int d, const int64_t* ranks, uint64_t seed,
+                          int64_t cap, double* out) {
+    return guarded([&] {
+        ttutv::TTTensor tt = ttutv::gen_planted_tt(
+            shape_of(dims, d), std::vector<std::int64_t>(ranks, ranks + d + 1), seed);
+        ttutv::DenseTensor x = ttutv::reconstruct(tt, cap);
+        std::memcpy(out, x.data(), sizeof(double) * static_cast<size_t>(x.element_count()));
+    });
+}
+
+// Raw cores of gen_planted_tt, concatenated in core order.
+int ref_gen_planted_cores(const int64_t* dims, int d, const int64_t* ranks, uint64_t seed,
+                          double* out) {
+    return guarded([&] {
+        ttutv::TTTensor tt = ttutv::gen_planted_tt(
+            shape_of(dims, d), std::vector<std::int64_t>(ranks, ranks + d + 1), seed);
+        for (const auto& c : tt.cores()) {
+            std::memcpy(out, c.data.data(), sizeof(double) * static_cast<size_t>(c.data.element_count()));
+            out += c.data.element_count();
+        }
+    });
+}
+
+double ref_frobenius_norm(const double* a, int64_t count) {
+    const int64_t dims[1] = {count};
+    return ttutv::frobenius_norm(tensor_of(a, dims, 1));
+}
+
+uint64_t ref_rng_u64(uint64_t seed, int64_t skip) {
+    ttutv::Rng rng(seed);
+    for (int64_t i = 0; i < skip; ++i) rng.next_u64();
+    return rng.next_u64();
+}
+
+}  // extern "C"

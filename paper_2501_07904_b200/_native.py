@@ -1,0 +1,122 @@
+"""ctypes binding of the C-ABI in include/ttutv_b200.h.
+
+The library is loaded from the in-tree build (``lib/libttutv_b200.so``). There is no
+fallback: if the library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libttutv_b200.so"
+
+c_double_p = C.POINTER(C.c_double)
+c_int64_p = C.POINTER(C.c_int64)
+
+
+class TTUTVError(RuntimeError):
+    """Base of all library errors (reference ttutv::Error, errors.hpp:10)."""
+
+
+class ArgumentError(TTUTVError):
+    pass
+
+
+class TTIndexError(TTUTVError):
+    pass
+
+
+class ParseError(TTUTVError):
+    pass
+
+
+class NumericalError(TTUTVError):
+    pass
+
+
+class ResourceError(TTUTVError):
+    pass
+
+
+class InvariantError(TTUTVError):
+    pass
+
+
+class CudaError(TTUTVError):
+    pass
+
+
+ERRORS = {1: ArgumentError, 2: TTIndexError, 3: ParseError, 4: NumericalError, 5: ResourceError,
+          6: InvariantError, 7: TTUTVError, 8: CudaError}
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("method", C.c_int), ("sweep", C.c_int), ("fixed_rank", C.c_int),
+        ("ranks", c_int64_p), ("nranks", C.c_int), ("eps", C.c_double), ("weights", c_double_p),
+        ("nweights", C.c_int), ("refine_passes", C.c_int), ("retain", C.c_int),
+        ("debug_checks", C.c_int), ("qlp_policy", C.c_int),
+    ]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "ttg_last_error": (C.c_char_p, []),
+    "ttg_abi_version": (C.c_int, []),
+    "ttg_device_count": (C.c_int, []),
+    "ttg_set_device": (C.c_int, [C.c_int]),
+    "ttg_kernel_launches": (C.c_int64, []),
+    "ttg_synchronize": (C.c_int, []),
+    "ttg_decompose": (C.c_int, [C.c_void_p, c_int64_p, C.c_int, C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_result_free": (None, [C.c_void_p]),
+    "ttg_result_order": (C.c_int, [C.c_void_p]),
+    "ttg_result_core_dims": (None, [C.c_void_p, C.c_int, c_int64_p]),
+    "ttg_result_core_copy": (C.c_int, [C.c_void_p, C.c_int, c_double_p]),
+    "ttg_result_core_device": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "ttg_result_report": (C.c_int, [C.c_void_p, c_double_p, c_int64_p, c_int64_p, c_double_p,
+                                    C.POINTER(C.c_int), c_double_p, c_double_p]),
+    "ttg_result_warning_count": (C.c_int, [C.c_void_p]),
+    "ttg_result_warning": (C.c_char_p, [C.c_void_p, C.c_int]),
+    "ttg_result_cut_diag": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int, c_int64_p]),
+    "ttg_verify_bound": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, c_double_p]),
+    "ttg_result_rse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, c_double_p]),
+    "ttg_qr_col_pivot": (C.c_int, [c_double_p, C.c_int64, C.c_int64, c_double_p, c_double_p, c_int64_p]),
+    "ttg_utv": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]),
+    "ttg_svd": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_double, c_double_p, c_double_p,
+                          c_double_p]),
+    "ttg_truncate": (C.c_int, [C.c_int, c_double_p, c_double_p, c_double_p, C.c_int64, C.c_int64, C.c_int64,
+                               C.c_int64, C.c_double, c_int64_p, c_double_p, c_double_p, c_double_p,
+                               c_double_p]),
+    "ttg_reconstruct": (C.c_int, [c_double_p, c_int64_p, c_int64_p, C.c_int, C.c_int64, c_double_p]),
+    "ttg_frobenius_norm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, c_double_p]),
+    "ttg_rse": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the native library; raises if it is not built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"native engine not built: {LIB_PATH} missing (run __graft_entry__.build())")
+        handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().ttg_last_error().decode(errors="replace")
+        raise ERRORS.get(status, TTUTVError)(msg)
+
+
+def require_gpu() -> None:
+    if lib().ttg_device_count() < 1:
+        raise CudaError("no CUDA device visible: the TT-UTV engine has no CPU path")

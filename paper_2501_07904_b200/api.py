@@ -1,0 +1,235 @@
+"""Python mirror of the reference's public API (include/ttutv/tt_decomp.hpp, factor.hpp,
+tt.hpp), implemented on the device through the C-ABI. Names, argument meaning and error
+classes follow the reference so tests read like its own.
+
+Tensors are numpy float64 arrays; an n-d array is taken in the reference's storage order
+(first index fastest, i.e. numpy order='F'); a flat array needs ``dims``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._native import Config, check, lib, require_gpu, c_double_p, c_int64_p
+
+METHODS = {"svd": 0, "ulv": 1, "urv": 2}
+SWEEPS = {"l2r": 0, "left_to_right": 0, "r2l": 1, "right_to_left": 1}
+RETAIN = {"l11_only": 0, "full_column": 1}
+QLP = {"early_exit": 0, "full": 1}
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(c_double_p)
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(c_int64_p)
+
+
+def _flat(a, dims):
+    a = np.asarray(a, dtype=np.float64)
+    if dims is None:
+        dims = a.shape
+        a = a.ravel(order="F")
+    a = np.ascontiguousarray(a.reshape(-1))
+    dims = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    return a, dims
+
+
+@dataclass
+class DecompReport:
+    """Mirror of DecompReport (tt_decomp.hpp:49-61) plus per-cut device diagnostics."""
+    step_errors: list
+    ranks_requested: list
+    ranks_chosen: list
+    bound: float
+    bound_kind: str
+    input_norm: float
+    wall_time_ms: float
+    warnings: list
+    achieved_error: Optional[float] = None
+    cuts: list = field(default_factory=list)  # dicts: steps, p, rank, extensions, m, n, diag
+
+
+@dataclass
+class DecompResult:
+    cores: list  # (r_{k-1}, I_k, r_k) arrays, order='F' semantics
+    report: DecompReport
+
+    @property
+    def ranks(self):
+        return [1] + [c.shape[2] for c in self.cores]
+
+
+class DeviceResult:
+    """Owning handle of a ttg_result (cores resident on the device)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ttg_result_free(self.h)
+            self.h = None
+
+    def order(self) -> int:
+        return lib().ttg_result_order(self.h)
+
+    def core_dims(self, k: int):
+        d = np.zeros(3, np.int64)
+        lib().ttg_result_core_dims(self.h, k, _iptr(d))
+        return tuple(int(x) for x in d)
+
+    def core(self, k: int) -> np.ndarray:
+        dims = self.core_dims(k)
+        out = np.empty(int(np.prod(dims)), np.float64)
+        check(lib().ttg_result_core_copy(self.h, k, _dptr(out)))
+        return out.reshape(dims, order="F")
+
+    def report(self) -> DecompReport:
+        d = self.order()
+        se = np.zeros(max(d - 1, 0), np.float64)
+        rc = np.zeros(d + 1, np.int64)
+        rr = np.zeros(d + 1, np.int64)
+        b, ni, wt = C.c_double(), C.c_double(), C.c_double()
+        bk = C.c_int()
+        nreq = lib().ttg_result_report(self.h, _dptr(se), _iptr(rc), _iptr(rr), C.byref(b), C.byref(bk),
+                                       C.byref(ni), C.byref(wt))
+        warns = [lib().ttg_result_warning(self.h, i).decode() for i in range(lib().ttg_result_warning_count(self.h))]
+        cuts = []
+        for c in range(max(d - 1, 0)):
+            diag = np.zeros(8192, np.float64)
+            info = np.zeros(6, np.int64)
+            n = lib().ttg_result_cut_diag(self.h, c, _dptr(diag), diag.size, _iptr(info))
+            cuts.append(dict(steps=int(info[0]), p=int(info[1]), rank=int(info[2]), extensions=int(info[3]),
+                             m=int(info[4]), n=int(info[5]), diag=diag[:n].copy()))
+        return DecompReport(se.tolist(), rr[:nreq].tolist(), rc.tolist(), b.value,
+                            "root_sum_square" if bk.value == 0 else "plain_sum", ni.value, wt.value, warns,
+                            cuts=cuts)
+
+    def rse(self, a, on_device: bool = False) -> float:
+        out = C.c_double()
+        if on_device:
+            check(lib().ttg_result_rse(self.h, C.c_void_p(a), 1, C.byref(out)))
+        else:
+            a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+            check(lib().ttg_result_rse(self.h, a.ctypes.data_as(C.c_void_p), 0, C.byref(out)))
+        return out.value
+
+
+def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, weights=(), refine_passes=1,
+                     retain="l11_only", debug_checks=False, qlp="early_exit", a_is_device_ptr=False) -> DeviceResult:
+    """decompose() (tt_decomp.hpp:100) returning the device-resident result handle.
+
+    With ``a_is_device_ptr`` the tensor is read in place from device memory (an integer
+    pointer, e.g. ``torch_tensor.data_ptr()``); otherwise it is copied from the host."""
+    require_gpu()
+    cfg = Config()
+    cfg.method = METHODS[method]
+    cfg.sweep = SWEEPS[sweep]
+    keep = []
+    if ranks is not None:
+        r = np.ascontiguousarray(np.asarray(ranks, dtype=np.int64))
+        keep.append(r)
+        cfg.fixed_rank = 1
+        cfg.ranks = _iptr(r)
+        cfg.nranks = int(r.size)
+    else:
+        cfg.fixed_rank = 0
+        cfg.eps = float(eps if eps is not None else 0.0)
+    w = np.ascontiguousarray(np.asarray(list(weights), dtype=np.float64))
+    keep.append(w)
+    cfg.weights = _dptr(w) if w.size else None
+    cfg.nweights = int(w.size)
+    cfg.refine_passes = int(refine_passes)
+    cfg.retain = RETAIN[retain]
+    cfg.debug_checks = int(bool(debug_checks))
+    cfg.qlp_policy = QLP[qlp]
+    dims = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    h = C.c_void_p()
+    if a_is_device_ptr:
+        ptr = C.c_void_p(int(a))
+        check(lib().ttg_decompose(ptr, _iptr(dims), int(dims.size), C.byref(cfg), 1, C.byref(h)))
+    else:
+        flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
+        check(lib().ttg_decompose(flat.ctypes.data_as(C.c_void_p), _iptr(dims), int(dims.size), C.byref(cfg), 0,
+                                  C.byref(h)))
+    return DeviceResult(h)
+
+
+def decompose(a, dims=None, method="urv", sweep="r2l", ranks=None, eps=None, weights=(), refine_passes=1,
+              retain="l11_only", debug_checks=False, qlp="early_exit") -> DecompResult:
+    """decompose() (tt_decomp.hpp:100): host tensor in, host cores + report out."""
+    flat, dims = _flat(a, dims)
+    res = decompose_device(flat, dims, method, sweep, ranks, eps, weights, refine_passes, retain, debug_checks, qlp)
+    cores = [res.core(k) for k in range(res.order())]
+    return DecompResult(cores, res.report())
+
+
+# The seven named entry points of tt_decomp.hpp:69-97.
+def tt_svd(a, dims=None, sweep="l2r", ranks=None, eps=None, weights=(), refine_passes=1):
+    return decompose(a, dims, "svd", sweep, ranks, eps, weights, refine_passes)
+
+
+def tt_ulv_fixed_rank_l2r(a, ranks, dims=None, refine_passes=1, **kw):
+    return decompose(a, dims, "ulv", "l2r", ranks=ranks, refine_passes=refine_passes, **kw)
+
+
+def tt_ulv_fixed_tol_l2r(a, eps, weights=(), dims=None, refine_passes=1, **kw):
+    return decompose(a, dims, "ulv", "l2r", eps=eps, weights=weights, refine_passes=refine_passes, **kw)
+
+
+def tt_urv_fixed_rank_r2l(a, ranks, dims=None, refine_passes=1, **kw):
+    return decompose(a, dims, "urv", "r2l", ranks=ranks, refine_passes=refine_passes, **kw)
+
+
+def tt_urv_fixed_tol_r2l(a, eps, weights=(), dims=None, refine_passes=1, **kw):
+    return decompose(a, dims, "urv", "r2l", eps=eps, weights=weights, refine_passes=refine_passes, **kw)
+
+
+def tt_ulv_fixed_rank_r2l(a, ranks, retain="l11_only", dims=None, refine_passes=1, **kw):
+    return decompose(a, dims, "ulv", "r2l", ranks=ranks, retain=retain, refine_passes=refine_passes, **kw)
+
+
+def left_orthogonal_via_urv(a, dims=None, ranks=None, eps=None, weights=(), refine_passes=1, **kw):
+    return decompose(a, dims, "urv", "l2r", ranks=ranks, eps=eps, weights=weights, refine_passes=refine_passes, **kw)
+
+
+# ---- factor level (factor.hpp) -------------------------------------------------------
+def qr_col_pivot(a: np.ndarray):
+    """qr_col_pivot (factor.hpp:19): returns (q m x p, r p x n, perm)."""
+    require_gpu()
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    p = min(m, n)
+    q = np.zeros((m, p), order="F")
+    r = np.zeros((p, n), order="F")
+    perm = np.zeros(n, np.int64)
+    check(lib().ttg_qr_col_pivot(_dptr(a), m, n, _dptr(q), _dptr(r), _iptr(perm)))
+    return q, r, perm
+
+
+def reconstruct(cores: Sequence[np.ndarray], element_cap: int = 100_000_000) -> np.ndarray:
+    """reconstruct (tt.hpp:60): dense tensor (order='F' n-d array) from cores."""
+    require_gpu()
+    dims = np.array([c.shape[1] for c in cores], np.int64)
+    ranks = np.array([1] + [c.shape[2] for c in cores], np.int64)
+    flat = np.concatenate([np.asarray(c, np.float64).ravel(order="F") for c in cores])
+    out = np.empty(int(np.prod(dims)), np.float64)
+    check(lib().ttg_reconstruct(_dptr(flat), _iptr(dims), _iptr(ranks), int(dims.size), int(element_cap), _dptr(out)))
+    return out.reshape(tuple(dims), order="F")
+
+
+def frobenius_norm(a) -> float:
+    require_gpu()
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    out = C.c_double()
+    check(lib().ttg_frobenius_norm(a.ctypes.data_as(C.c_void_p), a.size, 0, C.byref(out)))
+    return out.value
+
+
+def kernel_launches() -> int:
+    return int(lib().ttg_kernel_launches())

@@ -1,0 +1,297 @@
+// C-ABI boundary (include/ttutv_b200.h): argument marshalling, host<->device copies and
+// exception -> status translation. No computation happens here.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/ttutv_b200.h"
+#include "sweep.hpp"
+
+struct ttg_result {
+    ttg::TTResult r;
+};
+
+namespace {
+
+thread_local std::string t_msg;
+
+template <class F>
+ttg_status guard(F&& f) {
+    try {
+        f();
+        t_msg.clear();
+        return TTG_OK;
+    } catch (const ttg::Failure& e) {
+        t_msg = e.what();
+        return static_cast<ttg_status>(e.code);
+    } catch (const std::bad_alloc& e) {
+        t_msg = "out of host memory";
+        return TTG_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        t_msg = e.what();
+        return TTG_ERR_INTERNAL;
+    }
+}
+
+int64_t count_of(const int64_t* dims, int d) {
+    int64_t n = 1;
+    for (int i = 0; i < d; ++i) {
+        if (dims[i] < 1)
+            ttg::argument_error("shape dim " + std::to_string(i + 1) + " is " + std::to_string(dims[i]) +
+                                ", must be >= 1");
+        if (n > (INT64_MAX / 8) / dims[i]) ttg::argument_error("shape element count overflows the index range");
+        n *= dims[i];
+    }
+    return n;
+}
+
+// Device view of a possibly-host buffer.
+struct DeviceInput {
+    ttg::DevBuf<double> buf;
+    const double* ptr = nullptr;
+    DeviceInput(const double* a, int64_t n, bool on_device) {
+        if (on_device) {
+            ptr = a;
+        } else {
+            buf.alloc((size_t)n);
+            buf.upload(a, (size_t)n);
+            ptr = buf.get();
+        }
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ttg_last_error(void) { return t_msg.c_str(); }
+int ttg_abi_version(void) { return 1; }
+
+int ttg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+ttg_status ttg_set_device(int device) {
+    return guard([&] { TTG_CUDA(cudaSetDevice(device)); });
+}
+
+int64_t ttg_kernel_launches(void) { return ttg::launches(); }
+
+ttg_status ttg_synchronize(void) {
+    return guard([&] { ttg::sync(); });
+}
+
+ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_config* cfg, int a_on_device,
+                         ttg_result** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (!cfg) ttg::argument_error("null config");
+        if (d < 0) ttg::argument_error("negative order");
+        const auto start = std::chrono::steady_clock::now();
+        std::vector<int64_t> dv(dims, dims + d);
+        const int64_t n = count_of(dims, d);
+        ttg::SweepConfig sc;
+        sc.method = cfg->method;
+        sc.sweep = cfg->sweep;
+        if (sc.method < 0 || sc.method > 2) ttg::argument_error("unknown method");
+        sc.fixed_rank = cfg->fixed_rank != 0;
+        if (sc.fixed_rank && cfg->ranks && cfg->nranks > 0) sc.ranks.assign(cfg->ranks, cfg->ranks + cfg->nranks);
+        sc.eps = cfg->eps;
+        if (cfg->nweights > 0 && cfg->weights) sc.weights.assign(cfg->weights, cfg->weights + cfg->nweights);
+        sc.refine = cfg->refine_passes;
+        sc.retain = cfg->retain;
+        sc.debug = cfg->debug_checks != 0;
+        sc.policy = cfg->qlp_policy;
+        DeviceInput in(a, n, a_on_device != 0);
+        auto* res = new ttg_result{ttg::decompose(in.ptr, dv, sc)};
+        res->r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+        *out = res;
+    });
+}
+
+void ttg_result_free(ttg_result* res) { delete res; }
+
+int ttg_result_order(const ttg_result* res) { return (int)res->r.cores.size(); }
+
+void ttg_result_core_dims(const ttg_result* res, int k, int64_t dims3[3]) {
+    const auto& c = res->r.core_dims[(size_t)k];
+    dims3[0] = c[0];
+    dims3[1] = c[1];
+    dims3[2] = c[2];
+}
+
+ttg_status ttg_result_core_copy(const ttg_result* res, int k, double* host_out) {
+    return guard([&] {
+        const auto& c = res->r.core_dims[(size_t)k];
+        res->r.cores[(size_t)k].download(host_out, (size_t)(c[0] * c[1] * c[2]));
+        ttg::sync();
+    });
+}
+
+const double* ttg_result_core_device(const ttg_result* res, int k) { return res->r.cores[(size_t)k].get(); }
+
+int ttg_result_report(const ttg_result* res, double* step_errors, int64_t* ranks_chosen, int64_t* ranks_requested,
+                      double* bound, int* bound_kind, double* input_norm, double* wall_time_ms) {
+    const auto& r = res->r;
+    if (step_errors) std::copy(r.step_errors.begin(), r.step_errors.end(), step_errors);
+    if (ranks_chosen) std::copy(r.ranks_chosen.begin(), r.ranks_chosen.end(), ranks_chosen);
+    if (ranks_requested) std::copy(r.ranks_requested.begin(), r.ranks_requested.end(), ranks_requested);
+    if (bound) *bound = r.bound;
+    if (bound_kind) *bound_kind = r.bound_kind;
+    if (input_norm) *input_norm = r.input_norm;
+    if (wall_time_ms) *wall_time_ms = r.wall_ms;
+    return (int)r.ranks_requested.size();
+}
+
+int ttg_result_warning_count(const ttg_result* res) { return (int)res->r.warnings.size(); }
+const char* ttg_result_warning(const ttg_result* res, int i) { return res->r.warnings[(size_t)i].c_str(); }
+
+int ttg_result_cut_diag(const ttg_result* res, int cut, double* diag, int max, int64_t info[6]) {
+    if (cut < 0 || (size_t)cut >= res->r.cuts.size()) return 0;
+    const auto& c = res->r.cuts[(size_t)cut];
+    if (info) {
+        info[0] = c.steps;
+        info[1] = c.p;
+        info[2] = c.rank;
+        info[3] = c.extensions;
+        info[4] = c.m;
+        info[5] = c.n;
+    }
+    const int n = std::min<int>(max, (int)c.diag.size());
+    for (int i = 0; i < n; ++i) diag[i] = c.diag[(size_t)i];
+    return n;
+}
+
+ttg_status ttg_result_rse(const ttg_result* res, const double* a, int a_on_device, double* rse) {
+    return guard([&] {
+        int64_t n = 1;
+        for (int64_t v : res->r.dims) n *= v;
+        DeviceInput in(a, n, a_on_device != 0);
+        const double denom = std::sqrt(ttg::sum_squares(in.ptr, n));
+        if (denom == 0.0) ttg::argument_error("rse: truth has zero norm (domain error)");
+        *rse = std::sqrt(ttg::residual_squared(res->r, in.ptr)) / denom;
+    });
+}
+
+ttg_status ttg_verify_bound(const double* a, int a_on_device, const ttg_result* res, double slack_rel,
+                            double* achieved) {
+    return guard([&] {
+        int64_t n = 1;
+        for (int64_t v : res->r.dims) n *= v;
+        DeviceInput in(a, n, a_on_device != 0);
+        const double ach = std::sqrt(ttg::residual_squared(res->r, in.ptr));
+        *achieved = ach;
+        const double allowed = res->r.bound + slack_rel * res->r.input_norm;
+        if (ach > allowed) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "achieved error %.12e exceeds bound %.12e plus slack %.3e", ach,
+                          res->r.bound, slack_rel * res->r.input_norm);
+            ttg::fail(6, buf);
+        }
+    });
+}
+
+ttg_status ttg_qr_col_pivot(const double* a, int64_t m, int64_t n, double* q, double* r, int64_t* perm) {
+    return guard([&] {
+        if (m <= 0 || n <= 0) ttg::argument_error("qr_col_pivot: empty matrix");
+        const int64_t p = std::min(m, n);
+        ttg::DevBuf<double> A((size_t)(m * n));
+        A.upload(a, (size_t)(m * n));
+        if (m <= 4096) {
+            ttg::WideQrcp e1(A.get(), m, n, m, ttg::Layout::Col, p);
+            e1.run_to(p);
+            if (q) {
+                ttg::DevBuf<double> hq;
+                TTG_CUDA(cudaMemcpyAsync(q, e1.Q(), sizeof(double) * m * p, cudaMemcpyDeviceToHost, ttg::stream()));
+            }
+            if (r || perm) {
+                std::vector<int64_t> pm((size_t)n);
+                TTG_CUDA(cudaMemcpyAsync(pm.data(), e1.perm(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                                         ttg::stream()));
+                std::vector<double> rr((size_t)(p * n));
+                TTG_CUDA(cudaMemcpyAsync(rr.data(), e1.R(), sizeof(double) * p * n, cudaMemcpyDeviceToHost,
+                                         ttg::stream()));
+                ttg::sync();
+                if (perm) std::copy(pm.begin(), pm.end(), perm);
+                if (r)  // R(i, pos) = R1 row i at column perm[pos] (exact zeros below the diagonal)
+                    for (int64_t j = 0; j < n; ++j)
+                        for (int64_t i = 0; i < p; ++i) r[i + j * p] = rr[(size_t)(i * n + pm[(size_t)j])];
+            }
+            ttg::sync();
+        } else {
+            ttg::TallQrcp e2(A.get(), m, n, m);
+            e2.run(p);
+            if (r) {
+                ttg::DevBuf<double> R((size_t)(p * n));
+                e2.extract_r(R.get(), p);
+                R.download(r, (size_t)(p * n));
+            }
+            if (perm) TTG_CUDA(cudaMemcpyAsync(perm, e2.perm(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, ttg::stream()));
+            if (q) {
+                ttg::DevBuf<double> Q((size_t)(m * p));
+                e2.form_q(Q.get(), p, m);
+                Q.download(q, (size_t)(m * p));
+            }
+            ttg::sync();
+        }
+    });
+}
+
+ttg_status ttg_utv(const double*, int64_t, int64_t, int, int, double*, double*, double*) {
+    return guard([&] { ttg::fail(7, "ttg_utv: not implemented yet"); });
+}
+
+ttg_status ttg_svd(const double*, int64_t, int64_t, int, double, double*, double*, double*) {
+    return guard([&] { ttg::fail(7, "ttg_svd: not implemented yet"); });
+}
+
+ttg_status ttg_truncate(int, const double*, const double*, const double*, int64_t, int64_t, int64_t, int64_t, double,
+                        int64_t*, double*, double*, double*, double*) {
+    return guard([&] { ttg::fail(7, "ttg_truncate: not implemented yet"); });
+}
+
+ttg_status ttg_reconstruct(const double* cores, const int64_t* dims, const int64_t* ranks, int d, int64_t element_cap,
+                           double* out) {
+    return guard([&] {
+        if (d < 1) ttg::argument_error("train needs at least one core");
+        if (ranks[0] != 1 || ranks[d] != 1) ttg::argument_error("boundary ranks must both be 1");
+        const int64_t n = count_of(dims, d);
+        if (n > element_cap)
+            ttg::fail(5, "reconstruct would materialize " + std::to_string(n) + " elements (cap " +
+                             std::to_string(element_cap) + ")");
+        int64_t total = 0;
+        for (int k = 0; k < d; ++k) total += ranks[k] * dims[k] * ranks[k + 1];
+        ttg::DevBuf<double> C((size_t)total), O((size_t)n);
+        C.upload(cores, (size_t)total);
+        std::vector<const double*> cp;
+        int64_t off = 0;
+        for (int k = 0; k < d; ++k) {
+            cp.push_back(C.get() + off);
+            off += ranks[k] * dims[k] * ranks[k + 1];
+        }
+        ttg::reconstruct(cp, std::vector<int64_t>(dims, dims + d), std::vector<int64_t>(ranks, ranks + d + 1), O.get());
+        O.download(out, (size_t)n);
+        ttg::sync();
+    });
+}
+
+ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, double* out) {
+    return guard([&] {
+        DeviceInput in(a, count, a_on_device != 0);
+        *out = std::sqrt(ttg::sum_squares(in.ptr, count));
+    });
+}
+
+ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, double* out) {
+    return guard([&] {
+        DeviceInput e(estimate, count, false), t(truth, count, false);
+        const double denom = std::sqrt(ttg::sum_squares(t.ptr, count));
+        if (denom == 0.0) ttg::argument_error("rse: truth has zero norm (domain error)");
+        *out = std::sqrt(ttg::diff_squares(e.ptr, t.ptr, count)) / denom;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// Shared host/device plumbing for the TT-UTV engine: status exceptions, the per-thread
+// stream, stream-ordered device buffers and warp/block reduction helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ttg {
+
+// Internal exception carrying a ttg_status code; translated at the C-ABI boundary.
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Failure(code, msg); }
+inline void argument_error(const std::string& msg) { fail(1, msg); }
+
+#define TTG_CUDA(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            ::ttg::fail(8, std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " + \
+                               __FILE__ + ":" + std::to_string(__LINE__));               \
+    } while (0)
+
+// Every kernel launch goes through this macro so the launch counter is exact and
+// launch errors surface immediately.
+#define TTG_LAUNCH(kernel, grid, block, smem, stream, ...)                               \
+    do {                                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
+        ::ttg::count_launch();                                                           \
+        TTG_CUDA(cudaGetLastError());                                                    \
+        if (::ttg::debug_sync()) ::ttg::check_sync(#kernel, __FILE__, __LINE__);        \
+    } while (0)
+
+void count_launch();
+int64_t launches();
+// TTG_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel.
+bool debug_sync();
+void check_sync(const char* kernel, const char* file, int line);
+
+// Opt a kernel into more than 48 KB of dynamic shared memory (no-op below that).
+template <class K>
+inline void allow_smem(K* kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        TTG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// Stream of the calling host thread (created lazily on the current device).
+cudaStream_t stream();
+int sm_count();
+
+// Stream-ordered device allocation (cudaMallocAsync on the thread's stream).
+template <class T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n) {
+        release();
+        n_ = n;
+        if (n) TTG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), stream()));
+    }
+    void zero() {
+        if (n_) TTG_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), stream()));
+    }
+    void release() {
+        if (p_) cudaFreeAsync(p_, stream());
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    void upload(const T* host, size_t n, size_t offset = 0) {
+        if (n) TTG_CUDA(cudaMemcpyAsync(p_ + offset, host, n * sizeof(T), cudaMemcpyHostToDevice, stream()));
+    }
+    void download(T* host, size_t n, size_t offset = 0) const {
+        if (n) TTG_CUDA(cudaMemcpyAsync(host, p_ + offset, n * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+    }
+    std::vector<T> to_host(size_t n) const {
+        std::vector<T> h(n);
+        download(h.data(), n);
+        sync();
+        return h;
+    }
+    static void sync() { TTG_CUDA(cudaStreamSynchronize(stream())); }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+inline void sync() { TTG_CUDA(cudaStreamSynchronize(stream())); }
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-shape block reduction (deterministic: the same tree for every call).
+// `scratch` must hold blockDim.x/32 doubles. Result valid in every thread.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double t = lane < nw ? scratch[lane] : 0.0;
+    t = warp_sum(t);
+    return t;
+}
+
+// Pivot candidate: larger squared norm wins, ties go to the lowest position
+// (reference: strict '>' scan from the current step, factor.cpp:85-87).
+struct Cand {
+    double nu;
+    int64_t pos;
+    int64_t col;
+};
+
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+    return a.nu > b.nu || (a.nu == b.nu && a.pos < b.pos);
+}
+
+__device__ __forceinline__ Cand cand_none() { return Cand{-1.0, INT64_MAX, -1}; }
+
+__device__ __forceinline__ Cand warp_best(Cand c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Cand x;
+        x.nu = __shfl_xor_sync(0xffffffffu, c.nu, o);
+        x.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
+        x.col = __shfl_xor_sync(0xffffffffu, c.col, o);
+        if (better(x, c)) c = x;
+    }
+    return c;
+}
+
+// Block-wide best candidate; `scratch` holds blockDim.x/32 Cands. Valid in all threads.
+__device__ __forceinline__ Cand block_best(Cand c, Cand* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    c = warp_best(c);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = c;
+    __syncthreads();
+    Cand t = lane < nw ? scratch[lane] : cand_none();
+    return warp_best(t);
+}
+
+}  // namespace ttg

@@ -1,0 +1,181 @@
+// Dense device helpers: FP64 tensor-core GEMM (mma.sync m8n8k4 f64 -> SASS DMMA; sm_100a
+// has no tcgen05 kind for f64), tiled transpose and deterministic reductions.
+#include <cmath>
+
+#include "engine.hpp"
+
+namespace ttg {
+namespace {
+
+// ---------------------------------------------------------------------------
+// GEMM: C = alpha op(A) op(B) + beta C, column-major. CTA tile 64x64, K step 16,
+// 4 warps each owning a 32x32 sub-tile = 4x4 DMMA 8x8x4 fragments. Operand tiles are
+// staged in shared memory with a two-stage register prefetch.
+// ---------------------------------------------------------------------------
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) k_gemm(int64_t m, int64_t n, int64_t k, const double* __restrict__ A,
+                                              int64_t lda, const double* __restrict__ B, int64_t ldb, double* C,
+                                              int64_t ldc, double alpha, double beta) {
+    __shared__ double As[BK][BM + 1];
+    __shared__ double Bs[BK][BN + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // Each thread loads 8 elements of each tile per stage (64*16 / 128).
+    double ra[8], rb[8];
+    auto load = [&](int64_t k0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = tid + e * 128;
+            // A tile element (row r in [0,64), kk in [0,16))
+            int r, kk;
+            if (!TA) { r = idx & 63; kk = idx >> 6; } else { kk = idx & 15; r = idx >> 4; }
+            const int64_t gi = m0 + r, gk = k0 + kk;
+            ra[e] = (gi < m && gk < k) ? (TA ? A[gk + gi * lda] : A[gi + gk * lda]) : 0.0;
+            int c, kb;
+            if (!TB) { kb = idx & 15; c = idx >> 4; } else { c = idx & 63; kb = idx >> 6; }
+            const int64_t gj = n0 + c, gk2 = k0 + kb;
+            rb[e] = (gj < n && gk2 < k) ? (TB ? B[gj + gk2 * ldb] : B[gk2 + gj * ldb]) : 0.0;
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = tid + e * 128;
+            int r, kk;
+            if (!TA) { r = idx & 63; kk = idx >> 6; } else { kk = idx & 15; r = idx >> 4; }
+            As[kk][r] = ra[e];
+            int c, kb;
+            if (!TB) { kb = idx & 15; c = idx >> 4; } else { c = idx & 63; kb = idx >> 6; }
+            Bs[kb][c] = rb[e];
+        }
+    };
+    load(0);
+    for (int64_t k0 = 0; k0 < k; k0 += BK) {
+        __syncthreads();
+        store();
+        __syncthreads();
+        if (k0 + BK < k) load(k0 + BK);
+#pragma unroll
+        for (int ks = 0; ks < BK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = As[ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gi = m0 + wm + i * 8 + (lane >> 2);
+                const int64_t gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+                if (gi < m && gj < n) {
+                    double* cp = C + gi + gj * ldc;
+                    *cp = beta == 0.0 ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *cp);
+                }
+            }
+}
+
+__global__ void k_transpose(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, double* B,
+                            int64_t ldb) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + r;
+        if (i < m && j < n) tile[r][threadIdx.x] = A[i + j * lda];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + threadIdx.x, i = i0 + r;
+        if (i < m && j < n) B[j + i * ldb] = tile[threadIdx.x][r];
+    }
+}
+
+// Blocked sum of squares: partial per 4096-element block (the reference's kReduceBlock,
+// kernels.cpp:16), one block per CTA iteration.
+constexpr int64_t kBlock = 4096;
+
+template <bool DIFF>
+__global__ void __launch_bounds__(256) k_sq_part(const double* __restrict__ x, const double* __restrict__ y,
+                                                 int64_t n, double* part) {
+    __shared__ double sd[8];
+    const int64_t nb = cdiv(n, kBlock);
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t lo = b * kBlock, hi = min(n, lo + kBlock);
+        double s = 0.0;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += 256) {
+            const double v = DIFF ? x[i] - y[i] : x[i];
+            s = fma(v, v, s);
+        }
+        s = block_sum(s, sd);
+        if (threadIdx.x == 0) part[b] = s;
+    }
+}
+
+// Combine partials in block order with a fixed tree: 1 CTA.
+__global__ void __launch_bounds__(1024) k_sum_parts(const double* part, int64_t nb, double* out) {
+    __shared__ double sd[32];
+    double s = 0.0;
+    const int64_t chunk = cdiv(nb, 1024);
+    const int64_t lo = threadIdx.x * chunk, hi = min(nb, lo + chunk);
+    for (int64_t i = lo; i < hi; ++i) s += part[i];
+    s = block_sum(s, sd);
+    if (threadIdx.x == 0) *out = s;
+}
+
+double reduce_sq(const double* x, const double* y, int64_t n) {
+    if (n == 0) return 0.0;
+    const int64_t nb = cdiv(n, kBlock);
+    DevBuf<double> part(nb), out(1);
+    const int grid = (int)std::min<int64_t>(nb, (int64_t)sm_count() * 8);
+    if (y) TTG_LAUNCH(k_sq_part<true>, grid, 256, 0, stream(), x, y, n, part.get());
+    else TTG_LAUNCH(k_sq_part<false>, grid, 256, 0, stream(), x, y, n, part.get());
+    TTG_LAUNCH(k_sum_parts, 1, 1024, 0, stream(), part.get(), nb, out.get());
+    return out.to_host(1)[0];
+}
+
+}  // namespace
+
+void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+          int64_t ldb, double* C, int64_t ldc, double alpha, double beta) {
+    if (m <= 0 || n <= 0) return;
+    dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, BN));
+    if (grid.y > 65535) argument_error("gemm: n too large for one launch");
+    if (!ta && !tb) TTG_LAUNCH((k_gemm<false, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+    else if (ta && !tb) TTG_LAUNCH((k_gemm<true, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+    else if (!ta && tb) TTG_LAUNCH((k_gemm<false, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+    else TTG_LAUNCH((k_gemm<true, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+}
+
+void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb) {
+    if (m <= 0 || n <= 0) return;
+    dim3 grid((unsigned)cdiv(m, 32), (unsigned)cdiv(n, 32));
+    TTG_LAUNCH(k_transpose, grid, dim3(32, 8), 0, stream(), A, m, n, lda, B, ldb);
+}
+
+double sum_squares(const double* x, int64_t n) { return reduce_sq(x, nullptr, n); }
+double diff_squares(const double* x, const double* y, int64_t n) { return reduce_sq(x, y, n); }
+
+}  // namespace ttg

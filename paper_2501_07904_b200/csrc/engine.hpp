@@ -1,0 +1,105 @@
+// Host-side engine interfaces (internal; the public boundary is include/ttutv_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ttg {
+
+// Storage of the k x N matrix W whose columns are pivoted in pass 1.
+//   Col: W(i,j) = W[i + j*ld]  (the unfolding c itself, ULV / left-to-right)
+//   Row: W(i,j) = W[i*ld + j]  (c^T read in place from a column-major c, URV / right-to-left)
+enum class Layout { Col = 0, Row = 1 };
+
+// ---------------------------------------------------------------------------
+// Pass 1: greedy column-pivoted Householder QR of a k x N matrix W with k moderate
+// (the rank-times-mode side of an unfolding). W is never written: the engine keeps the
+// explicit k x k orthogonal factor Q_t = H_0...H_{t-1} and produces, per step t, row t of
+// R for every column with one streaming GEMV, R(t,j) = q_t^T w_j, downdating the column
+// norms exactly as factor.cpp:98-107 does. Any prefix of steps equals the prefix of the
+// reference's qr_col_pivot (factor.cpp:62-135) in exact arithmetic: same pivots (same
+// tie rule), same R rows, and Q[:, :s] = the first s columns of its economy Q.
+// ---------------------------------------------------------------------------
+class WideQrcp {
+public:
+    WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps);
+    void run_to(int64_t steps);  // advance the greedy factorisation to `steps` (<= p)
+    int64_t steps() const { return steps_; }
+    int64_t p() const { return p_; }
+    int64_t k() const { return k_; }
+    int64_t N() const { return N_; }
+    // Exact trailing mass sum_j nu_j of the not-yet-pivoted columns (host sync).
+    double trailing_mass();
+
+    const double* Q() const { return Q_.get(); }       // k x k, columns 0..steps-1 final
+    const double* R() const { return R_.get(); }       // rows 0..steps-1, row t at R + t*N
+    const int64_t* perm() const { return perm_.get(); } // position -> column
+    const int64_t* piv() const { return piv_.get(); }   // step -> column
+    const double* diag() const { return diag_.get(); }  // R(t,t)
+    int64_t R_stride() const { return N_; }
+
+private:
+    void grow(int64_t cap);
+    void step();
+    void gemv_step(int64_t t);
+
+    const double* W_;
+    int64_t k_, N_, ld_, p_;
+    Layout layout_;
+    int64_t steps_ = 0, cap_ = 0;
+    int ncand_ = 0, mode_ = 0;
+    DevBuf<double> nu_, cref_, Q_, R_, y_, diag_, beta_, mass_;
+    DevBuf<int64_t> pos_, perm_, piv_, flags_;
+    DevBuf<Cand> cand_;
+    DevBuf<int> nflag_;
+};
+
+// ---------------------------------------------------------------------------
+// Pass 2 (and any tall QRCP): in-place Householder QR with column pivoting of an
+// N x n column-major matrix B with n moderate, mirroring factor.cpp:62-135 step by step
+// (pivot, dlarfg reflector, reflector application, norm downdate with the 1e-16
+// recompute guard). Reduction over the long dimension is split across CTAs with a
+// fixed-order combine, so results are deterministic.
+// ---------------------------------------------------------------------------
+class TallQrcp {
+public:
+    TallQrcp(double* B, int64_t N, int64_t n, int64_t ld);
+    void run(int64_t steps);     // steps <= min(N, n)
+    int64_t steps() const { return steps_; }
+    // R over final positions (steps x n, col-major, ldo >= steps): R(t,q) for q >= t, 0 below.
+    void extract_r(double* out, int64_t ldo) const;
+    const int64_t* perm() const { return colmap_.get(); } // position -> physical column
+    const double* pivot_norm2() const { return pnorm_.get(); } // nu of the pivot at its step
+    const double* beta() const { return beta_.get(); }
+    // Explicit economy Q columns 0..q-1 (N x q, col-major, ldq >= N).
+    void form_q(double* Qout, int64_t q, int64_t ldq);
+
+private:
+    double* B_;
+    int64_t N_, n_, ld_, p_;
+    int64_t steps_ = 0;
+    int nblk_ = 0;
+    int64_t rows_per_blk_ = 0;
+    DevBuf<double> nu_, cref_, R_, part_, tq_, beta_, v0_, pnorm_;
+    DevBuf<int64_t> colmap_, pos_;
+    DevBuf<int> flag_;
+};
+
+// ---------------------------------------------------------------------------
+// Dense helpers on device buffers (column-major).
+// ---------------------------------------------------------------------------
+// C(m x n) = op(A) * op(B) with FP64 tensor-core (DMMA) tiles.
+void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double* C, int64_t ldc, double alpha = 1.0,
+          double beta = 0.0);
+void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb);
+// Deterministic sum of squares of a contiguous buffer (fixed 4096-element blocks combined
+// in block order, the reference's blocking, kernels.cpp:84-102).
+double sum_squares(const double* x, int64_t n);
+// sum_i (x_i - y_i)^2 with the same blocking.
+double diff_squares(const double* x, const double* y, int64_t n);
+
+}  // namespace ttg

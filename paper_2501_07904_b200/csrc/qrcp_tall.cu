@@ -1,0 +1,383 @@
+// Tall in-place Householder QR with column pivoting (pass 2 of the QLP and every tall
+// factor-level QRCP). Mirrors qr_col_pivot (factor.cpp:62-135) step by step on an
+// N x n column-major matrix: the long dimension is split over CTAs (partial sums combined
+// in CTA order by a single finishing CTA, so the arithmetic is fixed), the n columns are
+// addressed through a position -> physical-column map instead of swapping memory.
+//
+// Step t:
+//   K1 dots    (row blocks)  redundant pivot argmax; partial sigma = sum_{i>t} x_i^2 and
+//                            d_j = sum_{i>t} x_i c_j(i) for every active column j
+//   K2 house   (1 CTA)       combine partials; dlarfg reflector (factor.cpp:24-38);
+//                            row t of R; t_j = beta (c_j(t) + d_j / v0); norm downdate and
+//                            guard flags (factor.cpp:98-107); position swap
+//   K3 apply   (row blocks)  v_i = x_i / v0 stored in the pivot column; c_j(i) -= t_j v_i
+//                            (factor.cpp:43-58, no contraction)
+//   K4 guard   (row blocks + 1 CTA, only when flagged) recompute flagged norms from rows > t
+#include <cmath>
+
+#include "engine.hpp"
+
+namespace ttg {
+namespace {
+
+constexpr int kT = 256;
+constexpr int kSub = 1024;  // rows staged per sub-block in K1/K4
+
+struct TallView {
+    double* B;
+    int64_t N, n, ld;
+    double* nu;
+    double* cref;
+    int64_t* colmap;  // position -> physical
+    int64_t* pos;     // physical -> position
+    double* part;     // nblk x (n + 1)
+    double* tq;       // n (physical)
+    double* R;        // p x n over positions, ld = p
+    int64_t ldr;
+    double* beta;
+    double* v0;
+    double* pnorm;
+    int* flag;        // [0] any flagged, [1 + j] flagged(j)
+    int64_t rpb;      // rows per block
+};
+
+// Redundant pivot choice over positions t..n-1: (nu desc, position asc).
+__device__ int64_t pick_pivot(const TallView& s, int64_t t, int64_t* out_pos) {
+    __shared__ double bnu[kT / 32];
+    __shared__ int64_t bpos[kT / 32];
+    double best = -1.0;
+    int64_t bp = INT64_MAX;
+    for (int64_t q = t + threadIdx.x; q < s.n; q += kT) {
+        const double v = s.nu[s.colmap[q]];
+        if (v > best || (v == best && q < bp)) { best = v; bp = q; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int64_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ov > best || (ov == best && op < bp)) { best = ov; bp = op; }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) { bnu[warp] = best; bpos[warp] = bp; }
+    __syncthreads();
+    __shared__ int64_t spiv;
+    if (threadIdx.x == 0) {
+        best = -1.0;
+        bp = INT64_MAX;
+        for (int w = 0; w < kT / 32; ++w)
+            if (bnu[w] > best || (bnu[w] == best && bpos[w] < bp)) { best = bnu[w]; bp = bpos[w]; }
+        bpos[0] = bp;
+        spiv = s.colmap[bp];
+    }
+    __syncthreads();
+    *out_pos = bpos[0];
+    const int64_t piv = spiv;
+    __syncthreads();
+    return piv;
+}
+
+// Column norms of all n columns (partials per block, combined by k_norm_fin).
+__global__ void __launch_bounds__(kT) k_norm_part(TallView s, int64_t row0) {
+    __shared__ double acc[1];
+    (void)acc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = row0 + (int64_t)blockIdx.x * s.rpb;
+    const int64_t r1 = min(s.N, r0 + s.rpb);
+    for (int64_t j = warp; j < s.n; j += kT / 32) {
+        const double* c = s.B + j * s.ld;
+        double a = 0.0;
+        for (int64_t i = r0 + lane; i < r1; i += 32) a = fma(c[i], c[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s.part[(int64_t)blockIdx.x * (s.n + 1) + j] = a;
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_norm_fin(TallView s, int nblk) {
+    for (int64_t j = threadIdx.x; j < s.n; j += kT) {
+        double a = 0.0;
+        for (int b = 0; b < nblk; ++b) a += s.part[(int64_t)b * (s.n + 1) + j];
+        s.nu[j] = a;
+        s.cref[j] = a;
+        s.colmap[j] = j;
+        s.pos[j] = j;
+    }
+    if (threadIdx.x == 0) s.flag[0] = 0;
+}
+
+__global__ void __launch_bounds__(kT) k_dots(TallView s, int64_t t) {
+    extern __shared__ double x[];  // kSub
+    __shared__ double acc[1024];   // per physical column partial (n <= 1023 here; larger n use global)
+    int64_t pp;
+    const int64_t piv = pick_pivot(s, t, &pp);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = max(t + 1, (int64_t)blockIdx.x * s.rpb);
+    const int64_t r1 = min(s.N, (int64_t)(blockIdx.x + 1) * s.rpb);
+    double* outp = s.part + (int64_t)blockIdx.x * (s.n + 1);
+    const bool smem_acc = s.n < 1024;
+    for (int64_t j = threadIdx.x; j <= s.n; j += kT) {
+        if (smem_acc) acc[j < 1024 ? j : 0] = 0.0;
+        else outp[j] = 0.0;
+    }
+    __syncthreads();
+    double sig = 0.0;
+    const double* xp = s.B + piv * s.ld;
+    for (int64_t b0 = r0; b0 < r1; b0 += kSub) {
+        const int64_t b1 = min(r1, b0 + kSub);
+        __syncthreads();
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += kT) {
+            const double v = xp[i];
+            x[i - b0] = v;
+            sig = fma(v, v, sig);
+        }
+        __syncthreads();
+        for (int64_t q = t + warp; q < s.n; q += kT / 32) {
+            const int64_t j = s.colmap[q];
+            if (j == piv) continue;
+            const double* c = s.B + j * s.ld;
+            double a = 0.0;
+            for (int64_t i = b0 + lane; i < b1; i += 32) a = fma(x[i - b0], c[i], a);
+            a = warp_sum(a);
+            if (lane == 0) {
+                if (smem_acc) acc[j] += a;
+                else outp[j] += a;
+            }
+        }
+    }
+    __shared__ double sd[kT / 32];
+    sig = block_sum(sig, sd);
+    __syncthreads();
+    if (smem_acc)
+        for (int64_t j = threadIdx.x; j < s.n; j += kT) outp[j] = acc[j];
+    if (threadIdx.x == 0) outp[s.n] = sig;
+}
+
+__global__ void __launch_bounds__(kT) k_house(TallView s, int64_t t, int nblk) {
+    int64_t pp;
+    const int64_t piv = pick_pivot(s, t, &pp);
+    __shared__ double sh[4];
+    __shared__ double sd[kT / 32];
+    // sigma: combine partials in block order.
+    double sg = 0.0;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < nblk; ++b) sg += s.part[(int64_t)b * (s.n + 1) + s.n];
+        const double alpha = s.B[t + piv * s.ld];
+        const int64_t len = s.N - t;
+        double beta = 0.0, v0 = 1.0, rkk = alpha;
+        if (len > 1 && sg != 0.0) {
+            const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sg));
+            const double smu = copysign(mu, alpha);
+            v0 = __dadd_rn(alpha, smu);
+            beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+            rkk = -smu;
+        }
+        sh[0] = beta;
+        sh[1] = v0;
+        sh[2] = rkk;
+        s.beta[t] = beta;
+        s.v0[t] = v0;
+        s.pnorm[t] = s.nu[piv];
+        s.B[t + piv * s.ld] = rkk;
+        // position swap (factor.cpp:88-93)
+        const int64_t other = s.colmap[t];
+        s.colmap[t] = piv;
+        s.colmap[pp] = other;
+        s.pos[piv] = t;
+        s.pos[other] = pp;
+        s.flag[0] = 0;
+    }
+    __syncthreads();
+    (void)sd;
+    const double beta = sh[0], v0 = sh[1];
+    for (int64_t q = t + 1 + threadIdx.x; q < s.n; q += kT) {
+        const int64_t j = s.colmap[q];
+        double d = 0.0;
+        for (int b = 0; b < nblk; ++b) d += s.part[(int64_t)b * (s.n + 1) + j];
+        const double c0 = s.B[t + j * s.ld];
+        double tj = 0.0, rt = c0;
+        if (beta != 0.0) {
+            tj = __dmul_rn(beta, __dadd_rn(c0, __ddiv_rn(d, v0)));
+            rt = __dsub_rn(c0, tj);
+        }
+        s.tq[j] = tj;
+        s.B[t + j * s.ld] = rt;
+        const double nv = __dsub_rn(s.nu[j], __dmul_rn(rt, rt));
+        s.nu[j] = nv;
+        const int fl = (nv < __dmul_rn(1e-16, s.cref[j]) || nv < 0.0) ? 1 : 0;
+        s.flag[1 + j] = fl;
+        if (fl) atomicOr(&s.flag[0], 1);
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_apply(TallView s, int64_t t) {
+    const double beta = s.beta[t];
+    if (beta == 0.0) return;
+    const double v0 = s.v0[t];
+    const int64_t piv = s.colmap[t];
+    const int64_t r0 = max(t + 1, (int64_t)blockIdx.x * s.rpb);
+    const int64_t r1 = min(s.N, (int64_t)(blockIdx.x + 1) * s.rpb);
+    double* xp = s.B + piv * s.ld;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kT) {
+        const double v = __ddiv_rn(xp[i], v0);
+        xp[i] = v;
+        for (int64_t q = t + 1; q < s.n; ++q) {
+            const int64_t j = s.colmap[q];
+            double* c = s.B + j * s.ld + i;
+            *c = __dsub_rn(*c, __dmul_rn(s.tq[j], v));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_guard_part(TallView s, int64_t t) {
+    if (s.flag[0] == 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = max(t + 1, (int64_t)blockIdx.x * s.rpb);
+    const int64_t r1 = min(s.N, (int64_t)(blockIdx.x + 1) * s.rpb);
+    for (int64_t q = t + 1 + warp; q < s.n; q += kT / 32) {
+        const int64_t j = s.colmap[q];
+        if (!s.flag[1 + j]) continue;
+        const double* c = s.B + j * s.ld;
+        double a = 0.0;
+        for (int64_t i = r0 + lane; i < r1; i += 32) a = fma(c[i], c[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s.part[(int64_t)blockIdx.x * (s.n + 1) + j] = a;
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_guard_fin(TallView s, int64_t t, int nblk) {
+    if (s.flag[0] == 0) return;
+    for (int64_t q = t + 1 + threadIdx.x; q < s.n; q += kT) {
+        const int64_t j = s.colmap[q];
+        if (!s.flag[1 + j]) continue;
+        double a = 0.0;
+        for (int b = 0; b < nblk; ++b) {
+            // blocks entirely above row t+1 wrote nothing for this step: skip them
+            const int64_t r1 = min(s.N, (int64_t)(b + 1) * s.rpb);
+            if (r1 <= t + 1) continue;
+            a += s.part[(int64_t)b * (s.n + 1) + j];
+        }
+        s.nu[j] = a;
+        s.cref[j] = a;
+    }
+}
+
+// Q formation: reflector t applied to columns [t, q) of Q (backward accumulation,
+// factor.cpp:116-133). Partial dots per block, combine, apply.
+__global__ void __launch_bounds__(kT) k_q_dots(TallView s, int64_t t, const double* Q, int64_t ldq, int64_t q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = max(t + 1, (int64_t)blockIdx.x * s.rpb);
+    const int64_t r1 = min(s.N, (int64_t)(blockIdx.x + 1) * s.rpb);
+    const double* v = s.B + s.colmap[t] * s.ld;
+    for (int64_t j = t + warp; j < q; j += kT / 32) {
+        const double* c = Q + j * ldq;
+        double a = 0.0;
+        for (int64_t i = r0 + lane; i < r1; i += 32) a = fma(v[i], c[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s.part[(int64_t)blockIdx.x * (s.n + 1) + (j - t)] = a;
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_q_fin(TallView s, int64_t t, const double* Q, int64_t ldq, int64_t q,
+                                              int nblk) {
+    const double beta = s.beta[t];
+    for (int64_t j = t + threadIdx.x; j < q; j += kT) {
+        double a = Q[t + j * ldq];
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t r1 = min(s.N, (int64_t)(b + 1) * s.rpb);
+            if (r1 <= t + 1) continue;
+            a += s.part[(int64_t)b * (s.n + 1) + (j - t)];
+        }
+        s.tq[j - t] = __dmul_rn(a, beta);
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_q_apply(TallView s, int64_t t, double* Q, int64_t ldq, int64_t q) {
+    const int64_t r0 = max(t, (int64_t)blockIdx.x * s.rpb);
+    const int64_t r1 = min(s.N, (int64_t)(blockIdx.x + 1) * s.rpb);
+    const double* v = s.B + s.colmap[t] * s.ld;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kT) {
+        const double vi = i == t ? 1.0 : v[i];
+        for (int64_t j = t; j < q; ++j) {
+            double* c = Q + i + j * ldq;
+            *c = __dsub_rn(*c, __dmul_rn(s.tq[j - t], vi));
+        }
+    }
+}
+
+// R over final positions: R(t,q) = B(t, colmap[q]) for t <= q (rows < steps), else 0.
+__global__ void k_extract_r(TallView s, int64_t steps, double* out, int64_t ldo) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= steps * s.n) return;
+    const int64_t q = e / steps, t = e - q * steps;
+    out[t + q * ldo] = t <= q ? s.B[t + s.colmap[q] * s.ld] : 0.0;
+}
+
+__global__ void k_eye(double* Q, int64_t N, int64_t q, int64_t ldq) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < N * q) {
+        const int64_t j = e / N, i = e - j * N;
+        Q[i + j * ldq] = i == j ? 1.0 : 0.0;
+    }
+}
+
+TallView view_of(double* B, int64_t N, int64_t n, int64_t ld, DevBuf<double>& nu, DevBuf<double>& cref,
+                 DevBuf<int64_t>& colmap, DevBuf<int64_t>& pos, DevBuf<double>& part, DevBuf<double>& tq,
+                 DevBuf<double>& R, int64_t ldr, DevBuf<double>& beta, DevBuf<double>& v0, DevBuf<double>& pn,
+                 DevBuf<int>& flag, int64_t rpb) {
+    return TallView{B, N, n, ld, nu.get(), cref.get(), colmap.get(), pos.get(), part.get(), tq.get(),
+                    R.get(), ldr, beta.get(), v0.get(), pn.get(), flag.get(), rpb};
+}
+
+}  // namespace
+
+TallQrcp::TallQrcp(double* B, int64_t N, int64_t n, int64_t ld) : B_(B), N_(N), n_(n), ld_(ld), p_(std::min(N, n)) {
+    if (N <= 0 || n <= 0) argument_error("qr_col_pivot: empty matrix");
+    // Rows per block: enough blocks to fill the GPU, at least 256 rows each.
+    const int64_t target = (int64_t)sm_count() * 4;
+    rows_per_blk_ = std::max<int64_t>(256, cdiv(N, target));
+    rows_per_blk_ = cdiv(rows_per_blk_, 32) * 32;
+    nblk_ = (int)cdiv(N, rows_per_blk_);
+    nu_.alloc(n); cref_.alloc(n); colmap_.alloc(n); pos_.alloc(n);
+    part_.alloc((size_t)nblk_ * (n + 1)); tq_.alloc(std::max(n, p_));
+    R_.alloc(p_ * n); R_.zero();
+    beta_.alloc(p_); v0_.alloc(p_); pnorm_.alloc(p_); flag_.alloc(n + 1);
+    TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
+                         rows_per_blk_);
+    TTG_LAUNCH(k_norm_part, nblk_, kT, 0, stream(), s, (int64_t)0);
+    TTG_LAUNCH(k_norm_fin, 1, kT, 0, stream(), s, nblk_);
+}
+
+void TallQrcp::run(int64_t steps) {
+    steps = std::min(steps, p_);
+    TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
+                         rows_per_blk_);
+    for (int64_t t = steps_; t < steps; ++t) {
+        TTG_LAUNCH(k_dots, nblk_, kT, sizeof(double) * kSub, stream(), s, t);
+        TTG_LAUNCH(k_house, 1, kT, 0, stream(), s, t, nblk_);
+        TTG_LAUNCH(k_apply, nblk_, kT, 0, stream(), s, t);
+        TTG_LAUNCH(k_guard_part, nblk_, kT, 0, stream(), s, t);
+        TTG_LAUNCH(k_guard_fin, 1, kT, 0, stream(), s, t, nblk_);
+    }
+    steps_ = std::max(steps_, steps);
+}
+
+void TallQrcp::extract_r(double* out, int64_t ldo) const {
+    TallView s{B_, N_, n_, ld_, nullptr, nullptr, colmap_.get(), nullptr, nullptr, nullptr, nullptr, 0,
+               nullptr, nullptr, nullptr, nullptr, rows_per_blk_};
+    if (steps_ > 0) TTG_LAUNCH(k_extract_r, (int)cdiv(steps_ * n_, 256), 256, 0, stream(), s, steps_, out, ldo);
+}
+
+void TallQrcp::form_q(double* Q, int64_t q, int64_t ldq) {
+    TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
+                         rows_per_blk_);
+    TTG_LAUNCH(k_eye, (int)cdiv(N_ * q, 256), 256, 0, stream(), Q, N_, q, ldq);
+    std::vector<double> hb = beta_.to_host(p_);
+    const int64_t top = std::min(q, steps_);
+    for (int64_t t = top - 1; t >= 0; --t) {
+        if (hb[(size_t)t] == 0.0) continue;
+        TTG_LAUNCH(k_q_dots, nblk_, kT, 0, stream(), s, t, Q, ldq, q);
+        TTG_LAUNCH(k_q_fin, 1, kT, 0, stream(), s, t, Q, ldq, q, nblk_);
+        TTG_LAUNCH(k_q_apply, nblk_, kT, 0, stream(), s, t, Q, ldq, q);
+    }
+}
+
+}  // namespace ttg

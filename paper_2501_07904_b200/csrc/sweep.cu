@@ -1,0 +1,401 @@
+// Sweep drivers: TT-ULV left-to-right (Alg. 1/2) and TT-URV right-to-left (Alg. 3 and its
+// prescribed-accuracy analogue), reference tt_decomp.cpp:156-339.
+//
+// One cut on device (refine_passes = 1, the two-pass QLP of factor.cpp:376-430):
+//   W = c (ULV) or c^T read in place (URV), k x N with k = r * I the short side.
+//   pass 1  WideQrcp on W for s steps: pivots P1, explicit Q1[:, :s], R1 rows 0..s-1.
+//   pass 2  TallQrcp on B = R1[:s, :]^T (N x s, rows in P1 position order): P2, R2.
+//   kept masses from R2 columns (factor.cpp:479-499, same summation order), rank rule
+//   (factor.cpp:512-520) or the fixed rank, residual sqrt(total - kept[r]).
+//   core   ULV: U1 = Q1[:, P2[:r]]           URV: V1^T = Q1[:, P2[:r]]^T
+//   carry  ULV: L11 V1^T = U1^T c = R1[P2[:r], :]   URV: U1 R11 = c V1 = R1[P2[:r], :]^T
+// so neither the second orthogonal factor nor a carry GEMM is ever formed: the carry is a
+// gather of R1 rows (exactly equal in exact arithmetic, since c = U T V^T with T triangular).
+//
+// Early exit: s starts at the requested rank (fixed) or grows until the pass-1 trailing
+// mass T1(s) falls below the budget (tolerance). The result equals the full p-step QLP
+// in exact arithmetic when every pass-2 pivot norm^2 of the kept steps is >= T1(s), the
+// largest possible norm^2 of any R1 row not yet computed;
+// otherwise s is extended and pass 2 is redone. s = p is exactly the reference schedule.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <sstream>
+
+#include "sweep.hpp"
+
+namespace ttg {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+std::string fmt_g(double v) {
+    std::ostringstream os;
+    os << v;
+    return os.str();
+}
+
+// ---- small device kernels -----------------------------------------------------------
+
+// B(i, c) = R1(c, perm[i]) for the first s rows of R1 (row c stored at R + c*N).
+__global__ void k_gather_b(const double* __restrict__ R, const int64_t* __restrict__ perm, int64_t N, int64_t s,
+                           double* B) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * s) return;
+    const int64_t c = e / N, i = e - c * N;
+    B[i + c * N] = R[c * N + perm[i]];
+}
+
+// kept[0] = 0, kept[c+1] = kept[c] + sum_{i<=c} R2(i,c)^2, sequential sums without
+// contraction (kept_mass_upper / kept_mass_lower of factor.cpp:479-499).
+__global__ void k_kept(const double* __restrict__ R2, int64_t s, int64_t ldr, double* colmass, double* kept) {
+    for (int64_t c = threadIdx.x; c < s; c += blockDim.x) {
+        double a = 0.0;
+        for (int64_t i = 0; i <= c; ++i) {
+            const double v = R2[i + c * ldr];
+            a = __dadd_rn(a, __dmul_rn(v, v));
+        }
+        colmass[c] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        kept[0] = 0.0;
+        for (int64_t c = 0; c < s; ++c) {
+            acc = __dadd_rn(acc, colmass[c]);
+            kept[c + 1] = acc;
+        }
+    }
+}
+
+// out(:, q) = Q(:, sel[q]) (k x r), or transposed out(q, :) = Q(:, sel[q])^T (r x k).
+__global__ void k_gather_qcols(const double* __restrict__ Q, int64_t k, const int64_t* __restrict__ sel, int64_t r,
+                               bool transposed, double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= k * r) return;
+    if (!transposed) {
+        const int64_t q = e / k, i = e - q * k;
+        out[i + q * k] = Q[i + sel[q] * k];
+    } else {
+        const int64_t i = e / r, q = e - i * r;
+        out[q + i * r] = Q[i + sel[q] * k];
+    }
+}
+
+// ULV carry: out(q, j) = R1(sel[q], j), r x N column-major (tiled through shared memory).
+__global__ void k_carry_rows_t(const double* __restrict__ R, int64_t N, const int64_t* __restrict__ sel, int64_t r,
+                               double* out) {
+    __shared__ double tile[32][33];
+    const int64_t j0 = (int64_t)blockIdx.x * 32, q0 = (int64_t)blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t q = q0 + y, j = j0 + threadIdx.x;
+        if (q < r && j < N) tile[y][threadIdx.x] = R[sel[q] * N + j];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t j = j0 + y, q = q0 + threadIdx.x;
+        if (q < r && j < N) out[q + j * r] = tile[threadIdx.x][y];
+    }
+}
+
+// URV carry: out(j, q) = R1(sel[q], j), N x r column-major.
+__global__ void k_carry_rows(const double* __restrict__ R, int64_t N, const int64_t* __restrict__ sel, int64_t r,
+                             double* out) {
+    const int64_t q = blockIdx.y;
+    const int64_t src = sel[q];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+        out[j + q * N] = R[src * N + j];
+}
+
+// ---- mode resolution (tt_decomp.cpp:32-71) ---------------------------------------------
+struct Resolved {
+    bool fixed = false;
+    std::vector<int64_t> ranks;
+    std::vector<double> budgets;
+};
+
+Resolved resolve_mode(const SweepConfig& cfg, int64_t d, double norm_a, bool rss) {
+    const int64_t cuts = d - 1;
+    Resolved out;
+    if (cfg.fixed_rank) {
+        out.fixed = true;
+        if ((int64_t)cfg.ranks.size() != d + 1)
+            argument_error("rank chain has " + std::to_string(cfg.ranks.size()) + " entries, expected " +
+                           std::to_string(d + 1));
+        if (cfg.ranks.front() != 1 || cfg.ranks.back() != 1) argument_error("boundary ranks must both be 1");
+        for (int64_t r : cfg.ranks)
+            if (r < 1) argument_error("ranks must be >= 1");
+        out.ranks = cfg.ranks;
+        return out;
+    }
+    if (cfg.eps < 0.0) argument_error("tolerance must be >= 0");
+    std::vector<double> w = cfg.weights;
+    if (w.empty()) {
+        const double c = (double)std::max<int64_t>(cuts, 1);
+        w.assign((size_t)cuts, rss ? 1.0 / std::sqrt(c) : 1.0 / c);
+    } else {
+        if ((int64_t)w.size() != cuts)
+            argument_error(std::to_string(w.size()) + " weights given, expected " + std::to_string(cuts));
+        double total = 0.0;
+        for (double x : w) {
+            if (x < 0.0) argument_error("weights must be >= 0");
+            total += rss ? x * x : x;
+        }
+        if (std::abs(total - 1.0) > 1e-12)
+            argument_error(rss ? "squared weights must sum to 1" : "weights must sum to 1");
+    }
+    for (double x : w) out.budgets.push_back(x * cfg.eps * norm_a);
+    return out;
+}
+
+// ---- one cut ------------------------------------------------------------------------------
+struct CutOut {
+    int64_t rank = 0, steps = 0, extensions = 0;
+    double step_error = 0.0;
+    std::vector<double> diag;
+    DevBuf<int64_t> sel;  // P2[:rank] on device
+};
+
+struct CutRequest {
+    bool fixed;
+    int64_t rank;   // fixed mode (already clamped to p)
+    double budget;  // tolerance mode
+    int policy;
+};
+
+CutOut run_cut(WideQrcp& e1, const CutRequest& req) {
+    const int64_t p = e1.p();
+    const int64_t N = e1.N();
+    int64_t s;
+    if (req.policy == 1) s = p;
+    else if (req.fixed) s = req.rank;
+    else s = std::min<int64_t>(p, 16);
+    CutOut out;
+    for (;;) {
+        e1.run_to(s);
+        const double t1 = s == p ? 0.0 : std::max(0.0, e1.trailing_mass());
+        const double b2 = req.budget * req.budget;
+        if (!req.fixed && s < p && t1 > b2) {  // no r <= s can meet the budget yet
+            s = std::min(p, std::max(2 * s, s + 8));
+            ++out.extensions;
+            continue;
+        }
+        // pass 2 on B = R1[:s, :]^T
+        DevBuf<double> B((size_t)N * s);
+        TTG_LAUNCH(k_gather_b, (int)cdiv(N * s, 256), 256, 0, stream(), e1.R(), e1.perm(), N, s, B.get());
+        TallQrcp e2(B.get(), N, s, N);
+        e2.run(s);
+        const int64_t s2 = std::min(N, s);  // pass-2 steps actually available
+        DevBuf<double> R2((size_t)s2 * s), colmass(s), kept(s + 1);
+        e2.extract_r(R2.get(), s2);
+        TTG_LAUNCH(k_kept, 1, 256, 0, stream(), R2.get(), s2, s2, colmass.get(), kept.get());
+        std::vector<double> hk = kept.to_host(s2 + 1);
+        std::vector<double> pn(s2);
+        TTG_CUDA(cudaMemcpyAsync(pn.data(), e2.pivot_norm2(), sizeof(double) * s2, cudaMemcpyDeviceToHost, stream()));
+        std::vector<double> r2h((size_t)s2 * s);
+        R2.download(r2h.data(), r2h.size());
+        sync();
+        const double total = s == p ? hk[(size_t)s2] : hk[(size_t)s2] + t1;
+        int64_t r;
+        if (req.fixed) {
+            r = req.rank;
+        } else if (req.budget == 0.0) {  // pick_rank: eps == 0 keeps p
+            r = p;
+            if (s < p) { s = p; ++out.extensions; continue; }
+        } else {
+            const double target = total - b2;
+            r = -1;
+            const int64_t hi = std::min(s2, p - 1);
+            for (int64_t c = 1; c <= hi; ++c)
+                if (hk[(size_t)c] >= target) { r = c; break; }
+            if (r < 0) {
+                if (s == p) r = p;
+                else { s = std::min(p, std::max(2 * s, s + 8)); ++out.extensions; continue; }
+            }
+        }
+        // Early-exit validity: every kept pass-2 pivot must dominate any unseen R1 row.
+        bool valid = true;
+        if (s < p) {
+            const double slack = t1 * (1.0 + 1e-6) + 1e-14 * total;
+            for (int64_t t = 0; t < r && t < s2; ++t)
+                if (!(pn[(size_t)t] >= slack)) { valid = false; break; }
+        }
+        if (!valid) {
+            s = std::min(p, std::max(2 * s, s + 8));
+            ++out.extensions;
+            continue;
+        }
+        out.rank = r;
+        out.steps = s;
+        out.step_error = std::sqrt(std::max(0.0, total - hk[(size_t)r]));
+        out.diag.resize((size_t)r);
+        for (int64_t t = 0; t < r; ++t) out.diag[(size_t)t] = std::abs(r2h[(size_t)(t + t * s2)]);
+        out.sel.alloc(r);
+        TTG_CUDA(cudaMemcpyAsync(out.sel.get(), e2.perm(), sizeof(int64_t) * r, cudaMemcpyDeviceToDevice, stream()));
+        return out;
+    }
+}
+
+void check_refine(int refine) {
+    if (refine < 0) argument_error("refine_passes must be >= 0");
+    if (refine > 64) argument_error("refine_passes is unreasonably large");
+}
+
+int64_t product(const std::vector<int64_t>& v, size_t lo, size_t hi) {
+    int64_t p = 1;
+    for (size_t i = lo; i < hi; ++i) p *= v[i];
+    return p;
+}
+
+void finish(TTResult& res, bool rss, Clock::time_point start) {
+    double b = 0.0;
+    for (double e : res.step_errors) b += rss ? e * e : e;
+    res.bound = rss ? std::sqrt(b) : b;
+    res.bound_kind = rss ? 0 : 1;
+    sync();
+    res.wall_ms = std::chrono::duration<double, std::milli>(Clock::now() - start).count();
+}
+
+void set_core(TTResult& res, size_t k, DevBuf<double>&& buf, int64_t r0, int64_t n, int64_t r1) {
+    res.cores[k] = std::move(buf);
+    res.core_dims[k] = {r0, n, r1};
+}
+
+}  // namespace
+
+TTResult decompose(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg) {
+    const auto start = Clock::now();
+    const int64_t d = (int64_t)dims.size();
+    if (d < 1) argument_error("train needs at least one core");
+    for (size_t k = 0; k < dims.size(); ++k)
+        if (dims[k] < 1)
+            argument_error("shape dim " + std::to_string(k + 1) + " is " + std::to_string(dims[k]) + ", must be >= 1");
+    const int64_t total_n = product(dims, 0, dims.size());
+    const bool plain = cfg.method == 1 && cfg.sweep == 1 && cfg.retain == 0;  // bound_kind_for
+    const bool rss = !plain;
+
+    TTResult res;
+    res.dims = dims;
+    res.cores.resize((size_t)d);
+    res.core_dims.resize((size_t)d);
+    const double norm_a = std::sqrt(sum_squares(a, total_n));
+    const Resolved mode = resolve_mode(cfg, d, norm_a, rss);
+    res.input_norm = norm_a;
+    if (mode.fixed) res.ranks_requested = mode.ranks;
+
+    if (norm_a == 0.0) {  // zero_input_result (tt_decomp.cpp:126-142)
+        res.step_errors.assign((size_t)std::max<int64_t>(d - 1, 0), 0.0);
+        res.ranks_chosen.assign((size_t)d + 1, 1);
+        if (mode.fixed && *std::max_element(mode.ranks.begin(), mode.ranks.end()) > 1)
+            res.warnings.push_back("input tensor is zero; all ranks clamped to 1");
+        for (int64_t k = 0; k < d; ++k) {
+            DevBuf<double> z((size_t)dims[(size_t)k]);
+            z.zero();
+            set_core(res, (size_t)k, std::move(z), 1, dims[(size_t)k], 1);
+        }
+        finish(res, rss, start);
+        return res;
+    }
+    if (d == 1) {  // order_one_result
+        res.ranks_chosen = {1, 1};
+        DevBuf<double> c((size_t)total_n);
+        TTG_CUDA(cudaMemcpyAsync(c.get(), a, sizeof(double) * total_n, cudaMemcpyDeviceToDevice, stream()));
+        set_core(res, 0, std::move(c), 1, dims[0], 1);
+        finish(res, rss, start);
+        return res;
+    }
+    check_refine(cfg.refine);
+    const bool fast = cfg.refine == 1 && ((cfg.method == 1 && cfg.sweep == 0) || (cfg.method == 2 && cfg.sweep == 1));
+    if (!fast) fail(7, "this (method, sweep, refine_passes) combination is not implemented on the device yet");
+
+    res.step_errors.assign((size_t)(d - 1), 0.0);
+    res.ranks_chosen.assign((size_t)d + 1, 1);
+    res.cuts.resize((size_t)(d - 1));
+
+    DevBuf<double> carry;  // current working matrix when not the input itself
+    if (cfg.method == 1) {
+        // ---- TT-ULV left to right (tt_decomp.cpp:156-211) ----
+        const double* c = a;
+        int64_t m = dims[0], n = total_n / dims[0], r_prev = 1;
+        for (int64_t k = 1; k <= d - 1; ++k) {
+            const int64_t p = std::min(m, n);
+            CutRequest rq{mode.fixed, 0, 0.0, cfg.policy};
+            if (mode.fixed) {
+                const int64_t req = mode.ranks[(size_t)k];
+                rq.rank = std::min(req, p);
+                if (rq.rank < req)
+                    res.warnings.push_back("cut " + std::to_string(k) + ": requested rank " + std::to_string(req) +
+                                           " clamped to " + std::to_string(rq.rank));
+            } else {
+                rq.budget = mode.budgets[(size_t)(k - 1)];
+            }
+            WideQrcp e1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
+            CutOut co = run_cut(e1, rq);
+            const int64_t r = co.rank;
+            res.step_errors[(size_t)(k - 1)] = co.step_error;
+            res.ranks_chosen[(size_t)k] = r;
+            res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag};
+            DevBuf<double> core((size_t)(m * r));
+            TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1.Q(), m, co.sel.get(), r, false,
+                       core.get());
+            set_core(res, (size_t)(k - 1), std::move(core), r_prev, dims[(size_t)(k - 1)], r);
+            DevBuf<double> next((size_t)(r * n));
+            dim3 g((unsigned)cdiv(n, 32), (unsigned)cdiv(r, 32));
+            TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1.R(), n, co.sel.get(), r, next.get());
+            r_prev = r;
+            if (k < d - 1) {
+                carry = std::move(next);
+                c = carry.get();
+                m = r * dims[(size_t)k];
+                n = n / dims[(size_t)k];
+            } else {
+                set_core(res, (size_t)(d - 1), std::move(next), r, dims[(size_t)(d - 1)], 1);
+            }
+        }
+    } else {
+        // ---- TT-URV right to left (tt_decomp.cpp:216-339) ----
+        const double* c = a;
+        int64_t M = total_n / dims[(size_t)(d - 1)], n = dims[(size_t)(d - 1)], r_next = 1;
+        for (int64_t k = d; k >= 2; --k) {
+            const int64_t p = std::min(M, n);
+            CutRequest rq{mode.fixed, 0, 0.0, cfg.policy};
+            if (mode.fixed) {
+                const int64_t req = mode.ranks[(size_t)(k - 1)];
+                rq.rank = std::min(req, p);
+                if (rq.rank < req)
+                    res.warnings.push_back("cut " + std::to_string(k - 1) + ": requested rank " +
+                                           std::to_string(req) + " clamped to " + std::to_string(rq.rank));
+            } else {
+                rq.budget = mode.budgets[(size_t)(k - 2)];
+            }
+            // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
+            WideQrcp e1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
+            CutOut co = run_cut(e1, rq);
+            const int64_t r = co.rank;
+            res.step_errors[(size_t)(k - 2)] = co.step_error;
+            res.ranks_chosen[(size_t)(k - 1)] = r;
+            res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag};
+            DevBuf<double> core((size_t)(n * r));
+            TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1.Q(), n, co.sel.get(), r, true,
+                       core.get());
+            set_core(res, (size_t)(k - 1), std::move(core), r, dims[(size_t)(k - 1)], r_next);
+            DevBuf<double> next((size_t)(M * r));
+            dim3 g((unsigned)std::min<int64_t>(cdiv(M, 256), 4096), (unsigned)r);
+            TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1.R(), M, co.sel.get(), r, next.get());
+            r_next = r;
+            if (k > 2) {
+                carry = std::move(next);
+                c = carry.get();
+                n = dims[(size_t)(k - 2)] * r;
+                M = M / dims[(size_t)(k - 2)];
+            } else {
+                set_core(res, 0, std::move(next), 1, dims[0], r);
+            }
+        }
+    }
+    (void)fmt_g;
+    finish(res, rss, start);
+    return res;
+}
+
+}  // namespace ttg

@@ -1,0 +1,54 @@
+// Tensor-train sweep drivers (host orchestration of the device engine).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace ttg {
+
+struct SweepConfig {
+    int method = 0;  // 0 svd, 1 ulv, 2 urv
+    int sweep = 0;   // 0 l2r, 1 r2l
+    bool fixed_rank = true;
+    std::vector<int64_t> ranks;
+    double eps = 0.0;
+    std::vector<double> weights;
+    int refine = 1;
+    int retain = 0;  // 0 l11_only, 1 full_column
+    bool debug = false;
+    int policy = 0;  // 0 early exit, 1 full QLP
+};
+
+struct CutInfo {
+    int64_t m = 0, n = 0, p = 0, steps = 0, rank = 0, extensions = 0;
+    std::vector<double> diag;  // |T_ii|, i < rank
+};
+
+struct TTResult {
+    std::vector<int64_t> dims;
+    std::vector<DevBuf<double>> cores;
+    std::vector<std::array<int64_t, 3>> core_dims;
+    std::vector<double> step_errors;
+    std::vector<int64_t> ranks_requested, ranks_chosen;
+    double bound = 0.0;
+    int bound_kind = 0;  // 0 rss, 1 plain sum
+    double input_norm = 0.0;
+    double wall_ms = 0.0;
+    std::vector<std::string> warnings;
+    std::vector<CutInfo> cuts;  // unfolding order
+};
+
+// a: device pointer to the dense tensor (first index fastest).
+TTResult decompose(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg);
+
+// |A - reconstruct(tt)|^2 on device without materialising the full reconstruction.
+double residual_squared(const TTResult& r, const double* a);
+// Dense reconstruction (device output of prod(dims) doubles).
+void reconstruct(const std::vector<const double*>& cores, const std::vector<int64_t>& dims,
+                 const std::vector<int64_t>& ranks, double* out);
+
+}  // namespace ttg

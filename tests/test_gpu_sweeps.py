@@ -1,0 +1,147 @@
+"""Device sweeps vs the reference CPU oracle on identical seeded inputs.
+
+Parity contract: identical ranks; |RSE_gpu - RSE_ref| <= 1e-10
+(absolute difference of relative errors); kept-block diagonal | |T_ii|_gpu - |T_ii|_ref |
+<= 1e-10 |T_00| for every cut.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from tests.fixtures import cfg1, planted_plus_noise, shifted_hilbert
+from tests.replay import replay
+
+pytestmark = pytest.mark.gpu
+
+TOL_RSE = 1e-10
+TOL_DIAG = 1e-10
+
+
+def _check_parity(dev, ref, a, dims, method, ranks=None, eps=None, qlp="early_exit"):
+    sweep = "l2r" if method == "ulv" else "r2l"
+    res = dev.decompose_device(a, dims, method, sweep, ranks=ranks, eps=eps, qlp=qlp)
+    rep = res.report()
+    gpu_rse = res.rse(a)
+    rr = ref.decompose(a, dims, method, sweep, ranks=ranks, eps=eps or 0.0)
+    ref_rse = ref.rse(rr, a, dims)
+    assert rep.ranks_chosen == rr.ranks_chosen
+    assert abs(gpu_rse - ref_rse) <= TOL_RSE, (gpu_rse, ref_rse)
+    cuts = replay(ref, a, dims, method, ranks=ranks, eps=eps)
+    for c, (g, r) in enumerate(zip(rep.cuts, cuts)):
+        assert g["rank"] == r["rank"]
+        scale = r["diag"][0]
+        assert np.max(np.abs(g["diag"] - r["diag"])) <= TOL_DIAG * scale, (c, g["diag"], r["diag"])
+    return res, rep, rr, gpu_rse, ref_rse
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+@pytest.mark.parametrize("qlp", ["early_exit", "full"])
+def test_cfg1_fixed_rank(dev, ref, method, qlp):
+    a, dims, ranks = cfg1(ref)
+    _, rep, rr, g, r = _check_parity(dev, ref, a, dims, method, ranks=ranks, qlp=qlp)
+    assert rep.ranks_chosen == ranks
+    # the reference's TT-SVD check (BASELINE config 1): within 2x of TT-SVD's RSE
+    svd = ref.decompose(a, dims, "svd", "l2r", ranks=ranks)
+    assert g <= 2.0 * ref.rse(svd, a, dims)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_cfg1_tolerance_wellposed(dev, ref, method):
+    a, dims, _ = cfg1(ref)
+    _, rep, *_ = _check_parity(dev, ref, a, dims, method, eps=1e-6)
+    assert rep.ranks_chosen == [1, 5, 5, 5, 1]
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_planted_order6_fixed(dev, ref, method):
+    dims, ranks = [6] * 6, [1, 4, 5, 5, 5, 4, 1]
+    a = planted_plus_noise(ref, dims, ranks, 3, 1e-4)
+    _check_parity(dev, ref, a, dims, method, ranks=ranks)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_hilbert_small_tolerance(dev, ref, method):
+    dims = [10] * 4
+    a = shifted_hilbert(dims)
+    _check_parity(dev, ref, a, dims, method, eps=1e-6)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_planted_exact_recovery(dev, ref, method):
+    dims, ranks = [7, 6, 8, 5], [1, 3, 4, 2, 1]
+    a = ref.gen_planted_dense(dims, ranks, 301)
+    res = dev.decompose_device(a, dims, method, "l2r" if method == "ulv" else "r2l", ranks=ranks)
+    assert res.rse(a) <= 1e-10
+
+
+def test_clamping_and_warnings(dev, ref):
+    dims = [4, 6, 1]
+    a = ref.gen_gaussian(dims, 5)
+    res = dev.decompose(a, dims, "ulv", "l2r", ranks=[1, 9, 9, 1])
+    rr = ref.decompose(a, dims, "ulv", "l2r", ranks=[1, 9, 9, 1])
+    assert res.report.ranks_chosen == rr.ranks_chosen
+    assert res.report.warnings == rr.warnings
+
+
+def test_zero_tensor(dev, ref):
+    dims = [3, 4, 5]
+    a = np.zeros(60)
+    res = dev.decompose(a, dims, "urv", "r2l", ranks=[1, 2, 3, 1])
+    rr = ref.decompose(a, dims, "urv", "r2l", ranks=[1, 2, 3, 1])
+    assert res.report.ranks_chosen == rr.ranks_chosen == [1, 1, 1, 1]
+    assert res.report.warnings == rr.warnings
+    assert all(np.all(c == 0) for c in res.cores)
+
+
+def test_order_one(dev, ref):
+    a = np.arange(1.0, 8.0)
+    res = dev.decompose(a, [7], "ulv", "l2r", ranks=[1, 1])
+    assert res.report.ranks_chosen == [1, 1]
+    np.testing.assert_array_equal(res.cores[0].reshape(-1), a)
+
+
+def test_rank_chain_errors(dev):
+    from paper_2501_07904_b200 import ArgumentError
+    a = np.ones(24)
+    with pytest.raises(ArgumentError, match="rank chain has 3 entries, expected 4"):
+        dev.decompose(a, [2, 3, 4], "urv", "r2l", ranks=[1, 2, 1])
+    with pytest.raises(ArgumentError, match="boundary ranks must both be 1"):
+        dev.decompose(a, [2, 3, 4], "urv", "r2l", ranks=[2, 2, 2, 1])
+    with pytest.raises(ArgumentError, match="squared weights must sum to 1"):
+        dev.decompose(a, [2, 3, 4], "urv", "r2l", eps=0.1, weights=[0.5, 0.5])
+    with pytest.raises(ArgumentError, match="tolerance must be >= 0"):
+        dev.decompose(a, [2, 3, 4], "urv", "r2l", eps=-1.0)
+
+
+@pytest.mark.parametrize("shape", [(30, 20), (20, 30), (100, 400), (100, 20), (1, 7), (7, 1)])
+def test_qr_col_pivot_matches_reference(dev, ref, shape):
+    rng = np.random.default_rng(7)
+    a = np.asfortranarray(rng.standard_normal(shape))
+    q, r, perm = dev.qr_col_pivot(a)
+    q0, r0, perm0 = ref.qr_col_pivot(a)
+    np.testing.assert_array_equal(perm, perm0)
+    nrm = np.linalg.norm(a)
+    assert np.max(np.abs(r - r0)) <= 1e-12 * nrm
+    assert np.max(np.abs(q - q0)) <= 1e-12
+    # reference identities (test_factor.cpp:103-140)
+    assert np.max(np.abs(q @ r - a[:, perm])) <= 1e-12 * nrm
+    assert np.max(np.abs(q.T @ q - np.eye(q.shape[1]))) <= 1e-12
+    assert np.all(np.tril(r, -1) == 0.0)
+    d = np.abs(np.diag(r))
+    assert np.all(d[1:] <= d[:-1] * (1 + 1e-12) + 1e-300)
+
+
+def test_qr_col_pivot_zero_matrix(dev):
+    q, r, perm = dev.qr_col_pivot(np.zeros((5, 3), order="F"))
+    np.testing.assert_array_equal(q, np.eye(5, 3))
+    assert np.all(r == 0)
+    np.testing.assert_array_equal(perm, np.arange(3))
+
+
+def test_determinism(dev, ref):
+    a, dims, ranks = cfg1(ref)
+    r1 = dev.decompose(a, dims, "urv", "r2l", ranks=ranks)
+    r2 = dev.decompose(a, dims, "urv", "r2l", ranks=ranks)
+    for c1, c2 in zip(r1.cores, r2.cores):
+        np.testing.assert_array_equal(c1, c2)
