@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""TT-UTV throughput benchmark (BASELINE.json metric: tensor entries/s, FP64).
+
+Default workload (N=1): BASELINE config 2 -- the Hilbert-type 32^5 tensor
+A = 1/(i1+..+i5-4), rank-adaptive at eps = 1e-8. One step = one TT-ULV left-to-right
+plus one TT-URV right-to-left decomposition of the whole tensor (2 x 33.5M entries).
+
+  value   entries/s with the tensor resident in HBM (device-timed, CUDA events on the
+          engine's stream, max over ranks)
+  e2e     the same through the public API from pinned host memory: H2D of the tensor
+          and D2H of every core inside the timed region
+  roofline  the dominant kernel (pass-1 streaming GEMV, HBM-bound) timed live with
+          CUDA events around each launch inside the timed region
+  cpu_baseline  the reference CPU library (oracle/_ref, compiled from /root/reference)
+          on this host's cores, one step, rank 0 only
+
+`--impl reference` times the reference CPU implementation itself on the same workload.
+`--config {1,2,3,5}` selects another BASELINE config (parity/extra measurements).
+Multi-GPU (torchrun): config 2 does not shard, so every rank runs an independent
+replica ("replicas only", scaling weak); value = all ranks' entries / max rank time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+
+METRIC = "TT-UTV tensor entries/sec (FP64)"
+UNIT = "entries/s"
+FALLBACK_HBM = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload(cfg: int):
+    from paper_2501_07904_b200.inputs import CONFIGS
+    c = CONFIGS[cfg]
+    runs = [("ulv", "l2r"), ("urv", "r2l")]
+    desc = {1: "cfg1 20^4 planted TT (1,5,5,5,1) + 1e-8 noise, fixed rank",
+            2: "cfg2 Hilbert-type 32^5 A=1/(i1+..+i5-4), rank-adaptive eps=1e-8",
+            3: "cfg3 24^6 planted TT ranks 20 + 1e-4 noise, fixed rank 20",
+            5: "cfg5 1024^3 planted TT (1,128,128,1) + 1e-6 noise, fixed rank 128"}[cfg]
+    if cfg == 5:
+        runs = [("urv", "r2l")]
+    return c, runs, desc
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        import torch
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    return world, rank, local, dist
+
+
+def max_over_ranks(x: float, dist) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def ncu_traffic(cfg: int):
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get(str(cfg))
+    except Exception:
+        return None
+
+
+def reference_step(ref, a_host, c, runs):
+    """One step of the reference CPU library on the host buffer."""
+    out = []
+    for method, sweep in runs:
+        if c["mode"] == "tol":
+            rr = ref.decompose(a_host, c["dims"], method, sweep, eps=c["eps"])
+        else:
+            rr = ref.decompose(a_host, c["dims"], method, sweep, ranks=c["ranks"])
+        out.append(rr.ranks_chosen)
+    return out
+
+
+def run_reference(args):
+    world, rank, local, dist = dist_setup(args.gpus)
+    c, runs, desc = workload(args.config)
+    if rank != 0:
+        return 0
+    from oracle import ref
+    from paper_2501_07904_b200.inputs import build
+    import torch
+    a = build(args.config, "cuda" if torch.cuda.is_available() else "cpu").cpu().numpy()
+    n = a.size
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    small = ref.gen_gaussian([8, 8, 8], 1)
+    for _ in range(args.warmup):  # warm the OpenMP pool on a tiny problem (first region ~1 s)
+        ref.decompose(small, [8, 8, 8], "urv", "r2l", ranks=[1, 3, 3, 1])
+    t0 = time.perf_counter()
+    ranks = None
+    for _ in range(args.steps):
+        ranks = reference_step(ref, a, c, runs)
+    dt = time.perf_counter() - t0
+    value = args.steps * len(runs) * n / dt
+    sample = f"{args.steps} full step(s) of {desc} ({len(runs)} decomposition(s) each), ranks {ranks}"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "entries_per_step": len(runs) * n, "parallelism": "cpu-openmp"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    world, rank, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    from paper_2501_07904_b200 import api
+    from paper_2501_07904_b200._native import lib, check
+    from paper_2501_07904_b200.inputs import build
+    check(lib().ttg_set_device(local))
+    c, runs, desc = workload(args.config)
+    a = build(args.config, torch.device("cuda", local))
+    torch.cuda.synchronize()
+    n = a.numel()
+    dims = c["dims"]
+    stream = torch.cuda.ExternalStream(lib().ttg_stream(), device=torch.device("cuda", local))
+
+    def kw(method):
+        return dict(eps=c["eps"]) if c["mode"] == "tol" else dict(ranks=c["ranks"])
+
+    info = {}
+
+    def step_device():
+        for method, sweep in runs:
+            res = api.decompose_device(a.data_ptr(), dims, method, sweep, a_is_device_ptr=True, qlp=args.qlp,
+                                       **kw(method))
+            info[method] = res
+        return info
+
+    for _ in range(args.warmup):
+        step_device()
+    # ---- timed region: tensor resident in HBM ----
+    lib().ttg_profile_enable(1)
+    d0, d1 = C_double(), C_double()
+    lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))  # discard warm-up records
+    launches0 = lib().ttg_kernel_launches()
+    clocks = Clocks(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_device()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    launches = lib().ttg_kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    nk = lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))
+    lib().ttg_profile_enable(0)
+    kern_ms, kern_bytes = d0.value, d1.value
+    ms_max = max_over_ranks(ms, dist)
+    entries_per_step = len(runs) * n
+    value = world * args.steps * entries_per_step / (ms_max * 1e-3)
+
+    rep = {m: r.report() for m, r in info.items()}
+    rse = {m: r.rse(a.data_ptr(), on_device=True) for m, r in info.items()} if args.config != 5 else {}
+    info.clear()
+
+    # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region ----
+    host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host.copy_(a)
+    torch.cuda.synchronize()
+    h2d = d2h = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for method, sweep in runs:
+            res = api.decompose_device(host.data_ptr(), dims, method, sweep, qlp=args.qlp, **kw(method))
+            h2d += n * 8
+            for k in range(res.order()):
+                d2h += res.core(k).nbytes
+    e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(e2e_s, dist)
+    e2e_value = world * args.steps * entries_per_step / e2e_s
+
+    peak, peak_kind = hbm_peak()
+    achieved = kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+    traffic = ncu_traffic(args.config)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "entries_per_step": entries_per_step,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                       "l2": f"input {n * 8 / 1e6:.0f} MB vs 126 MB L2" + (" (larger than L2, no flush)" if n * 8 > 126e6 else " (L2-resident between steps)"),
+                       "qlp": args.qlp,
+                       "ranks": {m: r.ranks_chosen for m, r in rep.items()},
+                       "pass1_steps": {m: [cu["steps"] for cu in r.cuts] for m, r in rep.items()},
+                       "rse": rse},
+            "roofline": {"bound": "hbm", "kernel": "k_stream (pass-1 streaming GEMV + norm downdate)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "peak_source": f"hbm_gbs ({peak_kind})",
+                         "traffic": traffic, "launches": nk, "kernel_ms": kern_ms,
+                         "share_of_step": kern_ms / ms if ms > 0 else None},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps},
+            "gpu_launches": int(launches),
+            "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.cpu().numpy(), c, runs, desc)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(a_host, c, runs, desc):
+    try:
+        from oracle import ref
+        if not ref.available():
+            return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+        small = ref.gen_gaussian([8, 8, 8], 1)
+        ref.decompose(small, [8, 8, 8], "urv", "r2l", ranks=[1, 3, 3, 1])
+        t0 = time.perf_counter()
+        ranks = reference_step(ref, a_host, c, runs)
+        dt = time.perf_counter() - t0
+        return {"value": len(runs) * a_host.size / dt, "unit": UNIT,
+                "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "reference",
+                "sample": f"one full step of {desc} on the reference library, ranks {ranks}, {dt:.1f} s"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+
+def C_double():
+    import ctypes
+    return ctypes.c_double()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--qlp", default="early_exit", choices=["early_exit", "full"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -88,6 +88,14 @@ ttg_status ttg_set_device(int device);
 /* Number of CUDA kernels this thread has launched (monotone counter; for bench/tests). */
 int64_t ttg_kernel_launches(void);
 ttg_status ttg_synchronize(void);
+/* The calling thread's CUDA stream (cudaStream_t), on which every kernel of this thread
+ * is launched; lets a harness record events on the same stream. */
+void* ttg_stream(void);
+/* Event timing of the dominant kernel (pass-1 streaming GEMV) for roofline reports:
+ * enable, run, then read (host sync) the launch count, summed device time and summed
+ * algorithmic bytes since the last read. */
+ttg_status ttg_profile_enable(int on);
+int64_t ttg_profile_read(double* total_ms, double* algorithmic_bytes);
 
 /* ---- tensor-train sweeps ---------------------------------------------------- */
 /* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`

@@ -150,9 +150,11 @@ def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, w
     cfg.qlp_policy = QLP[qlp]
     dims = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
     h = C.c_void_p()
-    if a_is_device_ptr:
+    if a_is_device_ptr or isinstance(a, int):
+        # raw pointer: device memory when a_is_device_ptr, else (pinned) host memory
         ptr = C.c_void_p(int(a))
-        check(lib().ttg_decompose(ptr, _iptr(dims), int(dims.size), C.byref(cfg), 1, C.byref(h)))
+        check(lib().ttg_decompose(ptr, _iptr(dims), int(dims.size), C.byref(cfg), int(bool(a_is_device_ptr)),
+                                  C.byref(h)))
     else:
         flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
         check(lib().ttg_decompose(flat.ctypes.data_as(C.c_void_p), _iptr(dims), int(dims.size), C.byref(cfg), 0,

@@ -84,6 +84,26 @@ ttg_status ttg_synchronize(void) {
     return guard([&] { ttg::sync(); });
 }
 
+void* ttg_stream(void) {
+    try {
+        return (void*)ttg::stream();
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+ttg_status ttg_profile_enable(int on) {
+    return guard([&] { ttg::prof_enable(on != 0); });
+}
+
+int64_t ttg_profile_read(double* total_ms, double* algorithmic_bytes) {
+    try {
+        return ttg::prof_read(total_ms, algorithmic_bytes);
+    } catch (...) {
+        return -1;
+    }
+}
+
 ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_config* cfg, int a_on_device,
                          ttg_result** out) {
     *out = nullptr;

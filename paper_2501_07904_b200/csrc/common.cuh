@@ -56,6 +56,16 @@ inline void allow_smem(K* kernel, size_t bytes) {
 cudaStream_t stream();
 int sm_count();
 
+// Optional event timing of the dominant (pass-1 streaming) kernel for the roofline report:
+// when enabled, prof_begin/prof_end bracket each launch with CUDA events on the launching
+// stream and accumulate the algorithmic bytes of that launch.
+bool prof_enabled();
+void prof_enable(bool on);
+void prof_begin();
+void prof_end(double algorithmic_bytes);
+// Drains the recorded events (host sync). Returns launches; total device ms and bytes.
+int64_t prof_read(double* total_ms, double* bytes);
+
 // Stream-ordered device allocation (cudaMallocAsync on the thread's stream).
 template <class T>
 class DevBuf {

@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(128) k_gemm(int64_t m, int64_t n, int64_t k, c
     __shared__ double As[BK][BM + 1];
     __shared__ double Bs[BK][BN + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int64_t tm = cdiv(m, BM);
+    const int64_t m0 = ((int64_t)blockIdx.x % tm) * BM, n0 = ((int64_t)blockIdx.x / tm) * BN;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
     double acc[4][4][2];
 #pragma unroll
@@ -161,8 +162,9 @@ double reduce_sq(const double* x, const double* y, int64_t n) {
 void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
           int64_t ldb, double* C, int64_t ldc, double alpha, double beta) {
     if (m <= 0 || n <= 0) return;
-    dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, BN));
-    if (grid.y > 65535) argument_error("gemm: n too large for one launch");
+    const int64_t tiles = cdiv(m, BM) * cdiv(n, BN);
+    if (tiles > INT32_MAX) argument_error("gemm: problem too large for one launch");
+    const unsigned grid = (unsigned)tiles;
     if (!ta && !tb) TTG_LAUNCH((k_gemm<false, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
     else if (ta && !tb) TTG_LAUNCH((k_gemm<true, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
     else if (!ta && tb) TTG_LAUNCH((k_gemm<false, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);

@@ -31,8 +31,13 @@ public:
     int64_t p() const { return p_; }
     int64_t k() const { return k_; }
     int64_t N() const { return N_; }
-    // Exact trailing mass sum_j nu_j of the not-yet-pivoted columns (host sync).
+    // Trailing mass sum_j nu_j of the not-yet-pivoted columns from the downdated norms
+    // (host sync). Below ~1e-16 of a column's norm the downdates are rounding noise.
     double trailing_mass();
+    // Recomputes every unpivoted norm exactly from the projection residual
+    // |w_j - Q[:, :s] R(0:s, j)|^2 (one GEMM over W; also resets cref like the guard) and
+    // returns the exact trailing mass.
+    double refresh_exact();
 
     const double* Q() const { return Q_.get(); }       // k x k, columns 0..steps-1 final
     const double* R() const { return R_.get(); }       // rows 0..steps-1, row t at R + t*N
@@ -87,6 +92,20 @@ private:
     DevBuf<int64_t> colmap_, pos_;
     DevBuf<int> flag_;
 };
+
+// ---------------------------------------------------------------------------
+// TSQR and small pivoted QR (tsqr.cu)
+// ---------------------------------------------------------------------------
+// R factor (s x s, upper, col-major ld = s) of the N x s matrix B (column t at B + t*ld),
+// by a Householder TSQR tree in shared memory (one HBM pass over B). Requires tsqr_fits(s).
+bool tsqr_fits(int64_t s);
+void tsqr_r(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout);
+// One-CTA qr_col_pivot of a matrix that fits in shared memory (small_qrcp_fits): the
+// reference algorithm step for step. perm[n], R (p x n over positions, ld = p), pnorm[p]
+// (norm^2 of each pivot when chosen), Q (m x p, optional).
+bool small_qrcp_fits(int64_t m, int64_t n);
+void small_qrcp(const double* A, int64_t m, int64_t n, int64_t lda, int64_t* perm, double* R, double* pnorm,
+                double* Q);
 
 // ---------------------------------------------------------------------------
 // Dense helpers on device buffers (column-major).

@@ -327,6 +327,35 @@ __global__ void __launch_bounds__(kThreads) k_recand(int64_t N, int64_t t, const
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// Exact trailing norms from the residual Y = W - Q[:, :s] R(0:s, :) (already formed):
+// nu_j = cref_j = |y_j|^2 for every unpivoted column, then candidates and trailing mass.
+// Layout 0: Y is k x N col-major (ld k); layout 1: Y^T is N x k col-major (ld N).
+__global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__ Y, int64_t k, int64_t N,
+                                                      int layout, int64_t s, double* nu, double* cref,
+                                                      const int64_t* pos, Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
+        const int64_t pj = pos[j];
+        if (pj < s) continue;
+        double a = 0.0;
+        if (layout == 0)
+            for (int64_t i = 0; i < k; ++i) a = fma(Y[i + j * k], Y[i + j * k], a);
+        else
+            for (int64_t i = 0; i < k; ++i) a = fma(Y[j + i * N], Y[j + i * N], a);
+        nu[j] = a;
+        cref[j] = a;
+        Cand c{a, pj, j};
+        if (better(c, best)) best = c;
+        msum += a;
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 __global__ void k_identity(double* Q, int64_t k) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < k * k) Q[e] = (e % (k + 1) == 0) ? 1.0 : 0.0;
@@ -372,6 +401,26 @@ double WideQrcp::trailing_mass() {
     return s;
 }
 
+double WideQrcp::refresh_exact() {
+    const int64_t s = steps_;
+    if (s == 0) return trailing_mass();
+    DevBuf<double> Y((size_t)(k_ * N_));
+    if (layout_ == Layout::Col) {
+        TTG_CUDA(cudaMemcpy2DAsync(Y.get(), sizeof(double) * k_, W_, sizeof(double) * ld_, sizeof(double) * k_, N_,
+                                   cudaMemcpyDeviceToDevice, stream()));
+        // Y (k x N) -= Q[:, :s] * C with C(t, j) = R[t*N + j], i.e. C = (N x s col-major)^T
+        gemm(false, true, k_, N_, s, Q_.get(), k_, R_.get(), N_, Y.get(), k_, -1.0, 1.0);
+    } else {
+        TTG_CUDA(cudaMemcpy2DAsync(Y.get(), sizeof(double) * N_, W_, sizeof(double) * ld_, sizeof(double) * N_, k_,
+                                   cudaMemcpyDeviceToDevice, stream()));
+        // Y^T (N x k) -= C^T (N x s) * Q[:, :s]^T
+        gemm(false, true, N_, k_, s, R_.get(), N_, Q_.get(), k_, Y.get(), N_, -1.0, 1.0);
+    }
+    TTG_LAUNCH(k_resnorm, ncand_, kThreads, 0, stream(), Y.get(), k_, N_, (int)layout_, s, nu_.get(), cref_.get(),
+               pos_.get(), cand_.get(), mass_.get());
+    return trailing_mass();
+}
+
 void WideQrcp::run_to(int64_t steps) {
     steps = std::min(steps, p_);
     if (steps > cap_) grow(std::min(p_, std::max(steps, 2 * cap_)));
@@ -397,8 +446,12 @@ void WideQrcp::gemv_step(int64_t t) {
     const size_t smem = qbytes + (mode_ == 2 ? sizeof(double) * k_ * (kThreads + 1) : 0);
     auto kern = mode_ == 0 ? k_stream<0> : mode_ == 1 ? k_stream<1> : k_stream<2>;
     allow_smem(kern, smem);
+    prof_begin();
     TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Q_.get(), diag_.get(), piv_.get(),
                R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
+    // written once, and row t of R written.
+    prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
     TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_, t,
                Q_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
     TTG_LAUNCH(k_recand, ncand_, kThreads, 0, stream(), N_, t, nflag_.get(), nu_.get(), pos_.get(),

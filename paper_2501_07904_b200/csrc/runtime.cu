@@ -54,6 +54,63 @@ cudaStream_t stream() {
     return t_stream.s;
 }
 
+namespace {
+struct Prof {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t open = nullptr;
+    double bytes = 0.0;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        TTG_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+};
+thread_local Prof t_prof;
+}  // namespace
+
+bool prof_enabled() { return t_prof.on; }
+void prof_enable(bool on) { t_prof.on = on; }
+
+void prof_begin() {
+    if (!t_prof.on) return;
+    t_prof.open = t_prof.get();
+    TTG_CUDA(cudaEventRecord(t_prof.open, stream()));
+}
+
+void prof_end(double algorithmic_bytes) {
+    if (!t_prof.on || !t_prof.open) return;
+    cudaEvent_t e = t_prof.get();
+    TTG_CUDA(cudaEventRecord(e, stream()));
+    t_prof.pending.emplace_back(t_prof.open, e);
+    t_prof.open = nullptr;
+    t_prof.bytes += algorithmic_bytes;
+}
+
+int64_t prof_read(double* total_ms, double* bytes) {
+    double ms = 0.0;
+    for (auto& pr : t_prof.pending) {
+        TTG_CUDA(cudaEventSynchronize(pr.second));
+        float x = 0.f;
+        TTG_CUDA(cudaEventElapsedTime(&x, pr.first, pr.second));
+        ms += x;
+        t_prof.pool.push_back(pr.first);
+        t_prof.pool.push_back(pr.second);
+    }
+    const int64_t n = (int64_t)t_prof.pending.size();
+    t_prof.pending.clear();
+    *total_ms = ms;
+    *bytes = t_prof.bytes;
+    t_prof.bytes = 0.0;
+    return n;
+}
+
 int sm_count() {
     static thread_local int cached = 0, cached_dev = -1;
     int dev = 0;

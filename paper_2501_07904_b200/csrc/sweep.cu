@@ -163,75 +163,122 @@ struct CutRequest {
     int policy;
 };
 
-CutOut run_cut(WideQrcp& e1, const CutRequest& req) {
-    const int64_t p = e1.p();
+// Pass-2 outputs on the host: pivot order, kept masses, pivot norms, |diag R2|.
+struct Pass2 {
+    std::vector<double> kept, colmass, pnorm, diag;
+    DevBuf<int64_t> perm;  // positions -> R1 row (pass-1 step) index
+};
+
+Pass2 run_pass2(WideQrcp& e1, int64_t s) {
     const int64_t N = e1.N();
-    int64_t s;
-    if (req.policy == 1) s = p;
-    else if (req.fixed) s = req.rank;
-    else s = std::min<int64_t>(p, 16);
-    CutOut out;
-    for (;;) {
-        e1.run_to(s);
-        const double t1 = s == p ? 0.0 : std::max(0.0, e1.trailing_mass());
-        const double b2 = req.budget * req.budget;
-        if (!req.fixed && s < p && t1 > b2) {  // no r <= s can meet the budget yet
-            s = std::min(p, std::max(2 * s, s + 8));
-            ++out.extensions;
-            continue;
-        }
-        // pass 2 on B = R1[:s, :]^T
+    Pass2 out;
+    DevBuf<double> R2((size_t)s * s), colmass(s), kept(s + 1), pn(s);
+    out.perm.alloc(s);
+    if (tsqr_fits(s) && small_qrcp_fits(s, s)) {
+        // QRCP(R_B) with B = R1[:s,:]^T = Q_B R_B: same pivots and |R| as QRCP(B).
+        DevBuf<double> RB((size_t)s * s);
+        tsqr_r(e1.R(), N, s, N, RB.get());
+        small_qrcp(RB.get(), s, s, s, out.perm.get(), R2.get(), pn.get(), nullptr);
+    } else {
         DevBuf<double> B((size_t)N * s);
         TTG_LAUNCH(k_gather_b, (int)cdiv(N * s, 256), 256, 0, stream(), e1.R(), e1.perm(), N, s, B.get());
         TallQrcp e2(B.get(), N, s, N);
         e2.run(s);
-        const int64_t s2 = std::min(N, s);  // pass-2 steps actually available
-        DevBuf<double> R2((size_t)s2 * s), colmass(s), kept(s + 1);
-        e2.extract_r(R2.get(), s2);
-        TTG_LAUNCH(k_kept, 1, 256, 0, stream(), R2.get(), s2, s2, colmass.get(), kept.get());
-        std::vector<double> hk = kept.to_host(s2 + 1);
-        std::vector<double> pn(s2);
-        TTG_CUDA(cudaMemcpyAsync(pn.data(), e2.pivot_norm2(), sizeof(double) * s2, cudaMemcpyDeviceToHost, stream()));
-        std::vector<double> r2h((size_t)s2 * s);
-        R2.download(r2h.data(), r2h.size());
-        sync();
-        const double total = s == p ? hk[(size_t)s2] : hk[(size_t)s2] + t1;
+        e2.extract_r(R2.get(), s);
+        TTG_CUDA(cudaMemcpyAsync(pn.get(), e2.pivot_norm2(), sizeof(double) * s, cudaMemcpyDeviceToDevice, stream()));
+        TTG_CUDA(cudaMemcpyAsync(out.perm.get(), e2.perm(), sizeof(int64_t) * s, cudaMemcpyDeviceToDevice, stream()));
+    }
+    TTG_LAUNCH(k_kept, 1, 256, 0, stream(), R2.get(), s, s, colmass.get(), kept.get());
+    out.kept.resize((size_t)s + 1);
+    out.colmass.resize((size_t)s);
+    out.pnorm.resize((size_t)s);
+    std::vector<double> r2h((size_t)s * s);
+    kept.download(out.kept.data(), (size_t)s + 1);
+    colmass.download(out.colmass.data(), (size_t)s);
+    pn.download(out.pnorm.data(), (size_t)s);
+    R2.download(r2h.data(), r2h.size());
+    sync();
+    out.diag.resize((size_t)s);
+    for (int64_t t = 0; t < s; ++t) out.diag[(size_t)t] = std::abs(r2h[(size_t)(t + t * s)]);
+    return out;
+}
+
+CutOut run_cut(WideQrcp& e1, const CutRequest& req) {
+    const int64_t p = e1.p();
+    int64_t s;
+    if (req.policy == 1) s = p;
+    else if (req.fixed) s = req.rank;
+    else s = std::min<int64_t>(p, 16);
+    const double b2 = req.budget * req.budget;
+    CutOut out;
+    auto extend = [&] {
+        s = std::min(p, std::max(2 * s, s + 8));
+        ++out.extensions;
+    };
+    for (;;) {
+        e1.run_to(s);
+        // Trailing mass of pass 1 = total mass of the R1 rows not yet computed. Tolerance
+        // mode needs it exactly (the rank rule works at the budget^2 level, far below the
+        // rounding noise of downdated norms), fixed rank only for the validity bound.
+        double t1 = 0.0;
+        bool exact = false;
+        if (s < p) {
+            if (!req.fixed) {
+                t1 = e1.refresh_exact();
+                exact = true;
+            } else {
+                t1 = std::max(0.0, e1.trailing_mass());
+            }
+        }
+        if (!req.fixed && s < p && t1 > b2) {  // no r <= s can meet the budget yet
+            extend();
+            continue;
+        }
+        Pass2 p2 = run_pass2(e1, s);
+        const std::vector<double>& hk = p2.kept;
+        // total = kept[p] of the full factorisation = |R1[:s]|^2 + |R1[s:]|^2
+        const double total = s == p ? hk[(size_t)s] : hk[(size_t)s] + t1;
         int64_t r;
         if (req.fixed) {
             r = req.rank;
         } else if (req.budget == 0.0) {  // pick_rank: eps == 0 keeps p
-            r = p;
             if (s < p) { s = p; ++out.extensions; continue; }
-        } else {
+            r = p;
+        } else {  // pick_rank (factor.cpp:512-520) with the same target expression
             const double target = total - b2;
             r = -1;
-            const int64_t hi = std::min(s2, p - 1);
+            const int64_t hi = std::min(s, p - 1);
             for (int64_t c = 1; c <= hi; ++c)
                 if (hk[(size_t)c] >= target) { r = c; break; }
             if (r < 0) {
                 if (s == p) r = p;
-                else { s = std::min(p, std::max(2 * s, s + 8)); ++out.extensions; continue; }
+                else { extend(); continue; }
             }
         }
-        // Early-exit validity: every kept pass-2 pivot must dominate any unseen R1 row.
-        bool valid = true;
+        // Early-exit validity: every kept pass-2 pivot must dominate any unseen R1 row
+        // (each has norm^2 <= t1), so the full factorisation picks the same pivots.
         if (s < p) {
-            const double slack = t1 * (1.0 + 1e-6) + 1e-14 * total;
-            for (int64_t t = 0; t < r && t < s2; ++t)
-                if (!(pn[(size_t)t] >= slack)) { valid = false; break; }
-        }
-        if (!valid) {
-            s = std::min(p, std::max(2 * s, s + 8));
-            ++out.extensions;
-            continue;
+            // The bound is exact (refreshed) or an over-estimate; the factor 4 absorbs the
+            // rounding of the downdated pivot norms, which the 1e-16 guard keeps accurate.
+            auto valid = [&](double bound) {
+                const double slack = 4.0 * bound + 1e-300;
+                for (int64_t t = 0; t < r; ++t)
+                    if (!(p2.pnorm[(size_t)t] >= slack)) return false;
+                return true;
+            };
+            bool ok = valid(t1);
+            if (!ok && !exact) ok = valid(e1.refresh_exact());
+            if (!ok) { extend(); continue; }
         }
         out.rank = r;
         out.steps = s;
-        out.step_error = std::sqrt(std::max(0.0, total - hk[(size_t)r]));
-        out.diag.resize((size_t)r);
-        for (int64_t t = 0; t < r; ++t) out.diag[(size_t)t] = std::abs(r2h[(size_t)(t + t * s2)]);
-        out.sel.alloc(r);
-        TTG_CUDA(cudaMemcpyAsync(out.sel.get(), e2.perm(), sizeof(int64_t) * r, cudaMemcpyDeviceToDevice, stream()));
+        // Residual mass of the truncation computed directly (no kept[p] - kept[r]
+        // cancellation): discarded pass-2 columns plus the unseen R1 rows.
+        double disc = t1;
+        for (int64_t c = r; c < s; ++c) disc += p2.colmass[(size_t)c];
+        out.step_error = std::sqrt(std::max(0.0, disc));
+        out.diag.assign(p2.diag.begin(), p2.diag.begin() + r);
+        out.sel = std::move(p2.perm);
         return out;
     }
 }

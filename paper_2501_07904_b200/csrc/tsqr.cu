@@ -1,0 +1,284 @@
+// Pass 2 without BLAS-2 traffic, and a one-CTA pivoted QR for small matrices.
+//
+// The pass-2 decisions (pivot order P2, |R2|, pivot norms, kept masses) depend on
+// B = R1[:s,:]^T only through B^T B: QRCP(B) and QRCP(R_B) with B = Q_B R_B pick the
+// same pivots and produce the same R up to row signs in exact arithmetic (column norms
+// and their projections are invariant under Q_B^T). R_B comes from a Householder TSQR:
+// every CTA factors a row block of B in shared memory, and the stacked triangles are
+// factored again until one s x s triangle remains -- one HBM pass over B instead of the
+// 2s passes of the in-place algorithm. B is read straight out of R1's row storage (the
+// row order of B only changes rounding), so the gather is not needed either.
+//
+// k_small_qrcp is the reference's qr_col_pivot (factor.cpp:62-135) for a matrix that
+// fits in shared memory: physical column swaps, dlarfg reflectors, sequential norms,
+// the 1e-16 recompute guard -- one launch for the whole factorisation.
+#include <cmath>
+
+#include "engine.hpp"
+
+namespace ttg {
+namespace {
+
+constexpr int kT = 256;
+
+// Householder QR (no pivoting) of the rows x s block X (col-major, ld = rows) held in
+// shared memory; leaves R in the upper triangle. Deterministic fixed-shape reductions.
+__device__ void smem_householder(double* X, int rows, int s, int64_t ld, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int p = min(rows, s);
+    for (int c = 0; c < p; ++c) {
+        double* x = X + c * ld;
+        double part = 0.0;
+        for (int i = c + 1 + threadIdx.x; i < rows; i += blockDim.x) part = fma(x[i], x[i], part);
+        const double sigma = block_sum(part, red);
+        const double alpha = x[c];
+        if (rows - c <= 1 || sigma == 0.0) {
+            __syncthreads();
+            continue;
+        }
+        const double mu = sqrt(fma(alpha, alpha, sigma));
+        const double smu = copysign(mu, alpha);
+        const double v0 = alpha + smu;
+        const double beta = v0 / smu;
+        __syncthreads();
+        for (int i = c + 1 + threadIdx.x; i < rows; i += blockDim.x) x[i] /= v0;
+        if (threadIdx.x == 0) x[c] = -smu;
+        __syncthreads();
+        for (int j = c + 1 + warp; j < s; j += nw) {
+            double* y = X + j * ld;
+            double t = 0.0;
+            for (int i = c + 1 + lane; i < rows; i += 32) t = fma(x[i], y[i], t);
+            t = warp_sum(t);
+            t = beta * (y[c] + t);
+            for (int i = c + 1 + lane; i < rows; i += 32) y[i] = fma(-t, x[i], y[i]);
+            if (lane == 0) y[c] -= t;
+        }
+        __syncthreads();
+    }
+}
+
+// Level 0: block b of B (rows [b*rb, min(N, (b+1)*rb)), all s columns; column t of B is
+// at B + t*ld) -> its s x s triangle written at out + b*s (col-major, ld = ldo).
+__global__ void __launch_bounds__(kT) k_tsqr_leaf(const double* __restrict__ B, int64_t N, int s, int64_t ld,
+                                                  int rb, double* out, int64_t ldo) {
+    extern __shared__ double X[];
+    __shared__ double red[kT / 32];
+    const int64_t r0 = (int64_t)blockIdx.x * rb;
+    const int rows = (int)min((int64_t)rb, N - r0);
+    for (int c = 0; c < s; ++c)
+        for (int i = threadIdx.x; i < rows; i += kT) X[c * rows + i] = B[r0 + i + c * ld];
+    __syncthreads();
+    smem_householder(X, rows, s, rows, red);
+    // upper triangle (rows < s padded with zeros)
+    for (int e = threadIdx.x; e < s * s; e += kT) {
+        const int c = e / s, i = e - c * s;
+        out[(int64_t)blockIdx.x * s + i + c * ldo] = (i <= c && i < rows) ? X[c * rows + i] : 0.0;
+    }
+}
+
+// Levels >= 1: stack g consecutive s x s triangles (rows [b*g*s, ...)) and factor. When
+// the stack does not fit in shared memory it is factored in place in the (scratch) input.
+__global__ void __launch_bounds__(kT) k_tsqr_node(double* in, int64_t nrows, int s, int64_t ldi, int g,
+                                                  int in_smem, double* out, int64_t ldo) {
+    extern __shared__ double X[];
+    __shared__ double red[kT / 32];
+    const int64_t r0 = (int64_t)blockIdx.x * g * s;
+    const int rows = (int)min((int64_t)g * s, nrows - r0);
+    double* base;
+    int64_t ld;
+    if (in_smem) {
+        for (int c = 0; c < s; ++c)
+            for (int i = threadIdx.x; i < rows; i += kT) X[c * rows + i] = in[r0 + i + c * ldi];
+        __syncthreads();
+        base = X;
+        ld = rows;
+    } else {
+        base = in + r0;
+        ld = ldi;
+    }
+    smem_householder(base, rows, s, ld, red);
+    __syncthreads();
+    for (int e = threadIdx.x; e < s * s; e += kT) {
+        const int c = e / s, i = e - c * s;
+        out[(int64_t)blockIdx.x * s + i + c * ldo] = (i <= c && i < rows) ? base[c * ld + i] : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One-CTA qr_col_pivot of an m x n matrix (col-major, ld = m) held in smem.
+// Outputs: perm[n] (position -> source column), R over positions (p x n, ld = p),
+// pnorm[p] (norm^2 of the pivot when chosen), optional Q (m x p, ld = m) formed by
+// backward accumulation (factor.cpp:116-133).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_small_qrcp(const double* __restrict__ A, int m, int n, int64_t lda,
+                                                    int64_t* perm_out, double* R, double* pnorm, double* Q,
+                                                    int want_q) {
+    extern __shared__ double sm[];
+    double* X = sm;                       // m x n
+    double* nu = X + (size_t)m * n;       // n
+    double* cref = nu + n;                // n
+    double* beta = cref + n;              // p
+    double* tq = beta + min(m, n);        // n
+    int* perm = (int*)(tq + n);           // n
+    __shared__ double red[16];
+    __shared__ int spiv;
+    const int p = min(m, n);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = 0; c < n; ++c)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) X[c * m + i] = A[i + c * lda];
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double a = 0.0;
+        for (int i = 0; i < m; ++i) a = __dadd_rn(a, __dmul_rn(X[j * m + i], X[j * m + i]));
+        nu[j] = a;
+        cref[j] = a;
+        perm[j] = j;
+    }
+    __syncthreads();
+    for (int k = 0; k < p; ++k) {
+        if (threadIdx.x == 0) {  // strict '>' scan from position k (factor.cpp:85-87)
+            int piv = k;
+            for (int j = k + 1; j < n; ++j)
+                if (nu[j] > nu[piv]) piv = j;
+            spiv = piv;
+            pnorm[k] = nu[piv];
+        }
+        __syncthreads();
+        const int piv = spiv;
+        if (piv != k) {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const double t = X[k * m + i];
+                X[k * m + i] = X[piv * m + i];
+                X[piv * m + i] = t;
+            }
+            if (threadIdx.x == 0) {
+                int ti = perm[k]; perm[k] = perm[piv]; perm[piv] = ti;
+                double td = nu[k]; nu[k] = nu[piv]; nu[piv] = td;
+                td = cref[k]; cref[k] = cref[piv]; cref[piv] = td;
+            }
+        }
+        __syncthreads();
+        // make_householder (factor.cpp:24-38)
+        double* x = X + k * m;
+        double part = 0.0;
+        for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) part = fma(x[i], x[i], part);
+        const double sigma = block_sum(part, red);
+        const double alpha = x[k];
+        double b = 0.0;
+        if (m - k > 1 && sigma != 0.0) {
+            const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sigma));
+            const double smu = copysign(mu, alpha);
+            const double v0 = __dadd_rn(alpha, smu);
+            b = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+            __syncthreads();
+            for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) x[i] = __ddiv_rn(x[i], v0);
+            if (threadIdx.x == 0) x[k] = -smu;
+        }
+        if (threadIdx.x == 0) beta[k] = b;
+        __syncthreads();
+        // apply_reflector to columns k+1..n-1 (factor.cpp:43-58)
+        if (b != 0.0)
+            for (int j = k + 1 + warp; j < n; j += nw) {
+                double* y = X + j * m;
+                double t = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) t = fma(x[i], y[i], t);
+                t = warp_sum(t);
+                t = __dmul_rn(__dadd_rn(y[k], t), b);
+                for (int i = k + 1 + lane; i < m; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(t, x[i]));
+                if (lane == 0) y[k] = __dsub_rn(y[k], t);
+            }
+        __syncthreads();
+        // downdate + guard (factor.cpp:98-107), one warp per column
+        for (int j = k + 1 + warp; j < n; j += nw) {
+            double nv = 0.0;
+            if (lane == 0) {
+                const double rkj = X[j * m + k];
+                nv = __dsub_rn(nu[j], __dmul_rn(rkj, rkj));
+            }
+            nv = __shfl_sync(0xffffffffu, nv, 0);
+            if (nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0) {
+                double a = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) a = fma(X[j * m + i], X[j * m + i], a);
+                a = warp_sum(a);
+                nv = a;
+                if (lane == 0) cref[j] = a;
+            }
+            if (lane == 0) nu[j] = nv;
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < p * n; e += blockDim.x) {
+        const int c = e / p, i = e - c * p;
+        R[i + (int64_t)c * p] = i <= c ? X[c * m + i] : 0.0;
+    }
+    for (int j = threadIdx.x; j < n; j += blockDim.x) perm_out[j] = perm[j];
+    if (!want_q) return;
+    // economy Q, backward accumulation; Q lives in global memory (m x p)
+    for (int e = threadIdx.x; e < m * p; e += blockDim.x) {
+        const int c = e / m, i = e - c * m;
+        Q[i + (int64_t)c * m] = i == c ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int k = p - 1; k >= 0; --k) {
+        const double bk = beta[k];
+        if (bk == 0.0) continue;
+        const double* v = X + k * m;
+        for (int j = k + warp; j < p; j += nw) {
+            double* c = Q + (int64_t)j * m;
+            double t = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) t = fma(v[i], c[i], t);
+            t = warp_sum(t);
+            t = __dmul_rn(__dadd_rn(c[k], t), bk);
+            for (int i = k + 1 + lane; i < m; i += 32) c[i] = __dsub_rn(c[i], __dmul_rn(t, v[i]));
+            if (lane == 0) c[k] = __dsub_rn(c[k], t);
+        }
+        __syncthreads();
+    }
+    (void)tq;
+}
+
+}  // namespace
+
+size_t small_qrcp_smem(int64_t m, int64_t n) {
+    const int64_t p = std::min(m, n);
+    return sizeof(double) * (size_t)(m * n + 3 * n + p) + sizeof(int) * (size_t)n + 64;
+}
+
+bool small_qrcp_fits(int64_t m, int64_t n) { return small_qrcp_smem(m, n) <= 220 * 1024; }
+
+void small_qrcp(const double* A, int64_t m, int64_t n, int64_t lda, int64_t* perm, double* R, double* pnorm,
+                double* Q) {
+    const size_t smem = small_qrcp_smem(m, n);
+    allow_smem(k_small_qrcp, smem);
+    TTG_LAUNCH(k_small_qrcp, 1, 512, smem, stream(), A, (int)m, (int)n, lda, perm, R, pnorm, Q, Q ? 1 : 0);
+}
+
+bool tsqr_fits(int64_t s) { return s <= 160; }
+
+void tsqr_r(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout) {
+    // rows per leaf block: a multiple of s, >= 128, within ~200 KB of shared memory
+    int rb = (int)std::max<int64_t>(s, 128);
+    while ((int64_t)rb * 2 * s * 8 <= 160 * 1024 && rb < 1024) rb *= 2;
+    const int64_t nb = cdiv(N, rb);
+    DevBuf<double> lvl((size_t)(nb * s * s));
+    const size_t smem0 = sizeof(double) * (size_t)rb * s;
+    allow_smem(k_tsqr_leaf, smem0);
+    TTG_LAUNCH(k_tsqr_leaf, (int)nb, kT, smem0, stream(), B, N, (int)s, ld, rb, lvl.get(), nb * s);
+    int64_t rows = nb * s;
+    const int g = (int)std::max<int64_t>(2, std::min<int64_t>(16, (160 * 1024) / (8 * s * s)));
+    while (rows > s) {
+        const int64_t nbl = cdiv(rows, (int64_t)g * s);
+        DevBuf<double> nxt((size_t)(nbl * s * s));
+        const size_t need = sizeof(double) * (size_t)g * s * s;
+        const bool fits = need <= 200 * 1024;
+        const size_t smem = fits ? need : 0;
+        allow_smem(k_tsqr_node, smem);
+        TTG_LAUNCH(k_tsqr_node, (int)nbl, kT, smem, stream(), lvl.get(), rows, (int)s, rows, g, fits ? 1 : 0,
+                   nxt.get(), nbl * s);
+        lvl = std::move(nxt);
+        rows = nbl * s;
+    }
+    TTG_CUDA(cudaMemcpyAsync(Rout, lvl.get(), sizeof(double) * s * s, cudaMemcpyDeviceToDevice, stream()));
+}
+
+}  // namespace ttg
