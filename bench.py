@@ -61,7 +61,7 @@ def workload(cfg: int):
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -77,7 +77,7 @@ class Clocks:
         except OSError:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t_begin=None, t_end=None):
         if not self.proc:
             return None
         self.proc.terminate()
@@ -87,6 +87,17 @@ class Clocks:
             self.proc.kill()
             out, _ = self.proc.communicate()
         rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if t_begin is not None:
+            import datetime
+            inside = []
+            for r in rows:
+                try:
+                    ts = datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if t_begin - 0.15 <= ts <= t_end + 0.15:
+                    inside.append(r)
+            rows = inside or rows[-2:]
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
@@ -212,6 +223,10 @@ def run_ours(args):
             info[method] = res
         return info
 
+    # The nvidia-smi sampler starts before the warm-up so its start-up (fork + NVML init)
+    # never overlaps the timed region; only samples inside the region are kept.
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         step_device()
     # ---- timed region: tensor resident in HBM ----
@@ -219,19 +234,21 @@ def run_ours(args):
     d0, d1 = C_double(), C_double()
     lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))  # discard warm-up records
     launches0 = lib().ttg_kernel_launches()
-    clocks = Clocks(local)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    t_begin = time.time()
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        ts = time.perf_counter()
         step_device()
+        log(f"step {i}: {1e3 * (time.perf_counter() - ts):.1f} ms host wall")
     e1.record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    t_end = time.time()
+    clk = clocks.stop(t_begin, t_end)
     if dist:
         dist.barrier()
     launches = lib().ttg_kernel_launches() - launches0
@@ -319,7 +336,7 @@ def C_double():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])

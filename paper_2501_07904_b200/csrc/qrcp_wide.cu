@@ -36,6 +36,21 @@ __device__ __forceinline__ double ld_w(const double* __restrict__ W, int64_t ld,
     return layout == 0 ? W[i + j * ld] : W[i * ld + j];
 }
 
+// MODE 2 tile: columns [j0, j0+256) of a contiguous k x N (k < 64) matrix into smem as
+// tile[i*(256+1) + c]; one warp per column segment (coalesced, no integer division).
+__device__ __forceinline__ void load_tile_small_k(const double* __restrict__ W, int64_t k, int64_t N, int64_t j0,
+                                                  double* tile) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nc = (int)min((int64_t)kThreads, N - j0);
+    const int kk = (int)k;
+    __syncthreads();
+    for (int c = warp; c < nc; c += kThreads / 32) {
+        const double* src = W + (j0 + c) * k;
+        for (int i = lane; i < kk; i += 32) tile[i * (kThreads + 1) + c] = src[i];
+    }
+    __syncthreads();
+}
+
 // Per-column epilogue shared by the init and stream kernels.
 struct ColOut {
     Cand best;
@@ -76,13 +91,7 @@ __global__ void __launch_bounds__(kThreads) k_init(const double* __restrict__ W,
             const int64_t j = j0 + threadIdx.x;
             double a = 0.0;
             if (MODE == 2) {
-                const int64_t ncols = min((int64_t)kThreads, N - j0);
-                __syncthreads();
-                for (int64_t e = threadIdx.x; e < ncols * k; e += kThreads) {
-                    const int64_t c = e / k, i = e - c * k;
-                    tile[i * (kThreads + 1) + c] = W[j0 * k + e];
-                }
-                __syncthreads();
+                load_tile_small_k(W, k, N, j0, tile);
                 if (j < N)
                     for (int64_t i = 0; i < k; ++i) {
                         const double v = tile[i * (kThreads + 1) + threadIdx.x];
@@ -253,13 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
         for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
             const int64_t j = j0 + threadIdx.x;
             if (MODE == 2) {
-                const int64_t ncols = min((int64_t)kThreads, N - j0);
-                __syncthreads();
-                for (int64_t e = threadIdx.x; e < ncols * k; e += kThreads) {
-                    const int64_t c = e / k, i = e - c * k;
-                    tile[i * (kThreads + 1) + c] = W[j0 * k + e];
-                }
-                __syncthreads();
+                load_tile_small_k(W, k, N, j0, tile);
             }
             if (j >= N) continue;
             const int64_t pj = pos[j];
@@ -304,6 +307,39 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
         }
         s = warp_sum(s);
         if (lane == 0) { nu[j] = s; cref[j] = s; }
+    }
+}
+
+// D1 for k <= 64: the trailing norm is |Q_{t+1}[:, t+1:]^T w_j|^2, the sum of squares of
+// rows t+1.. of the reflected column -- exactly the quantity factor.cpp:103-105 sums.
+// The k x (k-t-1) complement of the explicit Q sits in shared memory; one thread per
+// flagged column keeps w_j in registers.
+__global__ void __launch_bounds__(kThreads) k_guard_perp(const double* __restrict__ W, int64_t k, int64_t N,
+                                                         int64_t ld, int layout, int64_t t,
+                                                         const double* __restrict__ Q, const int64_t* flags,
+                                                         const int* nflag, double* nu, double* cref) {
+    __shared__ double qp[64 * 64];
+    const int nf = *nflag;
+    if (nf == 0) return;
+    const int kk = (int)k, m = (int)(k - t - 1);
+    for (int e = threadIdx.x; e < kk * m; e += kThreads) qp[e] = Q[(t + 1) * k + e];
+    __syncthreads();
+    for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
+        const int64_t j = flags[f];
+        double w[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) w[i] = i < kk ? ld_w(W, ld, layout, i, j) : 0.0;
+        double s = 0.0;
+        for (int c = 0; c < m; ++c) {
+            const double* qc = qp + c * kk;
+            double d = 0.0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+                if (i < kk) d = fma(qc[i], w[i], d);
+            s = fma(d, d, s);
+        }
+        nu[j] = s;
+        cref[j] = s;
     }
 }
 
@@ -452,8 +488,12 @@ void WideQrcp::gemv_step(int64_t t) {
     // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
     // written once, and row t of R written.
     prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
-    TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_, t,
-               Q_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
+    if (k_ <= 64)
+        TTG_LAUNCH(k_guard_perp, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_,
+                   t, Q_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
+    else
+        TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_, t,
+                   Q_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
     TTG_LAUNCH(k_recand, ncand_, kThreads, 0, stream(), N_, t, nflag_.get(), nu_.get(), pos_.get(),
                cand_.get(), mass_.get());
 }
