@@ -153,6 +153,12 @@ ttg_status ttg_reconstruct(const double* cores, const int64_t* dims, const int64
                            int64_t element_cap, double* out);
 ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, double* out);
 ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, double* out);
+/* |x - y|_2 over count entries (verify_bound's achieved error, tt_decomp.cpp:449-454). */
+ttg_status ttg_diff_norm(const double* x, const double* y, int64_t count, double* out);
+/* C = op(A) op(B) on the device (DMMA tiles), host buffers, column-major; op = transpose
+ * when ta/tb is nonzero (kernels::matmul, include/ttutv/kernels.hpp:21). */
+ttg_status ttg_matmul(const double* a, int64_t a_rows, int64_t a_cols, int ta, const double* b,
+                      int64_t b_rows, int64_t b_cols, int tb, double* c);
 
 #ifdef __cplusplus
 }

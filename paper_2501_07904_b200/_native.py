@@ -94,6 +94,9 @@ SIGNATURES = {
     "ttg_reconstruct": (C.c_int, [c_double_p, c_int64_p, c_int64_p, C.c_int, C.c_int64, c_double_p]),
     "ttg_frobenius_norm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, c_double_p]),
     "ttg_rse": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
+    "ttg_diff_norm": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
+    "ttg_matmul": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, c_double_p, C.c_int64, C.c_int64, C.c_int,
+                             c_double_p]),
 }
 
 _lib = None

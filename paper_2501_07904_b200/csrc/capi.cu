@@ -7,6 +7,7 @@
 
 #include "../../include/ttutv_b200.h"
 #include "sweep.hpp"
+#include "utv.hpp"
 
 struct ttg_result {
     ttg::TTResult r;
@@ -260,17 +261,51 @@ ttg_status ttg_qr_col_pivot(const double* a, int64_t m, int64_t n, double* q, do
     });
 }
 
-ttg_status ttg_utv(const double*, int64_t, int64_t, int, int, double*, double*, double*) {
-    return guard([&] { ttg::fail(7, "ttg_utv: not implemented yet"); });
+ttg_status ttg_utv(const double* a, int64_t m, int64_t n, int lower, int refine, double* u, double* t, double* v) {
+    return guard([&] {
+        if (m <= 0 || n <= 0) ttg::argument_error("utv: empty matrix");
+        DeviceInput in(a, m * n, false);
+        ttg::DUtv f = ttg::utv(in.ptr, m, n, lower != 0, refine);
+        if (u) f.u.buf.download(u, (size_t)(f.u.rows * f.u.cols));
+        if (t) f.t.buf.download(t, (size_t)(f.t.rows * f.t.cols));
+        if (v) f.v.buf.download(v, (size_t)(f.v.rows * f.v.cols));
+        ttg::sync();
+    });
 }
 
-ttg_status ttg_svd(const double*, int64_t, int64_t, int, double, double*, double*, double*) {
-    return guard([&] { ttg::fail(7, "ttg_svd: not implemented yet"); });
+ttg_status ttg_svd(const double* a, int64_t m, int64_t n, int max_sweeps, double pair_tol, double* u, double* s,
+                   double* v) {
+    return guard([&] {
+        if (m <= 0 || n <= 0) ttg::argument_error("svd: empty matrix");
+        DeviceInput in(a, m * n, false);
+        ttg::DSvd f = ttg::svd(in.ptr, m, n, max_sweeps, pair_tol);
+        if (u) f.u.buf.download(u, (size_t)(f.u.rows * f.u.cols));
+        if (v) f.v.buf.download(v, (size_t)(f.v.rows * f.v.cols));
+        if (s) std::copy(f.s.begin(), f.s.end(), s);
+        ttg::sync();
+    });
 }
 
-ttg_status ttg_truncate(int, const double*, const double*, const double*, int64_t, int64_t, int64_t, int64_t, double,
-                        int64_t*, double*, double*, double*, double*) {
-    return guard([&] { ttg::fail(7, "ttg_truncate: not implemented yet"); });
+ttg_status ttg_truncate(int kind, const double* u, const double* t, const double* v, int64_t m, int64_t n, int64_t p,
+                        int64_t rank, double eps, int64_t* rank_out, double* residual, double* u1, double* t11,
+                        double* v1) {
+    return guard([&] {
+        if (kind < 0 || kind > 2) ttg::argument_error("unknown factor kind");
+        if (rank < 0 || rank > p)
+            ttg::argument_error("rank " + std::to_string(rank) + " out of range 1.." + std::to_string(p));
+        DeviceInput dt(t, kind == 0 ? p : p * p, false);
+        const ttg::DTrunc tr = ttg::truncate_rank(kind, dt.ptr, p, rank, eps);
+        const int64_t r = tr.rank;
+        *rank_out = r;
+        *residual = tr.residual;
+        // leading blocks (factor.cpp:458-469): column-major prefixes of the caller's factors
+        if (u1) std::memcpy(u1, u, sizeof(double) * (size_t)(m * r));
+        if (v1) std::memcpy(v1, v, sizeof(double) * (size_t)(n * r));
+        if (t11)
+            for (int64_t j = 0; j < r; ++j)
+                for (int64_t i = 0; i < r; ++i)
+                    t11[i + j * r] = kind == 0 ? (i == j ? t[i] : 0.0) : t[i + j * p];
+    });
 }
 
 ttg_status ttg_reconstruct(const double* cores, const int64_t* dims, const int64_t* ranks, int d, int64_t element_cap,
@@ -302,6 +337,28 @@ ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, d
     return guard([&] {
         DeviceInput in(a, count, a_on_device != 0);
         *out = std::sqrt(ttg::sum_squares(in.ptr, count));
+    });
+}
+
+ttg_status ttg_diff_norm(const double* x, const double* y, int64_t count, double* out) {
+    return guard([&] {
+        DeviceInput a(x, count, false), b(y, count, false);
+        *out = std::sqrt(ttg::diff_squares(a.ptr, b.ptr, count));
+    });
+}
+
+ttg_status ttg_matmul(const double* a, int64_t ar, int64_t ac, int ta, const double* b, int64_t br, int64_t bc, int tb,
+                      double* c) {
+    return guard([&] {
+        const int64_t m = ta ? ac : ar, k = ta ? ar : ac, kb = tb ? bc : br, n = tb ? br : bc;
+        if (k != kb) ttg::argument_error("matmul inner dimensions do not match");
+        ttg::DevBuf<double> A((size_t)(ar * ac)), B((size_t)(br * bc)), Cc((size_t)(m * n));
+        A.upload(a, (size_t)(ar * ac));
+        B.upload(b, (size_t)(br * bc));
+        if (k == 0) Cc.zero();
+        else ttg::gemm(ta != 0, tb != 0, m, n, k, A.get(), ar, B.get(), br, Cc.get(), m);
+        Cc.download(c, (size_t)(m * n));
+        ttg::sync();
     });
 }
 

@@ -40,13 +40,24 @@ __device__ __forceinline__ double ld_w(const double* __restrict__ W, int64_t ld,
 // tile[i*(256+1) + c]; one warp per column segment (coalesced, no integer division).
 __device__ __forceinline__ void load_tile_small_k(const double* __restrict__ W, int64_t k, int64_t N, int64_t j0,
                                                   double* tile) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // The tile is contiguous in memory (ld == k): flat coalesced loads, element e of the
+    // tile is (row e % k, column e / k), tracked incrementally (no division per element).
     const int nc = (int)min((int64_t)kThreads, N - j0);
     const int kk = (int)k;
+    const int total = nc * kk;
+    const int dq = kThreads / kk, dr = kThreads - dq * kk;
+    int c = threadIdx.x / kk, i = threadIdx.x - c * kk;
+    const double* __restrict__ base = W + j0 * k;
     __syncthreads();
-    for (int c = warp; c < nc; c += kThreads / 32) {
-        const double* src = W + (j0 + c) * k;
-        for (int i = lane; i < kk; i += 32) tile[i * (kThreads + 1) + c] = src[i];
+#pragma unroll 8
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        tile[i * (kThreads + 1) + c] = __ldg(base + e);
+        c += dq;
+        i += dr;
+        if (i >= kk) {
+            i -= kk;
+            ++c;
+        }
     }
     __syncthreads();
 }

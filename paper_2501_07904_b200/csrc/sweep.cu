@@ -23,6 +23,7 @@
 #include <sstream>
 
 #include "sweep.hpp"
+#include "utv.hpp"
 
 namespace ttg {
 namespace {
@@ -308,6 +309,225 @@ void set_core(TTResult& res, size_t k, DevBuf<double>&& buf, int64_t r0, int64_t
     res.core_dims[k] = {r0, n, r1};
 }
 
+// ---- general path: any method / sweep / refine_passes / retain -------------------------
+
+// kept[j+1] = kept[j] + |L(:, j)|^2 over all p rows (column_mass, tt_decomp.cpp:102-109)
+__global__ void k_colmass_full(const double* __restrict__ L, int64_t p, double* part, double* kept) {
+    for (int64_t j = threadIdx.x; j < p; j += blockDim.x) {
+        double a = 0.0;
+        for (int64_t i = 0; i < p; ++i) a = __dadd_rn(a, __dmul_rn(L[i + j * p], L[i + j * p]));
+        part[j] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        kept[0] = 0.0;
+        for (int64_t j = 0; j < p; ++j) {
+            acc = __dadd_rn(acc, part[j]);
+            kept[j + 1] = acc;
+        }
+    }
+}
+
+// B(i_d, ..., i_1) = A(i_1, ..., i_d) (reverse_indices, tensor_ops.cpp:128-143)
+struct Dims64 {
+    int d;
+    int64_t n[32];
+};
+__global__ void k_reverse_indices(const double* __restrict__ A, Dims64 dims, int64_t total, double* B) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        // e indexes B, whose mode k is A's mode d-1-k; rebuild A's linear index
+        int64_t rest = e, src = 0, stride_a[32];
+        int64_t s = 1;
+        for (int k = 0; k < dims.d; ++k) {
+            stride_a[k] = s;
+            s *= dims.n[k];
+        }
+        for (int k = 0; k < dims.d; ++k) {
+            const int64_t nk = dims.n[dims.d - 1 - k];
+            const int64_t ik = rest % nk;
+            rest /= nk;
+            src += ik * stride_a[dims.d - 1 - k];
+        }
+        B[e] = A[src];
+    }
+}
+
+// out(b, i, a) = in(a, i, b): core of the reversed train (reverse_tt, tt.cpp:108-123)
+__global__ void k_reverse_core(const double* __restrict__ in, int64_t rl, int64_t mid, int64_t rr, double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rl * mid * rr) return;
+    const int64_t a = e % rl, i = (e / rl) % mid, b = e / (rl * mid);
+    out[b + i * rr + a * rr * mid] = in[e];
+}
+
+DevBuf<double> leading_block(const double* t, int64_t p, int64_t r) {
+    DevBuf<double> o((size_t)(r * r));
+    if (r > 0)
+        TTG_CUDA(cudaMemcpy2DAsync(o.get(), sizeof(double) * r, t, sizeof(double) * p, sizeof(double) * r, r,
+                                   cudaMemcpyDeviceToDevice, stream()));
+    return o;
+}
+
+DevBuf<double> prefix(const double* x, int64_t count) {
+    DevBuf<double> o((size_t)count);
+    if (count > 0)
+        TTG_CUDA(cudaMemcpyAsync(o.get(), x, sizeof(double) * count, cudaMemcpyDeviceToDevice, stream()));
+    return o;
+}
+
+// One factorisation + truncation of a cut (factor level, any refine / method).
+struct GenCut {
+    int64_t r = 0;
+    double res = 0.0;
+    DevBuf<double> u1, t11, v1;  // m x r, r x r, n x r
+    DMat fu, ft;                 // full U and T (kept for Alg. 4 full column)
+};
+
+GenCut general_cut(int method, const double* c, int64_t m, int64_t n, int refine, bool fixed, int64_t want,
+                   double budget, bool keep_full) {
+    GenCut g;
+    const int64_t p = std::min(m, n);
+    DMat u, t, v;
+    int kind;
+    DevBuf<double> sdev;
+    if (method == 0) {
+        DSvd f = svd(c, m, n, 60, 1e-14);
+        kind = 0;
+        sdev.alloc((size_t)p);
+        sdev.upload(f.s.data(), (size_t)p);
+        u = std::move(f.u);
+        v = std::move(f.v);
+    } else {
+        DUtv f = utv(c, m, n, method == 1, refine);
+        kind = method;
+        u = std::move(f.u);
+        t = std::move(f.t);
+        v = std::move(f.v);
+    }
+    const double* tp = kind == 0 ? sdev.get() : t.get();
+    const DTrunc tr = truncate_rank(kind, tp, p, fixed ? want : 0, budget);
+    g.r = tr.rank;
+    g.res = tr.residual;
+    g.u1 = prefix(u.get(), m * g.r);
+    g.v1 = prefix(v.get(), n * g.r);
+    if (kind == 0) {
+        std::vector<double> hs = sdev.to_host((size_t)p), d((size_t)(g.r * g.r), 0.0);
+        for (int64_t i = 0; i < g.r; ++i) d[(size_t)(i + i * g.r)] = hs[(size_t)i];
+        g.t11.alloc(d.size());
+        g.t11.upload(d.data(), d.size());
+    } else {
+        g.t11 = leading_block(t.get(), p, g.r);
+    }
+    if (keep_full) {
+        g.fu = std::move(u);
+        g.ft = std::move(t);
+    }
+    return g;
+}
+
+void general_sweep(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg, const Resolved& mode,
+                   TTResult& res) {
+    const int64_t d = (int64_t)dims.size();
+    const int64_t total_n = product(dims, 0, dims.size());
+    DevBuf<double> carry;
+    if (cfg.sweep == 0) {  // sweep_l2r (tt_decomp.cpp:156-211) with svd or ulv
+        const double* c = a;
+        int64_t m = dims[0], n = total_n / dims[0], r_prev = 1;
+        for (int64_t k = 1; k <= d - 1; ++k) {
+            const int64_t p = std::min(m, n);
+            int64_t want = 0;
+            if (mode.fixed) {
+                const int64_t req = mode.ranks[(size_t)k];
+                want = std::min(req, p);
+                if (want < req)
+                    res.warnings.push_back("cut " + std::to_string(k) + ": requested rank " + std::to_string(req) +
+                                           " clamped to " + std::to_string(want));
+            }
+            GenCut g = general_cut(cfg.method, c, m, n, cfg.refine, mode.fixed, want,
+                                   mode.fixed ? 0.0 : mode.budgets[(size_t)(k - 1)], false);
+            const int64_t r = g.r;
+            res.step_errors[(size_t)(k - 1)] = g.res;
+            res.ranks_chosen[(size_t)k] = r;
+            res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, p, r, 0, {}};
+            DevBuf<double> next((size_t)(r * n));
+            gemm(false, true, r, n, r, g.t11.get(), r, g.v1.get(), n, next.get(), r);  // T11 V1^T (:192)
+            set_core(res, (size_t)(k - 1), std::move(g.u1), r_prev, dims[(size_t)(k - 1)], r);
+            r_prev = r;
+            if (k < d - 1) {
+                carry = std::move(next);
+                c = carry.get();
+                m = r * dims[(size_t)k];
+                n = n / dims[(size_t)k];
+            } else {
+                set_core(res, (size_t)(d - 1), std::move(next), r, dims[(size_t)(d - 1)], 1);
+            }
+        }
+        return;
+    }
+    // sweep_r2l (tt_decomp.cpp:216-339) with svd, urv or ulv (+ retain policy)
+    const double* c = a;
+    int64_t M = total_n / dims[(size_t)(d - 1)], n = dims[(size_t)(d - 1)], r_next = 1;
+    const bool full_column = cfg.method == 1 && cfg.retain == 1;
+    for (int64_t k = d; k >= 2; --k) {
+        const int64_t p = std::min(M, n);
+        int64_t want = 0;
+        if (mode.fixed) {
+            const int64_t req = mode.ranks[(size_t)(k - 1)];
+            want = std::min(req, p);
+            if (want < req)
+                res.warnings.push_back("cut " + std::to_string(k - 1) + ": requested rank " + std::to_string(req) +
+                                       " clamped to " + std::to_string(want));
+        }
+        const double budget = mode.fixed ? 0.0 : mode.budgets[(size_t)(k - 2)];
+        int64_t r;
+        double step_err;
+        DevBuf<double> next, v1;
+        if (full_column) {  // Alg. 4 keeping L(:, :r): carry = U L(:, :r) (:241-270)
+            GenCut g = general_cut(1, c, M, n, cfg.refine, true, p, 0.0, true);
+            DevBuf<double> part((size_t)p), kept((size_t)p + 1);
+            TTG_LAUNCH(k_colmass_full, 1, 256, 0, stream(), g.ft.get(), p, part.get(), kept.get());
+            const std::vector<double> hk = kept.to_host((size_t)p + 1);
+            if (mode.fixed) {
+                r = want;
+            } else {
+                r = p;
+                if (budget > 0.0) {
+                    const double target = hk[(size_t)p] - budget * budget;
+                    for (int64_t cand = 1; cand < p; ++cand)
+                        if (hk[(size_t)cand] >= target) { r = cand; break; }
+                }
+            }
+            step_err = std::sqrt(std::max(0.0, hk[(size_t)p] - hk[(size_t)r]));
+            next.alloc((size_t)(M * r));
+            gemm(false, false, M, r, p, g.fu.get(), M, g.ft.get(), p, next.get(), M);
+            v1 = prefix(g.v1.get(), n * r);
+        } else {
+            GenCut g = general_cut(cfg.method, c, M, n, cfg.refine, mode.fixed, want, budget, false);
+            r = g.r;
+            step_err = g.res;
+            next.alloc((size_t)(M * r));
+            gemm(false, false, M, r, r, g.u1.get(), M, g.t11.get(), r, next.get(), M);  // U1 T11 (:302)
+            v1 = std::move(g.v1);
+        }
+        res.step_errors[(size_t)(k - 2)] = step_err;
+        res.ranks_chosen[(size_t)(k - 1)] = r;
+        res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, p, r, 0, {}};
+        DevBuf<double> core((size_t)(r * n));  // V1^T (core_from_left_unfolding, :77-80)
+        transpose(v1.get(), n, r, n, core.get(), r);
+        set_core(res, (size_t)(k - 1), std::move(core), r, dims[(size_t)(k - 1)], r_next);
+        r_next = r;
+        if (k > 2) {
+            carry = std::move(next);
+            c = carry.get();
+            M = M / dims[(size_t)(k - 2)];
+            n = dims[(size_t)(k - 2)] * r;
+        } else {
+            set_core(res, 0, std::move(next), 1, dims[0], r);
+        }
+    }
+}
+
 }  // namespace
 
 TTResult decompose(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg) {
@@ -318,6 +538,44 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
         if (dims[k] < 1)
             argument_error("shape dim " + std::to_string(k + 1) + " is " + std::to_string(dims[k]) + ", must be >= 1");
     const int64_t total_n = product(dims, 0, dims.size());
+    if (cfg.method == 2 && cfg.sweep == 0) {
+        // left_orthogonal_via_urv (tt_decomp.cpp:408-427): sweep the index-reversed tensor
+        // right to left with the reversed rank chain / weights, then reverse the train.
+        if (d > 32) argument_error("order above 32 is not supported by the device reversal");
+        SweepConfig c2 = cfg;
+        c2.sweep = 1;
+        std::reverse(c2.ranks.begin(), c2.ranks.end());
+        std::reverse(c2.weights.begin(), c2.weights.end());
+        Dims64 dd{(int)d, {}};
+        for (int64_t k = 0; k < d; ++k) dd.n[k] = dims[(size_t)k];
+        DevBuf<double> rev((size_t)total_n);
+        TTG_LAUNCH(k_reverse_indices, (int)std::min<int64_t>(cdiv(total_n, 256), (int64_t)sm_count() * 16), 256, 0,
+                   stream(), a, dd, total_n, rev.get());
+        TTResult r = decompose(rev.get(), std::vector<int64_t>(dims.rbegin(), dims.rend()), c2);
+        TTResult out;
+        out.dims = dims;
+        out.cores.resize((size_t)d);
+        out.core_dims.resize((size_t)d);
+        for (int64_t k = 0; k < d; ++k) {
+            const auto& cd = r.core_dims[(size_t)(d - 1 - k)];
+            DevBuf<double> core((size_t)(cd[0] * cd[1] * cd[2]));
+            TTG_LAUNCH(k_reverse_core, (int)cdiv(cd[0] * cd[1] * cd[2], 256), 256, 0, stream(),
+                       r.cores[(size_t)(d - 1 - k)].get(), cd[0], cd[1], cd[2], core.get());
+            set_core(out, (size_t)k, std::move(core), cd[2], cd[1], cd[0]);
+        }
+        out.step_errors.assign(r.step_errors.rbegin(), r.step_errors.rend());
+        out.ranks_chosen.assign(r.ranks_chosen.rbegin(), r.ranks_chosen.rend());
+        out.ranks_requested.assign(r.ranks_requested.rbegin(), r.ranks_requested.rend());
+        out.cuts.assign(r.cuts.rbegin(), r.cuts.rend());
+        out.bound = r.bound;
+        out.bound_kind = r.bound_kind;
+        out.input_norm = r.input_norm;
+        out.warnings = r.warnings;
+        out.warnings.push_back("left-orthogonal train built by sweeping the reversed tensor");
+        sync();
+        out.wall_ms = std::chrono::duration<double, std::milli>(Clock::now() - start).count();
+        return out;
+    }
     const bool plain = cfg.method == 1 && cfg.sweep == 1 && cfg.retain == 0;  // bound_kind_for
     const bool rss = !plain;
 
@@ -353,11 +611,15 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
     }
     check_refine(cfg.refine);
     const bool fast = cfg.refine == 1 && ((cfg.method == 1 && cfg.sweep == 0) || (cfg.method == 2 && cfg.sweep == 1));
-    if (!fast) fail(7, "this (method, sweep, refine_passes) combination is not implemented on the device yet");
 
     res.step_errors.assign((size_t)(d - 1), 0.0);
     res.ranks_chosen.assign((size_t)d + 1, 1);
     res.cuts.resize((size_t)(d - 1));
+    if (!fast) {
+        general_sweep(a, dims, cfg, mode, res);
+        finish(res, rss, start);
+        return res;
+    }
 
     DevBuf<double> carry;  // current working matrix when not the input itself
     if (cfg.method == 1) {

@@ -145,3 +145,45 @@ def test_determinism(dev, ref):
     r2 = dev.decompose(a, dims, "urv", "r2l", ranks=ranks)
     for c1, c2 in zip(r1.cores, r2.cores):
         np.testing.assert_array_equal(c1, c2)
+
+
+# ---- general path: TT-SVD, Alg. 4, URV left-to-right, refine_passes 0/2 ---------------
+GENERAL = [("svd", "l2r", 0), ("svd", "r2l", 0), ("ulv", "r2l", 0), ("ulv", "r2l", 1), ("urv", "l2r", 0)]
+
+
+@pytest.mark.parametrize("method,sweep,retain", GENERAL)
+@pytest.mark.parametrize("mode", ["rank", "tol"])
+def test_general_paths_vs_reference(dev, ref, method, sweep, retain, mode):
+    dims, ranks = [6, 5, 7, 4], [1, 3, 4, 2, 1]
+    a = planted_plus_noise(ref, dims, ranks, 11, 1e-3)
+    kw = dict(ranks=ranks) if mode == "rank" else dict(eps=0.05)
+    res = dev.decompose_device(a, dims, method, sweep, retain=["l11_only", "full_column"][retain], **kw)
+    rep = res.report()
+    rr = ref.decompose(a, dims, method, sweep, retain=retain, **kw)
+    assert rep.ranks_chosen == rr.ranks_chosen
+    assert rep.bound_kind == ("plain_sum" if rr.bound_kind else "root_sum_square")
+    assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
+    assert abs(rep.bound - rr.bound) <= 1e-10 * rep.input_norm
+    assert rep.warnings == rr.warnings
+
+
+@pytest.mark.parametrize("refine", [0, 2])
+@pytest.mark.parametrize("method,sweep", [("ulv", "l2r"), ("urv", "r2l")])
+def test_refine_passes(dev, ref, refine, method, sweep):
+    dims, ranks = [6, 5, 7, 4], [1, 3, 4, 2, 1]
+    a = planted_plus_noise(ref, dims, ranks, 13, 1e-3)
+    res = dev.decompose_device(a, dims, method, sweep, ranks=ranks, refine_passes=refine)
+    rr = ref.decompose(a, dims, method, sweep, ranks=ranks, refine=refine)
+    assert res.report().ranks_chosen == rr.ranks_chosen
+    assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
+
+
+def test_cfg1_tt_svd_check(dev, ref):
+    """BASELINE config 1: TT-URV/TT-ULV checked against TT-SVD (device TT-SVD now)."""
+    a, dims, ranks = cfg1(ref)
+    s = dev.decompose_device(a, dims, "svd", "l2r", ranks=ranks)
+    s_ref = ref.decompose(a, dims, "svd", "l2r", ranks=ranks)
+    assert abs(s.rse(a) - ref.rse(s_ref, a, dims)) <= TOL_RSE
+    for method, sweep in (("urv", "r2l"), ("ulv", "l2r")):
+        r = dev.decompose_device(a, dims, method, sweep, ranks=ranks)
+        assert r.rse(a) <= 2.0 * s.rse(a)
