@@ -108,7 +108,10 @@ def lib() -> C.CDLL:
     if _lib is None:
         if not LIB_PATH.exists():
             raise ImportError(f"native engine not built: {LIB_PATH} missing (run __graft_entry__.build())")
-        handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+        # RTLD_LOCAL: the drop-in C++ layer exports the reference's ttutv:: symbol names;
+        # keeping them out of the global scope stops them interposing on the reference
+        # library that the tests load as the oracle.
+        handle = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)
             fn.restype = res

@@ -44,10 +44,11 @@ int64_t launches();
 bool debug_sync();
 void check_sync(const char* kernel, const char* file, int line);
 
-// Opt a kernel into more than 48 KB of dynamic shared memory (no-op below that).
+// Opt a kernel into large dynamic shared memory. Static + dynamic may not exceed 48 KB
+// without the opt-in, so any request above 40 KB (kernels keep <= 8 KB static) opts in.
 template <class K>
 inline void allow_smem(K* kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
+    if (bytes > 40 * 1024)
         TTG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
