@@ -78,5 +78,23 @@ def build(verbose: bool = False) -> Path:
     return out
 
 
+def build_dropin_check(verbose: bool = False) -> Path:
+    """tests/cpp/dropin_check.cpp: a caller written against the reference headers,
+    compiled through the compat forwarding headers and linked to libttutv_b200.so."""
+    src = ROOT / "tests" / "cpp" / "dropin_check.cpp"
+    out = LIBDIR / "dropin_check"
+    lib = LIBDIR / LIBNAME
+    if out.exists() and out.stat().st_mtime >= max(src.stat().st_mtime, lib.stat().st_mtime):
+        return out
+    cmd = ["/usr/bin/g++", "-std=c++20", "-O2", "-I" + str(ROOT / "include" / "ttutv_b200" / "compat"),
+           "-I" + str(ROOT / "include"), str(src), "-o", str(out), "-L" + str(LIBDIR), "-lttutv_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, env=_env())
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose=True))
+    print(build_dropin_check(verbose=True))
