@@ -81,6 +81,15 @@ public:
     const double* beta() const { return beta_.get(); }
     // Explicit economy Q columns 0..q-1 (N x q, col-major, ldq >= N).
     void form_q(double* Qout, int64_t q, int64_t ldq);
+    // Rows 0..steps-1 of R indexed by ORIGINAL column (row t at out + t*ldo), the layout
+    // the wide engine produces; exact zeros below the diagonal.
+    void r_rows_by_column(double* out, int64_t ldo) const;
+    // Trailing mass of the not-yet-pivoted columns, exactly: the sum of squares of rows
+    // steps.. of the in-place updated columns (host sync).
+    double trailing_mass_exact() const;
+    int64_t p() const { return p_; }
+    int64_t N() const { return N_; }
+    int64_t n() const { return n_; }
 
 private:
     double* B_;

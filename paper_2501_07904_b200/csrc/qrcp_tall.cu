@@ -360,6 +360,49 @@ void TallQrcp::run(int64_t steps) {
     steps_ = std::max(steps_, steps);
 }
 
+namespace {
+// out(t, colmap[q]) = R(t, q) = B(t, colmap[q]) for t <= q, else 0 (t < steps).
+__global__ void k_r_by_column(const double* __restrict__ B, int64_t ld, int64_t n, const int64_t* __restrict__ colmap,
+                              const int64_t* __restrict__ pos, int64_t steps, double* out, int64_t ldo) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= steps * n) return;
+    const int64_t t = e / n, j = e - t * n;  // j = physical (original) column
+    out[t * ldo + j] = pos[j] >= t ? B[t + j * ld] : 0.0;
+}
+
+// Partial sums of squares of rows >= s over the unpivoted columns (positions >= s).
+__global__ void __launch_bounds__(256) k_tail_mass(const double* __restrict__ B, int64_t N, int64_t ld, int64_t n,
+                                                   const int64_t* __restrict__ colmap, int64_t s, double* part) {
+    __shared__ double sd[8];
+    double a = 0.0;
+    for (int64_t q = s + blockIdx.y; q < n; q += gridDim.y) {
+        const double* c = B + colmap[q] * ld;
+        for (int64_t i = s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+            a = fma(c[i], c[i], a);
+    }
+    a = block_sum(a, sd);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = a;
+}
+}  // namespace
+
+void TallQrcp::r_rows_by_column(double* out, int64_t ldo) const {
+    if (steps_ > 0)
+        TTG_LAUNCH(k_r_by_column, (int)cdiv(steps_ * n_, 256), 256, 0, stream(), B_, ld_, n_, colmap_.get(), pos_.get(),
+                   steps_, out, ldo);
+}
+
+double TallQrcp::trailing_mass_exact() const {
+    if (steps_ >= std::min(N_, n_)) return 0.0;
+    const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(N_ - steps_, 256), 64)),
+                    (unsigned)std::min<int64_t>(n_ - steps_, 64));
+    DevBuf<double> part((size_t)grid.x * grid.y);
+    TTG_LAUNCH(k_tail_mass, grid, 256, 0, stream(), B_, N_, ld_, n_, colmap_.get(), steps_, part.get());
+    std::vector<double> h = part.to_host(part.size());
+    double s = 0.0;
+    for (double v : h) s += v;
+    return s;
+}
+
 void TallQrcp::extract_r(double* out, int64_t ldo) const {
     TallView s{B_, N_, n_, ld_, nullptr, nullptr, colmap_.get(), nullptr, nullptr, nullptr, nullptr, 0,
                nullptr, nullptr, nullptr, nullptr, rows_per_blk_};

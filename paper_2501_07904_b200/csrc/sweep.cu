@@ -19,6 +19,7 @@
 // otherwise s is extended and pass 2 is redone. s = p is exactly the reference schedule.
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cmath>
 #include <sstream>
 
@@ -164,13 +165,90 @@ struct CutRequest {
     int policy;
 };
 
+// Pass 1 of a cut behind one interface: the wide read-only engine (k moderate) or, when W
+// is tall (k >> N, e.g. the last URV cut of config 5: W = 131072 x 1024), the in-place
+// Householder engine on a column-major copy of W.
+struct Pass1 {
+    virtual ~Pass1() = default;
+    virtual int64_t p() const = 0;
+    virtual int64_t N() const = 0;
+    virtual int64_t k() const = 0;
+    virtual void run_to(int64_t s) = 0;
+    virtual double trailing_mass() = 0;  // may carry downdating noise
+    virtual double refresh_exact() = 0;  // exact trailing mass
+    virtual const double* R() = 0;       // R1 rows 0..s-1 by original column, row t at R + t*N
+    virtual const int64_t* perm() = 0;   // positions -> columns
+    virtual const double* Q() = 0;       // economy Q columns 0..s-1, leading dimension k
+};
+
+struct WidePass1 final : Pass1 {
+    WideQrcp e;
+    WidePass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap) : e(W, k, N, ld, l, cap) {}
+    int64_t p() const override { return e.p(); }
+    int64_t N() const override { return e.N(); }
+    int64_t k() const override { return e.k(); }
+    void run_to(int64_t s) override { e.run_to(s); }
+    double trailing_mass() override { return e.trailing_mass(); }
+    double refresh_exact() override { return e.refresh_exact(); }
+    const double* R() override { return e.R(); }
+    const int64_t* perm() override { return e.perm(); }
+    const double* Q() override { return e.Q(); }
+};
+
+struct TallPass1 final : Pass1 {
+    DevBuf<double> B, rrows, qbuf;
+    int64_t k_, N_, rs_ = -1, qs_ = -1;
+    std::unique_ptr<TallQrcp> e;
+    TallPass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l) : k_(k), N_(N) {
+        B.alloc((size_t)(k * N));
+        if (l == Layout::Col)
+            TTG_CUDA(cudaMemcpy2DAsync(B.get(), sizeof(double) * k, W, sizeof(double) * ld, sizeof(double) * k, N,
+                                       cudaMemcpyDeviceToDevice, stream()));
+        else  // W(i,j) = W[i*ld + j]: the buffer is an N x k column-major matrix
+            transpose(W, N, k, ld, B.get(), k);
+        e = std::make_unique<TallQrcp>(B.get(), k, N, k);
+    }
+    int64_t p() const override { return e->p(); }
+    int64_t N() const override { return N_; }
+    int64_t k() const override { return k_; }
+    void run_to(int64_t s) override { e->run(s); }
+    double trailing_mass() override { return e->trailing_mass_exact(); }
+    double refresh_exact() override { return e->trailing_mass_exact(); }
+    const double* R() override {
+        const int64_t s = e->steps();
+        if (rs_ != s) {
+            rrows.alloc((size_t)(s * N_));
+            e->r_rows_by_column(rrows.get(), N_);
+            rs_ = s;
+        }
+        return rrows.get();
+    }
+    const int64_t* perm() override { return e->perm(); }
+    const double* Q() override {
+        const int64_t s = e->steps();
+        if (qs_ != s) {
+            qbuf.alloc((size_t)(k_ * s));
+            e->form_q(qbuf.get(), s, k_);
+            qs_ = s;
+        }
+        return qbuf.get();
+    }
+};
+
+// Engine choice: the wide engine keeps a k x k orthogonal factor, so it is used while
+// k is moderate or W is not tall.
+std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap) {
+    if (k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
+}
+
 // Pass-2 outputs on the host: pivot order, kept masses, pivot norms, |diag R2|.
 struct Pass2 {
     std::vector<double> kept, colmass, pnorm, diag;
     DevBuf<int64_t> perm;  // positions -> R1 row (pass-1 step) index
 };
 
-Pass2 run_pass2(WideQrcp& e1, int64_t s) {
+Pass2 run_pass2(Pass1& e1, int64_t s) {
     const int64_t N = e1.N();
     Pass2 out;
     DevBuf<double> R2((size_t)s * s), colmass(s), kept(s + 1), pn(s);
@@ -204,7 +282,7 @@ Pass2 run_pass2(WideQrcp& e1, int64_t s) {
     return out;
 }
 
-CutOut run_cut(WideQrcp& e1, const CutRequest& req) {
+CutOut run_cut(Pass1& e1, const CutRequest& req) {
     const int64_t p = e1.p();
     int64_t s;
     if (req.policy == 1) s = p;
@@ -638,19 +716,19 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
             } else {
                 rq.budget = mode.budgets[(size_t)(k - 1)];
             }
-            WideQrcp e1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
-            CutOut co = run_cut(e1, rq);
+            auto e1 = make_pass1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
+            CutOut co = run_cut(*e1, rq);
             const int64_t r = co.rank;
             res.step_errors[(size_t)(k - 1)] = co.step_error;
             res.ranks_chosen[(size_t)k] = r;
             res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag};
             DevBuf<double> core((size_t)(m * r));
-            TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1.Q(), m, co.sel.get(), r, false,
+            TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1->Q(), m, co.sel.get(), r, false,
                        core.get());
             set_core(res, (size_t)(k - 1), std::move(core), r_prev, dims[(size_t)(k - 1)], r);
             DevBuf<double> next((size_t)(r * n));
             dim3 g((unsigned)cdiv(n, 32), (unsigned)cdiv(r, 32));
-            TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1.R(), n, co.sel.get(), r, next.get());
+            TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1->R(), n, co.sel.get(), r, next.get());
             r_prev = r;
             if (k < d - 1) {
                 carry = std::move(next);
@@ -678,19 +756,19 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
                 rq.budget = mode.budgets[(size_t)(k - 2)];
             }
             // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
-            WideQrcp e1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
-            CutOut co = run_cut(e1, rq);
+            auto e1 = make_pass1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
+            CutOut co = run_cut(*e1, rq);
             const int64_t r = co.rank;
             res.step_errors[(size_t)(k - 2)] = co.step_error;
             res.ranks_chosen[(size_t)(k - 1)] = r;
             res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag};
             DevBuf<double> core((size_t)(n * r));
-            TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1.Q(), n, co.sel.get(), r, true,
+            TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1->Q(), n, co.sel.get(), r, true,
                        core.get());
             set_core(res, (size_t)(k - 1), std::move(core), r, dims[(size_t)(k - 1)], r_next);
             DevBuf<double> next((size_t)(M * r));
             dim3 g((unsigned)std::min<int64_t>(cdiv(M, 256), 4096), (unsigned)r);
-            TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1.R(), M, co.sel.get(), r, next.get());
+            TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1->R(), M, co.sel.get(), r, next.get());
             r_next = r;
             if (k > 2) {
                 carry = std::move(next);

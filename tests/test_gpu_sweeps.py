@@ -187,3 +187,13 @@ def test_cfg1_tt_svd_check(dev, ref):
     for method, sweep in (("urv", "r2l"), ("ulv", "l2r")):
         r = dev.decompose_device(a, dims, method, sweep, ranks=ranks)
         assert r.rse(a) <= 2.0 * s.rse(a)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_tall_pass1_engine(dev, ref, method):
+    """Cuts whose pivoted matrix W is tall (k > 2048 and k > N) take the in-place engine
+    (URV: the last cut I_1 x (I_2 r); ULV: the last cut (r I_{d-1}) x I_d)."""
+    dims, ranks = ([9, 700, 5], [1, 6, 4, 1]) if method == "urv" else ([5, 700, 9], [1, 4, 6, 1])
+    a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
+    _, rep, *_ = _check_parity(dev, ref, a, dims, method, ranks=ranks)
+    _check_parity(dev, ref, a, dims, method, eps=1e-4)
