@@ -237,6 +237,68 @@ __device__ __forceinline__ void stream_epilogue(int64_t t, int64_t j, int64_t N,
     }
 }
 
+// MODE 3: Row layout with few columns (N too small to fill the GPU one thread per column,
+// e.g. k = 640, N = 32768): a CTA owns 32 columns, its 8 warps split the k rows (each row
+// read as a coalesced 256-byte segment), partials combined in warp order in smem.
+__global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __restrict__ W, int64_t k, int64_t N,
+                                                            int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                            const double* diag, const int64_t* piv, double* R,
+                                                            double* nu, const double* cref, const int64_t* pos,
+                                                            int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    __shared__ double part[kThreads / 32][33];
+    extern __shared__ double q[];
+    for (int64_t i = threadIdx.x; i < k; i += kThreads) q[i] = Q[i + t * k];
+    __syncthreads();
+    const int64_t jp = piv[t];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < N; j0 += (int64_t)gridDim.x * 32) {
+        const int64_t j = j0 + lane;
+        const bool active = j < N;
+        double a = 0.0;
+        if (active)
+#pragma unroll 4
+            for (int64_t i = warp; i < k; i += kThreads / 32) a = fma(q[i], W[i * ld + j], a);
+        part[warp][lane] = a;
+        __syncthreads();
+        if (warp == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) s += part[w][lane];
+            const int64_t pj = active ? pos[j] : 0;
+            const bool chosen = active && (pj < t || j == jp);
+            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+            bool fl = false;
+            if (active && !chosen) {
+                R[t * N + j] = s;
+                const double nv = __dsub_rn(nu[j], __dmul_rn(s, s));
+                nu[j] = nv;
+                fl = nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0;
+                if (!fl) {
+                    Cand c{nv, pj, j};
+                    if (better(c, best)) best = c;
+                    msum += nv;
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, fl);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(nflag, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (fl) flags[base + __popc(m & ((1u << lane) - 1u))] = j;
+            }
+        }
+        __syncthreads();
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ W, int64_t k, int64_t N,
                                                      int64_t ld, int64_t t, const double* __restrict__ Q,
@@ -275,20 +337,41 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
             if (MODE == 2) {
                 load_tile_small_k(W, k, N, j0, tile);
             }
-            if (j >= N) continue;
-            const int64_t pj = pos[j];
-            if (pj < t || j == jp) {
-                R[t * N + j] = j == jp ? diag[t] : 0.0;
-                continue;
-            }
-            double a = 0.0;
-            if (MODE == 2) {
-                for (int64_t i = 0; i < k; ++i) a = fma(q[i], tile[i * (kThreads + 1) + threadIdx.x], a);
-            } else {
+            // No early exits: every lane reaches the warp-aggregated flag append below.
+            const bool active = j < N;
+            const int64_t pj = active ? pos[j] : 0;
+            const bool chosen = active && (pj < t || j == jp);
+            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+            const bool work = active && !chosen;
+            bool fl = false;
+            if (work) {
+                double a = 0.0;
+                if (MODE == 2) {
+                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], tile[i * (kThreads + 1) + threadIdx.x], a);
+                } else {
 #pragma unroll 8
-                for (int64_t i = 0; i < k; ++i) a = fma(q[i], W[i * ld + j], a);
+                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], W[i * ld + j], a);
+                }
+                R[t * N + j] = a;
+                // factor.cpp:101-102: cnorm2 -= rkj*rkj; guard at 1e-16 * cref2 (no contraction).
+                const double nv = __dsub_rn(nu[j], __dmul_rn(a, a));
+                nu[j] = nv;
+                fl = nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0;
+                if (!fl) {
+                    Cand c{nv, pj, j};
+                    if (better(c, best)) best = c;
+                    msum += nv;
+                }
             }
-            stream_epilogue(t, j, N, a, R, nu, cref, pos, flags, nflag, best, msum);
+            // Hilbert-type ties flag thousands of columns per step: one atomic per warp.
+            const unsigned m = __ballot_sync(0xffffffffu, fl);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(nflag, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (fl) flags[base + __popc(m & ((1u << lane) - 1u))] = j;
+            }
         }
     }
     best = block_best(best, sc);
@@ -414,9 +497,9 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     : W_(W), k_(k), N_(N), ld_(ld), p_(std::min(k, N)), layout_(layout) {
     if (k <= 0 || N <= 0) argument_error("qr_col_pivot: empty matrix");
     if (layout == Layout::Col) mode_ = (k >= 64 || ld != k) ? 1 : 2;
-    else mode_ = 0;
+    else mode_ = (k >= 64 && N < (int64_t)sm_count() * 4 * kThreads) ? 3 : 0;
     const int per_sm = 8;
-    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : cdiv(N, kThreads);
+    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(N); flags_.alloc(N);
     cand_.alloc(ncand_); mass_.alloc(ncand_); nflag_.alloc(1); nflag_.zero();
@@ -425,7 +508,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     grow(std::max<int64_t>(1, std::min(p_, cap_steps)));
     TTG_LAUNCH(k_identity, cdiv(k * k, 256), 256, 0, stream(), Q_.get(), k);
     const size_t smem = mode_ == 2 ? sizeof(double) * k * (kThreads + 1) : 0;
-    auto init = mode_ == 0 ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
+    auto init = (mode_ == 0 || mode_ == 3) ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
     allow_smem(init, smem);
     TTG_LAUNCH(init, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
                perm_.get(), cand_.get(), mass_.get());
@@ -491,7 +574,7 @@ void WideQrcp::step() {
 void WideQrcp::gemv_step(int64_t t) {
     const size_t qbytes = sizeof(double) * ((k_ + 1) & ~int64_t(1));
     const size_t smem = qbytes + (mode_ == 2 ? sizeof(double) * k_ * (kThreads + 1) : 0);
-    auto kern = mode_ == 0 ? k_stream<0> : mode_ == 1 ? k_stream<1> : k_stream<2>;
+    auto kern = mode_ == 0 ? k_stream<0> : mode_ == 1 ? k_stream<1> : mode_ == 2 ? k_stream<2> : k_stream_splitk;
     allow_smem(kern, smem);
     prof_begin();
     TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Q_.get(), diag_.get(), piv_.get(),

@@ -104,6 +104,70 @@ __global__ void __launch_bounds__(kT) k_tsqr_node(double* in, int64_t nrows, int
     }
 }
 
+// Pairwise tree node for larger s: QR of two stacked upper triangles [T1; T2] with the
+// structure kept. Step c reflects T1(c,c) against T2(0..c, c) only, and touches rows c of
+// T1 and 0..c of T2 in the columns to the right, so T2 stays upper triangular and both
+// live packed in shared memory (s(s+1) doubles; s = 160 -> 206 KB) with about a sixth of
+// the flops of a dense 2s x s factorisation.
+__global__ void __launch_bounds__(kT) k_tsqr_pair(const double* __restrict__ in, int64_t nrows, int s, int64_t ldi,
+                                                  double* out, int64_t ldo) {
+    extern __shared__ double sm[];
+    const int tri = s * (s + 1) / 2;
+    double* T1 = sm;
+    double* T2 = sm + tri;
+    __shared__ double red[kT / 32];
+    __shared__ double sc[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kT / 32;
+    const int64_t r1 = (int64_t)blockIdx.x * 2 * s, r2 = r1 + s;
+    const bool has2 = r2 < nrows;
+    for (int e = threadIdx.x; e < tri; e += kT) {
+        int c = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // column of packed index e
+        while ((c + 1) * (c + 2) / 2 <= e) ++c;
+        while (c * (c + 1) / 2 > e) --c;
+        const int i = e - c * (c + 1) / 2;
+        T1[e] = in[r1 + i + (int64_t)c * ldi];
+        T2[e] = has2 ? in[r2 + i + (int64_t)c * ldi] : 0.0;
+    }
+    __syncthreads();
+    if (has2)
+        for (int c = 0; c < s; ++c) {
+            double* x2 = T2 + c * (c + 1) / 2;  // T2(0..c, c)
+            double part = 0.0;
+            for (int i = threadIdx.x; i <= c; i += kT) part = fma(x2[i], x2[i], part);
+            const double sigma = block_sum(part, red);
+            double* d1 = T1 + c * (c + 1) / 2 + c;  // T1(c, c)
+            const double alpha = *d1;
+            if (sigma == 0.0) {
+                __syncthreads();
+                continue;
+            }
+            const double mu = sqrt(fma(alpha, alpha, sigma));
+            const double smu = copysign(mu, alpha);
+            const double v0 = alpha + smu;
+            const double beta = v0 / smu;
+            __syncthreads();
+            for (int i = threadIdx.x; i <= c; i += kT) x2[i] /= v0;
+            if (threadIdx.x == 0) *d1 = -smu;
+            __syncthreads();
+            for (int j = c + 1 + warp; j < s; j += nw) {
+                double* y1 = T1 + j * (j + 1) / 2 + c;  // T1(c, j)
+                double* y2 = T2 + j * (j + 1) / 2;      // T2(0..c, j)
+                double w = 0.0;
+                for (int i = lane; i <= c; i += 32) w = fma(x2[i], y2[i], w);
+                w = warp_sum(w) + *y1;
+                const double tau = beta * w;
+                for (int i = lane; i <= c; i += 32) y2[i] = fma(-tau, x2[i], y2[i]);
+                if (lane == 0) *y1 -= tau;
+            }
+            __syncthreads();
+        }
+    (void)sc;
+    for (int e = threadIdx.x; e < s * s; e += kT) {
+        const int c = e / s, i = e - c * s;
+        out[(int64_t)blockIdx.x * s + i + (int64_t)c * ldo] = i <= c ? T1[c * (c + 1) / 2 + i] : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One-CTA qr_col_pivot of an m x n matrix (col-major, ld = m) held in smem.
 // Outputs: perm[n] (position -> source column), R over positions (p x n, ld = p),
@@ -266,6 +330,17 @@ void tsqr_r(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout) {
     TTG_LAUNCH(k_tsqr_leaf, (int)nb, kT, smem0, stream(), B, N, (int)s, ld, rb, lvl.get(), nb * s);
     int64_t rows = nb * s;
     const int g = (int)std::max<int64_t>(2, std::min<int64_t>(16, (160 * 1024) / (8 * s * s)));
+    if (g * s * s * 8 > 160 * 1024) {  // large s: structured pairwise tree in packed smem
+        const size_t smem = sizeof(double) * (size_t)(s * (s + 1));
+        allow_smem(k_tsqr_pair, smem);
+        while (rows > s) {
+            const int64_t nt = rows / s, nbl = cdiv(nt, 2);
+            DevBuf<double> nxt((size_t)(nbl * s * s));
+            TTG_LAUNCH(k_tsqr_pair, (int)nbl, kT, smem, stream(), lvl.get(), rows, (int)s, rows, nxt.get(), nbl * s);
+            lvl = std::move(nxt);
+            rows = nbl * s;
+        }
+    }
     while (rows > s) {
         const int64_t nbl = cdiv(rows, (int64_t)g * s);
         DevBuf<double> nxt((size_t)(nbl * s * s));
