@@ -128,6 +128,19 @@ ttg_status ttg_verify_bound(const double* a, int a_on_device, const ttg_result* 
                             double slack_rel, double* achieved);
 /* |A - reconstruct(tt)|_F / |A|_F on device (no element cap: Â is never materialised). */
 ttg_status ttg_result_rse(const ttg_result* res, const double* a, int a_on_device, double* rse);
+/* Dense reconstruction of the result's train into `out` (device pointer when
+ * out_on_device, else host), reconstruct() (tt.cpp:52-73) without an element cap. */
+ttg_status ttg_result_reconstruct(const ttg_result* res, double* out, int out_on_device);
+
+/* One completion step on device buffers of n entries (the reference's loop body,
+ * completion.cpp:161-186, with a step size of 1): y holds the reconstruction X on entry;
+ * on exit y = observed on the mask (mask != 0) and X elsewhere. Also returns
+ *   stats[0] = sum_mask (X - observed)^2     stats[1] = sum_mask observed^2
+ *   stats[2] = sum (X - truth)^2             stats[3] = sum truth^2
+ *   stats[4] = max truth                     (truth may be NULL: stats[2..4] = 0)
+ * with deterministic fixed-order reductions. */
+ttg_status ttg_completion_reset(double* y, const double* observed, const double* mask,
+                                const double* truth, int64_t n, double stats[5]);
 
 /* ---- factor level (host buffers, column-major) ------------------------------ */
 /* q: m x p, r: p x n, perm: n. Any of the outputs may be NULL. */

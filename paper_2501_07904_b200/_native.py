@@ -84,6 +84,8 @@ SIGNATURES = {
     "ttg_result_cut_diag": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int, c_int64_p]),
     "ttg_verify_bound": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, c_double_p]),
     "ttg_result_rse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, c_double_p]),
+    "ttg_result_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "ttg_completion_reset": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, c_double_p]),
     "ttg_qr_col_pivot": (C.c_int, [c_double_p, C.c_int64, C.c_int64, c_double_p, c_double_p, c_int64_p]),
     "ttg_utv": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]),
     "ttg_svd": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_double, c_double_p, c_double_p,

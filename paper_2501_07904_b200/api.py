@@ -200,6 +200,47 @@ def left_orthogonal_via_urv(a, dims=None, ranks=None, eps=None, weights=(), refi
     return decompose(a, dims, "urv", "l2r", ranks=ranks, eps=eps, weights=weights, refine_passes=refine_passes, **kw)
 
 
+# ---- completion with a rank-adaptive retraction (BASELINE config 4) -------------------
+@dataclass
+class CompletionTrace:
+    """Per-iteration trace like IterationTrace (completion.hpp:57-64) plus ranks."""
+    ranks: list = field(default_factory=list)
+    rse_observed: list = field(default_factory=list)
+    rse_full: list = field(default_factory=list)
+    psnr: list = field(default_factory=list)
+    wall_time_ms: list = field(default_factory=list)
+
+
+def complete_tol(y_ptr: int, observed_ptr: int, mask_ptr: int, dims, eps: float, iters: int,
+                 truth_ptr: int = 0, method: str = "urv", sweep: str = "r2l") -> CompletionTrace:
+    """Projected iteration Y <- P_Omega(M) + P_Omega^c(Retract_eps(Y)) on device buffers.
+
+    The reference's complete() (completion.cpp:131-211) retracts at fixed ranks with a
+    step size; BASELINE config 4 uses a rank-adaptive retraction with step 1, i.e.
+    X = TT-URV_eps(Y); Y = reconstruct(X); Y[Omega] = M[Omega]. `y_ptr` holds the initial
+    iterate (the observed values zero-filled, as initial_guess) and is updated in place.
+    All pointers are device pointers (e.g. torch ``data_ptr()``)."""
+    import time
+    n = int(np.prod(dims))
+    tr = CompletionTrace()
+    stats = (C.c_double * 5)()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        res = decompose_device(y_ptr, dims, method, sweep, eps=eps, a_is_device_ptr=True)
+        check(lib().ttg_result_reconstruct(res.h, C.c_void_p(y_ptr), 1))
+        tr.ranks.append(res.report().ranks_chosen)
+        del res
+        check(lib().ttg_completion_reset(C.c_void_p(y_ptr), C.c_void_p(observed_ptr), C.c_void_p(mask_ptr),
+                                         C.c_void_p(truth_ptr) if truth_ptr else None, n, stats))
+        tr.rse_observed.append(float(np.sqrt(stats[0] / stats[1])) if stats[1] > 0 else 0.0)
+        if truth_ptr:
+            tr.rse_full.append(float(np.sqrt(stats[2] / stats[3])))
+            mse = stats[2] / n
+            tr.psnr.append(float("inf") if mse == 0 else float(10.0 * np.log10(stats[4] ** 2 / mse)))
+        tr.wall_time_ms.append(1e3 * (time.perf_counter() - t0))
+    return tr
+
+
 # ---- factor level (factor.hpp) -------------------------------------------------------
 def qr_col_pivot(a: np.ndarray):
     """qr_col_pivot (factor.hpp:19): returns (q m x p, r p x n, perm)."""

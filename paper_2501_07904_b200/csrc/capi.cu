@@ -197,6 +197,35 @@ ttg_status ttg_result_rse(const ttg_result* res, const double* a, int a_on_devic
     });
 }
 
+ttg_status ttg_result_reconstruct(const ttg_result* res, double* out, int out_on_device) {
+    return guard([&] {
+        int64_t n = 1;
+        for (int64_t v : res->r.dims) n *= v;
+        std::vector<const double*> cores;
+        std::vector<int64_t> ranks{1};
+        for (size_t k = 0; k < res->r.cores.size(); ++k) {
+            cores.push_back(res->r.cores[k].get());
+            ranks.push_back(res->r.core_dims[k][2]);
+        }
+        if (out_on_device) {
+            ttg::reconstruct(cores, res->r.dims, ranks, out);
+        } else {
+            ttg::DevBuf<double> o((size_t)n);
+            ttg::reconstruct(cores, res->r.dims, ranks, o.get());
+            o.download(out, (size_t)n);
+        }
+        ttg::sync();
+    });
+}
+
+ttg_status ttg_completion_reset(double* y, const double* observed, const double* mask, const double* truth,
+                                int64_t n, double stats[5]) {
+    return guard([&] {
+        ttg::completion_reset(y, observed, mask, truth, n, stats);
+        ttg::sync();
+    });
+}
+
 ttg_status ttg_verify_bound(const double* a, int a_on_device, const ttg_result* res, double slack_rel,
                             double* achieved) {
     return guard([&] {

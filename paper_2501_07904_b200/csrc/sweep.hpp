@@ -47,6 +47,10 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
 
 // |A - reconstruct(tt)|^2 on device without materialising the full reconstruction.
 double residual_squared(const TTResult& r, const double* a);
+// Completion loop body on device (completion.cpp:161-186, step size 1): see
+// ttg_completion_reset in include/ttutv_b200.h.
+void completion_reset(double* y, const double* observed, const double* mask, const double* truth, int64_t n,
+                      double stats[5]);
 // Dense reconstruction (device output of prod(dims) doubles).
 void reconstruct(const std::vector<const double*>& cores, const std::vector<int64_t>& dims,
                  const std::vector<int64_t>& ranks, double* out);

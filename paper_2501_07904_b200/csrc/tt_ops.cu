@@ -35,6 +35,73 @@ void reconstruct(const std::vector<const double*>& cores, const std::vector<int6
     }
 }
 
+namespace {
+constexpr int64_t kChunk = 4096;
+
+// One pass: y <- mask ? observed : y, with the completion trace sums of the reconstruction
+// X (the incoming y) per 4096-entry chunk (combined in chunk order on the host side).
+__global__ void __launch_bounds__(256) k_completion_reset(double* y, const double* __restrict__ obs,
+                                                          const double* __restrict__ mask,
+                                                          const double* __restrict__ truth, int64_t n,
+                                                          double* part) {
+    __shared__ double sd[8];
+    const int64_t nchunk = cdiv(n, kChunk);
+    for (int64_t b = blockIdx.x; b < nchunk; b += gridDim.x) {
+        const int64_t lo = b * kChunk, hi = min(n, lo + kChunk);
+        double so = 0.0, sm = 0.0, sf = 0.0, st = 0.0, mx = -INFINITY;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += 256) {
+            const double x = y[i];
+            const bool on = mask[i] != 0.0;
+            if (on) {
+                const double d = x - obs[i];
+                so = fma(d, d, so);
+                sm = fma(obs[i], obs[i], sm);
+                y[i] = obs[i];
+            }
+            if (truth) {
+                const double d = x - truth[i];
+                sf = fma(d, d, sf);
+                st = fma(truth[i], truth[i], st);
+                mx = fmax(mx, truth[i]);
+            }
+        }
+        so = block_sum(so, sd);
+        sm = block_sum(sm, sd);
+        sf = block_sum(sf, sd);
+        st = block_sum(st, sd);
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        __shared__ double smx[8];
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m = smx[0];
+            for (int w = 1; w < 8; ++w) m = fmax(m, smx[w]);
+            part[5 * b + 0] = so;
+            part[5 * b + 1] = sm;
+            part[5 * b + 2] = sf;
+            part[5 * b + 3] = st;
+            part[5 * b + 4] = m;
+        }
+    }
+}
+}  // namespace
+
+void completion_reset(double* y, const double* observed, const double* mask, const double* truth, int64_t n,
+                      double stats[5]) {
+    const int64_t nchunk = cdiv(n, kChunk);
+    DevBuf<double> part((size_t)(5 * nchunk));
+    const int grid = (int)std::min<int64_t>(nchunk, (int64_t)sm_count() * 8);
+    TTG_LAUNCH(k_completion_reset, grid, 256, 0, stream(), y, observed, mask, truth, n, part.get());
+    std::vector<double> h = part.to_host((size_t)(5 * nchunk));
+    for (int k = 0; k < 4; ++k) stats[k] = 0.0;
+    stats[4] = truth ? -INFINITY : 0.0;
+    for (int64_t b = 0; b < nchunk; ++b) {
+        for (int k = 0; k < 4; ++k) stats[k] += h[(size_t)(5 * b + k)];
+        if (truth) stats[4] = std::max(stats[4], h[(size_t)(5 * b + 4)]);
+    }
+}
+
 double residual_squared(const TTResult& r, const double* a) {
     int64_t total = 1;
     for (int64_t v : r.dims) total *= v;

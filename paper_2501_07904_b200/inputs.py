@@ -18,6 +18,7 @@ CONFIGS = {
     1: dict(dims=[20] * 4, ranks=[1, 5, 5, 5, 1], rho=1e-8, seed=1, mode="rank"),
     2: dict(dims=[32] * 5, eps=1e-8, mode="tol"),
     3: dict(dims=[24] * 6, ranks=[1, 20, 20, 20, 20, 20, 1], rho=1e-4, seed=3, mode="rank"),
+    4: dict(dims=[4] * 12, eps=1e-3, mode="tol", iters=20),
     5: dict(dims=[1024] * 3, ranks=[1, 128, 128, 1], rho=1e-6, seed=5, mode="rank"),
 }
 
@@ -58,7 +59,34 @@ def planted(dims, ranks, seed, rho, device) -> torch.Tensor:
     return a
 
 
+def mri_like(device, seed=4, nblobs=64, n=256, noise=0.01):
+    """Config 4: sum of `nblobs` axis-aligned anisotropic Gaussian
+    blobs on an n^3 grid (centres U[0,n), widths sigma U[4,32], amplitudes U[0.2,1]) plus
+    Gaussian noise at `noise` relative Frobenius level. Returns the flat volume (first
+    index fastest: x + n*y + n^2*z), i.e. the 4^12 tensor by pure reinterpretation."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = lambda *s: torch.rand(*s, generator=g, device=device, dtype=torch.float64)
+    c = u(nblobs, 3) * n
+    w = 4.0 + 28.0 * u(nblobs, 3)
+    amp = 0.2 + 0.8 * u(nblobs)
+    ax = torch.arange(n, device=device, dtype=torch.float64)
+    f = [torch.exp(-0.5 * ((ax[None, :] - c[:, a, None]) / w[:, a, None]) ** 2) for a in range(3)]
+    v = torch.einsum("b,bx,by,bz->zyx", amp, f[0], f[1], f[2]).reshape(-1).contiguous()
+    e = torch.randn(v.numel(), generator=g, device=device, dtype=torch.float64)
+    v.add_(e, alpha=float(noise * v.norm() / e.norm()))
+    return v
+
+
+def bernoulli_mask(count: int, device, seed=41, p=0.5) -> torch.Tensor:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return (torch.rand(count, generator=g, device=device, dtype=torch.float64) < p).to(torch.float64)
+
+
 def build(cfg: int, device) -> torch.Tensor:
+    if cfg == 4:
+        return mri_like(device)
     c = CONFIGS[cfg]
     if cfg == 2:
         return hilbert_shifted(c["dims"], device)
