@@ -15,13 +15,13 @@ namespace ttg {
 enum class Layout { Col = 0, Row = 1 };
 
 // ---------------------------------------------------------------------------
-// Pass 1: greedy column-pivoted Householder QR of a k x N matrix W with k moderate
-// (the rank-times-mode side of an unfolding). W is never written: the engine keeps the
-// explicit k x k orthogonal factor Q_t = H_0...H_{t-1} and produces, per step t, row t of
-// R for every column with one streaming GEMV, R(t,j) = q_t^T w_j, downdating the column
-// norms exactly as factor.cpp:98-107 does. Any prefix of steps equals the prefix of the
-// reference's qr_col_pivot (factor.cpp:62-135) in exact arithmetic: same pivots (same
-// tie rule), same R rows, and Q[:, :s] = the first s columns of its economy Q.
+// Pass 1: greedy column-pivoted Householder QR of a k x N matrix W. W is never written.
+// The orthogonal factor Q_t = H_0...H_{t-1} is kept in compact WY form
+// Q_t = I - Y_t T_t Y_t^T (Y: k x t reflectors, T: t x t upper), so one step costs
+// O(k t) besides one streaming GEMV over W: R(t,j) = q_t^T w_j for every unpivoted
+// column, with the norm downdate of factor.cpp:98-107. Any prefix of steps equals the
+// prefix of the reference's qr_col_pivot (factor.cpp:62-135) in exact arithmetic: same
+// pivots (same tie rule), same R rows, and Q[:, :s] = its first s economy-Q columns.
 // ---------------------------------------------------------------------------
 class WideQrcp {
 public:
@@ -39,7 +39,7 @@ public:
     // returns the exact trailing mass.
     double refresh_exact();
 
-    const double* Q() const { return Q_.get(); }       // k x k, columns 0..steps-1 final
+    const double* Q() const { return Qt_.get(); }      // k x cap, columns 0..steps-1 = economy Q
     const double* R() const { return R_.get(); }       // rows 0..steps-1, row t at R + t*N
     const int64_t* perm() const { return perm_.get(); } // position -> column
     const int64_t* piv() const { return piv_.get(); }   // step -> column
@@ -49,14 +49,16 @@ public:
 private:
     void grow(int64_t cap);
     void step();
+    void reflect_step(int64_t t);
     void gemv_step(int64_t t);
 
     const double* W_;
     int64_t k_, N_, ld_, p_;
     Layout layout_;
     int64_t steps_ = 0, cap_ = 0;
-    int ncand_ = 0, mode_ = 0;
-    DevBuf<double> nu_, cref_, Q_, R_, y_, diag_, beta_, mass_;
+    int ncand_ = 0, mode_ = 0, nchunk_ = 1, ksplit_ = 1;
+    DevBuf<double> nu_, cref_, R_, diag_, beta_, mass_;
+    DevBuf<double> Y_, T_, Qt_, wv_, yv_, part_, vecs_, kpart_;  // WY state and scratch
     DevBuf<int64_t> pos_, perm_, piv_, flags_;
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;

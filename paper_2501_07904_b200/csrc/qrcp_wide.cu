@@ -1,19 +1,22 @@
-// Pass-1 engine: greedy column-pivoted Householder QR of a k x N matrix W (k moderate)
-// without ever writing W. See engine.hpp for the contract.
+// Pass-1 engine: greedy column-pivoted Householder QR of a k x N matrix W without ever
+// writing W. See engine.hpp for the contract.
 //
-// One pivot step t = four launches:
-//   A  pick:     every CTA reduces the per-CTA pivot candidates of step t-1 (key: larger
-//                norm, then lower position -- factor.cpp:85-87); CTA 0 applies the
-//                position swap (factor.cpp:88-93). Then y = Q_t[:, t:]^T w_piv (warp per
-//                output), i.e. the pivot column in reflected coordinates.
-//   B  reflect:  dlarfg-convention reflector from y (factor.cpp:24-38, same formulas and
-//                rounding), and the right update Q_{t+1} = Q_t H_t on row blocks of Q.
-//                Column t of Q_{t+1} is q_t, the t-th economy-Q column.
-//   C  stream:   R(t,j) = q_t^T w_j for every unpivoted column j (one HBM pass over W),
-//                norm downdate nu_j -= R(t,j)^2 with the 1e-16 recompute guard
-//                (factor.cpp:98-107), per-CTA pivot candidates and trailing mass.
-//   D  guard:    (only when C flagged columns) recompute flagged norms from the projected
-//                column, then recompute the candidates.
+// The orthogonal factor is kept in compact WY form, Q_t = H_0...H_{t-1} = I - Y T Y^T
+// (Y: k x t unit-lower reflectors, T: t x t upper). One pivot step t:
+//   pick     every CTA reduces the per-CTA pivot candidates of step t-1 (larger norm, then
+//            lower position -- factor.cpp:85-87); CTA 0 applies the position swap
+//            (factor.cpp:88-93); the pivot column w is staged and z = Y^T w started.
+//   y        y = Q_t^T w = w - Y T^T Y^T w (the pivot column in reflected coordinates).
+//   reflect  dlarfg-convention reflector from y (factor.cpp:24-38, same formulas and
+//            rounding) appended to Y; T grows by one column: T(:t,t) = -beta T Y^T v.
+//   q        q_t = Q_{t+1} e_t, the t-th economy-Q column, kept explicitly (Qt).
+//   stream   R(t,j) = q_t^T w_j for every unpivoted column (one HBM pass over W), norm
+//            downdate nu_j -= R(t,j)^2 with the 1e-16 recompute guard (factor.cpp:98-107),
+//            per-CTA pivot candidates and trailing mass.
+//   guard    (only when the stream flagged columns) recompute the flagged norms from
+//            the projection residual, then the candidates.
+// The WY phases cost O(k t) per step (one fused CTA when k (t+1) is small, otherwise
+// multi-CTA row chunks with fixed-order reductions), so k may be large (tall W).
 #include <cmath>
 
 #include "engine.hpp"
@@ -22,12 +25,16 @@ namespace ttg {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int64_t kQSmem = 16384;  // largest k whose q_t is staged in shared memory
 
 // ---- per-column streaming primitives -------------------------------------------------
 // MODE 0: Row layout, one thread per column, sequential accumulation over rows.
 // MODE 1: Col layout with k >= 64, one warp per column, lane-strided partials + shuffle tree.
 // MODE 2: Col layout with k < 64 and ld == k, a 256-column tile staged flat through smem,
 //         one thread per column, sequential accumulation.
+// MODE 3: Row layout with few columns: 32 columns per CTA, the 8 warps split the rows.
+// MODE 4: Row layout, very tall (k >> N): the rows are also split across CTAs; partial
+//         dots go through a scratch buffer and a finishing kernel does the epilogue.
 // Within one problem every column uses the same arithmetic order, so identical columns
 // produce bitwise identical results (Hilbert-type ties).
 
@@ -37,11 +44,10 @@ __device__ __forceinline__ double ld_w(const double* __restrict__ W, int64_t ld,
 }
 
 // MODE 2 tile: columns [j0, j0+256) of a contiguous k x N (k < 64) matrix into smem as
-// tile[i*(256+1) + c]; one warp per column segment (coalesced, no integer division).
+// tile[i*(256+1) + c]. The tile is contiguous in memory (ld == k): flat coalesced loads,
+// element e of the tile is (row e % k, column e / k), tracked incrementally.
 __device__ __forceinline__ void load_tile_small_k(const double* __restrict__ W, int64_t k, int64_t N, int64_t j0,
                                                   double* tile) {
-    // The tile is contiguous in memory (ld == k): flat coalesced loads, element e of the
-    // tile is (row e % k, column e / k), tracked incrementally (no division per element).
     const int nc = (int)min((int64_t)kThreads, N - j0);
     const int kk = (int)k;
     const int total = nc * kk;
@@ -62,11 +68,34 @@ __device__ __forceinline__ void load_tile_small_k(const double* __restrict__ W, 
     __syncthreads();
 }
 
-// Per-column epilogue shared by the init and stream kernels.
-struct ColOut {
-    Cand best;
-    double mass;
-};
+// Warp-aggregated append of flagged columns (one atomic per warp). All lanes call it.
+__device__ __forceinline__ void append_flag(bool fl, int64_t j, int64_t* flags, int* nflag) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, fl);
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(nflag, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (fl) flags[base + __popc(m & ((1u << lane) - 1u))] = j;
+    }
+}
+
+// Downdate + guard for one unpivoted column (factor.cpp:101-102: cnorm2 -= rkj*rkj, the
+// guard at 1e-16 * cref2, no contraction). Returns the flag.
+__device__ __forceinline__ bool downdate(int64_t t, int64_t j, int64_t N, double r, int64_t pj, double* R,
+                                        double* nu, const double* cref, Cand& best, double& mass) {
+    R[t * N + j] = r;
+    const double nv = __dsub_rn(nu[j], __dmul_rn(r, r));
+    nu[j] = nv;
+    const bool fl = nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0;
+    if (!fl) {
+        Cand c{nv, pj, j};
+        if (better(c, best)) best = c;
+        mass += nv;
+    }
+    return fl;
+}
 
 // ---------------------------------------------------------------------------
 // Init: nu_j = cref_j = |w_j|^2 (sequential, no contraction: sum_squares_serial),
@@ -128,118 +157,305 @@ __global__ void __launch_bounds__(kThreads) k_init(const double* __restrict__ W,
 }
 
 // ---------------------------------------------------------------------------
-// A: pick the pivot of step t, apply the position swap, y = Q_t[:, t:]^T w_piv.
-// grid.x = ceil((k - t) / 8) CTAs of 8 warps; one output per warp.
+// Compact-WY step phases. Scratch: wv (pivot column), yv (reflected column), part
+// (per-chunk partials: [chunk * (cap+1) + l], slot cap = sigma partial), vec (z | u | p |
+// g, each cap long, then scalars: vec[4cap] = v0, vec[4cap+1] = beta).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_pick(const double* __restrict__ W, int64_t k, int64_t N,
-                                                   int64_t ld, int layout, int64_t t, const Cand* cand,
-                                                   int ncand, int64_t* pos, int64_t* perm, int64_t* piv,
-                                                   int* nflag, const double* __restrict__ Q, double* y) {
+struct WY {
+    const double* W;
+    int64_t k, N, ld;
+    int layout;
+    int64_t cap;
+    double* Y;   // k x cap
+    double* T;   // cap x cap
+    double* Qt;  // k x cap
+    double* wv;
+    double* yv;
+    double* part;
+    double* vec;
+    double* diag;
+    double* beta;
+    int64_t* pos;
+    int64_t* perm;
+    int64_t* piv;
+    int* nflag;
+    const Cand* cand;
+    int ncand;
+    int nchunk;
+    int64_t rows;  // rows per chunk
+};
+
+// pick: pivot of step t (redundant per CTA), bookkeeping (CTA `chunk0` thread 0), stage
+// w for this chunk's rows and the chunk's partial z = Y[:, :t]^T w.
+__device__ void wy_pick(const WY& s, int64_t t, int chunk, bool bookkeep) {
     __shared__ Cand sc[kThreads / 32];
-    extern __shared__ double w[];  // k doubles
     Cand best = cand_none();
-    for (int i = threadIdx.x; i < ncand; i += kThreads)
-        if (better(cand[i], best)) best = cand[i];
+    for (int i = threadIdx.x; i < s.ncand; i += kThreads)
+        if (better(s.cand[i], best)) best = s.cand[i];
     best = block_best(best, sc);
     // No comparable candidate (all remaining norms NaN): the reference's strict '>' scan
     // then keeps the column already at position t (factor.cpp:85-87).
     const bool none = best.col < 0;
-    const int64_t jp = none ? perm[t] : best.col;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t jp = none ? s.perm[t] : best.col;
+    __syncthreads();
+    if (bookkeep && threadIdx.x == 0) {
         const int64_t pp = none ? t : best.pos;
-        const int64_t ct = perm[t];
-        perm[t] = jp;
-        perm[pp] = ct;
-        pos[jp] = t;
-        pos[ct] = pp;
-        piv[t] = jp;
-        *nflag = 0;
+        const int64_t ct = s.perm[t];
+        s.perm[t] = jp;
+        s.perm[pp] = ct;
+        s.pos[jp] = t;
+        s.pos[ct] = pp;
+        s.piv[t] = jp;
+        *s.nflag = 0;
     }
-    for (int64_t i = threadIdx.x; i < k; i += kThreads) w[i] = ld_w(W, ld, layout, i, jp);
+    const int64_t r0 = (int64_t)chunk * s.rows, r1 = min(s.k, r0 + s.rows);
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) s.wv[i] = ld_w(s.W, s.ld, s.layout, i, jp);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t out = t + (int64_t)blockIdx.x * (kThreads / 32) + warp;
-    if (out < k) {
-        const double* q = Q + out * k;
+    for (int64_t l = warp; l < t; l += kThreads / 32) {
+        const double* y = s.Y + l * s.k;
         double a = 0.0;
-        for (int64_t l = lane; l < k; l += 32) a = fma(q[l], w[l], a);
+        for (int64_t i = max(r0, l) + lane; i < r1; i += 32) a = fma(y[i], s.wv[i], a);
         a = warp_sum(a);
-        if (lane == 0) y[out] = a;
+        if (lane == 0) s.part[(int64_t)chunk * (s.cap + 1) + l] = a;
     }
 }
 
-// ---------------------------------------------------------------------------
-// B: reflector of step t from y (every CTA recomputes it identically) and
-// Q[:, t:] -= beta * (Q[:, t:] v) v^T on a block of 32 rows (256 threads = 32 rows x 8
-// column groups). CTA 0 records R(t,t) and beta.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_reflect(int64_t k, int64_t t, const double* __restrict__ y,
-                                                      double* Q, double* diag, double* betas) {
-    __shared__ double sd[kThreads / 32];
-    __shared__ double part[8][33];
-    extern __shared__ double v[];  // k - t doubles
-    const int64_t len = k - t;
-    double s = 0.0;
-    for (int64_t i = 1 + threadIdx.x; i < len; i += kThreads) s = fma(y[t + i], y[t + i], s);
-    const double sigma = block_sum(s, sd);
-    const double alpha = y[t];
-    // make_householder (factor.cpp:24-38): beta = 0 for len <= 1 or sigma == 0.
-    if (len <= 1 || sigma == 0.0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) { diag[t] = alpha; betas[t] = 0.0; }
-        return;
+// Fixed-order sum of the chunk partials of entry l (l < n) into dst[l].
+__device__ void wy_sum_parts(const WY& s, int64_t n, double* dst, int64_t first, int64_t stride) {
+    for (int64_t l = first; l < n; l += stride) {
+        double a = 0.0;
+        for (int c = 0; c < s.nchunk; ++c) a += s.part[(int64_t)c * (s.cap + 1) + l];
+        dst[l] = a;
     }
-    const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sigma));
-    const double smu = copysign(mu, alpha);
-    const double v0 = __dadd_rn(alpha, smu);
-    const double beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
-    if (blockIdx.x == 0 && threadIdx.x == 0) { diag[t] = -smu; betas[t] = beta; }
-    for (int64_t i = threadIdx.x; i < len; i += kThreads) v[i] = i == 0 ? 1.0 : __ddiv_rn(y[t + i], v0);
-    __syncthreads();
-    const int r = threadIdx.x & 31, g = threadIdx.x >> 5;
-    const int64_t row = (int64_t)blockIdx.x * 32 + r;
-    double u = 0.0;
-    if (row < k)
-        for (int64_t i = g; i < len; i += 8) u = fma(Q[row + (t + i) * k], v[i], u);
-    part[g][r] = u;
-    __syncthreads();
-    if (g == 0) {
-        double tot = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) tot += part[q][r];
-        part[0][r] = tot * beta;
+}
+
+// u = T^T z (u_r = sum_{l <= r} T(l, r) z_l), r < t.
+__device__ void wy_u(const WY& s, int64_t t, int64_t first, int64_t stride) {
+    const double* z = s.vec;
+    double* u = s.vec + s.cap;
+    for (int64_t r = first; r < t; r += stride) {
+        double a = 0.0;
+        for (int64_t l = 0; l <= r; ++l) a = fma(s.T[l + r * s.cap], z[l], a);
+        u[r] = a;
     }
-    __syncthreads();
-    const double bu = part[0][r];
-    if (row < k)
-        for (int64_t i = g; i < len; i += 8) {
-            double* qp = Q + row + (t + i) * k;
-            *qp = fma(-bu, v[i], *qp);
+}
+
+// y = w - Y[:, :t] u for this chunk's rows; partial sigma = sum_{i > t} y_i^2.
+__device__ void wy_y(const WY& s, int64_t t, int chunk, double* red) {
+    const double* u = s.vec + s.cap;
+    const int64_t r0 = (int64_t)chunk * s.rows, r1 = min(s.k, r0 + s.rows);
+    double sg = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+        double y = s.wv[i];
+        for (int64_t l = 0; l < t && l <= i; ++l) y = fma(-s.Y[i + l * s.k], u[l], y);
+        s.yv[i] = y;
+        if (i > t) sg = fma(y, y, sg);
+    }
+    sg = block_sum(sg, red);
+    if (threadIdx.x == 0) s.part[(int64_t)chunk * (s.cap + 1) + s.cap] = sg;
+}
+
+// Reflector from y (make_householder, factor.cpp:24-38): every CTA derives the same
+// scalars from the chunk sigma partials; the chunk's rows of Y[:, t] are written and the
+// chunk's partial p = Y[:, :t]^T v computed.
+__device__ void wy_reflect(const WY& s, int64_t t, int chunk, bool record, double* red) {
+    __shared__ double sh[2];
+    if (threadIdx.x == 0) {
+        double sg = 0.0;
+        for (int c = 0; c < s.nchunk; ++c) sg += s.part[(int64_t)c * (s.cap + 1) + s.cap];
+        const double alpha = s.yv[t];
+        const int64_t len = s.k - t;
+        double beta = 0.0, v0 = 1.0, rkk = alpha;
+        if (len > 1 && sg != 0.0) {
+            const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sg));
+            const double smu = copysign(mu, alpha);
+            v0 = __dadd_rn(alpha, smu);
+            beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+            rkk = -smu;
         }
+        sh[0] = v0;
+        sh[1] = beta;
+        if (record) {
+            s.diag[t] = rkk;
+            s.beta[t] = beta;
+            s.vec[4 * s.cap] = v0;
+            s.vec[4 * s.cap + 1] = beta;
+        }
+    }
+    __syncthreads();
+    const double v0 = sh[0], beta = sh[1];
+    const int64_t r0 = (int64_t)chunk * s.rows, r1 = min(s.k, r0 + s.rows);
+    double* yt = s.Y + t * s.k;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads)
+        yt[i] = i < t ? 0.0 : (i == t ? 1.0 : (beta == 0.0 ? 0.0 : __ddiv_rn(s.yv[i], v0)));
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t l = warp; l < t; l += kThreads / 32) {
+        const double* y = s.Y + l * s.k;
+        double a = 0.0;
+        for (int64_t i = max(r0, t) + lane; i < r1; i += 32) a = fma(y[i], yt[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s.part[(int64_t)chunk * (s.cap + 1) + l] = a;
+    }
+    (void)red;
 }
 
-// ---------------------------------------------------------------------------
-// C: R(t,j) = q_t^T w_j, downdate, guard, candidates for step t+1, trailing mass.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void stream_epilogue(int64_t t, int64_t j, int64_t N, double r, double* R,
-                                                double* nu, const double* cref, const int64_t* pos,
-                                                int64_t* flags, int* nflag, Cand& best, double& mass) {
-    R[t * N + j] = r;
-    // factor.cpp:101-102: cnorm2 -= rkj*rkj; guard at 1e-16 * cref2 (no contraction).
-    const double nv = __dsub_rn(nu[j], __dmul_rn(r, r));
-    nu[j] = nv;
-    if (nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0) {
-        const int slot = atomicAdd(nflag, 1);
-        flags[slot] = j;
-    } else {
-        Cand c{nv, pos[j], j};
-        if (better(c, best)) best = c;
-        mass += nv;
+// T column t (T(r,t) = -beta sum_{c=r}^{t-1} T(r,c) p_c, T(t,t) = beta), then
+// g = T[:t+1, :t+1] rho with rho = row t of Y (so q_t = e_t - Y g). Rows r in the stride.
+__device__ void wy_tcol(const WY& s, int64_t t, int64_t first, int64_t stride) {
+    const double beta = s.vec[4 * s.cap + 1];
+    const double* p = s.vec + 2 * s.cap;
+    for (int64_t r = first; r <= t; r += stride) {
+        double a = 0.0;
+        if (r < t)
+            for (int64_t c = r; c < t; ++c) a = fma(s.T[r + c * s.cap], p[c], a);
+        s.T[r + t * s.cap] = r == t ? beta : -beta * a;
     }
 }
 
-// MODE 3: Row layout with few columns (N too small to fill the GPU one thread per column,
-// e.g. k = 640, N = 32768): a CTA owns 32 columns, its 8 warps split the k rows (each row
-// read as a coalesced 256-byte segment), partials combined in warp order in smem.
+__device__ void wy_g(const WY& s, int64_t t, int64_t first, int64_t stride) {
+    double* g = s.vec + 3 * s.cap;
+    for (int64_t r = first; r <= t; r += stride) {
+        double a = 0.0;
+        for (int64_t c = r; c <= t; ++c) a = fma(s.T[r + c * s.cap], s.Y[t + c * s.k], a);
+        g[r] = a;
+    }
+}
+
+// q_t(i) = [i == t] - sum_{l <= t} Y(i, l) g_l for this chunk's rows.
+__device__ void wy_q(const WY& s, int64_t t, int chunk) {
+    const double* g = s.vec + 3 * s.cap;
+    const int64_t r0 = (int64_t)chunk * s.rows, r1 = min(s.k, r0 + s.rows);
+    double* q = s.Qt + t * s.k;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+        double a = i == t ? 1.0 : 0.0;
+        for (int64_t l = 0; l <= t && l <= i; ++l) a = fma(-s.Y[i + l * s.k], g[l], a);
+        q[i] = a;
+    }
+}
+
+// Whole step in one CTA (nchunk == 1).
+__global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
+    __shared__ double red[kThreads / 32];
+    wy_pick(s, t, 0, true);
+    __syncthreads();
+    wy_sum_parts(s, t, s.vec, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_u(s, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_y(s, t, 0, red);
+    __syncthreads();
+    wy_reflect(s, t, 0, true, red);
+    __syncthreads();
+    wy_sum_parts(s, t, s.vec + 2 * s.cap, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_tcol(s, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_g(s, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_q(s, t, 0);
+}
+
+// Multi-CTA phases (row chunks) and the small single-CTA glue between them.
+__global__ void __launch_bounds__(kThreads) k_wy_pick(WY s, int64_t t) { wy_pick(s, t, blockIdx.x, blockIdx.x == 0); }
+
+__global__ void __launch_bounds__(1024) k_wy_zu(WY s, int64_t t) {
+    wy_sum_parts(s, t, s.vec, threadIdx.x, blockDim.x);
+    __syncthreads();
+    wy_u(s, t, threadIdx.x, blockDim.x);
+}
+
+__global__ void __launch_bounds__(kThreads) k_wy_y(WY s, int64_t t) {
+    __shared__ double red[kThreads / 32];
+    wy_y(s, t, blockIdx.x, red);
+}
+
+__global__ void __launch_bounds__(kThreads) k_wy_reflect(WY s, int64_t t) {
+    __shared__ double red[kThreads / 32];
+    wy_reflect(s, t, blockIdx.x, blockIdx.x == 0, red);
+}
+
+__global__ void __launch_bounds__(1024) k_wy_tg(WY s, int64_t t) {
+    wy_sum_parts(s, t, s.vec + 2 * s.cap, threadIdx.x, blockDim.x);
+    __syncthreads();
+    wy_tcol(s, t, threadIdx.x, blockDim.x);
+    __syncthreads();
+    wy_g(s, t, threadIdx.x, blockDim.x);
+}
+
+__global__ void __launch_bounds__(kThreads) k_wy_q(WY s, int64_t t) { wy_q(s, t, blockIdx.x); }
+
+// ---------------------------------------------------------------------------
+// stream: R(t,j) = q_t^T w_j, downdate, guard, candidates for step t+1, trailing mass.
+// ---------------------------------------------------------------------------
+// QS: q_t staged in shared memory (k <= kQSmem), else read through L1/L2.
+template <int MODE, bool QS>
+__global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ W, int64_t k, int64_t N,
+                                                     int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                     const double* diag, const int64_t* piv, double* R,
+                                                     double* nu, const double* cref, const int64_t* pos,
+                                                     int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    extern __shared__ double sm[];  // q (k doubles) then the MODE-2 tile
+    double* tile = sm + ((k + 1) & ~int64_t(1));
+    if (QS)
+        for (int64_t i = threadIdx.x; i < k; i += kThreads) sm[i] = Q[i + t * k];
+    const double* __restrict__ q = QS ? sm : Q + t * k;
+    __syncthreads();
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (MODE == 1) {
+        const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+        const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+        for (int64_t j = gw; j < N; j += nwarps) {
+            const int64_t pj = pos[j];
+            if (pj < t || j == jp) {
+                if (lane == 0) R[t * N + j] = j == jp ? diag[t] : 0.0;
+                continue;
+            }
+            const double* w = W + j * ld;
+            double a = 0.0;
+            for (int64_t i = lane; i < k; i += 32) a = fma(q[i], w[i], a);
+            a = warp_sum(a);
+            if (lane == 0 && downdate(t, j, N, a, pj, R, nu, cref, best, msum)) {
+                const int slot = atomicAdd(nflag, 1);
+                flags[slot] = j;
+            }
+        }
+    } else {
+        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
+            const int64_t j = j0 + threadIdx.x;
+            if (MODE == 2) load_tile_small_k(W, k, N, j0, tile);
+            // No early exits: every lane reaches the warp-aggregated flag append below.
+            const bool active = j < N;
+            const int64_t pj = active ? pos[j] : 0;
+            const bool chosen = active && (pj < t || j == jp);
+            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+            bool fl = false;
+            if (active && !chosen) {
+                double a = 0.0;
+                if (MODE == 2) {
+                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], tile[i * (kThreads + 1) + threadIdx.x], a);
+                } else {
+#pragma unroll 8
+                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], W[i * ld + j], a);
+                }
+                fl = downdate(t, j, N, a, pj, R, nu, cref, best, msum);
+            }
+            append_flag(fl, j, flags, nflag);
+        }
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
+// MODE 3: a CTA owns 32 columns; its 8 warps split the k rows (each row read as a
+// coalesced 256-byte segment); partials combined in warp order in smem.
 __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __restrict__ W, int64_t k, int64_t N,
                                                             int64_t ld, int64_t t, const double* __restrict__ Q,
                                                             const double* diag, const int64_t* piv, double* R,
@@ -272,25 +488,8 @@ __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __rest
             const bool chosen = active && (pj < t || j == jp);
             if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
             bool fl = false;
-            if (active && !chosen) {
-                R[t * N + j] = s;
-                const double nv = __dsub_rn(nu[j], __dmul_rn(s, s));
-                nu[j] = nv;
-                fl = nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0;
-                if (!fl) {
-                    Cand c{nv, pj, j};
-                    if (better(c, best)) best = c;
-                    msum += nv;
-                }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, fl);
-            if (m) {
-                const int leader = __ffs(m) - 1;
-                int base = 0;
-                if (lane == leader) base = atomicAdd(nflag, __popc(m));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (fl) flags[base + __popc(m & ((1u << lane) - 1u))] = j;
-            }
+            if (active && !chosen) fl = downdate(t, j, N, s, pj, R, nu, cref, best, msum);
+            append_flag(fl, j, flags, nflag);
         }
         __syncthreads();
     }
@@ -299,80 +498,77 @@ __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __rest
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ W, int64_t k, int64_t N,
-                                                     int64_t ld, int64_t t, const double* __restrict__ Q,
-                                                     const double* diag, const int64_t* piv, double* R,
-                                                     double* nu, const double* cref, const int64_t* pos,
-                                                     int64_t* flags, int* nflag, Cand* cand, double* mass) {
+// MODE 4 (very tall Row layout) and the tall init: partial column dots over a row split.
+// grid = (ceil(N/32), ksplit); out[split * N + j]. square != 0: sum of squares (init).
+__global__ void __launch_bounds__(kThreads) k_col_part(const double* __restrict__ W, int64_t k, int64_t N,
+                                                       int64_t ld, const double* __restrict__ q, int square,
+                                                       int64_t krange, double* out) {
+    __shared__ double part[kThreads / 32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t i0 = (int64_t)blockIdx.y * krange, i1 = min(k, i0 + krange);
+    double a = 0.0;
+    if (j < N)
+#pragma unroll 4
+        for (int64_t i = i0 + warp; i < i1; i += kThreads / 32) {
+            const double x = W[i * ld + j];
+            a = square ? fma(x, x, a) : fma(q[i], x, a);
+        }
+    part[warp][lane] = a;
+    __syncthreads();
+    if (warp == 0 && j < N) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) s += part[w][lane];
+        out[blockIdx.y * N + j] = s;
+    }
+}
+
+// MODE 4 finish: combine the row-split partials in split order, then the epilogue.
+__global__ void __launch_bounds__(kThreads) k_stream_fin(const double* __restrict__ kpart, int ksplit, int64_t N,
+                                                         int64_t t, const double* diag, const int64_t* piv,
+                                                         double* R, double* nu, const double* cref,
+                                                         const int64_t* pos, int64_t* flags, int* nflag, Cand* cand,
+                                                         double* mass) {
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sd[kThreads / 32];
-    extern __shared__ double sm[];  // q (k doubles) then the MODE-2 tile
-    double* q = sm;
-    double* tile = sm + ((k + 1) & ~int64_t(1));
-    for (int64_t i = threadIdx.x; i < k; i += kThreads) q[i] = Q[i + t * k];
-    __syncthreads();
     const int64_t jp = piv[t];
     Cand best = cand_none();
     double msum = 0.0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (MODE == 1) {
-        const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-        const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
-        for (int64_t j = gw; j < N; j += nwarps) {
-            const int64_t pj = pos[j];
-            if (pj < t || j == jp) {
-                if (lane == 0) R[t * N + j] = j == jp ? diag[t] : 0.0;
-                continue;
-            }
-            const double* w = W + j * ld;
+    for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
+        const int64_t j = j0 + threadIdx.x;
+        const bool active = j < N;
+        const int64_t pj = active ? pos[j] : 0;
+        const bool chosen = active && (pj < t || j == jp);
+        if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+        bool fl = false;
+        if (active && !chosen) {
             double a = 0.0;
-            for (int64_t i = lane; i < k; i += 32) a = fma(q[i], w[i], a);
-            a = warp_sum(a);
-            if (lane == 0) stream_epilogue(t, j, N, a, R, nu, cref, pos, flags, nflag, best, msum);
+            for (int s = 0; s < ksplit; ++s) a += kpart[(int64_t)s * N + j];
+            fl = downdate(t, j, N, a, pj, R, nu, cref, best, msum);
         }
-    } else {
-        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
-            const int64_t j = j0 + threadIdx.x;
-            if (MODE == 2) {
-                load_tile_small_k(W, k, N, j0, tile);
-            }
-            // No early exits: every lane reaches the warp-aggregated flag append below.
-            const bool active = j < N;
-            const int64_t pj = active ? pos[j] : 0;
-            const bool chosen = active && (pj < t || j == jp);
-            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
-            const bool work = active && !chosen;
-            bool fl = false;
-            if (work) {
-                double a = 0.0;
-                if (MODE == 2) {
-                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], tile[i * (kThreads + 1) + threadIdx.x], a);
-                } else {
-#pragma unroll 8
-                    for (int64_t i = 0; i < k; ++i) a = fma(q[i], W[i * ld + j], a);
-                }
-                R[t * N + j] = a;
-                // factor.cpp:101-102: cnorm2 -= rkj*rkj; guard at 1e-16 * cref2 (no contraction).
-                const double nv = __dsub_rn(nu[j], __dmul_rn(a, a));
-                nu[j] = nv;
-                fl = nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0;
-                if (!fl) {
-                    Cand c{nv, pj, j};
-                    if (better(c, best)) best = c;
-                    msum += nv;
-                }
-            }
-            // Hilbert-type ties flag thousands of columns per step: one atomic per warp.
-            const unsigned m = __ballot_sync(0xffffffffu, fl);
-            if (m) {
-                const int leader = __ffs(m) - 1;
-                int base = 0;
-                if (lane == leader) base = atomicAdd(nflag, __popc(m));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (fl) flags[base + __popc(m & ((1u << lane) - 1u))] = j;
-            }
-        }
+        append_flag(fl, j, flags, nflag);
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
+// Tall init finish: nu = cref = sum of the squared partials, identity positions.
+__global__ void __launch_bounds__(kThreads) k_init_fin(const double* __restrict__ kpart, int ksplit, int64_t N,
+                                                       double* nu, double* cref, int64_t* pos, int64_t* perm,
+                                                       Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
+        double a = 0.0;
+        for (int s = 0; s < ksplit; ++s) a += kpart[(int64_t)s * N + j];
+        nu[j] = a; cref[j] = a; pos[j] = j; perm[j] = j;
+        Cand c{a, j, j};
+        if (better(c, best)) best = c;
+        msum += a;
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sd);
@@ -380,64 +576,45 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// D1: guard recompute. For each flagged column j, the trailing norm after step t is
+// guard: for each flagged column j the trailing norm after step t is
 // |w_j - Q[:, :t+1] R(0:t, j)|^2 (= the sum of squares of rows t+1.. of the updated
-// column, factor.cpp:103-105). One warp per flagged column.
+// column, factor.cpp:103-105). One warp per flagged column, R(0:t, j) staged per warp.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W, int64_t k, int64_t N,
                                                     int64_t ld, int layout, int64_t t,
                                                     const double* __restrict__ Q, const double* R,
                                                     const int64_t* flags, const int* nflag, double* nu,
-                                                    double* cref) {
+                                                    double* cref, int stage_q) {
+    extern __shared__ double qs[];  // Q[:, :t+1] when staged (dynamic smem > 0)
+    __shared__ double rbuf[kThreads / 32][64];
     const int nf = *nflag;
+    if (nf == 0) return;
+    const bool staged = stage_q != 0;
+    if (staged)
+        for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
+    __syncthreads();
+    const double* __restrict__ qq = staged ? qs : Q;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool rsm = t + 1 <= 64;
     for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf; f += (int64_t)gridDim.x * (kThreads / 32)) {
         const int64_t j = flags[f];
+        if (rsm) {
+            for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = R[l * N + j];
+            __syncwarp();
+        }
         double s = 0.0;
         for (int64_t i = lane; i < k; i += 32) {
             double x = ld_w(W, ld, layout, i, j);
-            for (int64_t l = 0; l <= t; ++l) x = fma(-Q[i + l * k], R[l * N + j], x);
+            for (int64_t l = 0; l <= t; ++l) x = fma(-qq[i + l * k], rsm ? rbuf[warp][l] : R[l * N + j], x);
             s = fma(x, x, s);
         }
         s = warp_sum(s);
         if (lane == 0) { nu[j] = s; cref[j] = s; }
+        __syncwarp();
     }
 }
 
-// D1 for k <= 64: the trailing norm is |Q_{t+1}[:, t+1:]^T w_j|^2, the sum of squares of
-// rows t+1.. of the reflected column -- exactly the quantity factor.cpp:103-105 sums.
-// The k x (k-t-1) complement of the explicit Q sits in shared memory; one thread per
-// flagged column keeps w_j in registers.
-__global__ void __launch_bounds__(kThreads) k_guard_perp(const double* __restrict__ W, int64_t k, int64_t N,
-                                                         int64_t ld, int layout, int64_t t,
-                                                         const double* __restrict__ Q, const int64_t* flags,
-                                                         const int* nflag, double* nu, double* cref) {
-    __shared__ double qp[64 * 64];
-    const int nf = *nflag;
-    if (nf == 0) return;
-    const int kk = (int)k, m = (int)(k - t - 1);
-    for (int e = threadIdx.x; e < kk * m; e += kThreads) qp[e] = Q[(t + 1) * k + e];
-    __syncthreads();
-    for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
-        const int64_t j = flags[f];
-        double w[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) w[i] = i < kk ? ld_w(W, ld, layout, i, j) : 0.0;
-        double s = 0.0;
-        for (int c = 0; c < m; ++c) {
-            const double* qc = qp + c * kk;
-            double d = 0.0;
-#pragma unroll
-            for (int i = 0; i < 64; ++i)
-                if (i < kk) d = fma(qc[i], w[i], d);
-            s = fma(d, d, s);
-        }
-        nu[j] = s;
-        cref[j] = s;
-    }
-}
-
-// D2: candidates and trailing mass over all unpivoted columns (after a guard recompute).
+// candidates and trailing mass over all unpivoted columns (after a guard recompute).
 __global__ void __launch_bounds__(kThreads) k_recand(int64_t N, int64_t t, const int* nflag, const double* nu,
                                                      const int64_t* pos, Cand* cand, double* mass) {
     if (*nflag == 0) return;
@@ -486,27 +663,39 @@ __global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
-__global__ void k_identity(double* Q, int64_t k) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < k * k) Q[e] = (e % (k + 1) == 0) ? 1.0 : 0.0;
-}
-
 }  // namespace
 
 WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps)
     : W_(W), k_(k), N_(N), ld_(ld), p_(std::min(k, N)), layout_(layout) {
     if (k <= 0 || N <= 0) argument_error("qr_col_pivot: empty matrix");
-    if (layout == Layout::Col) mode_ = (k >= 64 || ld != k) ? 1 : 2;
-    else mode_ = (k >= 64 && N < (int64_t)sm_count() * 4 * kThreads) ? 3 : 0;
+    const int sms = sm_count();
+    if (layout == Layout::Col) {
+        mode_ = (k >= 64 || ld != k) ? 1 : 2;
+    } else if (k >= 64 && N < (int64_t)sms * 4 * kThreads && (k <= kQSmem || cdiv(N, 32) < 2 * sms)) {
+        // few columns: split the rows inside a CTA (MODE 3), or also across CTAs when
+        // even 32-column groups cannot fill the GPU (MODE 4)
+        mode_ = cdiv(N, 32) < 2 * sms && k >= 8192 ? 4 : 3;
+    } else {
+        mode_ = 0;
+    }
+    if (mode_ == 4) ksplit_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 2048), cdiv(4 * sms, cdiv(N, 32))));
     const int per_sm = 8;
     const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : cdiv(N, kThreads);
-    ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));
+    ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
+    nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(N); flags_.alloc(N);
     cand_.alloc(ncand_); mass_.alloc(ncand_); nflag_.alloc(1); nflag_.zero();
-    Q_.alloc(k * k); y_.alloc(k);
+    wv_.alloc(k); yv_.alloc(k);
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
+    if (mode_ == 4) kpart_.alloc((size_t)ksplit_ * N);
     grow(std::max<int64_t>(1, std::min(p_, cap_steps)));
-    TTG_LAUNCH(k_identity, cdiv(k * k, 256), 256, 0, stream(), Q_.get(), k);
+    if (mode_ == 4) {
+        const dim3 g((unsigned)cdiv(N, 32), (unsigned)ksplit_);
+        TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, nullptr, 1, cdiv(k, ksplit_), kpart_.get());
+        TTG_LAUNCH(k_init_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, nu_.get(), cref_.get(),
+                   pos_.get(), perm_.get(), cand_.get(), mass_.get());
+        return;
+    }
     const size_t smem = mode_ == 2 ? sizeof(double) * k * (kThreads + 1) : 0;
     auto init = (mode_ == 0 || mode_ == 3) ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
     allow_smem(init, smem);
@@ -516,11 +705,20 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
 
 void WideQrcp::grow(int64_t cap) {
     if (cap <= cap_) return;
-    DevBuf<double> nr(cap * N_);
-    if (steps_ > 0)
-        TTG_CUDA(cudaMemcpyAsync(nr.get(), R_.get(), sizeof(double) * steps_ * N_, cudaMemcpyDeviceToDevice,
-                                 stream()));
+    DevBuf<double> nr(cap * N_), ny(k_ * cap), nq(k_ * cap), nt(cap * cap);
+    if (steps_ > 0) {
+        TTG_CUDA(cudaMemcpyAsync(nr.get(), R_.get(), sizeof(double) * steps_ * N_, cudaMemcpyDeviceToDevice, stream()));
+        TTG_CUDA(cudaMemcpyAsync(ny.get(), Y_.get(), sizeof(double) * k_ * steps_, cudaMemcpyDeviceToDevice, stream()));
+        TTG_CUDA(cudaMemcpyAsync(nq.get(), Qt_.get(), sizeof(double) * k_ * steps_, cudaMemcpyDeviceToDevice, stream()));
+        TTG_CUDA(cudaMemcpy2DAsync(nt.get(), sizeof(double) * cap, T_.get(), sizeof(double) * cap_,
+                                   sizeof(double) * steps_, steps_, cudaMemcpyDeviceToDevice, stream()));
+    }
     R_ = std::move(nr);
+    Y_ = std::move(ny);
+    Qt_ = std::move(nq);
+    T_ = std::move(nt);
+    part_.alloc((size_t)nchunk_ * (cap + 1));
+    vecs_.alloc((size_t)(4 * cap + 2));
     cap_ = cap;
 }
 
@@ -534,19 +732,19 @@ double WideQrcp::trailing_mass() {
 double WideQrcp::refresh_exact() {
     const int64_t s = steps_;
     if (s == 0) return trailing_mass();
-    DevBuf<double> Y((size_t)(k_ * N_));
+    DevBuf<double> Yr((size_t)(k_ * N_));
     if (layout_ == Layout::Col) {
-        TTG_CUDA(cudaMemcpy2DAsync(Y.get(), sizeof(double) * k_, W_, sizeof(double) * ld_, sizeof(double) * k_, N_,
+        TTG_CUDA(cudaMemcpy2DAsync(Yr.get(), sizeof(double) * k_, W_, sizeof(double) * ld_, sizeof(double) * k_, N_,
                                    cudaMemcpyDeviceToDevice, stream()));
-        // Y (k x N) -= Q[:, :s] * C with C(t, j) = R[t*N + j], i.e. C = (N x s col-major)^T
-        gemm(false, true, k_, N_, s, Q_.get(), k_, R_.get(), N_, Y.get(), k_, -1.0, 1.0);
+        // Yr (k x N) -= Q[:, :s] * C with C(t, j) = R[t*N + j], i.e. C = (N x s col-major)^T
+        gemm(false, true, k_, N_, s, Qt_.get(), k_, R_.get(), N_, Yr.get(), k_, -1.0, 1.0);
     } else {
-        TTG_CUDA(cudaMemcpy2DAsync(Y.get(), sizeof(double) * N_, W_, sizeof(double) * ld_, sizeof(double) * N_, k_,
+        TTG_CUDA(cudaMemcpy2DAsync(Yr.get(), sizeof(double) * N_, W_, sizeof(double) * ld_, sizeof(double) * N_, k_,
                                    cudaMemcpyDeviceToDevice, stream()));
-        // Y^T (N x k) -= C^T (N x s) * Q[:, :s]^T
-        gemm(false, true, N_, k_, s, R_.get(), N_, Q_.get(), k_, Y.get(), N_, -1.0, 1.0);
+        // Yr^T (N x k) -= C^T (N x s) * Q[:, :s]^T
+        gemm(false, true, N_, k_, s, R_.get(), N_, Qt_.get(), k_, Yr.get(), N_, -1.0, 1.0);
     }
-    TTG_LAUNCH(k_resnorm, ncand_, kThreads, 0, stream(), Y.get(), k_, N_, (int)layout_, s, nu_.get(), cref_.get(),
+    TTG_LAUNCH(k_resnorm, ncand_, kThreads, 0, stream(), Yr.get(), k_, N_, (int)layout_, s, nu_.get(), cref_.get(),
                pos_.get(), cand_.get(), mass_.get());
     return trailing_mass();
 }
@@ -559,37 +757,64 @@ void WideQrcp::run_to(int64_t steps) {
 
 void WideQrcp::step() {
     const int64_t t = steps_;
-    const int64_t nout = k_ - t;
-    allow_smem(k_pick, sizeof(double) * k_);
-    allow_smem(k_reflect, sizeof(double) * nout);
-    TTG_LAUNCH(k_pick, (int)cdiv(nout, kThreads / 32), kThreads, sizeof(double) * k_, stream(), W_, k_, N_,
-               ld_, (int)layout_, t, cand_.get(), ncand_, pos_.get(), perm_.get(), piv_.get(), nflag_.get(),
-               Q_.get(), y_.get());
-    TTG_LAUNCH(k_reflect, (int)cdiv(k_, 32), kThreads, sizeof(double) * nout, stream(), k_, t, y_.get(),
-               Q_.get(), diag_.get(), beta_.get());
+    reflect_step(t);
     gemv_step(t);
     steps_ = t + 1;
 }
 
+void WideQrcp::reflect_step(int64_t t) {
+    WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
+         vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
+         ncand_, 1, k_};
+    // one fused CTA while the O(k t) work is small, row chunks otherwise
+    const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(nchunk_, cdiv(k_ * (t + 1), 32768)));
+    if (nch == 1) {
+        TTG_LAUNCH(k_wy_fused, 1, kThreads, 0, stream(), s, t);
+        return;
+    }
+    s.nchunk = nch;
+    s.rows = cdiv(k_, nch);
+    TTG_LAUNCH(k_wy_pick, nch, kThreads, 0, stream(), s, t);
+    TTG_LAUNCH(k_wy_zu, 1, 1024, 0, stream(), s, t);
+    TTG_LAUNCH(k_wy_y, nch, kThreads, 0, stream(), s, t);
+    TTG_LAUNCH(k_wy_reflect, nch, kThreads, 0, stream(), s, t);
+    TTG_LAUNCH(k_wy_tg, 1, 1024, 0, stream(), s, t);
+    TTG_LAUNCH(k_wy_q, nch, kThreads, 0, stream(), s, t);
+}
+
 void WideQrcp::gemv_step(int64_t t) {
-    const size_t qbytes = sizeof(double) * ((k_ + 1) & ~int64_t(1));
-    const size_t smem = qbytes + (mode_ == 2 ? sizeof(double) * k_ * (kThreads + 1) : 0);
-    auto kern = mode_ == 0 ? k_stream<0> : mode_ == 1 ? k_stream<1> : mode_ == 2 ? k_stream<2> : k_stream_splitk;
-    allow_smem(kern, smem);
     prof_begin();
-    TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Q_.get(), diag_.get(), piv_.get(),
-               R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    if (mode_ == 4) {
+        const dim3 g((unsigned)cdiv(N_, 32), (unsigned)ksplit_);
+        TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, Qt_.get() + t * k_, 0, cdiv(k_, ksplit_),
+                   kpart_.get());
+        TTG_LAUNCH(k_stream_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, t, diag_.get(), piv_.get(),
+                   R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    } else {
+        const size_t qbytes = sizeof(double) * ((k_ + 1) & ~int64_t(1));
+        const size_t smem = (mode_ == 2 ? qbytes + sizeof(double) * k_ * (kThreads + 1)
+                                        : (k_ <= kQSmem || mode_ == 3 ? qbytes : 0));
+        const bool qs = k_ <= kQSmem;
+        auto kern = mode_ == 0   ? (qs ? k_stream<0, true> : k_stream<0, false>)
+                    : mode_ == 1 ? (qs ? k_stream<1, true> : k_stream<1, false>)
+                    : mode_ == 2 ? k_stream<2, true>
+                                 : k_stream_splitk;
+        allow_smem(kern, smem);
+        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Qt_.get(), diag_.get(), piv_.get(),
+                   R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    }
     // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
     // written once, and row t of R written.
     prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
-    if (k_ <= 64)
-        TTG_LAUNCH(k_guard_perp, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_,
-                   t, Q_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
-    else
-        TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, 0, stream(), W_, k_, N_, ld_, (int)layout_, t,
-                   Q_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get());
-    TTG_LAUNCH(k_recand, ncand_, kThreads, 0, stream(), N_, t, nflag_.get(), nu_.get(), pos_.get(),
-               cand_.get(), mass_.get());
+    // the guard stages Q[:, :t+1] in shared memory when it fits (<= 96 KB)
+    const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
+    const bool stage = gq <= 96 * 1024;
+    allow_smem(k_guard, stage ? gq : 0);
+    TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_,
+               (int)layout_, t, Qt_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(),
+               stage ? 1 : 0);
+    TTG_LAUNCH(k_recand, ncand_, kThreads, 0, stream(), N_, t, nflag_.get(), nu_.get(), pos_.get(), cand_.get(),
+               mass_.get());
 }
 
 }  // namespace ttg

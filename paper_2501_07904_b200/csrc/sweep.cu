@@ -21,7 +21,8 @@
 #include <chrono>
 #include <memory>
 #include <cmath>
-#include <sstream>
+#include <cstdio>
+#include <cstdlib>
 
 #include "sweep.hpp"
 #include "utv.hpp"
@@ -31,10 +32,13 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
-std::string fmt_g(double v) {
-    std::ostringstream os;
-    os << v;
-    return os.str();
+// TTG_CUT_TIMING=1: synchronise after every cut and print its wall time (diagnostics).
+bool cut_timing() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTG_CUT_TIMING");
+        return e && *e == '1';
+    }();
+    return on;
 }
 
 // ---- small device kernels -----------------------------------------------------------
@@ -235,10 +239,15 @@ struct TallPass1 final : Pass1 {
     }
 };
 
-// Engine choice: the wide engine keeps a k x k orthogonal factor, so it is used while
-// k is moderate or W is not tall.
+// Engine choice: the read-only WY engine costs O(k t) per step besides the stream over W,
+// so it serves wide and tall W alike; TTG_TALL_INPLACE=1 selects the in-place engine for
+// tall W instead (kept as a cross-check).
 std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap) {
-    if (k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    static const bool inplace = [] {
+        const char* e = std::getenv("TTG_TALL_INPLACE");
+        return e && *e == '1';
+    }();
+    if (inplace && k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
     return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
 }
 
@@ -716,8 +725,15 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
             } else {
                 rq.budget = mode.budgets[(size_t)(k - 1)];
             }
+            const auto tc0 = Clock::now();
             auto e1 = make_pass1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
             CutOut co = run_cut(*e1, rq);
+            if (cut_timing()) {
+                sync();
+                std::fprintf(stderr, "[ttg] ulv cut %lld (%lld x %lld): %lld steps, %.3f ms\n", (long long)k,
+                             (long long)m, (long long)n, (long long)co.steps,
+                             std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
+            }
             const int64_t r = co.rank;
             res.step_errors[(size_t)(k - 1)] = co.step_error;
             res.ranks_chosen[(size_t)k] = r;
@@ -756,8 +772,15 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
                 rq.budget = mode.budgets[(size_t)(k - 2)];
             }
             // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
+            const auto tc0 = Clock::now();
             auto e1 = make_pass1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
             CutOut co = run_cut(*e1, rq);
+            if (cut_timing()) {
+                sync();
+                std::fprintf(stderr, "[ttg] urv cut %lld (%lld x %lld): %lld steps, %.3f ms\n", (long long)(k - 1),
+                             (long long)M, (long long)n, (long long)co.steps,
+                             std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
+            }
             const int64_t r = co.rank;
             res.step_errors[(size_t)(k - 2)] = co.step_error;
             res.ranks_chosen[(size_t)(k - 1)] = r;
@@ -780,7 +803,6 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
             }
         }
     }
-    (void)fmt_g;
     finish(res, rss, start);
     return res;
 }
