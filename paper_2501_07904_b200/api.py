@@ -72,7 +72,10 @@ class DeviceResult:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().ttg_result_free(self.h)
+            try:
+                lib().ttg_result_free(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def order(self) -> int:

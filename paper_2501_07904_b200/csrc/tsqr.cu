@@ -76,6 +76,242 @@ __global__ void __launch_bounds__(kT) k_tsqr_leaf(const double* __restrict__ B, 
     }
 }
 
+// Register-resident Householder QR of a ROWS x s block (s <= S <= 32) for the TSQR tree:
+// thread `tid` holds rows i*256 + tid (i < RPT) of all S columns in registers, so a
+// reflector step is two block reductions (the column mass, then the S column dots in one
+// warp reduce-scatter) and a register update -- no shared-memory traffic over the data.
+// Column c's reflector has v = 1 at row c (thread c, slot 0) and x/v0 below, the
+// formulas of smem_householder. Columns padded past s are zero and stay zero.
+template <int S, int RPT>
+__global__ void __launch_bounds__(kT, 1) k_tsqr_reg(const double* __restrict__ B, int64_t N, int s, int64_t ld,
+                                                    double* __restrict__ out, int64_t ldo) {
+    constexpr int ROWS = kT * RPT, NW = kT / 32;
+    __shared__ double part[NW][S];
+    __shared__ double tau[S];
+    __shared__ double red[NW];
+    __shared__ double bc;
+    __shared__ double Rs[S * S];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    const int rows = (int)min((int64_t)ROWS, N - r0);
+    double x[RPT][S];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int row = i * kT + tid;
+#pragma unroll
+        for (int j = 0; j < S; ++j) x[i][j] = (row < rows && j < s) ? B[r0 + row + (int64_t)j * ld] : 0.0;
+    }
+    const int p = min(rows, s);
+    double* orow = out + (int64_t)blockIdx.x * s;
+    // Step c works on register column 0: after every step the columns shift left by one,
+    // so all register indices are static and the loop stays rolled (small code).
+#pragma unroll 1
+    for (int c = 0; c < p; ++c) {
+        // column mass below row c, and alpha = x(c, c)
+        double sg = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+            if (i * kT + tid > c) sg = fma(x[i][0], x[i][0], sg);
+        sg = warp_sum(sg);
+        if (lane == 0) red[warp] = sg;
+        if (tid == c) bc = x[0][0];
+        __syncthreads();
+        double sigma = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) sigma += red[w];
+        const double alpha = bc;
+        if (rows - c > 1 && sigma != 0.0) {
+            const double mu = sqrt(fma(alpha, alpha, sigma));
+            const double smu = copysign(mu, alpha);
+            const double v0 = alpha + smu;
+            const double beta = v0 / smu;
+            double v[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int row = i * kT + tid;
+                v[i] = row > c ? x[i][0] / v0 : (row == c ? 1.0 : 0.0);
+            }
+            // d_j = sum_rows v_i x_ij (register column j = matrix column c + j), reduce-
+            // scattered so lane j holds the warp sum of column j
+            // first reduce-scatter level fused with the dots, so only S/2 partials live
+            constexpr int H = S / 2;
+            double d[H];
+            {
+                const bool up = (lane & H) != 0;
+#pragma unroll
+                for (int j = 0; j < H; ++j) {
+                    double lo = 0.0, hi = 0.0;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        if (j > 0) lo = fma(v[i], x[i][j], lo);
+                        hi = fma(v[i], x[i][j + H], hi);
+                    }
+                    if (S < 32) {
+#pragma unroll
+                        for (int off = 16; off >= S; off >>= 1) {
+                            lo += __shfl_xor_sync(0xffffffffu, lo, off);
+                            hi += __shfl_xor_sync(0xffffffffu, hi, off);
+                        }
+                    }
+                    const double send = up ? lo : hi;
+                    const double keep = up ? hi : lo;
+                    d[j] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+                }
+            }
+#pragma unroll
+            for (int h = H / 2; h >= 1; h >>= 1) {
+                const bool up = (lane & h) != 0;
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    const double send = up ? d[j] : d[j + h];
+                    const double keep = up ? d[j + h] : d[j];
+                    d[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+                }
+            }
+            if (lane < S) part[warp][lane] = d[0];
+            __syncthreads();
+            if (tid < S) {
+                double w = 0.0;
+#pragma unroll
+                for (int q = 0; q < NW; ++q) w += part[q][tid];
+                tau[tid] = beta * w;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 1; j < S; ++j) {
+                const double tj = tau[j];
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) x[i][j] = fma(-tj, v[i], x[i][j]);
+            }
+            if (tid == c) x[0][0] = -smu;
+        } else {
+            __syncthreads();
+        }
+        // row c of R is final: thread c parks it in shared memory
+        if (tid == c) {
+#pragma unroll
+            for (int j = 0; j < S; ++j)
+                if (c + j < S) Rs[(c + j) * S + c] = x[0][j];
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+            for (int j = 0; j + 1 < S; ++j) x[i][j] = x[i][j + 1];
+            x[i][S - 1] = 0.0;
+        }
+    }
+    __syncthreads();
+    // upper triangle out (rows >= p, i.e. blocks with fewer than s rows, are zero)
+    for (int e = tid; e < s * s; e += kT) {
+        const int j = e / s, i = e - j * s;
+        orow[i + (int64_t)j * ldo] = (i <= j && i < p) ? Rs[j * S + i] : 0.0;
+    }
+}
+
+// Leaf variant of k_tsqr_reg with the column loop fully unrolled (static register
+// columns, no shifting, dead columns skipped at compile time). Its code is large, which
+// costs instruction fetch on a lone CTA but pays off when every SM runs the same blocks
+// (the leaf level); the rolled kernel serves the small upper levels.
+template <int S, int RPT>
+__global__ void __launch_bounds__(kT, 1) k_tsqr_unr(const double* __restrict__ B, int64_t N, int s, int64_t ld,
+                                                    double* __restrict__ out, int64_t ldo) {
+    constexpr int ROWS = kT * RPT, NW = kT / 32;
+    __shared__ double part[NW][S];
+    __shared__ double tau[S];
+    __shared__ double red[NW];
+    __shared__ double bc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    const int rows = (int)min((int64_t)ROWS, N - r0);
+    double x[RPT][S];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int row = i * kT + tid;
+#pragma unroll
+        for (int j = 0; j < S; ++j) x[i][j] = (row < rows && j < s) ? B[r0 + row + (int64_t)j * ld] : 0.0;
+    }
+    const int p = min(rows, s);
+#pragma unroll
+    for (int c = 0; c < S; ++c) {
+        if (c >= p) break;
+        double sg = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+            if (i * kT + tid > c) sg = fma(x[i][c], x[i][c], sg);
+        sg = warp_sum(sg);
+        if (lane == 0) red[warp] = sg;
+        if (tid == c) bc = x[0][c];
+        __syncthreads();
+        double sigma = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) sigma += red[w];
+        const double alpha = bc;
+        if (rows - c <= 1 || sigma == 0.0) {
+            __syncthreads();
+            continue;
+        }
+        const double mu = sqrt(fma(alpha, alpha, sigma));
+        const double smu = copysign(mu, alpha);
+        const double v0 = alpha + smu;
+        const double beta = v0 / smu;
+        double v[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int row = i * kT + tid;
+            v[i] = row > c ? x[i][c] / v0 : (row == c ? 1.0 : 0.0);
+        }
+        double d[S];
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            double t = 0.0;
+            if (j > c) {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) t = fma(v[i], x[i][j], t);
+            }
+            d[j] = t;
+        }
+        if (S < 32) {
+#pragma unroll
+            for (int off = 16; off >= S; off >>= 1)
+#pragma unroll
+                for (int j = 0; j < S; ++j) d[j] += __shfl_xor_sync(0xffffffffu, d[j], off);
+        }
+#pragma unroll
+        for (int h = S / 2; h >= 1; h >>= 1) {
+            const bool up = (lane & h) != 0;
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const double send = up ? d[j] : d[j + h];
+                const double keep = up ? d[j + h] : d[j];
+                d[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        if (lane < S) part[warp][lane] = d[0];
+        __syncthreads();
+        if (tid < S) {
+            double w = 0.0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w += part[q][tid];
+            tau[tid] = beta * w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            if (j > c) {
+                const double tj = tau[j];
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) x[i][j] = fma(-tj, v[i], x[i][j]);
+            }
+        }
+        if (tid == c) x[0][c] = -smu;
+    }
+    if (tid < s) {
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (j < s) out[(int64_t)blockIdx.x * s + tid + (int64_t)j * ldo] = (j >= tid && tid < rows) ? x[0][j] : 0.0;
+    }
+}
+
 // Levels >= 1: stack g consecutive s x s triangles (rows [b*g*s, ...)) and factor. When
 // the stack does not fit in shared memory it is factored in place in the (scratch) input.
 __global__ void __launch_bounds__(kT) k_tsqr_node(double* in, int64_t nrows, int s, int64_t ldi, int g,
@@ -319,7 +555,40 @@ void small_qrcp(const double* A, int64_t m, int64_t n, int64_t lda, int64_t* per
 
 bool tsqr_fits(int64_t s) { return s <= 160; }
 
+// Leaf level with the unrolled kernel <S, RL> when it spans at least a wave, then the
+// rolled kernel <S, RU> up the tree.
+template <int S, int RL, int RU>
+void tsqr_reg_tree(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout) {
+    DevBuf<double> lvl;
+    const double* in = B;
+    int64_t rows = N, ldi = ld;
+    bool leaf = true;
+    while (true) {
+        const bool unr = leaf && cdiv(rows, (int64_t)kT * RL) >= sm_count();
+        const int64_t nb = cdiv(rows, (int64_t)kT * (unr ? RL : RU));
+        double* dst = Rout;
+        DevBuf<double> nxt;
+        if (nb > 1) {
+            nxt = DevBuf<double>((size_t)(nb * s * s));
+            dst = nxt.get();
+        }
+        if (unr)
+            TTG_LAUNCH((k_tsqr_unr<S, RL>), (int)nb, kT, 0, stream(), in, rows, (int)s, ldi, dst, nb * s);
+        else
+            TTG_LAUNCH((k_tsqr_reg<S, RU>), (int)nb, kT, 0, stream(), in, rows, (int)s, ldi, dst, nb * s);
+        leaf = false;
+        if (nb == 1) break;
+        lvl = std::move(nxt);
+        in = lvl.get();
+        rows = nb * s;
+        ldi = rows;
+    }
+}
+
 void tsqr_r(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout) {
+    if (s <= 8) return tsqr_reg_tree<8, 8, 4>(B, N, s, ld, Rout);
+    if (s <= 16) return tsqr_reg_tree<16, 4, 2>(B, N, s, ld, Rout);
+    if (s <= 32) return tsqr_reg_tree<32, 2, 1>(B, N, s, ld, Rout);
     // rows per leaf block: a multiple of s, >= 128, within ~200 KB of shared memory
     int rb = (int)std::max<int64_t>(s, 128);
     while ((int64_t)rb * 2 * s * 8 <= 160 * 1024 && rb < 1024) rb *= 2;
