@@ -16,8 +16,11 @@ plus one TT-URV right-to-left decomposition of the whole tensor (2 x 33.5M entri
 
 `--impl reference` times the reference CPU implementation itself on the same workload.
 `--config {1,2,3,5}` selects another BASELINE config (parity/extra measurements).
-Multi-GPU (torchrun): config 2 does not shard, so every rank runs an independent
+Multi-GPU (torchrun): configs 1-3 do not shard, so every rank runs an independent
 replica ("replicas only", scaling weak); value = all ranks' entries / max rank time.
+Config 5 at N > 1 runs the column-sharded TT-URV (one tensor split across the ranks,
+NCCL all-gathers of the pivot records / TSQR triangles / carry; scaling strong); value =
+the tensor's entries / max rank time.
 """
 from __future__ import annotations
 
@@ -70,10 +73,12 @@ class Clocks:
         self.proc = None
 
     def start(self):
+        if os.environ.get("BENCH_NO_SMI") == "1":  # diagnostics: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "250"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
 
@@ -171,7 +176,12 @@ def run_reference(args):
     from oracle import ref
     from paper_2501_07904_b200.inputs import build
     import torch
-    a = build(args.config, "cuda" if torch.cuda.is_available() else "cpu").cpu().numpy()
+    full = build(args.config, "cuda" if torch.cuda.is_available() else "cpu")
+    a, dims, rk, note = cpu_sample(full, args.config, c)
+    del full
+    cs = dict(c, dims=dims)
+    if rk is not None:
+        cs["ranks"] = rk
     n = a.size
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     small = ref.gen_gaussian([8, 8, 8], 1)
@@ -180,10 +190,11 @@ def run_reference(args):
     t0 = time.perf_counter()
     ranks = None
     for _ in range(args.steps):
-        ranks = reference_step(ref, a, c, runs)
+        ranks = reference_step(ref, a, cs, runs)
     dt = time.perf_counter() - t0
     value = args.steps * len(runs) * n / dt
-    sample = f"{args.steps} full step(s) of {desc} ({len(runs)} decomposition(s) each), ranks {ranks}"
+    sample = (f"{args.steps} step(s) of {desc} ({len(runs)} decomposition(s) each) on {note}, dims {dims}, "
+              f"ranks {ranks}")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -210,16 +221,40 @@ def run_ours(args):
     n = a.numel()
     dims = c["dims"]
     stream = torch.cuda.ExternalStream(lib().ttg_stream(), device=torch.device("cuda", local))
+    sharded = args.sharded or (args.config == 5 and world > 1)
 
     def kw(method):
         return dict(eps=c["eps"]) if c["mode"] == "tol" else dict(ranks=c["ranks"])
+
+    comm = None
+    blk = None
+    if sharded:
+        # one NCCL communicator for the engine; its unique id travels over torch.distributed
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        if dist:
+            dist.broadcast_object_list(obj, src=0)
+        comm = api.nccl_comm(obj[0], world, rank)
+        method = runs[0][0]
+        lo, hi, rows, cols = api.shard_range(dims, method, world, rank)
+        if method == "ulv":
+            blk = a[rows * lo:rows * hi].clone()
+        else:  # rows [lo, hi) of c = A(i1..i(d-1); id): an (hi-lo) x Id column-major block
+            blk = a.view(cols, n // cols)[:, lo:hi].contiguous()
+        del a
+        torch.cuda.empty_cache()
+        a = None
+    src = blk if sharded else a
 
     info = {}
 
     def step_device():
         for method, sweep in runs:
-            res = api.decompose_device(a.data_ptr(), dims, method, sweep, a_is_device_ptr=True, qlp=args.qlp,
-                                       **kw(method))
+            if sharded:
+                res = api.decompose_sharded(blk.data_ptr(), dims, comm, method, sweep, a_is_device_ptr=True,
+                                            qlp=args.qlp, **kw(method))
+            else:
+                res = api.decompose_device(a.data_ptr(), dims, method, sweep, a_is_device_ptr=True, qlp=args.qlp,
+                                           **kw(method))
             info[method] = res
         return info
 
@@ -243,10 +278,13 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     t_begin = time.time()
     e0.record(stream)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     for i in range(args.steps):
         ts = time.perf_counter()
+        marks[i].record(stream)
         step_device()
         log(f"step {i}: {1e3 * (time.perf_counter() - ts):.1f} ms host wall")
+    marks[-1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     t_end = time.time()
@@ -255,41 +293,49 @@ def run_ours(args):
         dist.barrier()
     launches = lib().ttg_kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
+    log("device ms per step: " + " ".join(f"{marks[i].elapsed_time(marks[i + 1]):.1f}" for i in range(args.steps)))
     nk = lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))
     lib().ttg_profile_enable(0)
     kern_ms, kern_bytes = d0.value, d1.value
     ms_max = max_over_ranks(ms, dist)
     entries_per_step = len(runs) * n
-    value = world * args.steps * entries_per_step / (ms_max * 1e-3)
+    jobs = 1 if sharded else world  # sharded: one tensor across the ranks (strong scaling)
+    value = jobs * args.steps * entries_per_step / (ms_max * 1e-3)
 
     rep = {m: r.report() for m, r in info.items()}
     rse = {m: r.rse(a.data_ptr(), on_device=True) for m, r in info.items()} if args.config != 5 else {}
     info.clear()
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region ----
-    host = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    host.copy_(a)
+    host = torch.empty(src.numel(), dtype=torch.float64, pin_memory=True)
+    host.copy_(src.reshape(-1))
     torch.cuda.synchronize()
     h2d = d2h = 0
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for method, sweep in runs:
-            res = api.decompose_device(host.data_ptr(), dims, method, sweep, qlp=args.qlp, **kw(method))
-            h2d += n * 8
+            if sharded:
+                res = api.decompose_sharded(host.data_ptr(), dims, comm, method, sweep, qlp=args.qlp, **kw(method))
+            else:
+                res = api.decompose_device(host.data_ptr(), dims, method, sweep, qlp=args.qlp, **kw(method))
+            h2d += src.numel() * 8
             for k in range(res.order()):
                 d2h += res.core(k).nbytes
     e2e_s = time.perf_counter() - t0
     e2e_s = max_over_ranks(e2e_s, dist)
-    e2e_value = world * args.steps * entries_per_step / e2e_s
+    e2e_value = jobs * args.steps * entries_per_step / e2e_s
 
     peak, peak_kind = hbm_peak()
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
     traffic = ncu_traffic(args.config)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "entries_per_step": entries_per_step,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                       "parallelism": (f"column-sharded x{world} (NCCL)" if sharded else
+                                       f"replicas x{world}" if world > 1 else "single-gpu"),
                        "l2": f"input {n * 8 / 1e6:.0f} MB vs 126 MB L2" + (" (larger than L2, no flush)" if n * 8 > 126e6 else " (L2-resident between steps)"),
                        "qlp": args.qlp,
                        "ranks": {m: r.ranks_chosen for m, r in rep.items()},
@@ -305,7 +351,8 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(a.cpu().numpy(), c, runs, desc)
+        line["cpu_baseline"] = cpu_baseline(src, args.config, c, runs, desc)
+    comm = None
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -313,19 +360,45 @@ def run_ours(args):
     return 0
 
 
-def cpu_baseline(a_host, c, runs, desc):
+def cpu_sample(a, cfg: int, c):
+    """A bounded sample of the workload for the CPU reference (about 10-30 s on the box's
+    host cores): the whole tensor for configs 1-2; for the long configs a slice along one
+    mode (a slice of a TT tensor is a TT tensor of the same ranks, clamped to the mode):
+    config 3 keeps 3 of the 24 indices of the last mode, config 5 keeps 32 of the 1024
+    indices of the middle mode. Returns (host array, dims, ranks or None, note)."""
+    dims = list(c["dims"])
+    ranks = c.get("ranks")
+    if cfg == 3:
+        t = a.view(*reversed(dims))[:3].contiguous()  # reversed view: last mode first
+        dims2 = dims[:-1] + [3]
+        r2 = list(ranks)
+        r2[-2] = min(r2[-2], 3)
+        return t.cpu().numpy().reshape(-1), dims2, r2, "last mode sliced to 3 of 24 (1/8 of the entries)"
+    if cfg == 5:
+        t = a.view(*reversed(dims))[:, :32, :].contiguous()
+        dims2 = [dims[0], 32, dims[2]]
+        return t.cpu().numpy().reshape(-1), dims2, list(ranks), "middle mode sliced to 32 of 1024 (1/32 of the entries)"
+    return a.cpu().numpy().reshape(-1), dims, ranks, "the whole tensor"
+
+
+def cpu_baseline(a, cfg, c, runs, desc):
     try:
         from oracle import ref
         if not ref.available():
             return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+        a_host, dims, ranks, note = cpu_sample(a, cfg, c)
+        cs = dict(c, dims=dims)
+        if ranks is not None:
+            cs["ranks"] = ranks
         small = ref.gen_gaussian([8, 8, 8], 1)
         ref.decompose(small, [8, 8, 8], "urv", "r2l", ranks=[1, 3, 3, 1])
         t0 = time.perf_counter()
-        ranks = reference_step(ref, a_host, c, runs)
+        got = reference_step(ref, a_host, cs, runs)
         dt = time.perf_counter() - t0
         return {"value": len(runs) * a_host.size / dt, "unit": UNIT,
                 "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "reference",
-                "sample": f"one full step of {desc} on the reference library, ranks {ranks}, {dt:.1f} s"}
+                "sample": f"one step of {desc} on the reference library ({note}, dims {dims}), ranks {got}, "
+                          f"{dt:.1f} s"}
     except Exception as e:  # the baseline is reported, never required
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -344,6 +417,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
     ap.add_argument("--qlp", default="early_exit", choices=["early_exit", "full"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="column-sharded engine over NCCL even at one rank (default for config 5 at N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

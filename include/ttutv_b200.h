@@ -88,6 +88,9 @@ ttg_status ttg_set_device(int device);
 /* Number of CUDA kernels this thread has launched (monotone counter; for bench/tests). */
 int64_t ttg_kernel_launches(void);
 ttg_status ttg_synchronize(void);
+/* Grow this device's stream-ordered memory pool to hold at least `bytes` (allocate and
+ * free once; the pool keeps freed memory), so later calls do not pay for pool growth. */
+ttg_status ttg_reserve(int64_t bytes);
 /* The calling thread's CUDA stream (cudaStream_t), on which every kernel of this thread
  * is launched; lets a harness record events on the same stream. */
 void* ttg_stream(void);
@@ -141,6 +144,30 @@ ttg_status ttg_result_reconstruct(const ttg_result* res, double* out, int out_on
  * with deterministic fixed-order reductions. */
 ttg_status ttg_completion_reset(double* y, const double* observed, const double* mask,
                                 const double* truth, int64_t n, double stats[5]);
+
+/* ---- multi-GPU: column-sharded sweeps (no reference analogue) --------
+ * One process (or host thread) per GPU. A communicator is an NCCL communicator over the
+ * ranks (NVLink / NVSwitch inside a B200 box), or a loopback group whose endpoints are
+ * host threads of one process sharing one GPU (tests). The reference is single-process;
+ * these entry points extend ttg_decompose and return the same ttg_result, with the cores
+ * replicated on every rank. */
+typedef struct ttg_comm ttg_comm; /* opaque */
+/* 128-byte NCCL unique id: create on one rank, hand to every rank (any side channel). */
+ttg_status ttg_comm_nccl_unique_id(unsigned char id[128]);
+ttg_status ttg_comm_nccl_create(const unsigned char id[128], int nranks, int rank, ttg_comm** out);
+/* nranks endpoints in `out[0..nranks-1]`; endpoint g must be driven by its own host thread. */
+ttg_status ttg_comm_loopback_create(int nranks, ttg_comm** out);
+void ttg_comm_free(ttg_comm* comm);
+/* The block of the first unfolding a rank owns: out = {lo, hi, rows, cols}. ULV (l2r):
+ * columns [lo, hi) of c = A(i1; i2..id), a contiguous slice of A, rows x cols = I1 x (hi-lo).
+ * URV (r2l): rows [lo, hi) of c = A(i1..i(d-1); id), a (hi-lo) x Id column-major block. */
+ttg_status ttg_shard_range(const int64_t* dims, int d, int method, int nranks, int rank, int64_t out[4]);
+/* ttg_decompose over the ranks of `comm`: a_local is this rank's block (ttg_shard_range).
+ * Pass 1 of the first cut runs column-sharded (one all-gather of a pivot record per step),
+ * its pass 2 reduces the ranks' TSQR triangles, and the carry is all-gathered once; the
+ * remaining cuts run replicated. ULV-L2R and URV-R2L with refine_passes = 1. */
+ttg_status ttg_decompose_sharded(const double* a_local, const int64_t* dims, int d, const ttg_config* cfg,
+                                 int a_on_device, ttg_comm* comm, ttg_result** out);
 
 /* ---- factor level (host buffers, column-major) ------------------------------ */
 /* q: m x p, r: p x n, perm: n. Any of the outputs may be NULL. */

@@ -68,6 +68,7 @@ SIGNATURES = {
     "ttg_set_device": (C.c_int, [C.c_int]),
     "ttg_kernel_launches": (C.c_int64, []),
     "ttg_synchronize": (C.c_int, []),
+    "ttg_reserve": (C.c_int, [C.c_int64]),
     "ttg_stream": (C.c_void_p, []),
     "ttg_profile_enable": (C.c_int, [C.c_int]),
     "ttg_profile_read": (C.c_int64, [c_double_p, c_double_p]),
@@ -86,6 +87,13 @@ SIGNATURES = {
     "ttg_result_rse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, c_double_p]),
     "ttg_result_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "ttg_completion_reset": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, c_double_p]),
+    "ttg_comm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+    "ttg_comm_nccl_create": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_comm_loopback_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_comm_free": (None, [C.c_void_p]),
+    "ttg_shard_range": (C.c_int, [c_int64_p, C.c_int, C.c_int, C.c_int, C.c_int, c_int64_p]),
+    "ttg_decompose_sharded": (C.c_int, [C.c_void_p, c_int64_p, C.c_int, C.POINTER(Config), C.c_int, C.c_void_p,
+                                        C.POINTER(C.c_void_p)]),
     "ttg_qr_col_pivot": (C.c_int, [c_double_p, C.c_int64, C.c_int64, c_double_p, c_double_p, c_int64_p]),
     "ttg_utv": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]),
     "ttg_svd": (C.c_int, [c_double_p, C.c_int64, C.c_int64, C.c_int, C.c_double, c_double_p, c_double_p,

@@ -123,13 +123,9 @@ class DeviceResult:
         return out.value
 
 
-def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, weights=(), refine_passes=1,
-                     retain="l11_only", debug_checks=False, qlp="early_exit", a_is_device_ptr=False) -> DeviceResult:
-    """decompose() (tt_decomp.hpp:100) returning the device-resident result handle.
-
-    With ``a_is_device_ptr`` the tensor is read in place from device memory (an integer
-    pointer, e.g. ``torch_tensor.data_ptr()``); otherwise it is copied from the host."""
-    require_gpu()
+def _config(method, sweep, ranks, eps, weights, refine_passes, retain, debug_checks, qlp):
+    """ttg_config for DecompConfig + FixedRank/FixedTol (tt_decomp.hpp:24-45); the second
+    value keeps the arrays it points into alive."""
     cfg = Config()
     cfg.method = METHODS[method]
     cfg.sweep = SWEEPS[sweep]
@@ -151,6 +147,17 @@ def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, w
     cfg.retain = RETAIN[retain]
     cfg.debug_checks = int(bool(debug_checks))
     cfg.qlp_policy = QLP[qlp]
+    return cfg, keep
+
+
+def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, weights=(), refine_passes=1,
+                     retain="l11_only", debug_checks=False, qlp="early_exit", a_is_device_ptr=False) -> DeviceResult:
+    """decompose() (tt_decomp.hpp:100) returning the device-resident result handle.
+
+    With ``a_is_device_ptr`` the tensor is read in place from device memory (an integer
+    pointer, e.g. ``torch_tensor.data_ptr()``); otherwise it is copied from the host."""
+    require_gpu()
+    cfg, keep = _config(method, sweep, ranks, eps, weights, refine_passes, retain, debug_checks, qlp)
     dims = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
     h = C.c_void_p()
     if a_is_device_ptr or isinstance(a, int):
@@ -162,6 +169,86 @@ def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, w
         flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
         check(lib().ttg_decompose(flat.ctypes.data_as(C.c_void_p), _iptr(dims), int(dims.size), C.byref(cfg), 0,
                                   C.byref(h)))
+    del keep
+    return DeviceResult(h)
+
+
+# ---- multi-GPU (column-sharded first cut) ---------------------------------
+
+class Comm:
+    """Owning handle of a ttg_comm endpoint."""
+
+    def __init__(self, handle: C.c_void_p, rank: int, size: int):
+        self.h, self.rank, self.size = handle, rank, size
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().ttg_comm_free(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    check(lib().ttg_comm_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm(uid: bytes, size: int, rank: int) -> Comm:
+    """NCCL communicator over `size` ranks (one process per GPU); `uid` from rank 0's
+    nccl_unique_id(), passed to every rank over any side channel (torch.distributed)."""
+    require_gpu()
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    h = C.c_void_p()
+    check(lib().ttg_comm_nccl_create(buf, int(size), int(rank), C.byref(h)))
+    return Comm(h, rank, size)
+
+
+def loopback_group(size: int) -> list:
+    """`size` endpoints sharing this process's GPU; drive each from its own thread."""
+    require_gpu()
+    hs = (C.c_void_p * size)()
+    check(lib().ttg_comm_loopback_create(int(size), hs))
+    return [Comm(C.c_void_p(hs[r]), r, size) for r in range(size)]
+
+
+def shard_range(dims, method: str, size: int, rank: int):
+    """(lo, hi, rows, cols): the block of the first unfolding owned by `rank`."""
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    out = np.zeros(4, np.int64)
+    check(lib().ttg_shard_range(_iptr(d), int(d.size), METHODS[method], int(size), int(rank), _iptr(out)))
+    return tuple(int(x) for x in out)
+
+
+def shard_block(a, dims, method: str, size: int, rank: int) -> np.ndarray:
+    """This rank's block (column-major flat) of a full tensor `a` (host array)."""
+    lo, hi, rows, cols = shard_range(dims, method, size, rank)
+    flat = np.asarray(a, dtype=np.float64).reshape(-1, order="F")
+    if method == "ulv":
+        return np.ascontiguousarray(flat[rows * lo:rows * hi])
+    m = flat.size // cols
+    c = flat.reshape((m, cols), order="F")
+    return np.ascontiguousarray(c[lo:hi, :].reshape(-1, order="F"))
+
+
+def decompose_sharded(a_local, dims, comm: Comm, method="urv", sweep="r2l", ranks=None, eps=None, weights=(),
+                      qlp="early_exit", a_is_device_ptr=False) -> DeviceResult:
+    """Sharded decompose over the ranks of `comm`: `a_local` is this rank's block
+    (shard_range / shard_block); every rank gets the whole train."""
+    require_gpu()
+    cfg, keep = _config(method, sweep, ranks, eps, weights, 1, "l11_only", False, qlp)
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    h = C.c_void_p()
+    if a_is_device_ptr or isinstance(a_local, int):
+        src, on_dev = C.c_void_p(int(a_local)), int(bool(a_is_device_ptr))
+    else:
+        flat = np.ascontiguousarray(np.asarray(a_local, dtype=np.float64).reshape(-1))
+        keep.append(flat)
+        src, on_dev = flat.ctypes.data_as(C.c_void_p), 0
+    check(lib().ttg_decompose_sharded(src, _iptr(d), int(d.size), C.byref(cfg), on_dev, comm.h, C.byref(h)))
+    del keep
     return DeviceResult(h)
 
 

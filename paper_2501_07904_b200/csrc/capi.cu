@@ -13,6 +13,10 @@ struct ttg_result {
     ttg::TTResult r;
 };
 
+struct ttg_comm {
+    std::unique_ptr<ttg::Comm> c;
+};
+
 namespace {
 
 thread_local std::string t_msg;
@@ -45,6 +49,22 @@ int64_t count_of(const int64_t* dims, int d) {
         n *= dims[i];
     }
     return n;
+}
+
+ttg::SweepConfig sweep_config(const ttg_config* cfg) {
+    ttg::SweepConfig sc;
+    sc.method = cfg->method;
+    sc.sweep = cfg->sweep;
+    if (sc.method < 0 || sc.method > 2) ttg::argument_error("unknown method");
+    sc.fixed_rank = cfg->fixed_rank != 0;
+    if (sc.fixed_rank && cfg->ranks && cfg->nranks > 0) sc.ranks.assign(cfg->ranks, cfg->ranks + cfg->nranks);
+    sc.eps = cfg->eps;
+    if (cfg->nweights > 0 && cfg->weights) sc.weights.assign(cfg->weights, cfg->weights + cfg->nweights);
+    sc.refine = cfg->refine_passes;
+    sc.retain = cfg->retain;
+    sc.debug = cfg->debug_checks != 0;
+    sc.policy = cfg->qlp_policy;
+    return sc;
 }
 
 // Device view of a possibly-host buffer.
@@ -93,6 +113,17 @@ void* ttg_stream(void) {
     }
 }
 
+ttg_status ttg_reserve(int64_t bytes) {
+    return guard([&] {
+        if (bytes < 0) ttg::argument_error("negative reservation");
+        if (bytes == 0) return;
+        void* p = nullptr;
+        TTG_CUDA(cudaMallocAsync(&p, (size_t)bytes, ttg::stream()));
+        TTG_CUDA(cudaFreeAsync(p, ttg::stream()));
+        TTG_CUDA(cudaStreamSynchronize(ttg::stream()));
+    });
+}
+
 ttg_status ttg_profile_enable(int on) {
     return guard([&] { ttg::prof_enable(on != 0); });
 }
@@ -114,18 +145,7 @@ ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_
         const auto start = std::chrono::steady_clock::now();
         std::vector<int64_t> dv(dims, dims + d);
         const int64_t n = count_of(dims, d);
-        ttg::SweepConfig sc;
-        sc.method = cfg->method;
-        sc.sweep = cfg->sweep;
-        if (sc.method < 0 || sc.method > 2) ttg::argument_error("unknown method");
-        sc.fixed_rank = cfg->fixed_rank != 0;
-        if (sc.fixed_rank && cfg->ranks && cfg->nranks > 0) sc.ranks.assign(cfg->ranks, cfg->ranks + cfg->nranks);
-        sc.eps = cfg->eps;
-        if (cfg->nweights > 0 && cfg->weights) sc.weights.assign(cfg->weights, cfg->weights + cfg->nweights);
-        sc.refine = cfg->refine_passes;
-        sc.retain = cfg->retain;
-        sc.debug = cfg->debug_checks != 0;
-        sc.policy = cfg->qlp_policy;
+        const ttg::SweepConfig sc = sweep_config(cfg);
         DeviceInput in(a, n, a_on_device != 0);
         auto* res = new ttg_result{ttg::decompose(in.ptr, dv, sc)};
         res->r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
@@ -134,6 +154,55 @@ ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_
 }
 
 void ttg_result_free(ttg_result* res) { delete res; }
+
+ttg_status ttg_comm_nccl_unique_id(unsigned char id[128]) {
+    return guard([&] { ttg::nccl_unique_id(id); });
+}
+
+ttg_status ttg_comm_nccl_create(const unsigned char id[128], int nranks, int rank, ttg_comm** out) {
+    *out = nullptr;
+    return guard([&] { *out = new ttg_comm{ttg::make_nccl_comm(id, nranks, rank)}; });
+}
+
+ttg_status ttg_comm_loopback_create(int nranks, ttg_comm** out) {
+    return guard([&] {
+        auto group = ttg::make_loopback_group(nranks);
+        for (int r = 0; r < nranks; ++r) out[r] = new ttg_comm{std::move(group[(size_t)r])};
+    });
+}
+
+void ttg_comm_free(ttg_comm* comm) { delete comm; }
+
+ttg_status ttg_shard_range(const int64_t* dims, int d, int method, int nranks, int rank, int64_t out[4]) {
+    return guard([&] {
+        if (d < 0) ttg::argument_error("negative order");
+        count_of(dims, d);
+        const ttg::ShardRange r = ttg::shard_range(std::vector<int64_t>(dims, dims + d), method, nranks, rank);
+        out[0] = r.lo;
+        out[1] = r.hi;
+        out[2] = r.rows;
+        out[3] = r.cols;
+    });
+}
+
+ttg_status ttg_decompose_sharded(const double* a_local, const int64_t* dims, int d, const ttg_config* cfg,
+                                 int a_on_device, ttg_comm* comm, ttg_result** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (!cfg) ttg::argument_error("null config");
+        if (!comm || !comm->c) ttg::argument_error("null communicator");
+        if (d < 0) ttg::argument_error("negative order");
+        const auto start = std::chrono::steady_clock::now();
+        std::vector<int64_t> dv(dims, dims + d);
+        count_of(dims, d);
+        const ttg::SweepConfig sc = sweep_config(cfg);
+        const ttg::ShardRange sr = ttg::shard_range(dv, sc.method, comm->c->size(), comm->c->rank());
+        DeviceInput in(a_local, sr.rows * sr.cols, a_on_device != 0);
+        auto* res = new ttg_result{ttg::decompose_sharded(in.ptr, dv, sc, *comm->c)};
+        res->r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+        *out = res;
+    });
+}
 
 int ttg_result_order(const ttg_result* res) { return (int)res->r.cores.size(); }
 

@@ -19,6 +19,8 @@ struct Failure : std::runtime_error {
 
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Failure(code, msg); }
 inline void argument_error(const std::string& msg) { fail(1, msg); }
+[[noreturn]] inline void resource_error(const std::string& msg) { fail(5, msg); }
+[[noreturn]] inline void invariant_error(const std::string& msg) { fail(6, msg); }
 
 #define TTG_CUDA(expr)                                                                   \
     do {                                                                                 \
@@ -56,6 +58,10 @@ inline void allow_smem(K* kernel, size_t bytes) {
 // Stream of the calling host thread (created lazily on the current device).
 cudaStream_t stream();
 int sm_count();
+// Make sure this device's stream-ordered pool holds at least `bytes` (capped at half the
+// free memory): growing the pool maps new memory at ~10-40 ms per GB, and a pool grown
+// piecemeal by differently sized requests keeps growing; one up-front block does not.
+void ensure_pool(size_t bytes);
 
 // Optional event timing of the dominant (pass-1 streaming) kernel for the roofline report:
 // when enabled, prof_begin/prof_end bracket each launch with CUDA events on the launching

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -15,6 +16,35 @@ namespace ttg {
 enum class Layout { Col = 0, Row = 1 };
 
 // ---------------------------------------------------------------------------
+// Multi-GPU plumbing (comm.cu). One rank per GPU; every exchange on the data path is an
+// all-gather of a small device buffer, ordered on the calling thread's stream, followed
+// by a fixed-order combine, so every rank derives bitwise identical decisions.
+// ---------------------------------------------------------------------------
+class Comm {
+public:
+    virtual ~Comm() = default;
+    virtual int rank() const = 0;
+    virtual int size() const = 0;
+    // recv (device, size() * bytes) <- every rank's send (device, bytes), in rank order.
+    virtual void allgather(const void* send, void* recv, size_t bytes) = 0;
+};
+// Sum of one double per rank, combined in rank order (host result, identical everywhere).
+double global_sum(Comm& comm, double local);
+std::unique_ptr<Comm> make_nccl_comm(const unsigned char id[128], int nranks, int rank);
+void nccl_unique_id(unsigned char id[128]);
+// In-process group of `nranks` endpoints for one GPU, one host thread per endpoint (tests):
+// the exchange is a host barrier around device copies, no kernel ever waits on another.
+std::vector<std::unique_ptr<Comm>> make_loopback_group(int nranks);
+
+// Column sharding of pass 1: this engine holds columns [col_off, col_off + N) of a
+// k x N_global matrix whose other columns live on the other ranks of `comm`.
+struct ShardSpec {
+    Comm* comm = nullptr;
+    int64_t col_off = 0;
+    int64_t N_global = 0;
+};
+
+// ---------------------------------------------------------------------------
 // Pass 1: greedy column-pivoted Householder QR of a k x N matrix W. W is never written.
 // The orthogonal factor Q_t = H_0...H_{t-1} is kept in compact WY form
 // Q_t = I - Y_t T_t Y_t^T (Y: k x t reflectors, T: t x t upper), so one step costs
@@ -22,15 +52,24 @@ enum class Layout { Col = 0, Row = 1 };
 // column, with the norm downdate of factor.cpp:98-107. Any prefix of steps equals the
 // prefix of the reference's qr_col_pivot (factor.cpp:62-135) in exact arithmetic: same
 // pivots (same tie rule), same R rows, and Q[:, :s] = its first s economy-Q columns.
+//
+// Sharded (ShardSpec): positions are global; every step each rank exports its best local
+// candidate with its column, the records are all-gathered, and every rank picks the same
+// winner (norm desc, global position asc) and builds the same reflector from the winner's
+// column, then streams its own columns. Q and the reflectors are replicated; R rows and
+// norms stay local.
 // ---------------------------------------------------------------------------
 class WideQrcp {
 public:
-    WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps);
+    WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps,
+             const ShardSpec* shard = nullptr);
     void run_to(int64_t steps);  // advance the greedy factorisation to `steps` (<= p)
     int64_t steps() const { return steps_; }
     int64_t p() const { return p_; }
     int64_t k() const { return k_; }
-    int64_t N() const { return N_; }
+    int64_t N() const { return N_; }  // local columns
+    bool sharded() const { return comm_ != nullptr; }
+    Comm* comm() const { return comm_; }
     // Trailing mass sum_j nu_j of the not-yet-pivoted columns from the downdated norms
     // (host sync). Below ~1e-16 of a column's norm the downdates are rounding noise.
     double trailing_mass();
@@ -41,8 +80,8 @@ public:
 
     const double* Q() const { return Qt_.get(); }      // k x cap, columns 0..steps-1 = economy Q
     const double* R() const { return R_.get(); }       // rows 0..steps-1, row t at R + t*N
-    const int64_t* perm() const { return perm_.get(); } // position -> column
-    const int64_t* piv() const { return piv_.get(); }   // step -> column
+    const int64_t* perm() const { return perm_.get(); } // position -> column (global when sharded)
+    const int64_t* piv() const { return piv_.get(); }   // step -> local column (-1: other rank)
     const double* diag() const { return diag_.get(); }  // R(t,t)
     int64_t R_stride() const { return N_; }
 
@@ -57,8 +96,11 @@ private:
     Layout layout_;
     int64_t steps_ = 0, cap_ = 0;
     int ncand_ = 0, mode_ = 0, nchunk_ = 1, ksplit_ = 1;
+    Comm* comm_ = nullptr;
+    int64_t off_ = 0, Ng_ = 0;
     DevBuf<double> nu_, cref_, R_, diag_, beta_, mass_;
     DevBuf<double> Y_, T_, Qt_, wv_, yv_, part_, vecs_, kpart_;  // WY state and scratch
+    DevBuf<double> rec_, recs_;  // sharded: this rank's pivot record, all ranks' records
     DevBuf<int64_t> pos_, perm_, piv_, flags_;
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;

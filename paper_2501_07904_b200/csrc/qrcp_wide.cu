@@ -183,7 +183,16 @@ struct WY {
     int ncand;
     int nchunk;
     int64_t rows;  // rows per chunk
+    // sharded pass 1: all ranks' pivot records (stride k + 4), this rank's column range
+    const double* recs;
+    int nrec;
+    int64_t off, nloc;
 };
+
+// Sharded pivot record: [0] kind (0 none, 1 candidate, 2 the column at position t when no
+// rank has a comparable candidate), [1] norm^2, [2] global position, [3] global column,
+// [4..4+k) the column itself.
+constexpr int kRecHead = 4;
 
 // pick: pivot of step t (redundant per CTA), bookkeeping (CTA `chunk0` thread 0), stage
 // w for this chunk's rows and the chunk's partial z = Y[:, :t]^T w.
@@ -218,6 +227,96 @@ __device__ void wy_pick(const WY& s, int64_t t, int chunk, bool bookkeep) {
         for (int64_t i = max(r0, l) + lane; i < r1; i += 32) a = fma(y[i], s.wv[i], a);
         a = warp_sum(a);
         if (lane == 0) s.part[(int64_t)chunk * (s.cap + 1) + l] = a;
+    }
+}
+
+// Sharded pick: the winner among the all-gathered records (same rule as the single-GPU
+// candidate scan: norm desc, global position asc), bookkeeping on the replicated global
+// perm and on this rank's positions, and the winner's column staged from its record.
+__device__ void wy_pick_shard(const WY& s, int64_t t, int chunk, bool bookkeep) {
+    __shared__ int win;
+    if (threadIdx.x == 0) {
+        const int64_t stride = s.k + kRecHead;
+        Cand best = cand_none();
+        int w = -1, fallback = -1;
+        for (int g = 0; g < s.nrec; ++g) {
+            const double* r = s.recs + g * stride;
+            if (r[0] == 1.0) {
+                const Cand c{r[1], (int64_t)r[2], (int64_t)r[3]};
+                if (w < 0 || better(c, best)) { best = c; w = g; }
+            } else if (r[0] == 2.0) {
+                fallback = g;
+            }
+        }
+        win = w >= 0 ? w : fallback;
+    }
+    __syncthreads();
+    const double* rec = s.recs + (int64_t)max(win, 0) * (s.k + kRecHead);
+    if (bookkeep && threadIdx.x == 0) {
+        const int64_t gcol = (int64_t)rec[3], gpos = (int64_t)rec[2];
+        const int64_t ct = s.perm[t];
+        s.perm[t] = gcol;
+        s.perm[gpos] = ct;
+        if (gcol >= s.off && gcol < s.off + s.nloc) s.pos[gcol - s.off] = t;
+        if (ct != gcol && ct >= s.off && ct < s.off + s.nloc) s.pos[ct - s.off] = gpos;
+        s.piv[t] = (gcol >= s.off && gcol < s.off + s.nloc) ? gcol - s.off : -1;
+        *s.nflag = 0;
+    }
+    const int64_t r0 = (int64_t)chunk * s.rows, r1 = min(s.k, r0 + s.rows);
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) s.wv[i] = rec[kRecHead + i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t l = warp; l < t; l += kThreads / 32) {
+        const double* y = s.Y + l * s.k;
+        double a = 0.0;
+        for (int64_t i = max(r0, l) + lane; i < r1; i += 32) a = fma(y[i], s.wv[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s.part[(int64_t)chunk * (s.cap + 1) + l] = a;
+    }
+}
+
+// Sharded export of this rank's pivot record for step t.
+__global__ void __launch_bounds__(kThreads) k_shard_export(WY s, int64_t t, double* rec) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ int64_t jl_s;
+    __shared__ int kind_s;
+    Cand best = cand_none();
+    for (int i = threadIdx.x; i < s.ncand; i += kThreads)
+        if (better(s.cand[i], best)) best = s.cand[i];
+    best = block_best(best, sc);
+    if (threadIdx.x == 0) {
+        int kind = 0;
+        int64_t jl = -1, gpos = t;
+        if (best.col >= 0) {
+            kind = 1;
+            jl = best.col;
+            gpos = best.pos;
+        } else {
+            const int64_t ct = s.perm[t];
+            if (ct >= s.off && ct < s.off + s.nloc) { kind = 2; jl = ct - s.off; }
+        }
+        rec[0] = (double)kind;
+        rec[1] = kind == 1 ? best.nu : 0.0;
+        rec[2] = (double)gpos;
+        rec[3] = (double)(jl >= 0 ? jl + s.off : -1);
+        jl_s = jl;
+        kind_s = kind;
+    }
+    __syncthreads();
+    const int64_t jl = jl_s;
+    for (int64_t i = threadIdx.x; i < s.k; i += kThreads)
+        rec[kRecHead + i] = kind_s ? ld_w(s.W, s.ld, s.layout, i, jl) : 0.0;
+}
+
+// Sharded init fix-up: global positions for the local columns (and their candidates), the
+// replicated identity permutation over all N_global columns.
+__global__ void k_shard_init(int64_t off, int64_t nloc, int64_t Ng, int64_t* pos, int64_t* perm, Cand* cand,
+                             int ncand) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < Ng; j += stride) {
+        perm[j] = j;
+        if (j < nloc) pos[j] = j + off;
+        if (j < ncand && cand[j].col >= 0) cand[j].pos += off;
     }
 }
 
@@ -336,9 +435,11 @@ __device__ void wy_q(const WY& s, int64_t t, int chunk) {
 }
 
 // Whole step in one CTA (nchunk == 1).
+template <bool SH>
 __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
     __shared__ double red[kThreads / 32];
-    wy_pick(s, t, 0, true);
+    if (SH) wy_pick_shard(s, t, 0, true);
+    else wy_pick(s, t, 0, true);
     __syncthreads();
     wy_sum_parts(s, t, s.vec, threadIdx.x, kThreads);
     __syncthreads();
@@ -359,6 +460,9 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
 
 // Multi-CTA phases (row chunks) and the small single-CTA glue between them.
 __global__ void __launch_bounds__(kThreads) k_wy_pick(WY s, int64_t t) { wy_pick(s, t, blockIdx.x, blockIdx.x == 0); }
+__global__ void __launch_bounds__(kThreads) k_wy_pick_shard(WY s, int64_t t) {
+    wy_pick_shard(s, t, blockIdx.x, blockIdx.x == 0);
+}
 
 __global__ void __launch_bounds__(1024) k_wy_zu(WY s, int64_t t) {
     wy_sum_parts(s, t, s.vec, threadIdx.x, blockDim.x);
@@ -665,9 +769,18 @@ __global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__
 
 }  // namespace
 
-WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps)
+WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps,
+                   const ShardSpec* shard)
     : W_(W), k_(k), N_(N), ld_(ld), p_(std::min(k, N)), layout_(layout) {
     if (k <= 0 || N <= 0) argument_error("qr_col_pivot: empty matrix");
+    Ng_ = N;
+    if (shard && shard->comm) {
+        comm_ = shard->comm;
+        off_ = shard->col_off;
+        Ng_ = shard->N_global;
+        p_ = std::min(k, Ng_);
+        if (off_ < 0 || off_ + N > Ng_) argument_error("shard column range outside the matrix");
+    }
     const int sms = sm_count();
     if (layout == Layout::Col) {
         mode_ = (k >= 64 || ld != k) ? 1 : 2;
@@ -683,7 +796,11 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
-    nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(N); flags_.alloc(N);
+    nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(Ng_); flags_.alloc(N);
+    if (comm_) {
+        rec_.alloc((size_t)(k + kRecHead));
+        recs_.alloc((size_t)comm_->size() * (k + kRecHead));
+    }
     cand_.alloc(ncand_); mass_.alloc(ncand_); nflag_.alloc(1); nflag_.zero();
     wv_.alloc(k); yv_.alloc(k);
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
@@ -694,13 +811,16 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, nullptr, 1, cdiv(k, ksplit_), kpart_.get());
         TTG_LAUNCH(k_init_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, nu_.get(), cref_.get(),
                    pos_.get(), perm_.get(), cand_.get(), mass_.get());
-        return;
+    } else {
+        const size_t smem = mode_ == 2 ? sizeof(double) * k * (kThreads + 1) : 0;
+        auto init = (mode_ == 0 || mode_ == 3) ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
+        allow_smem(init, smem);
+        TTG_LAUNCH(init, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
+                   perm_.get(), cand_.get(), mass_.get());
     }
-    const size_t smem = mode_ == 2 ? sizeof(double) * k * (kThreads + 1) : 0;
-    auto init = (mode_ == 0 || mode_ == 3) ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
-    allow_smem(init, smem);
-    TTG_LAUNCH(init, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
-               perm_.get(), cand_.get(), mass_.get());
+    if (comm_)
+        TTG_LAUNCH(k_shard_init, (int)std::min<int64_t>(cdiv(Ng_, 256), 8 * sms), 256, 0, stream(), off_, N_, Ng_,
+                   pos_.get(), perm_.get(), cand_.get(), ncand_);
 }
 
 void WideQrcp::grow(int64_t cap) {
@@ -726,7 +846,7 @@ double WideQrcp::trailing_mass() {
     std::vector<double> h = mass_.to_host(ncand_);
     double s = 0.0;
     for (double v : h) s += v;
-    return s;
+    return comm_ ? global_sum(*comm_, s) : s;
 }
 
 double WideQrcp::refresh_exact() {
@@ -765,16 +885,22 @@ void WideQrcp::step() {
 void WideQrcp::reflect_step(int64_t t) {
     WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
          vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
-         ncand_, 1, k_};
+         ncand_, 1, k_, recs_.get(), comm_ ? comm_->size() : 0, off_, N_};
+    if (comm_) {  // exchange the ranks' pivot records before the (replicated) reflector
+        TTG_LAUNCH(k_shard_export, 1, kThreads, 0, stream(), s, t, rec_.get());
+        comm_->allgather(rec_.get(), recs_.get(), sizeof(double) * (size_t)(k_ + kRecHead));
+    }
     // one fused CTA while the O(k t) work is small, row chunks otherwise
     const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(nchunk_, cdiv(k_ * (t + 1), 32768)));
     if (nch == 1) {
-        TTG_LAUNCH(k_wy_fused, 1, kThreads, 0, stream(), s, t);
+        if (comm_) TTG_LAUNCH(k_wy_fused<true>, 1, kThreads, 0, stream(), s, t);
+        else TTG_LAUNCH(k_wy_fused<false>, 1, kThreads, 0, stream(), s, t);
         return;
     }
     s.nchunk = nch;
     s.rows = cdiv(k_, nch);
-    TTG_LAUNCH(k_wy_pick, nch, kThreads, 0, stream(), s, t);
+    if (comm_) TTG_LAUNCH(k_wy_pick_shard, nch, kThreads, 0, stream(), s, t);
+    else TTG_LAUNCH(k_wy_pick, nch, kThreads, 0, stream(), s, t);
     TTG_LAUNCH(k_wy_zu, 1, 1024, 0, stream(), s, t);
     TTG_LAUNCH(k_wy_y, nch, kThreads, 0, stream(), s, t);
     TTG_LAUNCH(k_wy_reflect, nch, kThreads, 0, stream(), s, t);

@@ -1,4 +1,5 @@
 // Per-thread CUDA stream, device properties and the launch counter.
+#include <mutex>
 #include <atomic>
 #include <cstdlib>
 
@@ -109,6 +110,26 @@ int64_t prof_read(double* total_ms, double* bytes) {
     *bytes = t_prof.bytes;
     t_prof.bytes = 0.0;
     return n;
+}
+
+void ensure_pool(size_t bytes) {
+    static std::mutex mu;
+    static size_t reserved[64] = {};
+    int dev = 0;
+    TTG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64 || bytes <= reserved[dev]) return;
+    size_t free_b = 0, total_b = 0;
+    TTG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t want = std::min(bytes, free_b / 2);
+    if (want <= reserved[dev]) return;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, want, stream()) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    TTG_CUDA(cudaFreeAsync(p, stream()));
+    reserved[dev] = want;
 }
 
 int sm_count() {

@@ -183,11 +183,31 @@ struct Pass1 {
     virtual const double* R() = 0;       // R1 rows 0..s-1 by original column, row t at R + t*N
     virtual const int64_t* perm() = 0;   // positions -> columns
     virtual const double* Q() = 0;       // economy Q columns 0..s-1, leading dimension k
+    virtual bool sharded() const { return false; }
+    // R_B (s x s, ld s) of B = R1[:s, :]^T over all columns (all ranks when sharded).
+    virtual void r_factor(int64_t s, double* RB) { tsqr_r(R(), N(), s, N(), RB); }
 };
 
 struct WidePass1 final : Pass1 {
     WideQrcp e;
-    WidePass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap) : e(W, k, N, ld, l, cap) {}
+    WidePass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap,
+              const ShardSpec* shard = nullptr)
+        : e(W, k, N, ld, l, cap, shard) {}
+    bool sharded() const override { return e.sharded(); }
+    // Sharded: every rank reduces its own rows of B to a triangle, the triangles are
+    // all-gathered and stacked in rank order, and every rank factors the same stack.
+    void r_factor(int64_t s, double* RB) override {
+        if (!e.sharded()) return tsqr_r(e.R(), e.N(), s, e.N(), RB);
+        Comm& comm = *e.comm();
+        const int G = comm.size();
+        DevBuf<double> mine((size_t)(s * s)), all((size_t)(G * s * s)), stack((size_t)(G * s * s));
+        tsqr_r(e.R(), e.N(), s, e.N(), mine.get());
+        comm.allgather(mine.get(), all.get(), sizeof(double) * (size_t)(s * s));
+        for (int g = 0; g < G; ++g)
+            TTG_CUDA(cudaMemcpy2DAsync(stack.get() + (int64_t)g * s, sizeof(double) * G * s, all.get() + (int64_t)g * s * s,
+                                       sizeof(double) * s, sizeof(double) * s, s, cudaMemcpyDeviceToDevice, stream()));
+        tsqr_r(stack.get(), G * s, s, G * s, RB);
+    }
     int64_t p() const override { return e.p(); }
     int64_t N() const override { return e.N(); }
     int64_t k() const override { return e.k(); }
@@ -265,9 +285,11 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
     if (tsqr_fits(s) && small_qrcp_fits(s, s)) {
         // QRCP(R_B) with B = R1[:s,:]^T = Q_B R_B: same pivots and |R| as QRCP(B).
         DevBuf<double> RB((size_t)s * s);
-        tsqr_r(e1.R(), N, s, N, RB.get());
+        e1.r_factor(s, RB.get());
         small_qrcp(RB.get(), s, s, s, out.perm.get(), R2.get(), pn.get(), nullptr);
     } else {
+        if (e1.sharded())
+            invariant_error("sharded pass 2 supports at most " + std::to_string(160) + " pass-1 steps per cut");
         DevBuf<double> B((size_t)N * s);
         TTG_LAUNCH(k_gather_b, (int)cdiv(N * s, 256), 256, 0, stream(), e1.R(), e1.perm(), N, s, B.get());
         TallQrcp e2(B.get(), N, s, N);
@@ -615,6 +637,100 @@ void general_sweep(const double* a, const std::vector<int64_t>& dims, const Swee
     }
 }
 
+// ---- fast sweeps (refine_passes = 1), resumable at any cut ------------------------------
+
+CutRequest make_request(TTResult& res, const Resolved& mode, const SweepConfig& cfg, int64_t cut, int64_t p) {
+    CutRequest rq{mode.fixed, 0, 0.0, cfg.policy};
+    if (mode.fixed) {
+        const int64_t req = mode.ranks[(size_t)cut];
+        rq.rank = std::min(req, p);
+        if (rq.rank < req)
+            res.warnings.push_back("cut " + std::to_string(cut) + ": requested rank " + std::to_string(req) +
+                                   " clamped to " + std::to_string(rq.rank));
+    } else {
+        rq.budget = mode.budgets[(size_t)(cut - 1)];
+    }
+    return rq;
+}
+
+void print_cut(const char* what, int64_t cut, int64_t m, int64_t n, const CutOut& co, Clock::time_point t0) {
+    if (!cut_timing()) return;
+    sync();
+    std::fprintf(stderr, "[ttg] %s cut %lld (%lld x %lld): %lld steps, %.3f ms\n", what, (long long)cut, (long long)m,
+                 (long long)n, (long long)co.steps, std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+}
+
+// TT-ULV left to right (tt_decomp.cpp:156-211) from cut k0 (1-based), c the m x n unfolding.
+void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, int64_t r_prev,
+              const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
+    const int64_t d = (int64_t)dims.size();
+    DevBuf<double> carry;  // current working matrix when not the input itself
+    for (int64_t k = k0; k <= d - 1; ++k) {
+        const int64_t p = std::min(m, n);
+        const CutRequest rq = make_request(res, mode, cfg, k, p);
+        const auto tc0 = Clock::now();
+        auto e1 = make_pass1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
+        CutOut co = run_cut(*e1, rq);
+        print_cut("ulv", k, m, n, co, tc0);
+        const int64_t r = co.rank;
+        res.step_errors[(size_t)(k - 1)] = co.step_error;
+        res.ranks_chosen[(size_t)k] = r;
+        res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag};
+        DevBuf<double> core((size_t)(m * r));
+        TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1->Q(), m, co.sel.get(), r, false,
+                   core.get());
+        set_core(res, (size_t)(k - 1), std::move(core), r_prev, dims[(size_t)(k - 1)], r);
+        DevBuf<double> next((size_t)(r * n));
+        dim3 g((unsigned)cdiv(n, 32), (unsigned)cdiv(r, 32));
+        TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1->R(), n, co.sel.get(), r, next.get());
+        r_prev = r;
+        if (k < d - 1) {
+            carry = std::move(next);
+            c = carry.get();
+            m = r * dims[(size_t)k];
+            n = n / dims[(size_t)k];
+        } else {
+            set_core(res, (size_t)(d - 1), std::move(next), r, dims[(size_t)(d - 1)], 1);
+        }
+    }
+}
+
+// TT-URV right to left (tt_decomp.cpp:216-339) from cut index k0 (the core k0-1 is next),
+// c the M x n unfolding.
+void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, int64_t r_next,
+              const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
+    DevBuf<double> carry;
+    for (int64_t k = k0; k >= 2; --k) {
+        const int64_t p = std::min(M, n);
+        const CutRequest rq = make_request(res, mode, cfg, k - 1, p);
+        // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
+        const auto tc0 = Clock::now();
+        auto e1 = make_pass1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
+        CutOut co = run_cut(*e1, rq);
+        print_cut("urv", k - 1, M, n, co, tc0);
+        const int64_t r = co.rank;
+        res.step_errors[(size_t)(k - 2)] = co.step_error;
+        res.ranks_chosen[(size_t)(k - 1)] = r;
+        res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag};
+        DevBuf<double> core((size_t)(n * r));
+        TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1->Q(), n, co.sel.get(), r, true,
+                   core.get());
+        set_core(res, (size_t)(k - 1), std::move(core), r, dims[(size_t)(k - 1)], r_next);
+        DevBuf<double> next((size_t)(M * r));
+        dim3 g((unsigned)std::min<int64_t>(cdiv(M, 256), 4096), (unsigned)r);
+        TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1->R(), M, co.sel.get(), r, next.get());
+        r_next = r;
+        if (k > 2) {
+            carry = std::move(next);
+            c = carry.get();
+            n = dims[(size_t)(k - 2)] * r;
+            M = M / dims[(size_t)(k - 2)];
+        } else {
+            set_core(res, 0, std::move(next), 1, dims[0], r);
+        }
+    }
+}
+
 }  // namespace
 
 TTResult decompose(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg) {
@@ -625,6 +741,9 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
         if (dims[k] < 1)
             argument_error("shape dim " + std::to_string(k + 1) + " is " + std::to_string(dims[k]) + ", must be >= 1");
     const int64_t total_n = product(dims, 0, dims.size());
+    // working set: the R1 rows / carry / exact-refresh residual of the first cut are each
+    // at most about the input's size
+    ensure_pool((size_t)(2.5 * 8.0 * (double)total_n) + ((size_t)256 << 20));
     if (cfg.method == 2 && cfg.sweep == 0) {
         // left_orthogonal_via_urv (tt_decomp.cpp:408-427): sweep the index-reversed tensor
         // right to left with the reversed rank chain / weights, then reverse the train.
@@ -708,100 +827,139 @@ TTResult decompose(const double* a, const std::vector<int64_t>& dims, const Swee
         return res;
     }
 
-    DevBuf<double> carry;  // current working matrix when not the input itself
-    if (cfg.method == 1) {
-        // ---- TT-ULV left to right (tt_decomp.cpp:156-211) ----
-        const double* c = a;
-        int64_t m = dims[0], n = total_n / dims[0], r_prev = 1;
-        for (int64_t k = 1; k <= d - 1; ++k) {
-            const int64_t p = std::min(m, n);
-            CutRequest rq{mode.fixed, 0, 0.0, cfg.policy};
-            if (mode.fixed) {
-                const int64_t req = mode.ranks[(size_t)k];
-                rq.rank = std::min(req, p);
-                if (rq.rank < req)
-                    res.warnings.push_back("cut " + std::to_string(k) + ": requested rank " + std::to_string(req) +
-                                           " clamped to " + std::to_string(rq.rank));
-            } else {
-                rq.budget = mode.budgets[(size_t)(k - 1)];
-            }
-            const auto tc0 = Clock::now();
-            auto e1 = make_pass1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
-            CutOut co = run_cut(*e1, rq);
-            if (cut_timing()) {
-                sync();
-                std::fprintf(stderr, "[ttg] ulv cut %lld (%lld x %lld): %lld steps, %.3f ms\n", (long long)k,
-                             (long long)m, (long long)n, (long long)co.steps,
-                             std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
-            }
-            const int64_t r = co.rank;
-            res.step_errors[(size_t)(k - 1)] = co.step_error;
-            res.ranks_chosen[(size_t)k] = r;
-            res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag};
-            DevBuf<double> core((size_t)(m * r));
-            TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1->Q(), m, co.sel.get(), r, false,
-                       core.get());
-            set_core(res, (size_t)(k - 1), std::move(core), r_prev, dims[(size_t)(k - 1)], r);
-            DevBuf<double> next((size_t)(r * n));
-            dim3 g((unsigned)cdiv(n, 32), (unsigned)cdiv(r, 32));
-            TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1->R(), n, co.sel.get(), r, next.get());
-            r_prev = r;
-            if (k < d - 1) {
-                carry = std::move(next);
-                c = carry.get();
-                m = r * dims[(size_t)k];
-                n = n / dims[(size_t)k];
-            } else {
-                set_core(res, (size_t)(d - 1), std::move(next), r, dims[(size_t)(d - 1)], 1);
-            }
+    if (cfg.method == 1) ulv_cuts(res, a, dims[0], total_n / dims[0], 1, 1, dims, mode, cfg);
+    else urv_cuts(res, a, total_n / dims[(size_t)(d - 1)], dims[(size_t)(d - 1)], d, 1, dims, mode, cfg);
+    finish(res, rss, start);
+    return res;
+}
+
+}  // namespace ttg
+
+namespace ttg {
+
+ShardRange shard_range(const std::vector<int64_t>& dims, int method, int nranks, int rank) {
+    const int64_t d = (int64_t)dims.size();
+    if (d < 2) argument_error("sharded decomposition needs order >= 2");
+    if (method != 1 && method != 2) argument_error("sharded decomposition supports ulv (l2r) and urv (r2l)");
+    if (nranks < 1 || rank < 0 || rank >= nranks) argument_error("invalid rank / size");
+    const int64_t total = product(dims, 0, dims.size());
+    // ULV: the columns of c = A(i1; rest); URV: the rows of c = A(i1..i(d-1); id).
+    const int64_t first = method == 1 ? dims[0] : dims[(size_t)(d - 1)];
+    const int64_t count = total / first;
+    if (count % nranks != 0)
+        argument_error("sharded dimension " + std::to_string(count) + " is not divisible by " + std::to_string(nranks) +
+                       " ranks");
+    ShardRange r;
+    const int64_t per = count / nranks;
+    r.lo = per * rank;
+    r.hi = r.lo + per;
+    r.rows = method == 1 ? first : per;
+    r.cols = method == 1 ? per : first;
+    return r;
+}
+
+TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& dims, const SweepConfig& cfg,
+                           Comm& comm) {
+    const auto start = Clock::now();
+    const int64_t d = (int64_t)dims.size();
+    for (size_t k = 0; k < dims.size(); ++k)
+        if (dims[k] < 1)
+            argument_error("shape dim " + std::to_string(k + 1) + " is " + std::to_string(dims[k]) + ", must be >= 1");
+    const bool ulv = cfg.method == 1 && cfg.sweep == 0, urv = cfg.method == 2 && cfg.sweep == 1;
+    if (!ulv && !urv) argument_error("sharded decomposition supports ulv (l2r) and urv (r2l)");
+    check_refine(cfg.refine);
+    if (cfg.refine != 1) argument_error("sharded decomposition supports refine_passes = 1");
+    const int G = comm.size();
+    const ShardRange sr = shard_range(dims, cfg.method, G, comm.rank());
+    const int64_t local_n = sr.rows * sr.cols;
+    ensure_pool((size_t)(4.5 * 8.0 * (double)local_n) + ((size_t)256 << 20));
+    const bool rss = !(cfg.method == 1 && cfg.sweep == 1 && cfg.retain == 0);
+
+    TTResult res;
+    res.dims = dims;
+    res.cores.resize((size_t)d);
+    res.core_dims.resize((size_t)d);
+    // |A|_F: local blocked sums, combined in rank order
+    const double norm_a = std::sqrt(global_sum(comm, sum_squares(a_local, local_n)));
+    if (cut_timing())
+        std::fprintf(stderr, "[ttg] sharded norm: %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(Clock::now() - start).count());
+    const Resolved mode = resolve_mode(cfg, d, norm_a, rss);
+    res.input_norm = norm_a;
+    if (mode.fixed) res.ranks_requested = mode.ranks;
+    res.step_errors.assign((size_t)(d - 1), 0.0);
+    res.ranks_chosen.assign((size_t)d + 1, 1);
+    res.cuts.resize((size_t)(d - 1));
+    if (norm_a == 0.0) {  // zero_input_result (tt_decomp.cpp:126-142)
+        if (mode.fixed && *std::max_element(mode.ranks.begin(), mode.ranks.end()) > 1)
+            res.warnings.push_back("input tensor is zero; all ranks clamped to 1");
+        for (int64_t k = 0; k < d; ++k) {
+            DevBuf<double> z((size_t)dims[(size_t)k]);
+            z.zero();
+            set_core(res, (size_t)k, std::move(z), 1, dims[(size_t)k], 1);
         }
+        res.cuts.clear();
+        finish(res, rss, start);
+        return res;
+    }
+
+    // First cut, sharded: W = c (ULV, columns of c) or c^T (URV, rows of c).
+    const int64_t cut = ulv ? 1 : d - 1;
+    const int64_t kW = ulv ? dims[0] : dims[(size_t)(d - 1)];
+    const int64_t Nl = sr.hi - sr.lo, Ng = Nl * G;
+    const int64_t p = std::min(kW, Ng);
+    const CutRequest rq = make_request(res, mode, cfg, cut, p);
+    const auto tc0 = Clock::now();
+    ShardSpec spec{&comm, sr.lo, Ng};
+    WidePass1 e1(a_local, kW, Nl, ulv ? kW : Nl, ulv ? Layout::Col : Layout::Row, mode.fixed ? rq.rank : 32, &spec);
+    CutOut co = run_cut(e1, rq);
+    print_cut(ulv ? "ulv(sharded)" : "urv(sharded)", cut, ulv ? kW : Ng, ulv ? Ng : kW, co, tc0);
+    const int64_t r = co.rank;
+    res.step_errors[(size_t)(cut - 1)] = co.step_error;
+    res.ranks_chosen[(size_t)cut] = r;
+    res.cuts[(size_t)(cut - 1)] = ulv ? CutInfo{kW, Ng, p, co.steps, r, co.extensions, co.diag}
+                                      : CutInfo{Ng, kW, p, co.steps, r, co.extensions, co.diag};
+    // the core from the replicated Q; the local carry block, then the all-gathered carry
+    DevBuf<double> core((size_t)(kW * r));
+    TTG_LAUNCH(k_gather_qcols, (int)cdiv(kW * r, 256), 256, 0, stream(), e1.Q(), kW, co.sel.get(), r, !ulv,
+               core.get());
+    DevBuf<double> mine((size_t)(Nl * r)), all((size_t)(Ng * r));
+    if (ulv) {
+        set_core(res, 0, std::move(core), 1, dims[0], r);
+        dim3 g((unsigned)cdiv(Nl, 32), (unsigned)cdiv(r, 32));
+        TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1.R(), Nl, co.sel.get(), r, mine.get());
+        // rank blocks of r x Nl are the column blocks of the r x Ng carry: no repack
+        comm.allgather(mine.get(), all.get(), sizeof(double) * (size_t)(Nl * r));
+        if (d == 2) set_core(res, 1, std::move(all), r, dims[1], 1);
+        else ulv_cuts(res, all.get(), r * dims[1], Ng / dims[1], 2, r, dims, mode, cfg);
     } else {
-        // ---- TT-URV right to left (tt_decomp.cpp:216-339) ----
-        const double* c = a;
-        int64_t M = total_n / dims[(size_t)(d - 1)], n = dims[(size_t)(d - 1)], r_next = 1;
-        for (int64_t k = d; k >= 2; --k) {
-            const int64_t p = std::min(M, n);
-            CutRequest rq{mode.fixed, 0, 0.0, cfg.policy};
-            if (mode.fixed) {
-                const int64_t req = mode.ranks[(size_t)(k - 1)];
-                rq.rank = std::min(req, p);
-                if (rq.rank < req)
-                    res.warnings.push_back("cut " + std::to_string(k - 1) + ": requested rank " +
-                                           std::to_string(req) + " clamped to " + std::to_string(rq.rank));
-            } else {
-                rq.budget = mode.budgets[(size_t)(k - 2)];
-            }
-            // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
-            const auto tc0 = Clock::now();
-            auto e1 = make_pass1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
-            CutOut co = run_cut(*e1, rq);
-            if (cut_timing()) {
-                sync();
-                std::fprintf(stderr, "[ttg] urv cut %lld (%lld x %lld): %lld steps, %.3f ms\n", (long long)(k - 1),
-                             (long long)M, (long long)n, (long long)co.steps,
-                             std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
-            }
-            const int64_t r = co.rank;
-            res.step_errors[(size_t)(k - 2)] = co.step_error;
-            res.ranks_chosen[(size_t)(k - 1)] = r;
-            res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag};
-            DevBuf<double> core((size_t)(n * r));
-            TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1->Q(), n, co.sel.get(), r, true,
-                       core.get());
-            set_core(res, (size_t)(k - 1), std::move(core), r, dims[(size_t)(k - 1)], r_next);
-            DevBuf<double> next((size_t)(M * r));
-            dim3 g((unsigned)std::min<int64_t>(cdiv(M, 256), 4096), (unsigned)r);
-            TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1->R(), M, co.sel.get(), r, next.get());
-            r_next = r;
-            if (k > 2) {
-                carry = std::move(next);
-                c = carry.get();
-                n = dims[(size_t)(k - 2)] * r;
-                M = M / dims[(size_t)(k - 2)];
-            } else {
-                set_core(res, 0, std::move(next), 1, dims[0], r);
-            }
+        set_core(res, (size_t)(d - 1), std::move(core), r, dims[(size_t)(d - 1)], 1);
+        dim3 g((unsigned)std::min<int64_t>(cdiv(Nl, 256), 4096), (unsigned)r);
+        TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1.R(), Nl, co.sel.get(), r, mine.get());
+        DevBuf<double> gathered((size_t)(Ng * r));
+        if (cut_timing()) {
+            sync();
+            std::fprintf(stderr, "[ttg] carry rows + allocs: %.3f ms since the cut began\n",
+                         std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
         }
+        comm.allgather(mine.get(), gathered.get(), sizeof(double) * (size_t)(Nl * r));
+        if (cut_timing()) {
+            sync();
+            std::fprintf(stderr, "[ttg] carry allgather: %.3f ms since the cut began\n",
+                         std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
+        }
+        // rank g's Nl x r block -> rows [g Nl, (g+1) Nl) of the Ng x r carry
+        for (int q = 0; q < G; ++q)
+            TTG_CUDA(cudaMemcpy2DAsync(all.get() + (int64_t)q * Nl, sizeof(double) * Ng,
+                                       gathered.get() + (int64_t)q * Nl * r, sizeof(double) * Nl, sizeof(double) * Nl,
+                                       r, cudaMemcpyDeviceToDevice, stream()));
+        if (cut_timing()) {
+            sync();
+            std::fprintf(stderr, "[ttg] carry gather: %.3f ms since the cut began\n",
+                         std::chrono::duration<double, std::milli>(Clock::now() - tc0).count());
+        }
+        if (d == 2) set_core(res, 0, std::move(all), 1, dims[0], r);
+        else urv_cuts(res, all.get(), Ng / dims[(size_t)(d - 2)], dims[(size_t)(d - 2)] * r, d - 1, r, dims, mode, cfg);
     }
     finish(res, rss, start);
     return res;

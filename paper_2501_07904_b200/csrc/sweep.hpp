@@ -45,6 +45,20 @@ struct TTResult {
 // a: device pointer to the dense tensor (first index fastest).
 TTResult decompose(const double* a, const std::vector<int64_t>& dims, const SweepConfig& cfg);
 
+// Column-sharded sweep over the ranks of `comm`. The first unfolding is
+// split into comm.size() equal blocks of its pass-1 columns: TT-ULV-L2R shards the
+// columns of c = A(i1; i2..id) (block g is a contiguous slice of A), TT-URV-R2L shards the
+// rows of c = A(i1..i(d-1); id) (block g is an M/G x I_d column-major matrix). Each rank
+// passes its own block; the cores come back replicated on every rank. Requirements: the
+// sharded count divisible by comm.size(), refine_passes = 1, ULV-L2R or URV-R2L.
+struct ShardRange {
+    int64_t lo = 0, hi = 0;      // sharded index range [lo, hi) of this rank
+    int64_t rows = 0, cols = 0;  // the local block's shape (column-major)
+};
+ShardRange shard_range(const std::vector<int64_t>& dims, int method, int nranks, int rank);
+TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& dims, const SweepConfig& cfg,
+                           Comm& comm);
+
 // |A - reconstruct(tt)|^2 on device without materialising the full reconstruction.
 double residual_squared(const TTResult& r, const double* a);
 // Completion loop body on device (completion.cpp:161-186, step size 1): see

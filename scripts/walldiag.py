@@ -10,6 +10,8 @@ a = build(cfg, torch.device("cuda", 0)); torch.cuda.synchronize()
 c = CONFIGS[cfg]
 kw = dict(eps=c["eps"]) if c["mode"] == "tol" else dict(ranks=c["ranks"])
 lib().ttg_synchronize()
+if len(sys.argv) > 2 and sys.argv[2] == "prof":
+    lib().ttg_profile_enable(1)
 s = torch.cuda.ExternalStream(lib().ttg_stream())
 for it in range(8):
     for m, sw in (("ulv", "l2r"), ("urv", "r2l")):
