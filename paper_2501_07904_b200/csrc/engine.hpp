@@ -95,7 +95,7 @@ private:
     int64_t k_, N_, ld_, p_;
     Layout layout_;
     int64_t steps_ = 0, cap_ = 0;
-    int ncand_ = 0, mode_ = 0, nchunk_ = 1, ksplit_ = 1;
+    int ncand_ = 0, ngc_ = 0, mode_ = 0, nchunk_ = 1, ksplit_ = 1;  // stream / guard candidate slots
     Comm* comm_ = nullptr;
     int64_t off_ = 0, Ng_ = 0;
     DevBuf<double> nu_, cref_, R_, diag_, beta_, mass_;

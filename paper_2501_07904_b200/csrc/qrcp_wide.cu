@@ -97,6 +97,21 @@ __device__ __forceinline__ bool downdate(int64_t t, int64_t j, int64_t N, double
     return fl;
 }
 
+// downdate() with nu_j and cref_j already loaded (staged through shared memory).
+__device__ __forceinline__ bool downdate_v(int64_t t, int64_t j, int64_t N, double r, int64_t pj, double nuj,
+                                          double crefj, double* R, double* nu, Cand& best, double& mass) {
+    R[t * N + j] = r;
+    const double nv = __dsub_rn(nuj, __dmul_rn(r, r));
+    nu[j] = nv;
+    const bool fl = nv < __dmul_rn(1e-16, crefj) || nv < 0.0;
+    if (!fl) {
+        Cand c{nv, pj, j};
+        if (better(c, best)) best = c;
+        mass += nv;
+    }
+    return fl;
+}
+
 // ---------------------------------------------------------------------------
 // Init: nu_j = cref_j = |w_j|^2 (sequential, no contraction: sum_squares_serial),
 // identity positions, candidates for step 0 and the initial mass.
@@ -558,6 +573,219 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// MODE 2 (Col layout, k <= 32*KC): a warp owns 32 consecutive columns at a time. Lane l
+// reads rows l, l+32, .. of each of the 32 columns (one coalesced segment per column, 32
+// independent loads in flight per lane), multiplies by its rows of q_t, and a warp
+// reduce-scatter leaves column c's dot in lane c, which runs the epilogue. Every column
+// sums in the same tree, so identical columns stay bitwise identical.
+template <int KC>
+__global__ void __launch_bounds__(kThreads) k_stream_c32(const double* __restrict__ W, int64_t k, int64_t N,
+                                                         int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                         const double* diag, const int64_t* piv, double* R,
+                                                         double* nu, const double* cref, const int64_t* pos,
+                                                         int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double q[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) q[c] = lane + 32 * c < k ? Q[lane + 32 * c + t * k] : 0.0;
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t j0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 32; j0 < N; j0 += nw * 32) {
+        double d[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int64_t j = j0 + c;
+            double a = 0.0;
+#pragma unroll
+            for (int r = 0; r < KC; ++r) {
+                const int64_t i = lane + 32 * r;
+                if (i < k && j < N) a = fma(q[r], __ldg(W + i + j * ld), a);
+            }
+            d[c] = a;
+        }
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = (lane & h) != 0;
+#pragma unroll
+            for (int c = 0; c < h; ++c) {
+                const double send = up ? d[c] : d[c + h];
+                const double keep = up ? d[c + h] : d[c];
+                d[c] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        const int64_t j = j0 + lane;
+        const bool active = j < N;
+        const int64_t pj = active ? pos[j] : 0;
+        const bool chosen = active && (pj < t || j == jp);
+        if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+        bool fl = false;
+        if (active && !chosen) fl = downdate(t, j, N, d[0], pj, R, nu, cref, best, msum);
+        append_flag(fl, j, flags, nflag);
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
+// ---- MODE 5: TMA-fed stream for narrow W (k <= 32) -------------------------------------
+// A persistent CTA walks chunks of 256 columns through a 3-stage ring in shared memory:
+// one thread arms an mbarrier with the chunk's byte count and issues cp.async.bulk copies
+// (one contiguous 256*k block for the Col layout with ld == k; k row segments of 2 KB for
+// the Row layout), so HBM streams continuously while the 8 warps work on the previous
+// chunks. Arithmetic is that of k_stream_c32 (Col) and k_stream<0> (Row), so results are
+// bitwise the same as the non-TMA kernels'.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+constexpr int kTmaCols = 256, kTmaStages = 3;
+
+// Dot of column j0 + threadIdx.x with q (Col layout, k <= 32): warp w takes the 32 columns
+// [j0 + 32w, j0 + 32w + 32) from `base` (column c at base + c*k, smem tile or global),
+// reduce-scatter leaves column c's dot in lane c.
+__device__ __forceinline__ double col_dot32(const double* base, int64_t k, int64_t ncols, const double* q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double ql = lane < k ? q[lane] : 0.0;
+    double d[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        const int64_t cc = warp * 32 + c;
+        d[c] = (lane < k && cc < ncols) ? ql * base[cc * k + lane] : 0.0;
+    }
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int c = 0; c < h; ++c) {
+            const double send = up ? d[c] : d[c + h];
+            const double keep = up ? d[c + h] : d[c];
+            d[c] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+    return d[0];
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(kThreads, 1) k_stream_tma(const double* __restrict__ W, int64_t k, int64_t N,
+                                                            int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                            const double* diag, const int64_t* piv, double* R,
+                                                            double* nu, const double* cref, const int64_t* pos,
+                                                            int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    extern __shared__ __align__(128) double ring[];  // kTmaStages x (kTmaCols * (k + 3)): W | nu | cref | pos
+    __shared__ __align__(8) uint64_t bars[kTmaStages];
+    __shared__ double qs[32];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    const int tid = threadIdx.x;
+    const int64_t nfull = N / kTmaCols;
+    const int64_t welems = (int64_t)kTmaCols * k, selems = welems + 3 * kTmaCols;
+    const uint32_t cbytes = (uint32_t)(kTmaCols * sizeof(double));
+    const uint32_t sbytes = (uint32_t)(welems * sizeof(double)) + 3 * cbytes;
+    const int64_t mine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](int s, int64_t ch) {
+        mbar_expect_tx(&bars[s], sbytes);
+        double* dst = ring + s * selems;
+        const int64_t j0 = ch * kTmaCols;
+        if (LAYOUT == 0) {
+            bulk_g2s(dst, W + j0 * k, (uint32_t)(welems * sizeof(double)), &bars[s]);
+        } else {
+            for (int64_t i = 0; i < k; ++i) bulk_g2s(dst + i * kTmaCols, W + i * ld + j0, cbytes, &bars[s]);
+        }
+        // the epilogue's per-column state rides in the same stage
+        bulk_g2s(dst + welems, nu + j0, cbytes, &bars[s]);
+        bulk_g2s(dst + welems + kTmaCols, cref + j0, cbytes, &bars[s]);
+        bulk_g2s(dst + welems + 2 * kTmaCols, pos + j0, cbytes, &bars[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < k) qs[tid] = Q[tid + t * k];
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < kTmaStages && s < mine; ++s) issue(s, blockIdx.x + (int64_t)s * gridDim.x);
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    auto epilogue = [&](int64_t j, double a, bool active) {
+        const int64_t pj = active ? pos[j] : 0;
+        const bool chosen = active && (pj < t || j == jp);
+        if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+        bool fl = false;
+        if (active && !chosen) fl = downdate(t, j, N, a, pj, R, nu, cref, best, msum);
+        append_flag(fl, j, flags, nflag);
+    };
+    for (int64_t i = 0; i < mine; ++i) {
+        const int s = (int)(i % kTmaStages);
+        mbar_wait(&bars[s], (uint32_t)((i / kTmaStages) & 1));
+        const double* tile = ring + s * selems;
+        const int64_t j0 = (blockIdx.x + i * gridDim.x) * kTmaCols;
+        double a;
+        if (LAYOUT == 0) {
+            a = col_dot32(tile, k, kTmaCols, qs);
+        } else {
+            a = 0.0;
+            for (int64_t r = 0; r < k; ++r) a = fma(qs[r], tile[r * kTmaCols + tid], a);
+        }
+        {
+            const int64_t j = j0 + tid;
+            const int64_t pj = reinterpret_cast<const int64_t*>(tile + welems + 2 * kTmaCols)[tid];
+            const bool chosen = pj < t || j == jp;
+            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+            bool fl = false;
+            if (!chosen)
+                fl = downdate_v(t, j, N, a, pj, tile[welems + tid], tile[welems + kTmaCols + tid], R, nu, best, msum);
+            append_flag(fl, j, flags, nflag);
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (tid == 0 && i + kTmaStages < mine) issue(s, blockIdx.x + (i + kTmaStages) * gridDim.x);
+    }
+    // the partial last chunk (plain loads, same arithmetic) on the CTA next in turn
+    const int64_t tail = N - nfull * kTmaCols;
+    if (tail > 0 && blockIdx.x == nfull % gridDim.x) {
+        const int64_t j0 = nfull * kTmaCols;
+        double a = 0.0;
+        if (LAYOUT == 0) {
+            a = col_dot32(W + j0 * k, k, tail, qs);
+        } else if (tid < tail) {
+            for (int64_t r = 0; r < k; ++r) a = fma(qs[r], W[r * ld + j0 + tid], a);
+        }
+        epilogue(j0 + tid, a, tid < tail);
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (tid == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 // MODE 3: a CTA owns 32 columns; its 8 warps split the k rows (each row read as a
 // coalesced 256-byte segment); partials combined in warp order in smem.
 __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __restrict__ W, int64_t k, int64_t N,
@@ -680,62 +908,117 @@ __global__ void __launch_bounds__(kThreads) k_init_fin(const double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// guard: for each flagged column j the trailing norm after step t is
-// |w_j - Q[:, :t+1] R(0:t, j)|^2 (= the sum of squares of rows t+1.. of the updated
-// column, factor.cpp:103-105). One warp per flagged column, R(0:t, j) staged per warp.
+// guard: for each flagged column j the trailing norm after step t is the squared norm of
+// w_j's residual against Q[:, :t+1] (= the sum of squares of rows t+1.. of the updated
+// column, factor.cpp:103-105); it resets cref like the reference's recompute. The guard
+// also emits per-CTA candidates and masses of the columns it recomputed (slots after the
+// stream kernel's), so no rescan of all columns is needed: k_stream left flagged columns
+// out of its candidates and masses.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void guard_out(Cand best, double msum, Cand* gcand, double* gmass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { gcand[blockIdx.x] = best; gmass[blockIdx.x] = msum; }
+}
+
+// k <= KM: one thread per flagged column, the column in registers, Q[:, :t+1] staged in
+// shared memory (broadcast reads), modified Gram-Schmidt residual.
+template <int KM>
+__global__ void __launch_bounds__(kThreads) k_guard_lane(const double* __restrict__ W, int64_t k, int64_t N,
+                                                         int64_t ld, int layout, int64_t t,
+                                                         const double* __restrict__ Q, const int64_t* flags,
+                                                         const int* nflag, double* nu, double* cref,
+                                                         const int64_t* pos, Cand* gcand, double* gmass) {
+    extern __shared__ double qs[];  // Q[:, :t+1]
+    const int nf = *nflag;
+    Cand best = cand_none();
+    double msum = 0.0;
+    if (nf > 0) {
+        for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
+        __syncthreads();
+        for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
+            const int64_t j = flags[f];
+            double x[KM];
+#pragma unroll
+            for (int i = 0; i < KM; ++i) x[i] = i < k ? ld_w(W, ld, layout, i, j) : 0.0;
+            for (int64_t l = 0; l <= t; ++l) {
+                const double* q = qs + l * k;
+                double z = 0.0;
+#pragma unroll
+                for (int i = 0; i < KM; ++i)
+                    if (i < k) z = fma(q[i], x[i], z);
+#pragma unroll
+                for (int i = 0; i < KM; ++i)
+                    if (i < k) x[i] = fma(-q[i], z, x[i]);
+            }
+            double sq = 0.0;
+#pragma unroll
+            for (int i = 0; i < KM; ++i) sq = fma(x[i], x[i], sq);
+            nu[j] = sq;
+            cref[j] = sq;
+            const Cand c{sq, pos[j], j};
+            if (better(c, best)) best = c;
+            msum += sq;
+        }
+    }
+    guard_out(best, msum, gcand, gmass);
+}
+
+// k > 32: one warp per flagged column, lane-strided rows, R(0:t, j) staged per warp.
 __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W, int64_t k, int64_t N,
                                                     int64_t ld, int layout, int64_t t,
                                                     const double* __restrict__ Q, const double* R,
                                                     const int64_t* flags, const int* nflag, double* nu,
-                                                    double* cref, int stage_q) {
+                                                    double* cref, int stage_q, const int64_t* pos, Cand* gcand,
+                                                    double* gmass) {
     extern __shared__ double qs[];  // Q[:, :t+1] when staged (dynamic smem > 0)
     __shared__ double rbuf[kThreads / 32][64];
     const int nf = *nflag;
-    if (nf == 0) return;
-    const bool staged = stage_q != 0;
-    if (staged)
-        for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
-    __syncthreads();
-    const double* __restrict__ qq = staged ? qs : Q;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool rsm = t + 1 <= 64;
-    for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf; f += (int64_t)gridDim.x * (kThreads / 32)) {
-        const int64_t j = flags[f];
-        if (rsm) {
-            for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = R[l * N + j];
-            __syncwarp();
-        }
-        double s = 0.0;
-        for (int64_t i = lane; i < k; i += 32) {
-            double x = ld_w(W, ld, layout, i, j);
-            for (int64_t l = 0; l <= t; ++l) x = fma(-qq[i + l * k], rsm ? rbuf[warp][l] : R[l * N + j], x);
-            s = fma(x, x, s);
-        }
-        s = warp_sum(s);
-        if (lane == 0) { nu[j] = s; cref[j] = s; }
-        __syncwarp();
-    }
-}
-
-// candidates and trailing mass over all unpivoted columns (after a guard recompute).
-__global__ void __launch_bounds__(kThreads) k_recand(int64_t N, int64_t t, const int* nflag, const double* nu,
-                                                     const int64_t* pos, Cand* cand, double* mass) {
-    if (*nflag == 0) return;
-    __shared__ Cand sc[kThreads / 32];
-    __shared__ double sd[kThreads / 32];
     Cand best = cand_none();
     double msum = 0.0;
-    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
-        const int64_t pj = pos[j];
-        if (pj <= t) continue;
-        Cand c{nu[j], pj, j};
-        if (better(c, best)) best = c;
-        msum += nu[j];
+    if (nf > 0) {
+        const bool staged = stage_q != 0;
+        if (staged)
+            for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
+        __syncthreads();
+        const double* __restrict__ qq = staged ? qs : Q;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const bool rsm = t + 1 <= 64;
+        for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
+             f += (int64_t)gridDim.x * (kThreads / 32)) {
+            const int64_t j = flags[f];
+            if (rsm) {
+                for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = R[l * N + j];
+                __syncwarp();
+            }
+            double sq = 0.0;
+            for (int64_t i = lane; i < k; i += 32) {
+                double x = ld_w(W, ld, layout, i, j);
+                for (int64_t l = 0; l <= t; ++l) x = fma(-qq[i + l * k], rsm ? rbuf[warp][l] : R[l * N + j], x);
+                sq = fma(x, x, sq);
+            }
+            sq = warp_sum(sq);
+            if (lane == 0) {
+                nu[j] = sq;
+                cref[j] = sq;
+                const Cand c{sq, pos[j], j};
+                if (better(c, best)) best = c;
+                msum += sq;
+            }
+            __syncwarp();
+        }
     }
-    best = block_best(best, sc);
-    msum = block_sum(msum, sd);
-    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+    guard_out(best, msum, gcand, gmass);
+}
+
+// Empty guard slots (after init / exact refresh, which cover every column themselves).
+__global__ void k_clear_slots(Cand* cand, double* mass, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        cand[i] = cand_none();
+        mass[i] = 0.0;
+    }
 }
 
 // Exact trailing norms from the residual Y = W - Q[:, :s] R(0:s, :) (already formed):
@@ -782,8 +1065,13 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         if (off_ < 0 || off_ + N > Ng_) argument_error("shard column range outside the matrix");
     }
     const int sms = sm_count();
-    if (layout == Layout::Col) {
-        mode_ = (k >= 64 || ld != k) ? 1 : 2;
+    const bool aligned16 = (reinterpret_cast<uintptr_t>(W) & 15) == 0;  // bulk copies need 16 B
+    if (aligned16 && layout == Layout::Col && k <= 32 && ld == k) {
+        mode_ = 5;  // TMA ring over contiguous 256-column blocks
+    } else if (aligned16 && layout == Layout::Row && k <= 32 && ld % 2 == 0) {
+        mode_ = 5;  // TMA ring over k row segments per 256-column block
+    } else if (layout == Layout::Col) {
+        mode_ = k <= 64 ? 2 : 1;
     } else if (k >= 64 && N < (int64_t)sms * 4 * kThreads && (k <= kQSmem || cdiv(N, 32) < 2 * sms)) {
         // few columns: split the rows inside a CTA (MODE 3), or also across CTAs when
         // even 32-column groups cannot fill the GPU (MODE 4)
@@ -793,15 +1081,17 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     }
     if (mode_ == 4) ksplit_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 2048), cdiv(4 * sms, cdiv(N, 32))));
     const int per_sm = 8;
-    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : cdiv(N, kThreads);
+    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
+    if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(Ng_); flags_.alloc(N);
     if (comm_) {
         rec_.alloc((size_t)(k + kRecHead));
         recs_.alloc((size_t)comm_->size() * (k + kRecHead));
     }
-    cand_.alloc(ncand_); mass_.alloc(ncand_); nflag_.alloc(1); nflag_.zero();
+    ngc_ = std::max(1, 2 * sms);
+    cand_.alloc(ncand_ + ngc_); mass_.alloc(ncand_ + ngc_); nflag_.alloc(1); nflag_.zero();
     wv_.alloc(k); yv_.alloc(k);
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
     if (mode_ == 4) kpart_.alloc((size_t)ksplit_ * N);
@@ -812,12 +1102,14 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         TTG_LAUNCH(k_init_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, nu_.get(), cref_.get(),
                    pos_.get(), perm_.get(), cand_.get(), mass_.get());
     } else {
-        const size_t smem = mode_ == 2 ? sizeof(double) * k * (kThreads + 1) : 0;
-        auto init = (mode_ == 0 || mode_ == 3) ? k_init<0> : mode_ == 1 ? k_init<1> : k_init<2>;
+        const bool tile = layout == Layout::Col && k < 64 && ld == k;  // contiguous narrow columns
+        const size_t smem = tile ? sizeof(double) * k * (kThreads + 1) : 0;
+        auto init = layout == Layout::Row ? k_init<0> : tile ? k_init<2> : k_init<1>;
         allow_smem(init, smem);
         TTG_LAUNCH(init, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
                    perm_.get(), cand_.get(), mass_.get());
     }
+    TTG_LAUNCH(k_clear_slots, 1, 256, 0, stream(), cand_.get() + ncand_, mass_.get() + ncand_, ngc_);
     if (comm_)
         TTG_LAUNCH(k_shard_init, (int)std::min<int64_t>(cdiv(Ng_, 256), 8 * sms), 256, 0, stream(), off_, N_, Ng_,
                    pos_.get(), perm_.get(), cand_.get(), ncand_);
@@ -843,7 +1135,7 @@ void WideQrcp::grow(int64_t cap) {
 }
 
 double WideQrcp::trailing_mass() {
-    std::vector<double> h = mass_.to_host(ncand_);
+    std::vector<double> h = mass_.to_host(ncand_ + ngc_);
     double s = 0.0;
     for (double v : h) s += v;
     return comm_ ? global_sum(*comm_, s) : s;
@@ -866,6 +1158,7 @@ double WideQrcp::refresh_exact() {
     }
     TTG_LAUNCH(k_resnorm, ncand_, kThreads, 0, stream(), Yr.get(), k_, N_, (int)layout_, s, nu_.get(), cref_.get(),
                pos_.get(), cand_.get(), mass_.get());
+    TTG_LAUNCH(k_clear_slots, 1, 256, 0, stream(), cand_.get() + ncand_, mass_.get() + ncand_, ngc_);
     return trailing_mass();
 }
 
@@ -885,7 +1178,7 @@ void WideQrcp::step() {
 void WideQrcp::reflect_step(int64_t t) {
     WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
          vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
-         ncand_, 1, k_, recs_.get(), comm_ ? comm_->size() : 0, off_, N_};
+         ncand_ + ngc_, 1, k_, recs_.get(), comm_ ? comm_->size() : 0, off_, N_};
     if (comm_) {  // exchange the ranks' pivot records before the (replicated) reflector
         TTG_LAUNCH(k_shard_export, 1, kThreads, 0, stream(), s, t, rec_.get());
         comm_->allgather(rec_.get(), recs_.get(), sizeof(double) * (size_t)(k_ + kRecHead));
@@ -916,14 +1209,19 @@ void WideQrcp::gemv_step(int64_t t) {
                    kpart_.get());
         TTG_LAUNCH(k_stream_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, t, diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    } else if (mode_ == 5) {
+        const size_t smem = sizeof(double) * (size_t)kTmaStages * kTmaCols * (size_t)(k_ + 3);
+        auto kern = layout_ == Layout::Col ? k_stream_tma<0> : k_stream_tma<1>;
+        allow_smem(kern, smem);
+        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Qt_.get(), diag_.get(), piv_.get(),
+                   R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
     } else {
         const size_t qbytes = sizeof(double) * ((k_ + 1) & ~int64_t(1));
-        const size_t smem = (mode_ == 2 ? qbytes + sizeof(double) * k_ * (kThreads + 1)
-                                        : (k_ <= kQSmem || mode_ == 3 ? qbytes : 0));
+        const size_t smem = mode_ == 2 ? 0 : (k_ <= kQSmem || mode_ == 3 ? qbytes : 0);
         const bool qs = k_ <= kQSmem;
         auto kern = mode_ == 0   ? (qs ? k_stream<0, true> : k_stream<0, false>)
                     : mode_ == 1 ? (qs ? k_stream<1, true> : k_stream<1, false>)
-                    : mode_ == 2 ? k_stream<2, true>
+                    : mode_ == 2 ? (k_ <= 32 ? k_stream_c32<1> : k_stream_c32<2>)
                                  : k_stream_splitk;
         allow_smem(kern, smem);
         TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Qt_.get(), diag_.get(), piv_.get(),
@@ -932,15 +1230,21 @@ void WideQrcp::gemv_step(int64_t t) {
     // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
     // written once, and row t of R written.
     prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
-    // the guard stages Q[:, :t+1] in shared memory when it fits (<= 96 KB)
+    // guard recompute of the flagged norms; its candidates / masses go to the slots after
+    // the stream kernel's
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
-    const bool stage = gq <= 96 * 1024;
-    allow_smem(k_guard, stage ? gq : 0);
-    TTG_LAUNCH(k_guard, std::max(1, sm_count() * 2), kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_,
-               (int)layout_, t, Qt_.get(), R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(),
-               stage ? 1 : 0);
-    TTG_LAUNCH(k_recand, ncand_, kThreads, 0, stream(), N_, t, nflag_.get(), nu_.get(), pos_.get(), cand_.get(),
-               mass_.get());
+    if (k_ <= 32) {
+        TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, Qt_.get(),
+                   flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get() + ncand_,
+                   mass_.get() + ncand_);
+    } else {
+        // Q[:, :t+1] staged in shared memory when it fits (<= 96 KB)
+        const bool stage = gq <= 96 * 1024;
+        allow_smem(k_guard, stage ? gq : 0);
+        TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, Qt_.get(),
+                   R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), stage ? 1 : 0, pos_.get(),
+                   cand_.get() + ncand_, mass_.get() + ncand_);
+    }
 }
 
 }  // namespace ttg
