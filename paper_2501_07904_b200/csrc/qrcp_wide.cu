@@ -1013,6 +1013,190 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
     guard_out(best, msum, gcand, gmass);
 }
 
+// ---------------------------------------------------------------------------
+// Exact refresh without materialising the residual: nu_j = cref_j = |w_j - Q[:, :s]
+// R(0:s, j)|^2 for every unpivoted column, one pass over W and R(0:s, :), then candidates
+// and trailing mass (slots 0..gridDim.x-1). s <= 32.
+// ---------------------------------------------------------------------------
+// Col layout: a warp owns 32 columns; lane = row within 32-row blocks; R(0:s, j0:j0+32)
+// staged per warp in shared memory; the column masses are reduce-scattered to lane c.
+__global__ void __launch_bounds__(kThreads) k_refresh_col(const double* __restrict__ W, int64_t k, int64_t N,
+                                                          int64_t ld, int64_t s, const double* __restrict__ Q,
+                                                          const double* __restrict__ R, double* nu, double* cref,
+                                                          const int64_t* pos, Cand* cand, double* mass) {
+    extern __shared__ double rdyn[];  // per warp: R(0:s, j0:j0+32), [l * 32 + c]
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* rt = rdyn + warp * 32 * 32;
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t j0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 32; j0 < N; j0 += nw * 32) {
+        for (int64_t l = 0; l < s; ++l) rt[l * 32 + lane] = j0 + lane < N ? R[l * N + j0 + lane] : 0.0;
+        __syncwarp();
+        double acc[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+        for (int64_t i0 = 0; i0 < k; i0 += 32) {
+            const int64_t i = i0 + lane;
+            double x[32];
+            const double* wp = W + i + j0 * ld;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                x[c] = (i < k && j0 + c < N) ? __ldg(wp) : 0.0;
+                wp += ld;
+            }
+            for (int64_t l = 0; l < s; ++l) {
+                const double q = i < k ? Q[i + l * k] : 0.0;
+                const double* rl = rt + l * 32;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) x[c] = fma(-q, rl[c], x[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = fma(x[c], x[c], acc[c]);
+        }
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = (lane & h) != 0;
+#pragma unroll
+            for (int c = 0; c < h; ++c) {
+                const double send = up ? acc[c] : acc[c + h];
+                const double keep = up ? acc[c + h] : acc[c];
+                acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        const int64_t j = j0 + lane;
+        if (j < N) {
+            const int64_t pj = pos[j];
+            if (pj >= s) {
+                nu[j] = acc[0];
+                cref[j] = acc[0];
+                const Cand c{acc[0], pj, j};
+                if (better(c, best)) best = c;
+                msum += acc[0];
+            }
+        }
+        __syncwarp();
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
+// Row layout: a CTA owns 32 columns at a time (lane = column, rows read as coalesced
+// 256-byte segments), its 8 warps split the rows; R(0:s, j) sits in registers, Q[:, :s]
+// in shared memory transposed to [i][l] (16-byte pair loads, broadcast across the warp);
+// the warps' partial masses combine in warp order in shared memory.
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_refresh_row(const double* __restrict__ W, int64_t k, int64_t N,
+                                                          int64_t ld, int64_t s, const double* __restrict__ Q,
+                                                          const double* __restrict__ R, double* nu, double* cref,
+                                                          const int64_t* pos, Cand* cand, double* mass) {
+    extern __shared__ double2 qt2[];  // k x S/2 pairs: qT[i][l]
+    __shared__ double part[kThreads / 32][33];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    double* qt = reinterpret_cast<double*>(qt2);
+    for (int64_t e = threadIdx.x; e < k * S; e += kThreads) {
+        const int64_t i = e / S, l = e - i * S;
+        qt[e] = l < s ? Q[i + l * k] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < N; j0 += (int64_t)gridDim.x * 32) {
+        const int64_t j = j0 + lane;
+        const bool active = j < N;
+        double r[S];
+#pragma unroll
+        for (int l = 0; l < S; ++l) r[l] = (active && l < s) ? R[l * N + j] : 0.0;
+        double acc = 0.0;
+        if (active)
+#pragma unroll 4
+            for (int64_t i = warp; i < k; i += kThreads / 32) {
+                double x = W[i * ld + j];
+                const double2* q = qt2 + i * (S / 2);
+#pragma unroll
+                for (int l = 0; l < S / 2; ++l) {
+                    const double2 qq = q[l];
+                    x = fma(-qq.x, r[2 * l], x);
+                    x = fma(-qq.y, r[2 * l + 1], x);
+                }
+                acc = fma(x, x, acc);
+            }
+        part[warp][lane] = acc;
+        __syncthreads();
+        if (warp == 0 && active) {
+            double m = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) m += part[w][lane];
+            const int64_t pj = pos[j];
+            if (pj >= s) {
+                nu[j] = m;
+                cref[j] = m;
+                const Cand c{m, pj, j};
+                if (better(c, best)) best = c;
+                msum += m;
+            }
+        }
+        __syncthreads();
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
+// Row layout with small k: a thread owns a column (R(0:s, j) in registers, Q[:, :s] in
+// shared memory transposed to [i][l] so pairs of q values come in one 16-byte load, rows
+// coalesced across the threads). S >= s is the compile-time width (zero-padded).
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_refresh_rowt(const double* __restrict__ W, int64_t k, int64_t N,
+                                                           int64_t ld, int64_t s, const double* __restrict__ Q,
+                                                           const double* __restrict__ R, double* nu, double* cref,
+                                                           const int64_t* pos, Cand* cand, double* mass) {
+    extern __shared__ double2 qt2[];  // k x S/2 pairs: qT[i][l]
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    double* qt = reinterpret_cast<double*>(qt2);
+    for (int64_t e = threadIdx.x; e < k * S; e += kThreads) {
+        const int64_t i = e / S, l = e - i * S;
+        qt[e] = l < s ? Q[i + l * k] : 0.0;
+    }
+    __syncthreads();
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
+        const int64_t pj = pos[j];
+        if (pj < s) continue;
+        double r[S];
+#pragma unroll
+        for (int l = 0; l < S; ++l) r[l] = l < s ? R[l * N + j] : 0.0;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int64_t i = 0; i < k; ++i) {
+            double x = W[i * ld + j];
+            const double2* q = qt2 + i * (S / 2);
+#pragma unroll
+            for (int l = 0; l < S / 2; ++l) {
+                const double2 qq = q[l];
+                x = fma(-qq.x, r[2 * l], x);
+                x = fma(-qq.y, r[2 * l + 1], x);
+            }
+            acc = fma(x, x, acc);
+        }
+        nu[j] = acc;
+        cref[j] = acc;
+        const Cand c{acc, pj, j};
+        if (better(c, best)) best = c;
+        msum += acc;
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 // Empty guard slots (after init / exact refresh, which cover every column themselves).
 __global__ void k_clear_slots(Cand* cand, double* mass, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1144,6 +1328,26 @@ double WideQrcp::trailing_mass() {
 double WideQrcp::refresh_exact() {
     const int64_t s = steps_;
     if (s == 0) return trailing_mass();
+    const size_t qrow = sizeof(double) * (size_t)(k_ * (s <= 8 ? 8 : s <= 16 ? 16 : 32));
+    if (s <= 32 && (layout_ == Layout::Col || qrow <= 200 * 1024)) {
+        // fused: one pass over W and R(0:s, :), no residual buffer
+        if (layout_ == Layout::Col) {
+            const size_t rsm = sizeof(double) * (kThreads / 32) * 32 * 32;
+            allow_smem(k_refresh_col, rsm);
+            TTG_LAUNCH(k_refresh_col, ncand_ + ngc_, kThreads, rsm, stream(), W_, k_, N_, ld_, s, Qt_.get(),
+                       R_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get(), mass_.get());
+        } else {
+            const int S = s <= 8 ? 8 : s <= 16 ? 16 : 32;
+            auto kern = k_ > 64 ? (S == 8 ? k_refresh_row<8> : S == 16 ? k_refresh_row<16> : k_refresh_row<32>)
+                                : (S == 8 ? k_refresh_rowt<8> : S == 16 ? k_refresh_rowt<16> : k_refresh_rowt<32>);
+            const size_t sm = sizeof(double) * (size_t)(k_ * S);
+            allow_smem(kern, sm);
+            TTG_LAUNCH(kern, ncand_ + ngc_, kThreads, sm, stream(), W_, k_, N_, ld_, s, Qt_.get(), R_.get(),
+                       nu_.get(), cref_.get(), pos_.get(), cand_.get(), mass_.get());
+        }
+        // (one CTA per candidate slot, the guard's slots included: no clearing needed)
+        return trailing_mass();
+    }
     DevBuf<double> Yr((size_t)(k_ * N_));
     if (layout_ == Layout::Col) {
         TTG_CUDA(cudaMemcpy2DAsync(Yr.get(), sizeof(double) * k_, W_, sizeof(double) * ld_, sizeof(double) * k_, N_,
