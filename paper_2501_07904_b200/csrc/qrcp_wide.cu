@@ -473,6 +473,56 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
     wy_q(s, t, 0);
 }
 
+// Whole step in one CTA with the WY state staged in shared memory: Y[:, :t] and T[:t, :t]
+// are copied in once, every phase then reads shared memory instead of dependent L2 loads,
+// and column t of Y and T is written back. The phase functions run unchanged on a WY view
+// whose T / vector / scratch pointers are the shared copies (leading dimension t+1).
+size_t wy_smem_doubles(int64_t k, int64_t t) {
+    const int64_t tp = t + 1;
+    return (size_t)(k * tp + tp * tp + 2 * k + (tp + 1) + 4 * tp + 2);
+}
+
+template <bool SH>
+__global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
+    extern __shared__ double wsm[];
+    __shared__ double red[kThreads / 32];
+    const int64_t k = s.k, tp = t + 1;
+    WY ls = s;
+    ls.cap = tp;
+    ls.Y = wsm;
+    ls.T = ls.Y + k * tp;
+    ls.wv = ls.T + tp * tp;
+    ls.yv = ls.wv + k;
+    ls.part = ls.yv + k;
+    ls.vec = ls.part + (tp + 1);
+    for (int64_t e = threadIdx.x; e < k * t; e += kThreads) ls.Y[e] = s.Y[e];
+    for (int64_t e = threadIdx.x; e < t * t; e += kThreads) {
+        const int64_t c = e / t, r = e - c * t;
+        ls.T[r + c * tp] = s.T[r + c * s.cap];
+    }
+    __syncthreads();
+    if (SH) wy_pick_shard(ls, t, 0, true);
+    else wy_pick(ls, t, 0, true);
+    __syncthreads();
+    wy_sum_parts(ls, t, ls.vec, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_u(ls, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_y(ls, t, 0, red);
+    __syncthreads();
+    wy_reflect(ls, t, 0, true, red);
+    __syncthreads();
+    wy_sum_parts(ls, t, ls.vec + 2 * ls.cap, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_tcol(ls, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_g(ls, t, threadIdx.x, kThreads);
+    __syncthreads();
+    wy_q(ls, t, 0);
+    for (int64_t i = threadIdx.x; i < k; i += kThreads) s.Y[i + t * k] = ls.Y[i + t * k];
+    for (int64_t r = threadIdx.x; r <= t; r += kThreads) s.T[r + t * s.cap] = ls.T[r + t * tp];
+}
+
 // Multi-CTA phases (row chunks) and the small single-CTA glue between them.
 __global__ void __launch_bounds__(kThreads) k_wy_pick(WY s, int64_t t) { wy_pick(s, t, blockIdx.x, blockIdx.x == 0); }
 __global__ void __launch_bounds__(kThreads) k_wy_pick_shard(WY s, int64_t t) {
@@ -1390,8 +1440,16 @@ void WideQrcp::reflect_step(int64_t t) {
     // one fused CTA while the O(k t) work is small, row chunks otherwise
     const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(nchunk_, cdiv(k_ * (t + 1), 32768)));
     if (nch == 1) {
-        if (comm_) TTG_LAUNCH(k_wy_fused<true>, 1, kThreads, 0, stream(), s, t);
-        else TTG_LAUNCH(k_wy_fused<false>, 1, kThreads, 0, stream(), s, t);
+        const size_t sm = sizeof(double) * wy_smem_doubles(k_, t);
+        if (sm <= 200 * 1024) {
+            auto kern = comm_ ? k_wy_fused_smem<true> : k_wy_fused_smem<false>;
+            allow_smem(kern, sm);
+            TTG_LAUNCH(kern, 1, kThreads, sm, stream(), s, t);
+        } else if (comm_) {
+            TTG_LAUNCH(k_wy_fused<true>, 1, kThreads, 0, stream(), s, t);
+        } else {
+            TTG_LAUNCH(k_wy_fused<false>, 1, kThreads, 0, stream(), s, t);
+        }
         return;
     }
     s.nchunk = nch;
