@@ -78,7 +78,7 @@ public:
     // returns the exact trailing mass.
     double refresh_exact();
 
-    const double* Q() const { return Qt_.get(); }      // k x cap, columns 0..steps-1 = economy Q
+    const double* Q() const { return explicit_ ? Qx_.get() : Qt_.get(); }  // columns 0..steps-1 = economy Q
     const double* R() const { return R_.get(); }       // rows 0..steps-1, row t at R + t*N
     const int64_t* perm() const { return perm_.get(); } // position -> column (global when sharded)
     const int64_t* piv() const { return piv_.get(); }   // step -> local column (-1: other rank)
@@ -89,7 +89,10 @@ private:
     void grow(int64_t cap);
     void step();
     void reflect_step(int64_t t);
+    void explicit_step(int64_t t);
+    void to_explicit(int64_t t);
     void gemv_step(int64_t t);
+    double* qptr() { return explicit_ ? Qx_.get() : Qt_.get(); }
 
     const double* W_;
     int64_t k_, N_, ld_, p_;
@@ -101,6 +104,8 @@ private:
     DevBuf<double> nu_, cref_, R_, diag_, beta_, mass_;
     DevBuf<double> Y_, T_, Qt_, wv_, yv_, part_, vecs_, kpart_;  // WY state and scratch
     DevBuf<double> rec_, recs_;  // sharded: this rank's pivot record, all ranks' records
+    bool explicit_ = false;      // explicit k x k Q (long factorisations)
+    DevBuf<double> Qx_, exz_;
     DevBuf<int64_t> pos_, perm_, piv_, flags_;
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;

@@ -523,6 +523,112 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
     for (int64_t r = threadIdx.x; r <= t; r += kThreads) s.T[r + t * s.cap] = ls.T[r + t * tp];
 }
 
+// ---- explicit-Q mode (long factorisations, t comparable to k) ----------------------------
+// The compact WY form costs O(k t + t^2) per step, which dominates once t approaches k
+// (config 4's near-full-rank cuts). Past a threshold the engine switches to the explicit
+// k x k factor Qx = Q_t (formed once from Y, T with two DMMA GEMMs) and applies each
+// reflector as a rank-1 update of its trailing columns: y = Qx[:, t:]^T w,
+// Qx[:, t:] -= beta (Qx[:, t:] v) v^T. Columns < t never change, so Qx[:, :s] stays the
+// economy Q and column t is q_t for the stream.
+__global__ void __launch_bounds__(kThreads) k_ex_pick(WY s, int64_t t) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ int64_t jps;
+    Cand best = cand_none();
+    for (int i = threadIdx.x; i < s.ncand; i += kThreads)
+        if (better(s.cand[i], best)) best = s.cand[i];
+    best = block_best(best, sc);
+    if (threadIdx.x == 0) {
+        const bool none = best.col < 0;
+        const int64_t jp = none ? s.perm[t] : best.col;
+        const int64_t pp = none ? t : best.pos;
+        const int64_t ct = s.perm[t];
+        s.perm[t] = jp;
+        s.perm[pp] = ct;
+        s.pos[jp] = t;
+        s.pos[ct] = pp;
+        s.piv[t] = jp;
+        *s.nflag = 0;
+        jps = jp;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < s.k; i += kThreads) s.wv[i] = ld_w(s.W, s.ld, s.layout, i, jps);
+}
+
+// y_j = Qx[:, j]^T w for j >= t (warp per column, lanes over rows).
+__global__ void __launch_bounds__(kThreads) k_ex_y(const double* __restrict__ Qx, int64_t k, int64_t t,
+                                                   const double* __restrict__ w, double* y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t j = t + (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); j < k; j += nw) {
+        const double* q = Qx + j * k;
+        double a = 0.0;
+        for (int64_t i = lane; i < k; i += 32) a = fma(q[i], w[i], a);
+        a = warp_sum(a);
+        if (lane == 0) y[j] = a;
+    }
+}
+
+// Reflector from y[t:] (make_householder, factor.cpp:24-38); v overwrites y (v_t = 1).
+__global__ void __launch_bounds__(kThreads) k_ex_reflect(double* y, int64_t k, int64_t t, double* diag, double* betas,
+                                                         double* scal) {
+    __shared__ double red[kThreads / 32];
+    __shared__ double sh[2];
+    double sg = 0.0;
+    for (int64_t i = t + 1 + threadIdx.x; i < k; i += kThreads) sg = fma(y[i], y[i], sg);
+    sg = block_sum(sg, red);
+    if (threadIdx.x == 0) {
+        const double alpha = y[t];
+        double beta = 0.0, v0 = 1.0, rkk = alpha;
+        if (k - t > 1 && sg != 0.0) {
+            const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sg));
+            const double smu = copysign(mu, alpha);
+            v0 = __dadd_rn(alpha, smu);
+            beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+            rkk = -smu;
+        }
+        diag[t] = rkk;
+        betas[t] = beta;
+        scal[0] = beta;
+        sh[0] = v0;
+        sh[1] = beta;
+    }
+    __syncthreads();
+    const double v0 = sh[0], beta = sh[1];
+    for (int64_t i = t + threadIdx.x; i < k; i += kThreads)
+        y[i] = i == t ? 1.0 : (beta == 0.0 ? 0.0 : __ddiv_rn(y[i], v0));
+}
+
+// Partial z_i = sum_{j in chunk} Qx(i, j) v_j; grid (row blocks, column chunks).
+__global__ void __launch_bounds__(kThreads) k_ex_z(const double* __restrict__ Qx, int64_t k, int64_t t,
+                                                   const double* __restrict__ v, int64_t cw, double* zpart) {
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= k) return;
+    const int64_t j0 = t + (int64_t)blockIdx.y * cw, j1 = min(k, j0 + cw);
+    double a = 0.0;
+#pragma unroll 4
+    for (int64_t j = j0; j < j1; ++j) a = fma(Qx[i + j * k], v[j], a);
+    zpart[(int64_t)blockIdx.y * k + i] = a;
+}
+
+// Qx(i, j) -= beta z_i v_j over the chunk, z_i summed over the chunks in order.
+__global__ void __launch_bounds__(kThreads) k_ex_upd(double* Qx, int64_t k, int64_t t, const double* __restrict__ v,
+                                                     int64_t cw, int nchk, const double* zpart, const double* scal) {
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= k) return;
+    double z = 0.0;
+    for (int c = 0; c < nchk; ++c) z += zpart[(int64_t)c * k + i];
+    z *= scal[0];
+    const int64_t j0 = t + (int64_t)blockIdx.y * cw, j1 = min(k, j0 + cw);
+#pragma unroll 4
+    for (int64_t j = j0; j < j1; ++j) Qx[i + j * k] = fma(-z, v[j], Qx[i + j * k]);
+}
+
+__global__ void k_set_identity(double* Qx, int64_t k) {
+    const int64_t n = k * k;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        Qx[e] = (e % (k + 1)) == 0 ? 1.0 : 0.0;
+}
+
 // Multi-CTA phases (row chunks) and the small single-CTA glue between them.
 __global__ void __launch_bounds__(kThreads) k_wy_pick(WY s, int64_t t) { wy_pick(s, t, blockIdx.x, blockIdx.x == 0); }
 __global__ void __launch_bounds__(kThreads) k_wy_pick_shard(WY s, int64_t t) {
@@ -1352,6 +1458,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
 void WideQrcp::grow(int64_t cap) {
     if (cap <= cap_) return;
     DevBuf<double> nr(cap * N_), ny(k_ * cap), nq(k_ * cap), nt(cap * cap);
+    nt.zero();  // T is upper triangular; the strictly lower part must read as zero (to_explicit)
     if (steps_ > 0) {
         TTG_CUDA(cudaMemcpyAsync(nr.get(), R_.get(), sizeof(double) * steps_ * N_, cudaMemcpyDeviceToDevice, stream()));
         TTG_CUDA(cudaMemcpyAsync(ny.get(), Y_.get(), sizeof(double) * k_ * steps_, cudaMemcpyDeviceToDevice, stream()));
@@ -1384,7 +1491,7 @@ double WideQrcp::refresh_exact() {
         if (layout_ == Layout::Col) {
             const size_t rsm = sizeof(double) * (kThreads / 32) * 32 * 32;
             allow_smem(k_refresh_col, rsm);
-            TTG_LAUNCH(k_refresh_col, ncand_ + ngc_, kThreads, rsm, stream(), W_, k_, N_, ld_, s, Qt_.get(),
+            TTG_LAUNCH(k_refresh_col, ncand_ + ngc_, kThreads, rsm, stream(), W_, k_, N_, ld_, s, qptr(),
                        R_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get(), mass_.get());
         } else {
             const int S = s <= 8 ? 8 : s <= 16 ? 16 : 32;
@@ -1392,7 +1499,7 @@ double WideQrcp::refresh_exact() {
                                 : (S == 8 ? k_refresh_rowt<8> : S == 16 ? k_refresh_rowt<16> : k_refresh_rowt<32>);
             const size_t sm = sizeof(double) * (size_t)(k_ * S);
             allow_smem(kern, sm);
-            TTG_LAUNCH(kern, ncand_ + ngc_, kThreads, sm, stream(), W_, k_, N_, ld_, s, Qt_.get(), R_.get(),
+            TTG_LAUNCH(kern, ncand_ + ngc_, kThreads, sm, stream(), W_, k_, N_, ld_, s, qptr(), R_.get(),
                        nu_.get(), cref_.get(), pos_.get(), cand_.get(), mass_.get());
         }
         // (one CTA per candidate slot, the guard's slots included: no clearing needed)
@@ -1403,12 +1510,12 @@ double WideQrcp::refresh_exact() {
         TTG_CUDA(cudaMemcpy2DAsync(Yr.get(), sizeof(double) * k_, W_, sizeof(double) * ld_, sizeof(double) * k_, N_,
                                    cudaMemcpyDeviceToDevice, stream()));
         // Yr (k x N) -= Q[:, :s] * C with C(t, j) = R[t*N + j], i.e. C = (N x s col-major)^T
-        gemm(false, true, k_, N_, s, Qt_.get(), k_, R_.get(), N_, Yr.get(), k_, -1.0, 1.0);
+        gemm(false, true, k_, N_, s, qptr(), k_, R_.get(), N_, Yr.get(), k_, -1.0, 1.0);
     } else {
         TTG_CUDA(cudaMemcpy2DAsync(Yr.get(), sizeof(double) * N_, W_, sizeof(double) * ld_, sizeof(double) * N_, k_,
                                    cudaMemcpyDeviceToDevice, stream()));
         // Yr^T (N x k) -= C^T (N x s) * Q[:, :s]^T
-        gemm(false, true, N_, k_, s, R_.get(), N_, Qt_.get(), k_, Yr.get(), N_, -1.0, 1.0);
+        gemm(false, true, N_, k_, s, R_.get(), N_, qptr(), k_, Yr.get(), N_, -1.0, 1.0);
     }
     TTG_LAUNCH(k_resnorm, ncand_, kThreads, 0, stream(), Yr.get(), k_, N_, (int)layout_, s, nu_.get(), cref_.get(),
                pos_.get(), cand_.get(), mass_.get());
@@ -1424,9 +1531,43 @@ void WideQrcp::run_to(int64_t steps) {
 
 void WideQrcp::step() {
     const int64_t t = steps_;
-    reflect_step(t);
+    // explicit Q once t is large enough that O(t^2) WY work beats a k x k rank-1 update
+    if (!explicit_ && !comm_ && t >= 256 && k_ <= 8192 && 2 * t >= k_ / 4) to_explicit(t);
+    if (explicit_) explicit_step(t);
+    else reflect_step(t);
     gemv_step(t);
     steps_ = t + 1;
+}
+
+void WideQrcp::to_explicit(int64_t t) {
+    Qx_.alloc((size_t)(k_ * k_));
+    TTG_LAUNCH(k_set_identity, std::min<int64_t>(cdiv(k_ * k_, 256), 8 * sm_count()), 256, 0, stream(), Qx_.get(),
+               k_);
+    // Qx = I - Y T Y^T (M = T Y^T is t x k), then columns < t are the stored q exactly
+    DevBuf<double> M((size_t)(t * k_));
+    gemm(false, true, t, k_, t, T_.get(), cap_, Y_.get(), k_, M.get(), t);
+    gemm(false, false, k_, k_, t, Y_.get(), k_, M.get(), t, Qx_.get(), k_, -1.0, 1.0);
+    TTG_CUDA(cudaMemcpyAsync(Qx_.get(), Qt_.get(), sizeof(double) * (size_t)(k_ * t), cudaMemcpyDeviceToDevice,
+                             stream()));
+    exz_.alloc((size_t)k_ * 64);
+    explicit_ = true;
+}
+
+void WideQrcp::explicit_step(int64_t t) {
+    WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
+         vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
+         ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_};
+    TTG_LAUNCH(k_ex_pick, 1, kThreads, 0, stream(), s, t);
+    const int64_t nw = cdiv(k_ - t, kThreads / 32);
+    TTG_LAUNCH(k_ex_y, (int)std::min<int64_t>(nw, 8 * sm_count()), kThreads, 0, stream(), Qx_.get(), k_, t,
+               wv_.get(), yv_.get());
+    TTG_LAUNCH(k_ex_reflect, 1, kThreads, 0, stream(), yv_.get(), k_, t, diag_.get(), beta_.get(), vecs_.get());
+    const int64_t rb = cdiv(k_, kThreads);
+    const int nchk = (int)std::max<int64_t>(1, std::min<int64_t>(64, cdiv(4 * sm_count(), rb)));
+    const int64_t cw = cdiv(k_ - t, nchk);
+    const dim3 g((unsigned)rb, (unsigned)nchk);
+    TTG_LAUNCH(k_ex_z, g, kThreads, 0, stream(), Qx_.get(), k_, t, yv_.get(), cw, exz_.get());
+    TTG_LAUNCH(k_ex_upd, g, kThreads, 0, stream(), Qx_.get(), k_, t, yv_.get(), cw, nchk, exz_.get(), vecs_.get());
 }
 
 void WideQrcp::reflect_step(int64_t t) {
@@ -1467,7 +1608,7 @@ void WideQrcp::gemv_step(int64_t t) {
     prof_begin();
     if (mode_ == 4) {
         const dim3 g((unsigned)cdiv(N_, 32), (unsigned)ksplit_);
-        TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, Qt_.get() + t * k_, 0, cdiv(k_, ksplit_),
+        TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, qptr() + t * k_, 0, cdiv(k_, ksplit_),
                    kpart_.get());
         TTG_LAUNCH(k_stream_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, t, diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
@@ -1475,7 +1616,7 @@ void WideQrcp::gemv_step(int64_t t) {
         const size_t smem = sizeof(double) * (size_t)kTmaStages * kTmaCols * (size_t)(k_ + 3);
         auto kern = layout_ == Layout::Col ? k_stream_tma<0> : k_stream_tma<1>;
         allow_smem(kern, smem);
-        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Qt_.get(), diag_.get(), piv_.get(),
+        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
     } else {
         const size_t qbytes = sizeof(double) * ((k_ + 1) & ~int64_t(1));
@@ -1486,7 +1627,7 @@ void WideQrcp::gemv_step(int64_t t) {
                     : mode_ == 2 ? (k_ <= 32 ? k_stream_c32<1> : k_stream_c32<2>)
                                  : k_stream_splitk;
         allow_smem(kern, smem);
-        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, Qt_.get(), diag_.get(), piv_.get(),
+        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
     }
     // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
@@ -1496,14 +1637,14 @@ void WideQrcp::gemv_step(int64_t t) {
     // the stream kernel's
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
     if (k_ <= 32) {
-        TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, Qt_.get(),
+        TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get() + ncand_,
                    mass_.get() + ncand_);
     } else {
         // Q[:, :t+1] staged in shared memory when it fits (<= 96 KB)
         const bool stage = gq <= 96 * 1024;
         allow_smem(k_guard, stage ? gq : 0);
-        TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, Qt_.get(),
+        TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), stage ? 1 : 0, pos_.get(),
                    cand_.get() + ncand_, mass_.get() + ncand_);
     }

@@ -52,6 +52,21 @@ __global__ void k_gather_b(const double* __restrict__ R, const int64_t* __restri
     B[i + c * N] = R[c * N + perm[i]];
 }
 
+// R2 over positions (s x s, col-major): R2(t, q) = R(t, piv[q]) for q >= t (row t of the
+// wide engine's R at R + t*s), zero below the diagonal.
+__global__ void k_r2_positions(const double* __restrict__ R, const int64_t* __restrict__ piv, int64_t s,
+                               double* R2) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= s * s) return;
+    const int64_t q = e / s, t = e - q * s;
+    R2[e] = q >= t ? R[t * s + piv[q]] : 0.0;
+}
+
+__global__ void k_sq_diag(const double* __restrict__ d, int64_t s, double* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s) out[i] = d[i] * d[i];
+}
+
 // kept[0] = 0, kept[c+1] = kept[c] + sum_{i<=c} R2(i,c)^2, sequential sums without
 // contraction (kept_mass_upper / kept_mass_lower of factor.cpp:479-499).
 __global__ void k_kept(const double* __restrict__ R2, int64_t s, int64_t ldr, double* colmass, double* kept) {
@@ -290,6 +305,18 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
     } else {
         if (e1.sharded())
             invariant_error("sharded pass 2 supports at most " + std::to_string(160) + " pass-1 steps per cut");
+        if (N <= 8192) {
+            // B = R1[:s, :]^T read in place (column c of B = row c of R1): the read-only engine,
+            // which switches to an explicit Q for these long factorisations
+            WideQrcp e2(e1.R(), N, s, N, Layout::Col, s);
+            e2.run_to(s);
+            TTG_LAUNCH(k_r2_positions, (int)cdiv(s * s, 256), 256, 0, stream(), e2.R(), e2.piv(), s, R2.get());
+            TTG_LAUNCH(k_sq_diag, (int)cdiv(s, 256), 256, 0, stream(), e2.diag(), s, pn.get());
+            TTG_CUDA(cudaMemcpyAsync(out.perm.get(), e2.piv(), sizeof(int64_t) * s, cudaMemcpyDeviceToDevice,
+                                     stream()));
+            goto kept;
+        }
+        {
         DevBuf<double> B((size_t)N * s);
         TTG_LAUNCH(k_gather_b, (int)cdiv(N * s, 256), 256, 0, stream(), e1.R(), e1.perm(), N, s, B.get());
         TallQrcp e2(B.get(), N, s, N);
@@ -297,7 +324,9 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
         e2.extract_r(R2.get(), s);
         TTG_CUDA(cudaMemcpyAsync(pn.get(), e2.pivot_norm2(), sizeof(double) * s, cudaMemcpyDeviceToDevice, stream()));
         TTG_CUDA(cudaMemcpyAsync(out.perm.get(), e2.perm(), sizeof(int64_t) * s, cudaMemcpyDeviceToDevice, stream()));
+        }
     }
+kept:
     TTG_LAUNCH(k_kept, 1, 256, 0, stream(), R2.get(), s, s, colmass.get(), kept.get());
     out.kept.resize((size_t)s + 1);
     out.colmass.resize((size_t)s);
@@ -325,8 +354,17 @@ CutOut run_cut(Pass1& e1, const CutRequest& req) {
         s = std::min(p, std::max(2 * s, s + 8));
         ++out.extensions;
     };
+    auto phase = [&](const char* what, Clock::time_point t0) {
+        if (!cut_timing()) return;
+        sync();
+        std::fprintf(stderr, "[ttg]   %s (s=%lld): %.3f ms\n", what, (long long)s,
+                     std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+    };
     for (;;) {
+        auto tp = Clock::now();
         e1.run_to(s);
+        phase("pass 1", tp);
+        tp = Clock::now();
         // Trailing mass of pass 1 = total mass of the R1 rows not yet computed. Tolerance
         // mode needs it exactly (the rank rule works at the budget^2 level, far below the
         // rounding noise of downdated norms), fixed rank only for the validity bound.
@@ -344,7 +382,10 @@ CutOut run_cut(Pass1& e1, const CutRequest& req) {
             extend();
             continue;
         }
+        phase("trailing mass", tp);
+        tp = Clock::now();
         Pass2 p2 = run_pass2(e1, s);
+        phase("pass 2", tp);
         const std::vector<double>& hk = p2.kept;
         // total = kept[p] of the full factorisation = |R1[:s]|^2 + |R1[s:]|^2
         const double total = s == p ? hk[(size_t)s] : hk[(size_t)s] + t1;
