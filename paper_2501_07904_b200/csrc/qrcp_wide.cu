@@ -18,6 +18,7 @@
 // The WY phases cost O(k t) per step (one fused CTA when k (t+1) is small, otherwise
 // multi-CTA row chunks with fixed-order reductions), so k may be large (tall W).
 #include <cmath>
+#include <cstdlib>
 
 #include "engine.hpp"
 
@@ -1635,6 +1636,11 @@ void WideQrcp::gemv_step(int64_t t) {
     prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
     // guard recompute of the flagged norms; its candidates / masses go to the slots after
     // the stream kernel's
+    static const bool no_guard = [] {  // diagnostics only: skip the recompute (wrong results)
+        const char* e = std::getenv("TTG_DIAG_NO_GUARD");
+        return e && *e == '1';
+    }();
+    if (no_guard) return;
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
     if (k_ <= 32) {
         TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
