@@ -20,10 +20,19 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// Split-K: blockIdx.y selects the K chunk [y kc, (y+1) kc); chunk y writes its partial
+// product to C + y * cstride (beta must be 0 then). kc = k, cstride = 0 for a plain GEMM.
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) k_gemm(int64_t m, int64_t n, int64_t k, const double* __restrict__ A,
                                               int64_t lda, const double* __restrict__ B, int64_t ldb, double* C,
-                                              int64_t ldc, double alpha, double beta) {
+                                              int64_t ldc, double alpha, double beta, int64_t kc, int64_t cstride) {
+    {
+        const int64_t kb = (int64_t)blockIdx.y * kc;
+        k = min(kc, k - kb);
+        A += TA ? kb : kb * lda;
+        B += TB ? kb * ldb : kb;
+        C += (int64_t)blockIdx.y * cstride;
+    }
     __shared__ double As[BK][BM + 1];
     __shared__ double Bs[BK][BN + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -157,6 +166,19 @@ double reduce_sq(const double* x, const double* y, int64_t n) {
     return out.to_host(1)[0];
 }
 
+// C = sum_c part[c] (+ beta C), chunks in order.
+__global__ void k_reduce_chunks(const double* __restrict__ part, int64_t ks, int64_t m, int64_t n, double* C,
+                                int64_t ldc, double beta) {
+    const int64_t mn = m * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int64_t c = 0; c < ks; ++c) a += part[c * mn + e];
+        const int64_t j = e / m, i = e - j * m;
+        double* cp = C + i + j * ldc;
+        *cp = beta == 0.0 ? a : fma(beta, *cp, a);
+    }
+}
+
 }  // namespace
 
 void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
@@ -164,11 +186,26 @@ void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, in
     if (m <= 0 || n <= 0) return;
     const int64_t tiles = cdiv(m, BM) * cdiv(n, BN);
     if (tiles > INT32_MAX) argument_error("gemm: problem too large for one launch");
-    const unsigned grid = (unsigned)tiles;
-    if (!ta && !tb) TTG_LAUNCH((k_gemm<false, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
-    else if (ta && !tb) TTG_LAUNCH((k_gemm<true, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
-    else if (!ta && tb) TTG_LAUNCH((k_gemm<false, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
-    else TTG_LAUNCH((k_gemm<true, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+    auto launch = [&](dim3 grid, double* Cp, int64_t ldcp, double al, double be, int64_t kc, int64_t cs) {
+        if (!ta && !tb) TTG_LAUNCH((k_gemm<false, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+        else if (ta && !tb) TTG_LAUNCH((k_gemm<true, false>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+        else if (!ta && tb) TTG_LAUNCH((k_gemm<false, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+        else TTG_LAUNCH((k_gemm<true, true>), grid, 128, 0, stream(), m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+    };
+    const int sms = sm_count();
+    if (tiles < sms && k >= 8192) {
+        // few output tiles, long K (Gram matrices of tall blocks): split K over the SMs,
+        // partials reduced in chunk order (deterministic)
+        int64_t ks = std::min<int64_t>(cdiv(2 * sms, tiles), cdiv(k, 2048));
+        const int64_t kc = cdiv(cdiv(k, ks), BK) * BK;
+        ks = cdiv(k, kc);
+        DevBuf<double> part((size_t)(ks * m * n));
+        launch(dim3((unsigned)tiles, (unsigned)ks), part.get(), m, alpha, 0.0, kc, m * n);
+        TTG_LAUNCH(k_reduce_chunks, (int)std::min<int64_t>(cdiv(m * n, 256), 8 * sms), 256, 0, stream(), part.get(),
+                   ks, m, n, C, ldc, beta);
+        return;
+    }
+    launch(dim3((unsigned)tiles), C, ldc, alpha, beta, k, 0);
 }
 
 void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb) {

@@ -157,6 +157,10 @@ private:
 // R factor (s x s, upper, col-major ld = s) of the N x s matrix B (column t at B + t*ld),
 // by a Householder TSQR tree in shared memory (one HBM pass over B). Requires tsqr_fits(s).
 bool tsqr_fits(int64_t s);
+// Upper Cholesky factor R (G = R^T R) of an s x s Gram matrix, one CTA (s^2 doubles of
+// shared memory). Returns false (R unusable) unless G is numerically positive definite
+// with min R_ii >= min_ratio * max R_ii (host sync).
+bool cholesky_r(const double* G, int64_t s, double min_ratio, double* R);
 void tsqr_r(const double* B, int64_t N, int64_t s, int64_t ld, double* Rout);
 // One-CTA qr_col_pivot of a matrix that fits in shared memory (small_qrcp_fits): the
 // reference algorithm step for step. perm[n], R (p x n over positions, ld = p), pnorm[p]

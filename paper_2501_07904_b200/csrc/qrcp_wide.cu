@@ -943,6 +943,58 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream_tma(const double* __rest
     if (tid == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// MODE 6 (Row layout, wide, ld even, 16-byte aligned): a thread owns two adjacent columns
+// and reads both with one 16-byte load per row (512-byte segments per warp instruction),
+// q_t staged in shared memory. Each column's arithmetic is k_stream<0>'s (sequential over
+// the rows), so results are bitwise those of MODE 0.
+__global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restrict__ W, int64_t k, int64_t N,
+                                                          int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                          const double* diag, const int64_t* piv, double* R,
+                                                          double* nu, const double* cref, const int64_t* pos,
+                                                          int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    extern __shared__ double q[];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    for (int64_t i = threadIdx.x; i < k; i += kThreads) q[i] = Q[i + t * k];
+    __syncthreads();
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int64_t npair = (N + 1) / 2;
+    for (int64_t p0 = (int64_t)blockIdx.x * kThreads; p0 < npair; p0 += (int64_t)gridDim.x * kThreads) {
+        const int64_t pr = p0 + threadIdx.x;
+        const int64_t j = 2 * pr;
+        double a0 = 0.0, a1 = 0.0;
+        if (j + 1 < N) {
+            const double2* w = reinterpret_cast<const double2*>(W + j);
+            const int64_t ld2 = ld / 2;
+#pragma unroll 8
+            for (int64_t i = 0; i < k; ++i) {
+                const double2 x = __ldg(w + i * ld2);
+                a0 = fma(q[i], x.x, a0);
+                a1 = fma(q[i], x.y, a1);
+            }
+        } else if (j < N) {
+#pragma unroll 8
+            for (int64_t i = 0; i < k; ++i) a0 = fma(q[i], W[i * ld + j], a0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t jj = j + h;
+            const bool active = jj < N;
+            const int64_t pj = active ? pos[jj] : 0;
+            const bool chosen = active && (pj < t || jj == jp);
+            if (chosen) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
+            bool fl = false;
+            if (active && !chosen) fl = downdate(t, jj, N, h ? a1 : a0, pj, R, nu, cref, best, msum);
+            append_flag(fl, jj, flags, nflag);
+        }
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 // MODE 3: a CTA owns 32 columns; its 8 warps split the k rows (each row read as a
 // coalesced 256-byte segment); partials combined in warp order in smem.
 __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __restrict__ W, int64_t k, int64_t N,
@@ -1418,11 +1470,11 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         // even 32-column groups cannot fill the GPU (MODE 4)
         mode_ = cdiv(N, 32) < 2 * sms && k >= 8192 ? 4 : 3;
     } else {
-        mode_ = 0;
+        mode_ = aligned16 && ld % 2 == 0 && k <= kQSmem ? 6 : 0;
     }
     if (mode_ == 4) ksplit_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 2048), cdiv(4 * sms, cdiv(N, 32))));
     const int per_sm = 8;
-    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : cdiv(N, kThreads);
+    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 2 * kThreads) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
@@ -1613,6 +1665,12 @@ void WideQrcp::gemv_step(int64_t t) {
                    kpart_.get());
         TTG_LAUNCH(k_stream_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, t, diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    } else if (mode_ == 6) {
+        const size_t smem = sizeof(double) * (size_t)k_;
+        allow_smem(k_stream_row2, smem);
+        TTG_LAUNCH(k_stream_row2, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(),
+                   piv_.get(), R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(),
+                   mass_.get());
     } else if (mode_ == 5) {
         const size_t smem = sizeof(double) * (size_t)kTmaStages * kTmaCols * (size_t)(k_ + 3);
         auto kern = layout_ == Layout::Col ? k_stream_tma<0> : k_stream_tma<1>;

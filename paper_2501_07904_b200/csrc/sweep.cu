@@ -52,6 +52,15 @@ __global__ void k_gather_b(const double* __restrict__ R, const int64_t* __restri
     B[i + c * N] = R[c * N + perm[i]];
 }
 
+// out[e] = sum_p in[p * n + e] in rank order (deterministic cross-rank sum).
+__global__ void k_sum_blocks(const double* __restrict__ in, int P, int64_t n, double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double a = 0.0;
+    for (int p = 0; p < P; ++p) a += in[(int64_t)p * n + e];
+    out[e] = a;
+}
+
 // R2 over positions (s x s, col-major): R2(t, q) = R(t, piv[q]) for q >= t (row t of the
 // wide engine's R at R + t*s), zero below the diagonal.
 __global__ void k_r2_positions(const double* __restrict__ R, const int64_t* __restrict__ piv, int64_t s,
@@ -187,6 +196,8 @@ struct CutRequest {
 // Pass 1 of a cut behind one interface: the wide read-only engine (k moderate) or, when W
 // is tall (k >> N, e.g. the last URV cut of config 5: W = 131072 x 1024), the in-place
 // Householder engine on a column-major copy of W.
+bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB);
+
 struct Pass1 {
     virtual ~Pass1() = default;
     virtual int64_t p() const = 0;
@@ -200,8 +211,38 @@ struct Pass1 {
     virtual const double* Q() = 0;       // economy Q columns 0..s-1, leading dimension k
     virtual bool sharded() const { return false; }
     // R_B (s x s, ld s) of B = R1[:s, :]^T over all columns (all ranks when sharded).
-    virtual void r_factor(int64_t s, double* RB) { tsqr_r(R(), N(), s, N(), RB); }
+    virtual void r_factor(int64_t s, double* RB) {
+        if (!gram_r(R(), N(), s, nullptr, RB)) tsqr_r(R(), N(), s, N(), RB);
+    }
 };
+
+// R_B from the Gram matrix B^T B = R1 R1^T (one DMMA GEMM over the s x N rows of R1, summed
+// over the ranks in rank order when sharded) and its Cholesky factor. Only for s > 32 (the
+// register TSQR is fast below) and only when the factor is well conditioned: the error of
+// a Gram-based R is about eps * cond(B) relative to |T_00|, so min/max R_ii >= 1e-4 keeps
+// it far inside the 1e-10 parity tolerance. Otherwise the caller falls back to TSQR.
+bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB) {
+    constexpr double kMinRatio = 1e-4;
+    if (s <= 32 || (size_t)(s * s) * sizeof(double) > 200 * 1024) return false;
+    DevBuf<double> G((size_t)(s * s));
+    gemm(true, false, s, s, N, R1, N, R1, N, G.get(), s);
+    if (comm && comm->size() > 1) {
+        const int P = comm->size();
+        DevBuf<double> all((size_t)(P * s * s));
+        comm->allgather(G.get(), all.get(), sizeof(double) * (size_t)(s * s));
+        TTG_LAUNCH(k_sum_blocks, (int)cdiv(s * s, 256), 256, 0, stream(), all.get(), P, s * s, G.get());
+    }
+    const bool ok = cholesky_r(G.get(), s, kMinRatio, RB);
+    if (cut_timing()) {
+        std::vector<double> r((size_t)(s * s));
+        TTG_CUDA(cudaMemcpyAsync(r.data(), RB, sizeof(double) * s * s, cudaMemcpyDeviceToHost, stream()));
+        sync();
+        double mx = 0.0, mn = 1e300;
+        for (int64_t i = 0; i < s; ++i) { mx = std::max(mx, r[(size_t)(i + i * s)]); mn = std::min(mn, r[(size_t)(i + i * s)]); }
+        std::fprintf(stderr, "[ttg]   gram R_B (s=%lld): %s, min/max diag %.3e\n", (long long)s, ok ? "used" : "rejected", mn / mx);
+    }
+    return ok;
+}
 
 struct WidePass1 final : Pass1 {
     WideQrcp e;
@@ -212,6 +253,7 @@ struct WidePass1 final : Pass1 {
     // Sharded: every rank reduces its own rows of B to a triangle, the triangles are
     // all-gathered and stacked in rank order, and every rank factors the same stack.
     void r_factor(int64_t s, double* RB) override {
+        if (gram_r(e.R(), e.N(), s, e.comm(), RB)) return;
         if (!e.sharded()) return tsqr_r(e.R(), e.N(), s, e.N(), RB);
         Comm& comm = *e.comm();
         const int G = comm.size();

@@ -555,6 +555,60 @@ void small_qrcp(const double* A, int64_t m, int64_t n, int64_t lda, int64_t* per
 
 bool tsqr_fits(int64_t s) { return s <= 160; }
 
+namespace {
+// In-place Cholesky G = R^T R of an s x s SPD matrix (col-major, ld s) in shared memory,
+// one CTA; R written upper (zeros below). ok[0] = 1 when every pivot is positive and
+// min_i R_ii >= min_ratio * max_i R_ii.
+__global__ void __launch_bounds__(kT) k_cholesky(const double* __restrict__ G, int64_t s, double min_ratio, double* R,
+                                                 int* ok) {
+    extern __shared__ double A[];
+    __shared__ int bad;
+    for (int64_t e = threadIdx.x; e < s * s; e += kT) A[e] = G[e];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int64_t j = 0; j < s; ++j) {
+        // A(j, j..) -= sum_{k<j} A(k, j) A(k, ..) is already applied (right-looking)
+        if (threadIdx.x == 0) {
+            const double d = A[j + j * s];
+            if (!(d > 0.0)) bad = 1;
+            A[j + j * s] = d > 0.0 ? sqrt(d) : 0.0;
+        }
+        __syncthreads();
+        const double rjj = A[j + j * s];
+        for (int64_t i = j + 1 + threadIdx.x; i < s; i += kT) A[j + i * s] = rjj > 0.0 ? A[j + i * s] / rjj : 0.0;
+        __syncthreads();
+        // trailing update A(a, b) -= R(j, a) R(j, b) for j < a <= b
+        const int64_t m = s - j - 1;
+        for (int64_t e = threadIdx.x; e < m * m; e += kT) {
+            const int64_t b = j + 1 + e / m, a = j + 1 + e % m;
+            if (a <= b) A[a + b * s] = fma(-A[j + a * s], A[j + b * s], A[a + b * s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double mx = 0.0, mn = INFINITY;
+        for (int64_t i = 0; i < s; ++i) {
+            mx = fmax(mx, A[i + i * s]);
+            mn = fmin(mn, A[i + i * s]);
+        }
+        ok[0] = (!bad && mn >= min_ratio * mx) ? 1 : 0;
+    }
+    for (int64_t e = threadIdx.x; e < s * s; e += kT) {
+        const int64_t c = e / s, r = e - c * s;
+        R[e] = r <= c ? A[e] : 0.0;
+    }
+}
+}  // namespace
+
+bool cholesky_r(const double* G, int64_t s, double min_ratio, double* R) {
+    const size_t smem = sizeof(double) * (size_t)(s * s);
+    if (smem > 200 * 1024) return false;
+    DevBuf<int> ok(1);
+    allow_smem(k_cholesky, smem);
+    TTG_LAUNCH(k_cholesky, 1, kT, smem, stream(), G, s, min_ratio, R, ok.get());
+    return ok.to_host(1)[0] == 1;
+}
+
 // Leaf level with the unrolled kernel <S, RL> when it spans at least a wave, then the
 // rolled kernel <S, RU> up the tree.
 template <int S, int RL, int RU>

@@ -129,3 +129,11 @@ def test_nccl_world_of_one(dev, ref):
     one = dev.decompose_device(a, dims, "urv", "r2l", ranks=ranks)
     assert res.report().ranks_chosen == one.report().ranks_chosen
     assert abs(res.rse(a) - one.rse(a)) <= 1e-13
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_planted_rank48_gram_sharded(dev, ref, method):
+    # the Gram matrices of the ranks' R1 blocks are all-gathered and summed in rank order
+    dims, ranks = [64, 64, 64], [1, 48, 48, 1]
+    a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
+    _check(dev, ref, a, dims, method, 4, ranks=ranks)

@@ -197,3 +197,12 @@ def test_tall_pass1_engine(dev, ref, method):
     a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
     _, rep, *_ = _check_parity(dev, ref, a, dims, method, ranks=ranks)
     _check_parity(dev, ref, a, dims, method, eps=1e-4)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_planted_rank48_gram_pass2(dev, ref, method):
+    # 33 <= s <= 160 with a well-conditioned R1: pass 2 takes R_B from the Gram matrix
+    # (split-K DMMA GEMM + Cholesky) instead of the TSQR tree
+    dims, ranks = [64, 64, 64], [1, 48, 48, 1]
+    a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
+    _check_parity(dev, ref, a, dims, method, ranks=ranks)
