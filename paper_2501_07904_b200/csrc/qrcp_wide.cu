@@ -995,6 +995,70 @@ __global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restri
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// MODE 7 (Row layout, few columns, ld even, 16-byte aligned): MODE 3 with 128 columns
+// per CTA iteration, lane l holding columns 4l..4l+3 through two 16-byte loads per row
+// (1 KB contiguous per warp instruction, 8 rows in flight per warp). Rows split across the
+// 8 warps exactly as in MODE 3 and combined in warp order, so results are bitwise MODE 3's.
+__global__ void __launch_bounds__(kThreads) k_stream_splitk4(const double* __restrict__ W, int64_t k, int64_t N,
+                                                             int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                             const double* diag, const int64_t* piv, double* R,
+                                                             double* nu, const double* cref, const int64_t* pos,
+                                                             int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    __shared__ double part[kThreads / 32][129];
+    extern __shared__ double q[];
+    for (int64_t i = threadIdx.x; i < k; i += kThreads) q[i] = Q[i + t * k];
+    __syncthreads();
+    const int64_t jp = piv[t];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j0 = (int64_t)blockIdx.x * 128; j0 < N; j0 += (int64_t)gridDim.x * 128) {
+        const int64_t jl = j0 + 4 * lane;
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        if (jl + 3 < N) {
+            const double* base = W + jl;
+#pragma unroll 8
+            for (int64_t i = warp; i < k; i += kThreads / 32) {
+                const double2 x0 = __ldg(reinterpret_cast<const double2*>(base + i * ld));
+                const double2 x1 = __ldg(reinterpret_cast<const double2*>(base + i * ld) + 1);
+                const double qi = q[i];
+                a[0] = fma(qi, x0.x, a[0]);
+                a[1] = fma(qi, x0.y, a[1]);
+                a[2] = fma(qi, x1.x, a[2]);
+                a[3] = fma(qi, x1.y, a[3]);
+            }
+        } else {
+            for (int64_t i = warp; i < k; i += kThreads / 32)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (jl + c < N) a[c] = fma(q[i], W[i * ld + jl + c], a[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) part[warp][4 * lane + c] = a[c];
+        __syncthreads();
+        // 128 columns, 256 threads: threads 0..127 finish one column each
+        bool fl = false;
+        const int64_t j = j0 + threadIdx.x;
+        if (threadIdx.x < 128) {
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) sum += part[w][threadIdx.x];
+            const bool active = j < N;
+            const int64_t pj = active ? pos[j] : 0;
+            const bool chosen = active && (pj < t || j == jp);
+            if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
+            if (active && !chosen) fl = downdate(t, j, N, sum, pj, R, nu, cref, best, msum);
+        }
+        if (warp < 4) append_flag(fl, j, flags, nflag);
+        __syncthreads();
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 // MODE 3: a CTA owns 32 columns; its 8 warps split the k rows (each row read as a
 // coalesced 256-byte segment); partials combined in warp order in smem.
 __global__ void __launch_bounds__(kThreads) k_stream_splitk(const double* __restrict__ W, int64_t k, int64_t N,
@@ -1469,12 +1533,13 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         // few columns: split the rows inside a CTA (MODE 3), or also across CTAs when
         // even 32-column groups cannot fill the GPU (MODE 4)
         mode_ = cdiv(N, 32) < 2 * sms && k >= 8192 ? 4 : 3;
+        if (mode_ == 3 && aligned16 && ld % 2 == 0 && cdiv(N, 128) >= sms) mode_ = 7;  // wide rows
     } else {
         mode_ = aligned16 && ld % 2 == 0 && k <= kQSmem ? 6 : 0;
     }
     if (mode_ == 4) ksplit_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 2048), cdiv(4 * sms, cdiv(N, 32))));
     const int per_sm = 8;
-    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 2 * kThreads) : cdiv(N, kThreads);
+    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 7 ? cdiv(N, 128) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 2 * kThreads) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
@@ -1665,6 +1730,12 @@ void WideQrcp::gemv_step(int64_t t) {
                    kpart_.get());
         TTG_LAUNCH(k_stream_fin, ncand_, kThreads, 0, stream(), kpart_.get(), ksplit_, N_, t, diag_.get(), piv_.get(),
                    R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+    } else if (mode_ == 7) {
+        const size_t smem = sizeof(double) * (size_t)k_;
+        allow_smem(k_stream_splitk4, smem);
+        TTG_LAUNCH(k_stream_splitk4, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(),
+                   piv_.get(), R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(),
+                   mass_.get());
     } else if (mode_ == 6) {
         const size_t smem = sizeof(double) * (size_t)k_;
         allow_smem(k_stream_row2, smem);
