@@ -1525,7 +1525,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     const bool aligned16 = (reinterpret_cast<uintptr_t>(W) & 15) == 0;  // bulk copies need 16 B
     if (aligned16 && layout == Layout::Col && k <= 32 && ld == k) {
         mode_ = 5;  // TMA ring over contiguous 256-column blocks
-    } else if (aligned16 && layout == Layout::Row && k <= 32 && ld % 2 == 0) {
+    } else if (aligned16 && layout == Layout::Row && k <= 32 && ld % 2 == 0 && std::getenv("TTG_ROW_TMA")) {
         mode_ = 5;  // TMA ring over k row segments per 256-column block
     } else if (layout == Layout::Col) {
         mode_ = k <= 64 ? 2 : 1;
@@ -1776,8 +1776,8 @@ void WideQrcp::gemv_step(int64_t t) {
                    flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get() + ncand_,
                    mass_.get() + ncand_);
     } else {
-        // Q[:, :t+1] staged in shared memory when it fits (<= 96 KB)
-        const bool stage = gq <= 96 * 1024;
+        // Q[:, :t+1] staged in shared memory when it fits
+        const bool stage = gq <= 200 * 1024;
         allow_smem(k_guard, stage ? gq : 0);
         TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), stage ? 1 : 0, pos_.get(),
