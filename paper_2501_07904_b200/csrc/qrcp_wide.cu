@@ -960,35 +960,50 @@ __global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restri
     const int64_t jp = piv[t];
     Cand best = cand_none();
     double msum = 0.0;
+    // a warp covers 2 x 32 pairs = 128 columns as two 512-byte halves of one 1 KB row segment
     const int64_t npair = (N + 1) / 2;
-    for (int64_t p0 = (int64_t)blockIdx.x * kThreads; p0 < npair; p0 += (int64_t)gridDim.x * kThreads) {
-        const int64_t pr = p0 + threadIdx.x;
-        const int64_t j = 2 * pr;
-        double a0 = 0.0, a1 = 0.0;
-        if (j + 1 < N) {
-            const double2* w = reinterpret_cast<const double2*>(W + j);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t g0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 64; g0 < npair;
+         g0 += (int64_t)gridDim.x * (kThreads / 32) * 64) {
+        double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const int64_t pr0 = g0 + lane, pr1 = g0 + 32 + lane;
+        const bool full0 = 2 * pr0 + 1 < N, full1 = 2 * pr1 + 1 < N;
+        if (full0 && full1) {
+            const double2* w0 = reinterpret_cast<const double2*>(W) + pr0;
+            const double2* w1 = reinterpret_cast<const double2*>(W) + pr1;
             const int64_t ld2 = ld / 2;
 #pragma unroll 8
             for (int64_t i = 0; i < k; ++i) {
-                const double2 x = __ldg(w + i * ld2);
-                a0 = fma(q[i], x.x, a0);
-                a1 = fma(q[i], x.y, a1);
+                const double2 x0 = __ldg(w0 + i * ld2), x1 = __ldg(w1 + i * ld2);
+                const double qi = q[i];
+                a[0][0] = fma(qi, x0.x, a[0][0]);
+                a[0][1] = fma(qi, x0.y, a[0][1]);
+                a[1][0] = fma(qi, x1.x, a[1][0]);
+                a[1][1] = fma(qi, x1.y, a[1][1]);
             }
-        } else if (j < N) {
-#pragma unroll 8
-            for (int64_t i = 0; i < k; ++i) a0 = fma(q[i], W[i * ld + j], a0);
+        } else {
+            for (int64_t i = 0; i < k; ++i)
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                        if (jj < N) a[u][h] = fma(q[i], W[i * ld + jj], a[u][h]);
+                    }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t jj = j + h;
-            const bool active = jj < N;
-            const int64_t pj = active ? pos[jj] : 0;
-            const bool chosen = active && (pj < t || jj == jp);
-            if (chosen) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
-            bool fl = false;
-            if (active && !chosen) fl = downdate(t, jj, N, h ? a1 : a0, pj, R, nu, cref, best, msum);
-            append_flag(fl, jj, flags, nflag);
-        }
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                const bool active = jj < N;
+                const int64_t pj = active ? pos[jj] : 0;
+                const bool chosen = active && (pj < t || jj == jp);
+                if (chosen) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
+                bool fl = false;
+                if (active && !chosen) fl = downdate(t, jj, N, a[u][h], pj, R, nu, cref, best, msum);
+                append_flag(fl, jj, flags, nflag);
+            }
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sd);
@@ -1539,7 +1554,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     }
     if (mode_ == 4) ksplit_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 2048), cdiv(4 * sms, cdiv(N, 32))));
     const int per_sm = 8;
-    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 7 ? cdiv(N, 128) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 2 * kThreads) : cdiv(N, kThreads);
+    const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 7 ? cdiv(N, 128) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 4 * kThreads) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
