@@ -48,11 +48,13 @@ void check_sync(const char* kernel, const char* file, int line);
 
 // Opt a kernel into large dynamic shared memory. Static + dynamic may not exceed 48 KB
 // without the opt-in, so any request above 40 KB (kernels keep <= 8 KB static) opts in.
+// The attribute is process-wide: it is raised once to the device's opt-in maximum (minus
+// the kernel's static shared memory) and never lowered, so concurrent host threads
+// launching the same kernel with different sizes cannot undercut each other.
+void raise_smem_limit(const void* kernel);
 template <class K>
 inline void allow_smem(K* kernel, size_t bytes) {
-    if (bytes > 40 * 1024)
-        TTG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (bytes > 40 * 1024) raise_smem_limit(reinterpret_cast<const void*>(kernel));
 }
 
 // Stream of the calling host thread (created lazily on the current device).

@@ -1,5 +1,6 @@
 // Per-thread CUDA stream, device properties and the launch counter.
 #include <mutex>
+#include <vector>
 #include <atomic>
 #include <cstdlib>
 
@@ -110,6 +111,23 @@ int64_t prof_read(double* total_ms, double* bytes) {
     *bytes = t_prof.bytes;
     t_prof.bytes = 0.0;
     return n;
+}
+
+void raise_smem_limit(const void* kernel) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
+    int dev = 0;
+    TTG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& d : done)
+        if (d.first == kernel && d.second == dev) return;
+    int optin = 0;
+    TTG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    TTG_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    TTG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - (int)fa.sharedSizeBytes));
+    done.emplace_back(kernel, dev);
 }
 
 void ensure_pool(size_t bytes) {
