@@ -1211,23 +1211,59 @@ __device__ __forceinline__ void guard_out(Cand best, double msum, Cand* gcand, d
     if (threadIdx.x == 0) { gcand[blockIdx.x] = best; gmass[blockIdx.x] = msum; }
 }
 
+// Lazy guard. A flagged column can only matter for the next pivot if its true norm^2 can
+// reach the best unflagged candidate's (the stream slots). Norms only decrease, so the
+// value before this step's downdate, nu_j + R(t,j)^2, bounds it from above; if even that
+// is below the best candidate, the recompute is deferred: the column is marked stale
+// (cref = +inf, so every later downdate flags it again) and nu_j keeps the bound, which
+// stays an upper bound when the stream downdates it. A stale column is recomputed exactly
+// as soon as its bound reaches the best candidate, so every pivot is the one the eager
+// recompute (factor.cpp:103-105) would give; trailing masses count stale bounds (upper
+// bounds) and the exact refresh resets everything.
+__device__ __forceinline__ double best_stream_nu(const Cand* cand, int ncand) {
+    __shared__ Cand sc[kThreads / 32];
+    Cand b = cand_none();
+    for (int i = threadIdx.x; i < ncand; i += kThreads)
+        if (better(cand[i], b)) b = cand[i];
+    b = block_best(b, sc);
+    return b.col >= 0 ? b.nu : -1.0;
+}
+
+__device__ __forceinline__ bool guard_defer(int64_t j, int64_t t, int64_t N, const double* R, double* nu,
+                                            double* cref, double bestnu, double& mass) {
+    const double r = R[t * N + j];
+    const double nv = nu[j];
+    const bool stale = isinf(cref[j]);
+    const double bound = stale ? nv : __dadd_rn(nv, __dmul_rn(r, r));
+    if (bestnu > 0.0 && bound < bestnu * (1.0 - 1e-10)) {
+        nu[j] = bound;
+        cref[j] = INFINITY;
+        mass += fmax(bound, 0.0);
+        return true;
+    }
+    return false;
+}
+
 // k <= KM: one thread per flagged column, the column in registers, Q[:, :t+1] staged in
 // shared memory (broadcast reads), modified Gram-Schmidt residual.
 template <int KM>
 __global__ void __launch_bounds__(kThreads) k_guard_lane(const double* __restrict__ W, int64_t k, int64_t N,
                                                          int64_t ld, int layout, int64_t t,
-                                                         const double* __restrict__ Q, const int64_t* flags,
-                                                         const int* nflag, double* nu, double* cref,
-                                                         const int64_t* pos, Cand* gcand, double* gmass) {
+                                                         const double* __restrict__ Q, const double* R,
+                                                         const int64_t* flags, const int* nflag, double* nu,
+                                                         double* cref, const int64_t* pos, const Cand* scand,
+                                                         int nscand, Cand* gcand, double* gmass) {
     extern __shared__ double qs[];  // Q[:, :t+1]
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
     if (nf > 0) {
+        const double bestnu = best_stream_nu(scand, nscand);
         for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
         __syncthreads();
         for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
             const int64_t j = flags[f];
+            if (guard_defer(j, t, N, R, nu, cref, bestnu, msum)) continue;
             double x[KM];
 #pragma unroll
             for (int i = 0; i < KM; ++i) x[i] = i < k ? ld_w(W, ld, layout, i, j) : 0.0;
@@ -1259,14 +1295,15 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
                                                     int64_t ld, int layout, int64_t t,
                                                     const double* __restrict__ Q, const double* R,
                                                     const int64_t* flags, const int* nflag, double* nu,
-                                                    double* cref, int stage_q, const int64_t* pos, Cand* gcand,
-                                                    double* gmass) {
+                                                    double* cref, int stage_q, const int64_t* pos,
+                                                    const Cand* scand, int nscand, Cand* gcand, double* gmass) {
     extern __shared__ double qs[];  // Q[:, :t+1] when staged (dynamic smem > 0)
     __shared__ double rbuf[kThreads / 32][64];
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
     if (nf > 0) {
+        const double bestnu = best_stream_nu(scand, nscand);
         const bool staged = stage_q != 0;
         if (staged)
             for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
@@ -1277,6 +1314,12 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
         for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
              f += (int64_t)gridDim.x * (kThreads / 32)) {
             const int64_t j = flags[f];
+            double dm = 0.0;
+            const bool defer = lane == 0 && guard_defer(j, t, N, R, nu, cref, bestnu, dm);
+            if (__shfl_sync(0xffffffffu, (int)defer, 0)) {
+                if (lane == 0) msum += dm;
+                continue;
+            }
             if (rsm) {
                 for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = R[l * N + j];
                 __syncwarp();
@@ -1788,15 +1831,15 @@ void WideQrcp::gemv_step(int64_t t) {
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
     if (k_ <= 32) {
         TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
-                   flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get() + ncand_,
-                   mass_.get() + ncand_);
+                   R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get(), ncand_,
+                   cand_.get() + ncand_, mass_.get() + ncand_);
     } else {
         // Q[:, :t+1] staged in shared memory when it fits
         const bool stage = gq <= 200 * 1024;
         allow_smem(k_guard, stage ? gq : 0);
         TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), stage ? 1 : 0, pos_.get(),
-                   cand_.get() + ncand_, mass_.get() + ncand_);
+                   cand_.get(), ncand_, cand_.get() + ncand_, mass_.get() + ncand_);
     }
 }
 
