@@ -203,6 +203,7 @@ struct WY {
     const double* recs;
     int nrec;
     int64_t off, nloc;
+    int64_t tld;  // leading dimension of T (cap in global memory; odd in shared memory)
 };
 
 // Sharded pivot record: [0] kind (0 none, 1 candidate, 2 the column at position t when no
@@ -351,7 +352,7 @@ __device__ void wy_u(const WY& s, int64_t t, int64_t first, int64_t stride) {
     double* u = s.vec + s.cap;
     for (int64_t r = first; r < t; r += stride) {
         double a = 0.0;
-        for (int64_t l = 0; l <= r; ++l) a = fma(s.T[l + r * s.cap], z[l], a);
+        for (int64_t l = 0; l <= r; ++l) a = fma(s.T[l + r * s.tld], z[l], a);
         u[r] = a;
     }
 }
@@ -424,8 +425,8 @@ __device__ void wy_tcol(const WY& s, int64_t t, int64_t first, int64_t stride) {
     for (int64_t r = first; r <= t; r += stride) {
         double a = 0.0;
         if (r < t)
-            for (int64_t c = r; c < t; ++c) a = fma(s.T[r + c * s.cap], p[c], a);
-        s.T[r + t * s.cap] = r == t ? beta : -beta * a;
+            for (int64_t c = r; c < t; ++c) a = fma(s.T[r + c * s.tld], p[c], a);
+        s.T[r + t * s.tld] = r == t ? beta : -beta * a;
     }
 }
 
@@ -433,7 +434,7 @@ __device__ void wy_g(const WY& s, int64_t t, int64_t first, int64_t stride) {
     double* g = s.vec + 3 * s.cap;
     for (int64_t r = first; r <= t; r += stride) {
         double a = 0.0;
-        for (int64_t c = r; c <= t; ++c) a = fma(s.T[r + c * s.cap], s.Y[t + c * s.k], a);
+        for (int64_t c = r; c <= t; ++c) a = fma(s.T[r + c * s.tld], s.Y[t + c * s.k], a);
         g[r] = a;
     }
 }
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
 // whose T / vector / scratch pointers are the shared copies (leading dimension t+1).
 size_t wy_smem_doubles(int64_t k, int64_t t) {
     const int64_t tp = t + 1;
-    return (size_t)(k * tp + tp * tp + 2 * k + (tp + 1) + 4 * tp + 2);
+    return (size_t)(k * tp + tp * (tp + 1) + 2 * k + (tp + 1) + 4 * tp + 2);
 }
 
 template <bool SH>
@@ -490,16 +491,17 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
     const int64_t k = s.k, tp = t + 1;
     WY ls = s;
     ls.cap = tp;
+    ls.tld = tp | 1;  // odd stride: the column-wise T reads of wy_u are bank-conflict free
     ls.Y = wsm;
     ls.T = ls.Y + k * tp;
-    ls.wv = ls.T + tp * tp;
+    ls.wv = ls.T + tp * (tp + 1);
     ls.yv = ls.wv + k;
     ls.part = ls.yv + k;
     ls.vec = ls.part + (tp + 1);
     for (int64_t e = threadIdx.x; e < k * t; e += kThreads) ls.Y[e] = s.Y[e];
     for (int64_t e = threadIdx.x; e < t * t; e += kThreads) {
         const int64_t c = e / t, r = e - c * t;
-        ls.T[r + c * tp] = s.T[r + c * s.cap];
+        ls.T[r + c * ls.tld] = s.T[r + c * s.cap];
     }
     __syncthreads();
     if (SH) wy_pick_shard(ls, t, 0, true);
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
     __syncthreads();
     wy_q(ls, t, 0);
     for (int64_t i = threadIdx.x; i < k; i += kThreads) s.Y[i + t * k] = ls.Y[i + t * k];
-    for (int64_t r = threadIdx.x; r <= t; r += kThreads) s.T[r + t * s.cap] = ls.T[r + t * tp];
+    for (int64_t r = threadIdx.x; r <= t; r += kThreads) s.T[r + t * s.cap] = ls.T[r + t * ls.tld];
 }
 
 // ---- explicit-Q mode (long factorisations, t comparable to k) ----------------------------
@@ -1732,7 +1734,7 @@ void WideQrcp::to_explicit(int64_t t) {
 void WideQrcp::explicit_step(int64_t t) {
     WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
          vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
-         ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_};
+         ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_, cap_};
     TTG_LAUNCH(k_ex_pick, 1, kThreads, 0, stream(), s, t);
     const int64_t nw = cdiv(k_ - t, kThreads / 32);
     TTG_LAUNCH(k_ex_y, (int)std::min<int64_t>(nw, 8 * sm_count()), kThreads, 0, stream(), Qx_.get(), k_, t,
@@ -1749,7 +1751,7 @@ void WideQrcp::explicit_step(int64_t t) {
 void WideQrcp::reflect_step(int64_t t) {
     WY s{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(), part_.get(),
          vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(), nflag_.get(), cand_.get(),
-         ncand_ + ngc_, 1, k_, recs_.get(), comm_ ? comm_->size() : 0, off_, N_};
+         ncand_ + ngc_, 1, k_, recs_.get(), comm_ ? comm_->size() : 0, off_, N_, cap_};
     if (comm_) {  // exchange the ranks' pivot records before the (replicated) reflector
         TTG_LAUNCH(k_shard_export, 1, kThreads, 0, stream(), s, t, rec_.get());
         comm_->allgather(rec_.get(), recs_.get(), sizeof(double) * (size_t)(k_ + kRecHead));
