@@ -316,6 +316,63 @@ struct TallPass1 final : Pass1 {
     }
 };
 
+// Small W (fits one CTA's shared memory): the whole pass 1 is the reference's
+// qr_col_pivot run step for step by one CTA (k_small_qrcp), one launch instead of a few
+// launches per step; every prefix s of the full factorisation is what the early exit
+// asks for, and the trailing mass of rows s.. is exact.
+__global__ void k_scatter_rows(const double* __restrict__ Rpos, const int64_t* __restrict__ perm, int64_t p,
+                               int64_t N, double* Rrow) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= p * N) return;
+    const int64_t q = e / p, t = e - q * p;
+    Rrow[t * N + perm[q]] = Rpos[t + q * p];
+}
+
+struct SmemPass1 final : Pass1 {
+    int64_t k_, N_, p_;
+    DevBuf<double> Wc, Rpos, Rrow, Qb, pn;
+    DevBuf<int64_t> permb;
+    std::vector<double> rowmass;  // |R row t|^2 over positions
+    SmemPass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l) : k_(k), N_(N), p_(std::min(k, N)) {
+        const double* A = W;
+        int64_t lda = ld;
+        if (l == Layout::Row) {  // W(i, j) = W[i*ld + j]: make the k x N column-major copy
+            Wc.alloc((size_t)(k * N));
+            transpose(W, N, k, ld, Wc.get(), k);
+            A = Wc.get();
+            lda = k;
+        }
+        Rpos.alloc((size_t)(p_ * N));
+        Rrow.alloc((size_t)(p_ * N));
+        Qb.alloc((size_t)(k * p_));
+        pn.alloc((size_t)p_);
+        permb.alloc((size_t)N);
+        small_qrcp(A, k, N, lda, permb.get(), Rpos.get(), pn.get(), Qb.get());
+        TTG_LAUNCH(k_scatter_rows, (int)cdiv(p_ * N, 256), 256, 0, stream(), Rpos.get(), permb.get(), p_, N,
+                   Rrow.get());
+        std::vector<double> h = Rpos.to_host((size_t)(p_ * N));
+        rowmass.assign((size_t)p_, 0.0);
+        for (int64_t q = 0; q < N; ++q)
+            for (int64_t t = 0; t < p_; ++t) rowmass[(size_t)t] += h[(size_t)(t + q * p_)] * h[(size_t)(t + q * p_)];
+    }
+    int64_t p() const override { return p_; }
+    int64_t N() const override { return N_; }
+    int64_t k() const override { return k_; }
+    void run_to(int64_t s) override { s_ = std::min(s, p_); }
+    double trailing_mass() override {
+        double m = 0.0;
+        for (int64_t t = s_; t < p_; ++t) m += rowmass[(size_t)t];
+        return m;
+    }
+    double refresh_exact() override { return trailing_mass(); }
+    const double* R() override { return Rrow.get(); }
+    const int64_t* perm() override { return permb.get(); }
+    const double* Q() override { return Qb.get(); }
+
+private:
+    int64_t s_ = 0;
+};
+
 // Engine choice: the read-only WY engine costs O(k t) per step besides the stream over W,
 // so it serves wide and tall W alike; TTG_TALL_INPLACE=1 selects the in-place engine for
 // tall W instead (kept as a cross-check).
@@ -325,6 +382,8 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         return e && *e == '1';
     }();
     if (inplace && k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    const int64_t p = std::min(k, N);
+    if (small_qrcp_fits(k, N) && (k * N <= 16384 || 2 * cap >= p)) return std::make_unique<SmemPass1>(W, k, N, ld, l);
     return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
 }
 
