@@ -99,6 +99,11 @@ void* ttg_stream(void);
  * algorithmic bytes since the last read. */
 ttg_status ttg_profile_enable(int on);
 int64_t ttg_profile_read(double* total_ms, double* algorithmic_bytes);
+/* Per-kernel totals of everything drained by ttg_profile_read since the last reset:
+ * name (static string), summed device ms, algorithmic bytes and launches for each pass-1
+ * stream kernel variant. Returns the number of kernels (<= max are written). */
+int ttg_profile_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches);
+void ttg_profile_reset_kernels(void);
 
 /* ---- tensor-train sweeps ---------------------------------------------------- */
 /* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`

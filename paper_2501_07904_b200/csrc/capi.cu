@@ -124,6 +124,16 @@ ttg_status ttg_reserve(int64_t bytes) {
     });
 }
 
+int ttg_profile_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches) {
+    try {
+        return ttg::prof_kernels(max, names, ms, bytes, launches);
+    } catch (...) {
+        return -1;
+    }
+}
+
+void ttg_profile_reset_kernels(void) { ttg::prof_reset_kernels(); }
+
 ttg_status ttg_profile_enable(int on) {
     return guard([&] { ttg::prof_enable(on != 0); });
 }

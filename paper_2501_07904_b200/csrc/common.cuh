@@ -71,9 +71,12 @@ void ensure_pool(size_t bytes);
 bool prof_enabled();
 void prof_enable(bool on);
 void prof_begin();
-void prof_end(double algorithmic_bytes);
+void prof_end(double algorithmic_bytes, const char* kernel);
 // Drains the recorded events (host sync). Returns launches; total device ms and bytes.
+// The drained records also accumulate into per-kernel totals (prof_kernels).
 int64_t prof_read(double* total_ms, double* bytes);
+int prof_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches);
+void prof_reset_kernels();
 
 // Stream-ordered device allocation (cudaMallocAsync on the thread's stream).
 template <class T>

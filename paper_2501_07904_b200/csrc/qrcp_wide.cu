@@ -1822,7 +1822,14 @@ void WideQrcp::gemv_step(int64_t t) {
     }
     // Algorithmic bytes: the unpivoted columns of W read once, their norms read and
     // written once, and row t of R written.
-    prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_);
+    static const char* const kNames[] = {"k_stream<0> (row, thread per column)", "k_stream<1> (col, warp per column)",
+                                         "k_stream_c32 (col, k<=64, warp per 32 columns)",
+                                         "k_stream_splitk (row, rows split across warps)",
+                                         "k_col_part + k_stream_fin (tall row, split-k across CTAs)",
+                                         "k_stream_tma (k<=32, cp.async.bulk ring)",
+                                         "k_stream_row2 (row, 16-byte paired columns)",
+                                         "k_stream_splitk4 (row, 128-column strips)"};
+    prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_, kNames[mode_]);
     // guard recompute of the flagged norms; its candidates / masses go to the slots after
     // the stream kernel's
     static const bool no_guard = [] {  // diagnostics only: skip the recompute (wrong results)

@@ -1,5 +1,7 @@
 // Per-thread CUDA stream, device properties and the launch counter.
 #include <mutex>
+#include <string>
+#include <algorithm>
 #include <vector>
 #include <atomic>
 #include <cstdlib>
@@ -59,10 +61,14 @@ cudaStream_t stream() {
 namespace {
 struct Prof {
     bool on = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    struct Rec {
+        cudaEvent_t a, b;
+        double bytes;
+        int kind;
+    };
+    std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
     cudaEvent_t open = nullptr;
-    double bytes = 0.0;
     cudaEvent_t get() {
         if (!pool.empty()) {
             cudaEvent_t e = pool.back();
@@ -72,6 +78,19 @@ struct Prof {
         cudaEvent_t e;
         TTG_CUDA(cudaEventCreate(&e));
         return e;
+    }
+    // per-kernel totals of the drained records
+    std::vector<std::string> names;
+    std::vector<double> kms, kbytes;
+    std::vector<int64_t> kcount;
+    int kind_of(const char* name) {
+        for (size_t i = 0; i < names.size(); ++i)
+            if (names[i] == name) return (int)i;
+        names.emplace_back(name);
+        kms.push_back(0.0);
+        kbytes.push_back(0.0);
+        kcount.push_back(0);
+        return (int)names.size() - 1;
     }
 };
 thread_local Prof t_prof;
@@ -86,31 +105,50 @@ void prof_begin() {
     TTG_CUDA(cudaEventRecord(t_prof.open, stream()));
 }
 
-void prof_end(double algorithmic_bytes) {
+void prof_end(double algorithmic_bytes, const char* kernel) {
     if (!t_prof.on || !t_prof.open) return;
     cudaEvent_t e = t_prof.get();
     TTG_CUDA(cudaEventRecord(e, stream()));
-    t_prof.pending.emplace_back(t_prof.open, e);
+    t_prof.pending.push_back({t_prof.open, e, algorithmic_bytes, t_prof.kind_of(kernel)});
     t_prof.open = nullptr;
-    t_prof.bytes += algorithmic_bytes;
 }
 
 int64_t prof_read(double* total_ms, double* bytes) {
-    double ms = 0.0;
-    for (auto& pr : t_prof.pending) {
-        TTG_CUDA(cudaEventSynchronize(pr.second));
+    double ms = 0.0, by = 0.0;
+    for (auto& r : t_prof.pending) {
+        TTG_CUDA(cudaEventSynchronize(r.b));
         float x = 0.f;
-        TTG_CUDA(cudaEventElapsedTime(&x, pr.first, pr.second));
+        TTG_CUDA(cudaEventElapsedTime(&x, r.a, r.b));
         ms += x;
-        t_prof.pool.push_back(pr.first);
-        t_prof.pool.push_back(pr.second);
+        by += r.bytes;
+        t_prof.kms[(size_t)r.kind] += x;
+        t_prof.kbytes[(size_t)r.kind] += r.bytes;
+        t_prof.kcount[(size_t)r.kind] += 1;
+        t_prof.pool.push_back(r.a);
+        t_prof.pool.push_back(r.b);
     }
     const int64_t n = (int64_t)t_prof.pending.size();
     t_prof.pending.clear();
     *total_ms = ms;
-    *bytes = t_prof.bytes;
-    t_prof.bytes = 0.0;
+    *bytes = by;
     return n;
+}
+
+int prof_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches) {
+    const int n = (int)t_prof.names.size();
+    for (int i = 0; i < n && i < max; ++i) {
+        names[i] = t_prof.names[(size_t)i].c_str();
+        ms[i] = t_prof.kms[(size_t)i];
+        bytes[i] = t_prof.kbytes[(size_t)i];
+        launches[i] = t_prof.kcount[(size_t)i];
+    }
+    return n;
+}
+
+void prof_reset_kernels() {
+    std::fill(t_prof.kms.begin(), t_prof.kms.end(), 0.0);
+    std::fill(t_prof.kbytes.begin(), t_prof.kbytes.end(), 0.0);
+    std::fill(t_prof.kcount.begin(), t_prof.kcount.end(), 0);
 }
 
 void raise_smem_limit(const void* kernel) {
