@@ -687,21 +687,35 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
     double msum = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (MODE == 1) {
+        // two columns per warp at a time: two independent load streams in flight, each
+        // column summed exactly as alone (lanes over rows, then the warp tree)
         const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
         const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
-        for (int64_t j = gw; j < N; j += nwarps) {
-            const int64_t pj = pos[j];
-            if (pj < t || j == jp) {
-                if (lane == 0) R[t * N + j] = j == jp ? diag[t] : 0.0;
-                continue;
-            }
+        for (int64_t j = gw; j < N; j += 2 * nwarps) {
+            const int64_t j2 = j + nwarps;
+            const bool two = j2 < N;
             const double* w = W + j * ld;
-            double a = 0.0;
-            for (int64_t i = lane; i < k; i += 32) a = fma(q[i], w[i], a);
+            const double* w2 = W + (two ? j2 : j) * ld;
+            double a = 0.0, b = 0.0;
+            for (int64_t i = lane; i < k; i += 32) {
+                a = fma(q[i], w[i], a);
+                b = fma(q[i], w2[i], b);
+            }
             a = warp_sum(a);
-            if (lane == 0 && downdate(t, j, N, a, pj, R, nu, cref, best, msum)) {
-                const int slot = atomicAdd(nflag, 1);
-                flags[slot] = j;
+            b = warp_sum(b);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !two) break;
+                const int64_t jj = h ? j2 : j;
+                const int64_t pj = pos[jj];
+                if (pj < t || jj == jp) {
+                    if (lane == 0) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
+                    continue;
+                }
+                if (lane == 0 && downdate(t, jj, N, h ? b : a, pj, R, nu, cref, best, msum)) {
+                    const int slot = atomicAdd(nflag, 1);
+                    flags[slot] = jj;
+                }
             }
         }
     } else {
