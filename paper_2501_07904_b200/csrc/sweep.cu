@@ -328,6 +328,197 @@ __global__ void k_scatter_rows(const double* __restrict__ Rpos, const int64_t* _
     Rrow[t * N + perm[q]] = Rpos[t + q * p];
 }
 
+// ---- tall W (k >> N), fixed rank: pivoted Cholesky of the Gram matrix -------------------
+// QRCP of W and pivoted Cholesky of G = W^T W choose the same pivots (the residual column
+// norms are the residual diagonal of G) and the same R in exact arithmetic, so for a tall
+// W the whole pass 1 runs on the N x N Gram matrix: one DMMA GEMM over W (split-K, summed
+// over the ranks when W's rows are sharded), then O(N t) per step. The economy Q columns
+// are Q[:, :s] = W[:, piv] R11^{-1} (a triangular solve per row). Gram-based factors carry
+// eps * cond^2 errors, so the engine only keeps this result when R_ss / R_00 >= 1e-4
+// (otherwise it falls back to the Householder engine): then every R entry is within about
+// eps * cond |R_00| of the Householder one, far inside the 1e-10 parity contract.
+__global__ void k_gc_init(const double* __restrict__ G, int64_t N, double* D, double* Dref, int64_t* pos,
+                          int64_t* perm) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+        D[j] = G[j + j * N];
+        Dref[j] = D[j];
+        pos[j] = j;
+        perm[j] = j;
+    }
+}
+
+// One step of the pivoted Cholesky (one CTA of 1024 threads): pivot by (D desc, position
+// asc) like qr_col_pivot (factor.cpp:85-93), row t of R, downdate of D.
+__global__ void __launch_bounds__(1024) k_gc_step(const double* __restrict__ G, int64_t N, int64_t t, double* D,
+                                                  int64_t* pos, int64_t* perm, int64_t* piv, double* R) {
+    __shared__ Cand sc[32];
+    extern __shared__ double rp[];  // R(0:t, piv) then the new row's pivot scalar
+    Cand best = cand_none();
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const int64_t pj = pos[j];
+        if (pj < t) continue;
+        const Cand c{D[j], pj, j};
+        if (better(c, best)) best = c;
+    }
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        best = warp_best(best);
+        if (lane == 0) sc[warp] = best;
+        __syncthreads();
+        Cand b = lane < nw ? sc[lane] : cand_none();
+        best = warp_best(b);
+    }
+    const int64_t jp = best.col >= 0 ? best.col : perm[t];
+    const int64_t pp = best.col >= 0 ? best.pos : t;
+    const int64_t ct = perm[t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        perm[t] = jp;
+        perm[pp] = ct;
+        pos[jp] = t;
+        pos[ct] = pp;
+        piv[t] = jp;
+    }
+    for (int64_t l = threadIdx.x; l < t; l += blockDim.x) rp[l] = R[l * N + jp];
+    __syncthreads();
+    const double dj = D[jp];
+    const double rtt = dj > 0.0 ? sqrt(dj) : 0.0;
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const int64_t pj = (j == jp) ? t : (j == ct ? pp : pos[j]);
+        double r;
+        if (j == jp) {
+            r = rtt;
+        } else if (pj < t) {
+            r = 0.0;
+        } else {
+            double a = G[jp + j * N];
+            for (int64_t l = 0; l < t; ++l) a = fma(-rp[l], R[l * N + j], a);
+            r = rtt > 0.0 ? a / rtt : 0.0;
+            D[j] = D[j] - r * r;
+        }
+        R[t * N + j] = r;
+    }
+}
+
+// Rows of Q[:, :s] = W[:, piv[:s]] R11^{-1}: q R11 = x by forward substitution, one thread
+// per row of W, R11 (s x s over positions) staged in shared memory.
+__global__ void k_gc_q(const double* __restrict__ W, int64_t k, int64_t ld, int layout,
+                       const double* __restrict__ R, int64_t N, const int64_t* __restrict__ piv, int64_t s,
+                       double* Q) {
+    extern __shared__ double r11[];  // r11[m + l*s] = R(m, piv_l)
+    for (int64_t e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int64_t l = e / s, m = e - l * s;
+        r11[e] = m <= l ? R[m * N + piv[l]] : 0.0;
+    }
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t l = 0; l < s; ++l) {
+            const int64_t c = piv[l];
+            double x = layout == 0 ? W[i + c * ld] : W[i * ld + c];
+            for (int64_t m = 0; m < l; ++m) x = fma(-Q[i + m * k], r11[m + l * s], x);
+            const double d = r11[l + l * s];
+            Q[i + l * k] = d != 0.0 ? x / d : 0.0;
+        }
+    }
+}
+
+__global__ void k_masked_sum(const double* __restrict__ D, const int64_t* __restrict__ pos, int64_t N, int64_t s,
+                             double* out) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t j = threadIdx.x; j < N; j += blockDim.x)
+        if (pos[j] >= s) a += fmax(D[j], 0.0);
+    a = block_sum(a, red);
+    if (threadIdx.x == 0) out[0] = a;
+}
+
+struct GramPass1 final : Pass1 {
+    const double* W_;
+    int64_t k_, N_, ld_, kg_;
+    Layout l_;
+    Comm* comm_;
+    int64_t s_ = 0, qs_ = -1;
+    DevBuf<double> G, D, Dref, Rb, Qb;
+    DevBuf<int64_t> posb, permb, pivb;
+    // W: k local rows (of kg in all) by N columns; comm non-null when the rows are sharded.
+    GramPass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, Comm* comm, int64_t cap)
+        : W_(W), k_(k), N_(N), ld_(ld), kg_(k), l_(l), comm_(comm) {
+        G.alloc((size_t)(N * N));
+        // G = W^T W; Col: W is k x N (ld); Row: W^T is N x k column-major (ld)
+        if (l == Layout::Col) gemm(true, false, N, N, k, W, ld, W, ld, G.get(), N);
+        else gemm(false, true, N, N, k, W, ld, W, ld, G.get(), N);
+        if (comm && comm->size() > 1) {
+            const int P = comm->size();
+            DevBuf<double> all((size_t)(P * N * N));
+            comm->allgather(G.get(), all.get(), sizeof(double) * (size_t)(N * N));
+            TTG_LAUNCH(k_sum_blocks, (int)cdiv(N * N, 256), 256, 0, stream(), all.get(), P, N * N, G.get());
+            kg_ = (int64_t)llround(global_sum(*comm, (double)k));
+        }
+        D.alloc((size_t)N);
+        Dref.alloc((size_t)N);
+        posb.alloc((size_t)N);
+        permb.alloc((size_t)N);
+        pivb.alloc((size_t)std::min(cap, N));
+        Rb.alloc((size_t)(std::min(cap, N) * N));
+        TTG_LAUNCH(k_gc_init, (int)cdiv(N, 256), 256, 0, stream(), G.get(), N, D.get(), Dref.get(), posb.get(),
+                   permb.get());
+    }
+    int64_t p() const override { return std::min(kg_, N_); }
+    int64_t N() const override { return N_; }
+    int64_t k() const override { return k_; }
+    bool sharded() const override { return comm_ != nullptr && comm_->size() > 1; }
+    void run_to(int64_t s) override {
+        s = std::min(s, p());
+        if ((size_t)(s * N_) > Rb.size()) {  // grow R rows and pivots
+            DevBuf<double> nr((size_t)(s * N_));
+            DevBuf<int64_t> np((size_t)s);
+            if (s_ > 0) {
+                TTG_CUDA(cudaMemcpyAsync(nr.get(), Rb.get(), sizeof(double) * s_ * N_, cudaMemcpyDeviceToDevice, stream()));
+                TTG_CUDA(cudaMemcpyAsync(np.get(), pivb.get(), sizeof(int64_t) * s_, cudaMemcpyDeviceToDevice, stream()));
+            }
+            Rb = std::move(nr);
+            pivb = std::move(np);
+        }
+        for (int64_t t = s_; t < s; ++t) {
+            const size_t sm = sizeof(double) * (size_t)(t + 1);
+            allow_smem(k_gc_step, sm);
+            TTG_LAUNCH(k_gc_step, 1, 1024, sm, stream(), G.get(), N_, t, D.get(), posb.get(), permb.get(), pivb.get(),
+                       Rb.get());
+        }
+        s_ = std::max(s_, s);
+    }
+    double trailing_mass() override {
+        DevBuf<double> m(1);
+        TTG_LAUNCH(k_masked_sum, 1, 1024, 0, stream(), D.get(), posb.get(), N_, s_, m.get());
+        return m.to_host(1)[0];
+    }
+    double refresh_exact() override { return trailing_mass(); }
+    const double* R() override { return Rb.get(); }
+    const int64_t* perm() override { return permb.get(); }
+    const double* Q() override {
+        if (qs_ != s_) {
+            Qb.alloc((size_t)(k_ * s_));
+            const size_t sm = sizeof(double) * (size_t)(s_ * s_);
+            allow_smem(k_gc_q, sm);
+            TTG_LAUNCH(k_gc_q, (int)std::min<int64_t>(cdiv(k_, 256), 4 * sm_count()), 256, sm, stream(), W_, k_, ld_,
+                       (int)l_, Rb.get(), N_, pivb.get(), s_, Qb.get());
+            qs_ = s_;
+        }
+        return Qb.get();
+    }
+    // R_ss / R_00 over the first s steps (host sync): the acceptance test of the Gram route.
+    double diag_ratio() {
+        if (s_ == 0) return 1.0;
+        std::vector<int64_t> pv = pivb.to_host((size_t)s_);
+        double r0 = 0.0, rs = 0.0;
+        TTG_CUDA(cudaMemcpyAsync(&r0, Rb.get() + pv[0], sizeof(double), cudaMemcpyDeviceToHost, stream()));
+        TTG_CUDA(cudaMemcpyAsync(&rs, Rb.get() + (s_ - 1) * N_ + pv[(size_t)(s_ - 1)], sizeof(double),
+                                 cudaMemcpyDeviceToHost, stream()));
+        sync();
+        return r0 > 0.0 ? rs / r0 : 0.0;
+    }
+};
+
 struct SmemPass1 final : Pass1 {
     int64_t k_, N_, p_;
     DevBuf<double> Wc, Rpos, Rrow, Qb, pn;
@@ -376,12 +567,20 @@ private:
 // Engine choice: the read-only WY engine costs O(k t) per step besides the stream over W,
 // so it serves wide and tall W alike; TTG_TALL_INPLACE=1 selects the in-place engine for
 // tall W instead (kept as a cross-check).
-std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap) {
+std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap,
+                                  bool fixed = false) {
     static const bool inplace = [] {
         const char* e = std::getenv("TTG_TALL_INPLACE");
         return e && *e == '1';
     }();
+    static const bool no_gram = [] {
+        const char* e = std::getenv("TTG_NO_GRAM_PASS1");
+        return e && *e == '1';
+    }();
     if (inplace && k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    // tall W, fixed rank: the pivoted Cholesky of W^T W (cut_with() checks its conditioning)
+    if (fixed && !no_gram && k >= 8 * N && N <= 4096 && cap <= 160 && cap >= 1)
+        return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
     const int64_t p = std::min(k, N);
     if (small_qrcp_fits(k, N) && (k * N <= 16384 || 2 * cap >= p)) return std::make_unique<SmemPass1>(W, k, N, ld, l);
     return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
@@ -802,6 +1001,24 @@ void print_cut(const char* what, int64_t cut, int64_t m, int64_t n, const CutOut
                  (long long)n, (long long)co.steps, std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
 }
 
+// run_cut with the engine make_pass1 chose; a Gram-route result that is not well
+// conditioned (R_ss / R_00 < 1e-4) is recomputed by the Householder engine.
+CutOut cut_with(std::unique_ptr<Pass1>& e1, const CutRequest& rq, const double* W, int64_t k, int64_t N, int64_t ld,
+                Layout l, int64_t cap) {
+    CutOut co = run_cut(*e1, rq);
+    if (auto* g = dynamic_cast<GramPass1*>(e1.get())) {
+        const double ratio = g->diag_ratio();
+        if (cut_timing())
+            std::fprintf(stderr, "[ttg]   gram pass 1 (%lld x %lld, s=%lld): R_ss/R_00 = %.3e, %s\n", (long long)k,
+                         (long long)N, (long long)co.steps, ratio, ratio >= 1e-4 ? "kept" : "redone");
+        if (!(ratio >= 1e-4)) {
+            e1 = std::make_unique<WidePass1>(W, k, N, ld, l, cap);
+            co = run_cut(*e1, rq);
+        }
+    }
+    return co;
+}
+
 // TT-ULV left to right (tt_decomp.cpp:156-211) from cut k0 (1-based), c the m x n unfolding.
 void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, int64_t r_prev,
               const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
@@ -811,8 +1028,9 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
         const int64_t p = std::min(m, n);
         const CutRequest rq = make_request(res, mode, cfg, k, p);
         const auto tc0 = Clock::now();
-        auto e1 = make_pass1(c, m, n, m, Layout::Col, mode.fixed ? rq.rank : 32);
-        CutOut co = run_cut(*e1, rq);
+        const int64_t cap = mode.fixed ? rq.rank : 32;
+        auto e1 = make_pass1(c, m, n, m, Layout::Col, cap, mode.fixed);
+        CutOut co = cut_with(e1, rq, c, m, n, m, Layout::Col, cap);
         print_cut("ulv", k, m, n, co, tc0);
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 1)] = co.step_error;
@@ -847,8 +1065,9 @@ void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, 
         const CutRequest rq = make_request(res, mode, cfg, k - 1, p);
         // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
         const auto tc0 = Clock::now();
-        auto e1 = make_pass1(c, n, M, M, Layout::Row, mode.fixed ? rq.rank : 32);
-        CutOut co = run_cut(*e1, rq);
+        const int64_t cap = mode.fixed ? rq.rank : 32;
+        auto e1 = make_pass1(c, n, M, M, Layout::Row, cap, mode.fixed);
+        CutOut co = cut_with(e1, rq, c, n, M, M, Layout::Row, cap);
         print_cut("urv", k - 1, M, n, co, tc0);
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 2)] = co.step_error;

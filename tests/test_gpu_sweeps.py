@@ -206,3 +206,19 @@ def test_planted_rank48_gram_pass2(dev, ref, method):
     dims, ranks = [64, 64, 64], [1, 48, 48, 1]
     a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
     _check_parity(dev, ref, a, dims, method, ranks=ranks)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_tall_cut_gram_pass1(dev, ref, method):
+    # a tall fixed-rank cut (k >= 8N): pass 1 runs as the pivoted Cholesky of W^T W
+    dims, ranks = [16, 64, 64], [1, 8, 8, 1]
+    a = planted_plus_noise(ref, dims, ranks, 33, 1e-6)
+    _check_parity(dev, ref, a, dims, method, ranks=ranks)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_tall_cut_gram_fallback_ill_conditioned(dev, ref, method):
+    # Hilbert-type tall cut at fixed rank: R_ss / R_00 < 1e-4, so the cut is redone by the
+    # Householder engine
+    dims, ranks = [8, 8, 96], [1, 8, 8, 1]
+    _check_parity(dev, ref, shifted_hilbert(dims), dims, method, ranks=ranks)
