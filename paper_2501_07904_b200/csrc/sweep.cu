@@ -1219,6 +1219,81 @@ ShardRange shard_range(const std::vector<int64_t>& dims, int method, int nranks,
     return r;
 }
 
+namespace {
+
+// Global core (r2 x n', n' = i + I * q, I = dims[d-2]) from the ranks' transposed local
+// cores (r2 x kl each, local row l = il + L q with il < L = I / G): rank g holds i in
+// [g L, (g+1) L).
+__global__ void k_core_from_shards(const double* __restrict__ parts, int G, int64_t r2, int64_t kl, int64_t L,
+                                   int64_t I, double* out) {
+    const int64_t total = (int64_t)G * kl * r2;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = e / (kl * r2), rem = e - g * kl * r2;
+        const int64_t l = rem / r2, q2 = rem - l * r2;
+        const int64_t il = l % L, q = l / L;
+        const int64_t np = g * L + il + I * q;
+        out[q2 + np * r2] = parts[e];
+    }
+}
+
+}  // namespace
+
+// Config 5's second URV cut without moving the carry: the previous cut's
+// carry rows held by this rank are a row block of W' = c'^T (Row layout, ld M'), so pass 1
+// runs as the pivoted Cholesky of the rank-summed Gram matrix (GramPass1 with the comm),
+// pass 2 and the next carry are replicated, and only the core rows (k' x r, distributed)
+// are all-gathered. Returns false (nothing done) when the cut does not qualify or the Gram
+// route is not well conditioned; the caller then gathers the carry.
+bool k_sharded_next(TTResult& res, const double* mine, int64_t Nl, int64_t Ng, int64_t r, Comm& comm,
+                    const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
+    const int64_t d = (int64_t)dims.size();
+    const int G = comm.size();
+    const int64_t I = dims[(size_t)(d - 2)];
+    const int64_t Mp = Ng / I;                 // M' = rows of c' = columns of W'
+    if (Nl % Mp != 0) {  // each rank must hold whole i_{d-1} slices
+        if (cut_timing()) std::fprintf(stderr, "[ttg]   k-sharded cut: %lld local rows not a multiple of %lld\n",
+                                       (long long)Nl, (long long)Mp);
+        return false;
+    }
+    const int64_t L = Nl / Mp, kl = L * r;     // local i_{d-1} range, local rows of W'
+    const int64_t kg = I * r, p = std::min(kg, Mp);
+    const CutRequest rq = make_request(res, mode, cfg, d - 2, p);
+    if (!(kg >= 8 * Mp && Mp <= 4096 && rq.rank <= 160 && rq.rank >= 1)) {
+        if (cut_timing())
+            std::fprintf(stderr, "[ttg]   k-sharded cut not eligible (k' %lld, N' %lld, rank %lld)\n", (long long)kg,
+                         (long long)Mp, (long long)rq.rank);
+        return false;
+    }
+    const auto tc0 = Clock::now();
+    GramPass1 gp(mine, kl, Mp, Mp, Layout::Row, &comm, rq.rank);
+    CutOut co = run_cut(gp, rq);
+    const double ratio = gp.diag_ratio();
+    if (cut_timing())
+        std::fprintf(stderr, "[ttg]   k-sharded gram pass 1 (%lld x %lld local rows %lld): R_ss/R_00 = %.3e\n",
+                     (long long)kg, (long long)Mp, (long long)kl, ratio);
+    if (!(ratio >= 1e-4)) return false;
+    print_cut("urv(k-sharded)", d - 2, Mp, kg, co, tc0);
+    const int64_t r2 = co.rank;
+    res.step_errors[(size_t)(d - 3)] = co.step_error;
+    res.ranks_chosen[(size_t)(d - 2)] = r2;
+    res.cuts[(size_t)(d - 3)] = CutInfo{Mp, kg, p, co.steps, r2, co.extensions, co.diag};
+    // core (r2 x I x r): local transposed core rows, all-gathered, scattered to n' order
+    DevBuf<double> mineT((size_t)(kl * r2)), parts((size_t)(G * kl * r2)), core((size_t)(kg * r2));
+    TTG_LAUNCH(k_gather_qcols, (int)cdiv(kl * r2, 256), 256, 0, stream(), gp.Q(), kl, co.sel.get(), r2, true,
+               mineT.get());
+    comm.allgather(mineT.get(), parts.get(), sizeof(double) * (size_t)(kl * r2));
+    TTG_LAUNCH(k_core_from_shards, (int)std::min<int64_t>(cdiv(G * kl * r2, 256), 8 * sm_count()), 256, 0, stream(),
+               parts.get(), G, r2, kl, L, I, core.get());
+    set_core(res, (size_t)(d - 2), std::move(core), r2, I, r);
+    // carry M' x r2 (replicated: R1 rows are replicated)
+    DevBuf<double> next((size_t)(Mp * r2));
+    dim3 g((unsigned)std::min<int64_t>(cdiv(Mp, 256), 4096), (unsigned)r2);
+    TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), gp.R(), Mp, co.sel.get(), r2, next.get());
+    if (d == 3) set_core(res, 0, std::move(next), 1, dims[0], r2);
+    else urv_cuts(res, next.get(), Mp / dims[(size_t)(d - 3)], dims[(size_t)(d - 3)] * r2, d - 2, r2, dims, mode, cfg);
+    return true;
+}
+
 TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& dims, const SweepConfig& cfg,
                            Comm& comm) {
     const auto start = Clock::now();
@@ -1297,6 +1372,10 @@ TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& di
         set_core(res, (size_t)(d - 1), std::move(core), r, dims[(size_t)(d - 1)], 1);
         dim3 g((unsigned)std::min<int64_t>(cdiv(Nl, 256), 4096), (unsigned)r);
         TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1.R(), Nl, co.sel.get(), r, mine.get());
+        if (d >= 3 && mode.fixed && k_sharded_next(res, mine.get(), Nl, Ng, r, comm, dims, mode, cfg)) {
+            finish(res, rss, start);
+            return res;
+        }
         DevBuf<double> gathered((size_t)(Ng * r));
         if (cut_timing()) {
             sync();

@@ -137,3 +137,12 @@ def test_planted_rank48_gram_sharded(dev, ref, method):
     dims, ranks = [64, 64, 64], [1, 48, 48, 1]
     a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
     _check(dev, ref, a, dims, method, 4, ranks=ranks)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_k_sharded_second_cut(dev, ref, G):
+    # URV: the second cut's W' = c'^T is tall and its rows are the ranks' carry blocks, so
+    # it runs k-sharded (rank-summed Gram matrix) without gathering the carry
+    dims, ranks = [16, 64, 64], [1, 8, 8, 1]
+    a = planted_plus_noise(ref, dims, ranks, 33, 1e-6)
+    _check(dev, ref, a, dims, "urv", G, ranks=ranks)
