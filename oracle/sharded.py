@@ -145,3 +145,41 @@ def gather_carry_ulv(mine: np.ndarray, allgather) -> np.ndarray:
     r, nl = mine.shape
     flat = allgather(mine.reshape(-1, order="F")).reshape(-1)
     return flat.reshape(r, -1, order="F")
+
+
+def kshard_gram_pass1(W_rows: np.ndarray, s: int, allgather):
+    """Row-sharded tall pass 1 (csrc/sweep.cu GramPass1 with a comm): each rank holds a row
+    block of the k x N matrix W; the ranks' Gram matrices are all-gathered and summed in
+    rank order, then the pivoted Cholesky of G = W^T W picks pivots by (residual diagonal
+    desc, position asc) -- the qr_col_pivot rule -- and builds R row by row.
+    Returns (piv, R rows by original column (s x N), local rows of Q[:, :s])."""
+    N = W_rows.shape[1]
+    Gl = W_rows.T @ W_rows
+    G = allgather(Gl.reshape(-1)).reshape(-1, N, N).sum(axis=0)
+    D = np.diag(G).copy()
+    pos = np.arange(N)
+    perm = np.arange(N)
+    R = np.zeros((s, N))
+    piv = []
+    for t in range(s):
+        live = np.flatnonzero(pos >= t)
+        order = np.lexsort((pos[live], -D[live]))
+        jp = live[order[0]]
+        pp, ct = pos[jp], perm[t]
+        perm[t], perm[pp] = jp, ct
+        pos[jp], pos[ct] = t, pp
+        piv.append(jp)
+        rtt = np.sqrt(max(D[jp], 0.0))
+        for j in range(N):
+            if j == jp:
+                R[t, j] = rtt
+            elif pos[j] < t:
+                R[t, j] = 0.0
+            else:
+                a = G[jp, j] - R[:t, jp] @ R[:t, j]
+                R[t, j] = a / rtt if rtt > 0 else 0.0
+                D[j] -= R[t, j] ** 2
+    piv = np.array(piv)
+    R11 = R[:, piv]  # s x s upper triangular over positions
+    Q = np.linalg.solve(R11.T, W_rows[:, piv].T).T  # q R11 = x
+    return piv, R, Q

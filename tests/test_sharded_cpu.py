@@ -128,3 +128,35 @@ def test_shard_block_tiles_the_tensor():
             c = a.reshape((m, dims[-1]), order="F")
             back = np.vstack([p.reshape((m // G, dims[-1]), order="F") for p in parts])
             np.testing.assert_array_equal(back, c)
+
+
+def _worker_kshard(rank, world, port_):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        k, N, s = 96, 12, 6
+        W = rng.standard_normal((k, 6)) @ rng.standard_normal((6, N)) + 1e-3 * rng.standard_normal((k, N))
+        kl = k // world
+        piv, R, Q = sh.kshard_gram_pass1(W[rank * kl:(rank + 1) * kl], s, _allgather_dist)
+        piv1, R1, Q1 = sh.kshard_gram_pass1(W, s, _allgather_one)
+        np.testing.assert_array_equal(piv, piv1)
+        np.testing.assert_allclose(R, R1, rtol=0, atol=1e-12 * np.abs(R1).max())
+        np.testing.assert_allclose(Q, Q1[rank * kl:(rank + 1) * kl], rtol=0, atol=1e-10)
+        # the Householder QRCP of the whole matrix picks the same pivots and |R|
+        if port.available():
+            _, Rref, perm = port.qr_col_pivot(W)
+            np.testing.assert_array_equal(piv1, perm[:s])
+            np.testing.assert_allclose(np.abs(np.diag(R1[:, piv1])), np.abs(np.diag(Rref)[:s]), rtol=1e-9)
+        # and the local Q rows stack into orthonormal columns
+        Qall = _allgather_dist(np.ascontiguousarray(Q.reshape(-1, order="F"))).reshape(world, -1)
+        Qs = np.vstack([q.reshape(kl, s, order="F") for q in Qall])
+        np.testing.assert_allclose(Qs.T @ Qs, np.eye(s), atol=1e-10)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_k_sharded_gram_pass1():
+    mp.spawn(_worker_kshard, args=(2, _free_port()), nprocs=2, join=True)
