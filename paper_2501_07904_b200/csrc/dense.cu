@@ -166,6 +166,67 @@ double reduce_sq(const double* x, const double* y, int64_t n) {
     return out.to_host(1)[0];
 }
 
+// ---------------------------------------------------------------------------
+// Gram matrix G = B^T B of a tall N x s block (s <= S <= 32, column t at B + t*ld) on the
+// FP64 tensor cores. A warp takes 4 rows at a time: lane l loads x_c = B(row0 + l%4,
+// 8c + l/4) for the S/8 column blocks -- in the m8n8k4 fragment layouts that one value is
+// both the A fragment (B^T, 8x4 row-major) and the B fragment (B, 4x8 col-major) -- and
+// issues (S/8)^2 DMMAs. Each warp writes its partial G; k_gram_sum adds the partials in
+// warp order (deterministic).
+// ---------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(256) k_gram_small(const double* __restrict__ B, int64_t N, int s, int64_t ld,
+                                                    double* part) {
+    constexpr int CB = S / 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+    double acc[CB][CB][2];
+#pragma unroll
+    for (int a = 0; a < CB; ++a)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int kr = lane & 3, mc = lane >> 2;
+    for (int64_t r0 = gw * 4; r0 < N; r0 += nw * 4) {
+        const int64_t row = r0 + kr;
+        double x[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            const int col = 8 * c + mc;
+            x[c] = (row < N && col < s) ? __ldg(B + row + (int64_t)col * ld) : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < CB; ++a)
+#pragma unroll
+            for (int b = 0; b < CB; ++b) dmma(acc[a][b], x[a], x[b]);
+    }
+    // the CTA's 8 warps add into one S x S tile in warp order, then one partial per CTA
+    __shared__ double tile[S * S];
+    for (int e = threadIdx.x; e < S * S; e += 256) tile[e] = 0.0;
+    for (int w = 0; w < 8; ++w) {
+        __syncthreads();
+        if (warp == w) {
+#pragma unroll
+            for (int a = 0; a < CB; ++a)
+#pragma unroll
+                for (int b = 0; b < CB; ++b)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) tile[(8 * a + mc) + (8 * b + 2 * kr + h) * S] += acc[a][b][h];
+        }
+    }
+    __syncthreads();
+    double* out = part + (int64_t)blockIdx.x * (S * S);
+    for (int e = threadIdx.x; e < S * S; e += 256) out[e] = tile[e];
+}
+
+__global__ void k_gram_sum(const double* __restrict__ part, int64_t nparts, int S, int s, double* G) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int j = e / s, i = e - j * s;
+        double a = 0.0;
+        for (int64_t p = 0; p < nparts; ++p) a += part[p * S * S + i + j * S];
+        G[e] = a;
+    }
+}
+
 // C = sum_c part[c] (+ beta C), chunks in order.
 __global__ void k_reduce_chunks(const double* __restrict__ part, int64_t ks, int64_t m, int64_t n, double* C,
                                 int64_t ldc, double beta) {
@@ -206,6 +267,20 @@ void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, in
         return;
     }
     launch(dim3((unsigned)tiles), C, ldc, alpha, beta, k, 0);
+}
+
+void gram_small(const double* B, int64_t N, int64_t s, int64_t ld, double* G) {
+    const int S = s <= 8 ? 8 : s <= 16 ? 16 : s <= 24 ? 24 : 32;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sm_count(), cdiv(N, 4 * 8)));
+    const int64_t nparts = blocks;
+    DevBuf<double> part((size_t)(nparts * S * S));
+    switch (S) {
+        case 8: TTG_LAUNCH(k_gram_small<8>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
+        case 16: TTG_LAUNCH(k_gram_small<16>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
+        case 24: TTG_LAUNCH(k_gram_small<24>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
+        default: TTG_LAUNCH(k_gram_small<32>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
+    }
+    TTG_LAUNCH(k_gram_sum, 1, 1024, 0, stream(), part.get(), nparts, S, (int)s, G);
 }
 
 void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb) {

@@ -196,7 +196,7 @@ struct CutRequest {
 // Pass 1 of a cut behind one interface: the wide read-only engine (k moderate) or, when W
 // is tall (k >> N, e.g. the last URV cut of config 5: W = 131072 x 1024), the in-place
 // Householder engine on a column-major copy of W.
-bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB);
+bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB, double r1_ratio);
 
 struct Pass1 {
     virtual ~Pass1() = default;
@@ -212,7 +212,7 @@ struct Pass1 {
     virtual bool sharded() const { return false; }
     // R_B (s x s, ld s) of B = R1[:s, :]^T over all columns (all ranks when sharded).
     virtual void r_factor(int64_t s, double* RB) {
-        if (!gram_r(R(), N(), s, nullptr, RB)) tsqr_r(R(), N(), s, N(), RB);
+        if (!gram_r(R(), N(), s, nullptr, RB, 0.0)) tsqr_r(R(), N(), s, N(), RB);
     }
 };
 
@@ -221,11 +221,15 @@ struct Pass1 {
 // register TSQR is fast below) and only when the factor is well conditioned: the error of
 // a Gram-based R is about eps * cond(B) relative to |T_00|, so min/max R_ii >= 1e-4 keeps
 // it far inside the 1e-10 parity tolerance. Otherwise the caller falls back to TSQR.
-bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB) {
+bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB, double r1_ratio) {
     constexpr double kMinRatio = 1e-4;
-    if (s <= 32 || (size_t)(s * s) * sizeof(double) > 200 * 1024) return false;
+    if ((size_t)(s * s) * sizeof(double) > 200 * 1024) return false;
+    // s <= 32: only when pass 1's own diagonal says R1 is well conditioned (the register
+    // TSQR is the fallback and costs about as much as a rejected Gram attempt)
+    if (s <= 32 && !(r1_ratio >= 1e-3)) return false;
     DevBuf<double> G((size_t)(s * s));
-    gemm(true, false, s, s, N, R1, N, R1, N, G.get(), s);
+    if (s <= 32) gram_small(R1, N, s, N, G.get());
+    else gemm(true, false, s, s, N, R1, N, R1, N, G.get(), s);
     if (comm && comm->size() > 1) {
         const int P = comm->size();
         DevBuf<double> all((size_t)(P * s * s));
@@ -252,8 +256,16 @@ struct WidePass1 final : Pass1 {
     bool sharded() const override { return e.sharded(); }
     // Sharded: every rank reduces its own rows of B to a triangle, the triangles are
     // all-gathered and stacked in rank order, and every rank factors the same stack.
+    // |R1(s-1, s-1)| / |R1(0, 0)| from pass 1's diagonal (host sync of two values)
+    double r1_ratio(int64_t s) {
+        double d0 = 0.0, ds = 0.0;
+        TTG_CUDA(cudaMemcpyAsync(&d0, e.diag(), sizeof(double), cudaMemcpyDeviceToHost, stream()));
+        TTG_CUDA(cudaMemcpyAsync(&ds, e.diag() + (s - 1), sizeof(double), cudaMemcpyDeviceToHost, stream()));
+        sync();
+        return d0 != 0.0 ? std::abs(ds) / std::abs(d0) : 0.0;
+    }
     void r_factor(int64_t s, double* RB) override {
-        if (gram_r(e.R(), e.N(), s, e.comm(), RB)) return;
+        if (gram_r(e.R(), e.N(), s, e.comm(), RB, s <= 32 ? r1_ratio(s) : 1.0)) return;
         if (!e.sharded()) return tsqr_r(e.R(), e.N(), s, e.N(), RB);
         Comm& comm = *e.comm();
         const int G = comm.size();
