@@ -18,6 +18,7 @@
 // The WY phases cost O(k t) per step (one fused CTA when k (t+1) is small, otherwise
 // multi-CTA row chunks with fixed-order reductions), so k may be large (tall W).
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "engine.hpp"
@@ -1247,6 +1248,7 @@ __device__ __forceinline__ double best_stream_nu(const Cand* cand, int ncand) {
 
 __device__ __forceinline__ bool guard_defer(int64_t j, int64_t t, int64_t N, const double* R, double* nu,
                                             double* cref, double bestnu, double& mass) {
+    if (bestnu == -2.0) return false;  // eager mode (the default, see k_guard launch)
     const double r = R[t * N + j];
     const double nv = nu[j];
     const bool stale = isinf(cref[j]);
@@ -1268,13 +1270,13 @@ __global__ void __launch_bounds__(kThreads) k_guard_lane(const double* __restric
                                                          const double* __restrict__ Q, const double* R,
                                                          const int64_t* flags, const int* nflag, double* nu,
                                                          double* cref, const int64_t* pos, const Cand* scand,
-                                                         int nscand, Cand* gcand, double* gmass) {
+                                                         int nscand, Cand* gcand, double* gmass, int lazy) {
     extern __shared__ double qs[];  // Q[:, :t+1]
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
     if (nf > 0) {
-        const double bestnu = best_stream_nu(scand, nscand);
+        const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
         for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
         __syncthreads();
         for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
@@ -1312,14 +1314,15 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
                                                     const double* __restrict__ Q, const double* R,
                                                     const int64_t* flags, const int* nflag, double* nu,
                                                     double* cref, int stage_q, const int64_t* pos,
-                                                    const Cand* scand, int nscand, Cand* gcand, double* gmass) {
+                                                    const Cand* scand, int nscand, Cand* gcand, double* gmass,
+                                                    int lazy) {
     extern __shared__ double qs[];  // Q[:, :t+1] when staged (dynamic smem > 0)
     __shared__ double rbuf[kThreads / 32][64];
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
     if (nf > 0) {
-        const double bestnu = best_stream_nu(scand, nscand);
+        const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
         const bool staged = stage_q != 0;
         if (staged)
             for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
@@ -1851,18 +1854,34 @@ void WideQrcp::gemv_step(int64_t t) {
         return e && *e == '1';
     }();
     if (no_guard) return;
+    // TTG_LAZY_GUARD=1 defers recomputes that cannot affect the next pivot (guard_defer);
+    // measured neutral on config 2 (stale columns are re-flagged every step), so the
+    // reference's eager recompute is the default.
+    static const int lazy = [] {
+        const char* e = std::getenv("TTG_LAZY_GUARD");
+        return e && *e == '1' ? 1 : 0;
+    }();
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
     if (k_ <= 32) {
         TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get(), ncand_,
-                   cand_.get() + ncand_, mass_.get() + ncand_);
+                   cand_.get() + ncand_, mass_.get() + ncand_, lazy);
     } else {
         // Q[:, :t+1] staged in shared memory when it fits
         const bool stage = gq <= 200 * 1024;
         allow_smem(k_guard, stage ? gq : 0);
         TTG_LAUNCH(k_guard, ngc_, kThreads, stage ? gq : 0, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), stage ? 1 : 0, pos_.get(),
-                   cand_.get(), ncand_, cand_.get() + ncand_, mass_.get() + ncand_);
+                   cand_.get(), ncand_, cand_.get() + ncand_, mass_.get() + ncand_, lazy);
+    }
+    static const bool flag_stats = [] {  // diagnostics: flags per step (host sync)
+        const char* e = std::getenv("TTG_DIAG_FLAGS");
+        return e && *e == '1';
+    }();
+    if (flag_stats) {
+        const int nf = nflag_.to_host(1)[0];
+        std::fprintf(stderr, "[ttg] step %lld (k %lld, N %lld): %d flagged\n", (long long)t, (long long)k_,
+                     (long long)N_, nf);
     }
 }
 
