@@ -78,8 +78,6 @@ __device__ int64_t pick_pivot(const TallView& s, int64_t t, int64_t* out_pos) {
 
 // Column norms of all n columns (partials per block, combined by k_norm_fin).
 __global__ void __launch_bounds__(kT) k_norm_part(TallView s, int64_t row0) {
-    __shared__ double acc[1];
-    (void)acc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t r0 = row0 + (int64_t)blockIdx.x * s.rpb;
     const int64_t r1 = min(s.N, r0 + s.rpb);
@@ -155,7 +153,6 @@ __global__ void __launch_bounds__(kT) k_house(TallView s, int64_t t, int nblk) {
     int64_t pp;
     const int64_t piv = pick_pivot(s, t, &pp);
     __shared__ double sh[4];
-    __shared__ double sd[kT / 32];
     // sigma: combine partials in block order.
     double sg = 0.0;
     if (threadIdx.x == 0) {
@@ -186,7 +183,6 @@ __global__ void __launch_bounds__(kT) k_house(TallView s, int64_t t, int nblk) {
         s.flag[0] = 0;
     }
     __syncthreads();
-    (void)sd;
     const double beta = sh[0], v0 = sh[1];
     for (int64_t q = t + 1 + threadIdx.x; q < s.n; q += kT) {
         const int64_t j = s.colmap[q];

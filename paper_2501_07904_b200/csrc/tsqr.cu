@@ -352,7 +352,6 @@ __global__ void __launch_bounds__(kT) k_tsqr_pair(const double* __restrict__ in,
     double* T1 = sm;
     double* T2 = sm + tri;
     __shared__ double red[kT / 32];
-    __shared__ double sc[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kT / 32;
     const int64_t r1 = (int64_t)blockIdx.x * 2 * s, r2 = r1 + s;
     const bool has2 = r2 < nrows;
@@ -397,7 +396,6 @@ __global__ void __launch_bounds__(kT) k_tsqr_pair(const double* __restrict__ in,
             }
             __syncthreads();
         }
-    (void)sc;
     for (int e = threadIdx.x; e < s * s; e += kT) {
         const int c = e / s, i = e - c * s;
         out[(int64_t)blockIdx.x * s + i + (int64_t)c * ldo] = i <= c ? T1[c * (c + 1) / 2 + i] : 0.0;
