@@ -106,6 +106,9 @@ private:
     DevBuf<double> rec_, recs_;  // sharded: this rank's pivot record, all ranks' records
     bool explicit_ = false;      // explicit k x k Q (long factorisations)
     DevBuf<double> Qx_, exz_;
+    bool coop_ = false;          // persistent cooperative step loop (small / medium W)
+    DevBuf<int> nflag2_;
+    bool coop_run(int64_t steps);
     DevBuf<int64_t> pos_, perm_, piv_, flags_;
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;

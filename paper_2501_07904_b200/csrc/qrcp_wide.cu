@@ -21,7 +21,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "engine.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace ttg {
 namespace {
@@ -376,7 +380,7 @@ __device__ void wy_y(const WY& s, int64_t t, int chunk, double* red) {
 // Reflector from y (make_householder, factor.cpp:24-38): every CTA derives the same
 // scalars from the chunk sigma partials; the chunk's rows of Y[:, t] are written and the
 // chunk's partial p = Y[:, :t]^T v computed.
-__device__ void wy_reflect(const WY& s, int64_t t, int chunk, bool record, double* red) {
+__device__ void wy_reflect(const WY& s, int64_t t, int chunk, bool record, double* red, bool local_vec = false) {
     __shared__ double sh[2];
     if (threadIdx.x == 0) {
         double sg = 0.0;
@@ -396,6 +400,8 @@ __device__ void wy_reflect(const WY& s, int64_t t, int chunk, bool record, doubl
         if (record) {
             s.diag[t] = rkk;
             s.beta[t] = beta;
+        }
+        if (record || local_vec) {
             s.vec[4 * s.cap] = v0;
             s.vec[4 * s.cap + 1] = beta;
         }
@@ -631,6 +637,216 @@ __global__ void k_set_identity(double* Qx, int64_t k) {
     const int64_t n = k * k;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
         Qx[e] = (e % (k + 1)) == 0 ? 1.0 : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent pass 1 for small and medium W (cooperative launch, one CTA per SM). A run of
+// steps t0..t1-1 is one kernel: every CTA keeps its own copy of Y and T in shared memory
+// and computes the step's reflector redundantly (same inputs, same arithmetic, so the
+// same bits everywhere), streams its block of columns, and the grid meets twice per
+// step -- after the stream (flags and candidates complete) and after the guard. No
+// kernel waits on another kernel; the only synchronisation is grid.sync inside one
+// cooperative launch. CTA 0 publishes Y[:, t], T[:, t], q_t, R_tt, beta and the
+// permutation bookkeeping. Each column's arithmetic is that of the per-step kernels:
+// VAR 0 (Col) = k_stream<1>'s warp per column, VAR 1 (Row) = k_stream<0>'s thread per
+// column.
+// ---------------------------------------------------------------------------
+struct CoopArgs {
+    WY g;            // global WY view (Y, T with ld cap, Qt, diag, beta, pos, perm, piv, cand ...)
+    double* R;
+    double* nu;
+    double* cref;
+    int64_t* flags;
+    int* nflag2;     // two flag counters, used by steps of alternating parity
+    Cand* cand;      // stream slots [0, G), guard slots [G, 2G)
+    double* mass;
+    int64_t t0, t1, capS;
+};
+
+size_t coop_smem_doubles(int64_t k, int64_t capS) {
+    const int64_t tld = capS | 1;
+    return (size_t)(k * capS + capS * tld + 3 * k + (capS + 1) + 4 * capS + 2 + 8);
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(kThreads, 1) k_pass1_coop(CoopArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double csm[];
+    __shared__ double red[kThreads / 32];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ int64_t pick_s[3];  // jp, pp, ct
+    const WY& g = A.g;
+    const int64_t k = g.k, N = g.N, capS = A.capS, tld = capS | 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    WY ls = g;
+    ls.cap = capS;
+    ls.tld = tld;
+    ls.nchunk = 1;
+    ls.rows = k;
+    ls.Y = csm;
+    ls.T = ls.Y + k * capS;
+    ls.wv = ls.T + capS * tld;
+    ls.yv = ls.wv + k;
+    double* qs = ls.yv + k;
+    ls.part = qs + k;
+    ls.vec = ls.part + (capS + 1);
+    for (int64_t e = tid; e < k * A.t0; e += kThreads) ls.Y[e] = g.Y[e];
+    for (int64_t e = tid; e < A.t0 * A.t0; e += kThreads) {
+        const int64_t c = e / A.t0, r = e - c * A.t0;
+        ls.T[r + c * tld] = g.T[r + c * g.cap];
+    }
+    // this CTA's columns
+    const int64_t per = cdiv(N, G), c0 = (int64_t)blockIdx.x * per, c1 = min(N, c0 + per);
+    __syncthreads();
+    for (int64_t t = A.t0; t < A.t1; ++t) {
+        // ---- pick (every CTA, identical): candidates of step t, no bookkeeping yet ----
+        Cand best = cand_none();
+        for (int i = tid; i < 2 * G; i += kThreads)
+            if (better(A.cand[i], best)) best = A.cand[i];
+        best = block_best(best, sc);
+        if (tid == 0) {
+            const bool none = best.col < 0;
+            pick_s[2] = g.perm[t];
+            pick_s[0] = none ? pick_s[2] : best.col;
+            pick_s[1] = none ? t : best.pos;
+        }
+        __syncthreads();
+        const int64_t jp = pick_s[0], pp = pick_s[1], ct = pick_s[2];
+        for (int64_t i = tid; i < k; i += kThreads) ls.wv[i] = ld_w(g.W, g.ld, g.layout, i, jp);
+        __syncthreads();
+        for (int64_t l = warp; l < t; l += kThreads / 32) {
+            const double* y = ls.Y + l * k;
+            double a = 0.0;
+            for (int64_t i = l + lane; i < k; i += 32) a = fma(y[i], ls.wv[i], a);
+            a = warp_sum(a);
+            if (lane == 0) ls.part[l] = a;
+        }
+        __syncthreads();
+        // ---- reflector, T column, q_t (the k_wy_fused_smem phases) ----
+        wy_sum_parts(ls, t, ls.vec, tid, kThreads);
+        __syncthreads();
+        wy_u(ls, t, tid, kThreads);
+        __syncthreads();
+        wy_y(ls, t, 0, red);
+        __syncthreads();
+        wy_reflect(ls, t, 0, blockIdx.x == 0, red, true);
+        __syncthreads();
+        wy_sum_parts(ls, t, ls.vec + 2 * capS, tid, kThreads);
+        __syncthreads();
+        wy_tcol(ls, t, tid, kThreads);
+        __syncthreads();
+        wy_g(ls, t, tid, kThreads);
+        __syncthreads();
+        {
+            const double* gv = ls.vec + 3 * capS;
+            for (int64_t i = tid; i < k; i += kThreads) {
+                double a = i == t ? 1.0 : 0.0;
+                for (int64_t l = 0; l <= t && l <= i; ++l) a = fma(-ls.Y[i + l * k], gv[l], a);
+                qs[i] = a;
+            }
+        }
+        __syncthreads();
+        if (blockIdx.x == 0) {
+            for (int64_t i = tid; i < k; i += kThreads) {
+                g.Qt[i + t * k] = qs[i];
+                g.Y[i + t * k] = ls.Y[i + t * k];
+            }
+            for (int64_t r = tid; r <= t; r += kThreads) g.T[r + t * g.cap] = ls.T[r + t * tld];
+        }
+        // ---- stream this CTA's columns ----
+        int* nflag = A.nflag2 + (t & 1);
+        Cand sbest = cand_none();
+        double msum = 0.0;
+        const double dt = (jp >= c0 && jp < c1) ? 0.0 : 0.0;  // (diag[t] is read below when needed)
+        (void)dt;
+        if (VAR == 0) {  // Col: warp per column (two in flight), lanes over rows
+            for (int64_t j = c0 + warp; j < c1; j += 2 * (kThreads / 32)) {
+                const int64_t j2 = j + kThreads / 32;
+                const bool two = j2 < c1;
+                const double* w = g.W + j * g.ld;
+                const double* w2 = g.W + (two ? j2 : j) * g.ld;
+                double a = 0.0, b = 0.0;
+                for (int64_t i = lane; i < k; i += 32) {
+                    a = fma(qs[i], w[i], a);
+                    b = fma(qs[i], w2[i], b);
+                }
+                a = warp_sum(a);
+                b = warp_sum(b);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && !two) break;
+                    const int64_t jj = h ? j2 : j;
+                    const int64_t pj = jj == jp ? t : (jj == ct ? pp : g.pos[jj]);
+                    if (pj < t || jj == jp) {
+                        if (lane == 0) A.R[t * N + jj] = jj == jp ? g.diag[t] : 0.0;
+                        continue;
+                    }
+                    if (lane == 0 && downdate(t, jj, N, h ? b : a, pj, A.R, A.nu, A.cref, sbest, msum))
+                        A.flags[atomicAdd(nflag, 1)] = jj;
+                }
+            }
+        } else {  // Row: thread per column, rows sequential
+            for (int64_t jb = c0; jb < c1; jb += kThreads) {
+                const int64_t j = jb + tid;
+                const bool active = j < c1;
+                const int64_t pj = !active ? 0 : (j == jp ? t : (j == ct ? pp : g.pos[j]));
+                const bool chosen = active && (pj < t || j == jp);
+                if (chosen) A.R[t * N + j] = j == jp ? g.diag[t] : 0.0;
+                bool fl = false;
+                if (active && !chosen) {
+                    double a = 0.0;
+                    for (int64_t i = 0; i < k; ++i) a = fma(qs[i], g.W[i * g.ld + j], a);
+                    fl = downdate(t, j, N, a, pj, A.R, A.nu, A.cref, sbest, msum);
+                }
+                append_flag(fl, j, A.flags, nflag);
+            }
+        }
+        sbest = block_best(sbest, sc);
+        msum = block_sum(msum, red);
+        if (tid == 0) {
+            A.cand[blockIdx.x] = sbest;
+            A.mass[blockIdx.x] = msum;
+        }
+        grid.sync();
+        // ---- bookkeeping (CTA 0) and guard (all CTAs) ----
+        if (blockIdx.x == 0 && tid == 0) {
+            g.perm[t] = jp;
+            g.perm[pp] = ct;
+            g.pos[jp] = t;
+            g.pos[ct] = pp;
+            g.piv[t] = jp;
+            A.nflag2[(t + 1) & 1] = 0;
+        }
+        const int nf = *nflag;
+        Cand gbest = cand_none();
+        double gsum = 0.0;
+        for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf; f += (int64_t)G * (kThreads / 32)) {
+            const int64_t j = A.flags[f];
+            double sq = 0.0;
+            for (int64_t i = lane; i < k; i += 32) {
+                double x = ld_w(g.W, g.ld, g.layout, i, j);
+                for (int64_t l = 0; l <= t; ++l) x = fma(-g.Qt[i + l * k], A.R[l * N + j], x);
+                sq = fma(x, x, sq);
+            }
+            sq = warp_sum(sq);
+            if (lane == 0) {
+                A.nu[j] = sq;
+                A.cref[j] = sq;
+                const int64_t pj = j == ct ? pp : g.pos[j];
+                const Cand c{sq, pj, j};
+                if (better(c, gbest)) gbest = c;
+                gsum += sq;
+            }
+        }
+        gbest = block_best(gbest, sc);
+        gsum = block_sum(gsum, red);
+        if (tid == 0) {
+            A.cand[G + blockIdx.x] = gbest;
+            A.mass[G + blockIdx.x] = gsum;
+        }
+        grid.sync();
+    }
 }
 
 // Multi-CTA phases (row chunks) and the small single-CTA glue between them.
@@ -1619,13 +1835,29 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 7 ? cdiv(N, 128) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 4 * kThreads) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
+    // small / medium W: the persistent cooperative step loop (one stream slot and one guard
+    // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps
+    {
+        static const bool no_coop = [] {
+            const char* e = std::getenv("TTG_NO_COOP");
+            return e && *e == '1';
+        }();
+        const bool shape_ok = (layout == Layout::Col && (mode_ == 1 || mode_ == 2)) ||
+                              (layout == Layout::Row && (mode_ == 0 || mode_ == 3 || mode_ == 7));
+        if (!no_coop && !shard && shape_ok && N <= 16384 &&
+            coop_smem_doubles(k, 32) * sizeof(double) <= 200 * 1024) {
+            coop_ = true;
+            ncand_ = sms;
+        }
+    }
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(Ng_); flags_.alloc(N);
     if (comm_) {
         rec_.alloc((size_t)(k + kRecHead));
         recs_.alloc((size_t)comm_->size() * (k + kRecHead));
     }
-    ngc_ = std::max(1, 2 * sms);
+    ngc_ = coop_ ? sms : std::max(1, 2 * sms);
+    if (coop_) { nflag2_.alloc(2); nflag2_.zero(); }
     cand_.alloc(ncand_ + ngc_); mass_.alloc(ncand_ + ngc_); nflag_.alloc(1); nflag_.zero();
     wv_.alloc(k); yv_.alloc(k);
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
@@ -1721,7 +1953,37 @@ double WideQrcp::refresh_exact() {
 void WideQrcp::run_to(int64_t steps) {
     steps = std::min(steps, p_);
     if (steps > cap_) grow(std::min(p_, std::max(steps, 2 * cap_)));
+    if (coop_ && steps > steps_ && coop_run(steps)) return;
     while (steps_ < steps) step();
+}
+
+bool WideQrcp::coop_run(int64_t steps) {
+    if (explicit_ || comm_) return false;
+    const size_t smem = coop_smem_doubles(k_, cap_) * sizeof(double);
+    if (smem > 200 * 1024) return false;
+    auto kern = layout_ == Layout::Col ? k_pass1_coop<0> : k_pass1_coop<1>;
+    allow_smem(kern, smem);
+    int per_sm = 0;
+    TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    if (per_sm < 1 || ncand_ > per_sm * sm_count()) return false;
+    CoopArgs A{WY{W_, k_, N_, ld_, (int)layout_, cap_, Y_.get(), T_.get(), Qt_.get(), wv_.get(), yv_.get(),
+                  part_.get(), vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(),
+                  nflag_.get(), cand_.get(), ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_, cap_},
+               R_.get(), nu_.get(), cref_.get(), flags_.get(), nflag2_.get(), cand_.get(), mass_.get(), steps_, steps,
+               cap_};
+    void* args[] = {&A};
+    double bytes = 0.0;
+    for (int64_t t = steps_; t < steps; ++t) bytes += 8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_;
+    // the flag counter of the first step starts at zero
+    TTG_CUDA(cudaMemsetAsync(nflag2_.get() + (steps_ & 1), 0, sizeof(int), stream()));
+    prof_begin();
+    TTG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)ncand_), dim3(kThreads),
+                                         args, smem, stream()));
+    count_launch();
+    if (debug_sync()) check_sync("k_pass1_coop", __FILE__, __LINE__);
+    prof_end(bytes, "k_pass1_coop (persistent step loop: reflector + stream + guard)");
+    steps_ = steps;
+    return true;
 }
 
 void WideQrcp::step() {
