@@ -222,3 +222,51 @@ def test_tall_cut_gram_fallback_ill_conditioned(dev, ref, method):
     # Householder engine
     dims, ranks = [8, 8, 96], [1, 8, 8, 1]
     _check_parity(dev, ref, shifted_hilbert(dims), dims, method, ranks=ranks)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+@pytest.mark.parametrize("eps", [0.3, 0.1, 0.01])
+def test_fixed_tol_guarantee(dev, ref, method, eps):
+    # test_tt_decomp.cpp:80-100 / acceptance 3: the prescribed-accuracy sweeps meet eps,
+    # and the device picks the reference's ranks
+    dims = [7, 8, 6, 9]
+    a = ref.gen_gaussian(dims, 17)
+    sweep = "l2r" if method == "ulv" else "r2l"
+    res = dev.decompose_device(a, dims, method, sweep, eps=eps)
+    assert res.rse(a) <= eps * (1 + 1e-12)
+    rr = ref.decompose(a, dims, method, sweep, eps=eps)
+    assert res.report().ranks_chosen == rr.ranks_chosen
+    assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
+
+
+def test_hilbert_error_decreases_with_eps(dev, ref):
+    # acceptance 9: Hilbert 20^3, the error strictly decreases as eps does
+    dims = [20, 20, 20]
+    a = shifted_hilbert(dims)
+    errs = [dev.decompose_device(a, dims, "urv", "r2l", eps=e).rse(a) for e in (1e-2, 1e-4, 1e-6, 1e-8)]
+    assert all(x > y for x, y in zip(errs, errs[1:])), errs
+    assert all(e <= t for e, t in zip(errs, (1e-2, 1e-4, 1e-6, 1e-8)))
+
+
+def test_weights_validation(dev):
+    from paper_2501_07904_b200._native import ArgumentError
+    dims = [4, 5, 6]
+    a = np.random.default_rng(0).standard_normal(int(np.prod(dims)))
+    with pytest.raises(ArgumentError, match="squared weights must sum to 1"):
+        dev.decompose_device(a, dims, "urv", "r2l", eps=0.1, weights=[0.5, 0.5])
+    with pytest.raises(ArgumentError, match="weights given, expected"):
+        dev.decompose_device(a, dims, "urv", "r2l", eps=0.1, weights=[1.0])
+    with pytest.raises(ArgumentError, match="tolerance must be >= 0"):
+        dev.decompose_device(a, dims, "urv", "r2l", eps=-1.0)
+    # valid unequal weights
+    w = [0.6, 0.8]
+    res = dev.decompose_device(a, dims, "urv", "r2l", eps=0.2, weights=w)
+    assert res.rse(a) <= 0.2 * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_order_two_fast_path(dev, ref, method):
+    dims, ranks = [30, 40], [1, 7, 1]
+    a = planted_plus_noise(ref, dims, ranks, 9, 1e-6)
+    _check_parity(dev, ref, a, dims, method, ranks=ranks)
+    _check_parity(dev, ref, a, dims, method, eps=1e-4)
