@@ -1180,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream_tma(const double* __rest
 // and reads both with one 16-byte load per row (512-byte segments per warp instruction),
 // q_t staged in shared memory. Each column's arithmetic is k_stream<0>'s (sequential over
 // the rows), so results are bitwise those of MODE 0.
+template <bool PF>
 __global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restrict__ W, int64_t k, int64_t N,
                                                           int64_t ld, int64_t t, const double* __restrict__ Q,
                                                           const double* diag, const int64_t* piv, double* R,
@@ -1201,11 +1202,29 @@ __global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restri
         double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         const int64_t pr0 = g0 + lane, pr1 = g0 + 32 + lane;
         const bool full0 = 2 * pr0 + 1 < N, full1 = 2 * pr1 + 1 < N;
+        // the epilogue's per-column state, requested before the row loop so its latency
+        // overlaps the stream
+        // (PF: short grids, where each thread streams one strip -- the epilogue's column
+        // state is requested before the row loop so its latency overlaps the stream)
+        int64_t pjv[2][2];
+        double nuv[2][2], crv[2][2];
+        if (PF) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                    const bool act = jj < N;
+                    pjv[u][h] = act ? pos[jj] : 0;
+                    nuv[u][h] = act ? nu[jj] : 0.0;
+                    crv[u][h] = act ? cref[jj] : 0.0;
+                }
+        }
         if (full0 && full1) {
             const double2* w0 = reinterpret_cast<const double2*>(W) + pr0;
             const double2* w1 = reinterpret_cast<const double2*>(W) + pr1;
             const int64_t ld2 = ld / 2;
-#pragma unroll 8
+#pragma unroll (PF ? 16 : 8)
             for (int64_t i = 0; i < k; ++i) {
                 const double2 x0 = __ldg(w0 + i * ld2), x1 = __ldg(w1 + i * ld2);
                 const double qi = q[i];
@@ -1230,11 +1249,14 @@ __global__ void __launch_bounds__(kThreads) k_stream_row2(const double* __restri
             for (int h = 0; h < 2; ++h) {
                 const int64_t jj = 2 * (u ? pr1 : pr0) + h;
                 const bool active = jj < N;
-                const int64_t pj = active ? pos[jj] : 0;
+                const int64_t pj = PF ? pjv[u][h] : (active ? pos[jj] : 0);
                 const bool chosen = active && (pj < t || jj == jp);
                 if (chosen) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
                 bool fl = false;
-                if (active && !chosen) fl = downdate(t, jj, N, a[u][h], pj, R, nu, cref, best, msum);
+                if (active && !chosen) {
+                    if (PF) fl = downdate_v(t, jj, N, a[u][h], pj, nuv[u][h], crv[u][h], R, nu, best, msum);
+                    else fl = downdate(t, jj, N, a[u][h], pj, R, nu, cref, best, msum);
+                }
                 append_flag(fl, jj, flags, nflag);
             }
     }
@@ -2077,8 +2099,11 @@ void WideQrcp::gemv_step(int64_t t) {
                    mass_.get());
     } else if (mode_ == 6) {
         const size_t smem = sizeof(double) * (size_t)k_;
-        allow_smem(k_stream_row2, smem);
-        TTG_LAUNCH(k_stream_row2, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(),
+        // short grids (every thread one strip) prefetch the epilogue state
+        const bool pf = N_ <= (int64_t)ncand_ * 4 * kThreads;
+        auto kern = pf ? k_stream_row2<true> : k_stream_row2<false>;
+        allow_smem(kern, smem);
+        TTG_LAUNCH(kern, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, t, qptr(), diag_.get(),
                    piv_.get(), R_.get(), nu_.get(), cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(),
                    mass_.get());
     } else if (mode_ == 5) {
