@@ -911,6 +911,10 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
         for (int64_t j = gw; j < N; j += 2 * nwarps) {
             const int64_t j2 = j + nwarps;
             const bool two = j2 < N;
+            // the epilogue's column state first: its latency overlaps the dot
+            const int64_t pjs[2] = {pos[j], two ? pos[j2] : 0};
+            const double nus[2] = {nu[j], two ? nu[j2] : 0.0};
+            const double crs[2] = {cref[j], two ? cref[j2] : 0.0};
             const double* w = W + j * ld;
             const double* w2 = W + (two ? j2 : j) * ld;
             double a = 0.0, b = 0.0;
@@ -924,12 +928,12 @@ __global__ void __launch_bounds__(kThreads) k_stream(const double* __restrict__ 
             for (int h = 0; h < 2; ++h) {
                 if (h == 1 && !two) break;
                 const int64_t jj = h ? j2 : j;
-                const int64_t pj = pos[jj];
+                const int64_t pj = pjs[h];
                 if (pj < t || jj == jp) {
                     if (lane == 0) R[t * N + jj] = jj == jp ? diag[t] : 0.0;
                     continue;
                 }
-                if (lane == 0 && downdate(t, jj, N, h ? b : a, pj, R, nu, cref, best, msum)) {
+                if (lane == 0 && downdate_v(t, jj, N, h ? b : a, pj, nus[h], crs[h], R, nu, best, msum)) {
                     const int slot = atomicAdd(nflag, 1);
                     flags[slot] = jj;
                 }
