@@ -1291,6 +1291,11 @@ __global__ void __launch_bounds__(kThreads) k_stream_splitk4(const double* __res
     for (int64_t j0 = (int64_t)blockIdx.x * 128; j0 < N; j0 += (int64_t)gridDim.x * 128) {
         const int64_t jl = j0 + 4 * lane;
         double a[4] = {0.0, 0.0, 0.0, 0.0};
+        // threads 0..127 finish column j0 + tid: request its state before the row loop
+        const int64_t jf = j0 + threadIdx.x;
+        const bool fin = threadIdx.x < 128 && jf < N;
+        const int64_t pjf = fin ? pos[jf] : 0;
+        const double nuf = fin ? nu[jf] : 0.0, crf = fin ? cref[jf] : 0.0;
         if (jl + 3 < N) {
             const double* base = W + jl;
 #pragma unroll 8
@@ -1320,10 +1325,10 @@ __global__ void __launch_bounds__(kThreads) k_stream_splitk4(const double* __res
 #pragma unroll
             for (int w = 0; w < kThreads / 32; ++w) sum += part[w][threadIdx.x];
             const bool active = j < N;
-            const int64_t pj = active ? pos[j] : 0;
+            const int64_t pj = pjf;
             const bool chosen = active && (pj < t || j == jp);
             if (chosen) R[t * N + j] = j == jp ? diag[t] : 0.0;
-            if (active && !chosen) fl = downdate(t, j, N, sum, pj, R, nu, cref, best, msum);
+            if (active && !chosen) fl = downdate_v(t, j, N, sum, pj, nuf, crf, R, nu, best, msum);
         }
         if (warp < 4) append_flag(fl, j, flags, nflag);
         __syncthreads();
