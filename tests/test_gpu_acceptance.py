@@ -80,3 +80,26 @@ def test_cpp_dropin_program(dev):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+
+
+@pytest.mark.parametrize("method,sweep", [("ulv", "l2r"), ("urv", "r2l")])
+@pytest.mark.parametrize("mode", ["rank", "tol"])
+def test_edge_shapes_random(dev, ref, method, sweep, mode):
+    """Ragged and degenerate shapes (modes of size 1, orders 2-6, wide and tall cuts, ranks
+    clamped by the shape), both rank modes, against the reference: identical ranks and
+    |dRSE| <= 1e-10."""
+    rng = np.random.default_rng(7 if mode == "rank" else 8)
+    for trial in range(40):
+        order = int(rng.integers(2, 7))
+        dims = [int(x) for x in rng.integers(1, 9 if order > 4 else 13, size=order)]
+        a = ref.gen_gaussian(dims, 5000 + trial)
+        if mode == "rank":
+            ranks = [1] + [int(rng.integers(1, 7)) for _ in range(order - 1)] + [1]
+            kw = dict(ranks=ranks)
+        else:
+            kw = dict(eps=float(rng.choice([0.5, 0.2, 0.05])))
+        res = dev.decompose_device(a, dims, method, sweep, **kw)
+        rr = ref.decompose(a, dims, method, sweep, **kw) if mode == "rank" else \
+            ref.decompose(a, dims, method, sweep, eps=kw["eps"])
+        assert res.report().ranks_chosen == rr.ranks_chosen, (trial, dims, kw)
+        assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= 1e-10, (trial, dims, kw)
