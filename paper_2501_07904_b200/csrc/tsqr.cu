@@ -535,6 +535,150 @@ __global__ void __launch_bounds__(512) k_small_qrcp(const double* __restrict__ A
     (void)tq;
 }
 
+// k_small_qrcp for n <= 32 columns with one warp per column (1024 threads): the pivot is
+// chosen by warp 0 (the strict '>' scan from position k as a warp argmax: first maximal
+// position, a NaN at position k keeps k), the reflector by the warp owning column k, and
+// each warp applies it to its own column and downdates that column's norm in the same
+// pass -- three barriers per step instead of five, no idle threads. Per-column arithmetic
+// is k_small_qrcp's (lanes over rows, warp tree), so R and the pivots are bitwise equal.
+__global__ void __launch_bounds__(1024) k_small_qrcp32(const double* __restrict__ A, int m, int n, int64_t lda,
+                                                      int64_t* perm_out, double* R, double* pnorm, double* Q,
+                                                      int want_q) {
+    extern __shared__ double sm[];
+    double* X = sm;                  // m x n
+    double* beta = X + (size_t)m * n; // p
+    __shared__ double nu[32], cref[32];
+    __shared__ int perm[32];
+    __shared__ int spiv;
+    __shared__ double sh[3];  // v0, beta, -smu of the step
+    const int p = min(m, n);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int c = warp; c < n; c += 32)
+        for (int i = lane; i < m; i += 32) X[c * m + i] = A[i + c * lda];
+    __syncthreads();
+    if (warp < n && lane == 0) {
+        double a = 0.0;
+        for (int i = 0; i < m; ++i) a = __dadd_rn(a, __dmul_rn(X[warp * m + i], X[warp * m + i]));
+        nu[warp] = a;
+        cref[warp] = a;
+        perm[warp] = warp;
+    }
+    __syncthreads();
+    for (int k = 0; k < p; ++k) {
+        if (warp == 0) {  // strict '>' scan from position k (factor.cpp:85-87)
+            const bool nan_k = isnan(nu[k]);
+            double v = (lane >= k && lane < n && !isnan(nu[lane])) ? nu[lane] : -INFINITY;
+            int idx = (lane >= k && lane < n) ? lane : 1 << 30;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+            }
+            if (lane == 0) {
+                // the scan keeps k unless a later value is strictly greater; -inf (all NaN) keeps k
+                int piv = idx;
+                if (nan_k || !(v > -INFINITY) || !(nu[piv] > nu[k])) piv = k;
+                spiv = piv;
+                pnorm[k] = nu[piv];
+            }
+        }
+        __syncthreads();
+        const int piv = spiv;
+        if (piv != k) {  // swap columns k and piv (warp k does the data, lane 0 of warp 0 the state)
+            if (warp == 0)
+                for (int i = lane; i < m; i += 32) {
+                    const double t = X[k * m + i];
+                    X[k * m + i] = X[piv * m + i];
+                    X[piv * m + i] = t;
+                }
+            if (threadIdx.x == 0) {
+                int ti = perm[k]; perm[k] = perm[piv]; perm[piv] = ti;
+                double td = nu[k]; nu[k] = nu[piv]; nu[piv] = td;
+                td = cref[k]; cref[k] = cref[piv]; cref[piv] = td;
+            }
+            __syncthreads();
+        }
+        // make_householder (factor.cpp:24-38) by warp 0
+        double* x = X + k * m;
+        if (warp == 0) {
+            double part = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) part = fma(x[i], x[i], part);
+            const double sigma = warp_sum(part);
+            const double alpha = x[k];
+            double b = 0.0, v0 = 1.0, smu = 0.0;
+            if (m - k > 1 && sigma != 0.0) {
+                const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sigma));
+                smu = copysign(mu, alpha);
+                v0 = __dadd_rn(alpha, smu);
+                b = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+                for (int i = k + 1 + lane; i < m; i += 32) x[i] = __ddiv_rn(x[i], v0);
+                __syncwarp();
+                if (lane == 0) x[k] = -smu;
+            }
+            if (lane == 0) beta[k] = b;
+        }
+        __syncthreads();
+        const double b = beta[k];
+        // apply_reflector to column j = warp (factor.cpp:43-58), then its downdate + guard
+        const int j = warp;
+        if (j > k && j < n) {
+            double* y = X + j * m;
+            if (b != 0.0) {
+                double t = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) t = fma(x[i], y[i], t);
+                t = warp_sum(t);
+                t = __dmul_rn(__dadd_rn(y[k], t), b);
+                for (int i = k + 1 + lane; i < m; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(t, x[i]));
+                __syncwarp();
+                if (lane == 0) y[k] = __dsub_rn(y[k], t);
+                __syncwarp();
+            }
+            double nv = 0.0;
+            if (lane == 0) {
+                const double rkj = y[k];
+                nv = __dsub_rn(nu[j], __dmul_rn(rkj, rkj));
+            }
+            nv = __shfl_sync(0xffffffffu, nv, 0);
+            if (nv < __dmul_rn(1e-16, cref[j]) || nv < 0.0) {
+                double a = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) a = fma(y[i], y[i], a);
+                a = warp_sum(a);
+                nv = a;
+                if (lane == 0) cref[j] = a;
+            }
+            if (lane == 0) nu[j] = nv;
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < p * n; e += blockDim.x) {
+        const int c = e / p, i = e - c * p;
+        R[i + (int64_t)c * p] = i <= c ? X[c * m + i] : 0.0;
+    }
+    for (int c = threadIdx.x; c < n; c += blockDim.x) perm_out[c] = perm[c];
+    if (!want_q) return;
+    for (int e = threadIdx.x; e < m * p; e += blockDim.x) {
+        const int c = e / m, i = e - c * m;
+        Q[i + (int64_t)c * m] = i == c ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int k = p - 1; k >= 0; --k) {
+        const double bk = beta[k];
+        if (bk == 0.0) continue;
+        const double* v = X + k * m;
+        const int c0 = warp;
+        if (c0 >= k && c0 < p) {
+            double* c = Q + (int64_t)c0 * m;
+            double t = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) t = fma(v[i], c[i], t);
+            t = warp_sum(t);
+            t = __dmul_rn(__dadd_rn(c[k], t), bk);
+            for (int i = k + 1 + lane; i < m; i += 32) c[i] = __dsub_rn(c[i], __dmul_rn(t, v[i]));
+            if (lane == 0) c[k] = __dsub_rn(c[k], t);
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 size_t small_qrcp_smem(int64_t m, int64_t n) {
@@ -546,6 +690,12 @@ bool small_qrcp_fits(int64_t m, int64_t n) { return small_qrcp_smem(m, n) <= 220
 
 void small_qrcp(const double* A, int64_t m, int64_t n, int64_t lda, int64_t* perm, double* R, double* pnorm,
                 double* Q) {
+    if (n <= 32) {
+        const size_t smem = sizeof(double) * (size_t)(m * n + std::min(m, n));
+        allow_smem(k_small_qrcp32, smem);
+        TTG_LAUNCH(k_small_qrcp32, 1, 1024, smem, stream(), A, (int)m, (int)n, lda, perm, R, pnorm, Q, Q ? 1 : 0);
+        return;
+    }
     const size_t smem = small_qrcp_smem(m, n);
     allow_smem(k_small_qrcp, smem);
     TTG_LAUNCH(k_small_qrcp, 1, 512, smem, stream(), A, (int)m, (int)n, lda, perm, R, pnorm, Q, Q ? 1 : 0);
