@@ -78,6 +78,22 @@ int64_t prof_read(double* total_ms, double* bytes);
 int prof_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches);
 void prof_reset_kernels();
 
+// TTG_PHASES=1 (diagnostics): event-timed phases on the thread's stream, totals printed at
+// exit. Use as `PhaseTimer pt("name");` around a phase.
+bool phases_on();
+cudaEvent_t phase_mark();
+void phase_add(cudaEvent_t begin, const char* name);
+struct PhaseTimer {
+    cudaEvent_t a = nullptr;
+    const char* name;
+    explicit PhaseTimer(const char* n) : name(n) {
+        if (phases_on()) a = phase_mark();
+    }
+    ~PhaseTimer() {
+        if (a) phase_add(a, name);
+    }
+};
+
 // Stream-ordered device allocation (cudaMallocAsync on the thread's stream).
 template <class T>
 class DevBuf {

@@ -106,6 +106,8 @@ private:
     DevBuf<double> rec_, recs_;  // sharded: this rank's pivot record, all ranks' records
     bool explicit_ = false;      // explicit k x k Q (long factorisations)
     DevBuf<double> Qx_, exz_;
+    DevBuf<double> Wt_;  // row-layout copy of a narrow Col W for k_pass1_big<5>
+    bool big_ = false;           // ... with the large-W stream variants (k_pass1_big)
     bool coop_ = false;          // persistent cooperative step loop (small / medium W)
     DevBuf<int> nflag2_;
     bool coop_run(int64_t steps);

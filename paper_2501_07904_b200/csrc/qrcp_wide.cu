@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include <cooperative_groups.h>
 
@@ -405,6 +406,7 @@ __device__ void wy_reflect(const WY& s, int64_t t, int chunk, bool record, doubl
             s.vec[4 * s.cap] = v0;
             s.vec[4 * s.cap + 1] = beta;
         }
+        if (local_vec) s.vec[4 * s.cap + 2] = rkk;  // R(t, piv) for this CTA's stream
     }
     __syncthreads();
     const double v0 = sh[0], beta = sh[1];
@@ -661,6 +663,9 @@ struct CoopArgs {
     Cand* cand;      // stream slots [0, G), guard slots [G, 2G)
     double* mass;
     int64_t t0, t1, capS;
+    const double* Ws;           // k_pass1_big<5>: row-layout copy of W (ld lds)
+    int64_t lds;
+    unsigned long long* trace;  // TTG_BIG_TRACE: CTA 0 phase timestamps, 8 per step
 };
 
 size_t coop_smem_doubles(int64_t k, int64_t capS) {
@@ -758,8 +763,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_coop(CoopArgs A) {
         int* nflag = A.nflag2 + (t & 1);
         Cand sbest = cand_none();
         double msum = 0.0;
-        const double dt = (jp >= c0 && jp < c1) ? 0.0 : 0.0;  // (diag[t] is read below when needed)
-        (void)dt;
         if (VAR == 0) {  // Col: warp per column (two in flight), lanes over rows
             for (int64_t j = c0 + warp; j < c1; j += 2 * (kThreads / 32)) {
                 const int64_t j2 = j + kThreads / 32;
@@ -779,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_coop(CoopArgs A) {
                     const int64_t jj = h ? j2 : j;
                     const int64_t pj = jj == jp ? t : (jj == ct ? pp : g.pos[jj]);
                     if (pj < t || jj == jp) {
-                        if (lane == 0) A.R[t * N + jj] = jj == jp ? g.diag[t] : 0.0;
+                        if (lane == 0) A.R[t * N + jj] = jj == jp ? ls.vec[4 * capS + 2] : 0.0;
                         continue;
                     }
                     if (lane == 0 && downdate(t, jj, N, h ? b : a, pj, A.R, A.nu, A.cref, sbest, msum))
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_coop(CoopArgs A) {
                 const bool active = j < c1;
                 const int64_t pj = !active ? 0 : (j == jp ? t : (j == ct ? pp : g.pos[j]));
                 const bool chosen = active && (pj < t || j == jp);
-                if (chosen) A.R[t * N + j] = j == jp ? g.diag[t] : 0.0;
+                if (chosen) A.R[t * N + j] = j == jp ? ls.vec[4 * capS + 2] : 0.0;
                 bool fl = false;
                 if (active && !chosen) {
                     double a = 0.0;
@@ -1794,6 +1797,411 @@ __global__ void __launch_bounds__(kThreads) k_refresh_rowt(const double* __restr
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent pass 1 for large W (cooperative launch, one CTA per SM): the k_pass1_coop
+// step loop with streaming loops built for large W (VAR = the per-step kernel's MODE):
+//   5: Col, k <= 32, ld == k  -- thread per column, 16-byte loads of its contiguous rows
+//   6: Row, 16-byte pairs     -- thread per two adjacent columns (k_stream_row2<true>)
+//   7: Row, few columns       -- 128-column strips, rows split over the warps (k_stream_splitk4)
+//   1: Col, k > 64            -- warp per column, two in flight (k_stream<1>)
+// Per step: every CTA picks the pivot from the previous step's candidate slots and builds
+// the reflector redundantly in shared memory (same inputs, same bits), streams its
+// columns, meets the grid, recomputes its share of the flagged norms with the per-step
+// guards' arithmetic (k_guard_lane for k <= 32 from Q in shared memory, k_guard above),
+// and meets the grid again: one launch per run of steps instead of three per step.
+// VARs 6, 7 and 1 sum each column exactly as their per-step kernels (bitwise the same
+// results); VAR 5 sums rows in order (k_stream<0>'s order) instead of k_stream_tma's
+// warp tree, so the persistent and per-step paths of that shape agree to rounding.
+// ---------------------------------------------------------------------------
+__host__ __device__ size_t big_smem_doubles(int64_t k, int64_t capS) {
+    const int64_t tld = capS | 1;
+    size_t d = (size_t)(k * capS + capS * tld + 3 * k + (capS + 1) + 4 * capS + 2 + 8);
+    if (k <= 32) d += (size_t)(k * capS);  // Q[:, :t+1] for the lane guard
+    return d;
+}
+constexpr size_t kBigSmemMax = 200 * 1024;
+
+// Row-layout copy of a narrow Col W (k <= 32, ld == k): Wt[i * ldt + j] = W[i + j * k],
+// 64 columns per CTA through shared memory (coalesced reads of the contiguous block,
+// coalesced row writes).
+__global__ void __launch_bounds__(kThreads) k_narrow_to_rows(const double* __restrict__ W, int64_t k, int64_t N,
+                                                             double* __restrict__ Wt, int64_t ldt) {
+    __shared__ double tile[32][65];
+    const int64_t j0 = (int64_t)blockIdx.x * 64;
+    const int nc = (int)min((int64_t)64, N - j0);
+    for (int e = threadIdx.x; e < nc * k; e += kThreads) {
+        const int c = e / (int)k, i = e - c * (int)k;
+        tile[i][c] = W[j0 * k + e];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * k; e += kThreads) {
+        const int i = e / 64, c = e - i * 64;
+        if (c < nc) Wt[i * ldt + j0 + c] = tile[i][c];
+    }
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) double csm[];
+    __shared__ double red[kThreads / 32];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ int64_t pick_s[3];  // jp, pp, ct
+    __shared__ double part7[VAR == 7 ? kThreads / 32 : 1][129];
+    __shared__ double rbuf[VAR == 5 ? 1 : kThreads / 32][64];
+    const WY& g = A.g;
+    const int64_t k = g.k, N = g.N, capS = A.capS, tld = capS | 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    WY ls = g;
+    ls.cap = capS;
+    ls.tld = tld;
+    ls.nchunk = 1;
+    ls.rows = k;
+    ls.Y = csm;
+    ls.T = ls.Y + k * capS;
+    ls.wv = ls.T + capS * tld;
+    ls.yv = ls.wv + k;
+    double* qs = ls.yv + k;
+    ls.part = qs + k;
+    ls.vec = ls.part + (capS + 1);
+    double* Qs = ls.vec + 4 * capS + 2 + 8;  // k x capS (k <= 32)
+    for (int64_t e = tid; e < k * A.t0; e += kThreads) ls.Y[e] = g.Y[e];
+    if (k <= 32)
+        for (int64_t e = tid; e < k * A.t0; e += kThreads) Qs[e] = g.Qt[e];
+    for (int64_t e = tid; e < A.t0 * A.t0; e += kThreads) {
+        const int64_t c = e / A.t0, r = e - c * A.t0;
+        ls.T[r + c * tld] = g.T[r + c * g.cap];
+    }
+    __syncthreads();
+    auto stamp = [&](int64_t t, int ph) {
+        if (A.trace && blockIdx.x == 0 && tid == 0) {
+            unsigned long long ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            A.trace[(t - A.t0) * 8 + ph] = ns;
+        }
+    };
+    for (int64_t t = A.t0; t < A.t1; ++t) {
+        stamp(t, 0);
+        // ---- pick (every CTA, identical): candidates of step t ----
+        Cand best = cand_none();
+        for (int i = tid; i < 2 * G; i += kThreads)
+            if (better(A.cand[i], best)) best = A.cand[i];
+        best = block_best(best, sc);
+        if (tid == 0) {
+            const bool none = best.col < 0;
+            pick_s[2] = g.perm[t];
+            pick_s[0] = none ? pick_s[2] : best.col;
+            pick_s[1] = none ? t : best.pos;
+        }
+        __syncthreads();
+        const int64_t jp = pick_s[0], pp = pick_s[1], ct = pick_s[2];
+        for (int64_t i = tid; i < k; i += kThreads) ls.wv[i] = ld_w(g.W, g.ld, g.layout, i, jp);
+        __syncthreads();
+        for (int64_t l = warp; l < t; l += kThreads / 32) {
+            const double* y = ls.Y + l * k;
+            double a = 0.0;
+            for (int64_t i = l + lane; i < k; i += 32) a = fma(y[i], ls.wv[i], a);
+            a = warp_sum(a);
+            if (lane == 0) ls.part[l] = a;
+        }
+        __syncthreads();
+        // ---- reflector, T column, q_t (the k_wy_fused_smem phases) ----
+        wy_sum_parts(ls, t, ls.vec, tid, kThreads);
+        __syncthreads();
+        wy_u(ls, t, tid, kThreads);
+        __syncthreads();
+        wy_y(ls, t, 0, red);
+        __syncthreads();
+        wy_reflect(ls, t, 0, blockIdx.x == 0, red, true);
+        __syncthreads();
+        wy_sum_parts(ls, t, ls.vec + 2 * capS, tid, kThreads);
+        __syncthreads();
+        wy_tcol(ls, t, tid, kThreads);
+        __syncthreads();
+        wy_g(ls, t, tid, kThreads);
+        __syncthreads();
+        {
+            const double* gv = ls.vec + 3 * capS;
+            for (int64_t i = tid; i < k; i += kThreads) {
+                double a = i == t ? 1.0 : 0.0;
+                for (int64_t l = 0; l <= t && l <= i; ++l) a = fma(-ls.Y[i + l * k], gv[l], a);
+                qs[i] = a;
+                if (k <= 32) Qs[i + t * k] = a;
+            }
+        }
+        __syncthreads();
+        const double dgt = ls.vec[4 * capS + 2];
+        stamp(t, 1);
+        if (blockIdx.x == 0) {
+            for (int64_t i = tid; i < k; i += kThreads) {
+                g.Qt[i + t * k] = qs[i];
+                g.Y[i + t * k] = ls.Y[i + t * k];
+            }
+            for (int64_t r = tid; r <= t; r += kThreads) g.T[r + t * g.cap] = ls.T[r + t * tld];
+        }
+        // ---- stream this CTA's columns (the per-step kernels' arithmetic) ----
+        int* nflag = A.nflag2 + (t & 1);
+        Cand sbest = cand_none();
+        double msum = 0.0;
+        // position of column j during step t (CTA 0 applies the swap after the grid sync)
+        auto posof = [&](int64_t j) -> int64_t { return j == jp ? t : (j == ct ? pp : g.pos[j]); };
+        const double* __restrict__ Ws = VAR == 5 ? A.Ws : g.W;
+        const int64_t lds = VAR == 5 ? A.lds : g.ld;
+        if (VAR == 5 || VAR == 6) {
+            // VAR 5 streams the row-layout copy of a narrow Col W (A.Ws, made once per cut).
+            // A thread owns two column pairs (16-byte loads, 1 KB contiguous per warp and
+            // row), rows summed in order (k_stream<0>'s arithmetic).
+            const int64_t npair = (N + 1) / 2, ld2 = lds / 2;
+            const double2* __restrict__ W2 = reinterpret_cast<const double2*>(Ws);
+            {
+            for (int64_t g0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 64; g0 < npair;
+                 g0 += (int64_t)G * (kThreads / 32) * 64) {
+                double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                const int64_t pr0 = g0 + lane, pr1 = g0 + 32 + lane;
+                const bool full0 = 2 * pr0 + 1 < N, full1 = 2 * pr1 + 1 < N;
+                int64_t pjv[2][2];
+                double nuv[2][2], crv[2][2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                        const bool act = jj < N;
+                        pjv[u][h] = act ? posof(jj) : 0;
+                        nuv[u][h] = act ? A.nu[jj] : 0.0;
+                        crv[u][h] = act ? A.cref[jj] : 0.0;
+                    }
+                if (full0 && full1) {
+                    const double2* w0 = W2 + pr0;
+                    const double2* w1 = W2 + pr1;
+#pragma unroll 16
+                    for (int64_t i = 0; i < k; ++i) {
+                        const double2 x0 = __ldg(w0 + i * ld2), x1 = __ldg(w1 + i * ld2);
+                        const double qi = qs[i];
+                        a[0][0] = fma(qi, x0.x, a[0][0]);
+                        a[0][1] = fma(qi, x0.y, a[0][1]);
+                        a[1][0] = fma(qi, x1.x, a[1][0]);
+                        a[1][1] = fma(qi, x1.y, a[1][1]);
+                    }
+                } else {
+                    for (int64_t i = 0; i < k; ++i)
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                                if (jj < N) a[u][h] = fma(qs[i], Ws[i * lds + jj], a[u][h]);
+                            }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t jj = 2 * (u ? pr1 : pr0) + h;
+                        const bool active = jj < N;
+                        const int64_t pj = pjv[u][h];
+                        const bool chosen = active && (pj < t || jj == jp);
+                        if (chosen) A.R[t * N + jj] = jj == jp ? dgt : 0.0;
+                        bool fl = false;
+                        if (active && !chosen)
+                            fl = downdate_v(t, jj, N, a[u][h], pj, nuv[u][h], crv[u][h], A.R, A.nu, sbest, msum);
+                        append_flag(fl, jj, A.flags, nflag);
+                    }
+            }
+            }
+        } else if (VAR == 7) {
+            for (int64_t j0 = (int64_t)blockIdx.x * 128; j0 < N; j0 += (int64_t)G * 128) {
+                const int64_t jl = j0 + 4 * lane;
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
+                const int64_t jf = j0 + tid;
+                const bool fin = tid < 128 && jf < N;
+                const int64_t pjf = fin ? posof(jf) : 0;
+                const double nuf = fin ? A.nu[jf] : 0.0, crf = fin ? A.cref[jf] : 0.0;
+                if (jl + 3 < N) {
+                    const double* b = g.W + jl;
+#pragma unroll 8
+                    for (int64_t i = warp; i < k; i += kThreads / 32) {
+                        const double2 x0 = __ldg(reinterpret_cast<const double2*>(b + i * g.ld));
+                        const double2 x1 = __ldg(reinterpret_cast<const double2*>(b + i * g.ld) + 1);
+                        const double qi = qs[i];
+                        a[0] = fma(qi, x0.x, a[0]);
+                        a[1] = fma(qi, x0.y, a[1]);
+                        a[2] = fma(qi, x1.x, a[2]);
+                        a[3] = fma(qi, x1.y, a[3]);
+                    }
+                } else {
+                    for (int64_t i = warp; i < k; i += kThreads / 32)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (jl + c < N) a[c] = fma(qs[i], g.W[i * g.ld + jl + c], a[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) part7[warp][4 * lane + c] = a[c];
+                __syncthreads();
+                bool fl = false;
+                const int64_t j = j0 + tid;
+                if (tid < 128) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < kThreads / 32; ++w) sum += part7[w][tid];
+                    const bool active = j < N;
+                    const bool chosen = active && (pjf < t || j == jp);
+                    if (chosen) A.R[t * N + j] = j == jp ? dgt : 0.0;
+                    if (active && !chosen) fl = downdate_v(t, j, N, sum, pjf, nuf, crf, A.R, A.nu, sbest, msum);
+                }
+                if (warp < 4) append_flag(fl, j, A.flags, nflag);
+                __syncthreads();
+            }
+        } else {  // VAR 1
+            const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+            const int64_t nwarps = (int64_t)G * (kThreads / 32);
+            for (int64_t j = gw; j < N; j += 2 * nwarps) {
+                const int64_t j2 = j + nwarps;
+                const bool two = j2 < N;
+                const int64_t pjs[2] = {posof(j), two ? posof(j2) : 0};
+                const double nus[2] = {A.nu[j], two ? A.nu[j2] : 0.0};
+                const double crs[2] = {A.cref[j], two ? A.cref[j2] : 0.0};
+                const double* w = g.W + j * g.ld;
+                const double* w2 = g.W + (two ? j2 : j) * g.ld;
+                double a = 0.0, b = 0.0;
+#pragma unroll 6
+                for (int64_t i = lane; i < k; i += 32) {
+                    a = fma(qs[i], w[i], a);
+                    b = fma(qs[i], w2[i], b);
+                }
+                a = warp_sum(a);
+                b = warp_sum(b);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && !two) break;
+                    const int64_t jj = h ? j2 : j;
+                    const int64_t pj = pjs[h];
+                    if (pj < t || jj == jp) {
+                        if (lane == 0) A.R[t * N + jj] = jj == jp ? dgt : 0.0;
+                        continue;
+                    }
+                    if (lane == 0 && downdate_v(t, jj, N, h ? b : a, pj, nus[h], crs[h], A.R, A.nu, sbest, msum))
+                        A.flags[atomicAdd(nflag, 1)] = jj;
+                }
+            }
+        }
+        sbest = block_best(sbest, sc);
+        msum = block_sum(msum, red);
+        if (tid == 0) {
+            A.cand[blockIdx.x] = sbest;
+            A.mass[blockIdx.x] = msum;
+        }
+        stamp(t, 2);
+        grid.sync();
+        stamp(t, 3);
+        // ---- bookkeeping (CTA 0) and guard (all CTAs) ----
+        if (blockIdx.x == 0 && tid == 0) {
+            g.perm[t] = jp;
+            g.perm[pp] = ct;
+            g.pos[jp] = t;
+            g.pos[ct] = pp;
+            g.piv[t] = jp;
+            A.nflag2[(t + 1) & 1] = 0;
+        }
+        const int nf = *nflag;
+        Cand gbest = cand_none();
+        double gsum = 0.0;
+        if (k <= 32) {
+            // k_guard_lane<32>'s arithmetic (thread per column, modified Gram-Schmidt residual
+            // against Q[:, :t+1] in shared memory), two columns per thread sharing the q loads
+            const int64_t nthr = (int64_t)G * kThreads;
+            const int64_t th = (int64_t)blockIdx.x * kThreads + tid;
+            for (int64_t f = th; f < nf; f += 2 * nthr) {
+                const int64_t f2 = f + nthr;
+                const bool two = f2 < nf;
+                const int64_t j = A.flags[f], j2 = two ? A.flags[f2] : j;
+                double x[32], y[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    x[i] = i < k ? ld_w(g.W, g.ld, g.layout, i, j) : 0.0;
+                    y[i] = i < k ? ld_w(g.W, g.ld, g.layout, i, j2) : 0.0;
+                }
+                for (int64_t l = 0; l <= t; ++l) {
+                    const double* q = Qs + l * k;
+                    double z = 0.0, z2 = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < k) {
+                            const double qi = q[i];
+                            z = fma(qi, x[i], z);
+                            z2 = fma(qi, y[i], z2);
+                        }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < k) {
+                            const double qi = q[i];
+                            x[i] = fma(-qi, z, x[i]);
+                            y[i] = fma(-qi, z2, y[i]);
+                        }
+                }
+                double sq = 0.0, sq2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    sq = fma(x[i], x[i], sq);
+                    sq2 = fma(y[i], y[i], sq2);
+                }
+                A.nu[j] = sq;
+                A.cref[j] = sq;
+                const Cand c{sq, j == ct ? pp : g.pos[j], j};
+                if (better(c, gbest)) gbest = c;
+                gsum += sq;
+                if (two) {
+                    A.nu[j2] = sq2;
+                    A.cref[j2] = sq2;
+                    const Cand c2{sq2, j2 == ct ? pp : g.pos[j2], j2};
+                    if (better(c2, gbest)) gbest = c2;
+                    gsum += sq2;
+                }
+            }
+        } else if (VAR != 5) {  // k_guard: warp per column, R(0:t, j) staged per warp
+            const bool rsm = t + 1 <= 64;
+            for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
+                 f += (int64_t)G * (kThreads / 32)) {
+                const int64_t j = A.flags[f];
+                if (rsm) {
+                    for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = A.R[l * N + j];
+                    __syncwarp();
+                }
+                double sq = 0.0;
+                for (int64_t i = lane; i < k; i += 32) {
+                    double x = ld_w(g.W, g.ld, g.layout, i, j);
+                    for (int64_t l = 0; l <= t; ++l) x = fma(-g.Qt[i + l * k], rsm ? rbuf[warp][l] : A.R[l * N + j], x);
+                    sq = fma(x, x, sq);
+                }
+                sq = warp_sum(sq);
+                if (lane == 0) {
+                    A.nu[j] = sq;
+                    A.cref[j] = sq;
+                    const Cand c{sq, j == ct ? pp : g.pos[j], j};
+                    if (better(c, gbest)) gbest = c;
+                    gsum += sq;
+                }
+                __syncwarp();
+            }
+        }
+        gbest = block_best(gbest, sc);
+        gsum = block_sum(gsum, red);
+        if (tid == 0) {
+            A.cand[G + blockIdx.x] = gbest;
+            A.mass[G + blockIdx.x] = gsum;
+        }
+        stamp(t, 4);
+        grid.sync();
+        stamp(t, 5);
+        if (A.trace && blockIdx.x == 0 && tid == 0) A.trace[(t - A.t0) * 8 + 6] = (unsigned long long)nf;
+    }
+}
+
 // Empty guard slots (after init / exact refresh, which cover every column themselves).
 __global__ void k_clear_slots(Cand* cand, double* mass, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1873,11 +2281,42 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_NO_COOP");
             return e && *e == '1';
         }();
-        const bool shape_ok = (layout == Layout::Col && (mode_ == 1 || mode_ == 2)) ||
-                              (layout == Layout::Row && (mode_ == 0 || mode_ == 3 || mode_ == 7));
-        if (!no_coop && !shard && shape_ok && N <= 16384 &&
+        static const int64_t coop_maxn = [] {  // experiment: TTG_COOP_MAXN
+            const char* e = std::getenv("TTG_COOP_MAXN");
+            return e ? (int64_t)std::atoll(e) : (int64_t)16384;
+        }();
+        const bool shape_ok = (layout == Layout::Col && (mode_ == 1 || mode_ == 2 || (mode_ == 5 && N > 16384))) ||
+                              (layout == Layout::Row && (mode_ == 0 || mode_ == 3 || mode_ == 7 || (mode_ == 6 && N > 16384)));
+        if (!no_coop && !shard && shape_ok && N <= coop_maxn &&
             coop_smem_doubles(k, 32) * sizeof(double) <= 200 * 1024) {
             coop_ = true;
+            ncand_ = sms;
+        }
+        // large W: the persistent step loop with the per-step kernels' stream arithmetic
+        // (TTG_BIG=0 disables it; TTG_BIG_MODES lists the stream modes it takes)
+        static const bool no_big = [] {
+            const char* e = std::getenv("TTG_BIG");
+            return e && *e == '0';
+        }();
+        static const std::string big_modes = [] {
+            const char* e = std::getenv("TTG_BIG_MODES");
+            return std::string(e ? e : "56");
+        }();
+        // W larger than this streams long enough per step that the per-step kernels' full
+        // occupancy beats the saved launches (measured: config 3's 24 x 7,962,624 cut)
+        static const double big_max_bytes = [] {
+            const char* e = std::getenv("TTG_BIG_MAXMB");
+            return (e ? std::atof(e) : 768.0) * 1048576.0;
+        }();
+        static const bool lazy_env = [] {
+            const char* e = std::getenv("TTG_LAZY_GUARD");
+            return e && *e == '1';
+        }();
+        if (!coop_ && !no_big && !no_coop && !shard && !lazy_env && N > 16384 &&
+            8.0 * (double)k * (double)N <= big_max_bytes &&
+            big_modes.find((char)('0' + mode_)) != std::string::npos &&
+            big_smem_doubles(k, 32) * sizeof(double) <= kBigSmemMax) {
+            coop_ = big_ = true;
             ncand_ = sms;
         }
     }
@@ -1990,9 +2429,14 @@ void WideQrcp::run_to(int64_t steps) {
 
 bool WideQrcp::coop_run(int64_t steps) {
     if (explicit_ || comm_) return false;
-    const size_t smem = coop_smem_doubles(k_, cap_) * sizeof(double);
+    PhaseTimer pt(big_ ? "p1 persistent (big)" : "p1 persistent (coop)");
+    const size_t smem = (big_ ? big_smem_doubles(k_, cap_) : coop_smem_doubles(k_, cap_)) * sizeof(double);
     if (smem > 200 * 1024) return false;
-    auto kern = layout_ == Layout::Col ? k_pass1_coop<0> : k_pass1_coop<1>;
+    auto kern = !big_        ? (layout_ == Layout::Col ? k_pass1_coop<0> : k_pass1_coop<1>)
+                : mode_ == 5 ? k_pass1_big<5>
+                : mode_ == 6 ? k_pass1_big<6>
+                : mode_ == 7 ? k_pass1_big<7>
+                             : k_pass1_big<1>;
     allow_smem(kern, smem);
     int per_sm = 0;
     TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
@@ -2001,7 +2445,27 @@ bool WideQrcp::coop_run(int64_t steps) {
                   part_.get(), vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(),
                   nflag_.get(), cand_.get(), ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_, cap_},
                R_.get(), nu_.get(), cref_.get(), flags_.get(), nflag2_.get(), cand_.get(), mass_.get(), steps_, steps,
-               cap_};
+               cap_, nullptr, 0, nullptr};
+    if (big_ && mode_ == 5) {  // stream a row-layout copy of the narrow W (16-byte paired loads)
+        const int64_t ldt = (N_ + 1) & ~int64_t(1);
+        if (!Wt_.get()) {
+            Wt_.alloc((size_t)(k_ * ldt));
+            const dim3 grid((unsigned)cdiv(N_, 64));
+            TTG_LAUNCH(k_narrow_to_rows, grid, kThreads, 0, stream(), W_, k_, N_, Wt_.get(), ldt);
+        }
+        A.Ws = Wt_.get();
+        A.lds = ldt;
+    }
+    static const bool trace = [] {
+        const char* e = std::getenv("TTG_BIG_TRACE");
+        return e && *e == '1';
+    }();
+    DevBuf<unsigned long long> tr;
+    if (trace && big_) {
+        tr.alloc((size_t)(steps - steps_) * 8);
+        tr.zero();
+        A.trace = tr.get();
+    }
     void* args[] = {&A};
     double bytes = 0.0;
     for (int64_t t = steps_; t < steps; ++t) bytes += 8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_;
@@ -2012,7 +2476,24 @@ bool WideQrcp::coop_run(int64_t steps) {
                                          args, smem, stream()));
     count_launch();
     if (debug_sync()) check_sync("k_pass1_coop", __FILE__, __LINE__);
-    prof_end(bytes, "k_pass1_coop (persistent step loop: reflector + stream + guard)");
+    if (A.trace) {
+        std::vector<unsigned long long> h = tr.to_host((size_t)(steps - steps_) * 8);
+        for (int64_t t = 0; t < steps - steps_; ++t) {
+            const unsigned long long* r = h.data() + t * 8;
+            std::fprintf(stderr,
+                         "[ttg big] k %lld N %lld step %lld: refl %.1f stream %.1f sync %.1f guard %.1f (nf %llu) sync "
+                         "%.1f us\n",
+                         (long long)k_, (long long)N_, (long long)(steps_ + t), 1e-3 * (double)(r[1] - r[0]),
+                         1e-3 * (double)(r[2] - r[1]), 1e-3 * (double)(r[3] - r[2]), 1e-3 * (double)(r[4] - r[3]),
+                         r[6], 1e-3 * (double)(r[5] - r[4]));
+        }
+    }
+    static const char* const kBigNames[] = {
+        "k_pass1_big<1> (persistent step loop, warp per column)", "", "", "", "",
+        "k_pass1_big<5> (persistent step loop, row-layout copy, 16-byte paired columns)",
+        "k_pass1_big<6> (persistent step loop, 16-byte paired columns)",
+        "k_pass1_big<7> (persistent step loop, 128-column strips)"};
+    prof_end(bytes, big_ ? kBigNames[mode_] : "k_pass1_coop (persistent step loop: reflector + stream + guard)");
     steps_ = steps;
     return true;
 }
@@ -2021,8 +2502,11 @@ void WideQrcp::step() {
     const int64_t t = steps_;
     // explicit Q once t is large enough that O(t^2) WY work beats a k x k rank-1 update
     if (!explicit_ && !comm_ && t >= 256 && k_ <= 8192 && 2 * t >= k_ / 4) to_explicit(t);
-    if (explicit_) explicit_step(t);
-    else reflect_step(t);
+    {
+        PhaseTimer pt(explicit_ ? "p1 explicit reflector" : "p1 reflector");
+        if (explicit_) explicit_step(t);
+        else reflect_step(t);
+    }
     gemv_step(t);
     steps_ = t + 1;
 }
@@ -2093,6 +2577,7 @@ void WideQrcp::reflect_step(int64_t t) {
 }
 
 void WideQrcp::gemv_step(int64_t t) {
+    PhaseTimer pt_all("p1 stream+guard");
     prof_begin();
     if (mode_ == 4) {
         const dim3 g((unsigned)cdiv(N_, 32), (unsigned)ksplit_);
@@ -2158,6 +2643,7 @@ void WideQrcp::gemv_step(int64_t t) {
         return e && *e == '1' ? 1 : 0;
     }();
     const size_t gq = sizeof(double) * (size_t)(k_ * (t + 1));
+    PhaseTimer pt_guard("p1 guard");
     if (k_ <= 32) {
         TTG_LAUNCH(k_guard_lane<32>, ngc_, kThreads, gq, stream(), W_, k_, N_, ld_, (int)layout_, t, qptr(),
                    R_.get(), flags_.get(), nflag_.get(), nu_.get(), cref_.get(), pos_.get(), cand_.get(), ncand_,

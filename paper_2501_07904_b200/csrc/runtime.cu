@@ -200,3 +200,63 @@ int sm_count() {
 }
 
 }  // namespace ttg
+
+// ---- TTG_PHASES=1: event-timed pass-1 phases (diagnostics; printed at exit) ----------
+namespace ttg {
+namespace {
+struct Phases {
+    struct Rec {
+        cudaEvent_t a, b;
+        int kind;
+    };
+    std::mutex mu;
+    std::vector<Rec> recs;
+    std::vector<std::string> names;
+    std::vector<double> ms;
+    std::vector<int64_t> n;
+    ~Phases() {
+        if (recs.empty()) return;
+        for (auto& r : recs) {
+            float x = 0.f;
+            if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&x, r.a, r.b) != cudaSuccess) break;
+            ms[(size_t)r.kind] += x;
+            n[(size_t)r.kind] += 1;
+        }
+        for (size_t i = 0; i < names.size(); ++i)
+            std::fprintf(stderr, "[ttg phase] %-28s n=%7lld total=%9.3f ms avg=%8.2f us\n", names[i].c_str(),
+                         (long long)n[i], ms[i], n[i] ? 1e3 * ms[i] / (double)n[i] : 0.0);
+    }
+};
+Phases g_phases;
+}  // namespace
+
+bool phases_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTG_PHASES");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
+cudaEvent_t phase_mark() {
+    cudaEvent_t e;
+    TTG_CUDA(cudaEventCreate(&e));
+    TTG_CUDA(cudaEventRecord(e, stream()));
+    return e;
+}
+
+void phase_add(cudaEvent_t a, const char* name) {
+    cudaEvent_t b = phase_mark();
+    std::lock_guard<std::mutex> lk(g_phases.mu);
+    int kind = -1;
+    for (size_t i = 0; i < g_phases.names.size(); ++i)
+        if (g_phases.names[i] == name) kind = (int)i;
+    if (kind < 0) {
+        g_phases.names.emplace_back(name);
+        g_phases.ms.push_back(0.0);
+        g_phases.n.push_back(0);
+        kind = (int)g_phases.names.size() - 1;
+    }
+    g_phases.recs.push_back({a, b, kind});
+}
+}  // namespace ttg

@@ -606,6 +606,7 @@ struct Pass2 {
 
 Pass2 run_pass2(Pass1& e1, int64_t s) {
     const int64_t N = e1.N();
+    PhaseTimer pt("pass2 (incl. host sync)");
     Pass2 out;
     DevBuf<double> R2((size_t)s * s), colmass(s), kept(s + 1), pn(s);
     out.perm.alloc(s);
@@ -684,6 +685,7 @@ CutOut run_cut(Pass1& e1, const CutRequest& req) {
         bool exact = false;
         if (s < p) {
             if (!req.fixed) {
+                PhaseTimer pt("refresh_exact");
                 t1 = e1.refresh_exact();
                 exact = true;
             } else {
