@@ -151,6 +151,7 @@ private:
     int64_t steps_ = 0;
     int nblk_ = 0;
     int64_t rows_per_blk_ = 0;
+    bool col_mode_ = false;  // one CTA per trailing column per step (N <= 25600)
     DevBuf<double> nu_, cref_, R_, part_, tq_, beta_, v0_, pnorm_;
     DevBuf<int64_t> colmap_, pos_;
     DevBuf<int> flag_;

@@ -315,6 +315,122 @@ __global__ void k_eye(double* Q, int64_t N, int64_t q, int64_t ldq) {
     }
 }
 
+
+// ---- column-parallel step (col mode: N <= kColRows) ------------------------------------
+// For square and moderately tall matrices the row blocks above leave most SMs idle and
+// loop over every column inside a CTA. Col mode keeps qr_col_pivot's per-column structure
+// instead: one CTA per trailing column does the dot, the update (factor.cpp:43-58), the
+// row-t value, the norm downdate and -- when the guard flags it -- the recompute of the
+// norm from the column it just updated (factor.cpp:98-107), in one read and one write of
+// the column. A single CTA picks the pivot and builds the reflector beforehand.
+constexpr int64_t kColRows = 25600;  // column staged in shared memory (<= 200 KB)
+
+__global__ void __launch_bounds__(kT) k_col_house(TallView s, int64_t t) {
+    int64_t pp;
+    const int64_t piv = pick_pivot(s, t, &pp);
+    __shared__ double sd[kT / 32];
+    __shared__ double sh[2];
+    double* x = s.B + piv * s.ld;
+    double sg = 0.0;
+#pragma unroll 4
+    for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) sg = fma(x[i], x[i], sg);
+    sg = block_sum(sg, sd);
+    if (threadIdx.x == 0) {
+        const double alpha = x[t];
+        const int64_t len = s.N - t;
+        double beta = 0.0, v0 = 1.0, rkk = alpha;
+        if (len > 1 && sg != 0.0) {  // make_householder (factor.cpp:24-38)
+            const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sg));
+            const double smu = copysign(mu, alpha);
+            v0 = __dadd_rn(alpha, smu);
+            beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+            rkk = -smu;
+        }
+        sh[0] = beta;
+        sh[1] = v0;
+        s.beta[t] = beta;
+        s.v0[t] = v0;
+        s.pnorm[t] = s.nu[piv];
+        x[t] = rkk;
+        const int64_t other = s.colmap[t];
+        s.colmap[t] = piv;
+        s.colmap[pp] = other;
+        s.pos[piv] = t;
+        s.pos[other] = pp;
+    }
+    __syncthreads();
+    const double beta = sh[0], v0 = sh[1];
+    if (beta != 0.0)
+#pragma unroll 4
+        for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) x[i] = __ddiv_rn(x[i], v0);
+}
+
+__global__ void __launch_bounds__(kT) k_col_apply(TallView s, int64_t t) {
+    extern __shared__ double cs[];  // rows t+1.. of this CTA's column
+    __shared__ double sd[kT / 32];
+    const int64_t j = s.colmap[t + 1 + blockIdx.x];
+    const double beta = s.beta[t];
+    const double* __restrict__ v = s.B + s.colmap[t] * s.ld;
+    double* c = s.B + j * s.ld;
+    double rt = c[t];
+    double sq = 0.0;
+    bool fl;
+    if (beta != 0.0) {
+        double d = 0.0;
+#pragma unroll 4
+        for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) {
+            const double xi = c[i];
+            cs[i - t - 1] = xi;
+            d = fma(v[i], xi, d);
+        }
+        d = block_sum(d, sd);
+        const double tj = __dmul_rn(beta, __dadd_rn(rt, d));
+        rt = __dsub_rn(rt, tj);
+#pragma unroll 4
+        for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) {
+            const double y = __dsub_rn(cs[i - t - 1], __dmul_rn(tj, v[i]));
+            c[i] = y;
+            sq = fma(y, y, sq);
+        }
+        sq = block_sum(sq, sd);
+        const double nv = __dsub_rn(s.nu[j], __dmul_rn(rt, rt));
+        fl = nv < __dmul_rn(1e-16, s.cref[j]) || nv < 0.0;
+        if (threadIdx.x == 0) {
+            c[t] = rt;
+            s.nu[j] = fl ? sq : nv;
+            if (fl) s.cref[j] = sq;
+        }
+    } else {  // H_t = I: the column is unchanged, only the norm downdate and the guard
+        const double nv = __dsub_rn(s.nu[j], __dmul_rn(rt, rt));
+        fl = nv < __dmul_rn(1e-16, s.cref[j]) || nv < 0.0;
+        if (fl) {
+            for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) sq = fma(c[i], c[i], sq);
+            sq = block_sum(sq, sd);
+        }
+        if (threadIdx.x == 0) {
+            s.nu[j] = fl ? sq : nv;
+            if (fl) s.cref[j] = sq;
+        }
+    }
+}
+
+// Q formation in col mode: reflector t applied to columns [t, q) of Q, one CTA per column
+// (the k_col_apply structure; factor.cpp:116-133 per column).
+__global__ void __launch_bounds__(kT) k_q_col(TallView s, int64_t t, double* Q, int64_t ldq) {
+    __shared__ double sd[kT / 32];
+    const double beta = s.beta[t];
+    const double* __restrict__ v = s.B + s.colmap[t] * s.ld;
+    double* c = Q + (t + blockIdx.x) * ldq;
+    double d = 0.0;
+#pragma unroll 4
+    for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) d = fma(v[i], c[i], d);
+    d = block_sum(d, sd);
+    const double tj = __dmul_rn(__dadd_rn(c[t], d), beta);
+#pragma unroll 4
+    for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) c[i] = __dsub_rn(c[i], __dmul_rn(tj, v[i]));
+    if (threadIdx.x == 0) c[t] = __dsub_rn(c[t], tj);
+}
+
 TallView view_of(double* B, int64_t N, int64_t n, int64_t ld, DevBuf<double>& nu, DevBuf<double>& cref,
                  DevBuf<int64_t>& colmap, DevBuf<int64_t>& pos, DevBuf<double>& part, DevBuf<double>& tq,
                  DevBuf<double>& R, int64_t ldr, DevBuf<double>& beta, DevBuf<double>& v0, DevBuf<double>& pn,
@@ -332,6 +448,8 @@ TallQrcp::TallQrcp(double* B, int64_t N, int64_t n, int64_t ld) : B_(B), N_(N), 
     rows_per_blk_ = std::max<int64_t>(256, cdiv(N, target));
     rows_per_blk_ = cdiv(rows_per_blk_, 32) * 32;
     nblk_ = (int)cdiv(N, rows_per_blk_);
+    // column-parallel steps unless the matrix is tall enough for the row blocks to fill the GPU
+    col_mode_ = N <= kColRows && n >= 64;
     nu_.alloc(n); cref_.alloc(n); colmap_.alloc(n); pos_.alloc(n);
     part_.alloc((size_t)nblk_ * (n + 1)); tq_.alloc(std::max(n, p_));
     R_.alloc(p_ * n); R_.zero();
@@ -346,6 +464,17 @@ void TallQrcp::run(int64_t steps) {
     steps = std::min(steps, p_);
     TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
                          rows_per_blk_);
+    if (col_mode_) {
+        allow_smem(k_col_apply, sizeof(double) * (size_t)N_);
+        for (int64_t t = steps_; t < steps; ++t) {
+            TTG_LAUNCH(k_col_house, 1, kT, 0, stream(), s, t);
+            if (t + 1 < n_)
+                TTG_LAUNCH(k_col_apply, (int)(n_ - t - 1), kT, sizeof(double) * (size_t)(N_ - t - 1), stream(), s,
+                           t);
+        }
+        steps_ = std::max(steps_, steps);
+        return;
+    }
     for (int64_t t = steps_; t < steps; ++t) {
         TTG_LAUNCH(k_dots, nblk_, kT, sizeof(double) * kSub, stream(), s, t);
         TTG_LAUNCH(k_house, 1, kT, 0, stream(), s, t, nblk_);
@@ -413,6 +542,10 @@ void TallQrcp::form_q(double* Q, int64_t q, int64_t ldq) {
     const int64_t top = std::min(q, steps_);
     for (int64_t t = top - 1; t >= 0; --t) {
         if (hb[(size_t)t] == 0.0) continue;
+        if (col_mode_) {
+            TTG_LAUNCH(k_q_col, (int)(q - t), kT, 0, stream(), s, t, Q, ldq);
+            continue;
+        }
         TTG_LAUNCH(k_q_dots, nblk_, kT, 0, stream(), s, t, Q, ldq, q);
         TTG_LAUNCH(k_q_fin, 1, kT, 0, stream(), s, t, Q, ldq, q, nblk_);
         TTG_LAUNCH(k_q_apply, nblk_, kT, 0, stream(), s, t, Q, ldq, q);

@@ -2553,6 +2553,7 @@ void WideQrcp::reflect_step(int64_t t) {
     // one fused CTA while the O(k t) work is small, row chunks otherwise
     const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(nchunk_, cdiv(k_ * (t + 1), 32768)));
     if (nch == 1) {
+        PhaseTimer pt("wy fused (1 CTA)");
         const size_t sm = sizeof(double) * wy_smem_doubles(k_, t);
         if (sm <= 200 * 1024) {
             auto kern = comm_ ? k_wy_fused_smem<true> : k_wy_fused_smem<false>;
@@ -2567,13 +2568,16 @@ void WideQrcp::reflect_step(int64_t t) {
     }
     s.nchunk = nch;
     s.rows = cdiv(k_, nch);
-    if (comm_) TTG_LAUNCH(k_wy_pick_shard, nch, kThreads, 0, stream(), s, t);
-    else TTG_LAUNCH(k_wy_pick, nch, kThreads, 0, stream(), s, t);
-    TTG_LAUNCH(k_wy_zu, 1, 1024, 0, stream(), s, t);
-    TTG_LAUNCH(k_wy_y, nch, kThreads, 0, stream(), s, t);
-    TTG_LAUNCH(k_wy_reflect, nch, kThreads, 0, stream(), s, t);
-    TTG_LAUNCH(k_wy_tg, 1, 1024, 0, stream(), s, t);
-    TTG_LAUNCH(k_wy_q, nch, kThreads, 0, stream(), s, t);
+    {
+        PhaseTimer pt("wy pick");
+        if (comm_) TTG_LAUNCH(k_wy_pick_shard, nch, kThreads, 0, stream(), s, t);
+        else TTG_LAUNCH(k_wy_pick, nch, kThreads, 0, stream(), s, t);
+    }
+    { PhaseTimer pt("wy zu"); TTG_LAUNCH(k_wy_zu, 1, 1024, 0, stream(), s, t); }
+    { PhaseTimer pt("wy y"); TTG_LAUNCH(k_wy_y, nch, kThreads, 0, stream(), s, t); }
+    { PhaseTimer pt("wy reflect"); TTG_LAUNCH(k_wy_reflect, nch, kThreads, 0, stream(), s, t); }
+    { PhaseTimer pt("wy tg"); TTG_LAUNCH(k_wy_tg, 1, 1024, 0, stream(), s, t); }
+    { PhaseTimer pt("wy q"); TTG_LAUNCH(k_wy_q, nch, kThreads, 0, stream(), s, t); }
 }
 
 void WideQrcp::gemv_step(int64_t t) {

@@ -589,7 +589,15 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         const char* e = std::getenv("TTG_NO_GRAM_PASS1");
         return e && *e == '1';
     }();
-    if (inplace && k > 2048 && k > N) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    // very tall W run to many steps (config 4's 16304 x 1024 cut in tolerance mode): the
+    // compact-WY reflector costs O(k t) per step and dominates once t ~ N, the in-place
+    // engine O(k N) (measured 1.34 s -> 0.43 s); short runs (N < 512) stay read-only
+    if ((inplace && k > 2048 && k > N) || (!fixed && k > 2048 && k >= 8 * N && N >= 512))
+        return std::make_unique<TallPass1>(W, k, N, ld, l);
+    // square near-full-rank cuts in tolerance mode (config 4's 4096 x 4096): the in-place
+    // engine's column-parallel steps (TallQrcp col mode) instead of O(k t) WY / O(k^2)
+    // explicit-Q work per step
+    if (!fixed && k >= 2048 && k >= N && k <= 25600 && N >= 2048) return std::make_unique<TallPass1>(W, k, N, ld, l);
     // tall W, fixed rank: the pivoted Cholesky of W^T W (cut_with() checks its conditioning)
     if (fixed && !no_gram && k >= 8 * N && N <= 4096 && cap <= 160 && cap >= 1)
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
@@ -618,9 +626,10 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
     } else {
         if (e1.sharded())
             invariant_error("sharded pass 2 supports at most " + std::to_string(160) + " pass-1 steps per cut");
-        if (N <= 8192) {
+        if (N <= 8192 && !(s >= 1024 && N <= 25600)) {
             // B = R1[:s, :]^T read in place (column c of B = row c of R1): the read-only engine,
-            // which switches to an explicit Q for these long factorisations
+            // which switches to an explicit Q for these long factorisations (s >= 1024: the
+            // in-place engine's column-parallel steps below)
             WideQrcp e2(e1.R(), N, s, N, Layout::Col, s);
             e2.run_to(s);
             TTG_LAUNCH(k_r2_positions, (int)cdiv(s * s, 256), 256, 0, stream(), e2.R(), e2.piv(), s, R2.get());
