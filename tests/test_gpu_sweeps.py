@@ -114,7 +114,9 @@ def test_rank_chain_errors(dev):
         dev.decompose(a, [2, 3, 4], "urv", "r2l", eps=-1.0)
 
 
-@pytest.mark.parametrize("shape", [(30, 20), (20, 30), (100, 400), (100, 20), (1, 7), (7, 1)])
+# (5000, 96): the in-place engine's column-parallel mode; (5000, 40): its row-block mode
+@pytest.mark.parametrize("shape", [(30, 20), (20, 30), (100, 400), (100, 20), (1, 7), (7, 1), (5000, 96),
+                                   (5000, 40)])
 def test_qr_col_pivot_matches_reference(dev, ref, shape):
     rng = np.random.default_rng(7)
     a = np.asfortranarray(rng.standard_normal(shape))
@@ -270,3 +272,18 @@ def test_order_two_fast_path(dev, ref, method):
     a = planted_plus_noise(ref, dims, ranks, 9, 1e-6)
     _check_parity(dev, ref, a, dims, method, ranks=ranks)
     _check_parity(dev, ref, a, dims, method, eps=1e-4)
+
+
+def test_square_near_full_rank_cut_in_place(dev, ref):
+    """A 2116 x 2116 middle cut kept at nearly full rank in tolerance mode (config 4's
+    regime): pass 1, pass 2 and the core's Q run on the in-place engine's column-parallel
+    steps. Ranks identical to the reference, RSE within the contract."""
+    rng = np.random.default_rng(46)
+    dims = [46, 46, 46, 46]
+    a = rng.standard_normal(int(np.prod(dims)))
+    res = dev.decompose_device(a, dims, "urv", "r2l", eps=1e-3)
+    rep = res.report()
+    assert max(c["n"] for c in rep.cuts) >= 2048 and max(c["m"] for c in rep.cuts) >= 2048
+    rr = ref.decompose(a, dims, "urv", "r2l", eps=1e-3)
+    assert rep.ranks_chosen == rr.ranks_chosen
+    assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
