@@ -431,6 +431,124 @@ __global__ void __launch_bounds__(kT) k_q_col(TallView s, int64_t t, double* Q, 
     if (threadIdx.x == 0) c[t] = __dsub_rn(c[t], tj);
 }
 
+// Short columns (N <= kWarpRows): a warp per column, the column held in registers (lane l
+// owns rows t+1+l, t+1+l+32, ...), eight columns per CTA.
+constexpr int64_t kWarpRows = 2048;
+
+__global__ void __launch_bounds__(kT) k_col_apply_warp(TallView s, int64_t t) {
+    constexpr int R = kWarpRows / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t q = t + 1 + (int64_t)blockIdx.x * (kT / 32) + warp;
+    if (q >= s.n) return;
+    const int64_t j = s.colmap[q];
+    const double beta = s.beta[t];
+    const double* __restrict__ v = s.B + s.colmap[t] * s.ld;
+    double* c = s.B + j * s.ld;
+    double rt = c[t];
+    double x[R];
+    double d = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = t + 1 + lane + 32 * r;
+        x[r] = i < s.N ? c[i] : 0.0;
+        if (i < s.N) d = fma(v[i], x[r], d);
+    }
+    double sq = 0.0;
+    if (beta != 0.0) {
+        d = warp_sum(d);
+        const double tj = __dmul_rn(beta, __dadd_rn(rt, d));
+        rt = __dsub_rn(rt, tj);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = t + 1 + lane + 32 * r;
+            if (i < s.N) {
+                const double y = __dsub_rn(x[r], __dmul_rn(tj, v[i]));
+                c[i] = y;
+                sq = fma(y, y, sq);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sq = fma(x[r], x[r], sq);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) {
+        const double nv = __dsub_rn(s.nu[j], __dmul_rn(rt, rt));
+        const bool fl = nv < __dmul_rn(1e-16, s.cref[j]) || nv < 0.0;
+        if (beta != 0.0) c[t] = rt;
+        s.nu[j] = fl ? sq : nv;
+        if (fl) s.cref[j] = sq;
+    }
+}
+
+// Col-mode initial norms: a warp per column over all rows (sequential lane partials + tree).
+__global__ void __launch_bounds__(kT) k_col_norms(TallView s) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * (kT / 32) + warp;
+    if (j >= s.n) return;
+    const double* c = s.B + j * s.ld;
+    double a = 0.0;
+#pragma unroll 8
+    for (int64_t i = lane; i < s.N; i += 32) a = fma(c[i], c[i], a);
+    a = warp_sum(a);
+    if (lane == 0) {
+        s.nu[j] = a;
+        s.cref[j] = a;
+        s.colmap[j] = j;
+        s.pos[j] = j;
+    }
+    if (j == 0 && lane == 0) s.flag[0] = 0;
+}
+
+// k_col_apply with the column in registers (thread r holds rows t+1+r, t+1+r+kT, ...):
+// no shared memory, so several CTAs share an SM (R * kT >= N - t - 1).
+template <int R>
+__global__ void __launch_bounds__(kT) k_col_apply_reg(TallView s, int64_t t) {
+    __shared__ double sd[kT / 32];
+    const int64_t j = s.colmap[t + 1 + blockIdx.x];
+    const double beta = s.beta[t];
+    const double* __restrict__ v = s.B + s.colmap[t] * s.ld;
+    double* c = s.B + j * s.ld;
+    double rt = c[t];
+    double x[R], w[R];
+    double d = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = t + 1 + threadIdx.x + (int64_t)kT * r;
+        const bool in = i < s.N;
+        x[r] = in ? c[i] : 0.0;
+        w[r] = in ? v[i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) d = fma(w[r], x[r], d);
+    double sq = 0.0;
+    if (beta != 0.0) {
+        d = block_sum(d, sd);
+        const double tj = __dmul_rn(beta, __dadd_rn(rt, d));
+        rt = __dsub_rn(rt, tj);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = t + 1 + threadIdx.x + (int64_t)kT * r;
+            if (i < s.N) {
+                const double y = __dsub_rn(x[r], __dmul_rn(tj, w[r]));
+                c[i] = y;
+                sq = fma(y, y, sq);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sq = fma(x[r], x[r], sq);
+    }
+    sq = block_sum(sq, sd);
+    if (threadIdx.x == 0) {
+        const double nv = __dsub_rn(s.nu[j], __dmul_rn(rt, rt));
+        const bool fl = nv < __dmul_rn(1e-16, s.cref[j]) || nv < 0.0;
+        if (beta != 0.0) c[t] = rt;
+        s.nu[j] = fl ? sq : nv;
+        if (fl) s.cref[j] = sq;
+    }
+}
+
 TallView view_of(double* B, int64_t N, int64_t n, int64_t ld, DevBuf<double>& nu, DevBuf<double>& cref,
                  DevBuf<int64_t>& colmap, DevBuf<int64_t>& pos, DevBuf<double>& part, DevBuf<double>& tq,
                  DevBuf<double>& R, int64_t ldr, DevBuf<double>& beta, DevBuf<double>& v0, DevBuf<double>& pn,
@@ -456,6 +574,10 @@ TallQrcp::TallQrcp(double* B, int64_t N, int64_t n, int64_t ld) : B_(B), N_(N), 
     beta_.alloc(p_); v0_.alloc(p_); pnorm_.alloc(p_); flag_.alloc(n + 1);
     TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
                          rows_per_blk_);
+    if (col_mode_) {
+        TTG_LAUNCH(k_col_norms, (int)cdiv(n, kT / 32), kT, 0, stream(), s);
+        return;
+    }
     TTG_LAUNCH(k_norm_part, nblk_, kT, 0, stream(), s, (int64_t)0);
     TTG_LAUNCH(k_norm_fin, 1, kT, 0, stream(), s, nblk_);
 }
@@ -468,7 +590,17 @@ void TallQrcp::run(int64_t steps) {
         allow_smem(k_col_apply, sizeof(double) * (size_t)N_);
         for (int64_t t = steps_; t < steps; ++t) {
             TTG_LAUNCH(k_col_house, 1, kT, 0, stream(), s, t);
-            if (t + 1 < n_)
+            if (t + 1 >= n_) continue;
+            const int64_t len = N_ - t - 1, nc = n_ - t - 1;
+            if (N_ <= kWarpRows)
+                TTG_LAUNCH(k_col_apply_warp, (int)cdiv(nc, kT / 32), kT, 0, stream(), s, t);
+            else if (len <= 16 * kT)
+                TTG_LAUNCH(k_col_apply_reg<16>, (int)nc, kT, 0, stream(), s, t);
+            else if (len <= 32 * kT)
+                TTG_LAUNCH(k_col_apply_reg<32>, (int)nc, kT, 0, stream(), s, t);
+            else if (len <= 64 * kT)
+                TTG_LAUNCH(k_col_apply_reg<64>, (int)nc, kT, 0, stream(), s, t);
+            else
                 TTG_LAUNCH(k_col_apply, (int)(n_ - t - 1), kT, sizeof(double) * (size_t)(N_ - t - 1), stream(), s,
                            t);
         }

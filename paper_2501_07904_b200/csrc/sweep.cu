@@ -592,12 +592,17 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
     // very tall W run to many steps (config 4's 16304 x 1024 cut in tolerance mode): the
     // compact-WY reflector costs O(k t) per step and dominates once t ~ N, the in-place
     // engine O(k N) (measured 1.34 s -> 0.43 s); short runs (N < 512) stay read-only
-    if ((inplace && k > 2048 && k > N) || (!fixed && k > 2048 && k >= 8 * N && N >= 512))
+    if ((inplace && k > 2048 && k > N) || (!fixed && k > 2048 && k >= 8 * N && N >= 64))
         return std::make_unique<TallPass1>(W, k, N, ld, l);
-    // square near-full-rank cuts in tolerance mode (config 4's 4096 x 4096): the in-place
+    // square / wide near-full-rank cuts in tolerance mode (config 4's 4096 x 4096 and
+    // 1024 x 16384; k >= 1024 keeps configs 2-3's short early-exit runs read-only): the in-place
     // engine's column-parallel steps (TallQrcp col mode) instead of O(k t) WY / O(k^2)
     // explicit-Q work per step
-    if (!fixed && k >= 2048 && k >= N && k <= 25600 && N >= 2048) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    static const int64_t inplace_mink = [] {  // experiment: TTG_INPLACE_MINK
+        const char* e = std::getenv("TTG_INPLACE_MINK");
+        return e ? (int64_t)std::atoll(e) : (int64_t)1024;
+    }();
+    if (!fixed && k >= inplace_mink && k <= 25600 && N >= 2048) return std::make_unique<TallPass1>(W, k, N, ld, l);
     // tall W, fixed rank: the pivoted Cholesky of W^T W (cut_with() checks its conditioning)
     if (fixed && !no_gram && k >= 8 * N && N <= 4096 && cap <= 160 && cap >= 1)
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
@@ -626,10 +631,15 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
     } else {
         if (e1.sharded())
             invariant_error("sharded pass 2 supports at most " + std::to_string(160) + " pass-1 steps per cut");
-        if (N <= 8192 && !(s >= 1024 && N <= 25600)) {
+        static const bool wide_pass2 = [] {  // TTG_WIDE_PASS2=1: the read-only engine below
+            const char* e = std::getenv("TTG_WIDE_PASS2");
+            return e && *e == '1';
+        }();
+        if (wide_pass2 && N <= 8192) {
             // B = R1[:s, :]^T read in place (column c of B = row c of R1): the read-only engine,
-            // which switches to an explicit Q for these long factorisations (s >= 1024: the
-            // in-place engine's column-parallel steps below)
+            // which switches to an explicit Q for these long factorisations. The default is the
+            // in-place engine below (column-parallel steps for N <= 25600): measured 28 -> 3 ms
+            // at s = 256, 800 -> 150 ms at s = 4096 (config 4)
             WideQrcp e2(e1.R(), N, s, N, Layout::Col, s);
             e2.run_to(s);
             TTG_LAUNCH(k_r2_positions, (int)cdiv(s * s, 256), 256, 0, stream(), e2.R(), e2.piv(), s, R2.get());
@@ -653,14 +663,15 @@ kept:
     out.kept.resize((size_t)s + 1);
     out.colmass.resize((size_t)s);
     out.pnorm.resize((size_t)s);
-    std::vector<double> r2h((size_t)s * s);
+    out.diag.resize((size_t)s);
     kept.download(out.kept.data(), (size_t)s + 1);
     colmass.download(out.colmass.data(), (size_t)s);
     pn.download(out.pnorm.data(), (size_t)s);
-    R2.download(r2h.data(), r2h.size());
+    // only the diagonal of R2 goes to the host (a strided copy: s values, not s^2)
+    TTG_CUDA(cudaMemcpy2DAsync(out.diag.data(), sizeof(double), R2.get(), sizeof(double) * (size_t)(s + 1),
+                               sizeof(double), (size_t)s, cudaMemcpyDeviceToHost, stream()));
     sync();
-    out.diag.resize((size_t)s);
-    for (int64_t t = 0; t < s; ++t) out.diag[(size_t)t] = std::abs(r2h[(size_t)(t + t * s)]);
+    for (int64_t t = 0; t < s; ++t) out.diag[(size_t)t] = std::abs(out.diag[(size_t)t]);
     return out;
 }
 
