@@ -365,11 +365,15 @@ def run_ours(args):
                        "ranks": {m: r.ranks_chosen for m, r in rep.items()},
                        "pass1_steps": {m: [cu["steps"] for cu in r.cuts] for m, r in rep.items()},
                        "rse": rse},
-            "roofline": {"bound": "hbm", "kernel": dom["kernel"] + " - pass-1 streaming GEMV + norm downdate",
+            "roofline": {"bound": "hbm",
+                         "kernel": dom["kernel"] + (" - pass-1 steps fused in one launch (reflector, streaming GEMV + "
+                                                    "norm downdate, guard); bytes = the streams' algorithmic bytes"
+                                                    if "k_pass1" in dom["kernel"] else
+                                                    " - pass-1 streaming GEMV + norm downdate"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "peak_source": f"hbm_gbs ({peak_kind})",
-                         "note": ("hbm_gbs is a read+write copy rate; a read-dominated stream can exceed it "
-                                  "(ncu: the same kernel at ~87% of its DRAM peak, profiles/traffic.json)"),
+                         "note": ("hbm_gbs is a read+write copy rate; a read-dominated stream can exceed it; "
+                                  "traffic = ncu DRAM bytes of one launch of this kernel (profiles/traffic.json)"),
                          "frac_vs_ncu_dram_peak": achieved / ncu_peak if ncu_peak else None,
                          "traffic": traffic, "launches": dom["launches"], "kernel_ms": dom["ms"],
                          "share_of_step": dom["ms"] / ms if ms > 0 else None,
