@@ -324,6 +324,7 @@ __global__ void k_eye(double* Q, int64_t N, int64_t q, int64_t ldq) {
 // norm from the column it just updated (factor.cpp:98-107), in one read and one write of
 // the column. A single CTA picks the pivot and builds the reflector beforehand.
 constexpr int64_t kColRows = 25600;  // column staged in shared memory (<= 200 KB)
+constexpr int64_t kQBlock = 32;     // reflectors per compact-WY block in form_q
 
 __global__ void __launch_bounds__(kT) k_col_house(TallView s, int64_t t) {
     int64_t pp;
@@ -549,6 +550,40 @@ __global__ void __launch_bounds__(kT) k_col_apply_reg(TallView s, int64_t t) {
     }
 }
 
+// Blocked Q formation (col mode): the reflectors of steps [b0, b0 + kb) as one compact-WY
+// block H_b0 ... H_{b0+kb-1} = I - V T V^T (V gathered from the pivot columns, T by the
+// forward column-wise recurrence from the Gram matrix V^T V), applied to Q[b0:, b0:q]
+// with three DMMA GEMMs (W = V^T Q, W = T W, Q -= V W), blocks taken last to first.
+__global__ void k_gather_v(TallView s, int64_t b0, int kb, double* V) {
+    const int64_t rows = s.N - b0;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * kb) return;
+    const int64_t jj = e / rows, i = e - jj * rows;
+    const int64_t r = b0 + i, j = b0 + jj;
+    V[e] = r < j ? 0.0 : (r == j ? 1.0 : s.B[r + s.colmap[j] * s.ld]);
+}
+
+// T (kb x kb, upper): T(j, j) = beta_j, T(0:j, j) = -beta_j T(0:j, 0:j) G(0:j, j).
+__global__ void k_larft(const double* __restrict__ G, const double* __restrict__ beta, int kb, double* T) {
+    __shared__ double Ts[64 * 65];
+    __shared__ double col[64];
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) Ts[(e % kb) + (e / kb) * 65] = 0.0;
+    __syncthreads();
+    for (int j = 0; j < kb; ++j) {
+        const double bj = beta[j];
+        if (threadIdx.x < j) {
+            double a = 0.0;
+            for (int l = threadIdx.x; l < j; ++l) a = fma(Ts[threadIdx.x + l * 65], G[l + j * kb], a);
+            col[threadIdx.x] = -bj * a;
+        }
+        __syncthreads();
+        if (threadIdx.x < j) Ts[threadIdx.x + j * 65] = col[threadIdx.x];
+        if (threadIdx.x == 0) Ts[j + j * 65] = bj;
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) T[e] = Ts[(e % kb) + (e / kb) * 65];
+}
+
 TallView view_of(double* B, int64_t N, int64_t n, int64_t ld, DevBuf<double>& nu, DevBuf<double>& cref,
                  DevBuf<int64_t>& colmap, DevBuf<int64_t>& pos, DevBuf<double>& part, DevBuf<double>& tq,
                  DevBuf<double>& R, int64_t ldr, DevBuf<double>& beta, DevBuf<double>& v0, DevBuf<double>& pn,
@@ -672,6 +707,23 @@ void TallQrcp::form_q(double* Q, int64_t q, int64_t ldq) {
     TTG_LAUNCH(k_eye, (int)cdiv(N_ * q, 256), 256, 0, stream(), Q, N_, q, ldq);
     std::vector<double> hb = beta_.to_host(p_);
     const int64_t top = std::min(q, steps_);
+    if (col_mode_ && top >= 2 * kQBlock && q >= 2 * kQBlock) {
+        const int64_t nbk = cdiv(top, kQBlock);
+        DevBuf<double> V((size_t)(N_ * kQBlock)), G((size_t)(kQBlock * kQBlock)), T((size_t)(kQBlock * kQBlock)),
+            W((size_t)(kQBlock * q)), W2((size_t)(kQBlock * q));
+        for (int64_t bi = nbk - 1; bi >= 0; --bi) {
+            const int64_t b0 = bi * kQBlock, kb = std::min<int64_t>(kQBlock, top - b0);
+            const int64_t rows = N_ - b0, cols = q - b0;
+            TTG_LAUNCH(k_gather_v, (int)cdiv(rows * kb, 256), 256, 0, stream(), s, b0, (int)kb, V.get());
+            gemm(true, false, kb, kb, rows, V.get(), rows, V.get(), rows, G.get(), kb);
+            TTG_LAUNCH(k_larft, 1, 64, 0, stream(), G.get(), beta_.get() + b0, (int)kb, T.get());
+            double* Qb = Q + b0 + b0 * ldq;
+            gemm(true, false, kb, cols, rows, V.get(), rows, Qb, ldq, W.get(), kb);
+            gemm(false, false, kb, cols, kb, T.get(), kb, W.get(), kb, W2.get(), kb);
+            gemm(false, false, rows, cols, kb, V.get(), rows, W2.get(), kb, Qb, ldq, -1.0, 1.0);
+        }
+        return;
+    }
     for (int64_t t = top - 1; t >= 0; --t) {
         if (hb[(size_t)t] == 0.0) continue;
         if (col_mode_) {
