@@ -75,6 +75,40 @@ __device__ __forceinline__ void load_tile_small_k(const double* __restrict__ W, 
     __syncthreads();
 }
 
+// Global -> shared staging with U loads in flight per thread. The plain loop
+// `dst[e] = src[e]` waits for every load before its store (the compiler cannot move the
+// next load above a store through an unrelated pointer), i.e. one L2 round trip per
+// element per thread: 20,000 doubles of Y cost ~25 µs in a one-CTA kernel that way.
+// `src_of(e)` returns element e (a load); the U loads of a batch are issued back to back.
+template <int U = 8, class F>
+__device__ __forceinline__ void stage_smem(double* dst, int64_t n, F src_of) {
+    const int64_t nt = blockDim.x;
+    int64_t e = threadIdx.x;
+    for (; e + (U - 1) * nt < n; e += U * nt) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = src_of(e + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u) dst[e + u * nt] = v[u];
+    }
+    for (; e < n; e += nt) dst[e] = src_of(e);
+}
+
+// The same with a destination index map: element e goes to dst[dst_of(e)].
+template <int U = 8, class F, class D>
+__device__ __forceinline__ void stage_smem_map(double* dst, int64_t n, F src_of, D dst_of) {
+    const int64_t nt = blockDim.x;
+    int64_t e = threadIdx.x;
+    for (; e + (U - 1) * nt < n; e += U * nt) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = src_of(e + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u) dst[dst_of(e + u * nt)] = v[u];
+    }
+    for (; e < n; e += nt) dst[dst_of(e)] = src_of(e);
+}
+
 // Warp-aggregated append of flagged columns (one atomic per warp). All lanes call it.
 __device__ __forceinline__ void append_flag(bool fl, int64_t j, int64_t* flags, int* nflag) {
     const int lane = threadIdx.x & 31;
@@ -484,6 +518,10 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
     wy_q(s, t, 0);
 }
 
+// TTG_WY_TRACE=1 diagnostics: k_wy_fused_smem phase times (thread 0, ns), accumulated
+__device__ int g_wy_trace = 0;
+__device__ unsigned long long g_wy_acc[16];
+
 // Whole step in one CTA with the WY state staged in shared memory: Y[:, :t] and T[:t, :t]
 // are copied in once, every phase then reads shared memory instead of dependent L2 loads,
 // and column t of Y and T is written back. The phase functions run unchanged on a WY view
@@ -497,6 +535,16 @@ template <bool SH>
 __global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
     extern __shared__ double wsm[];
     __shared__ double red[kThreads / 32];
+    const bool trace = g_wy_trace != 0;
+    unsigned long long t_prev = 0;
+    auto mark = [&](int ph) {  // TTG_WY_TRACE: per-phase time of thread 0 (ns), accumulated
+        if (!trace || threadIdx.x != 0) return;
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (ph > 0) atomicAdd(&g_wy_acc[ph], now - t_prev);
+        t_prev = now;
+    };
+    mark(0);
     const int64_t k = s.k, tp = t + 1;
     WY ls = s;
     ls.cap = tp;
@@ -507,32 +555,48 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused_smem(WY s, int64_t t) {
     ls.yv = ls.wv + k;
     ls.part = ls.yv + k;
     ls.vec = ls.part + (tp + 1);
-    for (int64_t e = threadIdx.x; e < k * t; e += kThreads) ls.Y[e] = s.Y[e];
-    for (int64_t e = threadIdx.x; e < t * t; e += kThreads) {
-        const int64_t c = e / t, r = e - c * t;
-        ls.T[r + c * ls.tld] = s.T[r + c * s.cap];
+    {
+        const double* __restrict__ gY = s.Y;
+        stage_smem(ls.Y, k * t, [&](int64_t e) { return gY[e]; });
+        // T: t x t from ld cap to ld tld, one column per pass of the helper
+        const double* __restrict__ gT = s.T;
+        const int64_t tld = ls.tld, cap = s.cap;
+        stage_smem_map(
+            ls.T, t * t, [&](int64_t e) { return gT[(e % t) + (e / t) * cap]; },
+            [&](int64_t e) { return (e % t) + (e / t) * tld; });
     }
     __syncthreads();
+    mark(1);
     if (SH) wy_pick_shard(ls, t, 0, true);
     else wy_pick(ls, t, 0, true);
     __syncthreads();
+    mark(2);
     wy_sum_parts(ls, t, ls.vec, threadIdx.x, kThreads);
     __syncthreads();
     wy_u(ls, t, threadIdx.x, kThreads);
     __syncthreads();
+    mark(3);
     wy_y(ls, t, 0, red);
     __syncthreads();
+    mark(4);
     wy_reflect(ls, t, 0, true, red);
     __syncthreads();
+    mark(5);
     wy_sum_parts(ls, t, ls.vec + 2 * ls.cap, threadIdx.x, kThreads);
     __syncthreads();
     wy_tcol(ls, t, threadIdx.x, kThreads);
     __syncthreads();
     wy_g(ls, t, threadIdx.x, kThreads);
     __syncthreads();
+    mark(6);
     wy_q(ls, t, 0);
+    __syncthreads();
+    mark(7);
     for (int64_t i = threadIdx.x; i < k; i += kThreads) s.Y[i + t * k] = ls.Y[i + t * k];
     for (int64_t r = threadIdx.x; r <= t; r += kThreads) s.T[r + t * s.cap] = ls.T[r + t * ls.tld];
+    __syncthreads();
+    mark(8);
+    if (trace && threadIdx.x == 0) atomicAdd(&g_wy_acc[0], 1ull);
 }
 
 // ---- explicit-Q mode (long factorisations, t comparable to k) ----------------------------
@@ -696,10 +760,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_coop(CoopArgs A) {
     double* qs = ls.yv + k;
     ls.part = qs + k;
     ls.vec = ls.part + (capS + 1);
-    for (int64_t e = tid; e < k * A.t0; e += kThreads) ls.Y[e] = g.Y[e];
-    for (int64_t e = tid; e < A.t0 * A.t0; e += kThreads) {
-        const int64_t c = e / A.t0, r = e - c * A.t0;
-        ls.T[r + c * tld] = g.T[r + c * g.cap];
+    {
+        const double* __restrict__ gY = g.Y;
+        const double* __restrict__ gT = g.T;
+        stage_smem(ls.Y, k * A.t0, [&](int64_t e) { return gY[e]; });
+        const int64_t t0 = A.t0, cap = g.cap;
+        if (t0 > 0)
+            stage_smem_map(
+                ls.T, t0 * t0, [&](int64_t e) { return gT[(e % t0) + (e / t0) * cap]; },
+                [&](int64_t e) { return (e % t0) + (e / t0) * tld; });
     }
     // this CTA's columns
     const int64_t per = cdiv(N, G), c0 = (int64_t)blockIdx.x * per, c1 = min(N, c0 + per);
@@ -1527,7 +1596,7 @@ __global__ void __launch_bounds__(kThreads) k_guard_lane(const double* __restric
     double msum = 0.0;
     if (nf > 0) {
         const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
-        for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
+        stage_smem(qs, k * (t + 1), [&](int64_t e) { return Q[e]; });
         __syncthreads();
         for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < nf; f += (int64_t)gridDim.x * kThreads) {
             const int64_t j = flags[f];
@@ -1575,7 +1644,7 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
         const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
         const bool staged = stage_q != 0;
         if (staged)
-            for (int64_t e = threadIdx.x; e < k * (t + 1); e += kThreads) qs[e] = Q[e];
+            stage_smem(qs, k * (t + 1), [&](int64_t e) { return Q[e]; });
         __syncthreads();
         const double* __restrict__ qq = staged ? qs : Q;
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1698,10 +1767,10 @@ __global__ void __launch_bounds__(kThreads) k_refresh_row(const double* __restri
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sd[kThreads / 32];
     double* qt = reinterpret_cast<double*>(qt2);
-    for (int64_t e = threadIdx.x; e < k * S; e += kThreads) {
+    stage_smem(qt, k * S, [&](int64_t e) {
         const int64_t i = e / S, l = e - i * S;
-        qt[e] = l < s ? Q[i + l * k] : 0.0;
-    }
+        return l < s ? Q[i + l * k] : 0.0;
+    });
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Cand best = cand_none();
@@ -1760,10 +1829,10 @@ __global__ void __launch_bounds__(kThreads) k_refresh_rowt(const double* __restr
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sd[kThreads / 32];
     double* qt = reinterpret_cast<double*>(qt2);
-    for (int64_t e = threadIdx.x; e < k * S; e += kThreads) {
+    stage_smem(qt, k * S, [&](int64_t e) {
         const int64_t i = e / S, l = e - i * S;
-        qt[e] = l < s ? Q[i + l * k] : 0.0;
-    }
+        return l < s ? Q[i + l * k] : 0.0;
+    });
     __syncthreads();
     Cand best = cand_none();
     double msum = 0.0;
@@ -1870,12 +1939,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
     ls.part = qs + k;
     ls.vec = ls.part + (capS + 1);
     double* Qs = ls.vec + 4 * capS + 2 + 8;  // k x capS (k <= 32)
-    for (int64_t e = tid; e < k * A.t0; e += kThreads) ls.Y[e] = g.Y[e];
-    if (k <= 32)
-        for (int64_t e = tid; e < k * A.t0; e += kThreads) Qs[e] = g.Qt[e];
-    for (int64_t e = tid; e < A.t0 * A.t0; e += kThreads) {
-        const int64_t c = e / A.t0, r = e - c * A.t0;
-        ls.T[r + c * tld] = g.T[r + c * g.cap];
+    {
+        const double* __restrict__ gY = g.Y;
+        const double* __restrict__ gQ = g.Qt;
+        const double* __restrict__ gT = g.T;
+        stage_smem(ls.Y, k * A.t0, [&](int64_t e) { return gY[e]; });
+        if (k <= 32) stage_smem(Qs, k * A.t0, [&](int64_t e) { return gQ[e]; });
+        const int64_t t0 = A.t0, cap = g.cap;
+        if (t0 > 0)
+            stage_smem_map(
+                ls.T, t0 * t0, [&](int64_t e) { return gT[(e % t0) + (e / t0) * cap]; },
+                [&](int64_t e) { return (e % t0) + (e / t0) * tld; });
     }
     __syncthreads();
     auto stamp = [&](int64_t t, int ph) {
@@ -2241,9 +2315,37 @@ __global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__
 
 }  // namespace
 
+namespace {
+struct WyTrace {
+    bool on = false;
+    WyTrace() {
+        const char* e = std::getenv("TTG_WY_TRACE");
+        on = e && *e == '1';
+    }
+    void enable() {
+        static bool done = false;
+        if (!on || done) return;
+        int one = 1;
+        TTG_CUDA(cudaMemcpyToSymbol(g_wy_trace, &one, sizeof(int)));
+        done = true;
+    }
+    ~WyTrace() {
+        if (!on) return;
+        unsigned long long h[16] = {};
+        if (cudaMemcpyFromSymbol(h, g_wy_acc, sizeof(h)) != cudaSuccess || h[0] == 0) return;
+        static const char* const names[] = {"", "stage Y,T", "pick+z", "u", "y", "reflect", "tcol+g", "q", "write"};
+        std::fprintf(stderr, "[ttg wy] %llu launches:", h[0]);
+        for (int i = 1; i <= 8; ++i) std::fprintf(stderr, " %s %.2f us;", names[i], 1e-3 * (double)h[i] / (double)h[0]);
+        std::fprintf(stderr, "\n");
+    }
+};
+WyTrace g_wytrace;
+}  // namespace
+
 WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps,
                    const ShardSpec* shard)
     : W_(W), k_(k), N_(N), ld_(ld), p_(std::min(k, N)), layout_(layout) {
+    g_wytrace.enable();
     if (k <= 0 || N <= 0) argument_error("qr_col_pivot: empty matrix");
     Ng_ = N;
     if (shard && shard->comm) {
