@@ -47,6 +47,8 @@ __device__ int64_t pick_pivot(const TallView& s, int64_t t, int64_t* out_pos) {
     __shared__ int64_t bpos[kT / 32];
     double best = -1.0;
     int64_t bp = INT64_MAX;
+    // unrolled so the colmap -> nu load pairs of several positions are in flight together
+#pragma unroll 8
     for (int64_t q = t + threadIdx.x; q < s.n; q += kT) {
         const double v = s.nu[s.colmap[q]];
         if (v > best || (v == best && q < bp)) { best = v; bp = q; }
@@ -624,8 +626,12 @@ void TallQrcp::run(int64_t steps) {
     if (col_mode_) {
         allow_smem(k_col_apply, sizeof(double) * (size_t)N_);
         for (int64_t t = steps_; t < steps; ++t) {
-            TTG_LAUNCH(k_col_house, 1, kT, 0, stream(), s, t);
+            {
+                PhaseTimer pt("col house");
+                TTG_LAUNCH(k_col_house, 1, kT, 0, stream(), s, t);
+            }
             if (t + 1 >= n_) continue;
+            PhaseTimer pt(N_ <= kWarpRows ? "col apply (warp)" : "col apply (cta)");
             const int64_t len = N_ - t - 1, nc = n_ - t - 1;
             if (N_ <= kWarpRows)
                 TTG_LAUNCH(k_col_apply_warp, (int)cdiv(nc, kT / 32), kT, 0, stream(), s, t);
