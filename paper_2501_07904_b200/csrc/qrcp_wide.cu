@@ -728,6 +728,7 @@ struct CoopArgs {
     double* mass;
     int64_t t0, t1, capS;
     const double* Ws;           // k_pass1_big<5>: row-layout copy of W (ld lds)
+    int lazy;                   // k_pass1_big: lazy guard (TTG_LAZY_GUARD=1)
     int64_t lds;
     unsigned long long* trace;  // TTG_BIG_TRACE: CTA 0 phase timestamps, 8 per step
 };
@@ -2190,10 +2191,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
             // against Q[:, :t+1] in shared memory), two columns per thread sharing the q loads
             const int64_t nthr = (int64_t)G * kThreads;
             const int64_t th = (int64_t)blockIdx.x * kThreads + tid;
+            // lazy mode (TTG_LAZY_GUARD=1): the best unflagged candidate of this step bounds
+            // which flagged columns can matter for the next pivot (guard_defer)
+            double bestnu = -2.0;
+            if (A.lazy && nf > 0) {
+                Cand b = cand_none();
+                for (int i = tid; i < G; i += kThreads)
+                    if (better(A.cand[i], b)) b = A.cand[i];
+                b = block_best(b, sc);
+                bestnu = b.col >= 0 ? b.nu : -1.0;
+            }
             for (int64_t f = th; f < nf; f += 2 * nthr) {
                 const int64_t f2 = f + nthr;
-                const bool two = f2 < nf;
-                const int64_t j = A.flags[f], j2 = two ? A.flags[f2] : j;
+                bool two = f2 < nf;
+                int64_t j = A.flags[f], j2 = two ? A.flags[f2] : j;
+                bool one = true;
+                if (A.lazy) {
+                    one = !guard_defer(j, t, N, A.R, A.nu, A.cref, bestnu, gsum);
+                    if (two) two = !guard_defer(j2, t, N, A.R, A.nu, A.cref, bestnu, gsum);
+                    if (!one && !two) continue;
+                    if (!one) {
+                        j = j2;
+                        one = true;
+                        two = false;
+                    }
+                    if (!two) j2 = j;
+                }
                 double x[32], y[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
@@ -2410,11 +2433,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_BIG_MAXMB");
             return (e ? std::atof(e) : 768.0) * 1048576.0;
         }();
-        static const bool lazy_env = [] {
-            const char* e = std::getenv("TTG_LAZY_GUARD");
-            return e && *e == '1';
-        }();
-        if (!coop_ && !no_big && !no_coop && !shard && !lazy_env && N > 16384 &&
+        if (!coop_ && !no_big && !no_coop && !shard && N > 16384 &&
             8.0 * (double)k * (double)N <= big_max_bytes &&
             big_modes.find((char)('0' + mode_)) != std::string::npos &&
             big_smem_doubles(k, 32) * sizeof(double) <= kBigSmemMax) {
@@ -2547,7 +2566,14 @@ bool WideQrcp::coop_run(int64_t steps) {
                   part_.get(), vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(),
                   nflag_.get(), cand_.get(), ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_, cap_},
                R_.get(), nu_.get(), cref_.get(), flags_.get(), nflag2_.get(), cand_.get(), mass_.get(), steps_, steps,
-               cap_, nullptr, 0, nullptr};
+               cap_, nullptr, 0, 0, nullptr};
+    {
+        static const bool lazy = [] {
+            const char* e = std::getenv("TTG_LAZY_GUARD");
+            return e && *e == '1';
+        }();
+        A.lazy = lazy ? 1 : 0;
+    }
     if (big_ && mode_ == 5) {  // stream a row-layout copy of the narrow W (16-byte paired loads)
         const int64_t ldt = (N_ + 1) & ~int64_t(1);
         if (!Wt_.get()) {
