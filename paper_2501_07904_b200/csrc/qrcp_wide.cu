@@ -729,6 +729,7 @@ struct CoopArgs {
     int64_t t0, t1, capS;
     const double* Ws;           // k_pass1_big<5>: row-layout copy of W (ld lds)
     int lazy;                   // k_pass1_big: lazy guard (TTG_LAZY_GUARD=1)
+    int64_t warp_guard_max;     // k_pass1_big: warp-per-column guard up to this many flags
     int64_t lds;
     unsigned long long* trace;  // TTG_BIG_TRACE: CTA 0 phase timestamps, 8 per step
 };
@@ -2186,7 +2187,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
         const int nf = *nflag;
         Cand gbest = cand_none();
         double gsum = 0.0;
-        if (k <= 32) {
+        if (k <= 32 && !A.lazy && nf <= A.warp_guard_max) {
+            // few flagged columns: a warp per column (lanes over rows, modified Gram-Schmidt
+            // with warp sums), so a step's guard costs one column's latency instead of one
+            // thread's whole serial chain (measured: 1139 flags 14.5 -> 4.0 µs; with many
+            // flags the thread-per-column form below is faster)
+            for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
+                 f += (int64_t)G * (kThreads / 32)) {
+                const int64_t j = A.flags[f];
+                double x = lane < k ? ld_w(g.W, g.ld, g.layout, lane, j) : 0.0;
+                for (int64_t l = 0; l <= t; ++l) {
+                    const double ql = lane < k ? Qs[lane + l * k] : 0.0;
+                    const double z = warp_sum(ql * x);
+                    x = fma(-ql, z, x);
+                }
+                const double sq = warp_sum(x * x);
+                if (lane == 0) {
+                    A.nu[j] = sq;
+                    A.cref[j] = sq;
+                    const Cand cj{sq, j == ct ? pp : g.pos[j], j};
+                    if (better(cj, gbest)) gbest = cj;
+                    gsum += sq;
+                }
+            }
+        } else if (k <= 32) {
             // k_guard_lane<32>'s arithmetic (thread per column, modified Gram-Schmidt residual
             // against Q[:, :t+1] in shared memory), two columns per thread sharing the q loads
             const int64_t nthr = (int64_t)G * kThreads;
@@ -2566,7 +2590,14 @@ bool WideQrcp::coop_run(int64_t steps) {
                   part_.get(), vecs_.get(), diag_.get(), beta_.get(), pos_.get(), perm_.get(), piv_.get(),
                   nflag_.get(), cand_.get(), ncand_ + ngc_, 1, k_, recs_.get(), 0, off_, N_, cap_},
                R_.get(), nu_.get(), cref_.get(), flags_.get(), nflag2_.get(), cand_.get(), mass_.get(), steps_, steps,
-               cap_, nullptr, 0, 0, nullptr};
+               cap_, nullptr, 0, 0, 0, nullptr};
+    {
+        static const int64_t wgm = [] {  // experiment: TTG_GUARD_WARP_MAX
+            const char* e = std::getenv("TTG_GUARD_WARP_MAX");
+            return e ? (int64_t)std::atoll(e) : (int64_t)-1;
+        }();
+        A.warp_guard_max = wgm >= 0 ? wgm : (int64_t)4 * (kThreads / 32) * ncand_;
+    }
     {
         static const bool lazy = [] {
             const char* e = std::getenv("TTG_LAZY_GUARD");
