@@ -2026,10 +2026,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
         double msum = 0.0;
         // position of column j during step t (CTA 0 applies the swap after the grid sync)
         auto posof = [&](int64_t j) -> int64_t { return j == jp ? t : (j == ct ? pp : g.pos[j]); };
-        const double* __restrict__ Ws = VAR == 5 ? A.Ws : g.W;
-        const int64_t lds = VAR == 5 ? A.lds : g.ld;
-        if (VAR == 5 || VAR == 6) {
-            // VAR 5 streams the row-layout copy of a narrow Col W (A.Ws, made once per cut).
+        const double* __restrict__ Ws = (VAR == 5 || VAR == 1) ? A.Ws : g.W;
+        const int64_t lds = (VAR == 5 || VAR == 1) ? A.lds : g.ld;
+        if (VAR == 5 || VAR == 6 || VAR == 1) {
+            // VARs 5 and 1 stream a row-layout copy of the Col W (A.Ws, made once per cut).
             // A thread owns two column pairs (16-byte loads, 1 KB contiguous per warp and
             // row), rows summed in order (k_stream<0>'s arithmetic).
             const int64_t npair = (N + 1) / 2, ld2 = lds / 2;
@@ -2132,38 +2132,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
                 }
                 if (warp < 4) append_flag(fl, j, A.flags, nflag);
                 __syncthreads();
-            }
-        } else {  // VAR 1
-            const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-            const int64_t nwarps = (int64_t)G * (kThreads / 32);
-            for (int64_t j = gw; j < N; j += 2 * nwarps) {
-                const int64_t j2 = j + nwarps;
-                const bool two = j2 < N;
-                const int64_t pjs[2] = {posof(j), two ? posof(j2) : 0};
-                const double nus[2] = {A.nu[j], two ? A.nu[j2] : 0.0};
-                const double crs[2] = {A.cref[j], two ? A.cref[j2] : 0.0};
-                const double* w = g.W + j * g.ld;
-                const double* w2 = g.W + (two ? j2 : j) * g.ld;
-                double a = 0.0, b = 0.0;
-#pragma unroll 6
-                for (int64_t i = lane; i < k; i += 32) {
-                    a = fma(qs[i], w[i], a);
-                    b = fma(qs[i], w2[i], b);
-                }
-                a = warp_sum(a);
-                b = warp_sum(b);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && !two) break;
-                    const int64_t jj = h ? j2 : j;
-                    const int64_t pj = pjs[h];
-                    if (pj < t || jj == jp) {
-                        if (lane == 0) A.R[t * N + jj] = jj == jp ? dgt : 0.0;
-                        continue;
-                    }
-                    if (lane == 0 && downdate_v(t, jj, N, h ? b : a, pj, nus[h], crs[h], A.R, A.nu, sbest, msum))
-                        A.flags[atomicAdd(nflag, 1)] = jj;
-                }
             }
         }
         sbest = block_best(sbest, sc);
@@ -2284,19 +2252,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
                     gsum += sq2;
                 }
             }
-        } else if (VAR != 5) {  // k_guard: warp per column, R(0:t, j) staged per warp
-            const bool rsm = t + 1 <= 64;
+        } else if (VAR != 5 && t + 1 <= 32) {
+            // k > 32: a warp per flagged column, the residual w - Q[:, :t+1] R(0:t+1, j) formed
+            // from the WY state in shared memory (Q_{t+1} r~ = r~ - Y T Y^T r~ with r~ = [r; 0]):
+            // p = Y[:t+1, :t+1]^T r, h = T p, x_i = w_i - [i <= t] r_i + Y(i, :) h
+            double* rw = rbuf[warp];       // r (t+1 values)
+            double* hw = rbuf[warp] + 32;  // p, then h
             for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
                  f += (int64_t)G * (kThreads / 32)) {
                 const int64_t j = A.flags[f];
-                if (rsm) {
-                    for (int64_t l = lane; l <= t; l += 32) rbuf[warp][l] = A.R[l * N + j];
-                    __syncwarp();
+                if (lane <= t) rw[lane] = A.R[(int64_t)lane * N + j];
+                __syncwarp();
+                if (lane <= t) {  // p_m = sum_{i=m..t} Y(i, m) r_i
+                    double a = 0.0;
+                    for (int64_t i = lane; i <= t; ++i) a = fma(ls.Y[i + (int64_t)lane * k], rw[i], a);
+                    hw[lane] = a;
                 }
+                __syncwarp();
+                double hl = 0.0;  // h_l = sum_{m=l..t} T(l, m) p_m
+                if (lane <= t)
+                    for (int64_t m = lane; m <= t; ++m) hl = fma(ls.T[lane + m * tld], hw[m], hl);
+                __syncwarp();
+                if (lane <= t) hw[lane] = hl;
+                __syncwarp();
                 double sq = 0.0;
                 for (int64_t i = lane; i < k; i += 32) {
                     double x = ld_w(g.W, g.ld, g.layout, i, j);
-                    for (int64_t l = 0; l <= t; ++l) x = fma(-g.Qt[i + l * k], rsm ? rbuf[warp][l] : A.R[l * N + j], x);
+                    if (i <= t) x -= rw[i];
+                    for (int64_t l = 0; l <= t && l <= i; ++l) x = fma(ls.Y[i + l * k], hw[l], x);
                     sq = fma(x, x, sq);
                 }
                 sq = warp_sum(sq);
@@ -2308,6 +2291,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
                     gsum += sq;
                 }
                 __syncwarp();
+            }
+        } else if (VAR != 5) {  // (t >= 32) k_guard: R(0:t, j) and Q from global memory
+            for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + warp; f < nf;
+                 f += (int64_t)G * (kThreads / 32)) {
+                const int64_t j = A.flags[f];
+                double sq = 0.0;
+                for (int64_t i = lane; i < k; i += 32) {
+                    double x = ld_w(g.W, g.ld, g.layout, i, j);
+                    for (int64_t l = 0; l <= t; ++l) x = fma(-g.Qt[i + l * k], A.R[l * N + j], x);
+                    sq = fma(x, x, sq);
+                }
+                sq = warp_sum(sq);
+                if (lane == 0) {
+                    A.nu[j] = sq;
+                    A.cref[j] = sq;
+                    const Cand c{sq, j == ct ? pp : g.pos[j], j};
+                    if (better(c, gbest)) gbest = c;
+                    gsum += sq;
+                }
             }
         }
         gbest = block_best(gbest, sc);
@@ -2449,7 +2451,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         }();
         static const std::string big_modes = [] {
             const char* e = std::getenv("TTG_BIG_MODES");
-            return std::string(e ? e : "56");
+            return std::string(e ? e : "567");
         }();
         // W larger than this streams long enough per step that the per-step kernels' full
         // occupancy beats the saved launches (measured: config 3's 24 x 7,962,624 cut)
@@ -2605,12 +2607,16 @@ bool WideQrcp::coop_run(int64_t steps) {
         }();
         A.lazy = lazy ? 1 : 0;
     }
-    if (big_ && mode_ == 5) {  // stream a row-layout copy of the narrow W (16-byte paired loads)
+    if (big_ && (mode_ == 5 || mode_ == 1)) {  // stream a row-layout copy of the Col W (16-byte pairs)
         const int64_t ldt = (N_ + 1) & ~int64_t(1);
         if (!Wt_.get()) {
             Wt_.alloc((size_t)(k_ * ldt));
-            const dim3 grid((unsigned)cdiv(N_, 64));
-            TTG_LAUNCH(k_narrow_to_rows, grid, kThreads, 0, stream(), W_, k_, N_, Wt_.get(), ldt);
+            if (mode_ == 5) {
+                const dim3 grid((unsigned)cdiv(N_, 64));
+                TTG_LAUNCH(k_narrow_to_rows, grid, kThreads, 0, stream(), W_, k_, N_, Wt_.get(), ldt);
+            } else {
+                transpose(W_, k_, N_, ld_, Wt_.get(), ldt);  // Wt[j + i * ldt] = W(i, j)
+            }
         }
         A.Ws = Wt_.get();
         A.lds = ldt;
@@ -2648,7 +2654,7 @@ bool WideQrcp::coop_run(int64_t steps) {
         }
     }
     static const char* const kBigNames[] = {
-        "k_pass1_big<1> (persistent step loop, warp per column)", "", "", "", "",
+        "k_pass1_big<1> (persistent step loop, row-layout copy, 16-byte paired columns)", "", "", "", "",
         "k_pass1_big<5> (persistent step loop, row-layout copy, 16-byte paired columns)",
         "k_pass1_big<6> (persistent step loop, 16-byte paired columns)",
         "k_pass1_big<7> (persistent step loop, 128-column strips)"};
