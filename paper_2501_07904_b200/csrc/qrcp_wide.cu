@@ -1596,7 +1596,8 @@ __global__ void __launch_bounds__(kThreads) k_guard_lane(const double* __restric
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
-    if (nf > 0) {
+    // CTAs without a flagged column skip the staging of Q (t+1 columns per CTA)
+    if (nf > (int64_t)blockIdx.x * kThreads) {
         const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
         stage_smem(qs, k * (t + 1), [&](int64_t e) { return Q[e]; });
         __syncthreads();
@@ -1642,7 +1643,8 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
     const int nf = *nflag;
     Cand best = cand_none();
     double msum = 0.0;
-    if (nf > 0) {
+    // CTAs without a flagged column skip the staging of Q (k (t+1) doubles per CTA)
+    if (nf > (int64_t)blockIdx.x * (kThreads / 32)) {
         const double bestnu = lazy ? best_stream_nu(scand, nscand) : -2.0;
         const bool staged = stage_q != 0;
         if (staged)
