@@ -2461,8 +2461,12 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_BIG_MAXMB");
             return (e ? std::atof(e) : 768.0) * 1048576.0;
         }();
-        if (!coop_ && !no_big && !no_coop && !shard && N > 16384 &&
-            8.0 * (double)k * (double)N <= big_max_bytes &&
+        // enough column pairs to give every thread of the loop work (a wide Col W streamed
+        // through its row-layout copy, or a long Row W of many rows)
+        const bool many_pairs = N >= (int64_t)sms * kThreads * 4;
+        const bool size_ok = 8.0 * (double)k * (double)N <= big_max_bytes || (k >= 64 && many_pairs);
+        if (!coop_ && !no_big && !no_coop && !shard && N > 16384 && size_ok &&
+            (mode_ != 1 || many_pairs) &&
             big_modes.find((char)('0' + mode_)) != std::string::npos &&
             big_smem_doubles(k, 32) * sizeof(double) <= kBigSmemMax) {
             coop_ = big_ = true;
