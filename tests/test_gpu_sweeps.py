@@ -288,3 +288,34 @@ def test_square_near_full_rank_cut_in_place(dev, ref):
     rr = ref.decompose(a, dims, "urv", "r2l", eps=1e-3)
     assert rep.ranks_chosen == rr.ranks_chosen
     assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
+
+
+def test_concurrent_host_threads_match_sequential(dev, ref):
+    """The API is reentrant: decompositions issued from several host threads at once (each
+    thread has its own stream; bench.py's e2e does this) give the same cores bit for bit
+    as the same calls made one after another."""
+    import threading
+
+    a, dims, ranks = cfg1(ref)
+    jobs = [("urv", "r2l", dict(ranks=ranks)), ("ulv", "l2r", dict(ranks=ranks)),
+            ("urv", "r2l", dict(eps=1e-6)), ("ulv", "l2r", dict(eps=1e-6))]
+
+    def run(m, s, kw):
+        r = dev.decompose_device(a, dims, m, s, **kw)
+        return [r.core(k) for k in range(r.order())]
+
+    seq = [run(*j) for j in jobs]
+    out = [None] * len(jobs)
+
+    def work(i):
+        out[i] = run(*jobs[i])
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for s_cores, c_cores in zip(seq, out):
+        assert len(s_cores) == len(c_cores)
+        for x, y in zip(s_cores, c_cores):
+            np.testing.assert_array_equal(x, y)
