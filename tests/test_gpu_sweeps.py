@@ -67,6 +67,28 @@ def test_hilbert_small_tolerance(dev, ref, method):
     _check_parity(dev, ref, a, dims, method, eps=1e-6)
 
 
+# 16^5: the first unfolding is 16 x 65,536 (ULV: Col, URV: Row), so pass 1 runs in the
+# persistent step loop (k_pass1_big<5> over the row-layout copy / <6>), its guard included
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+@pytest.mark.parametrize("mode", ["rank", "tol"])
+def test_persistent_loop_cuts(dev, ref, method, mode):
+    dims, ranks = [16] * 5, [1, 6, 8, 8, 6, 1]
+    a = planted_plus_noise(ref, dims, ranks, 9, 1e-6)
+    if mode == "rank":
+        _check_parity(dev, ref, a, dims, method, ranks=ranks)
+    else:
+        _check_parity(dev, ref, a, dims, method, eps=1e-4)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_persistent_loop_hilbert_guard(dev, ref, method):
+    """Shifted Hilbert 12 x 12 x 12 x 12 x 12 at a prescribed accuracy well above the noise
+    floor: many columns are flagged by the 1e-16 guard inside the persistent loop."""
+    dims = [12] * 5
+    a = shifted_hilbert(dims)
+    _check_parity(dev, ref, a, dims, method, eps=1e-5)
+
+
 @pytest.mark.parametrize("method", ["urv", "ulv"])
 def test_planted_exact_recovery(dev, ref, method):
     dims, ranks = [7, 6, 8, 5], [1, 3, 4, 2, 1]
