@@ -505,9 +505,9 @@ __global__ void __launch_bounds__(kT) k_col_norms(TallView s) {
 
 // k_col_apply with the column in registers (thread r holds rows t+1+r, t+1+r+kT, ...):
 // no shared memory, so several CTAs share an SM (R * kT >= N - t - 1).
-template <int R>
-__global__ void __launch_bounds__(kT) k_col_apply_reg(TallView s, int64_t t) {
-    __shared__ double sd[kT / 32];
+template <int R, int NT = kT>
+__global__ void __launch_bounds__(NT) k_col_apply_reg(TallView s, int64_t t) {
+    __shared__ double sd[NT / 32];
     const int64_t j = s.colmap[t + 1 + blockIdx.x];
     const double beta = s.beta[t];
     const double* __restrict__ v = s.B + s.colmap[t] * s.ld;
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kT) k_col_apply_reg(TallView s, int64_t t) {
     double d = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int64_t i = t + 1 + threadIdx.x + (int64_t)kT * r;
+        const int64_t i = t + 1 + threadIdx.x + (int64_t)NT * r;
         const bool in = i < s.N;
         x[r] = in ? c[i] : 0.0;
         w[r] = in ? v[i] : 0.0;
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kT) k_col_apply_reg(TallView s, int64_t t) {
         rt = __dsub_rn(rt, tj);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int64_t i = t + 1 + threadIdx.x + (int64_t)kT * r;
+            const int64_t i = t + 1 + threadIdx.x + (int64_t)NT * r;
             if (i < s.N) {
                 const double y = __dsub_rn(x[r], __dmul_rn(tj, w[r]));
                 c[i] = y;
@@ -635,6 +635,8 @@ void TallQrcp::run(int64_t steps) {
             const int64_t len = N_ - t - 1, nc = n_ - t - 1;
             if (N_ <= kWarpRows)
                 TTG_LAUNCH(k_col_apply_warp, (int)cdiv(nc, kT / 32), kT, 0, stream(), s, t);
+            else if (len <= 32 * 128)  // 128-thread CTAs: more columns resident per SM
+                TTG_LAUNCH((k_col_apply_reg<32, 128>), (int)nc, 128, 0, stream(), s, t);
             else if (len <= 16 * kT)
                 TTG_LAUNCH(k_col_apply_reg<16>, (int)nc, kT, 0, stream(), s, t);
             else if (len <= 32 * kT)
