@@ -215,100 +215,121 @@ __global__ void __launch_bounds__(kT, 1) k_tsqr_reg(const double* __restrict__ B
 template <int S, int RPT>
 __global__ void __launch_bounds__(kT, 1) k_tsqr_unr(const double* __restrict__ B, int64_t N, int s, int64_t ld,
                                                     double* __restrict__ out, int64_t ldo) {
+    // A CTA streams its share of the rows through the register block: the first chunk
+    // fills all ROWS rows, every later chunk keeps the running triangle in rows 0..S-1
+    // (threads 0..S-1, slot 0) and refills the other ROWS - S rows, so one triangle per
+    // CTA (one per SM) leaves the leaf level instead of one per ROWS rows.
     constexpr int ROWS = kT * RPT, NW = kT / 32;
     __shared__ double part[NW][S];
     __shared__ double tau[S];
     __shared__ double red[NW];
     __shared__ double bc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
-    const int rows = (int)min((int64_t)ROWS, N - r0);
+    const int64_t per = (N + gridDim.x - 1) / gridDim.x;
+    const int64_t g0 = (int64_t)blockIdx.x * per, g1 = min(N, g0 + per);
     double x[RPT][S];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-        const int row = i * kT + tid;
-#pragma unroll
-        for (int j = 0; j < S; ++j) x[i][j] = (row < rows && j < s) ? B[r0 + row + (int64_t)j * ld] : 0.0;
-    }
-    const int p = min(rows, s);
-#pragma unroll
-    for (int c = 0; c < S; ++c) {
-        if (c >= p) break;
-        double sg = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i)
-            if (i * kT + tid > c) sg = fma(x[i][c], x[i][c], sg);
-        sg = warp_sum(sg);
-        if (lane == 0) red[warp] = sg;
-        if (tid == c) bc = x[0][c];
-        __syncthreads();
-        double sigma = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) sigma += red[w];
-        const double alpha = bc;
-        if (rows - c <= 1 || sigma == 0.0) {
-            __syncthreads();
-            continue;
-        }
-        const double mu = sqrt(fma(alpha, alpha, sigma));
-        const double smu = copysign(mu, alpha);
-        const double v0 = alpha + smu;
-        const double beta = v0 / smu;
-        double v[RPT];
+    int p = 0;  // rows of the running triangle held in rows 0..p-1 of the block
+    for (int64_t base = g0; base < g1 || (base == g0 && g0 >= g1);) {
+        const int keep = p;  // rows 0..keep-1 hold R from the previous chunk
+        const int64_t avail = max((int64_t)0, g1 - base);
+        const int fresh = (int)min((int64_t)(ROWS - keep), avail);
+        const int rows = keep + fresh;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
             const int row = i * kT + tid;
-            v[i] = row > c ? x[i][c] / v0 : (row == c ? 1.0 : 0.0);
-        }
-        double d[S];
+            if (row < keep) {  // R row: zero below its diagonal
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-            double t = 0.0;
-            if (j > c) {
+                for (int j = 0; j < S; ++j)
+                    if (j < row) x[i][j] = 0.0;
+            } else {
+                const bool in = row < rows;
+                const int64_t gr = base + (row - keep);
 #pragma unroll
-                for (int i = 0; i < RPT; ++i) t = fma(v[i], x[i][j], t);
-            }
-            d[j] = t;
-        }
-        if (S < 32) {
-#pragma unroll
-            for (int off = 16; off >= S; off >>= 1)
-#pragma unroll
-                for (int j = 0; j < S; ++j) d[j] += __shfl_xor_sync(0xffffffffu, d[j], off);
-        }
-#pragma unroll
-        for (int h = S / 2; h >= 1; h >>= 1) {
-            const bool up = (lane & h) != 0;
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-                const double send = up ? d[j] : d[j + h];
-                const double keep = up ? d[j + h] : d[j];
-                d[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+                for (int j = 0; j < S; ++j) x[i][j] = (in && j < s) ? B[gr + (int64_t)j * ld] : 0.0;
             }
         }
-        if (lane < S) part[warp][lane] = d[0];
-        __syncthreads();
-        if (tid < S) {
-            double w = 0.0;
+        base += fresh;
+        p = min(rows, s);
 #pragma unroll
-            for (int q = 0; q < NW; ++q) w += part[q][tid];
-            tau[tid] = beta * w;
-        }
-        __syncthreads();
+        for (int c = 0; c < S; ++c) {
+            if (c >= p) break;
+            double sg = 0.0;
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-            if (j > c) {
-                const double tj = tau[j];
+            for (int i = 0; i < RPT; ++i)
+                if (i * kT + tid > c && i * kT + tid < rows) sg = fma(x[i][c], x[i][c], sg);
+            sg = warp_sum(sg);
+            if (lane == 0) red[warp] = sg;
+            if (tid == c) bc = x[0][c];
+            __syncthreads();
+            double sigma = 0.0;
 #pragma unroll
-                for (int i = 0; i < RPT; ++i) x[i][j] = fma(-tj, v[i], x[i][j]);
+            for (int w = 0; w < NW; ++w) sigma += red[w];
+            const double alpha = bc;
+            if (rows - c <= 1 || sigma == 0.0) {
+                __syncthreads();
+                continue;
             }
+            const double mu = sqrt(fma(alpha, alpha, sigma));
+            const double smu = copysign(mu, alpha);
+            const double v0 = alpha + smu;
+            const double beta = v0 / smu;
+            double v[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int row = i * kT + tid;
+                v[i] = (row > c && row < rows) ? x[i][c] / v0 : (row == c ? 1.0 : 0.0);
+            }
+            double d[S];
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                double t = 0.0;
+                if (j > c) {
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) t = fma(v[i], x[i][j], t);
+                }
+                d[j] = t;
+            }
+            if (S < 32) {
+#pragma unroll
+                for (int off = 16; off >= S; off >>= 1)
+#pragma unroll
+                    for (int j = 0; j < S; ++j) d[j] += __shfl_xor_sync(0xffffffffu, d[j], off);
+            }
+#pragma unroll
+            for (int h = S / 2; h >= 1; h >>= 1) {
+                const bool up = (lane & h) != 0;
+#pragma unroll
+                for (int j = 0; j < h; ++j) {
+                    const double send = up ? d[j] : d[j + h];
+                    const double keep2 = up ? d[j + h] : d[j];
+                    d[j] = keep2 + __shfl_xor_sync(0xffffffffu, send, h);
+                }
+            }
+            if (lane < S) part[warp][lane] = d[0];
+            __syncthreads();
+            if (tid < S) {
+                double w = 0.0;
+#pragma unroll
+                for (int q = 0; q < NW; ++q) w += part[q][tid];
+                tau[tid] = beta * w;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                if (j > c) {
+                    const double tj = tau[j];
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) x[i][j] = fma(-tj, v[i], x[i][j]);
+                }
+            }
+            if (tid == c) x[0][c] = -smu;
         }
-        if (tid == c) x[0][c] = -smu;
+        if (g0 >= g1) break;
     }
     if (tid < s) {
 #pragma unroll
         for (int j = 0; j < S; ++j)
-            if (j < s) out[(int64_t)blockIdx.x * s + tid + (int64_t)j * ldo] = (j >= tid && tid < rows) ? x[0][j] : 0.0;
+            if (j < s) out[(int64_t)blockIdx.x * s + tid + (int64_t)j * ldo] = (j >= tid && tid < p) ? x[0][j] : 0.0;
     }
 }
 
@@ -767,7 +788,8 @@ void tsqr_reg_tree(const double* B, int64_t N, int64_t s, int64_t ld, double* Ro
     bool leaf = true;
     while (true) {
         const bool unr = leaf && cdiv(rows, (int64_t)kT * RL) >= sm_count();
-        const int64_t nb = cdiv(rows, (int64_t)kT * (unr ? RL : RU));
+        // the unrolled leaf runs one CTA per SM, each streaming its share of the rows
+        const int64_t nb = unr ? (int64_t)sm_count() : cdiv(rows, (int64_t)kT * RU);
         double* dst = Rout;
         DevBuf<double> nxt;
         if (nb > 1) {
