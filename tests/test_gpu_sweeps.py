@@ -90,6 +90,16 @@ def test_persistent_loop_hilbert_guard(dev, ref, method):
 
 
 @pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_long_first_unfolding_tsqr(dev, ref, method):
+    """16^5 x 8 shifted Hilbert: the first unfolding has 524,288 (ULV) / 1,048,576 (URV)
+    columns and an ill-conditioned R1, so pass 2 takes the TSQR route with the streaming
+    leaf (one CTA per SM folding its rows into one triangle)."""
+    dims = [16, 16, 16, 16, 16, 8]
+    a = shifted_hilbert(dims)
+    _check_parity(dev, ref, a, dims, method, eps=1e-5)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
 def test_planted_exact_recovery(dev, ref, method):
     dims, ranks = [7, 6, 8, 5], [1, 3, 4, 2, 1]
     a = ref.gen_planted_dense(dims, ranks, 301)
