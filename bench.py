@@ -152,13 +152,21 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
-def ncu_traffic(cfg: int):
+def ncu_traffic(cfg: int, kernel: str = ""):
+    """ncu DRAM traffic of one launch of `kernel` on this config (profiles/traffic.json:
+    entries keyed by config, optionally with a suffix, each naming its kernel)."""
     p = ROOT / "profiles" / "traffic.json"
     try:
         d = json.loads(p.read_text())
     except Exception:
         return None
-    t = d.get(str(cfg))
+    t = None
+    for key, v in d.items():
+        if (key == str(cfg) or key.startswith(f"{cfg}_")) and v.get("kernel") and kernel.startswith(v["kernel"]):
+            t = v
+            break
+    if t is None:
+        t = d.get(str(cfg))
     # the DRAM peak ncu implies is a property of the part, not of the config
     if t is not None and "implied_dram_peak_gbs_ncu" not in t:
         for v in d.values():
@@ -381,7 +389,7 @@ def run_ours(args):
     dom = kernels[0] if kernels else {"kernel": "k_stream", "ms": kern_ms, "launches": nk,
                                       "achieved_gbs": achieved_family}
     achieved = dom["achieved_gbs"]
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config, dom["kernel"])
     ncu_peak = (traffic or {}).get("implied_dram_peak_gbs_ncu")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
