@@ -1892,7 +1892,7 @@ __host__ __device__ size_t big_smem_doubles(int64_t k, int64_t capS) {
     if (k <= 32) d += (size_t)(k * capS);  // Q[:, :t+1] for the lane guard
     return d;
 }
-constexpr size_t kBigSmemMax = 200 * 1024;
+constexpr size_t kBigSmemMax = 212 * 1024;  // + the kernel's ~14 KB of static shared memory <= 227 KB
 
 // Row-layout copy of a narrow Col W (k <= 32, ld == k): Wt[i * ldt + j] = W[i + j * k],
 // 64 columns per CTA through shared memory (coalesced reads of the contiguous block,
@@ -2584,7 +2584,7 @@ bool WideQrcp::coop_run(int64_t steps) {
     if (explicit_ || comm_) return false;
     PhaseTimer pt(big_ ? "p1 persistent (big)" : "p1 persistent (coop)");
     const size_t smem = (big_ ? big_smem_doubles(k_, cap_) : coop_smem_doubles(k_, cap_)) * sizeof(double);
-    if (smem > 200 * 1024) return false;
+    if (smem > (big_ ? kBigSmemMax : 200 * 1024)) return false;
     auto kern = !big_        ? (layout_ == Layout::Col ? k_pass1_coop<0> : k_pass1_coop<1>)
                 : mode_ == 5 ? k_pass1_big<5>
                 : mode_ == 6 ? k_pass1_big<6>
