@@ -352,6 +352,9 @@ def run_ours(args):
             if concurrent:
                 out = [None] * len(runs)
                 def work(i, m, s):
+                    # a new host thread starts on device 0: select this rank's GPU first
+                    torch.cuda.set_device(local)
+                    check(lib().ttg_set_device(local))
                     out[i] = e2e_one(m, s)
                 th = [threading.Thread(target=work, args=(i, m, s)) for i, (m, s) in enumerate(runs)]
                 for x in th:
