@@ -438,8 +438,8 @@ __global__ void __launch_bounds__(kT) k_q_col(TallView s, int64_t t, double* Q, 
 // owns rows t+1+l, t+1+l+32, ...), eight columns per CTA.
 constexpr int64_t kWarpRows = 2048;
 
+template <int R>  // rows per lane: R * 32 >= N - t - 1
 __global__ void __launch_bounds__(kT) k_col_apply_warp(TallView s, int64_t t) {
-    constexpr int R = kWarpRows / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t q = t + 1 + (int64_t)blockIdx.x * (kT / 32) + warp;
     if (q >= s.n) return;
@@ -634,7 +634,12 @@ void TallQrcp::run(int64_t steps) {
             PhaseTimer pt(N_ <= kWarpRows ? "col apply (warp)" : "col apply (cta)");
             const int64_t len = N_ - t - 1, nc = n_ - t - 1;
             if (N_ <= kWarpRows)
-                TTG_LAUNCH(k_col_apply_warp, (int)cdiv(nc, kT / 32), kT, 0, stream(), s, t);
+            {
+                auto kern = len <= 16 * 32 ? k_col_apply_warp<16>
+                            : len <= 32 * 32 ? k_col_apply_warp<32>
+                                             : k_col_apply_warp<kWarpRows / 32>;
+                TTG_LAUNCH(kern, (int)cdiv(nc, kT / 32), kT, 0, stream(), s, t);
+            }
             else if (len <= 32 * 128)  // 128-thread CTAs: more columns resident per SM
                 TTG_LAUNCH((k_col_apply_reg<32, 128>), (int)nc, 128, 0, stream(), s, t);
             else if (len <= 16 * kT)
