@@ -291,6 +291,8 @@ def run_ours(args):
     d0, d1 = C_double(), C_double()
     lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))  # discard warm-up records
     lib().ttg_profile_reset_kernels()
+    big_ph = (ctypes.c_double * 24)()
+    lib().ttg_profile_big_phases(big_ph, 1)  # zero the persistent loop's phase totals
     launches0 = lib().ttg_kernel_launches()
     if dist:
         dist.barrier()
@@ -317,6 +319,7 @@ def run_ours(args):
     log("device ms per step: " + " ".join(f"{marks[i].elapsed_time(marks[i + 1]):.1f}" for i in range(args.steps)))
     nk = lib().ttg_profile_read(ctypes.byref(d0), ctypes.byref(d1))
     lib().ttg_profile_enable(0)
+    lib().ttg_profile_big_phases(big_ph, 0)  # the timed steps' persistent-loop phase totals
     kern_ms, kern_bytes = d0.value, d1.value
     ms_max = max_over_ranks(ms, dist)
     entries_per_step = len(runs) * n
@@ -393,6 +396,18 @@ def run_ours(args):
                                       "achieved_gbs": achieved_family}
     achieved = dom["achieved_gbs"]
     traffic = ncu_traffic(args.config, dom["kernel"])
+    # persistent loop: its phase split (CTA 0's %globaltimer, summed over the timed steps),
+    # so the stream phase's own rate shows beside the whole-launch figure
+    phases = None
+    if dom["kernel"].startswith("k_pass1_big<"):
+        v = int(dom["kernel"][len("k_pass1_big<")])
+        refl, strm, grd = big_ph[3 * v], big_ph[3 * v + 1], big_ph[3 * v + 2]
+        sbytes = next((kby[i] for i in range(min(nk_kinds, nmax)) if names[i].decode() == dom["kernel"]), 0.0)
+        sgbs = sbytes / (strm * 1e-3) / 1e9 if strm > 0 else None
+        phases = {"reflector_ms": refl, "stream_ms": strm, "guard_ms": grd, "stream_achieved_gbs": sgbs,
+                  "stream_frac": sgbs / peak if (sgbs and peak) else None,
+                  "note": "CTA 0's %globaltimer per step: stream = reflector end to the first grid barrier "
+                          "(the slowest CTA's stream plus the barrier)"}
     ncu_peak = (traffic or {}).get("implied_dram_peak_gbs_ncu")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -415,7 +430,7 @@ def run_ours(args):
                          "note": ("hbm_gbs is a read+write copy rate; a read-dominated stream can exceed it; "
                                   "traffic = ncu DRAM bytes of one launch of this kernel (profiles/traffic.json)"),
                          "frac_vs_ncu_dram_peak": achieved / ncu_peak if ncu_peak else None,
-                         "traffic": traffic, "launches": dom["launches"], "kernel_ms": dom["ms"],
+                         "traffic": traffic, "phases": phases, "launches": dom["launches"], "kernel_ms": dom["ms"],
                          "share_of_step": dom["ms"] / ms if ms > 0 else None,
                          "stream_family": {"achieved": achieved_family, "frac": achieved_family / peak if peak else None,
                                            "launches": nk, "kernel_ms": kern_ms,

@@ -104,6 +104,10 @@ int64_t ttg_profile_read(double* total_ms, double* algorithmic_bytes);
  * stream kernel variant. Returns the number of kernels (<= max are written). */
 int ttg_profile_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches);
 void ttg_profile_reset_kernels(void);
+/* Phase split of the persistent pass-1 loop (k_pass1_big<v>, v < 8), device time of CTA 0
+ * in ms summed over steps since the last reset: out24[v*3 + 0] reflector, [+1] stream
+ * (through the first grid barrier), [+2] guard (through the second). Host sync. */
+ttg_status ttg_profile_big_phases(double* out24, int reset);
 
 /* ---- tensor-train sweeps ---------------------------------------------------- */
 /* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`

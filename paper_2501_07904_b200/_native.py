@@ -74,6 +74,7 @@ SIGNATURES = {
     "ttg_profile_read": (C.c_int64, [c_double_p, c_double_p]),
     "ttg_profile_kernels": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), c_double_p, c_double_p, c_int64_p]),
     "ttg_profile_reset_kernels": (None, []),
+    "ttg_profile_big_phases": (C.c_int, [c_double_p, C.c_int]),
     "ttg_decompose": (C.c_int, [C.c_void_p, c_int64_p, C.c_int, C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
     "ttg_result_free": (None, [C.c_void_p]),
     "ttg_result_order": (C.c_int, [C.c_void_p]),

@@ -134,6 +134,10 @@ int ttg_profile_kernels(int max, const char** names, double* ms, double* bytes, 
 
 void ttg_profile_reset_kernels(void) { ttg::prof_reset_kernels(); }
 
+ttg_status ttg_profile_big_phases(double* out24, int reset) {
+    return guard([&] { ttg::big_phase_stats(out24, reset != 0); });
+}
+
 ttg_status ttg_profile_enable(int on) {
     return guard([&] { ttg::prof_enable(on != 0); });
 }

@@ -77,6 +77,9 @@ void prof_end(double algorithmic_bytes, const char* kernel);
 int64_t prof_read(double* total_ms, double* bytes);
 int prof_kernels(int max, const char** names, double* ms, double* bytes, int64_t* launches);
 void prof_reset_kernels();
+// Persistent pass-1 loop phase totals (ms): out[v*3 + {0 reflector, 1 stream, 2 guard}]
+// for k_pass1_big<v>, v < 8 (host sync); reset zeroes them.
+void big_phase_stats(double* out, bool reset);
 
 // TTG_PHASES=1 (diagnostics): event-timed phases on the thread's stream, totals printed at
 // exit. Use as `PhaseTimer pt("name");` around a phase.

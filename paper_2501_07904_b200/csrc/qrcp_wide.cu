@@ -518,6 +518,10 @@ __global__ void __launch_bounds__(kThreads) k_wy_fused(WY s, int64_t t) {
     wy_q(s, t, 0);
 }
 
+// k_pass1_big phase totals (CTA 0, %globaltimer ns) per variant: [VAR][0] reflector (pick
+// to q_t), [1] stream (through the first grid barrier), [2] guard (through the second)
+__device__ unsigned long long g_big_phase[8][3];
+
 // TTG_WY_TRACE=1 diagnostics: k_wy_fused_smem phase times (thread 0, ns), accumulated
 __device__ int g_wy_trace = 0;
 __device__ unsigned long long g_wy_acc[16];
@@ -1956,11 +1960,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
                 [&](int64_t e) { return (e % t0) + (e / t0) * tld; });
     }
     __syncthreads();
+    unsigned long long ph_t[6] = {0, 0, 0, 0, 0, 0};
     auto stamp = [&](int64_t t, int ph) {
-        if (A.trace && blockIdx.x == 0 && tid == 0) {
+        if (blockIdx.x == 0 && tid == 0) {
             unsigned long long ns;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-            A.trace[(t - A.t0) * 8 + ph] = ns;
+            ph_t[ph] = ns;
+            if (A.trace) A.trace[(t - A.t0) * 8 + ph] = ns;
+            if (ph == 5) {  // step done: accumulate its phases
+                atomicAdd(&g_big_phase[VAR][0], ph_t[1] - ph_t[0]);
+                atomicAdd(&g_big_phase[VAR][1], ph_t[3] - ph_t[1]);
+                atomicAdd(&g_big_phase[VAR][2], ph_t[5] - ph_t[3]);
+            }
         }
     };
     for (int64_t t = A.t0; t < A.t1; ++t) {
@@ -2365,6 +2376,18 @@ __global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__
 }
 
 }  // namespace
+
+// Phase totals of the persistent loop (ms) per variant since the last reset (host sync).
+void big_phase_stats(double* out, bool reset) {
+    unsigned long long h[8][3] = {};
+    TTG_CUDA(cudaMemcpyFromSymbol(h, g_big_phase, sizeof(h)));
+    for (int v = 0; v < 8; ++v)
+        for (int p = 0; p < 3; ++p) out[v * 3 + p] = 1e-6 * (double)h[v][p];
+    if (reset) {
+        unsigned long long z[8][3] = {};
+        TTG_CUDA(cudaMemcpyToSymbol(g_big_phase, z, sizeof(z)));
+    }
+}
 
 namespace {
 struct WyTrace {
