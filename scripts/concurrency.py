@@ -30,3 +30,14 @@ for mode, ptr, dev in (("host", host.data_ptr(), False), ("device", a.data_ptr()
                 for m, s in runs: one(m, s, ptr, dev)
             ts.append(1e3 * (time.perf_counter() - t0))
         print(f"{mode} {'concurrent' if conc else 'sequential'}: " + " ".join(f"{x:.1f}" for x in ts) + f" ms  ranks {out}", flush=True)
+
+# independent worker threads: each thread runs all `reps` decompositions of its kind
+def loop(m, s, ptr, dev, n):
+    for _ in range(n):
+        one(m, s, ptr, dev)
+for mode, ptr, dev in (("host", host.data_ptr(), False),):
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=loop, args=(m, s, ptr, dev, reps)) for m, s in runs]
+    for x in th: x.start()
+    for x in th: x.join()
+    print(f"{mode} independent threads: {1e3 * (time.perf_counter() - t0) / reps:.1f} ms per step", flush=True)
