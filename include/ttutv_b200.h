@@ -109,12 +109,31 @@ void ttg_profile_reset_kernels(void);
  * (through the first grid barrier), [+2] guard (through the second). Host sync. */
 ttg_status ttg_profile_big_phases(double* out24, int reset);
 
+/* ---- files straight to and from the device --------------------------------------
+ * The reference's binary containers (include/ttutv/io.hpp:10-19): TTUTVTEN dense tensors
+ * and TTUTVCOR trains. Payloads stream through pinned chunks (the file read of one chunk
+ * overlapping the H2D copy of the previous one), so a tensor file never has a host copy;
+ * header checks, messages and offsets are read_tensor()'s (src/io.cpp:151-161).
+ *   ttg_tensor_file_header    <- read_tensor() header      src/io.cpp:151-161 (host only)
+ *   ttg_tensor_file_to_device <- read_tensor() payload
+ *   ttg_decompose_file        <- read_tensor() + decompose()
+ *   ttg_result_write_file     <- write_tt()                src/io.cpp:163-174
+ * dims must hold 255 entries. On TTG_ERR_PARSE, ttg_last_error_offset() is the byte
+ * offset the reference's ParseError carries. */
+ttg_status ttg_tensor_file_header(const char* path, int* order, int64_t* dims);
+ttg_status ttg_tensor_file_to_device(const char* path, double* dst, int64_t capacity);
+int64_t ttg_last_error_offset(void);
+
 /* ---- tensor-train sweeps ---------------------------------------------------- */
 /* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`
  * is a host pointer (copied in, timed in the report) or a device pointer (read in place). */
 ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_config* cfg,
                          int a_on_device, ttg_result** out);
+/* ttg_decompose() on the tensor in a TTUTVTEN file, read straight to the device. */
+ttg_status ttg_decompose_file(const char* path, const ttg_config* cfg, ttg_result** out);
 void ttg_result_free(ttg_result* res);
+/* The result's train as a TTUTVCOR file, byte-identical to the reference's write_tt(). */
+ttg_status ttg_result_write_file(const ttg_result* res, const char* path);
 int ttg_result_order(const ttg_result* res);
 void ttg_result_core_dims(const ttg_result* res, int k, int64_t dims3[3]); /* k is 0-based */
 ttg_status ttg_result_core_copy(const ttg_result* res, int k, double* host_out);

@@ -57,6 +57,9 @@ def lib():
         h.ref_frobenius_norm.argtypes = [dp, C.c_int64]
         h.ref_frobenius_norm.restype = C.c_double
         h.ref_set_parallel.argtypes = [C.c_int]
+        h.ref_read_tensor.argtypes = [C.c_char_p, ip, C.POINTER(C.c_int), ip, dp]
+        h.ref_write_tensor.argtypes = [C.c_char_p, dp, ip, C.c_int]
+        h.ref_write_tt.argtypes = [C.c_char_p, C.c_int, ip, ip, dp]
         _lib = h
     return _lib
 
@@ -208,3 +211,34 @@ def frobenius_norm(a) -> float:
 
 def set_parallel(enabled: bool):
     lib().ref_set_parallel(int(enabled))
+
+
+def read_tensor(path):
+    """The reference's read_tensor: (dims, flat payload) or raises RefError; a ParseError
+    (code 3) carries `.offset`."""
+    off = np.zeros(1, np.int64)
+    order = C.c_int()
+    dims = np.zeros(255, np.int64)
+    st = lib().ref_read_tensor(str(path).encode(), _i(off), C.byref(order), _i(dims), None)
+    if st != 0:
+        e = RefError(st, lib().ref_last_error().decode())
+        e.message, e.offset = lib().ref_last_error().decode(), int(off[0])
+        raise e
+    d = dims[: order.value].copy()
+    out = np.zeros(int(np.prod(d)), np.float64)
+    _check(lib().ref_read_tensor(str(path).encode(), _i(off), C.byref(order), _i(dims), _d(out)))
+    return d.tolist(), out
+
+
+def write_tensor(path, a, dims):
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    dims = np.asarray(dims, dtype=np.int64)
+    _check(lib().ref_write_tensor(str(path).encode(), _d(a), _i(dims), dims.size))
+
+
+def write_tt(path, cores):
+    """write_tt of cores given as (r_{k-1}, I_k, r_k) arrays in storage (Fortran) order."""
+    ranks = np.array([c.shape[0] for c in cores] + [cores[-1].shape[2]], np.int64)
+    dims = np.array([c.shape[1] for c in cores], np.int64)
+    flat = np.concatenate([np.asarray(c, np.float64).reshape(-1, order="F") for c in cores])
+    _check(lib().ref_write_tt(str(path).encode(), len(cores), _i(ranks), _i(dims), _d(flat)))

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "ttutv/io.hpp"
 #include "ttutv/errors.hpp"
 #include "ttutv/factor.hpp"
 #include "ttutv/generators.hpp"
@@ -279,6 +280,51 @@ uint64_t ref_rng_u64(uint64_t seed, int64_t skip) {
     ttutv::Rng rng(seed);
     for (int64_t i = 0; i < skip; ++i) rng.next_u64();
     return rng.next_u64();
+}
+
+// ---- binary containers (io.hpp) ---------------------------------------------
+// read_tensor: status, and on ParseError its message (ref_last_error, without the
+// " (at offset N)" suffix what() adds) and offset; on success order, dims and (if payload
+// is not null) the elements.
+int ref_read_tensor(const char* path, int64_t* offset, int* order, int64_t* dims, double* payload) {
+    *offset = -1;
+    try {
+        ttutv::DenseTensor t = ttutv::read_tensor(path);
+        *order = (int)t.order();
+        for (int k = 0; k < t.order(); ++k) dims[k] = t.shape().dims()[(size_t)k];
+        if (payload) std::memcpy(payload, t.data(), sizeof(double) * (size_t)t.element_count());
+        g_msg.clear();
+        return 0;
+    } catch (const ttutv::ParseError& e) {
+        const std::string w = e.what();
+        const std::string suffix = " (at offset " + std::to_string(e.offset()) + ")";
+        g_msg = w.size() >= suffix.size() && w.compare(w.size() - suffix.size(), suffix.size(), suffix) == 0
+                    ? w.substr(0, w.size() - suffix.size())
+                    : w;
+        *offset = e.offset();
+        return 3;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return 7;
+    }
+}
+
+int ref_write_tensor(const char* path, const double* a, const int64_t* dims, int d) {
+    return guarded([&] { ttutv::write_tensor(path, tensor_of(a, dims, d)); });
+}
+
+// write_tt of the train with cores (ranks[k], dims[k], ranks[k+1]) back to back in `flat`
+int ref_write_tt(const char* path, int d, const int64_t* ranks, const int64_t* dims, const double* flat) {
+    return guarded([&] {
+        std::vector<ttutv::TTCore> cores;
+        const double* p = flat;
+        for (int k = 0; k < d; ++k) {
+            const int64_t cd[3] = {ranks[k], dims[k], ranks[k + 1]};
+            cores.push_back(ttutv::TTCore{tensor_of(p, cd, 3)});
+            p += cd[0] * cd[1] * cd[2];
+        }
+        ttutv::write_tt(path, ttutv::TTTensor(std::move(cores)));
+    });
 }
 
 }  // extern "C"

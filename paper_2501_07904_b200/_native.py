@@ -28,7 +28,11 @@ class TTIndexError(TTUTVError):
 
 
 class ParseError(TTUTVError):
-    pass
+    """ttutv::ParseError: the message and the byte offset (errors.hpp:28-36)."""
+
+    def __init__(self, msg: str, offset: int = 0):
+        super().__init__(f"{msg} (at offset {offset})")
+        self.message, self.offset = msg, offset
 
 
 class NumericalError(TTUTVError):
@@ -75,6 +79,11 @@ SIGNATURES = {
     "ttg_profile_kernels": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), c_double_p, c_double_p, c_int64_p]),
     "ttg_profile_reset_kernels": (None, []),
     "ttg_profile_big_phases": (C.c_int, [c_double_p, C.c_int]),
+    "ttg_last_error_offset": (C.c_int64, []),
+    "ttg_tensor_file_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), c_int64_p]),
+    "ttg_tensor_file_to_device": (C.c_int, [C.c_char_p, C.c_void_p, C.c_int64]),
+    "ttg_decompose_file": (C.c_int, [C.c_char_p, C.POINTER(Config), C.POINTER(C.c_void_p)]),
+    "ttg_result_write_file": (C.c_int, [C.c_void_p, C.c_char_p]),
     "ttg_decompose": (C.c_int, [C.c_void_p, c_int64_p, C.c_int, C.POINTER(Config), C.c_int, C.POINTER(C.c_void_p)]),
     "ttg_result_free": (None, [C.c_void_p]),
     "ttg_result_order": (C.c_int, [C.c_void_p]),
@@ -136,6 +145,8 @@ def lib() -> C.CDLL:
 def check(status: int) -> None:
     if status != 0:
         msg = lib().ttg_last_error().decode(errors="replace")
+        if status == 3:
+            raise ParseError(msg, int(lib().ttg_last_error_offset()))
         raise ERRORS.get(status, TTUTVError)(msg)
 
 

@@ -173,6 +173,39 @@ def decompose_device(a, dims, method="urv", sweep="r2l", ranks=None, eps=None, w
     return DeviceResult(h)
 
 
+# ---- files straight to and from the device (io.hpp / io.cpp:139-211) -----------------------
+
+def tensor_file_header(path) -> list:
+    """Dims of a TTUTVTEN file (read_tensor's header checks; host only, no device needed)."""
+    order = C.c_int()
+    dims = np.zeros(255, np.int64)
+    check(lib().ttg_tensor_file_header(str(path).encode(), C.byref(order), _iptr(dims)))
+    return dims[: order.value].tolist()
+
+
+def tensor_file_to_device(path, dst_ptr: int, capacity: int) -> list:
+    """Stream a TTUTVTEN payload into device memory at dst_ptr (capacity in elements)."""
+    require_gpu()
+    check(lib().ttg_tensor_file_to_device(str(path).encode(), C.c_void_p(int(dst_ptr)), int(capacity)))
+    return tensor_file_header(path)
+
+
+def decompose_file(path, method="urv", sweep="r2l", ranks=None, eps=None, weights=(), refine_passes=1,
+                   retain="l11_only", debug_checks=False, qlp="early_exit") -> DeviceResult:
+    """decompose() of the tensor in a TTUTVTEN file, read straight to the device."""
+    require_gpu()
+    cfg, keep = _config(method, sweep, ranks, eps, weights, refine_passes, retain, debug_checks, qlp)
+    h = C.c_void_p()
+    check(lib().ttg_decompose_file(str(path).encode(), C.byref(cfg), C.byref(h)))
+    del keep
+    return DeviceResult(h)
+
+
+def write_result_file(res: DeviceResult, path) -> None:
+    """The result's train as a TTUTVCOR file (byte-identical to the reference's write_tt)."""
+    check(lib().ttg_result_write_file(res.h, str(path).encode()))
+
+
 # ---- multi-GPU (column-sharded first cut, SURVEY.md 8(e)) ---------------------------------
 
 class Comm:

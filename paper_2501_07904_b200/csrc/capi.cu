@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/ttutv_b200.h"
+#include "io.hpp"
 #include "sweep.hpp"
 #include "utv.hpp"
 
@@ -168,6 +169,50 @@ ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_
 }
 
 void ttg_result_free(ttg_result* res) { delete res; }
+
+// ---- files straight to and from the device (src/io.cpp:139-211) ----
+int64_t ttg_last_error_offset(void) { return ttg::last_parse_offset(); }
+
+ttg_status ttg_tensor_file_header(const char* path, int* order, int64_t* dims) {
+    return guard([&] {
+        if (!path) ttg::argument_error("null path");
+        const ttg::TensorFileHeader h = ttg::read_tensor_header(path);
+        *order = (int)h.dims.size();
+        if (dims) std::copy(h.dims.begin(), h.dims.end(), dims);
+    });
+}
+
+ttg_status ttg_tensor_file_to_device(const char* path, double* dst, int64_t capacity) {
+    return guard([&] {
+        if (!path) ttg::argument_error("null path");
+        ttg::tensor_file_to_device(path, dst, capacity);
+    });
+}
+
+ttg_status ttg_decompose_file(const char* path, const ttg_config* cfg, ttg_result** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (!cfg) ttg::argument_error("null config");
+        if (!path) ttg::argument_error("null path");
+        const auto start = std::chrono::steady_clock::now();
+        const ttg::TensorFileHeader h = ttg::read_tensor_header(path);
+        const ttg::SweepConfig sc = sweep_config(cfg);
+        ttg::DevBuf<double> a((size_t)h.count);
+        ttg::tensor_file_to_device(path, a.get(), h.count);
+        auto* res = new ttg_result{ttg::decompose(a.get(), h.dims, sc)};
+        res->r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+        *out = res;
+    });
+}
+
+ttg_status ttg_result_write_file(const ttg_result* res, const char* path) {
+    return guard([&] {
+        if (!res || !path) ttg::argument_error("null argument");
+        std::vector<const double*> cores;
+        for (const auto& c : res->r.cores) cores.push_back(c.get());
+        ttg::write_train_file(path, res->r.core_dims, cores);
+    });
+}
 
 ttg_status ttg_comm_nccl_unique_id(unsigned char id[128]) {
     return guard([&] { ttg::nccl_unique_id(id); });
