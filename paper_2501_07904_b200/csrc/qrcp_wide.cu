@@ -2509,6 +2509,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
     if (mode_ == 4) kpart_.alloc((size_t)ksplit_ * N);
     grow(std::max<int64_t>(1, std::min(p_, cap_steps)));
+    int init_grid = ncand_;
     if (mode_ == 4) {
         const dim3 g((unsigned)cdiv(N, 32), (unsigned)ksplit_);
         TTG_LAUNCH(k_col_part, g, kThreads, 0, stream(), W_, k_, N_, ld_, nullptr, 1, cdiv(k, ksplit_), kpart_.get());
@@ -2519,10 +2520,16 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         const size_t smem = tile ? sizeof(double) * k * (kThreads + 1) : 0;
         auto init = layout == Layout::Row ? k_init<0> : tile ? k_init<2> : k_init<1>;
         allow_smem(init, smem);
-        TTG_LAUNCH(init, ncand_, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
+        // every candidate slot (stream and guard) gets an init CTA: more CTAs per SM for
+        // the one full pass over W (the persistent TMA grid alone left the init
+        // latency-bound at ~1.8 TB/s); the sharded init keeps to the stream slots
+        init_grid = comm_ ? ncand_ : ncand_ + ngc_;
+        TTG_LAUNCH(init, init_grid, kThreads, smem, stream(), W_, k_, N_, ld_, nu_.get(), cref_.get(), pos_.get(),
                    perm_.get(), cand_.get(), mass_.get());
     }
-    TTG_LAUNCH(k_clear_slots, 1, 256, 0, stream(), cand_.get() + ncand_, mass_.get() + ncand_, ngc_);
+    if (init_grid < ncand_ + ngc_)
+        TTG_LAUNCH(k_clear_slots, 1, 256, 0, stream(), cand_.get() + init_grid, mass_.get() + init_grid,
+                   ncand_ + ngc_ - init_grid);
     if (comm_)
         TTG_LAUNCH(k_shard_init, (int)std::min<int64_t>(cdiv(Ng_, 256), 8 * sms), 256, 0, stream(), off_, N_, Ng_,
                    pos_.get(), perm_.get(), cand_.get(), ncand_);
