@@ -351,3 +351,18 @@ def test_concurrent_host_threads_match_sequential(dev, ref):
         assert len(s_cores) == len(c_cores)
         for x, y in zip(s_cores, c_cores):
             np.testing.assert_array_equal(x, y)
+
+
+def test_wide_near_full_rank_cut_in_place_warp_steps(dev, ref):
+    """64 x 32 x 64 x 64 Gaussian noise at eps 1e-3, TT-ULV: the second cut is a 2048 x 4096
+    unfolding kept at nearly full rank, so it runs in place with a warp per column (at most
+    2048 rows; 64, 32 and 16 rows per lane as the trailing rows shrink)."""
+    rng = np.random.default_rng(64)
+    dims = [64, 32, 64, 64]
+    a = rng.standard_normal(int(np.prod(dims)))
+    res = dev.decompose_device(a, dims, "ulv", "l2r", eps=1e-3)
+    rep = res.report()
+    assert any(c["m"] == 2048 and c["n"] == 4096 for c in rep.cuts)
+    rr = ref.decompose(a, dims, "ulv", "l2r", eps=1e-3)
+    assert rep.ranks_chosen == rr.ranks_chosen
+    assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
