@@ -80,6 +80,18 @@ def test_persistent_loop_cuts(dev, ref, method, mode):
         _check_parity(dev, ref, a, dims, method, eps=1e-4)
 
 
+@pytest.mark.parametrize("mode", ["rank", "tol"])
+def test_persistent_loop_odd_column_count(dev, ref, mode):
+    """16 x 243 x 243: the ULV first unfolding is 16 x 59,049 -- an odd column count through
+    the persistent loop's row-layout copy (the last column has no 16-byte partner)."""
+    dims, ranks = [16, 243, 243], [1, 8, 8, 1]
+    a = planted_plus_noise(ref, dims, ranks, 13, 1e-6)
+    if mode == "rank":
+        _check_parity(dev, ref, a, dims, "ulv", ranks=ranks)
+    else:
+        _check_parity(dev, ref, a, dims, "ulv", eps=1e-4)
+
+
 @pytest.mark.parametrize("method", ["urv", "ulv"])
 def test_persistent_loop_hilbert_guard(dev, ref, method):
     """Shifted Hilbert 12 x 12 x 12 x 12 x 12 at a prescribed accuracy well above the noise
