@@ -2289,11 +2289,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
                 if (lane <= t) hw[lane] = hl;
                 __syncwarp();
                 double sq = 0.0;
-                for (int64_t i = lane; i < k; i += 32) {
-                    double x = ld_w(g.W, g.ld, g.layout, i, j);
-                    if (i <= t) x -= rw[i];
-                    for (int64_t l = 0; l <= t && l <= i; ++l) x = fma(ls.Y[i + l * k], hw[l], x);
-                    sq = fma(x, x, sq);
+                // four rows per lane at a time: their loads in flight together and four
+                // independent FMA chains (Y(i, l) is stored as 0 for i < l, so the l loop
+                // needs no per-row bound)
+                for (int64_t i0 = lane; i0 < k; i0 += 128) {
+                    double x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + 32 * u;
+                        x[u] = i < k ? ld_w(g.W, g.ld, g.layout, i, j) - (i <= t ? rw[i] : 0.0) : 0.0;
+                    }
+                    for (int64_t l = 0; l <= t; ++l) {
+                        const double hl = hw[l];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int64_t i = i0 + 32 * u;
+                            if (i < k) x[u] = fma(ls.Y[i + l * k], hl, x[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) sq = fma(x[u], x[u], sq);
                 }
                 sq = warp_sum(sq);
                 if (lane == 0) {
