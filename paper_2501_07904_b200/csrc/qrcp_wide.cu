@@ -1671,10 +1671,32 @@ __global__ void __launch_bounds__(kThreads) k_guard(const double* __restrict__ W
                 __syncwarp();
             }
             double sq = 0.0;
-            for (int64_t i = lane; i < k; i += 32) {
-                double x = ld_w(W, ld, layout, i, j);
-                for (int64_t l = 0; l <= t; ++l) x = fma(-qq[i + l * k], rsm ? rbuf[warp][l] : R[l * N + j], x);
-                sq = fma(x, x, sq);
+            if (rsm) {
+                // four rows per lane at a time (loads in flight together, independent chains)
+                for (int64_t i0 = lane; i0 < k; i0 += 128) {
+                    double x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + 32 * u;
+                        x[u] = i < k ? ld_w(W, ld, layout, i, j) : 0.0;
+                    }
+                    for (int64_t l = 0; l <= t; ++l) {
+                        const double rl = rbuf[warp][l];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int64_t i = i0 + 32 * u;
+                            if (i < k) x[u] = fma(-qq[i + l * k], rl, x[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) sq = fma(x[u], x[u], sq);
+                }
+            } else {
+                for (int64_t i = lane; i < k; i += 32) {
+                    double x = ld_w(W, ld, layout, i, j);
+                    for (int64_t l = 0; l <= t; ++l) x = fma(-qq[i + l * k], R[l * N + j], x);
+                    sq = fma(x, x, sq);
+                }
             }
             sq = warp_sum(sq);
             if (lane == 0) {
