@@ -328,15 +328,58 @@ __global__ void k_eye(double* Q, int64_t N, int64_t q, int64_t ldq) {
 constexpr int64_t kColRows = 25600;  // column staged in shared memory (<= 200 KB)
 constexpr int64_t kQBlock = 32;     // reflectors per compact-WY block in form_q
 
-__global__ void __launch_bounds__(kT) k_col_house(TallView s, int64_t t) {
+// pick_pivot for NT threads
+template <int NT>
+__device__ int64_t pick_pivot_nt(const TallView& s, int64_t t, int64_t* out_pos) {
+    __shared__ double bnu[NT / 32];
+    __shared__ int64_t bpos[NT / 32];
+    __shared__ int64_t spiv;
+    double best = -1.0;
+    int64_t bp = INT64_MAX;
+#pragma unroll 4
+    for (int64_t q = t + threadIdx.x; q < s.n; q += NT) {
+        const double v = s.nu[s.colmap[q]];
+        if (v > best || (v == best && q < bp)) { best = v; bp = q; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int64_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ov > best || (ov == best && op < bp)) { best = ov; bp = op; }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { bnu[warp] = best; bpos[warp] = bp; }
+    __syncthreads();
+    if (warp == 0) {  // one warp folds the NT/32 warp results
+        best = lane < NT / 32 ? bnu[lane] : -1.0;
+        bp = lane < NT / 32 ? bpos[lane] : INT64_MAX;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int64_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (ov > best || (ov == best && op < bp)) { best = ov; bp = op; }
+        }
+        if (lane == 0) {
+            bpos[0] = bp;
+            spiv = s.colmap[bp];
+        }
+    }
+    __syncthreads();
+    *out_pos = bpos[0];
+    return spiv;
+}
+
+// Step t's pivot and reflector (make_householder, factor.cpp:24-38): one CTA of 1024
+// threads, so the pivot scan, the column mass and the normalisation are one batch of
+// loads per thread for columns of up to 4096 rows.
+constexpr int kHouseT = 1024;
+__global__ void __launch_bounds__(kHouseT) k_col_house(TallView s, int64_t t) {
     int64_t pp;
-    const int64_t piv = pick_pivot(s, t, &pp);
-    __shared__ double sd[kT / 32];
+    const int64_t piv = pick_pivot_nt<kHouseT>(s, t, &pp);
+    __shared__ double sd[kHouseT / 32];
     __shared__ double sh[2];
     double* x = s.B + piv * s.ld;
     double sg = 0.0;
 #pragma unroll 4
-    for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) sg = fma(x[i], x[i], sg);
+    for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kHouseT) sg = fma(x[i], x[i], sg);
     sg = block_sum(sg, sd);
     if (threadIdx.x == 0) {
         const double alpha = x[t];
@@ -365,7 +408,7 @@ __global__ void __launch_bounds__(kT) k_col_house(TallView s, int64_t t) {
     const double beta = sh[0], v0 = sh[1];
     if (beta != 0.0)
 #pragma unroll 4
-        for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kT) x[i] = __ddiv_rn(x[i], v0);
+        for (int64_t i = t + 1 + threadIdx.x; i < s.N; i += kHouseT) x[i] = __ddiv_rn(x[i], v0);
 }
 
 __global__ void __launch_bounds__(kT) k_col_apply(TallView s, int64_t t) {
@@ -628,7 +671,7 @@ void TallQrcp::run(int64_t steps) {
         for (int64_t t = steps_; t < steps; ++t) {
             {
                 PhaseTimer pt("col house");
-                TTG_LAUNCH(k_col_house, 1, kT, 0, stream(), s, t);
+                TTG_LAUNCH(k_col_house, 1, kHouseT, 0, stream(), s, t);
             }
             if (t + 1 >= n_) continue;
             PhaseTimer pt(N_ <= kWarpRows ? "col apply (warp)" : "col apply (cta)");

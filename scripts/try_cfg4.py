@@ -7,7 +7,7 @@ dev = torch.device("cuda", 0)
 m = build(4, dev); mask = bernoulli_mask(m.numel(), dev)
 y = m * mask
 torch.cuda.synchronize()
-for it in range(2):
+for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
     t0 = time.perf_counter()
     r = api.decompose_device(y.data_ptr(), c["dims"], "urv", "r2l", a_is_device_ptr=True, eps=c["eps"])
     rep = r.report()
