@@ -580,7 +580,7 @@ private:
 // so it serves wide and tall W alike; TTG_TALL_INPLACE=1 selects the in-place engine for
 // tall W instead (kept as a cross-check).
 std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap,
-                                  bool fixed = false) {
+                                  bool fixed = false, bool prev_near_full = false) {
     static const bool inplace = [] {
         const char* e = std::getenv("TTG_TALL_INPLACE");
         return e && *e == '1';
@@ -603,6 +603,11 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         return e ? (int64_t)std::atoll(e) : (int64_t)1024;
     }();
     if (!fixed && k >= inplace_mink && k <= 25600 && N >= 2048) return std::make_unique<TallPass1>(W, k, N, ld, l);
+    // shorter unfoldings go in place too when the previous cut of the sweep kept >= 90% of
+    // its p (a near-full-rank tensor: config 4's 256 x 65,536 cut 87 -> 54 ms); an early
+    // exit (config 2's mid cuts) keeps the read-only engine
+    if (!fixed && prev_near_full && k >= 256 && k <= 25600 && N >= 2048)
+        return std::make_unique<TallPass1>(W, k, N, ld, l);
     // tall W, fixed rank: the pivoted Cholesky of W^T W (cut_with() checks its conditioning)
     if (fixed && !no_gram && k >= 8 * N && N <= 4096 && cap <= 160 && cap >= 1)
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
@@ -1058,14 +1063,16 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
               const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
     const int64_t d = (int64_t)dims.size();
     DevBuf<double> carry;  // current working matrix when not the input itself
+    bool prev_near_full = false;
     for (int64_t k = k0; k <= d - 1; ++k) {
         const int64_t p = std::min(m, n);
         const CutRequest rq = make_request(res, mode, cfg, k, p);
         const auto tc0 = Clock::now();
         const int64_t cap = mode.fixed ? rq.rank : 32;
-        auto e1 = make_pass1(c, m, n, m, Layout::Col, cap, mode.fixed);
+        auto e1 = make_pass1(c, m, n, m, Layout::Col, cap, mode.fixed, prev_near_full);
         CutOut co = cut_with(e1, rq, c, m, n, m, Layout::Col, cap);
         print_cut("ulv", k, m, n, co, tc0);
+        prev_near_full = co.rank * 10 >= p * 9;
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 1)] = co.step_error;
         res.ranks_chosen[(size_t)k] = r;
@@ -1094,15 +1101,17 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
 void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, int64_t r_next,
               const std::vector<int64_t>& dims, const Resolved& mode, const SweepConfig& cfg) {
     DevBuf<double> carry;
+    bool prev_near_full = false;
     for (int64_t k = k0; k >= 2; --k) {
         const int64_t p = std::min(M, n);
         const CutRequest rq = make_request(res, mode, cfg, k - 1, p);
         // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
         const auto tc0 = Clock::now();
         const int64_t cap = mode.fixed ? rq.rank : 32;
-        auto e1 = make_pass1(c, n, M, M, Layout::Row, cap, mode.fixed);
+        auto e1 = make_pass1(c, n, M, M, Layout::Row, cap, mode.fixed, prev_near_full);
         CutOut co = cut_with(e1, rq, c, n, M, M, Layout::Row, cap);
         print_cut("urv", k - 1, M, n, co, tc0);
+        prev_near_full = co.rank * 10 >= p * 9;
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 2)] = co.step_error;
         res.ranks_chosen[(size_t)(k - 1)] = r;
