@@ -57,6 +57,13 @@ def lib():
         h.ref_frobenius_norm.argtypes = [dp, C.c_int64]
         h.ref_frobenius_norm.restype = C.c_double
         h.ref_set_parallel.argtypes = [C.c_int]
+        h.ref_sweep_trace.argtypes = [dp, ip, C.c_int, C.c_int, C.c_int, ip, C.c_double, C.POINTER(C.c_void_p)]
+        h.ref_trace_result.argtypes = [C.c_void_p]
+        h.ref_trace_result.restype = C.c_void_p
+        h.ref_trace_free.argtypes = [C.c_void_p]
+        h.ref_trace_cut.argtypes = [C.c_void_p, C.c_int, ip, ip, dp]
+        h.ref_trace_cut.restype = C.c_int64
+        h.ref_trace_cut_copy.argtypes = [C.c_void_p, C.c_int, dp, dp]
         h.ref_read_tensor.argtypes = [C.c_char_p, ip, C.POINTER(C.c_int), ip, dp]
         h.ref_write_tensor.argtypes = [C.c_char_p, dp, ip, C.c_int]
         h.ref_write_tt.argtypes = [C.c_char_p, C.c_int, ip, ip, dp]
@@ -134,6 +141,59 @@ def decompose(a, dims, method="urv", sweep="r2l", ranks=None, eps=0.0, weights=(
     warns = [lib().ref_result_warning(h, i).decode() for i in range(nw)]
     return RefResult(cores, se[: max(order - 1, 0)].tolist(), rc.tolist(), b.value, bk.value, ni.value, wt.value,
                      warns, hh)
+
+
+class _TraceHandle:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            lib().ref_trace_free(self.h)
+
+
+def _result_from(h, owner) -> RefResult:
+    order = lib().ref_result_order(h)
+    cores = []
+    for k in range(order):
+        cd = np.zeros(3, np.int64)
+        lib().ref_result_core_dims(h, k, _i(cd))
+        buf = np.empty(int(np.prod(cd)), np.float64)
+        lib().ref_result_core_copy(h, k, _d(buf))
+        cores.append(buf.reshape(tuple(cd), order="F"))
+    se = np.zeros(max(order - 1, 1), np.float64)
+    rc = np.zeros(order + 1, np.int64)
+    b, ni, wt = C.c_double(), C.c_double(), C.c_double()
+    bk = C.c_int()
+    nw = lib().ref_result_report(h, _d(se), _i(rc), C.byref(b), C.byref(bk), C.byref(ni), C.byref(wt))
+    warns = [lib().ref_result_warning(h, i).decode() for i in range(nw)]
+    return RefResult(cores, se[: max(order - 1, 0)].tolist(), rc.tolist(), b.value, bk.value, ni.value, wt.value,
+                     warns, owner)
+
+
+def sweep_trace(a, dims, method="urv", ranks=None, eps=0.0):
+    """ULV-L2R / URV-R2L through the reference's public calls (ref_shim.cpp ref_sweep_trace),
+    returning (RefResult, cuts) with per cut (unfolding order) m, n, |diag T| (all p), the
+    kept-mass vector and the directly computed discarded norm (-1 when skipped)."""
+    a = np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1))
+    dims = np.ascontiguousarray(np.asarray(dims, np.int64))
+    d = dims.size
+    r = np.ascontiguousarray(np.asarray(ranks if ranks is not None else [1] * (d + 1), np.int64))
+    h = C.c_void_p()
+    _check(lib().ref_sweep_trace(_d(a), _i(dims), d, {"ulv": 1, "urv": 2}[method], int(ranks is not None), _i(r),
+                                 float(eps), C.byref(h)))
+    owner = _TraceHandle(h)
+    res = _result_from(lib().ref_trace_result(h), owner)
+    cuts = []
+    for k in range(d - 1):
+        m, n, direct = C.c_int64(), C.c_int64(), C.c_double()
+        p = lib().ref_trace_cut(h, k, C.byref(m), C.byref(n), C.byref(direct))
+        dg = np.empty(p, np.float64)
+        kp = np.empty(p + 1, np.float64)
+        lib().ref_trace_cut_copy(h, k, _d(dg), _d(kp))
+        cuts.append(dict(m=m.value, n=n.value, diag=dg, kept=kp, direct=direct.value,
+                         rank=res.ranks_chosen[k + 1], step_error=res.step_errors[k]))
+    return res, cuts
 
 
 def rse(res: RefResult, a, dims, cap=10**10) -> float:

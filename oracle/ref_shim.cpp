@@ -13,6 +13,8 @@
 //   5 ResourceError 6 InvariantError 7 other ttutv::Error / std::exception
 // and the message is available from ref_last_error().
 
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -325,6 +327,167 @@ int ref_write_tt(const char* path, int d, const int64_t* ranks, const int64_t* d
         }
         ttutv::write_tt(path, ttutv::TTTensor(std::move(cores)));
     });
+}
+
+}  // extern "C"
+
+// ---- sweep trace (golden fixtures) ------------------------------------------
+// A restatement of sweep_l2r (ULV) / sweep_r2l (URV, l11_only) from
+// src/tt_decomp.cpp:156-339 built only from the reference's public calls (ulv/urv,
+// truncate_fixed_rank/tol, kernels::matmul, kernels::transpose), so every per-cut
+// quantity is the reference's own bits; it additionally records what decompose() does
+// not return: |diag T| (all p), the kept-mass vector (factor.cpp:479-499 order) and the
+// directly computed discarded mass ||c - U1 T11 V1^T||_F per cut.
+struct RefTrace {
+    ttutv::DecompResult res;
+    std::vector<std::vector<double>> diag, kept;
+    std::vector<int64_t> m, n;
+    std::vector<double> direct;
+};
+
+namespace {
+std::vector<double> kept_of(const ttutv::Matrix& t, bool lower) {
+    const int64_t p = t.rows();
+    std::vector<double> kept((size_t)p + 1, 0.0);
+    for (int64_t r = 1; r <= p; ++r) {
+        double s = 0.0;
+        for (int64_t j = 0; j < r; ++j) {
+            const double v = lower ? t(r - 1, j) : t(j, r - 1);
+            s += v * v;
+        }
+        kept[(size_t)r] = kept[(size_t)r - 1] + s;
+    }
+    return kept;
+}
+}  // namespace
+
+extern "C" {
+
+// method 1 ulv (l2r) or 2 urv (r2l); fixed_rank -> ranks[0..d], else eps (equal rss weights).
+int ref_sweep_trace(const double* a, const int64_t* dims, int d, int method, int fixed_rank,
+                    const int64_t* ranks, double eps, void** handle) {
+    *handle = nullptr;
+    return guarded([&] {
+        using namespace ttutv;
+        auto* tr = new RefTrace();
+        const auto start = std::chrono::steady_clock::now();
+        DenseTensor at = tensor_of(a, dims, d);
+        const double norm_a = frobenius_norm(at);
+        const Shape shp = at.shape();
+        const int64_t count = shp.element_count();
+        std::vector<double> budgets;
+        for (int k = 0; k < d - 1; ++k) budgets.push_back(eps * norm_a / std::sqrt((double)(d - 1)));
+        DecompReport& rep = tr->res.report;
+        rep.input_norm = norm_a;
+        rep.step_errors.assign((size_t)d - 1, 0.0);
+        rep.ranks_chosen.assign((size_t)d + 1, 1);
+        if (fixed_rank) rep.ranks_requested.assign(ranks, ranks + d + 1);
+        tr->diag.resize((size_t)d - 1);
+        tr->kept.resize((size_t)d - 1);
+        tr->m.resize((size_t)d - 1);
+        tr->n.resize((size_t)d - 1);
+        tr->direct.resize((size_t)d - 1);
+        std::vector<TTCore> cores;
+        auto record = [&](int cut, const Matrix& c, const Matrix& t, bool lower, int64_t r,
+                          const Matrix& u1, const Matrix& t11, const Matrix& v1) {
+            std::vector<double> dg;
+            for (int64_t i = 0; i < t.rows(); ++i) dg.push_back(std::abs(t(i, i)));
+            tr->diag[(size_t)cut] = dg;
+            tr->kept[(size_t)cut] = kept_of(t, lower);
+            tr->m[(size_t)cut] = c.rows();
+            tr->n[(size_t)cut] = c.cols();
+            if (c.size() > 300000000) {  // memory: skip the direct residual on config 5's first cut
+                tr->direct[(size_t)cut] = -1.0;
+                return;
+            }
+            const Matrix low = kernels::matmul(kernels::matmul(u1, t11), v1, false, true);
+            double s = 0.0;
+            for (int64_t i = 0; i < c.size(); ++i) {
+                const double e = c.data()[i] - low.data()[i];
+                s += e * e;
+            }
+            tr->direct[(size_t)cut] = std::sqrt(s);
+            (void)r;
+        };
+        if (method == 1) {
+            Matrix c(shp.dim(1), count / shp.dim(1), at.take_storage());
+            int64_t r_prev = 1;
+            for (int64_t k = 1; k <= d - 1; ++k) {
+                const int64_t p = std::min(c.rows(), c.cols());
+                UlvFactors f = ulv(c, 1);
+                TruncatedFactorization tf = fixed_rank
+                    ? truncate_fixed_rank(f, std::min(ranks[k], p))
+                    : truncate_fixed_tol(f, budgets[(size_t)k - 1]);
+                record((int)k - 1, c, f.l, true, tf.rank, tf.u1, tf.t11, tf.v1);
+                rep.step_errors[(size_t)k - 1] = tf.residual_norm;
+                rep.ranks_chosen[(size_t)k] = tf.rank;
+                Matrix carry = kernels::matmul(tf.t11, tf.v1, false, true);
+                cores.push_back(TTCore{DenseTensor(Shape({r_prev, shp.dim(k), tf.rank}),
+                                                   tf.u1.take_storage())});
+                r_prev = tf.rank;
+                if (k < d - 1) {
+                    const int64_t nr = r_prev * shp.dim(k + 1);
+                    const int64_t nc = carry.cols() / shp.dim(k + 1);
+                    c = Matrix(nr, nc, carry.take_storage());
+                } else {
+                    cores.push_back(TTCore{DenseTensor(Shape({r_prev, shp.dim(d), 1}),
+                                                       carry.take_storage())});
+                }
+            }
+        } else {
+            std::vector<TTCore> rev;
+            Matrix c(count / shp.dim(d), shp.dim(d), at.take_storage());
+            int64_t r_next = 1;
+            for (int64_t k = d; k >= 2; --k) {
+                const int64_t p = std::min(c.rows(), c.cols());
+                UrvFactors f = urv(c, 1);
+                TruncatedFactorization tf = fixed_rank
+                    ? truncate_fixed_rank(f, std::min(ranks[k - 1], p))
+                    : truncate_fixed_tol(f, budgets[(size_t)k - 2]);
+                record((int)k - 2, c, f.r, false, tf.rank, tf.u1, tf.t11, tf.v1);
+                rep.step_errors[(size_t)k - 2] = tf.residual_norm;
+                rep.ranks_chosen[(size_t)k - 1] = tf.rank;
+                Matrix carry = kernels::matmul(tf.u1, tf.t11);
+                Matrix v1t = kernels::transpose(tf.v1);
+                rev.push_back(TTCore{DenseTensor(Shape({tf.rank, shp.dim(k), r_next}),
+                                                 v1t.take_storage())});
+                r_next = tf.rank;
+                if (k > 2) {
+                    const int64_t nr = carry.rows() / shp.dim(k - 1);
+                    c = Matrix(nr, shp.dim(k - 1) * tf.rank, carry.take_storage());
+                } else {
+                    rev.push_back(TTCore{DenseTensor(Shape({1, shp.dim(1), tf.rank}),
+                                                     carry.take_storage())});
+                }
+            }
+            cores.assign(std::make_move_iterator(rev.rbegin()), std::make_move_iterator(rev.rend()));
+        }
+        double b2 = 0.0;
+        for (double e : rep.step_errors) b2 += e * e;
+        rep.bound = std::sqrt(b2);
+        rep.bound_kind = BoundKind::root_sum_square;
+        rep.wall_time_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+        tr->res.tt = TTTensor(std::move(cores));
+        *handle = tr;
+    });
+}
+
+void* ref_trace_result(void* h) { return &static_cast<RefTrace*>(h)->res; }
+void ref_trace_free(void* h) { delete static_cast<RefTrace*>(h); }
+// per cut (0-based unfolding index): p = diag length; kept has p+1 entries
+int64_t ref_trace_cut(void* h, int cut, int64_t* m, int64_t* n, double* direct) {
+    auto* t = static_cast<RefTrace*>(h);
+    *m = t->m[(size_t)cut];
+    *n = t->n[(size_t)cut];
+    *direct = t->direct[(size_t)cut];
+    return (int64_t)t->diag[(size_t)cut].size();
+}
+void ref_trace_cut_copy(void* h, int cut, double* diag, double* kept) {
+    auto* t = static_cast<RefTrace*>(h);
+    const auto& dg = t->diag[(size_t)cut];
+    const auto& kp = t->kept[(size_t)cut];
+    std::memcpy(diag, dg.data(), sizeof(double) * dg.size());
+    std::memcpy(kept, kp.data(), sizeof(double) * kp.size());
 }
 
 }  // extern "C"

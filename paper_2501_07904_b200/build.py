@@ -78,6 +78,24 @@ def build(verbose: bool = False) -> Path:
     return out
 
 
+def build_inputs(verbose: bool = False) -> Path:
+    """hostgen/inputs.cpp -> lib/libttutv_inputs.so: the seeded input generators of the
+    BASELINE configs (harness code for bench.py and the tests, not the product path).
+    Default x86-64 target and no FP contraction, like the reference build, so the buffers
+    are bitwise those of the reference's own generators."""
+    src = PKG / "hostgen" / "inputs.cpp"
+    out = LIBDIR / "libttutv_inputs.so"
+    LIBDIR.mkdir(parents=True, exist_ok=True)
+    if out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    cmd = ["/usr/bin/g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+           "-fno-fast-math", str(src), "-o", str(out)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, env=_env())
+    return out
+
+
 def build_dropin_check(verbose: bool = False) -> Path:
     """tests/cpp/dropin_check.cpp: a caller written against the reference headers,
     compiled through the compat forwarding headers and linked to libttutv_b200.so."""
@@ -97,4 +115,5 @@ def build_dropin_check(verbose: bool = False) -> Path:
 
 if __name__ == "__main__":
     print(build(verbose=True))
+    print(build_inputs(verbose=True))
     print(build_dropin_check(verbose=True))

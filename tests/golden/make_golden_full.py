@@ -1,0 +1,123 @@
+"""Regenerate the full-size BASELINE fixtures tests/golden/full_cfg{2,3,5}.npz from the
+UNMODIFIED reference library (oracle/_ref), following SURVEY.md Appendix A and C.
+
+Run in the build container (where /root/reference exists and `make -C oracle ref` has been
+run):  python tests/golden/make_golden_full.py cfg3 [cfg2 cfg5]
+
+Inputs come from the reference's own generators (generators.cpp through oracle/_ref:
+gen_planted_tt -> reconstruct, gen_gaussian), so the GPU tests rebuild bit-identical
+buffers on the box with the same calls (tests/fixtures.py). Every per-cut quantity is the
+reference's own: the sweep runs through ref_sweep_trace (oracle/ref_shim.cpp), which calls
+ulv/urv/truncate_*/kernels::matmul in sweep_l2r/sweep_r2l's order and is bitwise equal to
+decompose() (checked by tests/test_oracle.py on small fixtures).
+
+  cfg3  24^6 planted ranks 20 + 1e-4 noise (seeds 3/4), fixed rank 20, ULV-L2R and URV-R2L
+  cfg5  1024^3 planted ranks 128 + 1e-6 noise (seeds 5/6), fixed rank 128, URV-R2L
+  cfg2  32^5 shifted Hilbert, eps 1e-8 under the neutral rescales of Appendix A (the
+        oracle's own variability set) plus the well-posed eps 1e-6 extra
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from oracle import ref  # noqa: E402
+from tests.fixtures import planted_plus_noise, shifted_hilbert  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+# Appendix A's rescales {1, 3, 0.7} plus further neutral rescales: the ranks of the ulp-decided
+# 32-row cut are a function of rounding, so the set is sampled more densely than the survey did.
+CFG2_SCALES = [1.0, 3.0, 0.7, 0.9, 1.1, 1.3, 1.7, 2.3, 0.6, 5.0, 0.55, 1.9]
+
+
+def trace_arrays(prefix, res, cuts, out, keep_cores=True, sample_core=None):
+    out[f"{prefix}_ranks"] = np.asarray(res.ranks_chosen, np.int64)
+    out[f"{prefix}_step_errors"] = np.asarray(res.step_errors)
+    out[f"{prefix}_bound"] = np.float64(res.bound)
+    out[f"{prefix}_input_norm"] = np.float64(res.input_norm)
+    out[f"{prefix}_wall_ms"] = np.float64(res.wall_time_ms)
+    for k, c in enumerate(cuts):
+        out[f"{prefix}_cut{k}_mn"] = np.asarray([c["m"], c["n"]], np.int64)
+        out[f"{prefix}_cut{k}_diag"] = c["diag"]
+        out[f"{prefix}_cut{k}_kept"] = c["kept"]
+        out[f"{prefix}_cut{k}_direct"] = np.float64(c["direct"])
+    for k, core in enumerate(res.cores):
+        if keep_cores and core.size <= 2_000_000:
+            out[f"{prefix}_core{k}"] = core
+        else:  # big middle core: its norm and a slab of mode indices
+            out[f"{prefix}_core{k}_norm"] = np.float64(np.linalg.norm(core))
+            out[f"{prefix}_core{k}_slab"] = np.ascontiguousarray(core[:, : (sample_core or 8), :])
+
+
+def cfg3():
+    dims, ranks = [24] * 6, [1, 20, 20, 20, 20, 20, 1]
+    t0 = time.time()
+    a = planted_plus_noise(ref, dims, ranks, 3, 1e-4)
+    out = dict(dims=np.asarray(dims), ranks_req=np.asarray(ranks), seed=np.int64(3), rho=np.float64(1e-4),
+               a_norm=np.float64(ref.frobenius_norm(a)), a_sum=np.float64(a.sum()))
+    print(f"cfg3 input {time.time() - t0:.1f}s", flush=True)
+    for method in ("ulv", "urv"):
+        t0 = time.time()
+        res, cuts = ref.sweep_trace(a, dims, method, ranks=ranks)
+        t1 = time.time()
+        out[f"{method}_rse"] = np.float64(ref.rse(res, a, dims, cap=10**9))
+        trace_arrays(method, res, cuts, out)
+        print(f"cfg3 {method}: ranks {res.ranks_chosen} rse {out[method + '_rse']:.6e} sweep {t1 - t0:.1f}s",
+              flush=True)
+    np.savez_compressed(OUT / "full_cfg3.npz", **out)
+
+
+def cfg5():
+    dims, ranks = [1024] * 3, [1, 128, 128, 1]
+    t0 = time.time()
+    a = planted_plus_noise(ref, dims, ranks, 5, 1e-6)
+    out = dict(dims=np.asarray(dims), ranks_req=np.asarray(ranks), seed=np.int64(5), rho=np.float64(1e-6),
+               a_norm=np.float64(ref.frobenius_norm(a)), a_sum=np.float64(a.sum()))
+    print(f"cfg5 input {time.time() - t0:.1f}s", flush=True)
+    t0 = time.time()
+    res, cuts = ref.sweep_trace(a, dims, "urv", ranks=ranks)
+    t1 = time.time()
+    trace_arrays("urv", res, cuts, out, sample_core=8)
+    out["urv_sweep_s"] = np.float64(t1 - t0)
+    print(f"cfg5 urv: ranks {res.ranks_chosen} step errors {res.step_errors} sweep {t1 - t0:.1f}s", flush=True)
+    np.savez_compressed(OUT / "full_cfg5.npz", **out)  # saved before the (long) RSE
+    t0 = time.time()
+    out["urv_rse"] = np.float64(ref.rse(res, a, dims, cap=2 * 10**9))
+    print(f"cfg5 urv rse {out['urv_rse']:.6e} ({time.time() - t0:.1f}s)", flush=True)
+    np.savez_compressed(OUT / "full_cfg5.npz", **out)
+
+
+def cfg2():
+    dims = [32] * 5
+    base = shifted_hilbert(dims)
+    out = dict(dims=np.asarray(dims), scales=np.asarray(CFG2_SCALES))
+    summary = []
+    for eps, tag in ((1e-8, "e8"), (1e-6, "e6")):
+        scales = CFG2_SCALES if tag == "e8" else [1.0]
+        for i, s in enumerate(scales):
+            a = base * s if s != 1.0 else base
+            for method in ("ulv", "urv"):
+                t0 = time.time()
+                res, cuts = ref.sweep_trace(a, dims, method, eps=eps)
+                rse = ref.rse(res, a, dims, cap=10**9)
+                pre = f"{tag}_s{i}_{method}"
+                trace_arrays(pre, res, cuts, out)
+                out[f"{pre}_rse"] = np.float64(rse)
+                row = dict(eps=eps, scale=s, method=method, ranks=res.ranks_chosen, rse=rse,
+                           sec=round(time.time() - t0, 1))
+                summary.append(row)
+                print(json.dumps(row), flush=True)
+    out["summary_json"] = np.asarray(json.dumps(summary))
+    np.savez_compressed(OUT / "full_cfg2.npz", **out)
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:] or ["cfg3"]:
+        {"cfg2": cfg2, "cfg3": cfg3, "cfg5": cfg5}[name]()
