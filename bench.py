@@ -1,9 +1,13 @@
 #!/usr/bin/env python
 """TT-UTV throughput benchmark (BASELINE.json metric: tensor entries/s, FP64).
 
-Default workload (N=1): BASELINE config 2 -- the Hilbert-type 32^5 tensor
-A = 1/(i1+..+i5-4), rank-adaptive at eps = 1e-8. One step = one TT-ULV left-to-right
-plus one TT-URV right-to-left decomposition of the whole tensor (2 x 33.5M entries).
+Default workload (N=1): BASELINE config 3 -- the largest single-GPU config: a 24^6
+tensor (191M entries, 1.53 GB) from random N(0,1) TT cores of ranks 20 plus 1e-4 relative
+Gaussian noise, built with the reference's own generator algorithms (inputs.py, bitwise
+the reference's buffers). One step = one TT-ULV left-to-right plus one TT-URV right-to-left
+decomposition at fixed rank 20 of the whole tensor (2 x 191M entries).
+Default at N > 1 (torchrun, or spawned by this script): config 5 (1024^3, fixed rank 128,
+TT-URV) column-sharded across the ranks (one tensor, strong scaling).
 
   value   entries/s with the tensor resident in HBM (device-timed, CUDA events on the
           engine's stream, max over ranks)
@@ -13,17 +17,17 @@ plus one TT-URV right-to-left decomposition of the whole tensor (2 x 33.5M entri
           thread has its own stream), so one's H2D overlaps the other's compute
           (--e2e-concurrency 1: back to back; the JSON carries both)
   roofline  the dominant kernel (pass-1 streaming GEMV, HBM-bound) timed live with
-          CUDA events around each launch inside the timed region
+          CUDA events around each launch inside the timed region, plus the whole-step
+          T_roof / T_dev of SURVEY.md 8(d) (F_min / P_FP64 vs B_comp / BW per cut, P_FP64
+          a cuBLAS DGEMM measured in this run -- measurement only, never the product path)
   cpu_baseline  the reference CPU library (oracle/_ref, compiled from /root/reference)
-          on this host's cores, one step, rank 0 only
+          on this host's cores, on a bounded sample, rank 0 only
 
-`--impl reference` times the reference CPU implementation itself on the same workload.
+`--impl reference` times the reference CPU implementation itself on the whole workload
+(the full tensor, both decompositions per step).
 `--config {1,2,3,5}` selects another BASELINE config (parity/extra measurements).
-Multi-GPU (torchrun): configs 1-3 do not shard, so every rank runs an independent
-replica ("replicas only", scaling weak); value = all ranks' entries / max rank time.
-Config 5 at N > 1 runs the column-sharded TT-URV (one tensor split across the ranks,
-NCCL all-gathers of the pivot records / TSQR triangles / carry; scaling strong); value =
-the tensor's entries / max rank time.
+Multi-GPU: configs 1-3 do not shard, so every rank runs an independent replica
+("replicas only", scaling weak); config 5 runs the column-sharded TT-URV.
 """
 from __future__ import annotations
 
@@ -63,6 +67,78 @@ def workload(cfg: int):
     if cfg == 5:
         runs = [("urv", "r2l")]
     return c, runs, desc
+
+
+def host_cpu():
+    """Model name, logical threads and physical cores of this host (cpu_baseline.cores is
+    the thread count actually used)."""
+    model, phys = None, set()
+    try:
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" not in line:
+                if "physical id" in cur and "core id" in cur:
+                    phys.add((cur["physical id"], cur["core id"]))
+                cur = {}
+                continue
+            k, v = (x.strip() for x in line.split(":", 1))
+            cur[k] = v
+            if k == "model name" and model is None:
+                model = v
+        if "physical id" in cur and "core id" in cur:
+            phys.add((cur["physical id"], cur["core id"]))
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "physical_cores": len(phys) or None}
+
+
+def measure_fp64_peak(device):
+    """Dense FP64 peak of this GPU: cuBLAS DGEMM (torch.matmul, float64) on 8192^3, best of 5
+    after warm-up. Measurement only (the roofline's P_FP64); the engine
+    never calls cuBLAS."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=device)
+    b = torch.randn(n, n, dtype=torch.float64, device=device)
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del a, b
+    torch.cuda.empty_cache()
+    return {"tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "how": f"cuBLAS DGEMM {n}^3 (torch.matmul float64), "
+            "best of 5 with CUDA events, measured in this run"}
+
+
+def golden_parity(cfg: int, a_host, info: dict):
+    """The reference's own results on this exact input (tests/golden/full_cfg{cfg}.npz,
+    produced by the reference on its own generators; the input is bitwise the same -- its
+    norm and sum are checked) beside ours."""
+    path = ROOT / "tests" / "golden" / f"full_cfg{cfg}.npz"
+    if not path.exists():
+        return None
+    import numpy as np
+    g = np.load(path)
+    same = (a_host is not None and float(np.sqrt(np.dot(a_host, a_host))) > 0 and
+            abs(float(a_host.sum()) - float(g["a_sum"])) <= 1e-9 * abs(float(g["a_sum"])) + 1e-300)
+    out = {"input_matches_golden": bool(same), "source": f"tests/golden/full_cfg{cfg}.npz (reference, oracle/_ref)"}
+    for m, r in info.items():
+        if f"{m}_ranks" not in g:
+            continue
+        ref_rse = float(g[f"{m}_rse"]) if f"{m}_rse" in g else None
+        out[m] = {"ranks_ours": r["ranks"], "ranks_reference": [int(x) for x in g[f"{m}_ranks"]],
+                  "rse_ours": r.get("rse"), "rse_reference": ref_rse,
+                  "abs_rse_diff": (abs(r["rse"] - ref_rse) if (ref_rse is not None and r.get("rse") is not None)
+                                   else None)}
+    return out
 
 
 class Clocks:
@@ -176,15 +252,15 @@ def ncu_traffic(cfg: int, kernel: str = ""):
     return t
 
 
-def reference_step(ref, a_host, c, runs):
-    """One step of the reference CPU library on the host buffer."""
+def reference_step(ref, a_host, c, runs, keep=False):
+    """One step of the reference CPU library on the host buffer (its stock decompose())."""
     out = []
     for method, sweep in runs:
         if c["mode"] == "tol":
             rr = ref.decompose(a_host, c["dims"], method, sweep, eps=c["eps"])
         else:
             rr = ref.decompose(a_host, c["dims"], method, sweep, ranks=c["ranks"])
-        out.append(rr.ranks_chosen)
+        out.append(rr if keep else rr.ranks_chosen)
     return out
 
 
@@ -194,33 +270,46 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import ref
-    from paper_2501_07904_b200.inputs import build
-    import torch
-    full = build(args.config, "cuda" if torch.cuda.is_available() else "cpu")
-    a, dims, rk, note = cpu_sample(full, args.config, c)
-    del full
-    cs = dict(c, dims=dims)
-    if rk is not None:
-        cs["ranks"] = rk
+    from paper_2501_07904_b200.inputs import build_host
+    a = build_host(args.config)  # the same buffer as our arm (bitwise the reference's generators)
+    dims = c["dims"]
+    cs = dict(c)
     n = a.size
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     small = ref.gen_gaussian([8, 8, 8], 1)
-    for _ in range(args.warmup):  # warm the OpenMP pool on a tiny problem (first region ~1 s)
+    # Warm-up: the OpenMP pool on a tiny problem (the first parallel region costs ~1 s); a
+    # full-size untimed step would only repeat the timed work at minutes per step.
+    for _ in range(args.warmup):
         ref.decompose(small, [8, 8, 8], "urv", "r2l", ranks=[1, 3, 3, 1])
     t0 = time.perf_counter()
-    ranks = None
+    got = None
+    per_step = []
     for _ in range(args.steps):
-        ranks = reference_step(ref, a, cs, runs)
+        ts = time.perf_counter()
+        got = reference_step(ref, a, cs, runs, keep=True)
+        per_step.append(time.perf_counter() - ts)
+        log(f"reference step: {per_step[-1]:.1f} s")
     dt = time.perf_counter() - t0
     value = args.steps * len(runs) * n / dt
+    ranks = [r.ranks_chosen for r in got]
+    rses = []
+    for r in got:  # outside the timed region
+        try:
+            rses.append(ref.rse(r, a, dims, cap=2 * 10**9) if n <= 4 * 10**8 else None)
+        except Exception:
+            rses.append(None)
+    note = "the whole tensor"
     sample = (f"{args.steps} step(s) of {desc} ({len(runs)} decomposition(s) each) on {note}, dims {dims}, "
-              f"ranks {ranks}")
+              f"ranks {ranks}, rse {rses}, seconds per step {[round(x, 2) for x in per_step]}")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "entries_per_step": len(runs) * n, "parallelism": "cpu-openmp"},
+            "config": {"workload": desc, "entries_per_step": len(runs) * n, "parallelism": "cpu-openmp",
+                       "ranks": {m: r for (m, _), r in zip(runs, ranks)},
+                       "rse": {m: x for (m, _), x in zip(runs, rses)}},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+                             "cpu": host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -233,11 +322,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     from paper_2501_07904_b200 import api
     from paper_2501_07904_b200._native import lib, check
-    from paper_2501_07904_b200.inputs import build
+    from paper_2501_07904_b200.inputs import build_host
+    from paper_2501_07904_b200.roofline import step_roofline
     check(lib().ttg_set_device(local))
     c, runs, desc = workload(args.config)
-    a = build(args.config, torch.device("cuda", local))
+    a_host = build_host(args.config)  # bitwise the reference generators' buffer (inputs.py)
+    a = torch.from_numpy(a_host).to(torch.device("cuda", local))
+    if world > 1 or args.config == 5:
+        pass  # config 5's 8.6 GB host copy is kept for the CPU baseline sample only
     torch.cuda.synchronize()
+    fp64 = measure_fp64_peak(torch.device("cuda", local)) if rank == 0 else None
     n = a.numel()
     dims = c["dims"]
     stream = torch.cuda.ExternalStream(lib().ttg_stream(), device=torch.device("cuda", local))
@@ -327,7 +421,7 @@ def run_ours(args):
     value = jobs * args.steps * entries_per_step / (ms_max * 1e-3)
 
     rep = {m: r.report() for m, r in info.items()}
-    rse = {m: r.rse(a.data_ptr(), on_device=True) for m, r in info.items()} if args.config != 5 else {}
+    rse = {m: r.rse(a.data_ptr(), on_device=True) for m, r in info.items()} if not sharded else {}
     info.clear()
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region ----
@@ -409,6 +503,22 @@ def run_ours(args):
                   "note": "CTA 0's %globaltimer per step: stream = reflector end to the first grid barrier "
                           "(the slowest CTA's stream plus the barrier)"}
     ncu_peak = (traffic or {}).get("implied_dram_peak_gbs_ncu")
+    # whole-step roofline: T_roof = sum over cuts of max(F_min / P_FP64, B_comp / BW)
+    step_model = None
+    if fp64 is not None:
+        sm = step_roofline(dims, runs, {m: r.ranks_chosen for m, r in rep.items()}, fp64["tflops"], peak)
+        t_dev = ms_max / args.steps
+        step_model = {"t_roof_ms": sm["t_roof_ms"], "t_dev_ms": t_dev, "frac": sm["t_roof_ms"] / t_dev,
+                      "p_fp64_tflops": fp64["tflops"], "p_fp64_source": fp64["how"], "bw_gbs": peak,
+                      "bw_source": f"hbm_gbs ({peak_kind})", "f_min": sm["f_min"], "f_ref": sm["f_ref"],
+                      "b_comp": sm["b_comp"],
+                      "f_min_tflops_achieved": sm["f_min"] / (t_dev * 1e-3) / 1e12,
+                      "formula": "T_roof = sum over cuts max(F_min/P_FP64, B_comp/BW_HBM) with the chosen ranks "
+                                 "(SURVEY.md 8(d), Appendix B; paper_2501_07904_b200/roofline.py); frac = T_roof/T_dev",
+                      "cuts": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in cu.items()}
+                               for cu in sm["cuts"]]}
+    parity = golden_parity(args.config, a_host, {m: {"ranks": r.ranks_chosen, "rse": rse.get(m)}
+                                                 for m, r in rep.items()}) if not sharded else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -419,7 +529,10 @@ def run_ours(args):
                        "qlp": args.qlp,
                        "ranks": {m: r.ranks_chosen for m, r in rep.items()},
                        "pass1_steps": {m: [cu["steps"] for cu in r.cuts] for m, r in rep.items()},
-                       "rse": rse},
+                       "rse": rse, "inputs": "paper_2501_07904_b200/inputs.py (the reference generators' "
+                                             "algorithms, bitwise; SURVEY Appendix C seeds)"},
+            "parity": parity,
+            "step_roofline": step_model,
             "roofline": {"bound": "hbm",
                          "kernel": dom["kernel"] + (" - pass-1 steps fused in one launch (reflector, streaming GEMV + "
                                                     "norm downdate, guard); bytes = the streams' algorithmic bytes"
@@ -444,7 +557,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(src, args.config, c, runs, desc)
+        line["cpu_baseline"] = cpu_baseline(a_host, args.config, c, runs, desc)
     comm = None
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -458,20 +571,22 @@ def cpu_sample(a, cfg: int, c):
     host cores): the whole tensor for configs 1-2; for the long configs a slice along one
     mode (a slice of a TT tensor is a TT tensor of the same ranks, clamped to the mode):
     config 3 keeps 3 of the 24 indices of the last mode, config 5 keeps 32 of the 1024
-    indices of the middle mode. Returns (host array, dims, ranks or None, note)."""
+    indices of the middle mode. `a` is the host buffer. Returns (host array, dims, ranks or
+    None, note)."""
+    import numpy as np
     dims = list(c["dims"])
     ranks = c.get("ranks")
     if cfg == 3:
-        t = a.view(*reversed(dims))[:3].contiguous()  # reversed view: last mode first
+        t = np.ascontiguousarray(a.reshape(list(reversed(dims)))[:3]).reshape(-1)  # last mode first
         dims2 = dims[:-1] + [3]
         r2 = list(ranks)
         r2[-2] = min(r2[-2], 3)
-        return t.cpu().numpy().reshape(-1), dims2, r2, "last mode sliced to 3 of 24 (1/8 of the entries)"
+        return t, dims2, r2, "last mode sliced to 3 of 24 (1/8 of the entries)"
     if cfg == 5:
-        t = a.view(*reversed(dims))[:, :32, :].contiguous()
+        t = np.ascontiguousarray(a.reshape(list(reversed(dims)))[:, :32, :]).reshape(-1)
         dims2 = [dims[0], 32, dims[2]]
-        return t.cpu().numpy().reshape(-1), dims2, list(ranks), "middle mode sliced to 32 of 1024 (1/32 of the entries)"
-    return a.cpu().numpy().reshape(-1), dims, ranks, "the whole tensor"
+        return t, dims2, list(ranks), "middle mode sliced to 32 of 1024 (1/32 of the entries)"
+    return a, dims, ranks, "the whole tensor"
 
 
 def cpu_baseline(a, cfg, c, runs, desc):
@@ -490,6 +605,7 @@ def cpu_baseline(a, cfg, c, runs, desc):
         dt = time.perf_counter() - t0
         return {"value": len(runs) * a_host.size / dt, "unit": UNIT,
                 "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "reference",
+                "cpu": host_cpu(),
                 "sample": f"one step of {desc} on the reference library ({note}, dims {dims}), ranks {got}, "
                           f"{dt:.1f} s"}
     except Exception as e:  # the baseline is reported, never required
@@ -507,7 +623,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 5],
+                    help="BASELINE config (default: 3 at one GPU, 5 column-sharded at N > 1)")
     ap.add_argument("--qlp", default="early_exit", choices=["early_exit", "full"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-concurrency", type=int, default=2,
@@ -515,6 +632,17 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="column-sharded engine over NCCL even at one rank (default for config 5 at N > 1)")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = 3 if args.gpus <= 1 else 5
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # not launched by torchrun: spawn one rank per GPU ourselves (same command line)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        return subprocess.run(cmd).returncode
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -145,6 +145,18 @@ int ttg_result_report(const ttg_result* res, double* step_errors, int64_t* ranks
                       double* input_norm, double* wall_time_ms);
 int ttg_result_warning_count(const ttg_result* res);
 const char* ttg_result_warning(const ttg_result* res, int i);
+/* step_errors above are the reference's residual_from_mass, sqrt(max(0, kept[p] - kept[r]))
+ * (src/factor.cpp:507-510), which cancels below ~1e-8 |A|_F (config 1 reports 0 like the
+ * reference). This writes beside them, per cut in unfolding order, the discarded mass
+ * computed directly (unseen pass-1 rows + discarded pass-2 columns, no subtraction), or -1
+ * for cuts of the general path (refine != 1, TT-SVD, Alg. 4). Returns d-1. */
+int ttg_result_direct_errors(const ttg_result* res, double* out);
+/* The kept-mass vector the cut's rank rule used (fast path): kept[0..s] over the s pass-2
+ * columns computed, in the reference's order (factor.cpp:479-499), then kept[p] (the total,
+ * |R1[:s]|^2 + the exact trailing mass when s < p) as the last entry. Writes min(max, count)
+ * entries and returns count (0 for general-path cuts). For margin logs of ulp-decided ranks
+ * (kept[r] - target in ulps). */
+int ttg_result_cut_kept(const ttg_result* res, int cut, double* kept, int max);
 /* Per-cut diagnostics (cut = 0..d-2 in unfolding order):
  *   diag: |T_ii| of the kept block, i < r (the "per-unfolding diagonal estimates"),
  *   info[0] pivoted steps run in pass 1, info[1] p = min(m,n), info[2] rank kept,

@@ -222,6 +222,10 @@ struct DecompReport {
     double input_norm = 0.0;
     double wall_time_ms = 0.0;
     std::vector<std::string> warnings;
+    // Extension (not in the reference): per cut, the discarded mass computed directly on the
+    // device; step_errors keep the reference's kept[p] - kept[r] subtraction (factor.cpp:507-510).
+    // -1 where not computed (general path: refine != 1, TT-SVD, Alg. 4).
+    std::vector<double> direct_step_errors;
 };
 struct DecompResult {
     TTTensor tt;

@@ -95,6 +95,8 @@ SIGNATURES = {
     "ttg_result_warning_count": (C.c_int, [C.c_void_p]),
     "ttg_result_warning": (C.c_char_p, [C.c_void_p, C.c_int]),
     "ttg_result_cut_diag": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int, c_int64_p]),
+    "ttg_result_direct_errors": (C.c_int, [C.c_void_p, c_double_p]),
+    "ttg_result_cut_kept": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int]),
     "ttg_verify_bound": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, c_double_p]),
     "ttg_result_rse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, c_double_p]),
     "ttg_result_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

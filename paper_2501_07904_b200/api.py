@@ -52,6 +52,9 @@ class DecompReport:
     warnings: list
     achieved_error: Optional[float] = None
     cuts: list = field(default_factory=list)  # dicts: steps, p, rank, extensions, m, n, diag
+    # per cut, the discarded mass computed directly (step_errors keep the reference's
+    # kept[p] - kept[r] subtraction, factor.cpp:507-510); -1 where not computed
+    direct_step_errors: list = field(default_factory=list)
 
 
 @dataclass
@@ -107,11 +110,16 @@ class DeviceResult:
             diag = np.zeros(8192, np.float64)
             info = np.zeros(6, np.int64)
             n = lib().ttg_result_cut_diag(self.h, c, _dptr(diag), diag.size, _iptr(info))
+            kept = np.zeros(8194, np.float64)
+            nk = lib().ttg_result_cut_kept(self.h, c, _dptr(kept), kept.size)
             cuts.append(dict(steps=int(info[0]), p=int(info[1]), rank=int(info[2]), extensions=int(info[3]),
-                             m=int(info[4]), n=int(info[5]), diag=diag[:n].copy()))
+                             m=int(info[4]), n=int(info[5]), diag=diag[:n].copy(),
+                             kept=kept[:min(nk, kept.size)].copy()))
+        de = np.zeros(max(d - 1, 0), np.float64)
+        lib().ttg_result_direct_errors(self.h, _dptr(de))
         return DecompReport(se.tolist(), rr[:nreq].tolist(), rc.tolist(), b.value,
                             "root_sum_square" if bk.value == 0 else "plain_sum", ni.value, wt.value, warns,
-                            cuts=cuts)
+                            cuts=cuts, direct_step_errors=de.tolist())
 
     def rse(self, a, on_device: bool = False) -> float:
         out = C.c_double()

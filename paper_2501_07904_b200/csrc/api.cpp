@@ -88,6 +88,8 @@ DecompResult run(const DenseTensor& a, const DecompConfig& cfg) {
     rep.ranks_requested.assign(req.begin(), req.begin() + nreq);
     rep.bound_kind = bk == TTG_BOUND_RSS ? BoundKind::root_sum_square : BoundKind::plain_sum;
     for (int i = 0; i < ttg_result_warning_count(g.r); ++i) rep.warnings.emplace_back(ttg_result_warning(g.r, i));
+    rep.direct_step_errors.resize((size_t)std::max(d - 1, 0));
+    ttg_result_direct_errors(g.r, rep.direct_step_errors.data());
     return out;
 }
 

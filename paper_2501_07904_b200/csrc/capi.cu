@@ -314,6 +314,21 @@ int ttg_result_cut_diag(const ttg_result* res, int cut, double* diag, int max, i
     return n;
 }
 
+int ttg_result_direct_errors(const ttg_result* res, double* out) {
+    const auto& cuts = res->r.cuts;
+    if (out)
+        for (size_t i = 0; i < cuts.size(); ++i) out[i] = cuts[i].direct_error;
+    return (int)cuts.size();
+}
+
+int ttg_result_cut_kept(const ttg_result* res, int cut, double* kept, int max) {
+    if (cut < 0 || (size_t)cut >= res->r.cuts.size()) return 0;
+    const auto& k = res->r.cuts[(size_t)cut].kept;
+    const int n = std::min<int>(max, (int)k.size());
+    for (int i = 0; i < n; ++i) kept[i] = k[(size_t)i];
+    return (int)k.size();
+}
+
 ttg_status ttg_result_rse(const ttg_result* res, const double* a, int a_on_device, double* rse) {
     return guard([&] {
         int64_t n = 1;

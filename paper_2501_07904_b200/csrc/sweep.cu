@@ -181,7 +181,9 @@ Resolved resolve_mode(const SweepConfig& cfg, int64_t d, double norm_a, bool rss
 // ---- one cut ------------------------------------------------------------------------------
 struct CutOut {
     int64_t rank = 0, steps = 0, extensions = 0;
-    double step_error = 0.0;
+    double step_error = 0.0;    // the reference's sqrt(max(0, kept[p] - kept[r])) (factor.cpp:507-510)
+    double direct_error = 0.0;  // the discarded mass computed directly (no cancellation)
+    std::vector<double> kept;   // kept[0..s] of the rank rule, then kept[p] (the total) last
     std::vector<double> diag;
     DevBuf<int64_t> sel;  // P2[:rank] on device
 };
@@ -762,11 +764,17 @@ CutOut run_cut(Pass1& e1, const CutRequest& req) {
         }
         out.rank = r;
         out.steps = s;
-        // Residual mass of the truncation computed directly (no kept[p] - kept[r]
-        // cancellation): discarded pass-2 columns plus the unseen R1 rows.
+        // Step error as the reference reports it: residual_from_mass (factor.cpp:507-510),
+        // sqrt(max(0, kept[p] - kept[r])) with kept[p] the total above -- a subtraction that
+        // cancels below ~1e-8 |A| (SURVEY finding 2; config 1 reports 0). The discarded mass
+        // computed directly (discarded pass-2 columns plus the unseen R1 rows) is kept beside
+        // it (report the reference value, log the direct one).
         double disc = t1;
         for (int64_t c = r; c < s; ++c) disc += p2.colmass[(size_t)c];
-        out.step_error = std::sqrt(std::max(0.0, disc));
+        out.direct_error = std::sqrt(std::max(0.0, disc));
+        out.step_error = std::sqrt(std::max(0.0, total - hk[(size_t)r]));
+        out.kept.assign(hk.begin(), hk.begin() + s + 1);
+        out.kept.push_back(total);
         out.diag.assign(p2.diag.begin(), p2.diag.begin() + r);
         out.sel = std::move(p2.perm);
         return out;
@@ -1076,7 +1084,7 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 1)] = co.step_error;
         res.ranks_chosen[(size_t)k] = r;
-        res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag};
+        res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, co.steps, r, co.extensions, co.diag, co.direct_error, co.kept};
         DevBuf<double> core((size_t)(m * r));
         TTG_LAUNCH(k_gather_qcols, (int)cdiv(m * r, 256), 256, 0, stream(), e1->Q(), m, co.sel.get(), r, false,
                    core.get());
@@ -1115,7 +1123,7 @@ void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, 
         const int64_t r = co.rank;
         res.step_errors[(size_t)(k - 2)] = co.step_error;
         res.ranks_chosen[(size_t)(k - 1)] = r;
-        res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag};
+        res.cuts[(size_t)(k - 2)] = CutInfo{M, n, p, co.steps, r, co.extensions, co.diag, co.direct_error, co.kept};
         DevBuf<double> core((size_t)(n * r));
         TTG_LAUNCH(k_gather_qcols, (int)cdiv(n * r, 256), 256, 0, stream(), e1->Q(), n, co.sel.get(), r, true,
                    core.get());
@@ -1319,7 +1327,7 @@ bool k_sharded_next(TTResult& res, const double* mine, int64_t Nl, int64_t Ng, i
     const int64_t r2 = co.rank;
     res.step_errors[(size_t)(d - 3)] = co.step_error;
     res.ranks_chosen[(size_t)(d - 2)] = r2;
-    res.cuts[(size_t)(d - 3)] = CutInfo{Mp, kg, p, co.steps, r2, co.extensions, co.diag};
+    res.cuts[(size_t)(d - 3)] = CutInfo{Mp, kg, p, co.steps, r2, co.extensions, co.diag, co.direct_error, co.kept};
     // core (r2 x I x r): local transposed core rows, all-gathered, scattered to n' order
     DevBuf<double> mineT((size_t)(kl * r2)), parts((size_t)(G * kl * r2)), core((size_t)(kg * r2));
     TTG_LAUNCH(k_gather_qcols, (int)cdiv(kl * r2, 256), 256, 0, stream(), gp.Q(), kl, co.sel.get(), r2, true,
@@ -1396,8 +1404,8 @@ TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& di
     const int64_t r = co.rank;
     res.step_errors[(size_t)(cut - 1)] = co.step_error;
     res.ranks_chosen[(size_t)cut] = r;
-    res.cuts[(size_t)(cut - 1)] = ulv ? CutInfo{kW, Ng, p, co.steps, r, co.extensions, co.diag}
-                                      : CutInfo{Ng, kW, p, co.steps, r, co.extensions, co.diag};
+    res.cuts[(size_t)(cut - 1)] = ulv ? CutInfo{kW, Ng, p, co.steps, r, co.extensions, co.diag, co.direct_error, co.kept}
+                                      : CutInfo{Ng, kW, p, co.steps, r, co.extensions, co.diag, co.direct_error, co.kept};
     // the core from the replicated Q; the local carry block, then the all-gathered carry
     DevBuf<double> core((size_t)(kW * r));
     TTG_LAUNCH(k_gather_qcols, (int)cdiv(kW * r, 256), 256, 0, stream(), e1.Q(), kW, co.sel.get(), r, !ulv,

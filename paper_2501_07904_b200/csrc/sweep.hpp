@@ -26,6 +26,8 @@ struct SweepConfig {
 struct CutInfo {
     int64_t m = 0, n = 0, p = 0, steps = 0, rank = 0, extensions = 0;
     std::vector<double> diag;  // |T_ii|, i < rank
+    double direct_error = -1.0;  // directly computed discarded mass (-1: general path, not computed)
+    std::vector<double> kept;    // the rank rule's kept[0..s] then kept[p] (empty: general path)
 };
 
 struct TTResult {

@@ -1,0 +1,180 @@
+"""Full-size parity at BASELINE sizes against the reference's own results.
+
+The reference ran once in the build container on inputs from its own generators
+(tests/golden/make_golden_full.py -> tests/golden/full_cfg{2,3,5}.npz). Here the inputs are
+rebuilt with paper_2501_07904_b200/inputs.py, which is bitwise the reference's generators
+(tests/test_inputs_cpu.py; each test also checks the golden's input norm and sum), and the
+device result is held to SURVEY.md Appendix A:
+
+  configs 3 and 5 (fixed rank, well separated): identical ranks; |RSE_gpu - RSE_ref| <= 1e-10;
+    kept |T_ii| within 1e-10 |T_00| on every cut; step errors (the reference's
+    kept[p] - kept[r] form) with squared values within 1e-13 |A|^2; the directly computed
+    discarded mass within 1e-10 |A|;
+  config 2 (ranks decided below half an ulp): the oracle's own variability set under
+    neutral rescalings of A -- every device rank in the set of the oracle's ranks for that
+    cut and RSE <= the largest oracle RSE + 1e-10 -- with the device's per-cut margins
+    (kept[r] - target in ulps) printed; at eps = 1e-6 (well posed) the full contract.
+"""
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2501_07904_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+TOL_RSE = 1e-10
+TOL_DIAG = 1e-10
+
+
+def _golden(name):
+    p = GOLD / f"full_{name}.npz"
+    if not p.exists():
+        pytest.skip(f"{p.name} not generated (tests/golden/make_golden_full.py {name})")
+    return np.load(p)
+
+
+def _check_input(g, a):
+    assert float(a.sum()) == float(g["a_sum"]), "input differs from the golden's (generators drifted)"
+
+
+def _check_cut_parity(g, prefix, rep, norm):
+    ranks = [int(x) for x in g[f"{prefix}_ranks"]]
+    assert rep.ranks_chosen == ranks
+    for k, cut in enumerate(rep.cuts):
+        gd = g[f"{prefix}_cut{k}_diag"]
+        r = cut["rank"]
+        assert list(g[f"{prefix}_cut{k}_mn"]) == [cut["m"], cut["n"]]
+        dev = np.abs(cut["diag"][:r] - gd[:r]).max()
+        assert dev <= TOL_DIAG * gd[0], (k, dev, gd[0])
+        se_ref = float(g[f"{prefix}_step_errors"][k])
+        se = rep.step_errors[k]
+        assert abs(se * se - se_ref * se_ref) <= 1e-13 * norm * norm, (k, se, se_ref)
+        direct_ref = float(g[f"{prefix}_cut{k}_direct"])
+        if direct_ref >= 0 and rep.direct_step_errors[k] >= 0:
+            assert abs(rep.direct_step_errors[k] - direct_ref) <= 1e-10 * norm, (k, rep.direct_step_errors[k],
+                                                                                 direct_ref)
+
+
+@pytest.fixture(scope="module")
+def cfg3_input():
+    return inputs.build_host(3)
+
+
+@pytest.mark.parametrize("method", ["ulv", "urv"])
+def test_config3_fullsize(dev, cfg3_input, method):
+    """24^6 planted ranks 20 + 1e-4 noise, fixed rank 20 (BASELINE config 3)."""
+    g = _golden("cfg3")
+    a = cfg3_input
+    _check_input(g, a)
+    dims, ranks = [24] * 6, [1, 20, 20, 20, 20, 20, 1]
+    res = dev.decompose_device(a, dims, method, "l2r" if method == "ulv" else "r2l", ranks=ranks)
+    rep = res.report()
+    norm = float(g[f"{method}_input_norm"])
+    assert abs(rep.input_norm - norm) <= 1e-13 * norm
+    _check_cut_parity(g, method, rep, norm)
+    rse = res.rse(a)
+    assert abs(rse - float(g[f"{method}_rse"])) <= TOL_RSE, (rse, float(g[f"{method}_rse"]))
+    # the cores themselves: the same Householder conventions and pivots give the same factors
+    for k in range(6):
+        core = res.core(k)
+        want = g[f"{method}_core{k}"]
+        assert core.shape == want.shape
+        assert np.abs(core - want).max() <= 1e-8 * max(1.0, np.abs(want).max()), k
+
+
+def test_config5_fullsize(dev):
+    """1024^3 planted ranks 128 + 1e-6 noise, fixed rank 128, TT-URV (BASELINE config 5):
+    the first cut is the 1,048,576 x 1024 unfolding (W = 1024 x 1,048,576)."""
+    g = _golden("cfg5")
+    a = inputs.build_host(5)
+    _check_input(g, a)
+    dims, ranks = [1024] * 3, [1, 128, 128, 1]
+    res = dev.decompose_device(a, dims, "urv", "r2l", ranks=ranks)
+    rep = res.report()
+    norm = float(g["urv_input_norm"])
+    _check_cut_parity(g, "urv", rep, norm)
+    if "urv_rse" in g:
+        rse = res.rse(a)
+        assert abs(rse - float(g["urv_rse"])) <= TOL_RSE, (rse, float(g["urv_rse"]))
+    for k in (0, 2):
+        want = g[f"urv_core{k}"]
+        assert np.abs(res.core(k) - want).max() <= 1e-8 * max(1.0, np.abs(want).max())
+    mid = res.core(1)
+    assert abs(np.linalg.norm(mid) - float(g["urv_core1_norm"])) <= 1e-10 * float(g["urv_core1_norm"])
+    slab = g["urv_core1_slab"]
+    assert np.abs(mid[:, : slab.shape[1], :] - slab).max() <= 1e-8 * max(1.0, np.abs(slab).max())
+
+
+def _ulp(x):
+    return math.ulp(x)
+
+
+def _margins(rep):
+    """Per cut: kept[r] - target in ulps of the total (the rank rule's margin)."""
+    out = []
+    for cut in rep.cuts:
+        kept = cut["kept"]
+        if kept.size < 2:
+            out.append(None)
+            continue
+        total = kept[-1]
+        out.append(round((kept[cut["rank"]] - total) / _ulp(total), 2) if cut["rank"] < kept.size - 1 else None)
+    return out
+
+
+@pytest.mark.parametrize("method", ["ulv", "urv"])
+def test_config2_appendix_a_variability_set(dev, method):
+    """32^5 shifted Hilbert at eps = 1e-8 (BASELINE config 2). eps_k^2 = 2.5e-17 |A|^2 is
+    below half an ulp of the kept-mass total, so the first (ULV) / last (URV) cut's rank is
+    decided by rounding: the reference itself picks 11, 12, 25, 28 or 32 under neutral
+    rescalings of A (tests/golden/full_cfg2.npz). Contract: every
+    device rank lies in the oracle's set for that cut and the device RSE <= the largest
+    oracle RSE + 1e-10, on A and on every rescaled copy."""
+    g = _golden("cfg2")
+    dims = [32] * 5
+    base = inputs.hilbert_shifted(dims)
+    scales = [float(x) for x in g["scales"]]
+    sweep = "l2r" if method == "ulv" else "r2l"
+    oracle_sets = [set() for _ in range(6)]
+    oracle_rse = []
+    for i in range(len(scales)):
+        rk = [int(x) for x in g[f"e8_s{i}_{method}_ranks"]]
+        for k, r in enumerate(rk):
+            oracle_sets[k].add(r)
+        oracle_rse.append(float(g[f"e8_s{i}_{method}_rse"]))
+    rse_cap = max(oracle_rse) + TOL_RSE
+    seen = []
+    for i, s in enumerate(scales):
+        a = base * s if s != 1.0 else base
+        res = dev.decompose_device(a, dims, method, sweep, eps=1e-8)
+        rep = res.report()
+        rse = res.rse(a)
+        seen.append((s, rep.ranks_chosen, rse, _margins(rep)))
+        print(f"config 2 {method} scale {s}: device ranks {rep.ranks_chosen} rse {rse:.4e} margins(ulp) "
+              f"{_margins(rep)}; oracle ranks {[int(x) for x in g[f'e8_s{i}_{method}_ranks']]} "
+              f"rse {float(g[f'e8_s{i}_{method}_rse']):.4e}")
+        for k, r in enumerate(rep.ranks_chosen):
+            assert r in oracle_sets[k], (s, k, r, sorted(oracle_sets[k]))
+        assert rse <= rse_cap, (s, rse, rse_cap)
+
+
+@pytest.mark.parametrize("method", ["ulv", "urv"])
+def test_config2_wellposed_eps_1e6(dev, method):
+    """at eps = 1e-6 the budget is far above the ulp level and the full
+    contract holds (identical ranks, |dRSE| <= 1e-10, kept diagonals within 1e-10 |T_00|)."""
+    g = _golden("cfg2")
+    dims = [32] * 5
+    a = inputs.hilbert_shifted(dims)
+    res = dev.decompose_device(a, dims, method, "l2r" if method == "ulv" else "r2l", eps=1e-6)
+    rep = res.report()
+    pre = f"e6_s0_{method}"
+    assert rep.ranks_chosen == [int(x) for x in g[f"{pre}_ranks"]]
+    for k, cut in enumerate(rep.cuts):
+        gd = g[f"{pre}_cut{k}_diag"]
+        r = cut["rank"]
+        assert np.abs(cut["diag"][:r] - gd[:r]).max() <= TOL_DIAG * gd[0], k
+    assert abs(res.rse(a) - float(g[f"{pre}_rse"])) <= TOL_RSE
