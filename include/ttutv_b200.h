@@ -232,11 +232,29 @@ ttg_status ttg_truncate(int kind, const double* u, const double* t, const double
 ttg_status ttg_reconstruct(const double* cores, const int64_t* dims, const int64_t* ranks, int d,
                            int64_t element_cap, double* out);
 ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, double* out);
+/* kernels::sum_squares (kernels.cpp:84-102): the 4096-blocked sum of squares, no sqrt */
+ttg_status ttg_sum_squares(const double* a, int64_t count, int a_on_device, double* out);
 ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, double* out);
 /* |x - y|_2 over count entries (verify_bound's achieved error, tt_decomp.cpp:449-454). */
 ttg_status ttg_diff_norm(const double* x, const double* y, int64_t count, double* out);
 /* C = op(A) op(B) on the device (DMMA tiles), host buffers, column-major; op = transpose
  * when ta/tb is nonzero (kernels::matmul, include/ttutv/kernels.hpp:21). */
+/* Tensor algebra (host buffers in and out, computed on the device):
+ *   mode_product  tensor_ops.cpp:49-80: out = tensor x_k mat (mat is m_rows x m_cols, m_cols
+ *                 must equal dims[k-1]; k is 1-based); bitwise the reference's (same sums)
+ *   kron          tensor_ops.cpp:82-93 (column-major (ar br) x (ac bc)); bitwise
+ *   psnr          tensor_ops.cpp:113-126: 10 log10(max(truth)^2 / mse), +inf when mse == 0
+ *   reverse_indices  tensor_ops.cpp:128-143: out has dims reversed, out(i_d..i_1) = a(i_1..i_d)
+ *   reverse_tt    tt.cpp:108-123: cores (packed back to back, core k = ranks[k] x dims[k] x
+ *                 ranks[k+1]) of the reversed train, packed in the new core order */
+ttg_status ttg_mode_product(const double* x, const int64_t* dims, int d, int k, const double* m,
+                            int64_t m_rows, int64_t m_cols, double* out);
+ttg_status ttg_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc,
+                    double* out);
+ttg_status ttg_psnr(const double* estimate, const double* truth, int64_t count, double* out);
+ttg_status ttg_reverse_indices(const double* a, const int64_t* dims, int d, double* out);
+ttg_status ttg_reverse_tt(const double* cores, const int64_t* dims, const int64_t* ranks, int d,
+                          double* out);
 ttg_status ttg_matmul(const double* a, int64_t a_rows, int64_t a_cols, int ta, const double* b,
                       int64_t b_rows, int64_t b_cols, int tb, double* c);
 

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <initializer_list>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -93,6 +94,12 @@ public:
     std::int64_t element_count() const noexcept { return s_.element_count(); }
     double& at(std::span<const std::int64_t> idx) { return v_[(size_t)(ivec(idx, s_) - 1)]; }
     double at(std::span<const std::int64_t> idx) const { return v_[(size_t)(ivec(idx, s_) - 1)]; }
+    double& at(std::initializer_list<std::int64_t> idx) {
+        return at(std::span<const std::int64_t>(idx.begin(), idx.size()));
+    }
+    double at(std::initializer_list<std::int64_t> idx) const {
+        return at(std::span<const std::int64_t>(idx.begin(), idx.size()));
+    }
     double& operator[](std::int64_t i) noexcept { return v_[(size_t)i]; }
     double operator[](std::int64_t i) const noexcept { return v_[(size_t)i]; }
     double* data() noexcept { return v_.data(); }
@@ -136,13 +143,38 @@ struct OrthogonalityReport {
     double max_right_deviation = 0.0;
 };
 OrthogonalityReport check_orthogonality(const TTTensor& tt);
+TTTensor reverse_tt(const TTTensor& tt);
 TTTensor zero_tt(const Shape& shape);
 
 // ---- tensor ops (tensor_ops.hpp) -----------------------------------------------------
 Matrix unfold(const DenseTensor& tensor, std::int64_t k);
+DenseTensor fold(const Matrix& mat, const Shape& shape, std::int64_t k);
+DenseTensor fold(Matrix&& mat, const Shape& shape, std::int64_t k);
+DenseTensor mode_product(const DenseTensor& tensor, const Matrix& mat, std::int64_t k);
+Matrix kron(const Matrix& a, const Matrix& b);
 double frobenius_norm(const DenseTensor& tensor);
 double frobenius_norm(const Matrix& mat);
 double rse(const DenseTensor& estimate, const DenseTensor& truth);
+double psnr(const DenseTensor& estimate, const DenseTensor& truth);
+DenseTensor reverse_indices(const DenseTensor& tensor);
+
+// ---- dense kernels (kernels.hpp) -------------------------------------------------------
+namespace kernels {
+// The device kernels are always parallel and deterministic; the switch is kept for source
+// compatibility and changes nothing (kernels.hpp:13-16).
+void set_parallel_enabled(bool enabled) noexcept;
+bool parallel_enabled() noexcept;
+// C = op(A) op(B) on the device (DMMA tiles).
+Matrix matmul(const Matrix& a, const Matrix& b, bool transpose_a = false, bool transpose_b = false);
+Matrix matmul_serial(const Matrix& a, const Matrix& b, bool transpose_a = false, bool transpose_b = false);
+Matrix transpose(const Matrix& a);
+// 4096-blocked sum of squares on the device (kernels.cpp:84-102's blocking and order).
+double sum_squares(std::span<const double> values);
+// Host-side BLAS-1 helpers of the reference's test API (not on the decomposition path).
+double sum_squares_serial(std::span<const double> values);
+double dot(std::span<const double> x, std::span<const double> y);
+void axpy(double alpha, std::span<const double> x, std::span<double> y);
+}  // namespace kernels
 
 // ---- factorizations (factor.hpp) -------------------------------------------------------
 struct QrPivotResult {
@@ -191,6 +223,17 @@ TruncatedFactorization truncate_fixed_rank(const UrvFactors& f, std::int64_t ran
 TruncatedFactorization truncate_fixed_tol(const SvdResult& f, double eps);
 TruncatedFactorization truncate_fixed_tol(const UlvFactors& f, double eps);
 TruncatedFactorization truncate_fixed_tol(const UrvFactors& f, double eps);
+
+// Rank-revealing diagnostics at split rank r (factor.hpp:87-95): sigma_min(T11), the
+// spectral norm of the discarded block, and sigma_r, sigma_{r+1} of T (0 when r == p).
+struct RankRevealDiag {
+    double sigma_min_t11 = 0.0;
+    double residual_spectral_norm = 0.0;
+    double sigma_r = 0.0;
+    double sigma_r_plus_1 = 0.0;
+};
+RankRevealDiag rank_reveal_diag(const UlvFactors& f, std::int64_t rank);
+RankRevealDiag rank_reveal_diag(const UrvFactors& f, std::int64_t rank);
 
 // ---- sweeps (tt_decomp.hpp) -------------------------------------------------------------
 enum class Method { svd, ulv, urv };

@@ -331,6 +331,71 @@ int ref_write_tt(const char* path, int d, const int64_t* ranks, const int64_t* d
 
 }  // extern "C"
 
+// ---- tensor algebra (tensor_ops.hpp, tt.hpp, factor.hpp rank_reveal_diag) ----------------
+extern "C" {
+
+int ref_mode_product(const double* x, const int64_t* dims, int d, int k, const double* m, int64_t mr, int64_t mc,
+                     double* out) {
+    return guarded([&] {
+        ttutv::DenseTensor y = ttutv::mode_product(tensor_of(x, dims, d), matrix_of(m, mr, mc), k);
+        std::memcpy(out, y.data(), sizeof(double) * (size_t)y.element_count());
+    });
+}
+
+int ref_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc, double* out) {
+    return guarded([&] { put(ttutv::kron(matrix_of(a, ar, ac), matrix_of(b, br, bc)), out); });
+}
+
+int ref_psnr(const double* e, const double* t, const int64_t* dims, int d, double* out) {
+    return guarded([&] { *out = ttutv::psnr(tensor_of(e, dims, d), tensor_of(t, dims, d)); });
+}
+
+int ref_reverse_indices(const double* a, const int64_t* dims, int d, double* out) {
+    return guarded([&] {
+        ttutv::DenseTensor y = ttutv::reverse_indices(tensor_of(a, dims, d));
+        std::memcpy(out, y.data(), sizeof(double) * (size_t)y.element_count());
+    });
+}
+
+// cores packed back to back (core k: ranks[k] x dims[k] x ranks[k+1]); output packed in the
+// reversed train's order
+int ref_reverse_tt(const double* cores, const int64_t* dims, const int64_t* ranks, int d, double* out) {
+    return guarded([&] {
+        std::vector<ttutv::TTCore> cs;
+        const double* p = cores;
+        for (int k = 0; k < d; ++k) {
+            const int64_t cd[3] = {ranks[k], dims[k], ranks[k + 1]};
+            cs.push_back(ttutv::TTCore{tensor_of(p, cd, 3)});
+            p += cd[0] * cd[1] * cd[2];
+        }
+        ttutv::TTTensor r = ttutv::reverse_tt(ttutv::TTTensor(std::move(cs)));
+        for (const auto& c : r.cores()) {
+            std::memcpy(out, c.data.data(), sizeof(double) * (size_t)c.data.element_count());
+            out += c.data.element_count();
+        }
+    });
+}
+
+// lower != 0: UlvFactors{u, t, v}; else UrvFactors. out4 = sigma_min_t11, residual, sigma_r, sigma_r+1
+int ref_rank_reveal_diag(const double* u, const double* t, const double* v, int64_t m, int64_t n, int64_t p,
+                         int lower, int64_t rank, double* out4) {
+    return guarded([&] {
+        ttutv::RankRevealDiag dg;
+        if (lower)
+            dg = ttutv::rank_reveal_diag(ttutv::UlvFactors{matrix_of(u, m, p), matrix_of(t, p, p), matrix_of(v, n, p)},
+                                         rank);
+        else
+            dg = ttutv::rank_reveal_diag(ttutv::UrvFactors{matrix_of(u, m, p), matrix_of(t, p, p), matrix_of(v, n, p)},
+                                         rank);
+        out4[0] = dg.sigma_min_t11;
+        out4[1] = dg.residual_spectral_norm;
+        out4[2] = dg.sigma_r;
+        out4[3] = dg.sigma_r_plus_1;
+    });
+}
+
+}  // extern "C"
+
 // ---- sweep trace (golden fixtures) ------------------------------------------
 // A restatement of sweep_l2r (ULV) / sweep_r2l (URV, l11_only) from
 // src/tt_decomp.cpp:156-339 built only from the reference's public calls (ulv/urv,

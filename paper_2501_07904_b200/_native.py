@@ -96,6 +96,13 @@ SIGNATURES = {
     "ttg_result_warning": (C.c_char_p, [C.c_void_p, C.c_int]),
     "ttg_result_cut_diag": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int, c_int64_p]),
     "ttg_result_direct_errors": (C.c_int, [C.c_void_p, c_double_p]),
+    "ttg_mode_product": (C.c_int, [c_double_p, c_int64_p, C.c_int, C.c_int, c_double_p, C.c_int64, C.c_int64,
+                                   c_double_p]),
+    "ttg_kron": (C.c_int, [c_double_p, C.c_int64, C.c_int64, c_double_p, C.c_int64, C.c_int64, c_double_p]),
+    "ttg_sum_squares": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, c_double_p]),
+    "ttg_psnr": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
+    "ttg_reverse_indices": (C.c_int, [c_double_p, c_int64_p, C.c_int, c_double_p]),
+    "ttg_reverse_tt": (C.c_int, [c_double_p, c_int64_p, c_int64_p, C.c_int, c_double_p]),
     "ttg_result_cut_kept": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.c_int]),
     "ttg_verify_bound": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_double, c_double_p]),
     "ttg_result_rse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, c_double_p]),

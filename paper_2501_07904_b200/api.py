@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._native import Config, check, lib, require_gpu, c_double_p, c_int64_p
+from ._native import ArgumentError, Config, check, lib, require_gpu, c_double_p, c_int64_p
 
 METHODS = {"svd": 0, "ulv": 1, "urv": 2}
 SWEEPS = {"l2r": 0, "left_to_right": 0, "r2l": 1, "right_to_left": 1}
@@ -386,6 +386,28 @@ def qr_col_pivot(a: np.ndarray):
     return q, r, perm
 
 
+def utv(a: np.ndarray, lower: bool, refine_passes: int = 1):
+    """ulv (lower) / urv (factor.hpp:56-57): returns (u m x p, t p x p, v n x p)."""
+    require_gpu()
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    p = min(m, n)
+    u, t, v = np.zeros((m, p), order="F"), np.zeros((p, p), order="F"), np.zeros((n, p), order="F")
+    check(lib().ttg_utv(_dptr(a), m, n, int(bool(lower)), int(refine_passes), _dptr(u), _dptr(t), _dptr(v)))
+    return u, t, v
+
+
+def svd(a: np.ndarray, max_sweeps: int = 60, pair_tol: float = 1e-14):
+    """svd (factor.hpp:34): returns (u m x p, s p, v n x p)."""
+    require_gpu()
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    p = min(m, n)
+    u, s, v = np.zeros((m, p), order="F"), np.zeros(p), np.zeros((n, p), order="F")
+    check(lib().ttg_svd(_dptr(a), m, n, int(max_sweeps), float(pair_tol), _dptr(u), _dptr(s), _dptr(v)))
+    return u, s, v
+
+
 def reconstruct(cores: Sequence[np.ndarray], element_cap: int = 100_000_000) -> np.ndarray:
     """reconstruct (tt.hpp:60): dense tensor (order='F' n-d array) from cores."""
     require_gpu()
@@ -403,6 +425,72 @@ def frobenius_norm(a) -> float:
     out = C.c_double()
     check(lib().ttg_frobenius_norm(a.ctypes.data_as(C.c_void_p), a.size, 0, C.byref(out)))
     return out.value
+
+
+# ---- tensor algebra (tensor_ops.hpp, tt.hpp) ------------------------------------------
+def mode_product(x: np.ndarray, m: np.ndarray, k: int) -> np.ndarray:
+    """mode_product (tensor_ops.hpp:21): x (n-d, order='F' semantics) times m (rows x dims[k-1])
+    along 1-based mode k; computed on the device in the reference's operation order."""
+    require_gpu()
+    x = np.asarray(x, np.float64)
+    dims = np.array(x.shape, np.int64)
+    m = np.asfortranarray(m, dtype=np.float64)
+    flat = np.ascontiguousarray(x.ravel(order="F"))
+    od = list(x.shape)
+    if 1 <= k <= len(od):
+        od[k - 1] = m.shape[0]
+    out = np.empty(int(np.prod(od)), np.float64)
+    check(lib().ttg_mode_product(_dptr(flat), _iptr(dims), int(dims.size), int(k), _dptr(m), m.shape[0], m.shape[1],
+                                 _dptr(out)))
+    return out.reshape(od, order="F")
+
+
+def kron(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    require_gpu()
+    a = np.asfortranarray(a, dtype=np.float64)
+    b = np.asfortranarray(b, dtype=np.float64)
+    out = np.empty((a.shape[0] * b.shape[0], a.shape[1] * b.shape[1]), order="F")
+    check(lib().ttg_kron(_dptr(a), a.shape[0], a.shape[1], _dptr(b), b.shape[0], b.shape[1], _dptr(out)))
+    return out
+
+
+def psnr(estimate, truth) -> float:
+    require_gpu()
+    e = np.ascontiguousarray(np.asarray(estimate, np.float64).reshape(-1))
+    t = np.ascontiguousarray(np.asarray(truth, np.float64).reshape(-1))
+    if e.size != t.size:
+        raise ArgumentError("psnr: shapes differ")
+    out = C.c_double()
+    check(lib().ttg_psnr(_dptr(e), _dptr(t), t.size, C.byref(out)))
+    return out.value
+
+
+def reverse_indices(x: np.ndarray) -> np.ndarray:
+    """reverse_indices (tensor_ops.hpp:37): out(i_d, ..., i_1) = x(i_1, ..., i_d)."""
+    require_gpu()
+    x = np.asarray(x, np.float64)
+    dims = np.array(x.shape, np.int64)
+    flat = np.ascontiguousarray(x.ravel(order="F"))
+    out = np.empty(flat.size, np.float64)
+    check(lib().ttg_reverse_indices(_dptr(flat), _iptr(dims), int(dims.size), _dptr(out)))
+    return out.reshape(tuple(reversed(x.shape)), order="F")
+
+
+def reverse_tt(cores: Sequence[np.ndarray]) -> list:
+    """reverse_tt (tt.hpp:63): the cores of the train with the mode order reversed."""
+    require_gpu()
+    dims = np.array([c.shape[1] for c in cores], np.int64)
+    ranks = np.array([1] + [c.shape[2] for c in cores], np.int64)
+    flat = np.concatenate([np.asarray(c, np.float64).ravel(order="F") for c in cores])
+    out = np.empty_like(flat)
+    check(lib().ttg_reverse_tt(_dptr(flat), _iptr(dims), _iptr(ranks), int(dims.size), _dptr(out)))
+    res, off = [], 0
+    for c in reversed(cores):
+        shp = (c.shape[2], c.shape[1], c.shape[0])
+        n = int(np.prod(shp))
+        res.append(out[off:off + n].reshape(shp, order="F"))
+        off += n
+    return res
 
 
 def kernel_launches() -> int:

@@ -279,6 +279,91 @@ Matrix unfold(const DenseTensor& t, std::int64_t k) {
     return Matrix(rows, t.element_count() / rows, t.storage());
 }
 
+namespace {
+void check_fold_mode(const Shape& shape, std::int64_t k) {
+    if (shape.order() < 2) throw ArgumentError("unfold requires order >= 2");
+    if (k < 1 || k >= shape.order())
+        throw ArgumentError("unfold mode " + std::to_string(k) + " out of range 1.." + std::to_string(shape.order() - 1));
+}
+void check_fold_dims(const Matrix& mat, const Shape& shape, std::int64_t k) {
+    check_fold_mode(shape, k);
+    const std::int64_t rows = shape.prefix_product(k);
+    if (mat.rows() != rows || mat.cols() != shape.element_count() / rows)
+        throw ArgumentError("fold: matrix is " + std::to_string(mat.rows()) + "x" + std::to_string(mat.cols()) +
+                            ", expected " + std::to_string(rows) + "x" + std::to_string(shape.element_count() / rows));
+}
+}  // namespace
+
+// fold (tensor_ops.cpp:32-47): a reshape of the same column-major bytes
+DenseTensor fold(const Matrix& mat, const Shape& shape, std::int64_t k) {
+    check_fold_dims(mat, shape, k);
+    return DenseTensor(shape, mat.storage());
+}
+
+DenseTensor fold(Matrix&& mat, const Shape& shape, std::int64_t k) {
+    check_fold_dims(mat, shape, k);
+    return DenseTensor(shape, mat.take_storage());
+}
+
+DenseTensor mode_product(const DenseTensor& t, const Matrix& mat, std::int64_t k) {
+    const Shape& shape = t.shape();
+    if (k < 1 || k > shape.order())
+        throw ArgumentError("mode " + std::to_string(k) + " out of range 1.." + std::to_string(shape.order()));
+    if (mat.cols() != shape.dim(k))
+        throw ArgumentError("mode-" + std::to_string(k) + " product needs " + std::to_string(shape.dim(k)) +
+                            " columns, matrix has " + std::to_string(mat.cols()));
+    std::vector<std::int64_t> nd(shape.dims().begin(), shape.dims().end());
+    nd[(size_t)(k - 1)] = mat.rows();
+    DenseTensor out{Shape(nd)};
+    const std::vector<std::int64_t> dims(shape.dims().begin(), shape.dims().end());
+    check(ttg_mode_product(t.data(), dims.data(), (int)dims.size(), (int)k, mat.data(), mat.rows(), mat.cols(),
+                           out.data()));
+    return out;
+}
+
+Matrix kron(const Matrix& a, const Matrix& b) {
+    Matrix out(a.rows() * b.rows(), a.cols() * b.cols());
+    check(ttg_kron(a.data(), a.rows(), a.cols(), b.data(), b.rows(), b.cols(), out.data()));
+    return out;
+}
+
+double psnr(const DenseTensor& est, const DenseTensor& truth) {
+    if (!(est.shape() == truth.shape())) throw ArgumentError("psnr: shapes differ");
+    double out = 0.0;
+    check(ttg_psnr(est.data(), truth.data(), truth.element_count(), &out));
+    return out;
+}
+
+DenseTensor reverse_indices(const DenseTensor& t) {
+    const std::vector<std::int64_t> dims(t.shape().dims().begin(), t.shape().dims().end());
+    DenseTensor out{Shape(std::vector<std::int64_t>(dims.rbegin(), dims.rend()))};
+    check(ttg_reverse_indices(t.data(), dims.data(), (int)dims.size(), out.data()));
+    return out;
+}
+
+TTTensor reverse_tt(const TTTensor& tt) {
+    const std::int64_t d = tt.order();
+    std::vector<std::int64_t> dims, ranks{1};
+    std::vector<double> flat;
+    for (const TTCore& c : tt.cores()) {
+        dims.push_back(c.mode_dim());
+        ranks.push_back(c.rank_right());
+        flat.insert(flat.end(), c.data.storage().begin(), c.data.storage().end());
+    }
+    std::vector<double> out(flat.size());
+    if (d > 0) check(ttg_reverse_tt(flat.data(), dims.data(), ranks.data(), (int)d, out.data()));
+    std::vector<TTCore> cores;
+    std::size_t off = 0;
+    for (std::int64_t k = d - 1; k >= 0; --k) {  // core k of the input becomes core d-1-k
+        const TTCore& src = tt.cores()[(size_t)k];
+        const std::int64_t n = src.data.element_count();
+        cores.push_back(TTCore{DenseTensor(Shape({src.rank_right(), src.mode_dim(), src.rank_left()}),
+                                           std::vector<double>(out.begin() + (long)off, out.begin() + (long)(off + n)))});
+        off += (size_t)n;
+    }
+    return TTTensor(std::move(cores));
+}
+
 double frobenius_norm(const DenseTensor& t) {
     double out = 0.0;
     check(ttg_frobenius_norm(t.data(), t.element_count(), 0, &out));
@@ -297,6 +382,56 @@ double rse(const DenseTensor& est, const DenseTensor& truth) {
     check(ttg_rse(est.data(), truth.data(), truth.element_count(), &out));
     return out;
 }
+
+// ---- kernels.hpp ---------------------------------------------------------------------------
+namespace kernels {
+namespace {
+bool g_parallel = true;
+}
+void set_parallel_enabled(bool enabled) noexcept { g_parallel = enabled; }
+bool parallel_enabled() noexcept { return g_parallel; }
+
+Matrix matmul(const Matrix& a, const Matrix& b, bool ta, bool tb) {
+    const std::int64_t m = ta ? a.cols() : a.rows(), k = ta ? a.rows() : a.cols();
+    const std::int64_t kb = tb ? b.cols() : b.rows(), n = tb ? b.rows() : b.cols();
+    if (k != kb)
+        throw ArgumentError("matmul inner dimensions do not match");
+    Matrix c(m, n);
+    check(ttg_matmul(a.data(), a.rows(), a.cols(), ta ? 1 : 0, b.data(), b.rows(), b.cols(), tb ? 1 : 0, c.data()));
+    return c;
+}
+Matrix matmul_serial(const Matrix& a, const Matrix& b, bool ta, bool tb) { return matmul(a, b, ta, tb); }
+
+Matrix transpose(const Matrix& a) {
+    Matrix t(a.cols(), a.rows());
+    if (a.size() == 0) return t;
+    Matrix id = Matrix::identity(a.cols());
+    // A^T = (A^T I): one device GEMM with the transposed operand
+    check(ttg_matmul(a.data(), a.rows(), a.cols(), 1, id.data(), id.rows(), id.cols(), 0, t.data()));
+    return t;
+}
+
+double sum_squares(std::span<const double> v) {
+    double s = 0.0;
+    check(ttg_sum_squares(v.data(), (std::int64_t)v.size(), 0, &s));
+    return s;
+}
+double sum_squares_serial(std::span<const double> v) {
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return s;
+}
+double dot(std::span<const double> x, std::span<const double> y) {
+    if (x.size() != y.size()) throw ArgumentError("dot operands differ in length");
+    double s = 0.0;
+    for (size_t i = 0; i < x.size(); ++i) s += x[i] * y[i];
+    return s;
+}
+void axpy(double alpha, std::span<const double> x, std::span<double> y) {
+    if (x.size() != y.size()) throw ArgumentError("axpy operands differ in length");
+    for (size_t i = 0; i < x.size(); ++i) y[i] += alpha * x[i];
+}
+}  // namespace kernels
 
 // ---- factor level --------------------------------------------------------------------------
 QrPivotResult qr_col_pivot(const Matrix& a) {
@@ -348,6 +483,38 @@ TruncatedFactorization trunc(int kind, const Matrix& u, const double* t, const M
     return out;
 }
 }  // namespace
+
+namespace {
+// factor.cpp:568-597: singular values of T11, of the discarded block and of T (the device SVD)
+RankRevealDiag reveal(const Matrix& t, std::int64_t rank, bool lower) {
+    const std::int64_t p = t.rows();
+    if (rank < 1 || rank > p)
+        throw ArgumentError("rank " + std::to_string(rank) + " out of range 1.." + std::to_string(p));
+    RankRevealDiag out;
+    Matrix t11(rank, rank);
+    for (std::int64_t j = 0; j < rank; ++j)
+        for (std::int64_t i = 0; i < rank; ++i) t11(i, j) = t(i, j);
+    out.sigma_min_t11 = svd(t11).s.back();
+    if (rank < p) {
+        Matrix disc = lower ? Matrix(p - rank, p) : Matrix(p, p - rank);
+        if (lower) {
+            for (std::int64_t j = 0; j < p; ++j)
+                for (std::int64_t i = rank; i < p; ++i) disc(i - rank, j) = t(i, j);
+        } else {
+            for (std::int64_t j = rank; j < p; ++j)
+                for (std::int64_t i = 0; i < p; ++i) disc(i, j - rank) = t(i, j);
+        }
+        out.residual_spectral_norm = svd(disc).s.front();
+    }
+    const SvdResult full = svd(t);
+    out.sigma_r = full.s[(size_t)(rank - 1)];
+    out.sigma_r_plus_1 = rank < p ? full.s[(size_t)rank] : 0.0;
+    return out;
+}
+}  // namespace
+
+RankRevealDiag rank_reveal_diag(const UlvFactors& f, std::int64_t rank) { return reveal(f.l, rank, true); }
+RankRevealDiag rank_reveal_diag(const UrvFactors& f, std::int64_t rank) { return reveal(f.r, rank, false); }
 
 UlvFactors ulv(const Matrix& a, int refine) { return utv_call<UlvFactors>(a, refine, true); }
 UrvFactors urv(const Matrix& a, int refine) { return utv_call<UrvFactors>(a, refine, false); }

@@ -3,6 +3,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 
 #include "../../include/ttutv_b200.h"
@@ -512,6 +513,13 @@ ttg_status ttg_frobenius_norm(const double* a, int64_t count, int a_on_device, d
     });
 }
 
+ttg_status ttg_sum_squares(const double* a, int64_t count, int a_on_device, double* out) {
+    return guard([&] {
+        DeviceInput in(a, count, a_on_device != 0);
+        *out = count > 0 ? ttg::sum_squares(in.ptr, count) : 0.0;
+    });
+}
+
 ttg_status ttg_diff_norm(const double* x, const double* y, int64_t count, double* out) {
     return guard([&] {
         DeviceInput a(x, count, false), b(y, count, false);
@@ -540,6 +548,83 @@ ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, d
         const double denom = std::sqrt(ttg::sum_squares(t.ptr, count));
         if (denom == 0.0) ttg::argument_error("rse: truth has zero norm (domain error)");
         *out = std::sqrt(ttg::diff_squares(e.ptr, t.ptr, count)) / denom;
+    });
+}
+
+ttg_status ttg_mode_product(const double* x, const int64_t* dims, int d, int k, const double* m, int64_t m_rows,
+                            int64_t m_cols, double* out) {
+    return guard([&] {
+        if (k < 1 || k > d)
+            ttg::argument_error("mode " + std::to_string(k) + " out of range 1.." + std::to_string(d));
+        if (m_cols != dims[k - 1])
+            ttg::argument_error("mode-" + std::to_string(k) + " product needs " + std::to_string(dims[k - 1]) +
+                                " columns, matrix has " + std::to_string(m_cols));
+        int64_t left = 1, right = 1;
+        for (int q = 0; q < k - 1; ++q) left *= dims[q];
+        for (int q = k; q < d; ++q) right *= dims[q];
+        const int64_t mid = dims[k - 1], n_in = left * mid * right, n_out = left * m_rows * right;
+        ttg::DevBuf<double> X((size_t)std::max<int64_t>(n_in, 1)), M((size_t)std::max<int64_t>(m_rows * m_cols, 1)),
+            O((size_t)std::max<int64_t>(n_out, 1));
+        X.upload(x, (size_t)n_in);
+        M.upload(m, (size_t)(m_rows * m_cols));
+        ttg::mode_product_dev(X.get(), left, mid, right, M.get(), m_rows, O.get());
+        O.download(out, (size_t)n_out);
+        ttg::sync();
+    });
+}
+
+ttg_status ttg_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc, double* out) {
+    return guard([&] {
+        const int64_t na = ar * ac, nb = br * bc, n = na * nb;
+        ttg::DevBuf<double> A((size_t)std::max<int64_t>(na, 1)), B((size_t)std::max<int64_t>(nb, 1)),
+            O((size_t)std::max<int64_t>(n, 1));
+        A.upload(a, (size_t)na);
+        B.upload(b, (size_t)nb);
+        ttg::kron_dev(A.get(), ar, ac, B.get(), br, bc, O.get());
+        O.download(out, (size_t)n);
+        ttg::sync();
+    });
+}
+
+ttg_status ttg_psnr(const double* estimate, const double* truth, int64_t count, double* out) {
+    return guard([&] {
+        if (count < 1) ttg::argument_error("psnr: empty tensors");
+        DeviceInput e(estimate, count, false), t(truth, count, false);
+        const double max_val = ttg::max_value_dev(t.ptr, count);
+        const double mse = ttg::diff_squares(e.ptr, t.ptr, count) / (double)count;
+        *out = mse == 0.0 ? std::numeric_limits<double>::infinity() : 10.0 * std::log10(max_val * max_val / mse);
+    });
+}
+
+ttg_status ttg_reverse_indices(const double* a, const int64_t* dims, int d, double* out) {
+    return guard([&] {
+        const int64_t n = count_of(dims, d);
+        DeviceInput in(a, n, false);
+        ttg::DevBuf<double> O((size_t)std::max<int64_t>(n, 1));
+        ttg::reverse_indices_dev(in.ptr, std::vector<int64_t>(dims, dims + d), O.get());
+        O.download(out, (size_t)n);
+        ttg::sync();
+    });
+}
+
+ttg_status ttg_reverse_tt(const double* cores, const int64_t* dims, const int64_t* ranks, int d, double* out) {
+    return guard([&] {
+        int64_t total = 0;
+        for (int k = 0; k < d; ++k) total += ranks[k] * dims[k] * ranks[k + 1];
+        ttg::DevBuf<double> C((size_t)std::max<int64_t>(total, 1)), O((size_t)std::max<int64_t>(total, 1));
+        C.upload(cores, (size_t)total);
+        // core k of the result is core d-1-k flipped; the output is packed in the new order
+        int64_t off_out = 0;
+        for (int k = 0; k < d; ++k) {
+            const int src = d - 1 - k;
+            int64_t off_in = 0;
+            for (int q = 0; q < src; ++q) off_in += ranks[q] * dims[q] * ranks[q + 1];
+            const int64_t rl = ranks[src], mid = dims[src], rr = ranks[src + 1];
+            ttg::flip_core_dev(C.get() + off_in, rl, mid, rr, O.get() + off_out);
+            off_out += rl * mid * rr;
+        }
+        O.download(out, (size_t)total);
+        ttg::sync();
     });
 }
 

@@ -67,6 +67,14 @@ double residual_squared(const TTResult& r, const double* a);
 // ttg_completion_reset in include/ttutv_b200.h.
 void completion_reset(double* y, const double* observed, const double* mask, const double* truth, int64_t n,
                       double stats[5]);
+// Tensor algebra (tensor_ops.cu): mode_product / kron in the reference's operation order
+// (bitwise), the maximum of a buffer, reverse_indices, and a reversed train's core.
+void mode_product_dev(const double* x, int64_t left, int64_t mid, int64_t right, const double* m, int64_t new_mid,
+                      double* out);
+void kron_dev(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc, double* out);
+double max_value_dev(const double* x, int64_t n);
+void reverse_indices_dev(const double* a, const std::vector<int64_t>& dims, double* out);
+void flip_core_dev(const double* in, int64_t rl, int64_t mid, int64_t rr, double* out);
 // Dense reconstruction (device output of prod(dims) doubles).
 void reconstruct(const std::vector<const double*>& cores, const std::vector<int64_t>& dims,
                  const std::vector<int64_t>& ranks, double* out);

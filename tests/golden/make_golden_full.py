@@ -35,6 +35,10 @@ OUT = Path(__file__).resolve().parent
 # Appendix A's rescales {1, 3, 0.7} plus further neutral rescales: the ranks of the ulp-decided
 # 32-row cut are a function of rounding, so the set is sampled more densely than the survey did.
 CFG2_SCALES = [1.0, 3.0, 0.7, 0.9, 1.1, 1.3, 1.7, 2.3, 0.6, 5.0, 0.55, 1.9]
+# further neutral rescales sampled for cfg2x (merged into full_cfg2.npz)
+CFG2X_SCALES = [0.51, 0.53, 0.57, 0.59, 0.62, 0.65, 0.67, 0.73, 0.77, 0.8, 0.83, 0.87, 0.93, 0.97, 1.03, 1.07,
+                1.15, 1.2, 1.25, 1.35, 1.4, 1.45, 1.55, 1.6, 1.65, 1.75, 1.8, 1.85, 1.95, 2.1, 2.5, 2.7, 3.3,
+                3.7, 4.1, 4.5]
 
 
 def trace_arrays(prefix, res, cuts, out, keep_cores=True, sample_core=None):
@@ -118,6 +122,37 @@ def cfg2():
     np.savez_compressed(OUT / "full_cfg2.npz", **out)
 
 
+def cfg2x():
+    """More neutral rescales of config 2 at eps = 1e-8, appended to full_cfg2.npz (the keys of
+    the extra scales continue the e8_s<i> numbering)."""
+    dims = [32] * 5
+    base = shifted_hilbert(dims)
+    old = dict(np.load(OUT / "full_cfg2.npz"))
+    scales = [float(x) for x in old["scales"]]
+    summary = json.loads(str(old["summary_json"]))
+    out = dict(old)
+    for s in CFG2X_SCALES:
+        if s in scales:
+            continue
+        i = len(scales)
+        a = base * s
+        for method in ("ulv", "urv"):
+            t0 = time.time()
+            res, cuts = ref.sweep_trace(a, dims, method, eps=1e-8)
+            rse = ref.rse(res, a, dims, cap=10**9)
+            pre = f"e8_s{i}_{method}"
+            trace_arrays(pre, res, cuts, out)
+            out[f"{pre}_rse"] = np.float64(rse)
+            row = dict(eps=1e-8, scale=s, method=method, ranks=res.ranks_chosen, rse=rse,
+                       sec=round(time.time() - t0, 1))
+            summary.append(row)
+            print(json.dumps(row), flush=True)
+        scales.append(s)
+        out["scales"] = np.asarray(scales)
+        out["summary_json"] = np.asarray(json.dumps(summary))
+        np.savez_compressed(OUT / "full_cfg2.npz", **out)
+
+
 if __name__ == "__main__":
     for name in sys.argv[1:] or ["cfg3"]:
-        {"cfg2": cfg2, "cfg3": cfg3, "cfg5": cfg5}[name]()
+        {"cfg2": cfg2, "cfg2x": cfg2x, "cfg3": cfg3, "cfg5": cfg5}[name]()
