@@ -185,6 +185,42 @@ ttg_status ttg_result_reconstruct(const ttg_result* res, double* out, int out_on
 ttg_status ttg_completion_reset(double* y, const double* observed, const double* mask,
                                 const double* truth, int64_t n, double stats[5]);
 
+/* complete() / initial_guess() (include/ttutv/completion.hpp:73-81, completion.cpp:121-211) on
+ * the device: X_0 = Retract(P_Omega(M)), X_i = Retract(X_{i-1} + step_size P_Omega(M - X_{i-1})),
+ * with the reference's trace, 20-iteration divergence run and 5-iteration stop window. The
+ * fields mirror CompletionConfig (completion.hpp:40-55); extension: nranks == 0 with eps > 0
+ * retracts at the prescribed accuracy eps (rank-adaptive, equal rss weights), the retraction
+ * config 4 of BASELINE.json needs. `linear` holds the observations' 0-based linear indices
+ * (strictly increasing, like ObservationMask), `values` their values; with on_device the
+ * pointers (linear, values, truth) are device memory. truth may be NULL. */
+typedef struct ttg_completion_config {
+    const int64_t* ranks; /* target chain (r_0..r_d), or NULL with nranks = 0 (rank-adaptive) */
+    int nranks;
+    double eps;           /* rank-adaptive retraction tolerance (nranks == 0) */
+    int retraction;       /* TTG_METHOD_*; URV sweeps right to left, the others left to right */
+    double step_size;     /* default 1 */
+    int max_iters;        /* default 500 */
+    double stop_tol;      /* default 1e-6; 0 disables */
+    int refine_passes;    /* default 2 */
+    int64_t dense_cap;    /* default 1e7 */
+} ttg_completion_config;
+typedef struct ttg_completion ttg_completion; /* opaque */
+ttg_status ttg_complete(const int64_t* linear, const double* values, int64_t count, const int64_t* dims, int d,
+                        const ttg_completion_config* cfg, const double* truth, int on_device,
+                        ttg_completion** out);
+void ttg_completion_free(ttg_completion* c);
+int ttg_completion_iterations(const ttg_completion* c);
+int ttg_completion_status(const ttg_completion* c); /* 0 converged, 1 max_iters, 2 diverged */
+const char* ttg_completion_note(const ttg_completion* c);
+/* per iteration 1..n: observed RSE, full RSE and PSNR (only with truth: else untouched),
+ * cumulative wall ms; initial3 (nullable) = the initial guess's observed RSE, full RSE, PSNR */
+void ttg_completion_trace(const ttg_completion* c, double* rse_observed, double* rse_full, double* psnr,
+                          double* wall_time_ms, double* initial3);
+/* rank chain (d+1 entries) of iterate `iter` (0 = the initial guess); returns d+1 or 0 */
+int ttg_completion_ranks(const ttg_completion* c, int iter, int64_t* ranks);
+/* the final iterate's train (owned by the completion handle) */
+const ttg_result* ttg_completion_result(const ttg_completion* c);
+
 /* ---- multi-GPU: column-sharded sweeps (no reference analogue) --------
  * One process (or host thread) per GPU. A communicator is an NCCL communicator over the
  * ranks (NVLink / NVSwitch inside a B200 box), or a loopback group whose endpoints are

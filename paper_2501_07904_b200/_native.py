@@ -64,6 +64,15 @@ class Config(C.Structure):
     ]
 
 
+class CompletionConfig(C.Structure):
+    """ttg_completion_config (CompletionConfig, completion.hpp:40-55, plus eps)."""
+    _fields_ = [
+        ("ranks", c_int64_p), ("nranks", C.c_int), ("eps", C.c_double), ("retraction", C.c_int),
+        ("step_size", C.c_double), ("max_iters", C.c_int), ("stop_tol", C.c_double),
+        ("refine_passes", C.c_int), ("dense_cap", C.c_int64),
+    ]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "ttg_last_error": (C.c_char_p, []),
@@ -100,6 +109,15 @@ SIGNATURES = {
                                    c_double_p]),
     "ttg_kron": (C.c_int, [c_double_p, C.c_int64, C.c_int64, c_double_p, C.c_int64, C.c_int64, c_double_p]),
     "ttg_sum_squares": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, c_double_p]),
+    "ttg_complete": (C.c_int, [c_int64_p, c_double_p, C.c_int64, c_int64_p, C.c_int, C.c_void_p, c_double_p, C.c_int,
+                               C.POINTER(C.c_void_p)]),
+    "ttg_completion_free": (None, [C.c_void_p]),
+    "ttg_completion_iterations": (C.c_int, [C.c_void_p]),
+    "ttg_completion_status": (C.c_int, [C.c_void_p]),
+    "ttg_completion_note": (C.c_char_p, [C.c_void_p]),
+    "ttg_completion_trace": (None, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
+    "ttg_completion_ranks": (C.c_int, [C.c_void_p, C.c_int, c_int64_p]),
+    "ttg_completion_result": (C.c_void_p, [C.c_void_p]),
     "ttg_psnr": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
     "ttg_reverse_indices": (C.c_int, [c_double_p, c_int64_p, C.c_int, c_double_p]),
     "ttg_reverse_tt": (C.c_int, [c_double_p, c_int64_p, c_int64_p, C.c_int, c_double_p]),

@@ -7,12 +7,18 @@
 #include <string>
 
 #include "../../include/ttutv_b200.h"
+#include "completion.hpp"
 #include "io.hpp"
 #include "sweep.hpp"
 #include "utv.hpp"
 
 struct ttg_result {
     ttg::TTResult r;
+};
+
+struct ttg_completion {
+    ttg::CompletionRun run;
+    ttg_result res;
 };
 
 struct ttg_comm {
@@ -627,5 +633,74 @@ ttg_status ttg_reverse_tt(const double* cores, const int64_t* dims, const int64_
         ttg::sync();
     });
 }
+
+ttg_status ttg_complete(const int64_t* linear, const double* values, int64_t count, const int64_t* dims, int d,
+                        const ttg_completion_config* cfg, const double* truth, int on_device, ttg_completion** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (d < 1) ttg::argument_error("shape needs at least one mode");
+        ttg::CompletionSpec spec;
+        if (cfg->nranks > 0) spec.ranks.assign(cfg->ranks, cfg->ranks + cfg->nranks);
+        spec.adaptive = cfg->nranks == 0;
+        spec.eps = cfg->eps;
+        spec.retraction = cfg->retraction;
+        spec.step_size = cfg->step_size;
+        spec.max_iters = cfg->max_iters;
+        spec.stop_tol = cfg->stop_tol;
+        spec.refine_passes = cfg->refine_passes;
+        spec.dense_cap = cfg->dense_cap;
+        const int64_t n = count_of(dims, d);
+        ttg::DevBuf<int64_t> L;
+        const int64_t* lp = linear;
+        if (!on_device) {
+            for (int64_t i = 0; i < count; ++i)
+                if (linear[i] < 0 || linear[i] >= n || (i > 0 && linear[i] <= linear[i - 1]))
+                    ttg::argument_error("observation indices must be 0-based, in range and strictly increasing");
+            L.alloc((size_t)std::max<int64_t>(count, 1));
+            L.upload(linear, (size_t)count);
+            lp = L.get();
+        }
+        DeviceInput V(values, count, on_device != 0);
+        ttg::DevBuf<double> T;
+        const double* tp = truth;
+        if (truth && !on_device) {
+            T.alloc((size_t)n);
+            T.upload(truth, (size_t)n);
+            tp = T.get();
+        }
+        auto* c = new ttg_completion{ttg::complete(lp, V.ptr, count, std::vector<int64_t>(dims, dims + d), spec, tp), {}};
+        c->res.r = std::move(c->run.tt);
+        c->res.r.dims.assign(dims, dims + d);
+        *out = c;
+    });
+}
+
+void ttg_completion_free(ttg_completion* c) { delete c; }
+int ttg_completion_iterations(const ttg_completion* c) { return (int)c->run.rse_observed.size(); }
+int ttg_completion_status(const ttg_completion* c) { return c->run.status; }
+const char* ttg_completion_note(const ttg_completion* c) { return c->run.note.c_str(); }
+
+void ttg_completion_trace(const ttg_completion* c, double* rse_observed, double* rse_full, double* psnr,
+                          double* wall_time_ms, double* initial3) {
+    const auto& r = c->run;
+    if (rse_observed) std::copy(r.rse_observed.begin(), r.rse_observed.end(), rse_observed);
+    if (rse_full) std::copy(r.rse_full.begin(), r.rse_full.end(), rse_full);
+    if (psnr) std::copy(r.psnr.begin(), r.psnr.end(), psnr);
+    if (wall_time_ms) std::copy(r.wall_ms.begin(), r.wall_ms.end(), wall_time_ms);
+    if (initial3) {
+        initial3[0] = r.initial_obs.empty() ? 0.0 : r.initial_obs[0];
+        initial3[1] = r.initial_full.empty() ? 0.0 : r.initial_full[0];
+        initial3[2] = r.initial_psnr.empty() ? 0.0 : r.initial_psnr[0];
+    }
+}
+
+int ttg_completion_ranks(const ttg_completion* c, int iter, int64_t* ranks) {
+    if (iter < 0 || (size_t)iter >= c->run.ranks.size()) return 0;
+    const auto& r = c->run.ranks[(size_t)iter];
+    std::copy(r.begin(), r.end(), ranks);
+    return (int)r.size();
+}
+
+const ttg_result* ttg_completion_result(const ttg_completion* c) { return &c->res; }
 
 }  // extern "C"

@@ -72,6 +72,9 @@ bool prof_enabled();
 void prof_enable(bool on);
 void prof_begin();
 void prof_end(double algorithmic_bytes, const char* kernel);
+// prof_end for a launch whose work is chosen on the device: the int at `dflag` (read after
+// the launch, stream-ordered) selects kernel1/bytes1 (non-zero) or kernel0/bytes0 (zero).
+void prof_end_select(const int* dflag, double bytes1, const char* kernel1, double bytes0, const char* kernel0);
 // Drains the recorded events (host sync). Returns launches; total device ms and bytes.
 // The drained records also accumulate into per-kernel totals (prof_kernels).
 int64_t prof_read(double* total_ms, double* bytes);

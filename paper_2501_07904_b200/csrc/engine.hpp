@@ -92,6 +92,8 @@ private:
     void explicit_step(int64_t t);
     void to_explicit(int64_t t);
     void gemv_step(int64_t t);
+    void guard_step(int64_t t);
+    void sub_step(int64_t t);
     double* qptr() { return explicit_ ? Qx_.get() : Qt_.get(); }
 
     const double* W_;
@@ -109,6 +111,11 @@ private:
     DevBuf<double> Wt_;  // row-layout copy of a narrow Col W for k_pass1_big<5>
     bool big_ = false;           // ... with the large-W stream variants (k_pass1_big)
     bool coop_ = false;          // persistent cooperative step loop (small / medium W)
+    // subspace (lazy-exact) pivoting: R rows from Z = E^T W while q_t stays in span(E)
+    bool sub_ = false;
+    int subc_ = 8;  // predicted directions (basis size cap)
+    DevBuf<double> E_, a_, Z_;
+    DevBuf<int> subi_;  // [0] basis size nE, [1] hit flag of the current step
     DevBuf<int> nflag2_;
     bool coop_run(int64_t steps);
     DevBuf<int64_t> pos_, perm_, piv_, flags_;

@@ -2412,6 +2412,333 @@ __global__ void __launch_bounds__(kThreads) k_resnorm(const double* __restrict__
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// ---------------------------------------------------------------------------
+// Subspace (lazy-exact) pivoting for wide W with many rows (k >= 128).
+//
+// A pass-1 step needs row t of R, R(t, j) = q_t^T w_j for every unpivoted column, to
+// downdate the norms that pick the next pivot -- one HBM pass over W per step (BLAS-2).
+// When q_t lies in a small known subspace span(E) (E: k x c, orthonormal), q_t = E a with
+// a = E^T q_t, and R(t, j) = a^T z_j with z_j = E^T w_j: the step reads Z = E^T W (c
+// doubles per column) instead of W (k doubles per column). q_t is the normalised residual
+// of the pivot column against Q[:, :t], so it lies in span(E) whenever E spans the residuals
+// of a set of columns that contains the pivot. Every miss step (q_t outside span(E)) streams
+// W anyway; it then also predicts: E becomes the orthonormalised residuals of the next
+// kSubC best candidates, and the same pass over W computes Z = E^T W. Every step's argmax
+// runs over the exact downdated norms of ALL columns (no stale bounds), so the pivots are
+// the ones the per-step stream picks; only the source of R(t, j) differs, by rounding.
+// ---------------------------------------------------------------------------
+constexpr int kSubCMax = 16;   // candidate directions per prediction: 8 or 16 (chosen per cut)
+constexpr int kSubMaxK = 2048;  // E (k x C) and the gathered candidates fit in shared memory
+
+// One CTA of 1024 threads. In: q_t = Q[:, t], E/nE from the last prediction, the candidate
+// slots of step t. Out: hit (q_t in span(E) to `tol`) with a = E^T q_t, or a new E / nE from
+// up to C candidates.
+template <int C>
+__global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W, int64_t k, int64_t ld, int layout,
+                                                   const double* __restrict__ Q, int64_t t,
+                                                   const Cand* __restrict__ cand, int ncand,
+                                                   const int64_t* __restrict__ piv, double* E, double* a, int* nE,
+                                                   int* hit, double tol) {
+    extern __shared__ double sm[];
+    double* q = sm;                  // k
+    double* X = sm + k;              // k x C (candidate residuals / new basis)
+    __shared__ double red[32];
+    __shared__ double coef[C + 1];
+    __shared__ double dots[C * 80];  // CGS coefficients D[l * C + c] for a slice of l
+    __shared__ int64_t cols[C];
+    __shared__ int ncols, acc;
+    __shared__ Cand sc[32];
+    constexpr int64_t kSlice = 80;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t i = tid; i < k; i += nt) q[i] = Q[i + t * k];
+    __syncthreads();
+    const int n0 = *nE;
+    if (n0 > 0) {
+        // a = E^T q: one warp per coefficient
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp < n0) {
+            double s = 0.0;
+            for (int64_t i = lane; i < k; i += 32) s = fma(E[i + warp * k], q[i], s);
+            s = warp_sum(s);
+            if (lane == 0) coef[warp] = s;
+        }
+        __syncthreads();
+        double r2 = 0.0;
+        for (int64_t i = tid; i < k; i += nt) {
+            double r = q[i];
+            for (int c = 0; c < n0; ++c) r = fma(-E[i + c * k], coef[c], r);
+            r2 = fma(r, r, r2);
+        }
+        r2 = block_sum(r2, red);
+        if (r2 <= tol * tol) {
+            if (tid < n0) a[tid] = coef[tid];
+            if (tid == 0) *hit = 1;
+            return;
+        }
+    }
+    // ---- miss: predict the next pivots ------------------------------------------------
+    if (tid == 0) { *hit = 0; ncols = 0; }
+    __syncthreads();
+    const int64_t jp = piv[t];
+    for (int r = 0; r < C; ++r) {
+        Cand best = cand_none();
+        for (int i = tid; i < ncand; i += nt) {
+            const Cand c = cand[i];
+            if (c.col < 0 || c.col == jp) continue;
+            bool taken = false;
+            for (int u = 0; u < ncols; ++u) taken |= cols[u] == c.col;
+            if (!taken && better(c, best)) best = c;
+        }
+        best = block_best(best, sc);
+        if (tid == 0 && best.col >= 0) cols[ncols++] = best.col;
+        __syncthreads();
+        if (best.col < 0) break;
+    }
+    const int m = ncols;
+    for (int64_t e = tid; e < k * m; e += nt) {
+        const int c = (int)(e / k);
+        const int64_t i = e - (int64_t)c * k;
+        X[i + c * k] = layout == 0 ? W[i + cols[c] * ld] : W[i * ld + cols[c]];
+    }
+    __syncthreads();
+    // residuals against Q[:, :t+1]: classical Gram-Schmidt, twice, in slices of columns
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int64_t l0 = 0; l0 <= t; l0 += kSlice) {
+            const int64_t l1 = min(t + 1, l0 + kSlice);
+            for (int64_t e = warp; e < (l1 - l0) * m; e += nw) {
+                const int64_t l = l0 + e / m;
+                const int c = (int)(e % m);
+                double s = 0.0;
+                for (int64_t i = lane; i < k; i += 32) s = fma(Q[i + l * k], X[i + c * k], s);
+                s = warp_sum(s);
+                if (lane == 0) dots[(l - l0) * C + c] = s;
+            }
+            __syncthreads();
+            for (int64_t i = tid; i < k; i += nt) {
+                double x[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) x[c] = c < m ? X[i + c * k] : 0.0;
+                for (int64_t l = l0; l < l1; ++l) {
+                    const double ql = Q[i + l * k];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) x[c] = fma(-ql, dots[(l - l0) * C + c], x[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (c < m) X[i + c * k] = x[c];
+            }
+            __syncthreads();
+        }
+    }
+    // modified Gram-Schmidt with reorthogonalisation among the candidates; a candidate whose
+    // residual is (numerically) in the span of the earlier ones is dropped
+    if (tid == 0) acc = 0;
+    __syncthreads();
+    for (int c = 0; c < m; ++c) {
+        double n0s = 0.0;
+        for (int64_t i = tid; i < k; i += nt) n0s = fma(X[i + c * k], X[i + c * k], n0s);
+        n0s = block_sum(n0s, red);
+        const int na = acc;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int e = 0; e < na; ++e) {
+                double s = 0.0;
+                for (int64_t i = tid; i < k; i += nt) s = fma(X[i + e * k], X[i + c * k], s);
+                s = block_sum(s, red);
+                for (int64_t i = tid; i < k; i += nt) X[i + c * k] = fma(-s, X[i + e * k], X[i + c * k]);
+                __syncthreads();
+            }
+        double ns = 0.0;
+        for (int64_t i = tid; i < k; i += nt) ns = fma(X[i + c * k], X[i + c * k], ns);
+        ns = block_sum(ns, red);
+        if (ns > 1e-12 * n0s && ns > 0.0) {
+            const double inv = 1.0 / sqrt(ns);
+            for (int64_t i = tid; i < k; i += nt) X[i + na * k] = X[i + c * k] * inv;
+            __syncthreads();
+            if (tid == 0) acc = na + 1;
+        }
+        __syncthreads();
+    }
+    const int n1 = acc;
+    for (int64_t e = tid; e < k * n1; e += nt) E[e] = X[e];
+    if (tid == 0) *nE = n1;
+}
+
+// Shared epilogue of the subspace streams for one column: R(t, j) and the norm downdate.
+__device__ __forceinline__ bool sub_epilogue(int64_t t, int64_t j, int64_t N, int64_t jp, double r,
+                                             const double* diag, double* R, double* nu, const double* cref,
+                                             const int64_t* pos, Cand& best, double& msum) {
+    const int64_t pj = pos[j];
+    if (pj < t || j == jp) {
+        R[t * N + j] = j == jp ? diag[t] : 0.0;
+        return false;
+    }
+    return downdate(t, j, N, r, pj, R, nu, cref, best, msum);
+}
+
+// Row t of R for one step in subspace mode (grid-stride over columns; `hit` chosen on the
+// device by k_sub_prep). hit: R(t, j) = a^T z_j from Z (nE x N, row c at Z + c N).
+// miss: one pass over W computing R(t, j) = q_t^T w_j and the new Z = E^T w_j.
+// LAYOUT 1 (Row): a thread owns two adjacent columns (16-byte loads when `pair16`), q and
+//   E broadcast from shared memory;
+// LAYOUT 0 (Col, k >= 64): a warp owns four (C = 8) or two (C = 16) columns, lanes over rows
+//   (each lane's rows of q and E are read from shared memory once for all of them), then warp
+//   trees.
+template <int LAYOUT, int C>
+__global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_sub_stream(const double* __restrict__ W, int64_t k, int64_t N,
+                                                            int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                            const double* __restrict__ E,
+                                                            const double* __restrict__ a,
+                                                            const int* __restrict__ nE_p,
+                                                            const int* __restrict__ hit_p, double* Z, int pair16,
+                                                            const double* diag, const int64_t* piv, double* R,
+                                                            double* nu, const double* cref, const int64_t* pos,
+                                                            int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    extern __shared__ double sm[];  // miss: q (kp) then E column-major (er[c * kp + i]), kp = k rounded up to even
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    const int hit = *hit_p, nE = *nE_p;
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (hit) {
+        double av[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) av[c] = c < nE ? a[c] : 0.0;
+        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
+            const int64_t j = j0 + threadIdx.x;
+            bool fl = false;
+            if (j < N) {
+                double r = 0.0;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (c < nE) r = fma(av[c], Z[c * N + j], r);
+                fl = sub_epilogue(t, j, N, jp, r, diag, R, nu, cref, pos, best, msum);
+            }
+            append_flag(fl, j, flags, nflag);
+        }
+    } else {
+        const int64_t kp = (k + 1) & ~int64_t(1);
+        double* q = sm;
+        double* er = sm + kp;
+        for (int64_t i = threadIdx.x; i < k; i += kThreads) q[i] = Q[i + t * k];
+        for (int64_t e = threadIdx.x; e < kp * C; e += kThreads) {
+            const int c = (int)(e / kp);
+            const int64_t i = e - (int64_t)c * kp;
+            er[e] = (c < nE && i < k) ? E[i + c * k] : 0.0;
+        }
+        __syncthreads();
+        if (LAYOUT == 1) {
+            const int64_t npair = (N + 1) / 2;
+            for (int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;; g += (int64_t)gridDim.x * kThreads) {
+                const bool act = g < npair;
+                if (!__any_sync(0xffffffffu, act)) break;
+                double r0 = 0.0, r1 = 0.0, z0[C], z1[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) z0[c] = z1[c] = 0.0;
+                const int64_t j = 2 * g;
+                const bool two = act && j + 1 < N;
+                if (act) {
+                    if (pair16 && two) {
+                        const double2* w2 = reinterpret_cast<const double2*>(W) + g;
+                        const int64_t ld2 = ld / 2;
+#pragma unroll 4
+                        for (int64_t i = 0; i < k; ++i) {
+                            const double2 x = __ldg(w2 + i * ld2);
+                            const double qi = q[i];
+                            r0 = fma(qi, x.x, r0);
+                            r1 = fma(qi, x.y, r1);
+#pragma unroll
+                            for (int c = 0; c < C; ++c) {
+                                const double ec = er[c * kp + i];
+                                z0[c] = fma(ec, x.x, z0[c]);
+                                z1[c] = fma(ec, x.y, z1[c]);
+                            }
+                        }
+                    } else {
+                        for (int64_t i = 0; i < k; ++i) {
+                            const double x0 = W[i * ld + j], x1 = two ? W[i * ld + j + 1] : 0.0;
+                            const double qi = q[i];
+                            r0 = fma(qi, x0, r0);
+                            r1 = fma(qi, x1, r1);
+#pragma unroll
+                            for (int c = 0; c < C; ++c) {
+                                const double ec = er[c * kp + i];
+                                z0[c] = fma(ec, x0, z0[c]);
+                                z1[c] = fma(ec, x1, z1[c]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        if (c < nE) {
+                            Z[c * N + j] = z0[c];
+                            if (two) Z[c * N + j + 1] = z1[c];
+                        }
+                }
+                const bool f0 = act && sub_epilogue(t, j, N, jp, r0, diag, R, nu, cref, pos, best, msum);
+                append_flag(f0, j, flags, nflag);
+                const bool f1 = two && sub_epilogue(t, j + 1, N, jp, r1, diag, R, nu, cref, pos, best, msum);
+                append_flag(f1, j + 1, flags, nflag);
+            }
+        } else {
+            constexpr int CW = C == 16 ? 2 : 4;  // columns per warp
+            const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+            const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+            for (int64_t j0 = gw * CW; j0 < N; j0 += nwarps * CW) {
+                double r[CW], z[CW][C];
+#pragma unroll
+                for (int u = 0; u < CW; ++u) {
+                    r[u] = 0.0;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) z[u][c] = 0.0;
+                }
+                const double* w[CW];
+#pragma unroll
+                for (int u = 0; u < CW; ++u) w[u] = W + min(j0 + u, N - 1) * ld;
+                for (int64_t i = lane; i < k; i += 32) {
+                    double x[CW];
+#pragma unroll
+                    for (int u = 0; u < CW; ++u) x[u] = w[u][i];
+                    const double qi = q[i];
+#pragma unroll
+                    for (int u = 0; u < CW; ++u) r[u] = fma(qi, x[u], r[u]);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const double ec = er[c * kp + i];
+#pragma unroll
+                        for (int u = 0; u < CW; ++u) z[u][c] = fma(ec, x[u], z[u][c]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < CW; ++u) {
+                    r[u] = warp_sum(r[u]);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) z[u][c] = warp_sum(z[u][c]);
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < CW; ++u) {
+                        const int64_t j = j0 + u;
+                        if (j >= N) break;
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            if (c < nE) Z[c * N + j] = z[u][c];
+                        if (sub_epilogue(t, j, N, jp, r[u], diag, R, nu, cref, pos, best, msum)) {
+                            const int slot = atomicAdd(nflag, 1);
+                            flags[slot] = j;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 }  // namespace
 
 // Phase totals of the persistent loop (ms) per variant since the last reset (host sync).
@@ -2487,9 +2814,20 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     const int64_t want = mode_ == 1 ? cdiv(N, kThreads / 32) : mode_ == 3 ? cdiv(N, 32) : mode_ == 7 ? cdiv(N, 128) : mode_ == 2 ? cdiv(N, 32 * (kThreads / 32)) : mode_ == 6 ? cdiv(N, 4 * kThreads) : cdiv(N, kThreads);
     ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
     if (mode_ == 5) ncand_ = (int)std::max<int64_t>(1, std::min<int64_t>(N / kTmaCols, sms));  // persistent
+    // Subspace (lazy-exact) pivoting for wide W with many rows: most steps read Z = E^T W
+    // (kSubC doubles per column) instead of W (k doubles per column). TTG_SUBSPACE=0 turns
+    // it off (A/B measurements; same pivots either way).
+    {
+        static const bool no_sub = [] {
+            const char* e = std::getenv("TTG_SUBSPACE");
+            return e && *e == '0';
+        }();
+        sub_ = !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
+               (layout == Layout::Row || ld >= k);
+    }
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
     // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps
-    {
+    if (!sub_) {
         static const bool no_coop = [] {
             const char* e = std::getenv("TTG_NO_COOP");
             return e && *e == '1';
@@ -2534,6 +2872,19 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         }
     }
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
+    if (sub_) {
+        // 16 predicted directions for long rows (the miss pass has FMA headroom there), 8 otherwise
+        static const int env_c = [] {  // experiment: TTG_SUBSPACE_C = 8 or 16
+            const char* e = std::getenv("TTG_SUBSPACE_C");
+            return e ? std::atoi(e) : 0;
+        }();
+        subc_ = env_c == 8 || env_c == 16 ? env_c : (k >= 512 ? 16 : 8);
+        E_.alloc((size_t)(k * subc_));
+        a_.alloc(subc_);
+        Z_.alloc((size_t)(subc_ * N));
+        subi_.alloc(2);
+        subi_.zero();
+    }
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(Ng_); flags_.alloc(N);
     if (comm_) {
         rec_.alloc((size_t)(k + kRecHead));
@@ -2745,8 +3096,44 @@ void WideQrcp::step() {
         if (explicit_) explicit_step(t);
         else reflect_step(t);
     }
-    gemv_step(t);
+    if (sub_) sub_step(t);
+    else gemv_step(t);
     steps_ = t + 1;
+}
+
+// One step of the subspace engine after the reflector: k_sub_prep decides on the device
+// whether q_t lies in span(E) (and otherwise predicts the next pivots' subspace), then one
+// stream launch produces row t of R from Z (hit) or from W while refreshing Z (miss).
+void WideQrcp::sub_step(int64_t t) {
+    const int C = subc_;
+    {
+        PhaseTimer pt("p1 subspace prep");
+        const size_t psm = sizeof(double) * (size_t)(k_ + k_ * C);
+        auto prep = C == 16 ? k_sub_prep<16> : k_sub_prep<8>;
+        allow_smem(prep, psm);
+        TTG_LAUNCH(prep, 1, 1024, psm, stream(), W_, k_, ld_, (int)layout_, qptr(), t, cand_.get(), ncand_ + ngc_,
+                   piv_.get(), E_.get(), a_.get(), subi_.get(), subi_.get() + 1, 1e-12);
+    }
+    {
+        PhaseTimer pt("p1 subspace stream");
+        prof_begin();
+        const int64_t kp = (k_ + 1) & ~int64_t(1);
+        const size_t ssm = sizeof(double) * (size_t)(kp * (1 + C));
+        auto kern = layout_ == Layout::Row ? (C == 16 ? k_sub_stream<1, 16> : k_sub_stream<1, 8>)
+                                           : (C == 16 ? k_sub_stream<0, 16> : k_sub_stream<0, 8>);
+        allow_smem(kern, ssm);
+        const int pair16 = ((reinterpret_cast<uintptr_t>(W_) & 15) == 0 && ld_ % 2 == 0) ? 1 : 0;
+        TTG_LAUNCH(kern, ncand_, kThreads, ssm, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), a_.get(),
+                   subi_.get(), subi_.get() + 1, Z_.get(), pair16, diag_.get(), piv_.get(), R_.get(), nu_.get(),
+                   cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+        // algorithmic bytes: hit -- Z's C rows of the unpivoted columns, the norms read and
+        // written, row t of R; miss -- W's k rows instead, plus writing Z
+        prof_end_select(subi_.get() + 1, 8.0 * (double)(N_ - t) * (double)(C + 2) + 8.0 * (double)N_,
+                        "k_sub_stream hit (R row from Z = E^T W)",
+                        8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_ * (1.0 + C),
+                        "k_sub_stream miss (W pass: R row and Z = E^T W)");
+    }
+    guard_step(t);
 }
 
 void WideQrcp::to_explicit(int64_t t) {
@@ -2870,6 +3257,10 @@ void WideQrcp::gemv_step(int64_t t) {
                                          "k_stream_row2 (row, 16-byte paired columns)",
                                          "k_stream_splitk4 (row, 128-column strips)"};
     prof_end(8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_, kNames[mode_]);
+    guard_step(t);
+}
+
+void WideQrcp::guard_step(int64_t t) {
     // guard recompute of the flagged norms; its candidates / masses go to the slots after
     // the stream kernel's
     static const bool no_guard = [] {  // diagnostics only: skip the recompute (wrong results)

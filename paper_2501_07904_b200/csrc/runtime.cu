@@ -65,7 +65,22 @@ struct Prof {
         cudaEvent_t a, b;
         double bytes;
         int kind;
+        // kind chosen on the device: flag (pinned host copy) != 0 -> kind/bytes, else alt
+        int* flag = nullptr;
+        double alt_bytes = 0.0;
+        int alt_kind = -1;
     };
+    std::vector<int*> flag_pool;  // pinned host ints for device-selected records
+    int* get_flag() {
+        if (flag_pool.empty()) {
+            int* blk = nullptr;
+            TTG_CUDA(cudaMallocHost(&blk, sizeof(int) * 256));
+            for (int i = 0; i < 256; ++i) flag_pool.push_back(blk + i);
+        }
+        int* f = flag_pool.back();
+        flag_pool.pop_back();
+        return f;
+    }
     std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
     cudaEvent_t open = nullptr;
@@ -113,10 +128,31 @@ void prof_end(double algorithmic_bytes, const char* kernel) {
     t_prof.open = nullptr;
 }
 
+void prof_end_select(const int* dflag, double bytes1, const char* kernel1, double bytes0, const char* kernel0) {
+    if (!t_prof.on || !t_prof.open) return;
+    int* f = t_prof.get_flag();
+    TTG_CUDA(cudaMemcpyAsync(f, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    cudaEvent_t e = t_prof.get();
+    TTG_CUDA(cudaEventRecord(e, stream()));
+    Prof::Rec r{t_prof.open, e, bytes1, t_prof.kind_of(kernel1)};
+    r.flag = f;
+    r.alt_bytes = bytes0;
+    r.alt_kind = t_prof.kind_of(kernel0);
+    t_prof.pending.push_back(r);
+    t_prof.open = nullptr;
+}
+
 int64_t prof_read(double* total_ms, double* bytes) {
     double ms = 0.0, by = 0.0;
     for (auto& r : t_prof.pending) {
         TTG_CUDA(cudaEventSynchronize(r.b));
+        if (r.flag) {
+            if (*r.flag == 0) {
+                r.bytes = r.alt_bytes;
+                r.kind = r.alt_kind;
+            }
+            t_prof.flag_pool.push_back(r.flag);
+        }
         float x = 0.f;
         TTG_CUDA(cudaEventElapsedTime(&x, r.a, r.b));
         ms += x;

@@ -378,3 +378,17 @@ def test_wide_near_full_rank_cut_in_place_warp_steps(dev, ref):
     rr = ref.decompose(a, dims, "ulv", "l2r", eps=1e-3)
     assert rep.ranks_chosen == rr.ranks_chosen
     assert abs(res.rse(a) - ref.rse(rr, a, dims)) <= TOL_RSE
+
+
+# 160 x 240 x 240: the ULV first unfolding is 160 x 57,600 (Col) and the URV one has
+# W = c^T = 240 x 38,400 (Row): both run the subspace (lazy-exact) pivoting engine (k >= 128,
+# N >= 32768), whose steps take R rows from Z = E^T W while q_t stays in span(E)
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+@pytest.mark.parametrize("mode", ["rank", "tol"])
+def test_subspace_engine_cuts(dev, ref, method, mode):
+    dims, ranks = [160, 240, 240], [1, 12, 12, 1]
+    a = planted_plus_noise(ref, dims, ranks, 21, 1e-6)
+    if mode == "rank":
+        _check_parity(dev, ref, a, dims, method, ranks=ranks)
+    else:
+        _check_parity(dev, ref, a, dims, method, eps=1e-5)
