@@ -291,6 +291,57 @@ DecompResult decompose(const DenseTensor& a, const DecompConfig& config);
 double verify_bound(const DenseTensor& a, const TTTensor& tt, DecompReport& report, double slack_rel = 1e-8,
                     std::int64_t element_cap = 100'000'000);
 
+// ---- completion (completion.hpp) ----------------------------------------------------------
+class ObservationMask {
+public:
+    ObservationMask() = default;
+    ObservationMask(const Shape& shape, const std::vector<std::vector<std::int64_t>>& indices,
+                    const std::vector<double>& values);
+    ObservationMask(const DenseTensor& indicator, const DenseTensor& values);
+    const Shape& shape() const noexcept { return shape_; }
+    std::int64_t count() const noexcept { return (std::int64_t)linear_.size(); }
+    const std::vector<std::int64_t>& linear_indices() const noexcept { return linear_; }
+    const std::vector<double>& values() const noexcept { return values_; }
+    double values_norm() const;
+private:
+    Shape shape_;
+    std::vector<std::int64_t> linear_;
+    std::vector<double> values_;
+};
+DenseTensor project_observed(const DenseTensor& tensor, const ObservationMask& mask);
+
+struct CompletionConfig {
+    std::vector<std::int64_t> ranks;
+    Method retraction = Method::svd;
+    double step_size = 1.0;
+    int max_iters = 500;
+    double stop_tol = 1e-6;
+    std::uint64_t seed = 42;
+    int refine_passes = 2;
+    std::int64_t dense_cap = 10'000'000;
+    // Extension (BASELINE config 4): > 0 retracts at this prescribed accuracy (FixedTol, equal
+    // rss weights) instead of the fixed-rank chain, which may then be empty.
+    double retraction_eps = 0.0;
+};
+enum class CompletionStatus { converged, max_iters, diverged };
+struct IterationTrace {
+    std::vector<double> rse_observed;
+    std::vector<double> rse_full;
+    std::vector<double> psnr;
+    std::vector<double> wall_time_ms;
+    CompletionStatus status = CompletionStatus::max_iters;
+    std::string note;
+    // Extension: the rank chain of every iterate, [0] = the initial guess.
+    std::vector<std::vector<std::int64_t>> ranks;
+};
+struct CompletionResult {
+    TTTensor tt;
+    IterationTrace trace;
+};
+CompletionResult complete(const ObservationMask& mask, const Shape& shape, const CompletionConfig& config,
+                          const DenseTensor* truth = nullptr);
+TTTensor initial_guess(const ObservationMask& mask, const Shape& shape, const CompletionConfig& config);
+
 // ---- engine controls beyond the reference API ---------------------------------------------
 namespace gpu {
 // QLP policy for every subsequent sweep on this thread: false = early exit (default),

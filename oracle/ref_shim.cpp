@@ -18,9 +18,11 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
+#include "ttutv/completion.hpp"
 #include "ttutv/io.hpp"
 #include "ttutv/errors.hpp"
 #include "ttutv/factor.hpp"
@@ -391,6 +393,52 @@ int ref_rank_reveal_diag(const double* u, const double* t, const double* v, int6
         out4[1] = dg.residual_spectral_norm;
         out4[2] = dg.sigma_r;
         out4[3] = dg.sigma_r_plus_1;
+    });
+}
+
+}  // extern "C"
+
+// ---- completion (completion.hpp) ------------------------------------------------------
+extern "C" {
+
+int ref_gen_mask(const int64_t* dims, int d, double fraction, uint64_t seed, double* out) {
+    return guarded([&] {
+        ttutv::DenseTensor m = ttutv::gen_mask(shape_of(dims, d), fraction, seed);
+        std::memcpy(out, m.data(), sizeof(double) * (size_t)m.element_count());
+    });
+}
+
+// complete() with the mask given as 0/1 indicator + values (dense), fixed ranks; the trace
+// arrays hold max_iters entries; returns via n_out / status_out; cores of the final train
+// packed into cores_out (nullable) in core order.
+int ref_complete(const double* indicator, const double* values, const int64_t* dims, int d, const int64_t* ranks,
+                 int retraction, double step, int max_iters, double stop_tol, int refine, const double* truth,
+                 double* obs, double* full, double* ps, int* n_out, int* status_out, double* cores_out) {
+    return guarded([&] {
+        ttutv::ObservationMask mask(tensor_of(indicator, dims, d), tensor_of(values, dims, d));
+        ttutv::CompletionConfig cfg;
+        cfg.ranks.assign(ranks, ranks + d + 1);
+        cfg.retraction = static_cast<ttutv::Method>(retraction);
+        cfg.step_size = step;
+        cfg.max_iters = max_iters;
+        cfg.stop_tol = stop_tol;
+        cfg.refine_passes = refine;
+        std::unique_ptr<ttutv::DenseTensor> tr;
+        if (truth) tr = std::make_unique<ttutv::DenseTensor>(tensor_of(truth, dims, d));
+        ttutv::CompletionResult r = ttutv::complete(mask, shape_of(dims, d), cfg, tr.get());
+        const auto& t = r.trace;
+        *n_out = (int)t.rse_observed.size();
+        *status_out = (int)t.status;
+        std::copy(t.rse_observed.begin(), t.rse_observed.end(), obs);
+        if (truth) {
+            std::copy(t.rse_full.begin(), t.rse_full.end(), full);
+            std::copy(t.psnr.begin(), t.psnr.end(), ps);
+        }
+        if (cores_out)
+            for (const auto& c : r.tt.cores()) {
+                std::memcpy(cores_out, c.data.data(), sizeof(double) * (size_t)c.data.element_count());
+                cores_out += c.data.element_count();
+            }
     });
 }
 

@@ -74,6 +74,8 @@ class DeviceResult:
         self.h = handle
 
     def __del__(self):
+        if getattr(self, "_borrowed", False):
+            return
         if getattr(self, "h", None):
             try:
                 lib().ttg_result_free(self.h)
@@ -331,45 +333,97 @@ def left_orthogonal_via_urv(a, dims=None, ranks=None, eps=None, weights=(), refi
     return decompose(a, dims, "urv", "l2r", ranks=ranks, eps=eps, weights=weights, refine_passes=refine_passes, **kw)
 
 
-# ---- completion with a rank-adaptive retraction (BASELINE config 4) -------------------
+# ---- completion (completion.hpp; BASELINE config 4) ---------------------------------------
 @dataclass
 class CompletionTrace:
-    """Per-iteration trace like IterationTrace (completion.hpp:57-64) plus ranks."""
+    """IterationTrace (completion.hpp:57-64) plus the rank chain of every iterate
+    (ranks[0] = the initial guess) and the initial guess's own errors."""
     ranks: list = field(default_factory=list)
     rse_observed: list = field(default_factory=list)
     rse_full: list = field(default_factory=list)
     psnr: list = field(default_factory=list)
     wall_time_ms: list = field(default_factory=list)
+    status: str = "max_iters"
+    note: str = ""
+    initial: dict = field(default_factory=dict)
 
 
-def complete_tol(y_ptr: int, observed_ptr: int, mask_ptr: int, dims, eps: float, iters: int,
-                 truth_ptr: int = 0, method: str = "urv", sweep: str = "r2l") -> CompletionTrace:
-    """Projected iteration Y <- P_Omega(M) + P_Omega^c(Retract_eps(Y)) on device buffers.
+class Completion:
+    """Owning handle of a ttg_completion: the trace and the final train (on the device)."""
 
-    The reference's complete() (completion.cpp:131-211) retracts at fixed ranks with a
-    step size; BASELINE config 4 uses a rank-adaptive retraction with step 1, i.e.
-    X = TT-URV_eps(Y); Y = reconstruct(X); Y[Omega] = M[Omega]. `y_ptr` holds the initial
-    iterate (the observed values zero-filled, as initial_guess) and is updated in place.
-    All pointers are device pointers (e.g. torch ``data_ptr()``)."""
-    import time
-    n = int(np.prod(dims))
-    tr = CompletionTrace()
-    stats = (C.c_double * 5)()
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        res = decompose_device(y_ptr, dims, method, sweep, eps=eps, a_is_device_ptr=True)
-        check(lib().ttg_result_reconstruct(res.h, C.c_void_p(y_ptr), 1))
-        tr.ranks.append(res.report().ranks_chosen)
-        del res
-        check(lib().ttg_completion_reset(C.c_void_p(y_ptr), C.c_void_p(observed_ptr), C.c_void_p(mask_ptr),
-                                         C.c_void_p(truth_ptr) if truth_ptr else None, n, stats))
-        tr.rse_observed.append(float(np.sqrt(stats[0] / stats[1])) if stats[1] > 0 else 0.0)
-        if truth_ptr:
-            tr.rse_full.append(float(np.sqrt(stats[2] / stats[3])))
-            mse = stats[2] / n
-            tr.psnr.append(float("inf") if mse == 0 else float(10.0 * np.log10(stats[4] ** 2 / mse)))
-        tr.wall_time_ms.append(1e3 * (time.perf_counter() - t0))
-    return tr
+    def __init__(self, handle: C.c_void_p, d: int, has_truth: bool):
+        self.h = handle
+        n = lib().ttg_completion_iterations(handle)
+        obs, full, ps, wall = (np.zeros(max(n, 1)) for _ in range(4))
+        init = np.zeros(3)
+        lib().ttg_completion_trace(handle, _dptr(obs), _dptr(full), _dptr(ps), _dptr(wall), _dptr(init))
+        ranks = []
+        buf = np.zeros(d + 1, np.int64)
+        for it in range(n + 1):
+            if lib().ttg_completion_ranks(handle, it, _iptr(buf)):
+                ranks.append(buf.tolist())
+        st = lib().ttg_completion_status(handle)
+        self.trace = CompletionTrace(ranks, obs[:n].tolist(), full[:n].tolist() if has_truth else [],
+                                     ps[:n].tolist() if has_truth else [], wall[:n].tolist(),
+                                     ["converged", "max_iters", "diverged"][st],
+                                     lib().ttg_completion_note(handle).decode(),
+                                     {"rse_observed": init[0], **({"rse_full": init[1], "psnr": init[2]}
+                                                                  if has_truth else {})})
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().ttg_completion_free(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+    def result(self) -> "DeviceResult":
+        """The final iterate's train (a view: valid while this handle lives)."""
+        r = DeviceResult(C.c_void_p(lib().ttg_completion_result(self.h)))
+        r._owner = self
+        r._borrowed = True
+        return r
+
+
+def complete(linear, values, dims, ranks=None, eps=None, retraction="svd", step_size=1.0, max_iters=500,
+             stop_tol=1e-6, refine_passes=2, dense_cap=10_000_000, truth=None, on_device=False,
+             count=None) -> Completion:
+    """complete() (completion.hpp:73-75) on the device. ``linear``/``values``: the mask's
+    0-based increasing linear indices and observed values (ObservationMask); ``ranks``: the
+    fixed-rank chain, or ``eps`` for the rank-adaptive retraction (extension, config 4).
+    With ``on_device`` the three array arguments are device pointers (ints) and ``count`` is
+    the number of observations."""
+    require_gpu()
+    from ._native import CompletionConfig
+    dims = np.ascontiguousarray(np.asarray(dims, np.int64))
+    cfg = CompletionConfig()
+    keep = []
+    if ranks is not None:
+        r = np.ascontiguousarray(np.asarray(ranks, np.int64))
+        keep.append(r)
+        cfg.ranks, cfg.nranks, cfg.eps = _iptr(r), int(r.size), 0.0
+    else:
+        cfg.ranks, cfg.nranks, cfg.eps = None, 0, float(eps)
+    cfg.retraction = METHODS[retraction]
+    cfg.step_size, cfg.max_iters, cfg.stop_tol = float(step_size), int(max_iters), float(stop_tol)
+    cfg.refine_passes, cfg.dense_cap = int(refine_passes), int(dense_cap)
+    h = C.c_void_p()
+    if on_device:
+        if count is None:
+            raise ArgumentError("on_device completion needs the observation count")
+        check(lib().ttg_complete(C.cast(C.c_void_p(int(linear)), c_int64_p), C.cast(C.c_void_p(int(values)),
+                                                                                      c_double_p),
+                                 int(count), _iptr(dims), int(dims.size), C.byref(cfg),
+                                 C.cast(C.c_void_p(int(truth)), c_double_p) if truth else None, 1, C.byref(h)))
+    else:
+        li = np.ascontiguousarray(np.asarray(linear, np.int64))
+        va = np.ascontiguousarray(np.asarray(values, np.float64))
+        tr = np.ascontiguousarray(np.asarray(truth, np.float64).reshape(-1)) if truth is not None else None
+        check(lib().ttg_complete(_iptr(li), _dptr(va), int(li.size), _iptr(dims), int(dims.size), C.byref(cfg),
+                                 _dptr(tr) if tr is not None else None, 0, C.byref(h)))
+    del keep
+    return Completion(h, int(dims.size), truth is not None)
 
 
 # ---- factor level (factor.hpp) -------------------------------------------------------

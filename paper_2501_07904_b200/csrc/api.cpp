@@ -383,6 +383,134 @@ double rse(const DenseTensor& est, const DenseTensor& truth) {
     return out;
 }
 
+// ---- completion.hpp ------------------------------------------------------------------------
+ObservationMask::ObservationMask(const Shape& shape, const std::vector<std::vector<std::int64_t>>& indices,
+                                 const std::vector<double>& values)
+    : shape_(shape) {
+    if (indices.size() != values.size()) throw ArgumentError("observation indices and values differ in length");
+    std::vector<std::pair<std::int64_t, double>> entries;
+    entries.reserve(indices.size());
+    for (size_t i = 0; i < indices.size(); ++i) entries.emplace_back(ivec(indices[i], shape) - 1, values[i]);
+    std::sort(entries.begin(), entries.end());
+    for (size_t i = 1; i < entries.size(); ++i)
+        if (entries[i].first == entries[i - 1].first)
+            throw ArgumentError("duplicate observation at linear index " + std::to_string(entries[i].first + 1));
+    for (const auto& [idx, val] : entries) {
+        linear_.push_back(idx);
+        values_.push_back(val);
+    }
+    if (linear_.empty()) throw ArgumentError("observation set is empty");
+}
+
+ObservationMask::ObservationMask(const DenseTensor& indicator, const DenseTensor& values) : shape_(indicator.shape()) {
+    if (!(indicator.shape() == values.shape())) throw ArgumentError("indicator and value tensors differ in shape");
+    for (std::int64_t i = 0; i < indicator.element_count(); ++i)
+        if (indicator[i] != 0.0) {
+            linear_.push_back(i);
+            values_.push_back(values[i]);
+        }
+    if (linear_.empty()) throw ArgumentError("observation set is empty");
+}
+
+double ObservationMask::values_norm() const { return std::sqrt(kernels::sum_squares(values_)); }
+
+// a scatter of the observed entries (container code, no arithmetic)
+DenseTensor project_observed(const DenseTensor& tensor, const ObservationMask& mask) {
+    if (!(tensor.shape() == mask.shape())) throw ArgumentError("project_observed: shapes differ");
+    DenseTensor out{tensor.shape()};
+    for (std::int64_t i : mask.linear_indices()) out[i] = tensor[i];
+    return out;
+}
+
+namespace {
+struct CompletionGuard {
+    ttg_completion* c = nullptr;
+    CompletionGuard() = default;
+    CompletionGuard(const CompletionGuard&) = delete;
+    CompletionGuard(CompletionGuard&& o) noexcept : c(o.c) { o.c = nullptr; }
+    ~CompletionGuard() {
+        if (c) ttg_completion_free(c);
+    }
+};
+
+TTTensor tt_of(const ttg_result* r) {
+    std::vector<TTCore> cores;
+    for (int k = 0; k < ttg_result_order(r); ++k) {
+        std::int64_t cd[3];
+        ttg_result_core_dims(r, k, cd);
+        DenseTensor t{Shape({cd[0], cd[1], cd[2]})};
+        check(ttg_result_core_copy(r, k, t.data()));
+        cores.push_back(TTCore{std::move(t)});
+    }
+    return TTTensor(std::move(cores));
+}
+
+CompletionGuard run_completion(const ObservationMask& mask, const Shape& shape, const CompletionConfig& config,
+                               const DenseTensor* truth, int max_iters) {
+    if (!(mask.shape() == shape)) throw ArgumentError("mask was built against a different shape");
+    if (truth != nullptr && !(truth->shape() == shape)) throw ArgumentError("ground truth has a different shape");
+    const std::vector<std::int64_t> dims(shape.dims().begin(), shape.dims().end());
+    ttg_completion_config c{};
+    const bool adaptive = config.retraction_eps > 0.0;
+    c.ranks = adaptive ? nullptr : config.ranks.data();
+    c.nranks = adaptive ? 0 : (int)config.ranks.size();
+    c.eps = config.retraction_eps;
+    c.retraction = (int)config.retraction;
+    c.step_size = config.step_size;
+    c.max_iters = max_iters;
+    c.stop_tol = config.stop_tol;
+    c.refine_passes = config.refine_passes;
+    c.dense_cap = config.dense_cap;
+    if (!adaptive && config.ranks.size() != dims.size() + 1)
+        throw ArgumentError("rank chain has " + std::to_string(config.ranks.size()) + " entries, expected " +
+                            std::to_string(dims.size() + 1));
+    CompletionGuard g;
+    check(ttg_complete(mask.linear_indices().data(), mask.values().data(), mask.count(), dims.data(),
+                       (int)dims.size(), &c, truth ? truth->data() : nullptr, 0, &g.c));
+    return g;
+}
+}  // namespace
+
+CompletionResult complete(const ObservationMask& mask, const Shape& shape, const CompletionConfig& config,
+                          const DenseTensor* truth) {
+    CompletionGuard g = run_completion(mask, shape, config, truth, config.max_iters);
+    CompletionResult out;
+    const int n = ttg_completion_iterations(g.c);
+    IterationTrace& tr = out.trace;
+    tr.rse_observed.resize((size_t)n);
+    tr.wall_time_ms.resize((size_t)n);
+    if (truth) {
+        tr.rse_full.resize((size_t)n);
+        tr.psnr.resize((size_t)n);
+    }
+    ttg_completion_trace(g.c, tr.rse_observed.data(), truth ? tr.rse_full.data() : nullptr,
+                         truth ? tr.psnr.data() : nullptr, tr.wall_time_ms.data(), nullptr);
+    tr.status = (CompletionStatus)ttg_completion_status(g.c);
+    tr.note = ttg_completion_note(g.c);
+    std::vector<std::int64_t> rk(shape.dims().size() + 1);
+    for (int it = 0; it <= n; ++it)
+        if (ttg_completion_ranks(g.c, it, rk.data())) tr.ranks.push_back(rk);
+    out.tt = tt_of(ttg_completion_result(g.c));
+    return out;
+}
+
+TTTensor initial_guess(const ObservationMask& mask, const Shape& shape, const CompletionConfig& config) {
+    // the retraction of the zero-filled observations: decompose them directly
+    if (!(mask.shape() == shape)) throw ArgumentError("mask was built against a different shape");
+    if (shape.element_count() > config.dense_cap)
+        throw ResourceError("completion would materialize " + std::to_string(shape.element_count()) + " elements (cap " +
+                            std::to_string(config.dense_cap) + ")");
+    DenseTensor filled{shape};
+    for (std::int64_t i = 0; i < mask.count(); ++i) filled[mask.linear_indices()[(size_t)i]] = mask.values()[(size_t)i];
+    DecompConfig dc;
+    dc.method = config.retraction;
+    dc.sweep = config.retraction == Method::urv ? Sweep::right_to_left : Sweep::left_to_right;
+    if (config.retraction_eps > 0.0) dc.mode = FixedTol{config.retraction_eps, {}};
+    else dc.mode = FixedRank{config.ranks};
+    dc.refine_passes = config.refine_passes;
+    return decompose(filled, dc).tt;
+}
+
 // ---- kernels.hpp ---------------------------------------------------------------------------
 namespace kernels {
 namespace {

@@ -122,6 +122,39 @@ def cfg2():
     np.savez_compressed(OUT / "full_cfg2.npz", **out)
 
 
+def cfg4():
+    """BASELINE config 4, the reference harness loop:
+    Y = P_Omega(M); per iteration X = tt_urv_fixed_tol_r2l(Y, 1e-3) (refine 1), x = reconstruct(X),
+    RSE of x against the full tensor M, then Y = x with Y[Omega] = M[Omega]. Iterations 0 and 1.
+    M = the 256^3 blob volume + 1% noise from paper_2501_07904_b200/inputs.py (Rng 4 / 40), the
+    mask Rng(41).uniform() < 0.5 (8,389,438 observed, as the survey's)."""
+    from paper_2501_07904_b200 import inputs
+    dims = [4] * 12
+    m = inputs.mri_like()
+    mask = inputs.bernoulli_mask(m.size, seed=41)
+    out = dict(dims=np.asarray(dims), m_sum=np.float64(m.sum()), mask_count=np.int64(mask.sum()))
+    y = m * mask
+    for it in range(2):
+        t0 = time.time()
+        res = ref.decompose(y, dims, "urv", "r2l", eps=1e-3)
+        t1 = time.time()
+        x = np.empty(m.size)
+        ref._check(ref.lib().ref_result_reconstruct(res.handle.h, 10**9, ref._d(x)))
+        rse_full = float(np.sqrt(np.sum((x - m) ** 2)) / np.sqrt(np.sum(m ** 2)))
+        on = mask != 0
+        rse_obs = float(np.sqrt(np.sum((x[on] - m[on]) ** 2)) / np.sqrt(np.sum(m[on] ** 2)))
+        out[f"it{it}_ranks"] = np.asarray(res.ranks_chosen, np.int64)
+        out[f"it{it}_rse_full"] = np.float64(rse_full)
+        out[f"it{it}_rse_obs"] = np.float64(rse_obs)
+        out[f"it{it}_step_errors"] = np.asarray(res.step_errors)
+        out[f"it{it}_decomp_s"] = np.float64(t1 - t0)
+        print(json.dumps(dict(it=it, ranks=res.ranks_chosen, rse_full=rse_full, rse_obs=rse_obs,
+                              decomp_s=round(t1 - t0, 1), total_s=round(time.time() - t0, 1))), flush=True)
+        y = x.copy()
+        y[on] = m[on]
+        np.savez_compressed(OUT / "full_cfg4.npz", **out)
+
+
 def cfg2x():
     """More neutral rescales of config 2 at eps = 1e-8, appended to full_cfg2.npz (the keys of
     the extra scales continue the e8_s<i> numbering)."""
@@ -155,4 +188,4 @@ def cfg2x():
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or ["cfg3"]:
-        {"cfg2": cfg2, "cfg2x": cfg2x, "cfg3": cfg3, "cfg5": cfg5}[name]()
+        {"cfg2": cfg2, "cfg2x": cfg2x, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}[name]()
