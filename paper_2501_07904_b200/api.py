@@ -277,11 +277,11 @@ def shard_block(a, dims, method: str, size: int, rank: int) -> np.ndarray:
 
 
 def decompose_sharded(a_local, dims, comm: Comm, method="urv", sweep="r2l", ranks=None, eps=None, weights=(),
-                      qlp="early_exit", a_is_device_ptr=False) -> DeviceResult:
+                      qlp="early_exit", a_is_device_ptr=False, debug_checks=False) -> DeviceResult:
     """Sharded decompose over the ranks of `comm`: `a_local` is this rank's block
     (shard_range / shard_block); every rank gets the whole train."""
     require_gpu()
-    cfg, keep = _config(method, sweep, ranks, eps, weights, 1, "l11_only", False, qlp)
+    cfg, keep = _config(method, sweep, ranks, eps, weights, 1, "l11_only", debug_checks, qlp)
     d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
     h = C.c_void_p()
     if a_is_device_ptr or isinstance(a_local, int):

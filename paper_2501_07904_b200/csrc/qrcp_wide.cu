@@ -2873,12 +2873,13 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     }
     nchunk_ = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k, 256), 4 * sms));
     if (sub_) {
-        // 16 predicted directions for long rows (the miss pass has FMA headroom there), 8 otherwise
+        // 8 predicted directions: with 16 the miss pass turns FMA-bound (17 FMAs per element,
+        // 206 registers) and costs more than the misses it saves (config 5: 120 vs 152 ms)
         static const int env_c = [] {  // experiment: TTG_SUBSPACE_C = 8 or 16
             const char* e = std::getenv("TTG_SUBSPACE_C");
             return e ? std::atoi(e) : 0;
         }();
-        subc_ = env_c == 8 || env_c == 16 ? env_c : (k >= 512 ? 16 : 8);
+        subc_ = env_c == 16 ? 16 : 8;
         E_.alloc((size_t)(k * subc_));
         a_.alloc(subc_);
         Z_.alloc((size_t)(subc_ * N));
@@ -3263,11 +3264,6 @@ void WideQrcp::gemv_step(int64_t t) {
 void WideQrcp::guard_step(int64_t t) {
     // guard recompute of the flagged norms; its candidates / masses go to the slots after
     // the stream kernel's
-    static const bool no_guard = [] {  // diagnostics only: skip the recompute (wrong results)
-        const char* e = std::getenv("TTG_DIAG_NO_GUARD");
-        return e && *e == '1';
-    }();
-    if (no_guard) return;
     // TTG_LAZY_GUARD=1 defers recomputes that cannot affect the next pivot (guard_defer);
     // measured neutral on config 2 (stale columns are re-flagged every step), so the
     // reference's eager recompute is the default.

@@ -212,6 +212,9 @@ struct Pass1 {
     virtual const int64_t* perm() = 0;   // positions -> columns
     virtual const double* Q() = 0;       // economy Q columns 0..s-1, leading dimension k
     virtual bool sharded() const { return false; }
+    // Sharded with each rank holding only its own columns of R1 (the column-sharded wide
+    // engine); the Gram route's R1 is replicated on every rank.
+    virtual Comm* partitioned_comm() { return nullptr; }
     // R_B (s x s, ld s) of B = R1[:s, :]^T over all columns (all ranks when sharded).
     virtual void r_factor(int64_t s, double* RB) {
         if (!gram_r(R(), N(), s, nullptr, RB, 0.0)) tsqr_r(R(), N(), s, N(), RB);
@@ -256,6 +259,7 @@ struct WidePass1 final : Pass1 {
               const ShardSpec* shard = nullptr)
         : e(W, k, N, ld, l, cap, shard) {}
     bool sharded() const override { return e.sharded(); }
+    Comm* partitioned_comm() override { return e.sharded() ? e.comm() : nullptr; }
     // Sharded: every rank reduces its own rows of B to a triangle, the triangles are
     // all-gathered and stacked in rank order, and every rank factors the same stack.
     // |R1(s-1, s-1)| / |R1(0, 0)| from pass 1's diagonal (host sync of two values)
@@ -636,8 +640,25 @@ Pass2 run_pass2(Pass1& e1, int64_t s) {
         e1.r_factor(s, RB.get());
         small_qrcp(RB.get(), s, s, s, out.perm.get(), R2.get(), pn.get(), nullptr);
     } else {
-        if (e1.sharded())
-            invariant_error("sharded pass 2 supports at most " + std::to_string(160) + " pass-1 steps per cut");
+        if (Comm* comm = e1.partitioned_comm()) {
+            // Long sharded pass 1 (s beyond the TSQR / Gram sizes, e.g. a fixed rank above 160
+            // or a tolerance cut that grew): all-gather the ranks' blocks of B = R1[:s, :]^T
+            // (R1's rows are B's columns, N local rows each) and run the in-place QRCP on the
+            // stacked B, replicated. Row order does not change QRCP's pivots or R.
+            const int G = comm->size();
+            DevBuf<double> all((size_t)G * N * s), Bs((size_t)G * N * s);
+            comm->allgather(e1.R(), all.get(), sizeof(double) * (size_t)(N * s));
+            for (int g = 0; g < G; ++g)
+                TTG_CUDA(cudaMemcpy2DAsync(Bs.get() + (int64_t)g * N, sizeof(double) * (size_t)(G * N),
+                                           all.get() + (int64_t)g * N * s, sizeof(double) * (size_t)N,
+                                           sizeof(double) * (size_t)N, (size_t)s, cudaMemcpyDeviceToDevice, stream()));
+            TallQrcp e2(Bs.get(), G * N, s, G * N);
+            e2.run(s);
+            e2.extract_r(R2.get(), s);
+            TTG_CUDA(cudaMemcpyAsync(pn.get(), e2.pivot_norm2(), sizeof(double) * s, cudaMemcpyDeviceToDevice, stream()));
+            TTG_CUDA(cudaMemcpyAsync(out.perm.get(), e2.perm(), sizeof(int64_t) * s, cudaMemcpyDeviceToDevice, stream()));
+            goto kept;
+        }
         static const bool wide_pass2 = [] {  // TTG_WIDE_PASS2=1: the read-only engine below
             const char* e = std::getenv("TTG_WIDE_PASS2");
             return e && *e == '1';
@@ -801,6 +822,20 @@ void finish(TTResult& res, bool rss, Clock::time_point start) {
     res.wall_ms = std::chrono::duration<double, std::milli>(Clock::now() - start).count();
 }
 
+// DecompConfig::debug_checks (tt_decomp.cpp:82-98): the carried matrix must equal the
+// projection of the unfolding onto the kept factor, |carry - ref| <= 1e-10 |c|_F.
+void debug_carry_check(const double* carry, const double* refm, int64_t count, const double* c, int64_t csize,
+                       const char* where) {
+    const double scale = std::sqrt(sum_squares(c, csize));
+    const double dev = std::sqrt(diff_squares(carry, refm, count));
+    if (dev > 1e-10 * scale) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "%s: carried matrix deviates from the projected previous one by %.3e (allowed %.3e)",
+                      where, dev, 1e-10 * scale);
+        invariant_error(buf);
+    }
+}
+
 void set_core(TTResult& res, size_t k, DevBuf<double>&& buf, int64_t r0, int64_t n, int64_t r1) {
     res.cores[k] = std::move(buf);
     res.core_dims[k] = {r0, n, r1};
@@ -949,6 +984,11 @@ void general_sweep(const double* a, const std::vector<int64_t>& dims, const Swee
             res.cuts[(size_t)(k - 1)] = CutInfo{m, n, p, p, r, 0, {}};
             DevBuf<double> next((size_t)(r * n));
             gemm(false, true, r, n, r, g.t11.get(), r, g.v1.get(), n, next.get(), r);  // T11 V1^T (:192)
+            if (cfg.debug) {
+                DevBuf<double> refm((size_t)(r * n));
+                gemm(true, false, r, n, m, g.u1.get(), m, c, m, refm.get(), r);
+                debug_carry_check(next.get(), refm.get(), r * n, c, m * n, "left-to-right sweep");
+            }
             set_core(res, (size_t)(k - 1), std::move(g.u1), r_prev, dims[(size_t)(k - 1)], r);
             r_prev = r;
             if (k < d - 1) {
@@ -999,13 +1039,41 @@ void general_sweep(const double* a, const std::vector<int64_t>& dims, const Swee
             next.alloc((size_t)(M * r));
             gemm(false, false, M, r, p, g.fu.get(), M, g.ft.get(), p, next.get(), M);
             v1 = prefix(g.v1.get(), n * r);
+            if (cfg.debug) {
+                DevBuf<double> refm((size_t)(M * r));
+                gemm(false, false, M, r, n, c, M, v1.get(), n, refm.get(), M);
+                debug_carry_check(next.get(), refm.get(), M * r, c, M * n, "right-to-left sweep (full column)");
+            }
         } else {
-            GenCut g = general_cut(cfg.method, c, M, n, cfg.refine, mode.fixed, want, budget, false);
+            const bool coupling = cfg.debug && cfg.method == 1;  // ULV L11-only: L21 check
+            GenCut g = general_cut(cfg.method, c, M, n, cfg.refine, mode.fixed, want, budget, coupling);
             r = g.r;
             step_err = g.res;
             next.alloc((size_t)(M * r));
             gemm(false, false, M, r, r, g.u1.get(), M, g.t11.get(), r, next.get(), M);  // U1 T11 (:302)
             v1 = std::move(g.v1);
+            if (cfg.debug) {
+                DevBuf<double> refm((size_t)(M * r));
+                gemm(false, false, M, r, n, c, M, v1.get(), n, refm.get(), M);
+                if (coupling) {
+                    // the discarded coupling block is what the carry misses (tt_decomp.cpp:288-309)
+                    DevBuf<double> part((size_t)p), kept((size_t)p + 1);
+                    TTG_LAUNCH(k_colmass_full, 1, 256, 0, stream(), g.ft.get(), p, part.get(), kept.get());
+                    const std::vector<double> ck = kept.to_host((size_t)p + 1);
+                    const double l22 = ck[(size_t)p] - ck[(size_t)r];
+                    const double l21 = std::sqrt(std::max(0.0, step_err * step_err - l22));
+                    const double dev = std::sqrt(diff_squares(next.get(), refm.get(), M * r));
+                    const double scale = std::sqrt(sum_squares(c, M * n));
+                    if (std::abs(dev - l21) > 1e-10 * scale) {
+                        char buf[256];
+                        std::snprintf(buf, sizeof buf, "right-to-left sweep: carry deviation %.3e != coupling norm %.3e",
+                                      dev, l21);
+                        invariant_error(buf);
+                    }
+                } else {
+                    debug_carry_check(next.get(), refm.get(), M * r, c, M * n, "right-to-left sweep");
+                }
+            }
         }
         res.step_errors[(size_t)(k - 2)] = step_err;
         res.ranks_chosen[(size_t)(k - 1)] = r;
@@ -1092,6 +1160,11 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
         DevBuf<double> next((size_t)(r * n));
         dim3 g((unsigned)cdiv(n, 32), (unsigned)cdiv(r, 32));
         TTG_LAUNCH(k_carry_rows_t, g, dim3(32, 8), 0, stream(), e1->R(), n, co.sel.get(), r, next.get());
+        if (cfg.debug) {  // carry = T11 V1^T against U1^T c (tt_decomp.cpp:193-196)
+            DevBuf<double> refm((size_t)(r * n));
+            gemm(true, false, r, n, m, res.cores[(size_t)(k - 1)].get(), m, c, m, refm.get(), r);
+            debug_carry_check(next.get(), refm.get(), r * n, c, m * n, "left-to-right sweep");
+        }
         r_prev = r;
         if (k < d - 1) {
             carry = std::move(next);
@@ -1131,6 +1204,11 @@ void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, 
         DevBuf<double> next((size_t)(M * r));
         dim3 g((unsigned)std::min<int64_t>(cdiv(M, 256), 4096), (unsigned)r);
         TTG_LAUNCH(k_carry_rows, g, 256, 0, stream(), e1->R(), M, co.sel.get(), r, next.get());
+        if (cfg.debug) {  // carry = U1 T11 against c V1 (tt_decomp.cpp:310-317); the core is V1^T
+            DevBuf<double> refm((size_t)(M * r));
+            gemm(false, true, M, r, n, c, M, res.cores[(size_t)(k - 1)].get(), r, refm.get(), M);
+            debug_carry_check(next.get(), refm.get(), M * r, c, M * n, "right-to-left sweep");
+        }
         r_next = r;
         if (k > 2) {
             carry = std::move(next);
@@ -1347,6 +1425,7 @@ bool k_sharded_next(TTResult& res, const double* mine, int64_t Nl, int64_t Ng, i
 
 TTResult decompose_sharded(const double* a_local, const std::vector<int64_t>& dims, const SweepConfig& cfg,
                            Comm& comm) {
+    if (cfg.debug) argument_error("debug_checks is not supported by the column-sharded sweep");
     const auto start = Clock::now();
     const int64_t d = (int64_t)dims.size();
     for (size_t k = 0; k < dims.size(); ++k)

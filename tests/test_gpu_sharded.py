@@ -146,3 +146,17 @@ def test_k_sharded_second_cut(dev, ref, G):
     dims, ranks = [16, 64, 64], [1, 8, 8, 1]
     a = planted_plus_noise(ref, dims, ranks, 33, 1e-6)
     _check(dev, ref, a, dims, "urv", G, ranks=ranks)
+
+
+@pytest.mark.parametrize("method", ["urv", "ulv"])
+def test_long_pass2_beyond_160_steps_sharded(dev, ref, method):
+    """A fixed rank above 160 on the sharded first cut: pass 2 no longer fits the TSQR / Gram
+    routes, so the ranks' blocks of B = R1^T are all-gathered and factored in place (before:
+    an InvariantError). 176 x 48 x 48, first-cut rank 170."""
+    dims, ranks = [176, 48, 48], [1, 170, 30, 1]
+    a = planted_plus_noise(ref, dims, [1, 24, 12, 1], 31, 1e-3)
+    rk = [1, 170, 30, 1] if method == "ulv" else [1, 30, 40, 1]
+    if method == "urv":  # URV shards the last mode: its first cut has W = 48 x 36,864 (p = 48)
+        dims, rk = [48, 48, 176], [1, 30, 170, 1]
+        a = planted_plus_noise(ref, dims, [1, 12, 24, 1], 31, 1e-3)
+    _check(dev, ref, a, dims, method, 2, ranks=rk)

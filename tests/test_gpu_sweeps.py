@@ -392,3 +392,29 @@ def test_subspace_engine_cuts(dev, ref, method, mode):
         _check_parity(dev, ref, a, dims, method, ranks=ranks)
     else:
         _check_parity(dev, ref, a, dims, method, eps=1e-5)
+
+
+@pytest.mark.parametrize("method,sweep,retain", [("ulv", "l2r", "l11_only"), ("urv", "r2l", "l11_only"),
+                                                 ("svd", "l2r", "l11_only"), ("svd", "r2l", "l11_only"),
+                                                 ("ulv", "r2l", "l11_only"), ("ulv", "r2l", "full_column"),
+                                                 ("urv", "l2r", "l11_only")])
+@pytest.mark.parametrize("refine", [1, 2])
+def test_debug_checks_carry_identities(dev, ref, method, sweep, retain, refine):
+    """DecompConfig::debug_checks (tt_decomp.cpp:82-98, 193-196, 268-317): the device checks the
+    carried matrix against the projected unfolding on every cut, like the reference (which
+    passes on the same inputs; test_tt_decomp.cpp:47-78)."""
+    dims, ranks = [6, 5, 7, 4], [1, 3, 4, 2, 1]
+    a = planted_plus_noise(ref, dims, ranks, 11, 1e-3)
+    rr = ref.decompose(a, dims, method, sweep, ranks=ranks, refine=refine, retain=1 if retain == "full_column" else 0,
+                       debug=True)
+    res = dev.decompose_device(a, dims, method, sweep, ranks=ranks, refine_passes=refine, retain=retain,
+                               debug_checks=True)
+    assert res.report().ranks_chosen == rr.ranks_chosen
+
+
+def test_debug_checks_rejected_by_sharded(dev, ref):
+    a, dims, ranks = cfg1(ref)
+    comms = dev.loopback_group(1)
+    blk = dev.shard_block(a, dims, "urv", 1, 0)
+    with pytest.raises(Exception, match="debug_checks is not supported by the column-sharded sweep"):
+        dev.decompose_sharded(blk, dims, comms[0], "urv", "r2l", ranks=ranks, debug_checks=True)
