@@ -291,6 +291,13 @@ ttg_status ttg_psnr(const double* estimate, const double* truth, int64_t count, 
 ttg_status ttg_reverse_indices(const double* a, const int64_t* dims, int d, double* out);
 ttg_status ttg_reverse_tt(const double* cores, const int64_t* dims, const int64_t* ranks, int d,
                           double* out);
+/* C = alpha op(A) op(B) + beta C on DEVICE buffers, column-major, on this thread's stream
+ * (ttg_stream()), no synchronisation: the engine's FP64 tensor-core (DMMA) GEMM -- a 128 x 128
+ * cp.async-pipelined kernel for aligned operands with even leading dimensions, split over K for
+ * long reductions with a deterministic combine. The dense kernel of the carry/Gram/reconstruct
+ * contractions, exported for measurement and for callers that keep data on the device. */
+ttg_status ttg_gemm_device(int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 ttg_status ttg_matmul(const double* a, int64_t a_rows, int64_t a_cols, int ta, const double* b,
                       int64_t b_rows, int64_t b_cols, int tb, double* c);
 

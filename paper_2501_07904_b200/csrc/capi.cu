@@ -548,6 +548,20 @@ ttg_status ttg_matmul(const double* a, int64_t ar, int64_t ac, int ta, const dou
     });
 }
 
+ttg_status ttg_gemm_device(int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+    return guard([&] {
+        if (m < 0 || n < 0 || k < 0) ttg::argument_error("matrix dims must be nonnegative");
+        if (k == 0) {
+            if (beta == 0.0)
+                for (int64_t j = 0; j < n; ++j)
+                    TTG_CUDA(cudaMemsetAsync(C + j * ldc, 0, sizeof(double) * (size_t)m, ttg::stream()));
+            return;
+        }
+        ttg::gemm(ta != 0, tb != 0, m, n, k, A, lda, B, ldb, C, ldc, alpha, beta);
+    });
+}
+
 ttg_status ttg_rse(const double* estimate, const double* truth, int64_t count, double* out) {
     return guard([&] {
         DeviceInput e(estimate, count, false), t(truth, count, false);

@@ -1,6 +1,7 @@
 // Dense device helpers: FP64 tensor-core GEMM (mma.sync m8n8k4 f64 -> SASS DMMA; sm_100a
 // has no tcgen05 kind for f64), tiled transpose and deterministic reductions.
 #include <cmath>
+#include <cstdlib>
 
 #include "engine.hpp"
 
@@ -101,6 +102,139 @@ __global__ void __launch_bounds__(128) k_gemm(int64_t m, int64_t n, int64_t k, c
             for (int h = 0; h < 2; ++h) {
                 const int64_t gi = m0 + wm + i * 8 + (lane >> 2);
                 const int64_t gj = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+                if (gi < m && gj < n) {
+                    double* cp = C + gi + gj * ldc;
+                    *cp = beta == 0.0 ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *cp);
+                }
+            }
+}
+
+// ---------------------------------------------------------------------------
+// Large GEMM: CTA tile 128 x 128, K step 16, 8 warps (2 x 4) each owning a 64 x 32 sub-tile
+// = 8 x 4 DMMA 8x8x4 fragments (64 accumulators per thread). Operand tiles move global ->
+// shared with 16-byte cp.async (LDGSTS) through a 4-stage ring, so the next three K steps are
+// in flight while the DMMAs of the current one run. Shared layouts are chosen per operand so
+// that the 16-byte copies land contiguously and the fragment loads are conflict-free:
+//   A (!TA, m contiguous): As[k][m], row stride 132;  A (TA, k contiguous): As[m][k], stride 20
+//   B (TB,  n contiguous): Bs[k][n], row stride 132;  B (!TB, k contiguous): Bs[n][k], stride 20
+// (strides = 4 mod 16 doubles: the 16 lanes of a half-warp hit 16 distinct bank pairs).
+// Requires 16-byte aligned A, B and even lda, ldb (the dispatcher checks); edges zero-fill.
+// Split-K over blockIdx.y like k_gemm (kc, cstride).
+// ---------------------------------------------------------------------------
+constexpr int G2M = 128, G2N = 128, G2K = 16, G2STAGES = 4;
+constexpr int G2WIDE = 132, G2NARROW = 20;
+constexpr int G2TILE = G2M * G2NARROW > G2K * G2WIDE ? G2M * G2NARROW : G2K * G2WIDE;  // doubles per operand tile
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// elements (0..2) of a 16-byte chunk that lie inside the matrix, `left` = extent - index
+__device__ __forceinline__ int g2cnt(int64_t left) { return left <= 0 ? 0 : left >= 2 ? 2 : 1; }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256, 1) k_gemm128(int64_t m, int64_t n, int64_t k, const double* __restrict__ A,
+                                                    int64_t lda, const double* __restrict__ B, int64_t ldb, double* C,
+                                                    int64_t ldc, double alpha, double beta, int64_t kc,
+                                                    int64_t cstride) {
+    {
+        const int64_t kb = (int64_t)blockIdx.y * kc;
+        k = min(kc, k - kb);
+        A += TA ? kb : kb * lda;
+        B += TB ? kb * ldb : kb;
+        C += (int64_t)blockIdx.y * cstride;
+    }
+    extern __shared__ double g2s[];  // G2STAGES x (A tile, B tile)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tm = cdiv(m, G2M);
+    const int64_t m0 = ((int64_t)blockIdx.x % tm) * G2M, n0 = ((int64_t)blockIdx.x / tm) * G2N;
+    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+
+    auto load_stage = [&](int stage, int64_t k0) {
+        double* As = g2s + (size_t)stage * 2 * G2TILE;
+        double* Bs = As + G2TILE;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // 1024 16-byte chunks per operand tile
+            const int c = tid + e * 256;
+            if (!TA) {
+                const int kk = c >> 6, mm = (c & 63) * 2;
+                const int64_t gi = m0 + mm, gk = k0 + kk;
+                const int bytes = gk < k ? g2cnt(m - gi) * 8 : 0;
+                cp_async16(As + kk * G2WIDE + mm, bytes ? A + gi + gk * lda : A, bytes);
+            } else {
+                const int mm = c >> 3, kk = (c & 7) * 2;
+                const int64_t gi = m0 + mm, gk = k0 + kk;
+                const int bytes = gi < m ? g2cnt(k - gk) * 8 : 0;
+                cp_async16(As + mm * G2NARROW + kk, bytes ? A + gk + gi * lda : A, bytes);
+            }
+            if (TB) {
+                const int kk = c >> 6, nn = (c & 63) * 2;
+                const int64_t gj = n0 + nn, gk = k0 + kk;
+                const int bytes = gk < k ? g2cnt(n - gj) * 8 : 0;
+                cp_async16(Bs + kk * G2WIDE + nn, bytes ? B + gj + gk * ldb : B, bytes);
+            } else {
+                const int nn = c >> 3, kk = (c & 7) * 2;
+                const int64_t gj = n0 + nn, gk = k0 + kk;
+                const int bytes = gj < n ? g2cnt(k - gk) * 8 : 0;
+                cp_async16(Bs + nn * G2NARROW + kk, bytes ? B + gk + gj * ldb : B, bytes);
+            }
+        }
+    };
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int64_t nk = cdiv(k, G2K);
+#pragma unroll
+    for (int s = 0; s < G2STAGES - 1; ++s) {
+        if (s < nk) load_stage(s, (int64_t)s * G2K);
+        cp_async_commit();
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int64_t kt = 0; kt < nk; ++kt) {
+        cp_async_wait<G2STAGES - 2>();
+        __syncthreads();
+        {  // refill the stage consumed G2STAGES - 1 steps ago
+            const int64_t nxt = kt + G2STAGES - 1;
+            if (nxt < nk) load_stage((int)(nxt % G2STAGES), nxt * G2K);
+            cp_async_commit();
+        }
+        const double* As = g2s + (size_t)(kt % G2STAGES) * 2 * G2TILE;
+        const double* Bs = As + G2TILE;
+#pragma unroll
+        for (int ks = 0; ks < G2K; ks += 4) {
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = wm + i * 8 + fr;
+                af[i] = TA ? As[r * G2NARROW + ks + fk] : As[(ks + fk) * G2WIDE + r];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cidx = wn + j * 8 + fr;
+                bf[j] = TB ? Bs[(ks + fk) * G2WIDE + cidx] : Bs[cidx * G2NARROW + ks + fk];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gi = m0 + wm + i * 8 + fr;
+                const int64_t gj = n0 + wn + j * 8 + 2 * fk + h;
                 if (gi < m && gj < n) {
                     double* cp = C + gi + gj * ldc;
                     *cp = beta == 0.0 ? alpha * acc[i][j][h] : fma(alpha, acc[i][j][h], beta * *cp);
@@ -242,9 +376,57 @@ __global__ void k_reduce_chunks(const double* __restrict__ part, int64_t ks, int
 
 }  // namespace
 
+namespace {
+// The pipelined 128 x 128 kernel for problems that fill its tiles; operands 16-byte aligned
+// with even leading dimensions (cp.async). TTG_GEMM128=0 keeps every call on k_gemm.
+bool gemm128_ok(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb) {
+    static const bool off = [] {
+        const char* e = std::getenv("TTG_GEMM128");
+        return e && *e == '0';
+    }();
+    const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return !off && m >= 96 && n >= 96 && k >= 32 && al(A) && al(B) && lda % 2 == 0 && ldb % 2 == 0;
+}
+
+template <bool TA, bool TB>
+void launch128(dim3 grid, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+               int64_t ldb, double* C, int64_t ldc, double al, double be, int64_t kc, int64_t cs) {
+    const size_t smem = sizeof(double) * (size_t)G2STAGES * 2 * G2TILE;
+    allow_smem(k_gemm128<TA, TB>, smem);
+    TTG_LAUNCH((k_gemm128<TA, TB>), grid, 256, smem, stream(), m, n, k, A, lda, B, ldb, C, ldc, al, be, kc, cs);
+}
+}  // namespace
+
 void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
           int64_t ldb, double* C, int64_t ldc, double alpha, double beta) {
     if (m <= 0 || n <= 0) return;
+    if (k > 0 && gemm128_ok(m, n, k, A, lda, B, ldb)) {
+        const int sms = sm_count();
+        const int64_t tiles = cdiv(m, G2M) * cdiv(n, G2N);
+        if (tiles > INT32_MAX) argument_error("gemm: problem too large for one launch");
+        auto go = [&](dim3 grid, double* Cp, int64_t ldcp, double al, double be, int64_t kc, int64_t cs) {
+            if (!ta && !tb) launch128<false, false>(grid, m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+            else if (ta && !tb) launch128<true, false>(grid, m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+            else if (!ta && tb) launch128<false, true>(grid, m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+            else launch128<true, true>(grid, m, n, k, A, lda, B, ldb, Cp, ldcp, al, be, kc, cs);
+        };
+        if (tiles < 2 * sms && k >= 4096) {
+            // few output tiles and a long K (Gram matrices of tall blocks): split K so every SM
+            // gets work, partials reduced in chunk order (deterministic)
+            int64_t ks = std::min<int64_t>(cdiv(2 * sms, tiles), cdiv(k, 1024));
+            const int64_t kc = cdiv(cdiv(k, ks), G2K) * G2K;
+            ks = cdiv(k, kc);
+            if (ks > 1) {
+                DevBuf<double> part((size_t)(ks * m * n));
+                go(dim3((unsigned)tiles, (unsigned)ks), part.get(), m, alpha, 0.0, kc, m * n);
+                TTG_LAUNCH(k_reduce_chunks, (int)std::min<int64_t>(cdiv(m * n, 256), 8 * sms), 256, 0, stream(),
+                           part.get(), ks, m, n, C, ldc, beta);
+                return;
+            }
+        }
+        go(dim3((unsigned)tiles), C, ldc, alpha, beta, k, 0);
+        return;
+    }
     const int64_t tiles = cdiv(m, BM) * cdiv(n, BN);
     if (tiles > INT32_MAX) argument_error("gemm: problem too large for one launch");
     auto launch = [&](dim3 grid, double* Cp, int64_t ldcp, double al, double be, int64_t kc, int64_t cs) {

@@ -2697,18 +2697,29 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
                 const double* w[CW];
 #pragma unroll
                 for (int u = 0; u < CW; ++u) w[u] = W + min(j0 + u, N - 1) * ld;
-                for (int64_t i = lane; i < k; i += 32) {
-                    double x[CW];
+                // two 32-row blocks per iteration: 2 * CW independent loads in flight per lane
+                for (int64_t i0 = lane; i0 < k; i0 += 64) {
+                    const int64_t i1 = i0 + 32;
+                    const bool h1 = i1 < k;
+                    double x[2][CW];
 #pragma unroll
-                    for (int u = 0; u < CW; ++u) x[u] = w[u][i];
-                    const double qi = q[i];
+                    for (int u = 0; u < CW; ++u) {
+                        x[0][u] = w[u][i0];
+                        x[1][u] = h1 ? w[u][i1] : 0.0;
+                    }
 #pragma unroll
-                    for (int u = 0; u < CW; ++u) r[u] = fma(qi, x[u], r[u]);
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int64_t i = hh ? i1 : i0;
+                        if (hh && !h1) break;
+                        const double qi = q[i];
 #pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        const double ec = er[c * kp + i];
+                        for (int u = 0; u < CW; ++u) r[u] = fma(qi, x[hh][u], r[u]);
 #pragma unroll
-                        for (int u = 0; u < CW; ++u) z[u][c] = fma(ec, x[u], z[u][c]);
+                        for (int c = 0; c < C; ++c) {
+                            const double ec = er[c * kp + i];
+#pragma unroll
+                            for (int u = 0; u < CW; ++u) z[u][c] = fma(ec, x[hh][u], z[u][c]);
+                        }
                     }
                 }
 #pragma unroll
@@ -3132,7 +3143,8 @@ void WideQrcp::sub_step(int64_t t) {
         prof_end_select(subi_.get() + 1, 8.0 * (double)(N_ - t) * (double)(C + 2) + 8.0 * (double)N_,
                         "k_sub_stream hit (R row from Z = E^T W)",
                         8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_ * (1.0 + C),
-                        "k_sub_stream miss (W pass: R row and Z = E^T W)");
+                        layout_ == Layout::Row ? "k_sub_stream miss, row (W pass: R row and Z = E^T W)"
+                                               : "k_sub_stream miss, col (W pass: R row and Z = E^T W)");
     }
     guard_step(t);
 }
