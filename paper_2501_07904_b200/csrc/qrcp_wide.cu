@@ -2833,8 +2833,15 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_SUBSPACE");
             return e && *e == '0';
         }();
+        // Row layout only for now: the Col miss pass (warp per column group) runs at ~1.7 TB/s
+        // (one CTA per SM at 192 registers: too few loads in flight), slower than the per-step
+        // stream it would replace (config 3's 480 x 331,776 ULV cut: 0.75 vs 0.22 ms per pass)
+        static const bool sub_col = [] {  // experiment: TTG_SUBSPACE_COL=1
+            const char* e = std::getenv("TTG_SUBSPACE_COL");
+            return e && *e == '1';
+        }();
         sub_ = !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
-               (layout == Layout::Row || ld >= k);
+               (layout == Layout::Row || (sub_col && ld >= k));
     }
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
     // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps

@@ -28,7 +28,7 @@ def _run(ta, tb, m, n, k, lda_pad=0, alpha=1.0, beta=0.0):
     check(lib().ttg_synchronize())
     got = Cm.T
     err = (got - want).abs().max().item()
-    scale = (Aop.abs() @ Bop.abs()).max().item() * alpha + abs(beta) * 4
+    scale = (Aop.abs() @ Bop.abs()).max().item() * abs(alpha) + abs(beta) * 4
     return err, scale
 
 
