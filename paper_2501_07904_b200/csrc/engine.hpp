@@ -124,6 +124,30 @@ private:
 };
 
 // ---------------------------------------------------------------------------
+// Bitwise pass 1 for narrow W (k <= 32): the reference's qr_col_pivot operation for operation
+// on a row-major working copy (qrcp_exact.cu), for tolerance-mode cuts whose rank the rounding
+// of pass 1 decides (BASELINE config 2).
+// ---------------------------------------------------------------------------
+class ExactQrcp {
+public:
+    ExactQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout);
+    void run_to(int64_t s);
+    int64_t steps() const { return steps_; }
+    int64_t p() const { return p_; }
+    double trailing_mass_exact();
+    void r_rows(double* R, int64_t s) const;  // rows 0..s-1 by original column, row t at R + t N
+    void form_q(double* Q, int64_t s) const;  // economy Q columns 0..s-1, k x s
+    const int64_t* perm() const { return perm_.get(); }
+    const double* diag() const { return diag_.get(); }
+
+private:
+    int64_t k_, N_, p_, steps_ = 0;
+    int grid_ = 1;
+    DevBuf<double> work_, cn_, cr_, betas_, diag_, cand_, step_;
+    DevBuf<int64_t> pos_, perm_;
+};
+
+// ---------------------------------------------------------------------------
 // Pass 2 (and any tall QRCP): in-place Householder QR with column pivoting of an
 // N x n column-major matrix B with n moderate, mirroring factor.cpp:62-135 step by step
 // (pivot, dlarfg reflector, reflector application, norm downdate with the 1e-16

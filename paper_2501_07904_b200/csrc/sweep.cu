@@ -334,6 +334,41 @@ struct TallPass1 final : Pass1 {
     }
 };
 
+// Narrow W (k <= 32) in tolerance mode: the bitwise engine (qrcp_exact.cu), so the R1 rows past
+// the numerical rank -- pass 1's rounding residue, which decides an ulp-level rank -- are the
+// reference's own.
+struct ExactPass1 final : Pass1 {
+    ExactQrcp e;
+    int64_t k_, N_, rs_ = -1, qs_ = -1;
+    DevBuf<double> rrows, qbuf;
+    ExactPass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l) : e(W, k, N, ld, l), k_(k), N_(N) {}
+    int64_t p() const override { return e.p(); }
+    int64_t N() const override { return N_; }
+    int64_t k() const override { return k_; }
+    void run_to(int64_t s) override { e.run_to(s); }
+    double trailing_mass() override { return e.trailing_mass_exact(); }
+    double refresh_exact() override { return e.trailing_mass_exact(); }
+    const double* R() override {
+        const int64_t s = e.steps();
+        if (rs_ != s) {
+            rrows.alloc((size_t)(s * N_));
+            e.r_rows(rrows.get(), s);
+            rs_ = s;
+        }
+        return rrows.get();
+    }
+    const int64_t* perm() override { return e.perm(); }
+    const double* Q() override {
+        const int64_t s = e.steps();
+        if (qs_ != s) {
+            qbuf.alloc((size_t)(k_ * s));
+            e.form_q(qbuf.get(), s);
+            qs_ = s;
+        }
+        return qbuf.get();
+    }
+};
+
 // Small W (fits one CTA's shared memory): the whole pass 1 is the reference's
 // qr_col_pivot run step for step by one CTA (k_small_qrcp), one launch instead of a few
 // launches per step; every prefix s of the full factorisation is what the early exit
@@ -619,6 +654,13 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
     const int64_t p = std::min(k, N);
     if (small_qrcp_fits(k, N) && (k * N <= 16384 || 2 * cap >= p)) return std::make_unique<SmemPass1>(W, k, N, ld, l);
+    // narrow W at a prescribed accuracy: the bitwise engine, whose rounding residue (and so any
+    // ulp-decided rank, config 2) is the reference's. TTG_EXACT_PASS1=0 keeps the WY engine.
+    static const bool no_exact = [] {
+        const char* e = std::getenv("TTG_EXACT_PASS1");
+        return e && *e == '0';
+    }();
+    if (!fixed && !no_exact && k <= 32) return std::make_unique<ExactPass1>(W, k, N, ld, l);
     return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
 }
 
