@@ -156,6 +156,14 @@ __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 
 // Device helpers
 // ---------------------------------------------------------------------------
 
+// One FP64 tensor-core MMA, D(8x8) += A(8x4) B(4x8): lane l holds A[l/4][l%4], B[l%4][l/4]
+// and D[l/4][2(l%4) + {0,1}] (mma.sync m8n8k4 f64 -> SASS DMMA on sm_100a).
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -15,11 +15,6 @@ namespace {
 // ---------------------------------------------------------------------------
 constexpr int BM = 64, BN = 64, BK = 16;
 
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
 
 // Split-K: blockIdx.y selects the K chunk [y kc, (y+1) kc); chunk y writes its partial
 // product to C + y * cstride (beta must be 0 then). kc = k, cstride = 0 for a plain GEMM.

@@ -2584,7 +2584,7 @@ __device__ __forceinline__ bool sub_epilogue(int64_t t, int64_t j, int64_t N, in
 // LAYOUT 0 (Col, k >= 64): a warp owns four (C = 8) or two (C = 16) columns, lanes over rows
 //   (each lane's rows of q and E are read from shared memory once for all of them), then warp
 //   trees.
-template <int LAYOUT, int C>
+template <int LAYOUT, int C, bool MISS = true>
 __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_sub_stream(const double* __restrict__ W, int64_t k, int64_t N,
                                                             int64_t ld, int64_t t, const double* __restrict__ Q,
                                                             const double* __restrict__ E,
@@ -2598,6 +2598,7 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sd[kThreads / 32];
     const int hit = *hit_p, nE = *nE_p;
+    if (!MISS && !hit) return;  // a miss: k_sub_miss_mma does this step (same grid, same slots)
     const int64_t jp = piv[t];
     Cand best = cand_none();
     double msum = 0.0;
@@ -2618,7 +2619,7 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
             }
             append_flag(fl, j, flags, nflag);
         }
-    } else {
+    } else if (MISS) {
         const int64_t kp = (k + 1) & ~int64_t(1);
         double* q = sm;
         double* er = sm + kp;
@@ -2750,6 +2751,128 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
     if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
 }
 
+// Miss pass of the subspace engine on the FP64 tensor cores: [q_t E]^T W as DMMA 8x8x4 tiles.
+// A warp owns 32 columns (four 8-column n-fragments) per iteration and walks the rows in steps
+// of 4: the B fragments are W's elements (row i0 + lane%4, column j0 + 8n + lane/4) loaded
+// straight from global memory (32-byte sectors, fully used, 16 loads in flight per lane), the
+// A fragments are [q E]^T rows from shared memory (row 0 = q_t, rows 1..C = E's columns). The
+// MF m-fragments cover 8 MF >= C + 1 rows. Row 0 of the product is R(t, j); rows 1..nE are
+// Z = E^T W. Then a shuffle gives each lane one column for the epilogue (downdate, guard flag,
+// candidate).
+template <int LAYOUT, int C>
+__global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restrict__ W, int64_t k, int64_t N,
+                                                          int64_t ld, int64_t t, const double* __restrict__ Q,
+                                                          const double* __restrict__ E,
+                                                          const int* __restrict__ nE_p,
+                                                          const int* __restrict__ hit_p, double* Z,
+                                                          const double* diag, const int64_t* piv, double* R,
+                                                          double* nu, const double* cref, const int64_t* pos,
+                                                          int64_t* flags, int* nflag, Cand* cand, double* mass) {
+    constexpr int MF = (C + 1 + 7) / 8;
+    extern __shared__ double am[];  // (8 MF) x kq: row 0 = q_t, rows 1..C = E^T, zero elsewhere
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    if (*hit_p) return;  // a hit: k_sub_stream did this step (same grid, same slots)
+    const int nE = *nE_p;
+    const int64_t k4 = (k + 3) & ~int64_t(3);
+    const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);  // row stride = 4 mod 16 doubles: conflict-free A loads
+    for (int64_t e = threadIdx.x; e < 8 * MF * kq; e += kThreads) {
+        const int r = (int)(e / kq);
+        const int64_t i = e - (int64_t)r * kq;
+        double v = 0.0;
+        if (i < k) {
+            if (r == 0) v = Q[i + t * k];
+            else if (r <= nE) v = E[i + (r - 1) * k];
+        }
+        am[e] = v;
+    }
+    __syncthreads();
+    const int64_t jp = piv[t];
+    Cand best = cand_none();
+    double msum = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int64_t ngroups = cdiv(N, 32);
+    for (int64_t g = (int64_t)blockIdx.x * (kThreads / 32) + warp; g < ngroups; g += (int64_t)gridDim.x * (kThreads / 32)) {
+        const int64_t j0 = g * 32;
+        double acc[MF][4][2];
+#pragma unroll
+        for (int f = 0; f < MF; ++f)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) acc[f][n][0] = acc[f][n][1] = 0.0;
+        int64_t colb[4];
+        bool cok[4];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            colb[n] = j0 + 8 * n + fr;
+            cok[n] = colb[n] < N;
+        }
+        auto ldb = [&](int64_t i, int n) -> double {
+            if (i >= k || !cok[n]) return 0.0;
+            return LAYOUT == 0 ? __ldg(W + i + colb[n] * ld) : __ldg(W + i * ld + colb[n]);
+        };
+        int64_t i0 = 0;
+        for (; i0 + 16 <= k4; i0 += 16) {  // four k4 steps per iteration: 16 loads in flight
+            double b[4][4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+#pragma unroll
+                for (int n = 0; n < 4; ++n) b[s][n] = ldb(i0 + 4 * s + fk, n);
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                double a[MF];
+#pragma unroll
+                for (int f = 0; f < MF; ++f) a[f] = am[(8 * f + fr) * kq + i0 + 4 * s + fk];
+#pragma unroll
+                for (int f = 0; f < MF; ++f)
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) dmma(acc[f][n], a[f], b[s][n]);
+            }
+        }
+        for (; i0 < k4; i0 += 4) {
+            double b[4];
+#pragma unroll
+            for (int n = 0; n < 4; ++n) b[n] = ldb(i0 + fk, n);
+            double a[MF];
+#pragma unroll
+            for (int f = 0; f < MF; ++f) a[f] = am[(8 * f + fr) * kq + i0 + fk];
+#pragma unroll
+            for (int f = 0; f < MF; ++f)
+#pragma unroll
+                for (int n = 0; n < 4; ++n) dmma(acc[f][n], a[f], b[n]);
+        }
+        // D fragment: lane holds rows (8 f + fr), columns j0 + 8 n + 2 fk + h
+#pragma unroll
+        for (int f = 0; f < MF; ++f) {
+            const int row = 8 * f + fr;
+            if (row >= 1 && row <= nE) {
+#pragma unroll
+                for (int n = 0; n < 4; ++n)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t col = j0 + 8 * n + 2 * fk + h;
+                        if (col < N) Z[(int64_t)(row - 1) * N + col] = acc[f][n][h];
+                    }
+            }
+        }
+        // row 0 (R(t, j)) lives in lanes 0..3 of m-fragment 0: lane c of the warp takes column j0 + c
+        double rv = 0.0;
+        const int src = (lane & 7) >> 1;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const double v0 = __shfl_sync(0xffffffffu, acc[0][n][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, acc[0][n][1], src);
+            if ((lane >> 3) == n) rv = (lane & 1) ? v1 : v0;
+        }
+        const int64_t j = j0 + lane;
+        const bool fl = j < N && sub_epilogue(t, j, N, jp, rv, diag, R, nu, cref, pos, best, msum);
+        append_flag(fl, j, flags, nflag);
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sd);
+    if (threadIdx.x == 0) { cand[blockIdx.x] = best; mass[blockIdx.x] = msum; }
+}
+
 }  // namespace
 
 // Phase totals of the persistent loop (ms) per variant since the last reset (host sync).
@@ -2833,15 +2956,14 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_SUBSPACE");
             return e && *e == '0';
         }();
-        // Row layout only for now: the Col miss pass (warp per column group) runs at ~1.7 TB/s
-        // (one CTA per SM at 192 registers: too few loads in flight), slower than the per-step
-        // stream it would replace (config 3's 480 x 331,776 ULV cut: 0.75 vs 0.22 ms per pass)
-        static const bool sub_col = [] {  // experiment: TTG_SUBSPACE_COL=1
-            const char* e = std::getenv("TTG_SUBSPACE_COL");
-            return e && *e == '1';
+        // Col layout needs the DMMA miss pass (the FMA one, TTG_SUB_MMA=0, is latency-bound there:
+        // 0.75 vs 0.22 ms per pass on config 3's 480 x 331,776 ULV cut)
+        static const bool fma_miss = [] {
+            const char* e = std::getenv("TTG_SUB_MMA");
+            return e && *e == '0';
         }();
         sub_ = !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
-               (layout == Layout::Row || (sub_col && ld >= k));
+               (layout == Layout::Row || (!fma_miss && ld >= k));
     }
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
     // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps
@@ -3133,7 +3255,14 @@ void WideQrcp::sub_step(int64_t t) {
         TTG_LAUNCH(prep, 1, 1024, psm, stream(), W_, k_, ld_, (int)layout_, qptr(), t, cand_.get(), ncand_ + ngc_,
                    piv_.get(), E_.get(), a_.get(), subi_.get(), subi_.get() + 1, 1e-12);
     }
-    {
+    static const bool fma_miss = [] {  // TTG_SUB_MMA=0: the FMA miss pass (A/B)
+        const char* e = std::getenv("TTG_SUB_MMA");
+        return e && *e == '0';
+    }();
+    const int pair16 = ((reinterpret_cast<uintptr_t>(W_) & 15) == 0 && ld_ % 2 == 0) ? 1 : 0;
+    const double hit_bytes = 8.0 * (double)(N_ - t) * (double)(C + 2) + 8.0 * (double)N_;
+    const double miss_bytes = 8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_ * (1.0 + C);
+    if (fma_miss) {
         PhaseTimer pt("p1 subspace stream");
         prof_begin();
         const int64_t kp = (k_ + 1) & ~int64_t(1);
@@ -3141,17 +3270,38 @@ void WideQrcp::sub_step(int64_t t) {
         auto kern = layout_ == Layout::Row ? (C == 16 ? k_sub_stream<1, 16> : k_sub_stream<1, 8>)
                                            : (C == 16 ? k_sub_stream<0, 16> : k_sub_stream<0, 8>);
         allow_smem(kern, ssm);
-        const int pair16 = ((reinterpret_cast<uintptr_t>(W_) & 15) == 0 && ld_ % 2 == 0) ? 1 : 0;
         TTG_LAUNCH(kern, ncand_, kThreads, ssm, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), a_.get(),
                    subi_.get(), subi_.get() + 1, Z_.get(), pair16, diag_.get(), piv_.get(), R_.get(), nu_.get(),
                    cref_.get(), pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
         // algorithmic bytes: hit -- Z's C rows of the unpivoted columns, the norms read and
         // written, row t of R; miss -- W's k rows instead, plus writing Z
-        prof_end_select(subi_.get() + 1, 8.0 * (double)(N_ - t) * (double)(C + 2) + 8.0 * (double)N_,
-                        "k_sub_stream hit (R row from Z = E^T W)",
-                        8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_ * (1.0 + C),
+        prof_end_select(subi_.get() + 1, hit_bytes, "k_sub_stream hit (R row from Z = E^T W)", miss_bytes,
                         layout_ == Layout::Row ? "k_sub_stream miss, row (W pass: R row and Z = E^T W)"
                                                : "k_sub_stream miss, col (W pass: R row and Z = E^T W)");
+    } else {
+        PhaseTimer pt("p1 subspace stream");
+        prof_begin();
+        auto hk = layout_ == Layout::Row ? (C == 16 ? k_sub_stream<1, 16, false> : k_sub_stream<1, 8, false>)
+                                         : (C == 16 ? k_sub_stream<0, 16, false> : k_sub_stream<0, 8, false>);
+        TTG_LAUNCH(hk, ncand_, kThreads, 0, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), a_.get(), subi_.get(),
+                   subi_.get() + 1, Z_.get(), pair16, diag_.get(), piv_.get(), R_.get(), nu_.get(), cref_.get(),
+                   pos_.get(), flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+        prof_end_select(subi_.get() + 1, hit_bytes, "k_sub_stream hit (R row from Z = E^T W)", 0.0,
+                        "k_sub_stream (idle on a miss)");
+        prof_begin();
+        const int MF = (C + 1 + 7) / 8;
+        const int64_t k4 = (k_ + 3) & ~int64_t(3);
+        const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
+        const size_t msm = sizeof(double) * (size_t)(8 * MF * kq);
+        auto mk = layout_ == Layout::Row ? (C == 16 ? k_sub_miss_mma<1, 16> : k_sub_miss_mma<1, 8>)
+                                         : (C == 16 ? k_sub_miss_mma<0, 16> : k_sub_miss_mma<0, 8>);
+        allow_smem(mk, msm);
+        TTG_LAUNCH(mk, ncand_, kThreads, msm, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), subi_.get(),
+                   subi_.get() + 1, Z_.get(), diag_.get(), piv_.get(), R_.get(), nu_.get(), cref_.get(), pos_.get(),
+                   flags_.get(), nflag_.get(), cand_.get(), mass_.get());
+        prof_end_select(subi_.get() + 1, 0.0, "k_sub_miss_mma (idle on a hit)", miss_bytes,
+                        layout_ == Layout::Row ? "k_sub_miss_mma row (W pass on DMMA: R row and Z = E^T W)"
+                                               : "k_sub_miss_mma col (W pass on DMMA: R row and Z = E^T W)");
     }
     guard_step(t);
 }
