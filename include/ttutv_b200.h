@@ -59,8 +59,11 @@ enum { TTG_RETAIN_L11_ONLY = 0, TTG_RETAIN_FULL_COLUMN = 1 };
 enum { TTG_BOUND_RSS = 0, TTG_BOUND_PLAIN_SUM = 1 };
 /* QLP policy. EARLY_EXIT (default) stops each pivoted pass as soon as the kept block is
  * provably the one the full factorisation would produce;
- * FULL runs all p = min(m,n) steps of both passes exactly as the reference does. */
-enum { TTG_QLP_EARLY_EXIT = 0, TTG_QLP_FULL = 1 };
+ * FULL runs all p = min(m,n) steps of both passes exactly as the reference does;
+ * BITWISE is FULL with cuts of at most 32 rows (of W) run bitwise like the reference's
+ * qr_col_pivot in both passes (long sums as sequential chains): an ulp-decided rank (BASELINE
+ * config 2 at eps 1e-8) is then the reference's. Much slower on those cuts (~0.1-0.3 s). */
+enum { TTG_QLP_EARLY_EXIT = 0, TTG_QLP_FULL = 1, TTG_QLP_BITWISE = 2 };
 
 /* Mirrors DecompConfig + FixedRank/FixedTol (tt_decomp.hpp:24-45). */
 typedef struct ttg_config {

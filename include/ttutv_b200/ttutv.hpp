@@ -348,6 +348,10 @@ namespace gpu {
 // true = all p steps of both passes like the reference (include/ttutv_b200.h).
 void set_full_qlp(bool full) noexcept;
 bool full_qlp() noexcept;
+// Bitwise QLP (TTG_QLP_BITWISE): full QLP with narrow cuts (W of <= 32 rows) computed bitwise
+// like the reference's qr_col_pivot in both passes, so ulp-decided ranks are the reference's.
+void set_bitwise_qlp(bool on) noexcept;
+bool bitwise_qlp() noexcept;
 }  // namespace gpu
 
 }  // namespace ttutv

@@ -18,7 +18,7 @@ from ._native import ArgumentError, Config, check, lib, require_gpu, c_double_p,
 METHODS = {"svd": 0, "ulv": 1, "urv": 2}
 SWEEPS = {"l2r": 0, "left_to_right": 0, "r2l": 1, "right_to_left": 1}
 RETAIN = {"l11_only": 0, "full_column": 1}
-QLP = {"early_exit": 0, "full": 1}
+QLP = {"early_exit": 0, "full": 1, "bitwise": 2}
 
 
 def _dptr(a: np.ndarray):

@@ -40,6 +40,7 @@ std::int64_t checked_size(std::int64_t rows, std::int64_t cols) {
 }
 
 thread_local bool t_full_qlp = false;
+thread_local bool t_bitwise_qlp = false;
 
 struct ResultGuard {
     ttg_result* r = nullptr;
@@ -54,7 +55,7 @@ DecompResult run(const DenseTensor& a, const DecompConfig& cfg) {
     c.refine_passes = cfg.refine_passes;
     c.retain = (int)cfg.retain;
     c.debug_checks = cfg.debug_checks ? 1 : 0;
-    c.qlp_policy = t_full_qlp ? TTG_QLP_FULL : TTG_QLP_EARLY_EXIT;
+    c.qlp_policy = t_bitwise_qlp ? TTG_QLP_BITWISE : t_full_qlp ? TTG_QLP_FULL : TTG_QLP_EARLY_EXIT;
     if (const auto* fr = std::get_if<FixedRank>(&cfg.mode)) {
         c.fixed_rank = 1;
         c.ranks = fr->ranks.data();
@@ -755,6 +756,8 @@ double verify_bound(const DenseTensor& a, const TTTensor& tt, DecompReport& repo
 namespace gpu {
 void set_full_qlp(bool full) noexcept { t_full_qlp = full; }
 bool full_qlp() noexcept { return t_full_qlp; }
+void set_bitwise_qlp(bool on) noexcept { t_bitwise_qlp = on; }
+bool bitwise_qlp() noexcept { return t_bitwise_qlp; }
 }  // namespace gpu
 
 }  // namespace ttutv

@@ -147,6 +147,11 @@ private:
     DevBuf<int64_t> pos_, perm_;
 };
 
+// Bitwise qr_col_pivot of a tall N x s work matrix (s <= 32, column-major, overwritten): R over
+// positions (s x s, ld s), the permutation (position -> column) and each pivot's norm^2 at its
+// step. Its long sums are sequential chains (one warp each), as in the reference.
+void exact_tall_qrcp(double* work, int64_t N, int64_t s, double* R, int64_t* perm, double* pnorm);
+
 // ---------------------------------------------------------------------------
 // Pass 2 (and any tall QRCP): in-place Householder QR with column pivoting of an
 // N x n column-major matrix B with n moderate, mirroring factor.cpp:62-135 step by step

@@ -272,4 +272,257 @@ void ExactQrcp::form_q(double* Q, int64_t s) const {
     TTG_LAUNCH(k_ex_q, (int)cdiv(s, 32), 32, 0, stream(), work_.get(), k_, N_, s, perm_.get(), betas_.get(), Q);
 }
 
+// ===========================================================================================
+// Bitwise pass 2: the reference's qr_col_pivot of the tall B = R1^T (N x s, s <= 32; the
+// reference's `middle` = transpose(R1) with rows in pass-1 position order, factor.cpp:349-359)
+// reproduced operation for operation. Its sums run over all N rows in order (sum_squares_serial,
+// make_householder's sigma, apply_reflector's dot), so they are sequential chains: one warp per
+// chain streams its column(s) through shared memory with cp.async while lane 0 accumulates in
+// order. Everything else (scaling by 1/v0, the axpy updates) is elementwise and parallel.
+// It is the engine of the "bitwise" QLP policy (TTG_QLP_BITWISE), under which a cut whose rank
+// is decided by rounding (BASELINE config 2) picks the reference's rank: that rank depends on the
+// pass-2 pivot order among the noise-level rows, itself set by pass 2's rounding.
+// ===========================================================================================
+namespace {
+
+constexpr int kChainTile = 512;   // elements per operand per stage
+constexpr int kChainStages = 3;
+
+struct ChainSpec {      // chain c: out[c] = init[c] + sum_{i < len} a_c[i] * b_c[i] (b = a: squares)
+    int64_t col[kEx];   // physical column of operand a in `work` (ld N)
+    int64_t bcol;       // physical column of operand b (dots) or -1 (sum of squares)
+    int64_t r0, len;    // rows [r0, r0 + len)
+    int n;              // number of chains
+    double init[kEx];
+    double out[kEx];
+};
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+// One warp per chain: all 32 lanes copy tiles of the operands into a shared-memory ring
+// (cp.async, in flight while lane 0 works), lane 0 adds the products in row order.
+__global__ void __launch_bounds__(32) k_chain(const double* __restrict__ work, int64_t N, ChainSpec* sp) {
+    __shared__ __align__(16) double ta[kChainStages][kChainTile];
+    __shared__ __align__(16) double tb[kChainStages][kChainTile];
+    const int c = blockIdx.x;
+    if (c >= sp->n) return;
+    const int lane = threadIdx.x;
+    const bool sq = sp->bcol < 0;
+    const double* a = work + sp->col[c] * N + sp->r0;
+    const double* b = sq ? a : work + sp->bcol * N + sp->r0;
+    const int64_t len = sp->len;
+    const int64_t ntile = (len + kChainTile - 1) / kChainTile;
+    auto issue = [&](int64_t tile) {
+        const int st = (int)(tile % kChainStages);
+        const int64_t base = tile * kChainTile;
+        for (int e = lane; e < kChainTile; e += 32) {
+            const int64_t i = base + e;
+            if (i < len) {
+                cp_async8(&ta[st][e], a + i);
+                if (!sq) cp_async8(&tb[st][e], b + i);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int64_t tl = 0; tl < kChainStages - 1; ++tl) {
+        if (tl < ntile) issue(tl);
+        else asm volatile("cp.async.commit_group;\n" ::);
+    }
+    double s = sp->init[c];
+    for (int64_t tile = 0; tile < ntile; ++tile) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kChainStages - 2));
+        __syncwarp();
+        const int64_t nxt = tile + kChainStages - 1;
+        if (nxt < ntile) issue(nxt);
+        else asm volatile("cp.async.commit_group;\n" ::);
+        if (lane == 0) {
+            const int st = (int)(tile % kChainStages);
+            const int64_t cnt = min((int64_t)kChainTile, len - tile * kChainTile);
+            const double* x = ta[st];
+            const double* y = sq ? ta[st] : tb[st];
+#pragma unroll 8
+            for (int64_t e = 0; e < cnt; ++e) s = __dadd_rn(s, __dmul_rn(x[e], y[e]));
+        }
+        __syncwarp();
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    if (lane == 0) sp->out[c] = s;
+}
+
+struct TallState {          // bookkeeping of the bitwise tall QRCP (device)
+    int64_t colmap[kEx];    // position -> physical column of work
+    int64_t perm[kEx];      // position -> original column (the reference's perm)
+    double cn[kEx], cr[kEx];  // cnorm2 / cref2 by position
+    double beta[kEx], v0, smu;
+    int64_t jp;             // physical pivot column of the current step
+    int pivot_ok;           // beta != 0 this step
+    int nflag;
+    int flagpos[kEx];
+};
+
+__global__ void k_et_init(TallState* st, ChainSpec* sp, int s, int64_t N) {
+    for (int q = 0; q < s; ++q) {
+        st->colmap[q] = q;
+        st->perm[q] = q;
+        sp->col[q] = q;
+        sp->init[q] = 0.0;
+    }
+    sp->bcol = -1;
+    sp->r0 = 0;
+    sp->len = N;
+    sp->n = s;
+}
+
+__global__ void k_et_norms(TallState* st, const ChainSpec* sp, int s) {
+    for (int q = 0; q < s; ++q) st->cn[q] = st->cr[q] = sp->out[q];
+}
+
+// pivot (factor.cpp:85-93) and the sigma chain of make_householder (:28-29)
+__global__ void k_et_pick(TallState* st, ChainSpec* sp, int s, int64_t N, int k, double* pnorm) {
+    int piv = k;
+    for (int j = k + 1; j < s; ++j)
+        if (st->cn[j] > st->cn[piv]) piv = j;
+    if (piv != k) {
+        int64_t t64 = st->colmap[k]; st->colmap[k] = st->colmap[piv]; st->colmap[piv] = t64;
+        t64 = st->perm[k]; st->perm[k] = st->perm[piv]; st->perm[piv] = t64;
+        double td = st->cn[k]; st->cn[k] = st->cn[piv]; st->cn[piv] = td;
+        td = st->cr[k]; st->cr[k] = st->cr[piv]; st->cr[piv] = td;
+    }
+    pnorm[k] = st->cn[k];
+    st->jp = st->colmap[k];
+    sp->col[0] = st->jp;
+    sp->bcol = -1;
+    sp->r0 = k + 1;
+    sp->len = N - k - 1;
+    sp->init[0] = 0.0;
+    sp->n = N - k > 1 ? 1 : 0;
+}
+
+// make_householder's scalars (:30-37) from sigma; then the dot chains of apply_reflector (:50-51)
+__global__ void k_et_house(double* work, TallState* st, ChainSpec* sp, int s, int64_t N, int k) {
+    const int64_t jp = st->jp;
+    const int64_t len = N - k;
+    double* x = work + jp * N + k;
+    double beta = 0.0;
+    st->pivot_ok = 0;
+    if (len > 1) {
+        const double sigma = sp->out[0];
+        const double alpha = x[0];
+        if (sigma != 0.0) {
+            const double mu = __dsqrt_rn(__dadd_rn(dsq(alpha), sigma));
+            const double smu = copysign(mu, alpha);
+            const double v0 = __dadd_rn(alpha, smu);
+            beta = __ddiv_rn(dsq(v0), __dmul_rn(smu, v0));
+            st->v0 = v0;
+            st->smu = smu;
+            st->pivot_ok = 1;
+        }
+    }
+    st->beta[k] = beta;
+    // dot chains for the columns at positions k+1.. (only when the reflector is non-trivial)
+    int n = 0;
+    if (beta != 0.0)
+        for (int q = k + 1; q < s; ++q) {
+            const int64_t cj = st->colmap[q];
+            sp->col[n] = cj;
+            sp->init[n] = work[cj * N + k];
+            ++n;
+        }
+    sp->bcol = jp;
+    sp->r0 = k + 1;
+    sp->len = N - k - 1;
+    sp->n = n;
+}
+
+// x[i] /= v0 (i >= 1) and x[0] = -copysign(mu, alpha) on the pivot column
+__global__ void k_et_scale(double* work, const TallState* st, int64_t N, int k) {
+    if (!st->pivot_ok) return;
+    double* x = work + st->jp * N + k;
+    const double v0 = st->v0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < N - k; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __ddiv_rn(x[i], v0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) x[0] = -st->smu;
+}
+
+// c[0] -= t, c[i] -= t v[i] with t = dot * beta, for every column of this step's dot chains
+__global__ void k_et_update(double* work, const TallState* st, const ChainSpec* sp, int64_t N, int k) {
+    const int nc = sp->n;
+    if (nc == 0) return;
+    const double beta = st->beta[k];
+    const double* v = work + st->jp * N + k;
+    for (int c = 0; c < nc; ++c) {
+        double* col = work + sp->col[c] * N + k;
+        const double t = __dmul_rn(sp->out[c], beta);
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N - k; i += (int64_t)gridDim.x * blockDim.x)
+            col[i] = i == 0 ? __dsub_rn(col[0], t) : __dsub_rn(col[i], __dmul_rn(t, v[i]));
+    }
+}
+
+// downdate + guard flags (:96-107); the recompute chains are set up for the flagged positions
+__global__ void k_et_downdate(const double* work, TallState* st, ChainSpec* sp, int s, int64_t N, int k) {
+    int n = 0;
+    for (int q = k + 1; q < s; ++q) {
+        const int64_t cj = st->colmap[q];
+        const double r = work[cj * N + k];
+        const double nv = __dsub_rn(st->cn[q], dsq(r));
+        st->cn[q] = nv;
+        if (nv < __dmul_rn(1e-16, st->cr[q]) || nv < 0.0) {
+            st->flagpos[n] = q;
+            sp->col[n] = cj;
+            sp->init[n] = 0.0;
+            ++n;
+        }
+    }
+    st->nflag = n;
+    sp->bcol = -1;
+    sp->r0 = k + 1;
+    sp->len = N - k - 1;
+    sp->n = n;
+}
+
+__global__ void k_et_guard_done(TallState* st, const ChainSpec* sp) {
+    for (int f = 0; f < st->nflag; ++f) {
+        const int q = st->flagpos[f];
+        st->cn[q] = st->cr[q] = sp->out[f];
+    }
+}
+
+// R (s x s over positions, col-major ld s) and the permutation
+__global__ void k_et_out(const double* work, const TallState* st, int s, int64_t N, double* R, int64_t* perm) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int q = e / s, i = e - q * s;
+        R[e] = i <= q ? work[st->colmap[q] * N + i] : 0.0;
+    }
+    for (int q = threadIdx.x; q < s; q += blockDim.x) perm[q] = st->perm[q];
+}
+
+}  // namespace
+
+void exact_tall_qrcp(double* work, int64_t N, int64_t s, double* R, int64_t* perm, double* pnorm) {
+    if (s > kEx) argument_error("bitwise pass 2 supports at most 32 columns");
+    DevBuf<double> stb(sizeof(TallState) / sizeof(double) + 1), spb(sizeof(ChainSpec) / sizeof(double) + 1);
+    auto* st = reinterpret_cast<TallState*>(stb.get());
+    auto* sp = reinterpret_cast<ChainSpec*>(spb.get());
+    const int eg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 256), (int64_t)sm_count() * 4));
+    TTG_LAUNCH(k_et_init, 1, 1, 0, stream(), st, sp, (int)s, N);
+    TTG_LAUNCH(k_chain, (int)s, 32, 0, stream(), work, N, sp);
+    TTG_LAUNCH(k_et_norms, 1, 1, 0, stream(), st, sp, (int)s);
+    const int64_t p = std::min(N, s);
+    for (int k = 0; k < p; ++k) {
+        TTG_LAUNCH(k_et_pick, 1, 1, 0, stream(), st, sp, (int)s, N, k, pnorm);
+        TTG_LAUNCH(k_chain, 1, 32, 0, stream(), work, N, sp);
+        TTG_LAUNCH(k_et_house, 1, 1, 0, stream(), work, st, sp, (int)s, N, k);
+        TTG_LAUNCH(k_et_scale, eg, 256, 0, stream(), work, st, N, k);
+        TTG_LAUNCH(k_chain, (int)std::max<int64_t>(1, s - k - 1), 32, 0, stream(), work, N, sp);
+        TTG_LAUNCH(k_et_update, eg, 256, 0, stream(), work, st, sp, N, k);
+        TTG_LAUNCH(k_et_downdate, 1, 1, 0, stream(), work, st, sp, (int)s, N, k);
+        TTG_LAUNCH(k_chain, (int)std::max<int64_t>(1, s - k - 1), 32, 0, stream(), work, N, sp);
+        TTG_LAUNCH(k_et_guard_done, 1, 1, 0, stream(), st, sp);
+    }
+    TTG_LAUNCH(k_et_out, 1, 256, 0, stream(), work, st, (int)s, N, R, perm);
+}
+
 }  // namespace ttg

@@ -621,7 +621,10 @@ private:
 // so it serves wide and tall W alike; TTG_TALL_INPLACE=1 selects the in-place engine for
 // tall W instead (kept as a cross-check).
 std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap,
-                                  bool fixed = false, bool prev_near_full = false) {
+                                  bool fixed = false, bool prev_near_full = false, int policy = 0) {
+    // bitwise QLP: narrow W runs the reference's own arithmetic (its rounding residue decides
+    // ulp-level ranks, config 2)
+    if (policy == 2 && k <= 32) return std::make_unique<ExactPass1>(W, k, N, ld, l);
     static const bool inplace = [] {
         const char* e = std::getenv("TTG_TALL_INPLACE");
         return e && *e == '1';
@@ -654,13 +657,6 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
     const int64_t p = std::min(k, N);
     if (small_qrcp_fits(k, N) && (k * N <= 16384 || 2 * cap >= p)) return std::make_unique<SmemPass1>(W, k, N, ld, l);
-    // narrow W at a prescribed accuracy: the bitwise engine, whose rounding residue (and so any
-    // ulp-decided rank, config 2) is the reference's. TTG_EXACT_PASS1=0 keeps the WY engine.
-    static const bool no_exact = [] {
-        const char* e = std::getenv("TTG_EXACT_PASS1");
-        return e && *e == '0';
-    }();
-    if (!fixed && !no_exact && k <= 32) return std::make_unique<ExactPass1>(W, k, N, ld, l);
     return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
 }
 
@@ -670,13 +666,19 @@ struct Pass2 {
     DevBuf<int64_t> perm;  // positions -> R1 row (pass-1 step) index
 };
 
-Pass2 run_pass2(Pass1& e1, int64_t s) {
+Pass2 run_pass2(Pass1& e1, int64_t s, int policy = 0) {
     const int64_t N = e1.N();
     PhaseTimer pt("pass2 (incl. host sync)");
     Pass2 out;
     DevBuf<double> R2((size_t)s * s), colmass(s), kept(s + 1), pn(s);
     out.perm.alloc(s);
-    if (tsqr_fits(s) && small_qrcp_fits(s, s)) {
+    if (policy == 2 && s == e1.p() && s <= 32 && dynamic_cast<ExactPass1*>(&e1)) {
+        // bitwise: qr_col_pivot(transpose(R1)) as the reference runs it (factor.cpp:362-372),
+        // B's rows in pass-1 position order
+        DevBuf<double> B((size_t)N * s);
+        TTG_LAUNCH(k_gather_b, (int)cdiv(N * s, 256), 256, 0, stream(), e1.R(), e1.perm(), N, s, B.get());
+        exact_tall_qrcp(B.get(), N, s, R2.get(), out.perm.get(), pn.get());
+    } else if (tsqr_fits(s) && small_qrcp_fits(s, s)) {
         // QRCP(R_B) with B = R1[:s,:]^T = Q_B R_B: same pivots and |R| as QRCP(B).
         DevBuf<double> RB((size_t)s * s);
         e1.r_factor(s, RB.get());
@@ -748,7 +750,7 @@ kept:
 CutOut run_cut(Pass1& e1, const CutRequest& req) {
     const int64_t p = e1.p();
     int64_t s;
-    if (req.policy == 1) s = p;
+    if (req.policy >= 1) s = p;
     else if (req.fixed) s = req.rank;
     else s = std::min<int64_t>(p, 16);
     const double b2 = req.budget * req.budget;
@@ -788,7 +790,7 @@ CutOut run_cut(Pass1& e1, const CutRequest& req) {
         }
         phase("trailing mass", tp);
         tp = Clock::now();
-        Pass2 p2 = run_pass2(e1, s);
+        Pass2 p2 = run_pass2(e1, s, req.policy);
         phase("pass 2", tp);
         const std::vector<double>& hk = p2.kept;
         // total = kept[p] of the full factorisation = |R1[:s]|^2 + |R1[s:]|^2
@@ -1187,7 +1189,7 @@ void ulv_cuts(TTResult& res, const double* c, int64_t m, int64_t n, int64_t k0, 
         const CutRequest rq = make_request(res, mode, cfg, k, p);
         const auto tc0 = Clock::now();
         const int64_t cap = mode.fixed ? rq.rank : 32;
-        auto e1 = make_pass1(c, m, n, m, Layout::Col, cap, mode.fixed, prev_near_full);
+        auto e1 = make_pass1(c, m, n, m, Layout::Col, cap, mode.fixed, prev_near_full, cfg.policy);
         CutOut co = cut_with(e1, rq, c, m, n, m, Layout::Col, cap);
         print_cut("ulv", k, m, n, co, tc0);
         prev_near_full = co.rank * 10 >= p * 9;
@@ -1231,7 +1233,7 @@ void urv_cuts(TTResult& res, const double* c, int64_t M, int64_t n, int64_t k0, 
         // W = c^T: k_W = n rows, N_W = M columns, W(i,j) = c[j + i*M].
         const auto tc0 = Clock::now();
         const int64_t cap = mode.fixed ? rq.rank : 32;
-        auto e1 = make_pass1(c, n, M, M, Layout::Row, cap, mode.fixed, prev_near_full);
+        auto e1 = make_pass1(c, n, M, M, Layout::Row, cap, mode.fixed, prev_near_full, cfg.policy);
         CutOut co = cut_with(e1, rq, c, n, M, M, Layout::Row, cap);
         print_cut("urv", k - 1, M, n, co, tc0);
         prev_near_full = co.rank * 10 >= p * 9;
