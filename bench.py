@@ -634,7 +634,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 5],
                     help="BASELINE config (default: 3 at one GPU, 5 column-sharded at N > 1)")
-    ap.add_argument("--qlp", default="early_exit", choices=["early_exit", "full"])
+    ap.add_argument("--qlp", default="early_exit", choices=["early_exit", "full", "bitwise"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=900.0,
                     help="--impl reference: stop timing whole-workload steps after this many seconds")

@@ -3255,10 +3255,15 @@ void WideQrcp::sub_step(int64_t t) {
         TTG_LAUNCH(prep, 1, 1024, psm, stream(), W_, k_, ld_, (int)layout_, qptr(), t, cand_.get(), ncand_ + ngc_,
                    piv_.get(), E_.get(), a_.get(), subi_.get(), subi_.get() + 1, 1e-12);
     }
-    static const bool fma_miss = [] {  // TTG_SUB_MMA=0: the FMA miss pass (A/B)
+    // The miss pass: DMMA for Col W and for Row W of moderate k (config 3's 480-row cuts: 0.31 /
+    // 0.37 ms per pass), the FMA stream for long Row W rows (config 5's 1024 x 1M: 1.76 ms vs
+    // 2.37 ms -- its 512-byte row segments per warp keep HBM pages open). TTG_SUB_MMA=0 / 1
+    // forces one for A/B.
+    static const int mma_env = [] {
         const char* e = std::getenv("TTG_SUB_MMA");
-        return e && *e == '0';
+        return e ? (*e == '0' ? 0 : 1) : -1;
     }();
+    const bool fma_miss = mma_env == 0 || (mma_env < 0 && layout_ == Layout::Row && k_ >= 768);
     const int pair16 = ((reinterpret_cast<uintptr_t>(W_) & 15) == 0 && ld_ % 2 == 0) ? 1 : 0;
     const double hit_bytes = 8.0 * (double)(N_ - t) * (double)(C + 2) + 8.0 * (double)N_;
     const double miss_bytes = 8.0 * (double)(N_ - t) * (double)(k_ + 2) + 8.0 * (double)N_ * (1.0 + C);
