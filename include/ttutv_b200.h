@@ -236,6 +236,11 @@ ttg_status ttg_comm_nccl_unique_id(unsigned char id[128]);
 ttg_status ttg_comm_nccl_create(const unsigned char id[128], int nranks, int rank, ttg_comm** out);
 /* nranks endpoints in `out[0..nranks-1]`; endpoint g must be driven by its own host thread. */
 ttg_status ttg_comm_loopback_create(int nranks, ttg_comm** out);
+/* A communicator over a host transport the caller provides (gloo, MPI, sockets): fn must
+ * all-gather `bytes` from every rank into recv (nranks * bytes, rank order) and return 0. The
+ * engine stages the exchanged buffers through pinned host memory. */
+typedef int (*ttg_host_allgather)(const void* send, void* recv, size_t bytes, void* user);
+ttg_status ttg_comm_callback_create(int nranks, int rank, ttg_host_allgather fn, void* user, ttg_comm** out);
 void ttg_comm_free(ttg_comm* comm);
 /* The block of the first unfolding a rank owns: out = {lo, hi, rows, cols}. ULV (l2r):
  * columns [lo, hi) of c = A(i1; i2..id), a contiguous slice of A, rows x cols = I1 x (hi-lo).

@@ -120,6 +120,7 @@ SIGNATURES = {
     "ttg_completion_result": (C.c_void_p, [C.c_void_p]),
     "ttg_gemm_device": (C.c_int, [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                   C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
+    "ttg_comm_callback_create": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ttg_psnr": (C.c_int, [c_double_p, c_double_p, C.c_int64, c_double_p]),
     "ttg_reverse_indices": (C.c_int, [c_double_p, c_int64_p, C.c_int, c_double_p]),
     "ttg_reverse_tt": (C.c_int, [c_double_p, c_int64_p, c_int64_p, C.c_int, c_double_p]),

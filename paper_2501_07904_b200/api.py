@@ -257,6 +257,33 @@ def loopback_group(size: int) -> list:
     return [Comm(C.c_void_p(hs[r]), r, size) for r in range(size)]
 
 
+_HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+def callback_comm(allgather, size: int, rank: int) -> Comm:
+    """A communicator over a host transport: ``allgather(send: bytes) -> bytes`` must return the
+    concatenation of every rank's `send` in rank order (e.g. torch.distributed.all_gather_object
+    or all_gather of uint8 tensors over gloo). The engine stages exchanges through host memory."""
+    require_gpu()
+
+    def _cb(send, recv, nbytes, _user):
+        try:
+            out = allgather(C.string_at(send, nbytes))
+            if len(out) != nbytes * size:
+                return 2
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # reported to the engine as a failed exchange
+            return 1
+
+    fn = _HOST_ALLGATHER(_cb)
+    h = C.c_void_p()
+    check(lib().ttg_comm_callback_create(int(size), int(rank), C.cast(fn, C.c_void_p), None, C.byref(h)))
+    comm = Comm(h, rank, size)
+    comm._keep = fn  # the callback must outlive the communicator
+    return comm
+
+
 def shard_range(dims, method: str, size: int, rank: int):
     """(lo, hi, rows, cols): the block of the first unfolding owned by `rank`."""
     d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))

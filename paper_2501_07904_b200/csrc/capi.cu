@@ -230,6 +230,11 @@ ttg_status ttg_comm_nccl_create(const unsigned char id[128], int nranks, int ran
     return guard([&] { *out = new ttg_comm{ttg::make_nccl_comm(id, nranks, rank)}; });
 }
 
+ttg_status ttg_comm_callback_create(int nranks, int rank, ttg_host_allgather fn, void* user, ttg_comm** out) {
+    *out = nullptr;
+    return guard([&] { *out = new ttg_comm{ttg::make_callback_comm(nranks, rank, fn, user)}; });
+}
+
 ttg_status ttg_comm_loopback_create(int nranks, ttg_comm** out) {
     return guard([&] {
         auto group = ttg::make_loopback_group(nranks);

@@ -131,7 +131,53 @@ private:
     int rank_;
 };
 
+// ---- host-callback transport (any host collective: gloo, MPI, sockets) -------------------
+// The exchange leaves the device: the send buffer is copied to pinned host memory, the
+// caller's all-gather runs on the host, and the gathered bytes go back to the device. Used
+// with torch.distributed's gloo backend to drive the real engine from separate processes
+// (tests), and as the integration point for hosts that bring their own collective library.
+class CallbackComm final : public Comm {
+public:
+    CallbackComm(int nranks, int rank, ttg_host_allgather_fn fn, void* user)
+        : rank_(rank), size_(nranks), fn_(fn), user_(user) {}
+    ~CallbackComm() override {
+        if (hsend_) cudaFreeHost(hsend_);
+        if (hrecv_) cudaFreeHost(hrecv_);
+    }
+    int rank() const override { return rank_; }
+    int size() const override { return size_; }
+    void allgather(const void* send, void* recv, size_t bytes) override {
+        const size_t total = bytes * (size_t)size_;
+        if (cap_ < total) {
+            if (hsend_) TTG_CUDA(cudaFreeHost(hsend_));
+            if (hrecv_) TTG_CUDA(cudaFreeHost(hrecv_));
+            TTG_CUDA(cudaMallocHost(&hsend_, total));
+            TTG_CUDA(cudaMallocHost(&hrecv_, total));
+            cap_ = total;
+        }
+        TTG_CUDA(cudaMemcpyAsync(hsend_, send, bytes, cudaMemcpyDeviceToHost, stream()));
+        TTG_CUDA(cudaStreamSynchronize(stream()));
+        const int st = fn_(hsend_, hrecv_, bytes, user_);
+        if (st != 0) fail(8, "host all-gather callback failed with status " + std::to_string(st));
+        TTG_CUDA(cudaMemcpyAsync(recv, hrecv_, total, cudaMemcpyHostToDevice, stream()));
+        TTG_CUDA(cudaStreamSynchronize(stream()));
+    }
+
+private:
+    int rank_, size_;
+    ttg_host_allgather_fn fn_;
+    void* user_;
+    void* hsend_ = nullptr;
+    void* hrecv_ = nullptr;
+    size_t cap_ = 0;
+};
+
 }  // namespace
+
+std::unique_ptr<Comm> make_callback_comm(int nranks, int rank, ttg_host_allgather_fn fn, void* user) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !fn) argument_error("invalid callback communicator");
+    return std::make_unique<CallbackComm>(nranks, rank, fn, user);
+}
 
 double global_sum(Comm& comm, double local) {
     DevBuf<double> one(1), all((size_t)comm.size());

@@ -35,6 +35,10 @@ void nccl_unique_id(unsigned char id[128]);
 // In-process group of `nranks` endpoints for one GPU, one host thread per endpoint (tests):
 // the exchange is a host barrier around device copies, no kernel ever waits on another.
 std::vector<std::unique_ptr<Comm>> make_loopback_group(int nranks);
+// A communicator whose all-gather is a host callback: recv (size() * bytes, rank order) <-
+// every rank's send (bytes); returns 0 on success.
+typedef int (*ttg_host_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
+std::unique_ptr<Comm> make_callback_comm(int nranks, int rank, ttg_host_allgather_fn fn, void* user);
 
 // Column sharding of pass 1: this engine holds columns [col_off, col_off + N) of a
 // k x N_global matrix whose other columns live on the other ranks of `comm`.
