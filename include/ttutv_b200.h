@@ -129,7 +129,10 @@ int64_t ttg_last_error_offset(void);
 
 /* ---- tensor-train sweeps ---------------------------------------------------- */
 /* a: tensor of shape dims[0..d-1], first index fastest. a_on_device selects whether `a`
- * is a host pointer (copied in, timed in the report) or a device pointer (read in place). */
+ * is a host pointer (copied in, timed in the report) or a device pointer (read in place).
+ * Device inputs: the engine works on its own non-blocking per-thread stream (ttg_stream()); it
+ * waits for the work already queued on the legacy default stream before reading `a`, but work
+ * the caller queued on other streams must be complete (or ordered before ttg_stream()) first. */
 ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_config* cfg,
                          int a_on_device, ttg_result** out);
 /* ttg_decompose() on the tensor in a TTUTVTEN file, read straight to the device. */

@@ -81,6 +81,14 @@ struct DeviceInput {
     const double* ptr = nullptr;
     DeviceInput(const double* a, int64_t n, bool on_device) {
         if (on_device) {
+            // the engine runs on its own non-blocking stream: order the read after any work the
+            // caller queued on the legacy default stream (work on other streams of the caller's
+            // must be synchronised by the caller, as ttutv_b200.h states)
+            cudaEvent_t ev;
+            TTG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            TTG_CUDA(cudaEventRecord(ev, cudaStreamLegacy));
+            TTG_CUDA(cudaStreamWaitEvent(ttg::stream(), ev, 0));
+            TTG_CUDA(cudaEventDestroy(ev));
             ptr = a;
         } else {
             buf.alloc((size_t)n);

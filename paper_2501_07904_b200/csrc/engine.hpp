@@ -118,6 +118,9 @@ private:
     // subspace (lazy-exact) pivoting: R rows from Z = E^T W while q_t stays in span(E)
     bool sub_ = false;
     int subc_ = 8;  // predicted directions (basis size cap)
+    bool coop_ok_ = false, big_ok_ = false;  // the persistent loop, for after a subspace fallback
+    int ncand_coop_ = 0, sms_ = 0;
+    int sub_hits();
     DevBuf<double> E_, a_, Z_;
     DevBuf<int> subi_;  // [0] basis size nE, [1] hit flag of the current step
     DevBuf<int> nflag2_;

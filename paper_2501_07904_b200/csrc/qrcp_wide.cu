@@ -2376,6 +2376,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1_big(CoopArgs A) {
 }
 
 // Empty guard slots (after init / exact refresh, which cover every column themselves).
+// slot 0 <- the best of slots [0, nold) and their total mass; slots [1, nclear) cleared
+__global__ void __launch_bounds__(kThreads) k_fold_slots(Cand* cand, double* mass, int nold, int nclear) {
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sd[kThreads / 32];
+    Cand b = cand_none();
+    double m = 0.0;
+    for (int i = threadIdx.x; i < nold; i += kThreads) {
+        if (better(cand[i], b)) b = cand[i];
+        m += mass[i];
+    }
+    b = block_best(b, sc);
+    m = block_sum(m, sd);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nclear; i += kThreads) {
+        cand[i] = i == 0 ? b : cand_none();
+        mass[i] = i == 0 ? m : 0.0;
+    }
+}
+
 __global__ void k_clear_slots(Cand* cand, double* mass, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         cand[i] = cand_none();
@@ -2472,7 +2491,10 @@ __global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W,
         r2 = block_sum(r2, red);
         if (r2 <= tol * tol) {
             if (tid < n0) a[tid] = coef[tid];
-            if (tid == 0) *hit = 1;
+            if (tid == 0) {
+                *hit = 1;
+                hit[1] += 1;  // running hit count (hit[1] = subi_[2])
+            }
             return;
         }
     }
@@ -2928,6 +2950,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         if (off_ < 0 || off_ + N > Ng_) argument_error("shard column range outside the matrix");
     }
     const int sms = sm_count();
+    sms_ = sms;
     const bool aligned16 = (reinterpret_cast<uintptr_t>(W) & 15) == 0;  // bulk copies need 16 B
     if (aligned16 && layout == Layout::Col && k <= 32 && ld == k) {
         mode_ = 5;  // TMA ring over contiguous 256-column blocks
@@ -2965,9 +2988,10 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         sub_ = !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
                (layout == Layout::Row || (!fma_miss && ld >= k));
     }
+    const int ncand_stream = ncand_;
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
     // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps
-    if (!sub_) {
+    {
         static const bool no_coop = [] {
             const char* e = std::getenv("TTG_NO_COOP");
             return e && *e == '1';
@@ -3023,7 +3047,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         E_.alloc((size_t)(k * subc_));
         a_.alloc(subc_);
         Z_.alloc((size_t)(subc_ * N));
-        subi_.alloc(2);
+        subi_.alloc(3);  // nE, hit flag, running hit count
         subi_.zero();
     }
     nu_.alloc(N); cref_.alloc(N); pos_.alloc(N); perm_.alloc(Ng_); flags_.alloc(N);
@@ -3031,9 +3055,19 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         rec_.alloc((size_t)(k + kRecHead));
         recs_.alloc((size_t)comm_->size() * (k + kRecHead));
     }
+    // the subspace engine starts with the per-step slots; the persistent loop stays available
+    // for the steps after a fallback (WideQrcp::run_to)
+    coop_ok_ = coop_;
+    big_ok_ = big_;
+    ncand_coop_ = ncand_;
+    if (sub_) {
+        coop_ = big_ = false;
+        ncand_ = ncand_stream;
+    }
     ngc_ = coop_ ? sms : std::max(1, 2 * sms);
-    if (coop_) { nflag2_.alloc(2); nflag2_.zero(); }
-    cand_.alloc(ncand_ + ngc_); mass_.alloc(ncand_ + ngc_); nflag_.alloc(1); nflag_.zero();
+    if (coop_ok_) { nflag2_.alloc(2); nflag2_.zero(); }
+    const int nslots = std::max(ncand_ + ngc_, ncand_coop_ + sms);
+    cand_.alloc(nslots); mass_.alloc(nslots); nflag_.alloc(1); nflag_.zero();
     wv_.alloc(k); yv_.alloc(k);
     diag_.alloc(p_); beta_.alloc(p_); piv_.alloc(p_);
     if (mode_ == 4) kpart_.alloc((size_t)ksplit_ * N);
@@ -3135,8 +3169,37 @@ double WideQrcp::refresh_exact() {
 void WideQrcp::run_to(int64_t steps) {
     steps = std::min(steps, p_);
     if (steps > cap_) grow(std::min(p_, std::max(steps, 2 * cap_)));
+    while (sub_ && steps_ < steps) {
+        // subspace steps in windows of 8; a window with fewer than 2 hits (e.g. Hilbert-type
+        // columns whose predicted residuals are dependent) turns the engine back to the plain
+        // per-step / persistent stream for the rest of the factorisation
+        const int64_t w = std::min(steps, steps_ + 8);
+        const int h0 = sub_hits();
+        while (steps_ < w) step();
+        if (sub_hits() - h0 < 2) {
+            sub_ = false;
+            if (coop_ok_ && steps_ < steps) {
+                // the persistent loop reads ncand_coop_ + sms slots: fold the current ones into
+                // slot 0 first (best candidate, total mass), clear the rest
+                const int nold = ncand_ + ngc_, nnew = ncand_coop_ + sms;
+                TTG_LAUNCH(k_fold_slots, 1, kThreads, 0, stream(), cand_.get(), mass_.get(), nold,
+                           std::max(nold, nnew));
+                ncand_ = ncand_coop_;
+                ngc_ = sms_;
+                coop_ = true;
+                big_ = big_ok_;
+            }
+        }
+    }
     if (coop_ && steps > steps_ && coop_run(steps)) return;
     while (steps_ < steps) step();
+}
+
+int WideQrcp::sub_hits() {
+    int h = 0;
+    TTG_CUDA(cudaMemcpyAsync(&h, subi_.get() + 2, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    sync();
+    return h;
 }
 
 bool WideQrcp::coop_run(int64_t steps) {
