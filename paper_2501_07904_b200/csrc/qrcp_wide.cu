@@ -3181,7 +3181,7 @@ void WideQrcp::run_to(int64_t steps) {
             if (coop_ok_ && steps_ < steps) {
                 // the persistent loop reads ncand_coop_ + sms slots: fold the current ones into
                 // slot 0 first (best candidate, total mass), clear the rest
-                const int nold = ncand_ + ngc_, nnew = ncand_coop_ + sms;
+                const int nold = ncand_ + ngc_, nnew = ncand_coop_ + sms_;
                 TTG_LAUNCH(k_fold_slots, 1, kThreads, 0, stream(), cand_.get(), mass_.get(), nold,
                            std::max(nold, nnew));
                 ncand_ = ncand_coop_;
