@@ -65,8 +65,9 @@ struct ShardSpec {
 // ---------------------------------------------------------------------------
 class WideQrcp {
 public:
+    // subspace: allow the subspace (lazy-exact) stream (fixed-rank cuts; see qrcp_wide.cu)
     WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps,
-             const ShardSpec* shard = nullptr);
+             const ShardSpec* shard = nullptr, bool subspace = false);
     void run_to(int64_t steps);  // advance the greedy factorisation to `steps` (<= p)
     int64_t steps() const { return steps_; }
     int64_t p() const { return p_; }

@@ -2937,7 +2937,7 @@ WyTrace g_wytrace;
 }  // namespace
 
 WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout layout, int64_t cap_steps,
-                   const ShardSpec* shard)
+                   const ShardSpec* shard, bool subspace)
     : W_(W), k_(k), N_(N), ld_(ld), p_(std::min(k, N)), layout_(layout) {
     g_wytrace.enable();
     if (k <= 0 || N <= 0) argument_error("qr_col_pivot: empty matrix");
@@ -2985,7 +2985,9 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
             const char* e = std::getenv("TTG_SUB_MMA");
             return e && *e == '0';
         }();
-        sub_ = !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
+        // fixed-rank cuts only: in tolerance mode the early exit runs short, Hilbert-type cuts
+        // (config 2) whose predicted residuals are mostly dependent (315 misses in 320 steps)
+        sub_ = subspace && !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
                (layout == Layout::Row || (!fma_miss && ld >= k));
     }
     const int ncand_stream = ncand_;

@@ -256,8 +256,8 @@ bool gram_r(const double* R1, int64_t N, int64_t s, Comm* comm, double* RB, doub
 struct WidePass1 final : Pass1 {
     WideQrcp e;
     WidePass1(const double* W, int64_t k, int64_t N, int64_t ld, Layout l, int64_t cap,
-              const ShardSpec* shard = nullptr)
-        : e(W, k, N, ld, l, cap, shard) {}
+              const ShardSpec* shard = nullptr, bool subspace = false)
+        : e(W, k, N, ld, l, cap, shard, subspace) {}
     bool sharded() const override { return e.sharded(); }
     Comm* partitioned_comm() override { return e.sharded() ? e.comm() : nullptr; }
     // Sharded: every rank reduces its own rows of B to a triangle, the triangles are
@@ -657,7 +657,7 @@ std::unique_ptr<Pass1> make_pass1(const double* W, int64_t k, int64_t N, int64_t
         return std::make_unique<GramPass1>(W, k, N, ld, l, nullptr, cap);
     const int64_t p = std::min(k, N);
     if (small_qrcp_fits(k, N) && (k * N <= 16384 || 2 * cap >= p)) return std::make_unique<SmemPass1>(W, k, N, ld, l);
-    return std::make_unique<WidePass1>(W, k, N, ld, l, cap);
+    return std::make_unique<WidePass1>(W, k, N, ld, l, cap, nullptr, fixed);
 }
 
 // Pass-2 outputs on the host: pivot order, kept masses, pivot norms, |diag R2|.
@@ -1171,7 +1171,7 @@ CutOut cut_with(std::unique_ptr<Pass1>& e1, const CutRequest& rq, const double* 
             std::fprintf(stderr, "[ttg]   gram pass 1 (%lld x %lld, s=%lld): R_ss/R_00 = %.3e, %s\n", (long long)k,
                          (long long)N, (long long)co.steps, ratio, ratio >= 1e-4 ? "kept" : "redone");
         if (!(ratio >= 1e-4)) {
-            e1 = std::make_unique<WidePass1>(W, k, N, ld, l, cap);
+            e1 = std::make_unique<WidePass1>(W, k, N, ld, l, cap, nullptr, true);
             co = run_cut(*e1, rq);
         }
     }
