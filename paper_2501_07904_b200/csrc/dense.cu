@@ -134,7 +134,7 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(256, 1) k_gemm128(int64_t m, int64_t n, int64_t k, const double* __restrict__ A,
                                                     int64_t lda, const double* __restrict__ B, int64_t ldb, double* C,
                                                     int64_t ldc, double alpha, double beta, int64_t kc,
-                                                    int64_t cstride) {
+                                                    int64_t cstride, int sym) {
     {
         const int64_t kb = (int64_t)blockIdx.y * kc;
         k = min(kc, k - kb);
@@ -145,7 +145,15 @@ __global__ void __launch_bounds__(256, 1) k_gemm128(int64_t m, int64_t n, int64_
     extern __shared__ double g2s[];  // G2STAGES x (A tile, B tile)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tm = cdiv(m, G2M);
-    const int64_t m0 = ((int64_t)blockIdx.x % tm) * G2M, n0 = ((int64_t)blockIdx.x / tm) * G2N;
+    int64_t m0 = ((int64_t)blockIdx.x % tm) * G2M, n0 = ((int64_t)blockIdx.x / tm) * G2N;
+    if (sym) {  // symmetric product: only the tiles on and above the diagonal (tile row <= col)
+        const int64_t idx = blockIdx.x;
+        int64_t tn = (int64_t)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+        while ((tn + 1) * (tn + 2) / 2 <= idx) ++tn;
+        while (tn * (tn + 1) / 2 > idx) --tn;
+        m0 = (idx - tn * (tn + 1) / 2) * G2M;
+        n0 = tn * G2N;
+    }
     const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
 
     auto load_stage = [&](int stage, int64_t k0) {
@@ -347,13 +355,31 @@ __global__ void __launch_bounds__(256) k_gram_small(const double* __restrict__ B
     for (int e = threadIdx.x; e < S * S; e += 256) out[e] = tile[e];
 }
 
-__global__ void k_gram_sum(const double* __restrict__ part, int64_t nparts, int S, int s, double* G) {
+// two-level fixed-order sum of the per-CTA Gram partials: block b of the grid sums parts
+// [b*per, (b+1)*per) into mid[b]; the last CTA to finish (atomic ticket) adds mid[] in order
+__global__ void k_gram_sum(const double* __restrict__ part, int64_t nparts, int S, int s, double* G, double* mid,
+                           unsigned* ticket) {
+    const int64_t per = cdiv(nparts, (int64_t)gridDim.x);
+    const int64_t p0 = (int64_t)blockIdx.x * per, p1 = min(nparts, p0 + per);
     for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
         const int j = e / s, i = e - j * s;
         double a = 0.0;
-        for (int64_t p = 0; p < nparts; ++p) a += part[p * S * S + i + j * S];
+        for (int64_t p = p0; p < p1; ++p) a += part[p * S * S + i + j * S];
+        mid[(int64_t)blockIdx.x * s * s + e] = a;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        double a = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) a += mid[(int64_t)b * s * s + e];
         G[e] = a;
     }
+    if (threadIdx.x == 0) *ticket = 0;
 }
 
 // C = sum_c part[c] (+ beta C), chunks in order.
@@ -385,10 +411,19 @@ bool gemm128_ok(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, c
 
 template <bool TA, bool TB>
 void launch128(dim3 grid, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
-               int64_t ldb, double* C, int64_t ldc, double al, double be, int64_t kc, int64_t cs) {
+               int64_t ldb, double* C, int64_t ldc, double al, double be, int64_t kc, int64_t cs, int sym = 0) {
     const size_t smem = sizeof(double) * (size_t)G2STAGES * 2 * G2TILE;
     allow_smem(k_gemm128<TA, TB>, smem);
-    TTG_LAUNCH((k_gemm128<TA, TB>), grid, 256, smem, stream(), m, n, k, A, lda, B, ldb, C, ldc, al, be, kc, cs);
+    TTG_LAUNCH((k_gemm128<TA, TB>), grid, 256, smem, stream(), m, n, k, A, lda, B, ldb, C, ldc, al, be, kc, cs,
+               sym);
+}
+
+// C(i, j) = C(j, i) for i > j (the lower triangle from the upper)
+__global__ void k_mirror_lower(double* C, int64_t n, int64_t ldc) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / n, i = e - j * n;
+        if (i > j) C[i + j * ldc] = C[j + i * ldc];
+    }
 }
 }  // namespace
 
@@ -446,6 +481,38 @@ void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, in
     launch(dim3((unsigned)tiles), C, ldc, alpha, beta, k, 0);
 }
 
+void syrk(bool ta, int64_t n, int64_t k, const double* A, int64_t lda, double* C, int64_t ldc) {
+    // C = op(A) op(A)^T (op(A) n x k): the tiles on and above the diagonal on the DMMA kernel,
+    // then the lower triangle mirrored (about half the flops of the full product)
+    if (n <= 0) return;
+    const double* B = A;
+    if (k <= 0 || !gemm128_ok(n, n, k, A, lda, B, lda)) {
+        gemm(ta, !ta, n, n, k, A, lda, A, lda, C, ldc);
+        return;
+    }
+    const int sms = sm_count();
+    const int64_t tn = cdiv(n, G2N), tiles = tn * (tn + 1) / 2;
+    auto go = [&](dim3 grid, double* Cp, int64_t ldcp, int64_t kc, int64_t cs) {
+        if (ta) launch128<true, false>(grid, n, n, k, A, lda, A, lda, Cp, ldcp, 1.0, 0.0, kc, cs, 1);
+        else launch128<false, true>(grid, n, n, k, A, lda, A, lda, Cp, ldcp, 1.0, 0.0, kc, cs, 1);
+    };
+    int64_t ks = 1, kc = k;
+    if (tiles < 2 * sms && k >= 4096) {
+        ks = std::min<int64_t>(cdiv(2 * sms, tiles), cdiv(k, 1024));
+        kc = cdiv(cdiv(k, ks), G2K) * G2K;
+        ks = cdiv(k, kc);
+    }
+    if (ks > 1) {
+        DevBuf<double> part((size_t)(ks * n * n));
+        go(dim3((unsigned)tiles, (unsigned)ks), part.get(), n, kc, n * n);
+        TTG_LAUNCH(k_reduce_chunks, (int)std::min<int64_t>(cdiv(n * n, 256), 8 * sms), 256, 0, stream(), part.get(),
+                   ks, n, n, C, ldc, 0.0);
+    } else {
+        go(dim3((unsigned)tiles), C, ldc, k, 0);
+    }
+    TTG_LAUNCH(k_mirror_lower, (int)std::min<int64_t>(cdiv(n * n, 256), 8 * sms), 256, 0, stream(), C, n, ldc);
+}
+
 void gram_small(const double* B, int64_t N, int64_t s, int64_t ld, double* G) {
     const int S = s <= 8 ? 8 : s <= 16 ? 16 : s <= 24 ? 24 : 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sm_count(), cdiv(N, 4 * 8)));
@@ -457,7 +524,11 @@ void gram_small(const double* B, int64_t N, int64_t s, int64_t ld, double* G) {
         case 24: TTG_LAUNCH(k_gram_small<24>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
         default: TTG_LAUNCH(k_gram_small<32>, blocks, 256, 0, stream(), B, N, (int)s, ld, part.get()); break;
     }
-    TTG_LAUNCH(k_gram_sum, 1, 1024, 0, stream(), part.get(), nparts, S, (int)s, G);
+    const int g2 = (int)std::min<int64_t>(32, nparts);
+    DevBuf<double> mid((size_t)g2 * s * s);
+    DevBuf<unsigned> ticket(1);
+    ticket.zero();
+    TTG_LAUNCH(k_gram_sum, g2, 256, 0, stream(), part.get(), nparts, S, (int)s, G, mid.get(), ticket.get());
 }
 
 void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb) {

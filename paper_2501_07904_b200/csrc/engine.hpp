@@ -227,6 +227,9 @@ void gemm(bool ta, bool tb, int64_t m, int64_t n, int64_t k, const double* A, in
           const double* B, int64_t ldb, double* C, int64_t ldc, double alpha = 1.0,
           double beta = 0.0);
 void transpose(const double* A, int64_t m, int64_t n, int64_t lda, double* B, int64_t ldb);
+// C (n x n) = op(A) op(A)^T with op(A) = A^T (ta, A k x n) or A (A n x k): symmetric tiles only
+// on the DMMA kernel, the lower triangle mirrored.
+void syrk(bool ta, int64_t n, int64_t k, const double* A, int64_t lda, double* C, int64_t ldc);
 // G (s x s, ld s) = B^T B for a tall N x s block, s <= 32, on the DMMA tensor cores.
 void gram_small(const double* B, int64_t N, int64_t s, int64_t ld, double* G);
 // Deterministic sum of squares of a contiguous buffer (fixed 4096-element blocks combined

@@ -3296,7 +3296,15 @@ bool WideQrcp::coop_run(int64_t steps) {
 void WideQrcp::step() {
     const int64_t t = steps_;
     // explicit Q once t is large enough that O(t^2) WY work beats a k x k rank-1 update
-    if (!explicit_ && !comm_ && t >= 256 && k_ <= 8192 && 2 * t >= k_ / 4) to_explicit(t);
+    // (and from the first step for 512 <= k <= 2048: there the compact-WY reflector needs its
+    // multi-kernel chunked path from t ~ 32 on, ~150-200 us per step on config 5's 1024-row cut)
+    static const int64_t ex_mink = [] {  // experiment: TTG_EXPLICIT_MINK
+        const char* e = std::getenv("TTG_EXPLICIT_MINK");
+        return e ? (int64_t)std::atoll(e) : (int64_t)512;
+    }();
+    if (!explicit_ && !comm_ && k_ <= 8192 &&
+        ((t >= 256 && 2 * t >= k_ / 4) || (k_ >= ex_mink && k_ <= 2048)))
+        to_explicit(t);
     {
         PhaseTimer pt(explicit_ ? "p1 explicit reflector" : "p1 reflector");
         if (explicit_) explicit_step(t);

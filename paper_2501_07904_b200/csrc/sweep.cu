@@ -475,6 +475,37 @@ __global__ void k_gc_q(const double* __restrict__ W, int64_t k, int64_t ld, int 
     }
 }
 
+// R11^{-1} (s x s upper, col-major) with R11(m, l) = R(m, piv_l): column j solves R11 x = e_j
+// by back substitution, one thread per column.
+__global__ void k_gc_rinv(const double* __restrict__ R, int64_t N, const int64_t* __restrict__ piv, int64_t s,
+                          double* Rinv) {
+    extern __shared__ double r11[];  // r11[m + l s]
+    for (int64_t e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int64_t l = e / s, m = e - l * s;
+        r11[e] = m <= l ? R[m * N + piv[l]] : 0.0;
+    }
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < s; j += blockDim.x) {
+        double* x = Rinv + j * s;
+        for (int64_t i = s - 1; i >= 0; --i) {
+            if (i > j) { x[i] = 0.0; continue; }
+            double a = i == j ? 1.0 : 0.0;
+            for (int64_t l = i + 1; l <= j; ++l) a = fma(-r11[i + l * s], x[l], a);
+            const double d = r11[i + i * s];
+            x[i] = d != 0.0 ? a / d : 0.0;
+        }
+    }
+}
+
+// X (k x s, col-major) = W[:, piv[0..s)]
+__global__ void k_gc_gather(const double* __restrict__ W, int64_t k, int64_t ld, int layout,
+                            const int64_t* __restrict__ piv, int64_t s, double* X) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < k * s; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = e / k, i = e - l * k;
+        X[e] = layout == 0 ? W[i + piv[l] * ld] : W[i * ld + piv[l]];
+    }
+}
+
 __global__ void k_masked_sum(const double* __restrict__ D, const int64_t* __restrict__ pos, int64_t N, int64_t s,
                              double* out) {
     __shared__ double red[32];
@@ -498,8 +529,8 @@ struct GramPass1 final : Pass1 {
         : W_(W), k_(k), N_(N), ld_(ld), kg_(k), l_(l), comm_(comm) {
         G.alloc((size_t)(N * N));
         // G = W^T W; Col: W is k x N (ld); Row: W^T is N x k column-major (ld)
-        if (l == Layout::Col) gemm(true, false, N, N, k, W, ld, W, ld, G.get(), N);
-        else gemm(false, true, N, N, k, W, ld, W, ld, G.get(), N);
+        if (l == Layout::Col) syrk(true, N, k, W, ld, G.get(), N);
+        else syrk(false, N, k, W, ld, G.get(), N);
         if (comm && comm->size() > 1) {
             const int P = comm->size();
             DevBuf<double> all((size_t)(P * N * N));
@@ -552,9 +583,15 @@ struct GramPass1 final : Pass1 {
         if (qs_ != s_) {
             Qb.alloc((size_t)(k_ * s_));
             const size_t sm = sizeof(double) * (size_t)(s_ * s_);
-            allow_smem(k_gc_q, sm);
-            TTG_LAUNCH(k_gc_q, (int)std::min<int64_t>(cdiv(k_, 256), 4 * sm_count()), 256, sm, stream(), W_, k_, ld_,
-                       (int)l_, Rb.get(), N_, pivb.get(), s_, Qb.get());
+            // Q[:, :s] = W[:, piv] R11^{-1}: the triangular inverse (one CTA) and one DMMA GEMM
+            // (config 5's 131072 x 128: 5 ms of per-row substitution before). R11 is well
+            // conditioned here (cut_with keeps the route only for R_ss / R_00 >= 1e-4).
+            DevBuf<double> Rinv((size_t)(s_ * s_)), X((size_t)(k_ * s_));
+            allow_smem(k_gc_rinv, sm);
+            TTG_LAUNCH(k_gc_rinv, 1, 128, sm, stream(), Rb.get(), N_, pivb.get(), s_, Rinv.get());
+            TTG_LAUNCH(k_gc_gather, (int)std::min<int64_t>(cdiv(k_ * s_, 256), 16 * sm_count()), 256, 0, stream(), W_,
+                       k_, ld_, (int)l_, pivb.get(), s_, X.get());
+            gemm(false, false, k_, s_, s_, X.get(), k_, Rinv.get(), s_, Qb.get(), k_);
             qs_ = s_;
         }
         return Qb.get();
