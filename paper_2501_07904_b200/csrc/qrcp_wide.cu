@@ -2463,19 +2463,20 @@ __global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W,
     double* X = sm + k;              // k x C (candidate residuals / new basis)
     __shared__ double red[32];
     __shared__ double coef[C + 1];
-    __shared__ double dots[C * 80];  // CGS coefficients D[l * C + c] for a slice of l
+    __shared__ double dots[C * 32];  // CGS coefficients of one 32-column slice of Q, D[l * C + c]
+    __shared__ double Gm[C * C];     // Gram matrix of the candidates (CholQR)
+    __shared__ double Rm[C * C];
+    __shared__ int keep[C];
     __shared__ int64_t cols[C];
-    __shared__ int ncols, acc;
-    __shared__ Cand sc[32];
-    constexpr int64_t kSlice = 80;
+    __shared__ Cand wl[32 * C];      // every warp's C best candidates
+    __shared__ int ncols, nkeep;
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     for (int64_t i = tid; i < k; i += nt) q[i] = Q[i + t * k];
     __syncthreads();
     const int n0 = *nE;
     if (n0 > 0) {
-        // a = E^T q: one warp per coefficient
-        const int warp = tid >> 5, lane = tid & 31;
-        if (warp < n0) {
+        if (warp < n0) {  // a = E^T q: one warp per coefficient
             double s = 0.0;
             for (int64_t i = lane; i < k; i += 32) s = fma(E[i + warp * k], q[i], s);
             s = warp_sum(s);
@@ -2499,22 +2500,43 @@ __global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W,
         }
     }
     // ---- miss: predict the next pivots ------------------------------------------------
-    if (tid == 0) { *hit = 0; ncols = 0; }
-    __syncthreads();
+    if (tid == 0) *hit = 0;
     const int64_t jp = piv[t];
-    for (int r = 0; r < C; ++r) {
-        Cand best = cand_none();
-        for (int i = tid; i < ncand; i += nt) {
-            const Cand c = cand[i];
-            if (c.col < 0 || c.col == jp) continue;
-            bool taken = false;
-            for (int u = 0; u < ncols; ++u) taken |= cols[u] == c.col;
-            if (!taken && better(c, best)) best = c;
+    {  // the C best candidate slots (norm desc, position asc), excluding this step's pivot:
+        // each warp its C best of a strided slice, then warp 0 merges the 32 lists
+        int64_t taken[C];
+        for (int r = 0; r < C; ++r) {
+            Cand b = cand_none();
+            for (int i = warp * 32 + lane; i < ncand; i += nw * 32) {
+                const Cand c = cand[i];
+                bool tk = c.col < 0 || c.col == jp;
+                for (int u = 0; u < r; ++u) tk |= taken[u] == c.col;
+                if (!tk && better(c, b)) b = c;
+            }
+            b = warp_best(b);
+            taken[r] = b.col;
+            if (lane == 0) wl[warp * C + r] = b;
         }
-        best = block_best(best, sc);
-        if (tid == 0 && best.col >= 0) cols[ncols++] = best.col;
         __syncthreads();
-        if (best.col < 0) break;
+        if (warp == 0) {
+            int cnt = 0;
+            for (int r = 0; r < C; ++r) {
+                Cand b = cand_none();
+                for (int i = lane; i < nw * C; i += 32) {
+                    const Cand c = wl[i];
+                    bool tk = c.col < 0;
+                    for (int u = 0; u < cnt; ++u) tk |= cols[u] == c.col;
+                    if (!tk && better(c, b)) b = c;
+                }
+                b = warp_best(b);
+                if (b.col < 0) break;
+                if (lane == 0) cols[cnt] = b.col;
+                __syncwarp();
+                ++cnt;
+            }
+            if (lane == 0) ncols = cnt;
+        }
+        __syncthreads();
     }
     const int m = ncols;
     for (int64_t e = tid; e < k * m; e += nt) {
@@ -2523,18 +2545,26 @@ __global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W,
         X[i + c * k] = layout == 0 ? W[i + cols[c] * ld] : W[i * ld + cols[c]];
     }
     __syncthreads();
-    // residuals against Q[:, :t+1]: classical Gram-Schmidt, twice, in slices of columns
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    // residuals against Q[:, :t+1]: classical Gram-Schmidt, twice, 32 columns of Q at a time
+    // (a warp per column of Q computes its dots with all m candidates)
     for (int pass = 0; pass < 2; ++pass) {
-        for (int64_t l0 = 0; l0 <= t; l0 += kSlice) {
-            const int64_t l1 = min(t + 1, l0 + kSlice);
-            for (int64_t e = warp; e < (l1 - l0) * m; e += nw) {
-                const int64_t l = l0 + e / m;
-                const int c = (int)(e % m);
-                double s = 0.0;
-                for (int64_t i = lane; i < k; i += 32) s = fma(Q[i + l * k], X[i + c * k], s);
-                s = warp_sum(s);
-                if (lane == 0) dots[(l - l0) * C + c] = s;
+        for (int64_t l0 = 0; l0 <= t; l0 += 32) {
+            const int64_t l1 = min(t + 1, l0 + 32);
+            for (int64_t l = l0 + warp; l < l1; l += nw) {
+                double sd[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) sd[c] = 0.0;
+                for (int64_t i = lane; i < k; i += 32) {
+                    const double ql = Q[i + l * k];
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        if (c < m) sd[c] = fma(ql, X[i + c * k], sd[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const double v = warp_sum(sd[c]);
+                    if (lane == 0 && c < m) dots[(l - l0) * C + c] = v;
+                }
             }
             __syncthreads();
             for (int64_t i = tid; i < k; i += nt) {
@@ -2553,35 +2583,71 @@ __global__ void __launch_bounds__(1024) k_sub_prep(const double* __restrict__ W,
             __syncthreads();
         }
     }
-    // modified Gram-Schmidt with reorthogonalisation among the candidates; a candidate whose
-    // residual is (numerically) in the span of the earlier ones is dropped
-    if (tid == 0) acc = 0;
+    // orthonormalise the candidates' residuals: Cholesky QR twice on the m x m Gram matrix,
+    // dropping (in the first pass) a candidate whose residual is numerically in the span of
+    // the earlier ones (Schur complement <= 1e-12 of its own mass)
+    if (tid == 0) nkeep = m;
+    for (int c = 0; c < C; ++c)
+        if (tid == c) keep[c] = c < m ? 1 : 0;
     __syncthreads();
-    for (int c = 0; c < m; ++c) {
-        double n0s = 0.0;
-        for (int64_t i = tid; i < k; i += nt) n0s = fma(X[i + c * k], X[i + c * k], n0s);
-        n0s = block_sum(n0s, red);
-        const int na = acc;
-        for (int pass = 0; pass < 2; ++pass)
-            for (int e = 0; e < na; ++e) {
-                double s = 0.0;
-                for (int64_t i = tid; i < k; i += nt) s = fma(X[i + e * k], X[i + c * k], s);
-                s = block_sum(s, red);
-                for (int64_t i = tid; i < k; i += nt) X[i + c * k] = fma(-s, X[i + e * k], X[i + c * k]);
-                __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+        const int mm = nkeep;
+        for (int e = warp; e < mm * mm; e += nw) {
+            const int i = e % mm, j = e / mm;
+            if (i > j) continue;
+            double sacc = 0.0;
+            for (int64_t r = lane; r < k; r += 32) sacc = fma(X[r + i * k], X[r + j * k], sacc);
+            sacc = warp_sum(sacc);
+            if (lane == 0) { Gm[i + j * C] = sacc; Gm[j + i * C] = sacc; }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // Cholesky G = R^T R (upper R) with the drop rule; kept columns compacted
+            int cnt = 0;
+            int idx[C];
+            for (int j = 0; j < mm; ++j) {
+                double d = Gm[j + j * C];
+                const double d0 = d;
+                double rj[C];
+                for (int i = 0; i < cnt; ++i) {
+                    double v = Gm[idx[i] + j * C];
+                    for (int l = 0; l < i; ++l) v -= Rm[l + i * C] * rj[l];
+                    rj[i] = v / Rm[i + i * C];
+                    d -= rj[i] * rj[i];
+                }
+                if (d > (pass == 0 ? 1e-12 : 1e-20) * d0 && d > 0.0) {
+                    for (int i = 0; i < cnt; ++i) Rm[i + cnt * C] = rj[i];
+                    Rm[cnt + cnt * C] = sqrt(d);
+                    idx[cnt] = j;
+                    ++cnt;
+                }
             }
-        double ns = 0.0;
-        for (int64_t i = tid; i < k; i += nt) ns = fma(X[i + c * k], X[i + c * k], ns);
-        ns = block_sum(ns, red);
-        if (ns > 1e-12 * n0s && ns > 0.0) {
-            const double inv = 1.0 / sqrt(ns);
-            for (int64_t i = tid; i < k; i += nt) X[i + na * k] = X[i + c * k] * inv;
-            __syncthreads();
-            if (tid == 0) acc = na + 1;
+            for (int i = 0; i < cnt; ++i) keep[i] = idx[i];
+            nkeep = cnt;
+        }
+        __syncthreads();
+        const int nk = nkeep;
+        // X[:, :nk] = X[:, keep] R^{-1} row by row (forward substitution on the row vector)
+        for (int64_t r = tid; r < k; r += nt) {
+            double y[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) y[c] = c < nk ? X[r + keep[c] * k] : 0.0;
+            double o[C];
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                if (j >= nk) break;
+                double v = y[j];
+                for (int l = 0; l < j; ++l) v -= o[l] * Rm[l + j * C];
+                o[j] = v / Rm[j + j * C];
+            }
+            // row r belongs to this thread alone: read (y) before write (o) suffices
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                if (c < nk) X[r + c * k] = o[c];
         }
         __syncthreads();
     }
-    const int n1 = acc;
+    const int n1 = nkeep;
     for (int64_t e = tid; e < k * n1; e += nt) E[e] = X[e];
     if (tid == 0) *nE = n1;
 }
@@ -2781,7 +2847,7 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
 // MF m-fragments cover 8 MF >= C + 1 rows. Row 0 of the product is R(t, j); rows 1..nE are
 // Z = E^T W. Then a shuffle gives each lane one column for the epilogue (downdate, guard flag,
 // candidate).
-template <int LAYOUT, int C>
+template <int LAYOUT, int C, int NF>
 __global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restrict__ W, int64_t k, int64_t N,
                                                           int64_t ld, int64_t t, const double* __restrict__ Q,
                                                           const double* __restrict__ E,
@@ -2814,18 +2880,18 @@ __global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restr
     double msum = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fk = lane & 3;
-    const int64_t ngroups = cdiv(N, 32);
+    const int64_t ngroups = cdiv(N, 8 * NF);
     for (int64_t g = (int64_t)blockIdx.x * (kThreads / 32) + warp; g < ngroups; g += (int64_t)gridDim.x * (kThreads / 32)) {
-        const int64_t j0 = g * 32;
-        double acc[MF][4][2];
+        const int64_t j0 = g * 8 * NF;
+        double acc[MF][NF][2];
 #pragma unroll
         for (int f = 0; f < MF; ++f)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) acc[f][n][0] = acc[f][n][1] = 0.0;
-        int64_t colb[4];
-        bool cok[4];
+            for (int n = 0; n < NF; ++n) acc[f][n][0] = acc[f][n][1] = 0.0;
+        int64_t colb[NF];
+        bool cok[NF];
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
+        for (int n = 0; n < NF; ++n) {
             colb[n] = j0 + 8 * n + fr;
             cok[n] = colb[n] < N;
         }
@@ -2834,34 +2900,35 @@ __global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restr
             return LAYOUT == 0 ? __ldg(W + i + colb[n] * ld) : __ldg(W + i * ld + colb[n]);
         };
         int64_t i0 = 0;
-        for (; i0 + 16 <= k4; i0 += 16) {  // four k4 steps per iteration: 16 loads in flight
-            double b[4][4];
+        constexpr int KS = 16 / NF;  // k4 steps per iteration: 16 loads in flight per lane
+        for (; i0 + 4 * KS <= k4; i0 += 4 * KS) {
+            double b[KS][NF];
 #pragma unroll
-            for (int s = 0; s < 4; ++s)
+            for (int s = 0; s < KS; ++s)
 #pragma unroll
-                for (int n = 0; n < 4; ++n) b[s][n] = ldb(i0 + 4 * s + fk, n);
+                for (int n = 0; n < NF; ++n) b[s][n] = ldb(i0 + 4 * s + fk, n);
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
+            for (int s = 0; s < KS; ++s) {
                 double a[MF];
 #pragma unroll
                 for (int f = 0; f < MF; ++f) a[f] = am[(8 * f + fr) * kq + i0 + 4 * s + fk];
 #pragma unroll
                 for (int f = 0; f < MF; ++f)
 #pragma unroll
-                    for (int n = 0; n < 4; ++n) dmma(acc[f][n], a[f], b[s][n]);
+                    for (int n = 0; n < NF; ++n) dmma(acc[f][n], a[f], b[s][n]);
             }
         }
         for (; i0 < k4; i0 += 4) {
-            double b[4];
+            double b[NF];
 #pragma unroll
-            for (int n = 0; n < 4; ++n) b[n] = ldb(i0 + fk, n);
+            for (int n = 0; n < NF; ++n) b[n] = ldb(i0 + fk, n);
             double a[MF];
 #pragma unroll
             for (int f = 0; f < MF; ++f) a[f] = am[(8 * f + fr) * kq + i0 + fk];
 #pragma unroll
             for (int f = 0; f < MF; ++f)
 #pragma unroll
-                for (int n = 0; n < 4; ++n) dmma(acc[f][n], a[f], b[n]);
+                for (int n = 0; n < NF; ++n) dmma(acc[f][n], a[f], b[n]);
         }
         // D fragment: lane holds rows (8 f + fr), columns j0 + 8 n + 2 fk + h
 #pragma unroll
@@ -2869,7 +2936,7 @@ __global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restr
             const int row = 8 * f + fr;
             if (row >= 1 && row <= nE) {
 #pragma unroll
-                for (int n = 0; n < 4; ++n)
+                for (int n = 0; n < NF; ++n)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int64_t col = j0 + 8 * n + 2 * fk + h;
@@ -2877,18 +2944,21 @@ __global__ void __launch_bounds__(kThreads) k_sub_miss_mma(const double* __restr
                     }
             }
         }
-        // row 0 (R(t, j)) lives in lanes 0..3 of m-fragment 0: lane c of the warp takes column j0 + c
-        double rv = 0.0;
+        // row 0 (R(t, j)) lives in lanes 0..3 of m-fragment 0: lane c takes columns j0 + 32 h + c
         const int src = (lane & 7) >> 1;
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-            const double v0 = __shfl_sync(0xffffffffu, acc[0][n][0], src);
-            const double v1 = __shfl_sync(0xffffffffu, acc[0][n][1], src);
-            if ((lane >> 3) == n) rv = (lane & 1) ? v1 : v0;
+        for (int h = 0; h < NF / 4; ++h) {
+            double rv = 0.0;
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+                const double v0 = __shfl_sync(0xffffffffu, acc[0][4 * h + n][0], src);
+                const double v1 = __shfl_sync(0xffffffffu, acc[0][4 * h + n][1], src);
+                if ((lane >> 3) == n) rv = (lane & 1) ? v1 : v0;
+            }
+            const int64_t j = j0 + 32 * h + lane;
+            const bool fl = j < N && sub_epilogue(t, j, N, jp, rv, diag, R, nu, cref, pos, best, msum);
+            append_flag(fl, j, flags, nflag);
         }
-        const int64_t j = j0 + lane;
-        const bool fl = j < N && sub_epilogue(t, j, N, jp, rv, diag, R, nu, cref, pos, best, msum);
-        append_flag(fl, j, flags, nflag);
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sd);
@@ -3371,8 +3441,10 @@ void WideQrcp::sub_step(int64_t t) {
         const int64_t k4 = (k_ + 3) & ~int64_t(3);
         const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
         const size_t msm = sizeof(double) * (size_t)(8 * MF * kq);
-        auto mk = layout_ == Layout::Row ? (C == 16 ? k_sub_miss_mma<1, 16> : k_sub_miss_mma<1, 8>)
-                                         : (C == 16 ? k_sub_miss_mma<0, 16> : k_sub_miss_mma<0, 8>);
+        // Row W: eight 8-column fragments per warp (4 rows x 512 contiguous bytes per step, like
+        // the FMA stream's row segments); Col W: four
+        auto mk = layout_ == Layout::Row ? (C == 16 ? k_sub_miss_mma<1, 16, 8> : k_sub_miss_mma<1, 8, 8>)
+                                         : (C == 16 ? k_sub_miss_mma<0, 16, 4> : k_sub_miss_mma<0, 8, 4>);
         allow_smem(mk, msm);
         TTG_LAUNCH(mk, ncand_, kThreads, msm, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), subi_.get(),
                    subi_.get() + 1, Z_.get(), diag_.get(), piv_.get(), R_.get(), nu_.get(), cref_.get(), pos_.get(),
