@@ -33,6 +33,10 @@ struct NcclApi {
     nccl_result_t (*all_gather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
     nccl_result_t (*comm_destroy)(nccl_comm_t) = nullptr;
     const char* (*error_string)(nccl_result_t) = nullptr;
+    nccl_result_t (*send)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*recv)(void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*group_start)() = nullptr;
+    nccl_result_t (*group_end)() = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -48,6 +52,11 @@ const NcclApi& nccl() {
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
         if (!a.get_unique_id || !a.comm_init_rank || !a.all_gather || !a.comm_destroy || !a.error_string)
             resource_error("NCCL library lacks a required symbol");
+        // point-to-point (NCCL >= 2.7); absent symbols leave has_p2p() false
+        a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+        a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+        a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+        a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
         return a;
     }();
     return api;
@@ -71,6 +80,14 @@ public:
     int size() const override { return size_; }
     void allgather(const void* send, void* recv, size_t bytes) override {
         nccl_check(nccl().all_gather(send, recv, bytes, kNcclInt8, comm_, stream()), "ncclAllGather");
+    }
+    bool has_p2p() const override { return nccl().send && nccl().recv && nccl().group_start && nccl().group_end; }
+    void sendrecv(const void* send, int to, void* recv, int from, size_t bytes) override {
+        if (to < 0 && from < 0) return;
+        nccl_check(nccl().group_start(), "ncclGroupStart");
+        if (to >= 0) nccl_check(nccl().send(send, bytes, kNcclInt8, to, comm_, stream()), "ncclSend");
+        if (from >= 0) nccl_check(nccl().recv(recv, bytes, kNcclInt8, from, comm_, stream()), "ncclRecv");
+        nccl_check(nccl().group_end(), "ncclGroupEnd");
     }
 
 private:
@@ -123,6 +140,28 @@ public:
         sh_->barrier();
         TTG_CUDA(cudaMemcpyAsync(recv, sh_->stage, total, cudaMemcpyDeviceToDevice, stream()));
         TTG_CUDA(cudaStreamSynchronize(stream()));
+        sh_->barrier();
+    }
+    bool has_p2p() const override { return true; }
+    // every sender parks its buffer in its own stage slot; receivers copy from the sender's slot
+    void sendrecv(const void* send, int to, void* recv, int from, size_t bytes) override {
+        const size_t total = bytes * (size_t)sh_->n;
+        sh_->barrier();
+        if (rank_ == 0 && sh_->cap < total) {
+            if (sh_->stage) TTG_CUDA(cudaFree(sh_->stage));
+            TTG_CUDA(cudaMalloc(reinterpret_cast<void**>(&sh_->stage), total));
+            sh_->cap = total;
+        }
+        sh_->barrier();
+        if (to >= 0) {
+            TTG_CUDA(cudaMemcpyAsync(sh_->stage + bytes * rank_, send, bytes, cudaMemcpyDeviceToDevice, stream()));
+            TTG_CUDA(cudaStreamSynchronize(stream()));
+        }
+        sh_->barrier();
+        if (from >= 0) {
+            TTG_CUDA(cudaMemcpyAsync(recv, sh_->stage + bytes * from, bytes, cudaMemcpyDeviceToDevice, stream()));
+            TTG_CUDA(cudaStreamSynchronize(stream()));
+        }
         sh_->barrier();
     }
 

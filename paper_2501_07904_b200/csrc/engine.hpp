@@ -27,6 +27,13 @@ public:
     virtual int size() const = 0;
     // recv (device, size() * bytes) <- every rank's send (device, bytes), in rank order.
     virtual void allgather(const void* send, void* recv, size_t bytes) = 0;
+    // Point-to-point round (every rank calls it): send `bytes` to rank `to` and receive `bytes`
+    // from rank `from`; -1 skips either side. Only when has_p2p().
+    virtual bool has_p2p() const { return false; }
+    virtual void sendrecv(const void* send, int to, void* recv, int from, size_t bytes) {
+        (void)send; (void)to; (void)recv; (void)from; (void)bytes;
+        fail(8, "this communicator has no point-to-point transport");
+    }
 };
 // Sum of one double per rank, combined in rank order (host result, identical everywhere).
 double global_sum(Comm& comm, double local);

@@ -275,6 +275,33 @@ struct WidePass1 final : Pass1 {
         if (!e.sharded()) return tsqr_r(e.R(), e.N(), s, e.N(), RB);
         Comm& comm = *e.comm();
         const int G = comm.size();
+        if (comm.has_p2p() && G > 1) {
+            // binary TSQR tree over the ranks (log2 G point-to-point rounds): at round l, rank
+            // g with g % 2l == 0 receives the triangle of rank g + l, stacks the two and
+            // refactors; rank 0's final triangle is then broadcast (all-gather, block 0)
+            DevBuf<double> mine((size_t)(s * s)), other((size_t)(s * s)), stack((size_t)(2 * s * s));
+            tsqr_r(e.R(), e.N(), s, e.N(), mine.get());
+            const int g = comm.rank();
+            for (int l = 1; l < G; l <<= 1) {
+                const bool recv = g % (2 * l) == 0 && g + l < G;
+                const bool send = g % (2 * l) == l;
+                comm.sendrecv(mine.get(), send ? g - l : -1, other.get(), recv ? g + l : -1,
+                              sizeof(double) * (size_t)(s * s));
+                if (recv) {
+                    TTG_CUDA(cudaMemcpy2DAsync(stack.get(), sizeof(double) * 2 * s, mine.get(), sizeof(double) * s,
+                                               sizeof(double) * s, s, cudaMemcpyDeviceToDevice, stream()));
+                    TTG_CUDA(cudaMemcpy2DAsync(stack.get() + s, sizeof(double) * 2 * s, other.get(),
+                                               sizeof(double) * s, sizeof(double) * s, s, cudaMemcpyDeviceToDevice,
+                                               stream()));
+                    tsqr_r(stack.get(), 2 * s, s, 2 * s, mine.get());
+                }
+            }
+            DevBuf<double> all((size_t)(G * s * s));
+            comm.allgather(mine.get(), all.get(), sizeof(double) * (size_t)(s * s));
+            TTG_CUDA(cudaMemcpyAsync(RB, all.get(), sizeof(double) * (size_t)(s * s), cudaMemcpyDeviceToDevice,
+                                     stream()));
+            return;
+        }
         DevBuf<double> mine((size_t)(s * s)), all((size_t)(G * s * s)), stack((size_t)(G * s * s));
         tsqr_r(e.R(), e.N(), s, e.N(), mine.get());
         comm.allgather(mine.get(), all.get(), sizeof(double) * (size_t)(s * s));
