@@ -2732,7 +2732,7 @@ __global__ void __launch_bounds__(kThreads, (LAYOUT == 1 && C == 8) ? 2 : 1) k_s
                     if (pair16 && two) {
                         const double2* w2 = reinterpret_cast<const double2*>(W) + g;
                         const int64_t ld2 = ld / 2;
-#pragma unroll 4
+#pragma unroll 8
                         for (int64_t i = 0; i < k; ++i) {
                             const double2 x = __ldg(w2 + i * ld2);
                             const double qi = q[i];
@@ -3441,9 +3441,9 @@ void WideQrcp::sub_step(int64_t t) {
         const int64_t k4 = (k_ + 3) & ~int64_t(3);
         const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
         const size_t msm = sizeof(double) * (size_t)(8 * MF * kq);
-        // Row W: eight 8-column fragments per warp (4 rows x 512 contiguous bytes per step, like
-        // the FMA stream's row segments); Col W: four
-        auto mk = layout_ == Layout::Row ? (C == 16 ? k_sub_miss_mma<1, 16, 8> : k_sub_miss_mma<1, 8, 8>)
+        // four 8-column fragments per warp (eight measured slower on Row W: config 3 0.37 ->
+        // 0.45 ms, config 5 2.4 -> 3.0 ms per pass)
+        auto mk = layout_ == Layout::Row ? (C == 16 ? k_sub_miss_mma<1, 16, 4> : k_sub_miss_mma<1, 8, 4>)
                                          : (C == 16 ? k_sub_miss_mma<0, 16, 4> : k_sub_miss_mma<0, 8, 4>);
         allow_smem(mk, msm);
         TTG_LAUNCH(mk, ncand_, kThreads, msm, stream(), W_, k_, N_, ld_, t, qptr(), E_.get(), subi_.get(),
