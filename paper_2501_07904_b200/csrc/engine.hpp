@@ -70,6 +70,8 @@ struct ShardSpec {
 // column, then streams its own columns. Q and the reflectors are replicated; R rows and
 // norms stay local.
 // ---------------------------------------------------------------------------
+struct LzArgs;
+
 class WideQrcp {
 public:
     // subspace: allow the subspace (lazy-exact) stream (fixed-rank cuts; see qrcp_wide.cu)
@@ -136,6 +138,15 @@ private:
     DevBuf<int64_t> pos_, perm_, piv_, flags_;
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;
+    // candidate (lazy-exact) pivoting for narrow W (qrcp_wide.cu, k_lz_*)
+    bool lz_ = false;
+    DevBuf<int64_t> lzst_, lzidx_, lzposc_;
+    DevBuf<Cand> lzubest_;
+    DevBuf<double> lzsd_, lzwc_, lznuc_, lzcrefc_;
+    DevBuf<int> lzhist_;
+    LzArgs lz_args();
+    void lz_step(int64_t t);
+    void lz_refresh(int64_t t1, bool force);
 };
 
 // ---------------------------------------------------------------------------
@@ -203,7 +214,9 @@ private:
     int nblk_ = 0;
     int64_t rows_per_blk_ = 0;
     bool col_mode_ = false;  // one CTA per trailing column per step (N <= 25600)
+    bool run_persist(int64_t steps);
     DevBuf<double> nu_, cref_, R_, part_, tq_, beta_, v0_, pnorm_;
+    DevBuf<double> Vp_, F_;  // persistent blocked engine (panel state)
     DevBuf<int64_t> colmap_, pos_;
     DevBuf<int> flag_;
 };

@@ -13,12 +13,17 @@
 //   K3 apply   (row blocks)  v_i = x_i / v0 stored in the pivot column; c_j(i) -= t_j v_i
 //                            (factor.cpp:43-58, no contraction)
 //   K4 guard   (row blocks + 1 CTA, only when flagged) recompute flagged norms from rows > t
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "engine.hpp"
 
 namespace ttg {
 namespace {
+namespace cg = cooperative_groups;
 
 constexpr int kT = 256;
 constexpr int kSub = 1024;  // rows staged per sub-block in K1/K4
@@ -629,6 +634,333 @@ __global__ void k_larft(const double* __restrict__ G, const double* __restrict__
     for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) T[e] = Ts[(e % kb) + (e / kb) * 65];
 }
 
+// ---- persistent blocked steps (one cooperative launch per run) --------------------------
+// Per-step application of H_t to every trailing column reads AND writes the whole trailing
+// matrix once per step. A panel of kb steps (the dlaqps organisation) instead leaves the
+// trailing columns untouched below the panel's rows and keeps the pending update in
+// factored form, B <- B - V F^T (V: the panel's reflectors, F(j, l) = beta_l
+// (H_{l-1}..H_0 b_j)^T v_l), so a step only READS the trailing matrix, and the whole update
+// lands once per panel as FP64 tensor-core (DMMA) tiles. The grid stays resident for the run:
+// two grid barriers per step, every per-column quantity (norm, position, the column's row of
+// F) in the owning CTA's shared memory. Exact arithmetic gives factor.cpp's values; the
+// rounding differs from its column-by-column order at the ulp level.
+//  * physical column j belongs to CTA j mod G for the run (pivoting relabels positions, so a
+//    pivot only leaves its owner's list);
+//  * phase P (after barrier A): every CTA reads the G candidate records and picks the same
+//    pivot (factor.cpp:85-87); CTA g brings rows slice g of the pivot column up to date,
+//    x = b_p - V F(p, :)^T, and publishes its partial sigma, V^T x (and x(t) if it holds row
+//    t); the owners update the position map (factor.cpp:88-93);
+//  * phase G (after barrier B): every CTA combines the G partials in CTA order and rebuilds
+//    the same reflector (make_householder, factor.cpp:24-38), stages v, and runs the
+//    read-only GEMV, F(j, k), R(t, j), downdate and guard (factor.cpp:98-107) for its own
+//    columns; publishes its best candidate;
+//  * panel end: each CTA applies B(t1:, j) -= V F(j, :)^T to its own columns as DMMA tiles
+//    (V from L2, F from shared memory) and stores the finished reflectors in their pivot
+//    columns.
+constexpr int kNb = 32;  // reflectors per panel
+
+struct BlkView {
+    double* B;
+    int64_t N, n, ld;
+    double* nu;
+    double* cref;
+    int64_t* colmap;
+    int64_t* pos;
+    double* beta;
+    double* v0;
+    double* pnorm;
+    double* Vp;  // N x kNb, column l = reflector t0 + l (1 at its row, 0 above)
+    double* F;   // n x kNb by physical column
+};
+
+constexpr int kPT = 512;  // threads per CTA
+
+struct PersistArgs {
+    BlkView s;
+    double* part;    // [G][kNb + 2]: sigma, V^T x (kNb), x(t)
+    Cand* pcand;     // [2][G]
+    int64_t t0, t1;
+    int nloc;        // owned-column capacity per CTA
+};
+
+__global__ void __launch_bounds__(kPT, 1) k_qrcp_persist(PersistArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double psm[];
+    const BlkView& s = A.s;
+    const int64_t N = s.N, n = s.n;
+    const int G = gridDim.x, me = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kPT / 32;
+    const int nloc = A.nloc;
+    // shared: vsm[N] | ofl[nloc * kNb] (F rows of owned columns) | onu | ocref [nloc] | ocol | opos (int64)
+    double* vsm = psm;
+    double* ofl = vsm + N;
+    double* onu = ofl + (size_t)nloc * kNb;
+    double* ocref = onu + nloc;
+    int64_t* ocol = reinterpret_cast<int64_t*>(ocref + nloc);
+    int64_t* opos = ocol + nloc;
+    __shared__ int cnt_s;
+    __shared__ Cand sc[NW];
+    __shared__ double red[NW];
+    __shared__ double fp[kNb];
+    __shared__ double hsm[3 + kNb];
+    __shared__ double vt[kNb];
+    __shared__ double comb[kNb + 2];
+    __shared__ Cand win_s;
+
+    if (tid == 0) {
+        int c = 0;
+        for (int64_t j = me; j < n; j += G) {
+            const int64_t q = s.pos[j];
+            if (q >= A.t0) {
+                ocol[c] = j;
+                opos[c] = q;
+                onu[c] = s.nu[j];
+                ocref[c] = s.cref[j];
+                ++c;
+            }
+        }
+        cnt_s = c;
+    }
+    __syncthreads();
+    int cnt = cnt_s;
+    auto publish = [&](int64_t slot) {
+        Cand b = cand_none();
+        for (int l = tid; l < cnt; l += kPT) {
+            const Cand c{onu[l], opos[l], ocol[l]};
+            if (better(c, b)) b = c;
+        }
+        b = block_best(b, sc);
+        if (tid == 0) A.pcand[slot * G + me] = b;
+    };
+    publish(A.t0 & 1);
+    for (int64_t t0 = A.t0; t0 < A.t1; t0 += kNb) {
+        const int kb = (int)min((int64_t)kNb, A.t1 - t0);
+        // panel start: V's rows above each reflector read as zero
+        for (int64_t e = (int64_t)me * kPT + tid; e < N * kb; e += (int64_t)G * kPT) s.Vp[e] = 0.0;
+        grid.sync();
+        for (int k = 0; k < kb; ++k) {
+            const int64_t t = t0 + k;
+            // ---- phase P ----
+            if (warp == 0) {
+                Cand b = cand_none();
+                for (int g = lane; g < G; g += 32) {
+                    const Cand* cp = A.pcand + (t & 1) * G + g;
+                    const Cand c{__ldcg(&cp->nu), __ldcg(&cp->pos), __ldcg(&cp->col)};
+                    if (better(c, b)) b = c;
+                }
+                b = warp_best(b);
+                if (lane == 0) win_s = b;
+            }
+            __syncthreads();
+            const Cand win = win_s;
+            const int64_t piv = win.col, pp = win.pos;
+            if (tid < k) fp[tid] = __ldcg(s.F + piv + (int64_t)tid * n);
+            // bookkeeping (factor.cpp:88-93): the pivot leaves its owner's list; the column
+            // at position t moves to pp
+            if (tid == 0) {
+                int c = cnt;
+                for (int l = 0; l < c; ++l) {
+                    if (ocol[l] == piv) {
+                        s.colmap[t] = piv;
+                        s.pos[piv] = t;
+                        s.pnorm[t] = onu[l];
+                        --c;
+                        ocol[l] = ocol[c]; opos[l] = opos[c]; onu[l] = onu[c]; ocref[l] = ocref[c];
+                        for (int q = 0; q < k; ++q) ofl[(size_t)l * kNb + q] = ofl[(size_t)c * kNb + q];
+                        --l;
+                        continue;
+                    }
+                    if (opos[l] == t && pp != t) {
+                        opos[l] = pp;
+                        s.colmap[pp] = ocol[l];
+                        s.pos[ocol[l]] = pp;
+                    }
+                }
+                cnt_s = c;
+            }
+            __syncthreads();
+            cnt = cnt_s;
+            {
+                // rows slice `me` of [t, N): x = b_p - V F(p, :)^T and the partial sums
+                const int64_t per = cdiv(N - t, G);
+                const int64_t r0 = t + (int64_t)me * per, r1 = min(N, r0 + per);
+                double* x = s.B + piv * s.ld;
+                double* part = A.part + (size_t)me * (kNb + 2);
+                for (int64_t i = r0 + tid; i < r1; i += kPT) {
+                    double xi = __ldcg(x + i);
+                    double vl[kNb];
+#pragma unroll
+                    for (int l = 0; l < kNb; ++l) vl[l] = l < k ? __ldcg(s.Vp + i + l * N) : 0.0;
+#pragma unroll
+                    for (int l = 0; l < kNb; ++l)
+                        if (l < k) xi = fma(-vl[l], fp[l], xi);
+                    __stcg(x + i, xi);
+                    vsm[i - r0] = xi;  // scratch: this slice's x
+                    if (i == t) part[kNb + 1] = xi;
+                }
+                __syncthreads();
+                // sigma and V(t+1:, l)^T x over the slice: a warp per quantity, lanes over rows
+                for (int q = warp; q <= k; q += NW) {
+                    double a = 0.0;
+                    for (int64_t i = max(r0, t + 1) + lane; i < r1; i += 32) {
+                        const double xi = vsm[i - r0];
+                        a = fma(q == 0 ? xi : __ldcg(s.Vp + i + (q - 1) * N), xi, a);
+                    }
+                    a = warp_sum(a);
+                    if (lane == 0) part[q] = a;
+                }
+            }
+            grid.sync();  // barrier B
+            // ---- phase G ----
+            for (int q = warp; q <= k; q += NW) {  // combine the G partials in CTA order
+                double a = 0.0;
+                for (int g = lane; g < G; g += 32) a += __ldcg(A.part + (size_t)g * (kNb + 2) + q);
+                a = warp_sum(a);
+                if (lane == 0) comb[q] = a;
+            }
+            if (tid < k) vt[tid] = __ldcg(s.Vp + t + (int64_t)tid * N);
+            __syncthreads();
+            if (tid == 0) {
+                const double sg = comb[0], alpha = __ldcg(A.part + (kNb + 1));  // CTA 0 holds row t
+                double beta = 0.0, v0 = 1.0, rkk = alpha;
+                if (N - t > 1 && sg != 0.0) {  // make_householder (factor.cpp:24-38)
+                    const double mu = __dsqrt_rn(__dadd_rn(__dmul_rn(alpha, alpha), sg));
+                    const double smu = copysign(mu, alpha);
+                    v0 = __dadd_rn(alpha, smu);
+                    beta = __ddiv_rn(__dmul_rn(v0, v0), __dmul_rn(smu, v0));
+                    rkk = -smu;
+                }
+                hsm[0] = beta;
+                hsm[1] = v0;
+                hsm[2] = rkk;
+            }
+            __syncthreads();
+            const double beta = hsm[0], v0 = hsm[1];
+            if (tid < k) hsm[3 + tid] = -beta * (vt[tid] + comb[1 + tid] / v0);
+            {
+                // v over rows t.. (v_t = 1); this CTA stores its rows slice of V's column k
+                const double* x = s.B + piv * s.ld;
+                const int64_t per = cdiv(N - t, G);
+                const int64_t r0 = t + (int64_t)me * per, r1 = min(N, r0 + per);
+                for (int64_t i = t + tid; i < N; i += kPT) {
+                    const double v = i == t ? 1.0 : (beta != 0.0 ? __ddiv_rn(__ldcg(x + i), v0) : 0.0);
+                    vsm[i - t] = v;
+                    if (i >= r0 && i < r1) s.Vp[i + (int64_t)k * N] = v;
+                }
+            }
+            if ((int)(piv % G) == me && tid == 0) {
+                s.beta[t] = beta;
+                s.v0[t] = v0;
+                s.B[t + piv * s.ld] = hsm[2];
+            }
+            __syncthreads();
+            // own trailing columns: GEMV, epilogue, downdate + guard
+            for (int l = warp; l < cnt; l += NW) {
+                const int64_t j = ocol[l];
+                const double* c = s.B + j * s.ld;
+                double a = 0.0;
+                if (beta != 0.0) {
+#pragma unroll 16
+                    for (int64_t i = t + lane; i < N; i += 32) a = fma(vsm[i - t], __ldcg(c + i), a);
+                    a = warp_sum(a);
+                }
+                double p1 = 0.0, p2 = 0.0;
+                if (lane < k) {
+                    const double fl = ofl[(size_t)l * kNb + lane];
+                    p1 = fl * hsm[3 + lane];
+                    p2 = vt[lane] * fl;
+                }
+                p1 = warp_sum(p1);
+                p2 = warp_sum(p2);
+                const double f = fma(beta, a, p1);
+                const double rt = __dsub_rn(__dsub_rn(__ldcg(c + t), p2), f);
+                double nv = __dsub_rn(onu[l], __dmul_rn(rt, rt));
+                const bool flag = nv < __dmul_rn(1e-16, ocref[l]) || nv < 0.0;
+                if (flag) {  // guard (factor.cpp:103-105): |b_j(t+1:) - V F(j, :)^T|^2
+                    double q = 0.0;
+                    for (int64_t i = t + 1 + lane; i < N; i += 32) {
+                        double y = __ldcg(c + i);
+                        for (int m = 0; m < k; ++m) y = fma(-__ldcg(s.Vp + i + (int64_t)m * N), ofl[(size_t)l * kNb + m], y);
+                        y = fma(-vsm[i - t], f, y);
+                        q = fma(y, y, q);
+                    }
+                    nv = warp_sum(q);
+                }
+                if (lane == 0) {
+                    ofl[(size_t)l * kNb + k] = f;
+                    s.F[j + (int64_t)k * n] = f;
+                    s.B[t + j * s.ld] = rt;
+                    onu[l] = nv;
+                    if (flag) ocref[l] = nv;
+                }
+            }
+            __syncthreads();
+            publish((t + 1) & 1);
+            grid.sync();  // barrier A
+        }
+        // ---- panel end: own trailing columns B(t1:, j) -= V(t1:, :kb) F(j, :kb)^T (DMMA) ----
+        const int64_t t1 = t0 + kb;
+        if (t1 < N && t1 < n) {
+            const int ar = lane >> 2, ak = lane & 3;
+            const int64_t nrt = cdiv(N - t1, 32), nct = cdiv(cnt, 8);
+            for (int64_t u = warp; u < nrt * nct; u += NW) {
+                const int64_t rt = u % nrt, ct = u / nrt;
+                const int64_t row0 = t1 + rt * 32;
+                const int cl = (int)(ct * 8 + ar);             // B fragment column (owned index)
+                const bool cok = cl < cnt;
+                double d[4][2];
+                int64_t dj[2];
+                bool dok[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int ce = (int)(ct * 8 + 2 * ak + e);
+                    dok[e] = ce < cnt;
+                    dj[e] = dok[e] ? ocol[ce] : 0;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int64_t r = row0 + a * 8 + ar;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) d[a][e] = (r < N && dok[e]) ? -__ldcg(s.B + r + dj[e] * s.ld) : 0.0;
+                }
+                for (int kk = 0; kk < kb; kk += 4) {
+                    const int kq = kk + ak;
+                    const double bf = (cok && kq < kb) ? ofl[(size_t)cl * kNb + kq] : 0.0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const int64_t r = row0 + a * 8 + ar;
+                        const double af = (r < N && kq < kb) ? __ldcg(s.Vp + r + (int64_t)kq * N) : 0.0;
+                        dmma(d[a], af, bf);
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int64_t r = row0 + a * 8 + ar;
+                    if (r >= N) continue;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (dok[e]) __stcg(s.B + r + dj[e] * s.ld, -d[a][e]);
+                }
+            }
+        }
+        // the panel's reflectors into their pivot columns (owners), below the diagonal
+        for (int u = 0; u < kb; ++u) {
+            const int64_t t = t0 + u;
+            const int64_t pj = __ldcg(s.colmap + t);
+            if ((int)(pj % G) != me) continue;
+            if (__ldcg(s.beta + t) == 0.0) continue;
+            double* x = s.B + pj * s.ld;
+            for (int64_t i = t + 1 + tid; i < N; i += kPT) x[i] = __ldcg(s.Vp + i + (int64_t)u * N);
+        }
+        grid.sync();
+    }
+    for (int l = tid; l < cnt; l += kPT) {
+        s.nu[ocol[l]] = onu[l];
+        s.cref[ocol[l]] = ocref[l];
+    }
+}
+
 TallView view_of(double* B, int64_t N, int64_t n, int64_t ld, DevBuf<double>& nu, DevBuf<double>& cref,
                  DevBuf<int64_t>& colmap, DevBuf<int64_t>& pos, DevBuf<double>& part, DevBuf<double>& tq,
                  DevBuf<double>& R, int64_t ldr, DevBuf<double>& beta, DevBuf<double>& v0, DevBuf<double>& pn,
@@ -662,8 +994,50 @@ TallQrcp::TallQrcp(double* B, int64_t N, int64_t n, int64_t ld) : B_(B), N_(N), 
     TTG_LAUNCH(k_norm_fin, 1, kT, 0, stream(), s, nblk_);
 }
 
+// Persistent blocked run (k_qrcp_persist); false when the shape does not suit it (fewer
+// columns than CTAs, or the pivot column does not fit in shared memory).
+bool TallQrcp::run_persist(int64_t steps) {
+    const int G = sm_count();
+    if (n_ < G || N_ > 16384) return false;
+    const int64_t nloc = cdiv(n_, G);
+    const size_t smem = sizeof(double) * (size_t)(N_ + nloc * kNb + 2 * nloc) + sizeof(int64_t) * 2 * (size_t)nloc;
+    if (smem > 200 * 1024) return false;
+    raise_smem_limit(reinterpret_cast<const void*>(k_qrcp_persist));
+    int occ = 0;
+    TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qrcp_persist, kPT, smem));
+    if (occ < 1) return false;
+    if (!Vp_.get()) {
+        Vp_.alloc((size_t)N_ * kNb);
+        F_.alloc((size_t)n_ * kNb);
+    }
+    DevBuf<double> part((size_t)G * (kNb + 2));
+    DevBuf<Cand> pc((size_t)2 * G);
+    BlkView s{B_, N_, n_, ld_, nu_.get(), cref_.get(), colmap_.get(), pos_.get(), beta_.get(), v0_.get(),
+              pnorm_.get(), Vp_.get(), F_.get()};
+    PersistArgs A{s, part.get(), pc.get(), steps_, steps, (int)nloc};
+    void* args[] = {&A};
+    PhaseTimer pt("in-place persistent (blocked)");
+    TTG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_qrcp_persist), dim3((unsigned)G), dim3(kPT),
+                                         args, smem, stream()));
+    count_launch();
+    if (debug_sync()) check_sync("k_qrcp_persist", __FILE__, __LINE__);
+    steps_ = std::max(steps_, steps);
+    return true;
+}
+
 void TallQrcp::run(int64_t steps) {
     steps = std::min(steps, p_);
+    // The persistent blocked engine (DMMA panel updates) measured faster than the per-step
+    // kernels only on square matrices (config 4's 4096 x 4096 pass 2: 116 vs 131 ms) and
+    // slower on every other config-4 shape (the per-step latency chain, not the trailing
+    // traffic, bounds both). TTG_TALL_ENGINE=steps / persist forces one (A/B, tests).
+    static const int engine = [] {
+        const char* e = std::getenv("TTG_TALL_ENGINE");
+        if (!e) return -1;
+        return std::string(e) == "steps" ? 0 : 1;
+    }();
+    const bool persist = engine == 1 || (engine < 0 && N_ == n_ && n_ >= 2048);
+    if (steps > steps_ && persist && run_persist(steps)) return;
     TallView s = view_of(B_, N_, n_, ld_, nu_, cref_, colmap_, pos_, part_, tq_, R_, p_, beta_, v0_, pnorm_, flag_,
                          rows_per_blk_);
     if (col_mode_) {
@@ -763,7 +1137,7 @@ void TallQrcp::form_q(double* Q, int64_t q, int64_t ldq) {
     TTG_LAUNCH(k_eye, (int)cdiv(N_ * q, 256), 256, 0, stream(), Q, N_, q, ldq);
     std::vector<double> hb = beta_.to_host(p_);
     const int64_t top = std::min(q, steps_);
-    if (col_mode_ && top >= 2 * kQBlock && q >= 2 * kQBlock) {
+    if (top >= 2 * kQBlock && q >= 2 * kQBlock) {
         const int64_t nbk = cdiv(top, kQBlock);
         DevBuf<double> V((size_t)(N_ * kQBlock)), G((size_t)(kQBlock * kQBlock)), T((size_t)(kQBlock * kQBlock)),
             W((size_t)(kQBlock * q)), W2((size_t)(kQBlock * q));

@@ -710,6 +710,335 @@ __global__ void k_set_identity(double* Qx, int64_t k) {
 }
 
 // ---------------------------------------------------------------------------
+// Candidate (lazy-exact) pivoting for narrow W (k <= 32, fixed rank, N >= 1M: the first cut
+// of config 3, W = 24 x 7,962,624). A plain step streams all of W to produce row t of R,
+// i.e. every unpivoted column's downdated norm. Norms only fall (nu_j -= R(t, j)^2), so
+// after an exact pass at step t0 no column outside S = {j : nu_j(t0) > M} can reach M before
+// it is touched again. The engine keeps S (<= kLzCap columns, gathered into a compact copy)
+// and its norms exact step by step; while the best member of S beats M it is the true
+// pivot, and a step reads only S. A miss (or the end of the run) triggers one pass over W
+// that replays rows t0..t-1 of R for every column with the same arithmetic the S updates
+// use (so R, the norms and the guard recomputes are those of a plain step-by-step run
+// with that arithmetic) and picks a new S from a histogram of the norms. Config 3: 4-5
+// passes over W instead of 21. The steps' reflectors are the plain engine's.
+// ---------------------------------------------------------------------------
+constexpr int kLzK = 32;            // largest k
+constexpr int kLzBins = 512;        // 1/32-octave bins below the largest norm
+constexpr int64_t kLzCap = 65536;   // target |S|
+constexpr int64_t kLzBuf = 131072;  // |S| capacity (bin edges vs. exact comparisons)
+
+}  // namespace
+
+struct LzArgs {
+    const double* W;
+    int64_t k, N, ld;
+    const double* Q;    // k x cap, column t = q_t
+    const double* diag;
+    const int64_t* pos;
+    double* R;          // row t at R + t * N
+    double* nu;
+    double* cref;
+    Cand* cand;         // candidate slots [0, nslots)
+    double* mass;
+    int nslots;
+    int64_t* st;        // [0] miss flag, [1] disabled, [2] |S|, [3] t of the last exact pass
+    double* sd;         // [0] M, [1] largest original norm^2, [2] largest current norm^2
+    int* hist;
+    int64_t* idx;       // S
+    double* wc;         // S's columns, row-major: wc[i * kLzBuf + c]
+    double* nuc;
+    double* crefc;
+    int64_t* posc;      // S's current positions (-1 once pivoted)
+    Cand* ubest;        // k_lz_update's per-CTA best member
+    int nubest;
+};
+
+namespace {
+
+// Guard recompute (factor.cpp:103-105): |w - Q[:, :s+1] Q[:, :s+1]^T w|^2 by modified
+// Gram-Schmidt (k_guard_lane's arithmetic); w(i) = wp[i * stride]. Rare: kept out of line
+// so the streaming loops keep their registers.
+__device__ __noinline__ double lz_resid(const double* __restrict__ Q, int64_t k, int64_t s, const double* wp,
+                                        int64_t stride) {
+    double x[kLzK];  // dynamically indexed: local memory, so the callers keep their registers
+#pragma unroll 1
+    for (int64_t i = 0; i < k; ++i) x[i] = wp[i * stride];
+#pragma unroll 1
+    for (int64_t l = 0; l <= s; ++l) {
+        const double* q = Q + l * k;
+        double z = 0.0;
+#pragma unroll 1
+        for (int64_t i = 0; i < k; ++i) z = fma(q[i], x[i], z);
+#pragma unroll 1
+        for (int64_t i = 0; i < k; ++i) x[i] = fma(-q[i], z, x[i]);
+    }
+    double sq = 0.0;
+#pragma unroll 1
+    for (int64_t i = 0; i < k; ++i) sq = fma(x[i], x[i], sq);
+    return sq;
+}
+
+// Downdate + guard of one column for step s (factor.cpp:101-106); the column at wp (stride).
+__device__ __forceinline__ void lz_downdate(const LzArgs& A, int64_t s, double r, const double* wp, int64_t stride,
+                                            double& nuj, double& crefj) {
+    const double nv = __dsub_rn(nuj, __dmul_rn(r, r));
+    if (nv < __dmul_rn(1e-16, crefj) || nv < 0.0) {
+        nuj = lz_resid(A.Q, A.k, s, wp, stride);
+        crefj = nuj;
+    } else {
+        nuj = nv;
+    }
+}
+
+// Step 1 (1 CTA): the pivot candidate and the hit test. The first choice takes the best member
+// of S from k_lz_update's per-CTA records (S's norms are exact through the previous step); a
+// hit if it beats M. FINAL (after this step's exact pass): the refresh's slots hold the true
+// best, which belongs to the new S if it beats the new M; otherwise S is unusable and the
+// engine falls back to an exact pass per step (those slots then give the pivot).
+template <bool FINAL>
+__global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
+    __shared__ Cand sc[32];
+    if (FINAL && A.st[0] == 0) return;  // decided by the first choice
+    if (A.st[1]) {  // fallback: an exact pass per step, its slots hold the pivot
+        if (threadIdx.x == 0) {
+            A.st[0] = 1;
+            if (FINAL) A.st[3] = t;
+        }
+        return;
+    }
+    Cand b = cand_none();
+    const Cand* rec = FINAL ? A.cand : A.ubest;
+    const int nrec = FINAL ? A.nslots : (A.st[2] > 0 ? A.nubest : 0);
+    for (int g = threadIdx.x; g < nrec; g += blockDim.x)
+        if (better(rec[g], b)) b = rec[g];
+    b = block_best(b, sc);
+    const double M = A.sd[0];
+    const bool ok = A.st[2] <= kLzBuf && b.col >= 0 && b.nu > M * (1.0 + 1e-12) && b.nu > 1e-12 * A.sd[1];
+    __syncthreads();
+    if (ok) {
+        for (int g = threadIdx.x; g < A.nslots; g += blockDim.x) A.cand[g] = g == 0 ? b : cand_none();
+        if (threadIdx.x == 0) A.st[0] = 0;
+    } else if (threadIdx.x == 0) {
+        A.st[0] = 1;
+        if (FINAL) A.st[1] = 1;
+    }
+    if (FINAL && threadIdx.x == 0) A.st[3] = t;  // this step's exact pass brought R and nu to t
+}
+
+// Step 2 (grid, on a miss or forced): rows t0..t1-1 of R for every column, norms brought to
+// step t1-1, candidate slots and masses (as the stream kernels leave them). Columns go
+// through a shared-memory tile of 256 (tile[i * 257 + c]); a thread per column takes its KK
+// values into registers and replays the rows from them (q_s broadcast from shared memory).
+template <int LAYOUT, int KK>
+__global__ void __launch_bounds__(kThreads, 3) k_lz_refresh(LzArgs A, int64_t t1, int force) {
+    __shared__ double qs[kLzK * kLzK];
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sdm[kThreads / 32];
+    extern __shared__ double tile[];
+    if (!force && A.st[0] == 0) return;
+    const int64_t t0 = A.st[3], k = A.k, N = A.N;
+    const int64_t nq = t1 - t0;
+    for (int64_t e = threadIdx.x; e < k * nq; e += kThreads) qs[e] = A.Q[t0 * k + e];
+    Cand best = cand_none();
+    double msum = 0.0;
+    for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < N; j0 += (int64_t)gridDim.x * kThreads) {
+        const int64_t j = j0 + threadIdx.x;
+        double w[KK];
+        if (nq > 0) {
+            if (LAYOUT == 0) {
+                load_tile_small_k(A.W, k, N, j0, tile);
+            } else {
+                __syncthreads();
+                const int64_t nc = min((int64_t)kThreads, N - j0);
+                stage_smem_map<8>(tile, k * kThreads, [&](int64_t e) {
+                    const int64_t i = e / kThreads, c = e - i * kThreads;
+                    return c < nc ? __ldcs(A.W + i * A.ld + j0 + c) : 0.0;
+                }, [&](int64_t e) { const int64_t i = e / kThreads; return i * (kThreads + 1) + (e - i * kThreads); });
+                __syncthreads();
+            }
+#pragma unroll
+            for (int i = 0; i < KK; ++i) w[i] = i < k ? tile[i * (kThreads + 1) + threadIdx.x] : 0.0;
+        }
+        if (j >= N) continue;
+        const int64_t pj = A.pos[j];
+        double nuj = A.nu[j], crefj = A.cref[j];
+        for (int64_t s = t0; s < t1; ++s) {
+            if (pj < t1 && s >= pj) {
+                A.R[s * N + j] = s == pj ? A.diag[s] : 0.0;
+                continue;
+            }
+            const double* q = qs + (s - t0) * k;
+            double r = 0.0;
+#pragma unroll
+            for (int i = 0; i < KK; ++i)
+                if (i < k) r = fma(q[i], w[i], r);
+            A.R[s * N + j] = r;
+            if (pj >= t1)
+                lz_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj, crefj);
+        }
+        if (pj >= t1) {
+            if (nq > 0) {
+                A.nu[j] = nuj;
+                A.cref[j] = crefj;
+            }
+            const Cand c{nuj, pj, j};
+            if (better(c, best)) best = c;
+            msum += nuj;
+        }
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sdm);
+    if (threadIdx.x == 0) {
+        A.cand[blockIdx.x] = best;
+        A.mass[blockIdx.x] = msum;
+    }
+    if (blockIdx.x == 0)  // slots past the grid hold nothing
+        for (int g = (int)gridDim.x + threadIdx.x; g < A.nslots; g += kThreads) {
+            A.cand[g] = cand_none();
+            A.mass[g] = 0.0;
+        }
+}
+
+// Step 3 (grid, on a miss): histogram of the unpivoted norms in 1/32-octave bins below the
+// largest one.
+__global__ void __launch_bounds__(kThreads) k_lz_hist(LzArgs A, int64_t t) {
+    __shared__ int h[kLzBins];
+    __shared__ Cand sc[kThreads / 32];
+    if (A.st[0] == 0 || A.st[1]) return;
+    Cand b = cand_none();
+    for (int g = threadIdx.x; g < A.nslots; g += kThreads)
+        if (better(A.cand[g], b)) b = A.cand[g];
+    b = block_best(b, sc);
+    const double numax = b.nu;
+    for (int e = threadIdx.x; e < kLzBins; e += kThreads) h[e] = 0;
+    __syncthreads();
+    if (numax > 0.0) {
+        // lanes falling in one bin add once (warp-aggregated: the norms crowd a few bins)
+        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < A.N; j0 += (int64_t)gridDim.x * kThreads) {
+            const int64_t j = j0 + threadIdx.x;
+            int bin = -1;
+            if (j < A.N && A.pos[j] >= t) {
+                const double v = A.nu[j];
+                if (v > 0.0) {
+                    const double e = -log2(v / numax) * 32.0;
+                    if (e < (double)kLzBins) bin = max(0, (int)e);
+                }
+            }
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&h[bin], __popc(m));
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kLzBins; e += kThreads)
+        if (h[e]) atomicAdd(&A.hist[e], h[e]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.sd[2] = numax;
+        if (A.sd[1] == 0.0) A.sd[1] = numax;  // first exact pass: the largest original norm^2
+    }
+}
+
+// Step 4 (1 CTA, on a miss): the threshold M = the lowest bin edge keeping |S| <= kLzCap.
+__global__ void __launch_bounds__(kLzBins) k_lz_thresh(LzArgs A, int64_t t) {
+    __shared__ int cum[kLzBins];
+    if (A.st[0] == 0 || A.st[1]) return;
+    cum[threadIdx.x] = A.hist[threadIdx.x];
+    __syncthreads();
+    for (int o = 1; o < kLzBins; o <<= 1) {  // inclusive scan
+        const int v = threadIdx.x >= o ? cum[threadIdx.x - o] : 0;
+        __syncthreads();
+        cum[threadIdx.x] += v;
+        __syncthreads();
+    }
+    A.hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        int b = -1;
+        for (int e = 0; e < kLzBins; ++e)
+            if (cum[e] <= kLzCap) b = e;
+        A.st[2] = 0;
+        if (b < 0) {
+            A.st[1] = 1;  // the top bin alone is too dense: exact passes from here on
+        } else {
+            A.sd[0] = A.sd[2] * exp2(-(double)(b + 1) / 32.0);
+        }
+    }
+}
+
+// Step 5 (grid, on a miss): S = {unpivoted j : nu_j > M} with copies of its columns.
+template <int LAYOUT>
+__global__ void __launch_bounds__(kThreads) k_lz_gather(LzArgs A, int64_t t) {
+    if (A.st[0] == 0 || A.st[1]) return;
+    const double M = A.sd[0];
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < A.N; j += (int64_t)gridDim.x * kThreads) {
+        if (A.pos[j] < t) continue;
+        const double v = A.nu[j];
+        if (!(v > M)) continue;
+        const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long*>(&A.st[2]), 1ull);
+        if (c >= (unsigned long long)kLzBuf) continue;
+        A.idx[c] = j;
+        A.nuc[c] = v;
+        A.crefc[c] = A.cref[j];
+        A.posc[c] = A.pos[j];
+        for (int64_t i = 0; i < A.k; ++i) A.wc[i * kLzBuf + c] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
+    }
+}
+
+// Step 7 (after the reflector): row t of R for S only (norm downdate + guard); positions
+// follow the step's swap (only the pivot and the column it displaced move); the best member
+// per CTA for the next step's choice.
+template <int KK>
+__global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
+    __shared__ double q[kLzK];
+    __shared__ Cand sc[kThreads / 32];
+    if (A.st[1]) return;
+    if (threadIdx.x < A.k) q[threadIdx.x] = A.Q[t * A.k + threadIdx.x];
+    __syncthreads();
+    const int64_t cnt = min(A.st[2], kLzBuf);
+    Cand best = cand_none();
+    for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < cnt; c += (int64_t)gridDim.x * kThreads) {
+        int64_t pc = A.posc[c];
+        if (pc < 0) continue;
+        if (pc == t) {  // the pivot or the column displaced by it
+            const int64_t j = A.idx[c];
+            pc = A.pos[j];
+            if (pc <= t) pc = -1;
+            A.posc[c] = pc;
+            if (pc < 0) continue;
+        }
+        double w[KK];
+#pragma unroll
+        for (int i = 0; i < KK; ++i) w[i] = i < A.k ? A.wc[i * kLzBuf + c] : 0.0;
+        double r = 0.0;
+#pragma unroll
+        for (int i = 0; i < KK; ++i)
+            if (i < A.k) r = fma(q[i], w[i], r);
+        double nuj = A.nuc[c], crefj = A.crefc[c];
+        lz_downdate(A, t, r, A.wc + c, kLzBuf, nuj, crefj);
+        A.nuc[c] = nuj;
+        A.crefc[c] = crefj;
+        const Cand x{nuj, pc, A.idx[c]};
+        if (better(x, best)) best = x;
+    }
+    best = block_best(best, sc);
+    if (threadIdx.x == 0) A.ubest[blockIdx.x] = best;
+}
+
+// After the run's exact pass: the next run starts with a refresh at its first step.
+__global__ void k_lz_mark(LzArgs A, int64_t t) {
+    A.st[0] = 1;
+    A.st[3] = t;
+}
+
+__global__ void k_lz_init(LzArgs A) {
+    A.st[0] = 1;
+    A.st[1] = 0;
+    A.st[2] = 0;
+    A.st[3] = 0;
+    A.sd[0] = 0.0;
+    A.sd[1] = 0.0;
+    A.sd[2] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
 // Persistent pass 1 for small and medium W (cooperative launch, one CTA per SM). A run of
 // steps t0..t1-1 is one kernel: every CTA keeps its own copy of Y and T in shared memory
 // and computes the step's reflector redundantly (same inputs, same arithmetic, so the
@@ -3060,6 +3389,15 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         sub_ = subspace && !no_sub && !shard && k >= 128 && k <= kSubMaxK && N >= 32768 && cap_steps >= 4 &&
                (layout == Layout::Row || (!fma_miss && ld >= k));
     }
+    // candidate (lazy-exact) pivoting for narrow, very wide W in fixed-rank cuts (TTG_LAZY=0: off)
+    {
+        static const bool no_lz = [] {
+            const char* e = std::getenv("TTG_LAZY");
+            return e && *e == '0';
+        }();
+        lz_ = subspace && !no_lz && !shard && k <= kLzK && N >= (int64_t)1 << 20 && cap_steps >= 4 &&
+              (mode_ == 5 || mode_ == 6);
+    }
     const int ncand_stream = ncand_;
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
     // slot per CTA); its shared-memory copy of Y, T must fit at 32 steps
@@ -3136,6 +3474,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         coop_ = big_ = false;
         ncand_ = ncand_stream;
     }
+    if (lz_) coop_ = big_ = coop_ok_ = big_ok_ = false;
     ngc_ = coop_ ? sms : std::max(1, 2 * sms);
     if (coop_ok_) { nflag2_.alloc(2); nflag2_.zero(); }
     const int nslots = std::max(ncand_ + ngc_, ncand_coop_ + sms);
@@ -3168,6 +3507,68 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     if (comm_)
         TTG_LAUNCH(k_shard_init, (int)std::min<int64_t>(cdiv(Ng_, 256), 8 * sms), 256, 0, stream(), off_, N_, Ng_,
                    pos_.get(), perm_.get(), cand_.get(), ncand_);
+    if (lz_) {
+        lzst_.alloc(4);
+        lzsd_.alloc(4);
+        lzhist_.alloc(kLzBins);
+        lzhist_.zero();
+        lzidx_.alloc(kLzBuf);
+        lzposc_.alloc(kLzBuf);
+        lzwc_.alloc((size_t)kLzBuf * k);
+        lznuc_.alloc(kLzBuf);
+        lzcrefc_.alloc(kLzBuf);
+        lzubest_.alloc((size_t)cdiv(kLzBuf, kThreads));
+        TTG_LAUNCH(k_lz_init, 1, 1, 0, stream(), lz_args());
+    }
+}
+
+LzArgs WideQrcp::lz_args() {
+    return LzArgs{W_, k_, N_, ld_, Qt_.get(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
+                  cand_.get(), mass_.get(), ncand_ + ngc_, lzst_.get(), lzsd_.get(), lzhist_.get(), lzidx_.get(),
+                  lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(),
+                  (int)cdiv(kLzBuf, kThreads)};
+}
+
+// One candidate-pivoting step (see k_lz_choose .. k_lz_update); the miss kernels return at
+// once on a hit (device-side decision, no host synchronisation).
+void WideQrcp::lz_step(int64_t t) {
+    {
+        PhaseTimer pt("p1 lazy choose + exact pass on a miss");
+        LzArgs A = lz_args();
+        TTG_LAUNCH(k_lz_choose<false>, 1, 1024, 0, stream(), A, t);
+        lz_refresh(t, false);
+        const int g = std::min<int>(ncand_ + ngc_, 4 * sms_);
+        TTG_LAUNCH(k_lz_hist, g, kThreads, 0, stream(), A, t);
+        TTG_LAUNCH(k_lz_thresh, 1, kLzBins, 0, stream(), A, t);
+        auto gk = layout_ == Layout::Col ? k_lz_gather<0> : k_lz_gather<1>;
+        TTG_LAUNCH(gk, g, kThreads, 0, stream(), A, t);
+        TTG_LAUNCH(k_lz_choose<true>, 1, 1024, 0, stream(), A, t);
+    }
+    {
+        PhaseTimer pt("p1 reflector");
+        reflect_step(t);
+    }
+    PhaseTimer pt("p1 lazy update");
+    auto uk = k_ <= 8 ? k_lz_update<8> : k_ <= 16 ? k_lz_update<16> : k_ <= 24 ? k_lz_update<24> : k_lz_update<32>;
+    TTG_LAUNCH(uk, (int)cdiv(kLzBuf, kThreads), kThreads, 0, stream(), lz_args(), t);
+}
+
+void WideQrcp::lz_refresh(int64_t t1, bool force) {
+    LzArgs A = lz_args();
+    const size_t smem = sizeof(double) * (size_t)k_ * (kThreads + 1);  // the column tile (both layouts)
+    auto kern = layout_ == Layout::Col
+                    ? (k_ <= 8 ? k_lz_refresh<0, 8> : k_ <= 16 ? k_lz_refresh<0, 16> : k_ <= 24 ? k_lz_refresh<0, 24> : k_lz_refresh<0, 32>)
+                    : (k_ <= 8 ? k_lz_refresh<1, 8> : k_ <= 16 ? k_lz_refresh<1, 16> : k_ <= 24 ? k_lz_refresh<1, 24> : k_lz_refresh<1, 32>);
+    allow_smem(kern, smem);
+    prof_begin();
+    // three resident CTAs per SM (one tile each): one loads while the others compute
+    TTG_LAUNCH(kern, std::min(ncand_ + ngc_, 3 * sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
+    // algorithmic bytes: W once, norms / positions read and written (the replayed R rows,
+    // at most a few per pass, are not counted)
+    const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
+    if (force) prof_end(bytes, "k_lz_refresh (exact pass over W: replayed R rows, norms)");
+    else prof_end_select(reinterpret_cast<const int*>(lzst_.get()), bytes,
+                         "k_lz_refresh (exact pass over W: replayed R rows, norms)", 0.0, "k_lz_refresh (idle on a hit)");
 }
 
 void WideQrcp::grow(int64_t cap) {
@@ -3241,6 +3642,18 @@ double WideQrcp::refresh_exact() {
 void WideQrcp::run_to(int64_t steps) {
     steps = std::min(steps, p_);
     if (steps > cap_) grow(std::min(p_, std::max(steps, 2 * cap_)));
+    if (lz_) {
+        if (steps <= steps_) return;
+        while (steps_ < steps) {
+            lz_step(steps_);
+            ++steps_;
+        }
+        // every row and norm up to date (the R rows, trailing mass and slots other code reads)
+        PhaseTimer pt("p1 lazy final exact pass");
+        lz_refresh(steps_, true);
+        TTG_LAUNCH(k_lz_mark, 1, 1, 0, stream(), lz_args(), steps_);
+        return;
+    }
     while (sub_ && steps_ < steps) {
         // subspace steps in windows of 8; a window with fewer than 2 hits (e.g. Hilbert-type
         // columns whose predicted residuals are dependent) turns the engine back to the plain

@@ -161,7 +161,7 @@ def test_rank_chain_errors(dev):
 # (5000, 96): the in-place engine's column-parallel mode; (5000, 300): the same with panel
 # (delayed) updates; (5000, 40): its row-block mode
 @pytest.mark.parametrize("shape", [(30, 20), (20, 30), (100, 400), (100, 20), (1, 7), (7, 1), (5000, 96),
-                                   (5000, 300), (5000, 40)])
+                                   (5000, 300), (5000, 40), (4500, 1200)])
 def test_qr_col_pivot_matches_reference(dev, ref, shape):
     rng = np.random.default_rng(7)
     a = np.asfortranarray(rng.standard_normal(shape))
