@@ -751,6 +751,7 @@ struct LzArgs {
     int64_t* posc;      // S's current positions (-1 once pivoted)
     Cand* ubest;        // k_lz_update's per-CTA best member
     int nubest;
+    const int64_t* piv; // step -> pivot column
 };
 
 namespace {
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
 // through a shared-memory tile of 256 (tile[i * 257 + c]); a thread per column takes its KK
 // values into registers and replays the rows from them (q_s broadcast from shared memory).
 template <int LAYOUT, int KK>
-__global__ void __launch_bounds__(kThreads, 3) k_lz_refresh(LzArgs A, int64_t t1, int force) {
+__global__ void __launch_bounds__(kThreads, 2) k_lz_refresh(LzArgs A, int64_t t1, int force) {
     __shared__ double qs[kLzK * kLzK];
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sdm[kThreads / 32];
@@ -856,8 +857,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_lz_refresh(LzArgs A, int64_t t1
                 }, [&](int64_t e) { const int64_t i = e / kThreads; return i * (kThreads + 1) + (e - i * kThreads); });
                 __syncthreads();
             }
+            // k == KK (config 3's k = 24): no per-element predicates (zero padding otherwise)
 #pragma unroll
-            for (int i = 0; i < KK; ++i) w[i] = i < k ? tile[i * (kThreads + 1) + threadIdx.x] : 0.0;
+            for (int i = 0; i < KK; ++i) w[i] = (k == KK || i < k) ? tile[i * (kThreads + 1) + threadIdx.x] : 0.0;
         }
         if (j >= N) continue;
         const int64_t pj = A.pos[j];
@@ -869,9 +871,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_lz_refresh(LzArgs A, int64_t t1
             }
             const double* q = qs + (s - t0) * k;
             double r = 0.0;
+            if (k == KK) {
 #pragma unroll
-            for (int i = 0; i < KK; ++i)
-                if (i < k) r = fma(q[i], w[i], r);
+                for (int i = 0; i < KK; ++i) r = fma(q[i], w[i], r);
+            } else {
+#pragma unroll
+                for (int i = 0; i < KK; ++i)
+                    if (i < k) r = fma(q[i], w[i], r);
+            }
             A.R[s * N + j] = r;
             if (pj >= t1)
                 lz_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj, crefj);
@@ -990,15 +997,17 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
     __shared__ double q[kLzK];
     __shared__ Cand sc[kThreads / 32];
     if (A.st[1]) return;
-    if (threadIdx.x < A.k) q[threadIdx.x] = A.Q[t * A.k + threadIdx.x];
+    if (threadIdx.x < kLzK) q[threadIdx.x] = threadIdx.x < A.k ? A.Q[t * A.k + threadIdx.x] : 0.0;
     __syncthreads();
     const int64_t cnt = min(A.st[2], kLzBuf);
+    const int64_t jp = A.piv[t];
     Cand best = cand_none();
     for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < cnt; c += (int64_t)gridDim.x * kThreads) {
         int64_t pc = A.posc[c];
         if (pc < 0) continue;
-        if (pc == t) {  // the pivot or the column displaced by it
-            const int64_t j = A.idx[c];
+        const int64_t jc = A.idx[c];
+        if (pc == t || jc == jp) {  // the column displaced by the pivot, or the pivot itself
+            const int64_t j = jc;
             pc = A.pos[j];
             if (pc <= t) pc = -1;
             A.posc[c] = pc;
@@ -1006,16 +1015,15 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
         }
         double w[KK];
 #pragma unroll
-        for (int i = 0; i < KK; ++i) w[i] = i < A.k ? A.wc[i * kLzBuf + c] : 0.0;
+        for (int i = 0; i < KK; ++i) w[i] = (A.k == KK || i < A.k) ? A.wc[i * kLzBuf + c] : 0.0;
         double r = 0.0;
 #pragma unroll
-        for (int i = 0; i < KK; ++i)
-            if (i < A.k) r = fma(q[i], w[i], r);
+        for (int i = 0; i < KK; ++i) r = fma(q[i], w[i], r);  // q is zero past k
         double nuj = A.nuc[c], crefj = A.crefc[c];
         lz_downdate(A, t, r, A.wc + c, kLzBuf, nuj, crefj);
         A.nuc[c] = nuj;
         A.crefc[c] = crefj;
-        const Cand x{nuj, pc, A.idx[c]};
+        const Cand x{nuj, pc, jc};
         if (better(x, best)) best = x;
     }
     best = block_best(best, sc);
@@ -3526,7 +3534,7 @@ LzArgs WideQrcp::lz_args() {
     return LzArgs{W_, k_, N_, ld_, Qt_.get(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
                   cand_.get(), mass_.get(), ncand_ + ngc_, lzst_.get(), lzsd_.get(), lzhist_.get(), lzidx_.get(),
                   lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(),
-                  (int)cdiv(kLzBuf, kThreads)};
+                  (int)cdiv(kLzBuf, kThreads), piv_.get()};
 }
 
 // One candidate-pivoting step (see k_lz_choose .. k_lz_update); the miss kernels return at
@@ -3561,8 +3569,8 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
                     : (k_ <= 8 ? k_lz_refresh<1, 8> : k_ <= 16 ? k_lz_refresh<1, 16> : k_ <= 24 ? k_lz_refresh<1, 24> : k_lz_refresh<1, 32>);
     allow_smem(kern, smem);
     prof_begin();
-    // three resident CTAs per SM (one tile each): one loads while the others compute
-    TTG_LAUNCH(kern, std::min(ncand_ + ngc_, 3 * sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
+    // two resident CTAs per SM (one tile each): one loads while the other computes
+    TTG_LAUNCH(kern, std::min(ncand_ + ngc_, 2 * sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
     // algorithmic bytes: W once, norms / positions read and written (the replayed R rows,
     // at most a few per pass, are not counted)
     const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
