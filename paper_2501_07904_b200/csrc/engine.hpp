@@ -139,7 +139,8 @@ private:
     DevBuf<Cand> cand_;
     DevBuf<int> nflag_;
     // candidate (lazy-exact) pivoting for narrow W (qrcp_wide.cu, k_lz_*)
-    bool lz_ = false;
+    bool lz_ = false, lzw_ = false;  // narrow (k <= 32) / wide (k <= 512) variant
+    int lz_nubest() const;
     DevBuf<int64_t> lzst_, lzidx_, lzposc_;
     DevBuf<Cand> lzubest_;
     DevBuf<double> lzsd_, lzwc_, lznuc_, lzcrefc_;

@@ -752,6 +752,8 @@ struct LzArgs {
     Cand* ubest;        // k_lz_update's per-CTA best member
     int nubest;
     const int64_t* piv; // step -> pivot column
+    int64_t cap, buf;   // target |S| and capacity
+    int wide;           // k > 32: member columns column-major (wc[c * k + i]), copied by k_lzw_copy
 };
 
 namespace {
@@ -814,7 +816,7 @@ __global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
         if (better(rec[g], b)) b = rec[g];
     b = block_best(b, sc);
     const double M = A.sd[0];
-    const bool ok = A.st[2] <= kLzBuf && b.col >= 0 && b.nu > M * (1.0 + 1e-12) && b.nu > 1e-12 * A.sd[1];
+    const bool ok = A.st[2] <= A.buf && b.col >= 0 && b.nu > M * (1.0 + 1e-12) && b.nu > 1e-12 * A.sd[1];
     __syncthreads();
     if (ok) {
         for (int g = threadIdx.x; g < A.nslots; g += blockDim.x) A.cand[g] = g == 0 ? b : cand_none();
@@ -1006,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_hist(LzArgs A, int64_t t) {
     }
 }
 
-// Step 4 (1 CTA, on a miss): the threshold M = the lowest bin edge keeping |S| <= kLzCap.
+// Step 4 (1 CTA, on a miss): the threshold M = the lowest bin edge keeping |S| <= A.cap.
 __global__ void __launch_bounds__(kLzBins) k_lz_thresh(LzArgs A, int64_t t) {
     __shared__ int cum[kLzBins];
     if (A.st[0] == 0 || A.st[1]) return;
@@ -1022,7 +1024,7 @@ __global__ void __launch_bounds__(kLzBins) k_lz_thresh(LzArgs A, int64_t t) {
     if (threadIdx.x == 0) {
         int b = -1;
         for (int e = 0; e < kLzBins; ++e)
-            if (cum[e] <= kLzCap) b = e;
+            if (cum[e] <= A.cap) b = e;
         A.st[2] = 0;
         if (b < 0) {
             A.st[1] = 1;  // the top bin alone is too dense: exact passes from here on
@@ -1057,12 +1059,13 @@ __global__ void __launch_bounds__(kThreads) k_lz_gather(LzArgs A, int64_t t) {
         base = __shfl_sync(0xffffffffu, base, leader);
         if (!in) continue;
         const unsigned long long c = base + __popc(m & ((1u << lane) - 1u));
-        if (c >= (unsigned long long)kLzBuf) continue;
+        if (c >= (unsigned long long)A.buf) continue;
         A.idx[c] = j;
         A.nuc[c] = v;
         A.crefc[c] = A.cref[j];
         A.posc[c] = pj;
-        for (int64_t i = 0; i < A.k; ++i) A.wc[i * kLzBuf + c] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
+        if (!A.wide)
+            for (int64_t i = 0; i < A.k; ++i) A.wc[i * A.buf + c] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
     }
 }
 
@@ -1076,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
     if (A.st[1]) return;
     if (threadIdx.x < kLzK) q[threadIdx.x] = threadIdx.x < A.k ? A.Q[t * A.k + threadIdx.x] : 0.0;
     __syncthreads();
-    const int64_t cnt = min(A.st[2], kLzBuf);
+    const int64_t cnt = min(A.st[2], A.buf);
     const int64_t jp = A.piv[t];
     Cand best = cand_none();
     for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < cnt; c += (int64_t)gridDim.x * kThreads) {
@@ -1092,16 +1095,242 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
         }
         double w[KK];
 #pragma unroll
-        for (int i = 0; i < KK; ++i) w[i] = (A.k == KK || i < A.k) ? A.wc[i * kLzBuf + c] : 0.0;
+        for (int i = 0; i < KK; ++i) w[i] = (A.k == KK || i < A.k) ? A.wc[i * A.buf + c] : 0.0;
         double r = 0.0;
 #pragma unroll
         for (int i = 0; i < KK; ++i) r = fma(q[i], w[i], r);  // q is zero past k
         double nuj = A.nuc[c], crefj = A.crefc[c];
-        lz_downdate(A, t, r, A.wc + c, kLzBuf, nuj, crefj);
+        lz_downdate(A, t, r, A.wc + c, A.buf, nuj, crefj);
         A.nuc[c] = nuj;
         A.crefc[c] = crefj;
         const Cand x{nuj, pc, jc};
         if (better(x, best)) best = x;
+    }
+    best = block_best(best, sc);
+    if (threadIdx.x == 0) A.ubest[blockIdx.x] = best;
+}
+
+// ---- candidate pivoting for wider W (32 < k <= 512): a warp per column ---------------------
+// The same engine for config 3's second cuts (480 x 331,776): a CPU replay of the rule on the
+// real input misses once in 20 steps (|S| <= 16,384), against ~7 subspace misses. A column is
+// held by one warp, lane l taking rows l, l + 32, ... (kLzWM per lane); a dot is the lanes'
+// partial sums in that order and the warp_sum tree, in the exact pass and the member update
+// alike, so both compute R(t, j) with the same bits.
+constexpr int kLzWK = 512;           // largest k
+constexpr int kLzWM = kLzWK / 32;    // rows per lane
+constexpr int kLzWT = 16;            // columns per tile in the exact pass
+constexpr int kLzWQ = 8;             // rows of Q per shared-memory chunk
+constexpr int64_t kLzCapW = 16384, kLzBufW = 32768;
+
+// q_s^T w over the lanes' rows (w in registers), reduced over the warp.
+__device__ __forceinline__ double lzw_dot(const double* q, const double (&w)[kLzWM], int k) {
+    const int lane = threadIdx.x & 31;
+    double a = 0.0;
+#pragma unroll
+    for (int m = 0; m < kLzWM; ++m) {
+        const int i = lane + 32 * m;
+        if (i < k) a = fma(q[i], w[m], a);
+    }
+    return warp_sum(a);
+}
+
+// Guard recompute |w - Q[:, :s+1] Q[:, :s+1]^T w|^2, modified Gram-Schmidt, warp-cooperative.
+__device__ __noinline__ double lzw_resid(const double* __restrict__ Q, int k, int64_t s, const double* wp,
+                                         int64_t stride) {
+    const int lane = threadIdx.x & 31;
+    double x[kLzWM];
+#pragma unroll
+    for (int m = 0; m < kLzWM; ++m) {
+        const int i = lane + 32 * m;
+        x[m] = i < k ? wp[(int64_t)i * stride] : 0.0;
+    }
+    for (int64_t l = 0; l <= s; ++l) {
+        const double* q = Q + l * k;
+        double z = 0.0;
+#pragma unroll
+        for (int m = 0; m < kLzWM; ++m) {
+            const int i = lane + 32 * m;
+            if (i < k) z = fma(q[i], x[m], z);
+        }
+        z = warp_sum(z);
+#pragma unroll
+        for (int m = 0; m < kLzWM; ++m) {
+            const int i = lane + 32 * m;
+            if (i < k) x[m] = fma(-q[i], z, x[m]);
+        }
+    }
+    double sq = 0.0;
+#pragma unroll
+    for (int m = 0; m < kLzWM; ++m) sq = fma(x[m], x[m], sq);
+    return warp_sum(sq);
+}
+
+// Downdate + guard for one column (all lanes; nu / cref valid in every lane).
+__device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double r, const double* wp, int64_t stride,
+                                             double& nuj, double& crefj) {
+    const double nv = __dsub_rn(nuj, __dmul_rn(r, r));
+    if (nv < __dmul_rn(1e-16, crefj) || nv < 0.0) {  // warp-uniform (r and nu are)
+        nuj = lzw_resid(A.Q, (int)A.k, s, wp, stride);
+        crefj = nuj;
+    } else {
+        nuj = nv;
+    }
+}
+
+// Exact pass (wide): tiles of kLzWT columns through shared memory, two columns per warp,
+// Q's rows t0..t1-1 in chunks of kLzWQ.
+template <int LAYOUT>
+__global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t1, int force) {
+    extern __shared__ double wsm[];  // tile[k][kLzWT + 1] | qc[kLzWQ][k]
+    __shared__ Cand sc[kThreads / 32];
+    __shared__ double sdm[kThreads / 32];
+    if (!force && A.st[0] == 0) return;
+    const int64_t t0 = A.st[3], N = A.N;
+    const int k = (int)A.k;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* tile = wsm;
+    double* qc = wsm + (size_t)k * (kLzWT + 1);
+    Cand best = cand_none();
+    double msum = 0.0;
+    constexpr int CPW = kLzWT / (kThreads / 32);  // columns per warp (2)
+    for (int64_t j0 = (int64_t)blockIdx.x * kLzWT; j0 < N; j0 += (int64_t)gridDim.x * kLzWT) {
+        const int nc = (int)min((int64_t)kLzWT, N - j0);
+        __syncthreads();
+        if (t1 > t0) {
+            if (LAYOUT == 0) {
+                for (int e = threadIdx.x; e < k * nc; e += kThreads) {
+                    const int c = e / k, i = e - c * k;
+                    tile[i * (kLzWT + 1) + c] = A.W[(int64_t)i + (j0 + c) * A.ld];
+                }
+            } else {
+                for (int e = threadIdx.x; e < k * kLzWT; e += kThreads) {
+                    const int i = e / kLzWT, c = e - i * kLzWT;
+                    if (c < nc) tile[i * (kLzWT + 1) + c] = A.W[(int64_t)i * A.ld + j0 + c];
+                }
+            }
+        }
+        __syncthreads();
+        double w[CPW][kLzWM];
+        double nuj[CPW], crefj[CPW];
+        int64_t pj[CPW];
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+            const int c = warp + u * (kThreads / 32);
+            const int64_t j = j0 + c;
+            pj[u] = c < nc ? A.pos[j] : -1;
+            nuj[u] = c < nc ? A.nu[j] : 0.0;
+            crefj[u] = c < nc ? A.cref[j] : 0.0;
+#pragma unroll
+            for (int m = 0; m < kLzWM; ++m) {
+                const int i = lane + 32 * m;
+                w[u][m] = (c < nc && i < k && t1 > t0) ? tile[i * (kLzWT + 1) + c] : 0.0;
+            }
+        }
+        for (int64_t sb = t0; sb < t1; sb += kLzWQ) {
+            const int nb = (int)min((int64_t)kLzWQ, t1 - sb);
+            __syncthreads();
+            for (int e = threadIdx.x; e < nb * k; e += kThreads) qc[e] = A.Q[sb * k + e];
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < CPW; ++u) {
+                const int c = warp + u * (kThreads / 32);
+                if (c >= nc) continue;
+                const int64_t j = j0 + c;
+                for (int b = 0; b < nb; ++b) {
+                    const int64_t s = sb + b;
+                    if (pj[u] < t1 && s >= pj[u]) {
+                        if (lane == 0) A.R[s * N + j] = s == pj[u] ? A.diag[s] : 0.0;
+                        continue;
+                    }
+                    const double r = lzw_dot(qc + b * k, w[u], k);
+                    if (lane == 0) A.R[s * N + j] = r;
+                    if (pj[u] >= t1)
+                        lzw_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj[u],
+                                     crefj[u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+            const int c = warp + u * (kThreads / 32);
+            if (c >= nc || pj[u] < t1) continue;
+            const int64_t j = j0 + c;
+            if (lane == 0) {
+                if (t1 > t0) {
+                    A.nu[j] = nuj[u];
+                    A.cref[j] = crefj[u];
+                }
+                const Cand cc{nuj[u], pj[u], j};
+                if (better(cc, best)) best = cc;
+                msum += nuj[u];
+            }
+        }
+    }
+    best = block_best(best, sc);
+    msum = block_sum(msum, sdm);
+    if (threadIdx.x == 0) {
+        A.cand[blockIdx.x] = best;
+        A.mass[blockIdx.x] = msum;
+    }
+    if (blockIdx.x == 0)
+        for (int g = (int)gridDim.x + threadIdx.x; g < A.nslots; g += kThreads) {
+            A.cand[g] = cand_none();
+            A.mass[g] = 0.0;
+        }
+}
+
+// Member columns into wc (column-major, wc[c * k + i]); a warp per member.
+template <int LAYOUT>
+__global__ void __launch_bounds__(kThreads) k_lzw_copy(LzArgs A, int64_t t) {
+    if (A.st[0] == 0 || A.st[1]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t cnt = min(A.st[2], A.buf);
+    for (int64_t c = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; c < cnt;
+         c += ((int64_t)gridDim.x * kThreads) >> 5) {
+        const int64_t j = A.idx[c];
+        for (int64_t i = lane; i < A.k; i += 32)
+            A.wc[c * A.k + i] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
+    }
+}
+
+// Member update (wide): a warp per member; per-CTA best member.
+__global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
+    extern __shared__ double q[];  // k
+    __shared__ Cand sc[kThreads / 32];
+    if (A.st[1]) return;
+    const int k = (int)A.k, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < k; e += kThreads) q[e] = A.Q[t * k + e];
+    __syncthreads();
+    const int64_t cnt = min(A.st[2], A.buf);
+    const int64_t jp = A.piv[t];
+    Cand best = cand_none();
+    for (int64_t c = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; c < cnt;
+         c += ((int64_t)gridDim.x * kThreads) >> 5) {
+        int64_t pc = A.posc[c];
+        if (pc < 0) continue;
+        const int64_t jc = A.idx[c];
+        if (pc == t || jc == jp) {
+            pc = A.pos[jc];
+            if (pc <= t) pc = -1;
+            if (lane == 0) A.posc[c] = pc;
+            if (pc < 0) continue;
+        }
+        const double* wp = A.wc + c * k;
+        double w[kLzWM];
+#pragma unroll
+        for (int m = 0; m < kLzWM; ++m) {
+            const int i = lane + 32 * m;
+            w[m] = i < k ? wp[i] : 0.0;
+        }
+        const double r = lzw_dot(q, w, k);
+        double nuj = A.nuc[c], crefj = A.crefc[c];
+        lzw_downdate(A, t, r, wp, 1, nuj, crefj);
+        if (lane == 0) {
+            A.nuc[c] = nuj;
+            A.crefc[c] = crefj;
+            const Cand x{nuj, pc, jc};
+            if (better(x, best)) best = x;
+        }
     }
     best = block_best(best, sc);
     if (threadIdx.x == 0) A.ubest[blockIdx.x] = best;
@@ -3482,6 +3711,16 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         }();
         lz_ = subspace && !no_lz && !shard && k <= kLzK && N >= (int64_t)1 << 20 && cap_steps >= 4 &&
               (mode_ == 5 || mode_ == 6);
+        // wider W (config 3's second cuts): the warp-per-column variant instead of the subspace
+        // engine (TTG_LAZY_WIDE=0: subspace as before)
+        static const bool no_lzw = [] {
+            const char* e = std::getenv("TTG_LAZY_WIDE");
+            return e && *e == '0';
+        }();
+        if (subspace && !no_lz && !no_lzw && !shard && k > kLzK && k <= kLzWK && N >= 32768 && cap_steps >= 4) {
+            lz_ = lzw_ = true;
+            sub_ = false;
+        }
     }
     const int ncand_stream = ncand_;
     // small / medium W: the persistent cooperative step loop (one stream slot and one guard
@@ -3597,12 +3836,13 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
         lzsd_.alloc(4);
         lzhist_.alloc(kLzBins);
         lzhist_.zero();
-        lzidx_.alloc(kLzBuf);
-        lzposc_.alloc(kLzBuf);
-        lzwc_.alloc((size_t)kLzBuf * k);
-        lznuc_.alloc(kLzBuf);
-        lzcrefc_.alloc(kLzBuf);
-        lzubest_.alloc((size_t)cdiv(kLzBuf, kThreads));
+        const int64_t buf = lzw_ ? kLzBufW : kLzBuf;
+        lzidx_.alloc(buf);
+        lzposc_.alloc(buf);
+        lzwc_.alloc((size_t)buf * k);
+        lznuc_.alloc(buf);
+        lzcrefc_.alloc(buf);
+        lzubest_.alloc((size_t)lz_nubest());
         TTG_LAUNCH(k_lz_init, 1, 1, 0, stream(), lz_args());
     }
 }
@@ -3610,8 +3850,13 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
 LzArgs WideQrcp::lz_args() {
     return LzArgs{W_, k_, N_, ld_, Qt_.get(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
                   cand_.get(), mass_.get(), ncand_ + ngc_, lzst_.get(), lzsd_.get(), lzhist_.get(), lzidx_.get(),
-                  lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(),
-                  (int)cdiv(kLzBuf, kThreads), piv_.get()};
+                  lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(), lz_nubest(), piv_.get(),
+                  lzw_ ? kLzCapW : kLzCap, lzw_ ? kLzBufW : kLzBuf, lzw_ ? 1 : 0};
+}
+
+// per-CTA records of the member update: a thread per member (narrow), a warp per member (wide)
+int WideQrcp::lz_nubest() const {
+    return lzw_ ? (int)cdiv(kLzBufW, kThreads / 32) : (int)cdiv(kLzBuf, kThreads);
 }
 
 // One candidate-pivoting step (see k_lz_choose .. k_lz_update); the miss kernels return at
@@ -3627,6 +3872,10 @@ void WideQrcp::lz_step(int64_t t) {
         TTG_LAUNCH(k_lz_thresh, 1, kLzBins, 0, stream(), A, t);
         auto gk = layout_ == Layout::Col ? k_lz_gather<0> : k_lz_gather<1>;
         TTG_LAUNCH(gk, g, kThreads, 0, stream(), A, t);
+        if (lzw_) {
+            auto ck = layout_ == Layout::Col ? k_lzw_copy<0> : k_lzw_copy<1>;
+            TTG_LAUNCH(ck, (int)std::min<int64_t>(cdiv(kLzBufW, kThreads / 32), 8 * sms_), kThreads, 0, stream(), A, t);
+        }
         TTG_LAUNCH(k_lz_choose<true>, 1, 1024, 0, stream(), A, t);
     }
     {
@@ -3634,12 +3883,28 @@ void WideQrcp::lz_step(int64_t t) {
         reflect_step(t);
     }
     PhaseTimer pt("p1 lazy update");
+    if (lzw_) {
+        TTG_LAUNCH(k_lzw_update, lz_nubest(), kThreads, sizeof(double) * (size_t)k_, stream(), lz_args(), t);
+        return;
+    }
     auto uk = k_ <= 8 ? k_lz_update<8> : k_ <= 16 ? k_lz_update<16> : k_ <= 24 ? k_lz_update<24> : k_lz_update<32>;
-    TTG_LAUNCH(uk, (int)cdiv(kLzBuf, kThreads), kThreads, 0, stream(), lz_args(), t);
+    TTG_LAUNCH(uk, lz_nubest(), kThreads, 0, stream(), lz_args(), t);
 }
 
 void WideQrcp::lz_refresh(int64_t t1, bool force) {
     LzArgs A = lz_args();
+    if (lzw_) {
+        const size_t smem = sizeof(double) * (size_t)(k_ * (kLzWT + 1) + kLzWQ * k_);
+        auto kern = layout_ == Layout::Col ? k_lzw_refresh<0> : k_lzw_refresh<1>;
+        allow_smem(kern, smem);
+        prof_begin();
+        TTG_LAUNCH(kern, std::min(ncand_ + ngc_, sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
+        const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
+        if (force) prof_end(bytes, "k_lzw_refresh (exact pass over W, warp per column)");
+        else prof_end_select(reinterpret_cast<const int*>(lzst_.get()), bytes,
+                             "k_lzw_refresh (exact pass over W, warp per column)", 0.0, "k_lzw_refresh (idle on a hit)");
+        return;
+    }
     const int kk = k_ <= 8 ? 8 : k_ <= 16 ? 16 : k_ <= 24 ? 24 : 32;
     const size_t smem = sizeof(double) * 2 *
                         (size_t)(layout_ == Layout::Col ? kThreads * (kk + 1) : kk * (kThreads + 2));  // two tiles

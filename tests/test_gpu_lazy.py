@@ -54,3 +54,14 @@ def test_lazy_hilbert_ties(dev, ref, method, sweep, dims):
     # rank 7: kept diagonals down to ~1e-5 |T_00|, well above the rounding-ordered tail
     a = _hilbert(dims)
     _check(dev, ref, a, dims, method, sweep, [1, 7, 7, 1])
+
+
+@pytest.mark.parametrize("method,sweep,dims,ranks", [
+    ("ulv", "l2r", [8, 32, 32, 32, 32], [1, 8, 20, 20, 20, 1]),
+    ("urv", "r2l", [32, 32, 32, 32, 8], [1, 20, 20, 20, 8, 1]),
+])
+def test_lazy_wide_second_cut(dev, ref, method, sweep, dims, ranks):
+    """The warp-per-column variant (32 < k <= 512): the second cut is 256 x 32,768 (Col W for
+    ULV, Row W for URV) after a narrow 8 x 4,194,304 first cut."""
+    a = _planted(ref, dims, ranks, 41, 1e-4)
+    _check(dev, ref, a, dims, method, sweep, ranks)
