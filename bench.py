@@ -164,16 +164,25 @@ class Clocks:
         except OSError:
             self.proc = None
 
-    def stop(self, t_begin=None, t_end=None):
+    def stop(self, t_begin=None, t_end=None, windows=None):
+        """Stops the sampler; summary of the samples inside [t_begin, t_end] (and of each extra
+        (t0, t1) in `windows`, returned as a list after it)."""
         if not self.proc:
-            return None
+            return None if windows is None else (None, [None] * len(windows))
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        self.proc = None
+        all_rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if windows is None:
+            return self._summary(all_rows, t_begin, t_end)
+        return self._summary(all_rows, t_begin, t_end), [self._summary(all_rows, a, b) for a, b in windows]
+
+    def _summary(self, all_rows, t_begin, t_end):
+        rows = list(all_rows)
         if t_begin is not None:
             import datetime
             inside = []
@@ -416,7 +425,6 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     t_end = time.time()
-    clk = clocks.stop(t_begin, t_end)
     if dist:
         dist.barrier()
     launches = lib().ttg_kernel_launches() - launches0
@@ -442,7 +450,9 @@ def run_ours(args):
     # an event recorded on the main stream, and records an end event on its stream. Device
     # time = start event to the last end event (CUDA events, no host clock), so one
     # decomposition's latency-bound phases (one-CTA reflectors, host round trips) overlap the
-    # other's streaming passes. `value` is this figure; the one-stream figure is kept beside it.
+    # other's streaming passes. Reported beside `value` (the one-stream figure): on the B200 it
+    # measured 19-20 ms per config-3 step in some runs and 100+ ms in others (cooperative
+    # launches of one stream waiting on the other's resident grids), so it is not the headline.
     def device_concurrent(steps):
         st0 = torch.cuda.current_stream()
         start = torch.cuda.Event(enable_timing=True)
@@ -481,19 +491,19 @@ def run_ours(args):
         return max(start.elapsed_time(e) for e in ends)
 
     conc_dev = len(runs) > 1 and not sharded and world == 1 and args.e2e_concurrency > 1
+    tb = te = None
+    conc_ms_max = None
     if conc_dev:
         device_concurrent(1)  # the worker threads' streams and memory pools
-        clocks2 = Clocks(local)
-        clocks2.start()
-        time.sleep(0.3)
         tb = time.time()
         ms_conc = device_concurrent(args.steps)
         te = time.time()
-        clk2 = clocks2.stop(tb, te)
-        ms_max = max_over_ranks(ms_conc, dist)
-        value = jobs * args.steps * entries_per_step / (ms_max * 1e-3)
-        if clk2 and clk:
-            clk = dict(clk, concurrent_region=clk2)
+        log(f"concurrent: {ms_conc / args.steps:.2f} ms per step (one stream: {seq_ms_max / args.steps:.2f})")
+        conc_ms_max = max_over_ranks(ms_conc, dist)
+    # one sampler for both timed regions (its start-up never overlaps either)
+    clk, (clk2,) = clocks.stop(t_begin, t_end, windows=[(tb or t_begin, te or t_end)])
+    if conc_dev and clk is not None:
+        clk = dict(clk, concurrent_region=clk2)
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region ----
     host = torch.empty(src.numel(), dtype=torch.float64, pin_memory=True)
@@ -590,7 +600,6 @@ def run_ours(args):
                                for cu in sm["cuts"]]}
     parity = golden_parity(args.config, a_host, {m: {"ranks": r.ranks_chosen, "rse": rse.get(m)}
                                                  for m, r in rep.items()}) if not sharded else None
-    seq_value = jobs * args.steps * entries_per_step / (seq_ms_max * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -604,10 +613,13 @@ def run_ours(args):
                        "rse": rse, "inputs": "paper_2501_07904_b200/inputs.py (the reference generators' "
                                              "algorithms, bitwise; SURVEY Appendix C seeds)"},
             "device_timing": {
-                "value": ("the step's decompositions in flight together, one host thread and engine stream each "
-                          "(CUDA events: a start event on the main stream that every engine stream waits on, "
-                          "to the last engine stream's end event)") if conc_dev else "one stream, decompositions in turn",
-                "sequential_value": seq_value, "sequential_ms_per_step": seq_ms_max / args.steps},
+                "value": "one stream, the step's decompositions in turn (CUDA events on the engine stream)",
+                "concurrent_value": (jobs * args.steps * entries_per_step / (conc_ms_max * 1e-3)) if conc_dev else None,
+                "concurrent_ms_per_step": (conc_ms_max / args.steps) if conc_dev else None,
+                "concurrent": ("the step's decompositions in flight together, one host thread and engine stream each "
+                               "(CUDA events: a start event on the main stream that every engine stream waits on, "
+                               "to the last engine stream's end event); not the headline (unstable, see bench.py)")
+                              if conc_dev else None},
             "parity": parity,
             "step_roofline": step_model,
             "roofline": {"bound": "hbm",

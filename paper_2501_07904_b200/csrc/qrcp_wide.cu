@@ -1177,39 +1177,57 @@ __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double 
     }
 }
 
-// Exact pass (wide): tiles of kLzWT columns through shared memory, two columns per warp,
-// Q's rows t0..t1-1 in chunks of kLzWQ.
-template <int LAYOUT>
+// Exact pass (wide): tiles of kLzWT columns stream through two shared-memory buffers
+// (8-byte cp.async: the next tile lands while the current one is computed), two columns per
+// warp; Q's rows t0..t1-1 stay in shared memory for the whole pass when they fit (QALL),
+// else they are streamed in chunks of kLzWQ per tile.
+template <int LAYOUT, bool QALL>
 __global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t1, int force) {
-    extern __shared__ double wsm[];  // tile[k][kLzWT + 1] | qc[kLzWQ][k]
+    extern __shared__ __align__(16) double wsm[];  // tiles[2][k][kLzWT + 1] | q rows
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sdm[kThreads / 32];
     if (!force && A.st[0] == 0) return;
     const int64_t t0 = A.st[3], N = A.N;
     const int k = (int)A.k;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* tile = wsm;
-    double* qc = wsm + (size_t)k * (kLzWT + 1);
+    const int TD = k * (kLzWT + 1);
+    double* qv = wsm + 2 * (size_t)TD;
+    const int nq = (int)(t1 - t0);
+    if (QALL)
+        for (int e = threadIdx.x; e < nq * k; e += kThreads) qv[e] = A.Q[t0 * k + e];
+    auto issue = [&](int64_t j0, int b) {
+        double* tb = wsm + (size_t)b * TD;
+        const int nc = (int)min((int64_t)kLzWT, N - j0);
+        if (LAYOUT == 0) {  // column c contiguous (ld >= k): a warp per column
+            for (int c = warp; c < nc; c += kThreads / 32)
+                for (int i = lane; i < k; i += 32) lz_cp8(tb + i * (kLzWT + 1) + c, A.W + i + (j0 + c) * A.ld);
+        } else {  // row i: kLzWT contiguous doubles
+            for (int e = threadIdx.x; e < k * kLzWT; e += kThreads) {
+                const int i = e / kLzWT, c = e - i * kLzWT;
+                if (c < nc) lz_cp8(tb + i * (kLzWT + 1) + c, A.W + (int64_t)i * A.ld + j0 + c);
+            }
+        }
+        lz_cp_commit();
+    };
     Cand best = cand_none();
     double msum = 0.0;
     constexpr int CPW = kLzWT / (kThreads / 32);  // columns per warp (2)
-    for (int64_t j0 = (int64_t)blockIdx.x * kLzWT; j0 < N; j0 += (int64_t)gridDim.x * kLzWT) {
+    const int64_t stride = (int64_t)gridDim.x * kLzWT;
+    int64_t j0 = (int64_t)blockIdx.x * kLzWT;
+    int buf = 0;
+    if (nq > 0 && j0 < N) issue(j0, 0);
+    for (; j0 < N; j0 += stride) {
         const int nc = (int)min((int64_t)kLzWT, N - j0);
-        __syncthreads();
-        if (t1 > t0) {
-            if (LAYOUT == 0) {
-                for (int e = threadIdx.x; e < k * nc; e += kThreads) {
-                    const int c = e / k, i = e - c * k;
-                    tile[i * (kLzWT + 1) + c] = A.W[(int64_t)i + (j0 + c) * A.ld];
-                }
+        if (nq > 0) {
+            if (j0 + stride < N) {
+                issue(j0 + stride, buf ^ 1);
+                lz_cp_wait<1>();
             } else {
-                for (int e = threadIdx.x; e < k * kLzWT; e += kThreads) {
-                    const int i = e / kLzWT, c = e - i * kLzWT;
-                    if (c < nc) tile[i * (kLzWT + 1) + c] = A.W[(int64_t)i * A.ld + j0 + c];
-                }
+                lz_cp_wait<0>();
             }
         }
         __syncthreads();
+        const double* tile = wsm + (size_t)buf * TD;
         double w[CPW][kLzWM];
         double nuj[CPW], crefj[CPW];
         int64_t pj[CPW];
@@ -1223,26 +1241,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t
 #pragma unroll
             for (int m = 0; m < kLzWM; ++m) {
                 const int i = lane + 32 * m;
-                w[u][m] = (c < nc && i < k && t1 > t0) ? tile[i * (kLzWT + 1) + c] : 0.0;
+                w[u][m] = (c < nc && i < k && nq > 0) ? tile[i * (kLzWT + 1) + c] : 0.0;
             }
         }
-        for (int64_t sb = t0; sb < t1; sb += kLzWQ) {
-            const int nb = (int)min((int64_t)kLzWQ, t1 - sb);
-            __syncthreads();
-            for (int e = threadIdx.x; e < nb * k; e += kThreads) qc[e] = A.Q[sb * k + e];
-            __syncthreads();
+        for (int sb = 0; sb < nq; sb += (QALL ? nq : kLzWQ)) {
+            const int nb = QALL ? nq : min(kLzWQ, nq - sb);
+            const double* qc = QALL ? qv : qv;
+            if (!QALL) {
+                __syncthreads();
+                for (int e = threadIdx.x; e < nb * k; e += kThreads) qv[e] = A.Q[(t0 + sb) * k + e];
+                __syncthreads();
+            }
 #pragma unroll
             for (int u = 0; u < CPW; ++u) {
                 const int c = warp + u * (kThreads / 32);
                 if (c >= nc) continue;
                 const int64_t j = j0 + c;
                 for (int b = 0; b < nb; ++b) {
-                    const int64_t s = sb + b;
+                    const int64_t s = t0 + sb + b;
                     if (pj[u] < t1 && s >= pj[u]) {
                         if (lane == 0) A.R[s * N + j] = s == pj[u] ? A.diag[s] : 0.0;
                         continue;
                     }
-                    const double r = lzw_dot(qc + b * k, w[u], k);
+                    const double r = lzw_dot(qc + (QALL ? sb + b : b) * k, w[u], k);
                     if (lane == 0) A.R[s * N + j] = r;
                     if (pj[u] >= t1)
                         lzw_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj[u],
@@ -1256,7 +1277,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t
             if (c >= nc || pj[u] < t1) continue;
             const int64_t j = j0 + c;
             if (lane == 0) {
-                if (t1 > t0) {
+                if (nq > 0) {
                     A.nu[j] = nuj[u];
                     A.cref[j] = crefj[u];
                 }
@@ -1265,6 +1286,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t
                 msum += nuj[u];
             }
         }
+        __syncthreads();  // buffer `buf` is refilled two tiles later
+        buf ^= 1;
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sdm);
@@ -3894,8 +3917,12 @@ void WideQrcp::lz_step(int64_t t) {
 void WideQrcp::lz_refresh(int64_t t1, bool force) {
     LzArgs A = lz_args();
     if (lzw_) {
-        const size_t smem = sizeof(double) * (size_t)(k_ * (kLzWT + 1) + kLzWQ * k_);
-        auto kern = layout_ == Layout::Col ? k_lzw_refresh<0> : k_lzw_refresh<1>;
+        // Q rows t0..t1-1 (at most steps_ of them) resident when they fit beside the two tiles
+        const size_t tiles = sizeof(double) * 2 * (size_t)(k_ * (kLzWT + 1));
+        const bool qall = tiles + sizeof(double) * (size_t)(std::max<int64_t>(steps_, 1) * k_) <= 210 * 1024;
+        const size_t smem = tiles + sizeof(double) * (size_t)((qall ? std::max<int64_t>(steps_, 1) : kLzWQ) * k_);
+        auto kern = layout_ == Layout::Col ? (qall ? k_lzw_refresh<0, true> : k_lzw_refresh<0, false>)
+                                           : (qall ? k_lzw_refresh<1, true> : k_lzw_refresh<1, false>);
         allow_smem(kern, smem);
         prof_begin();
         TTG_LAUNCH(kern, std::min(ncand_ + ngc_, sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
