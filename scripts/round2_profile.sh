@@ -2,7 +2,7 @@
 # Round-2 profile pass (GPU box): all GPU tests, smoke, bench lines for configs 3 (headline),
 # 5, 2, 1, the reference arm, the config-4 loop, the ncu launch list of the headline bench and
 # an ncu --set full capture of its dominant kernel (a non-idle exact pass of the candidate engine).
-O=gpurun_out/r2b
+O=gpurun_out/r2c
 mkdir -p $O
 nvidia-smi > $O/nvidia_smi.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1
