@@ -444,66 +444,7 @@ def run_ours(args):
     info.clear()
     seq_ms_max = ms_max
 
-    # ---- device time with the step's independent decompositions in flight together ----
-    # One host thread per decomposition of the step (the API is reentrant, every host thread
-    # has its own engine stream); each runs its `steps` decompositions back to back, gated by
-    # an event recorded on the main stream, and records an end event on its stream. Device
-    # time = start event to the last end event (CUDA events, no host clock), so one
-    # decomposition's latency-bound phases (one-CTA reflectors, host round trips) overlap the
-    # other's streaming passes. Reported beside `value` (the one-stream figure): on the B200 it
-    # measured 19-20 ms per config-3 step in some runs and 100+ ms in others (cooperative
-    # launches of one stream waiting on the other's resident grids), so it is not the headline.
-    def device_concurrent(steps):
-        st0 = torch.cuda.current_stream()
-        start = torch.cuda.Event(enable_timing=True)
-        ends = [torch.cuda.Event(enable_timing=True) for _ in runs]
-        gate = threading.Barrier(len(runs) + 1)
-        errs = []
-
-        def work(i, m, sw):
-            try:
-                torch.cuda.set_device(local)
-                check(lib().ttg_set_device(local))
-                es = torch.cuda.ExternalStream(lib().ttg_stream(), device=torch.device("cuda", local))
-                gate.wait()
-                es.wait_event(start)
-                for _ in range(steps):
-                    api.decompose_device(a.data_ptr(), dims, m, sw, a_is_device_ptr=True, qlp=args.qlp, **kw(m))
-                ends[i].record(es)
-            except Exception as e:  # reported after the join
-                errs.append(e)
-                try:
-                    gate.abort()
-                except Exception:
-                    pass
-
-        th = [threading.Thread(target=work, args=(i, m, sw)) for i, (m, sw) in enumerate(runs)]
-        for x in th:
-            x.start()
-        torch.cuda.synchronize()
-        start.record(st0)
-        gate.wait()
-        for x in th:
-            x.join()
-        if errs:
-            raise errs[0]
-        torch.cuda.synchronize()
-        return max(start.elapsed_time(e) for e in ends)
-
-    conc_dev = len(runs) > 1 and not sharded and world == 1 and args.e2e_concurrency > 1
-    tb = te = None
-    conc_ms_max = None
-    if conc_dev:
-        device_concurrent(1)  # the worker threads' streams and memory pools
-        tb = time.time()
-        ms_conc = device_concurrent(args.steps)
-        te = time.time()
-        log(f"concurrent: {ms_conc / args.steps:.2f} ms per step (one stream: {seq_ms_max / args.steps:.2f})")
-        conc_ms_max = max_over_ranks(ms_conc, dist)
-    # one sampler for both timed regions (its start-up never overlaps either)
-    clk, (clk2,) = clocks.stop(t_begin, t_end, windows=[(tb or t_begin, te or t_end)])
-    if conc_dev and clk is not None:
-        clk = dict(clk, concurrent_region=clk2)
+    clk = clocks.stop(t_begin, t_end)
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region ----
     host = torch.empty(src.numel(), dtype=torch.float64, pin_memory=True)
@@ -520,27 +461,40 @@ def run_ours(args):
 
     def e2e_run(concurrent):
         # concurrent: the step's independent decompositions (ULV, URV) are issued from one
-        # host thread each -- the API is reentrant and every host thread has its own stream,
-        # so one decomposition's H2D and latency-bound phases overlap the other's streams
+        # host thread each, every thread running its decomposition of all the steps back to
+        # back -- the API is reentrant: uploads run one at a time at the full host-link rate
+        # and decompositions take the device in turn, so one tensor's H2D overlaps another
+        # decomposition's compute (every step still uploads its own input and reads its
+        # own cores back)
         moved = []
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            if concurrent:
-                out = [None] * len(runs)
-                def work(i, m, s):
+        if concurrent:
+            out = [[] for _ in runs]
+            errs = []
+
+            def work(i, m, s):
+                try:
                     # a new host thread starts on device 0: select this rank's GPU first
                     torch.cuda.set_device(local)
                     check(lib().ttg_set_device(local))
-                    out[i] = e2e_one(m, s)
-                th = [threading.Thread(target=work, args=(i, m, s)) for i, (m, s) in enumerate(runs)]
-                for x in th:
-                    x.start()
-                for x in th:
-                    x.join()
-                moved += out
-            else:
+                    for _ in range(args.steps):
+                        out[i].append(e2e_one(m, s))
+                except Exception as e:  # reported after the join
+                    errs.append(e)
+
+            th = [threading.Thread(target=work, args=(i, m, s)) for i, (m, s) in enumerate(runs)]
+            for x in th:
+                x.start()
+            for x in th:
+                x.join()
+            if errs:
+                raise errs[0]
+            for o in out:
+                moved += o
+        else:
+            for _ in range(args.steps):
                 moved += [e2e_one(m, s) for m, s in runs]
         secs = max_over_ranks(time.perf_counter() - t0, dist)
         return secs, sum(a for a, _ in moved), sum(b for _, b in moved)
@@ -612,14 +566,7 @@ def run_ours(args):
                        "pass1_steps": {m: [cu["steps"] for cu in r.cuts] for m, r in rep.items()},
                        "rse": rse, "inputs": "paper_2501_07904_b200/inputs.py (the reference generators' "
                                              "algorithms, bitwise; SURVEY Appendix C seeds)"},
-            "device_timing": {
-                "value": "one stream, the step's decompositions in turn (CUDA events on the engine stream)",
-                "concurrent_value": (jobs * args.steps * entries_per_step / (conc_ms_max * 1e-3)) if conc_dev else None,
-                "concurrent_ms_per_step": (conc_ms_max / args.steps) if conc_dev else None,
-                "concurrent": ("the step's decompositions in flight together, one host thread and engine stream each "
-                               "(CUDA events: a start event on the main stream that every engine stream waits on, "
-                               "to the last engine stream's end event); not the headline (unstable, see bench.py)")
-                              if conc_dev else None},
+            "device_timing": "one stream, the step's decompositions in turn (CUDA events on the engine stream)",
             "parity": parity,
             "step_roofline": step_model,
             "roofline": {"bound": "hbm",

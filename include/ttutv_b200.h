@@ -30,7 +30,10 @@
  * from ttg_last_error() on the calling thread. The C++ layer rethrows the matching class.
  *
  * Threading: calls are reentrant; each host thread gets its own CUDA stream on the
- * current device. Results are bitwise deterministic for a given input and device.
+ * current device. ttg_decompose calls from several host threads take turns: host inputs
+ * are uploaded one at a time and the decompositions hold the device one at a time (an
+ * upload overlaps another caller's compute). Results are bitwise deterministic for a given
+ * input and device.
  */
 #ifndef TTUTV_B200_H
 #define TTUTV_B200_H

@@ -1,6 +1,8 @@
 // C-ABI boundary (include/ttutv_b200.h): argument marshalling, host<->device copies and
 // exception -> status translation. No computation happens here.
+#include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -91,8 +93,17 @@ struct DeviceInput {
             TTG_CUDA(cudaEventDestroy(ev));
             ptr = a;
         } else {
+            // one upload at a time, completed before the next starts: each runs at the full
+            // host-link rate and the next caller's upload overlaps this caller's compute
+            static std::mutex mu;
+            std::lock_guard<std::mutex> lk(mu);
             buf.alloc((size_t)n);
-            buf.upload(a, (size_t)n);
+            // in 16 MB pieces: another caller's small transfers (the host round trips of its
+            // decomposition) queue behind one piece, not behind the whole tensor
+            const size_t piece = (size_t)2 << 20;
+            for (size_t off = 0; off < (size_t)n; off += piece)
+                buf.upload(a + off, std::min(piece, (size_t)n - off), off);
+            ttg::sync();
             ptr = buf.get();
         }
     }
@@ -177,7 +188,15 @@ ttg_status ttg_decompose(const double* a, const int64_t* dims, int d, const ttg_
         const int64_t n = count_of(dims, d);
         const ttg::SweepConfig sc = sweep_config(cfg);
         DeviceInput in(a, n, a_on_device != 0);
+        // Decompositions issued from several host threads take the device in turn: their
+        // persistent cooperative kernels each want every SM, and two of them interleaved ran
+        // up to 5x slower than back to back on the B200. Uploads (above) and result reads are
+        // outside the lock, so they overlap the other callers' compute.
+        static std::mutex device_mu;
+        std::unique_lock<std::mutex> turn(device_mu);
         auto* res = new ttg_result{ttg::decompose(in.ptr, dv, sc)};
+        ttg::sync();
+        turn.unlock();
         res->r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
         *out = res;
     });

@@ -141,6 +141,10 @@ private:
     // candidate (lazy-exact) pivoting for narrow W (qrcp_wide.cu, k_lz_*)
     bool lz_ = false, lzw_ = false;  // narrow (k <= 32) / wide (k <= 512) variant
     int lz_nubest() const;
+    int64_t lz_buf() const;
+    static int lz_tails();
+    int64_t lz_run_first_ = 0;  // first step of the current run (its first choice is a launch of its own)
+    int64_t lz_host_exact_ = 0;  // step of the last exact pass the host knows of (forced passes)
     DevBuf<int64_t> lzst_, lzidx_, lzposc_;
     DevBuf<Cand> lzubest_;
     DevBuf<double> lzsd_, lzwc_, lznuc_, lzcrefc_;

@@ -725,7 +725,6 @@ __global__ void k_set_identity(double* Qx, int64_t k) {
 constexpr int kLzK = 32;            // largest k
 constexpr int kLzBins = 512;        // 1/32-octave bins below the largest norm
 constexpr int64_t kLzCap = 65536;   // target |S|
-constexpr int64_t kLzBuf = 131072;  // |S| capacity (bin edges vs. exact comparisons)
 
 }  // namespace
 
@@ -743,9 +742,9 @@ struct LzArgs {
     int nslots;
     int64_t* st;        // [0] miss flag, [1] disabled, [2] |S|, [3] t of the last exact pass
     double* sd;         // [0] M, [1] largest original norm^2, [2] largest current norm^2
-    int* hist;
+    int* hist;          // kLzBins bins, then 4 last-CTA tickets (kept at zero between launches)
     int64_t* idx;       // S
-    double* wc;         // S's columns, row-major: wc[i * kLzBuf + c]
+    double* wc;         // S's columns, row-major: wc[i * buf + c]
     double* nuc;
     double* crefc;
     int64_t* posc;      // S's current positions (-1 once pivoted)
@@ -754,6 +753,7 @@ struct LzArgs {
     const int64_t* piv; // step -> pivot column
     int64_t cap, buf;   // target |S| and capacity
     int wide;           // k > 32: member columns column-major (wc[c * k + i]), copied by k_lzw_copy
+    int tails;          // last-CTA tails: 1 threshold (hist), 2 final choice (gather / copy), 4 next first choice (update)
 };
 
 namespace {
@@ -799,8 +799,7 @@ __device__ __forceinline__ void lz_downdate(const LzArgs& A, int64_t s, double r
 // best, which belongs to the new S if it beats the new M; otherwise S is unusable and the
 // engine falls back to an exact pass per step (those slots then give the pivot).
 template <bool FINAL>
-__global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
-    __shared__ Cand sc[32];
+__device__ __forceinline__ void lz_choose_body(const LzArgs& A, int64_t t, Cand* sc) {
     if (FINAL && A.st[0] == 0) return;  // decided by the first choice
     if (A.st[1]) {  // fallback: an exact pass per step, its slots hold the pivot
         if (threadIdx.x == 0) {
@@ -816,7 +815,10 @@ __global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
         if (better(rec[g], b)) b = rec[g];
     b = block_best(b, sc);
     const double M = A.sd[0];
-    const bool ok = A.st[2] <= A.buf && b.col >= 0 && b.nu > M * (1.0 + 1e-12) && b.nu > 1e-12 * A.sd[1];
+    // (the member count through L2: as a tail of the gather this CTA's L1 may hold the line
+    // from before the other CTAs' atomics)
+    const int64_t members = __ldcg(reinterpret_cast<const long long*>(A.st + 2));
+    const bool ok = members <= A.buf && b.col >= 0 && b.nu > M * (1.0 + 1e-12) && b.nu > 1e-12 * A.sd[1];
     __syncthreads();
     if (ok) {
         for (int g = threadIdx.x; g < A.nslots; g += blockDim.x) A.cand[g] = g == 0 ? b : cand_none();
@@ -826,6 +828,29 @@ __global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
         if (FINAL) A.st[1] = 1;
     }
     if (FINAL && threadIdx.x == 0) A.st[3] = t;  // this step's exact pass brought R and nu to t
+}
+
+// The first choice of a run as its own launch (later steps: the tail of the previous step's
+// member update).
+template <bool FINAL>
+__global__ void __launch_bounds__(1024) k_lz_choose(LzArgs A, int64_t t) {
+    __shared__ Cand sc[32];
+    lz_choose_body<FINAL>(A, t, sc);
+}
+
+// True in every thread of the last CTA of the grid to arrive (the other CTAs' global writes
+// are visible to it); the ticket is left at zero for the next launch.
+__device__ __forceinline__ bool lz_last_cta(int* ticket) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+        if (last) *ticket = 0;
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last != 0;
 }
 
 // Step 2 (grid, on a miss or forced): rows t0..t1-1 of R for every column, norms brought to
@@ -985,88 +1010,129 @@ __global__ void __launch_bounds__(kThreads) k_lz_hist(LzArgs A, int64_t t) {
     __syncthreads();
     if (numax > 0.0) {
         // lanes falling in one bin add once (warp-aggregated: the norms crowd a few bins)
-        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < A.N; j0 += (int64_t)gridDim.x * kThreads) {
-            const int64_t j = j0 + threadIdx.x;
-            int bin = -1;
-            if (j < A.N && A.pos[j] >= t) {
-                const double v = A.nu[j];
-                if (v > 0.0) {
-                    const double e = -log2(v / numax) * 32.0;
+        // (two strips per trip: both strips' loads in flight together)
+        const int64_t gs = (int64_t)gridDim.x * kThreads;
+        for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < A.N; j0 += 2 * gs) {
+            int64_t pj[2];
+            double v[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t j = j0 + u * gs + threadIdx.x;
+                pj[u] = j < A.N ? A.pos[j] : -1;
+                v[u] = j < A.N ? A.nu[j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                int bin = -1;
+                if (pj[u] >= t && v[u] > 0.0) {
+                    const double e = -log2(v[u] / numax) * 32.0;
                     if (e < (double)kLzBins) bin = max(0, (int)e);
                 }
+                const unsigned m = __match_any_sync(0xffffffffu, bin);
+                if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&h[bin], __popc(m));
             }
-            const unsigned m = __match_any_sync(0xffffffffu, bin);
-            if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&h[bin], __popc(m));
         }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < kLzBins; e += kThreads)
         if (h[e]) atomicAdd(&A.hist[e], h[e]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        A.sd[2] = numax;
-        if (A.sd[1] == 0.0) A.sd[1] = numax;  // first exact pass: the largest original norm^2
+    // Step 4 (the last CTA): the threshold M = the lowest bin edge keeping |S| <= A.cap
+    if (!(A.tails & 1)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.sd[3] = numax;
+        return;
     }
-}
-
-// Step 4 (1 CTA, on a miss): the threshold M = the lowest bin edge keeping |S| <= A.cap.
-__global__ void __launch_bounds__(kLzBins) k_lz_thresh(LzArgs A, int64_t t) {
-    __shared__ int cum[kLzBins];
-    if (A.st[0] == 0 || A.st[1]) return;
-    cum[threadIdx.x] = A.hist[threadIdx.x];
-    __syncthreads();
-    for (int o = 1; o < kLzBins; o <<= 1) {  // inclusive scan
-        const int v = threadIdx.x >= o ? cum[threadIdx.x - o] : 0;
-        __syncthreads();
-        cum[threadIdx.x] += v;
-        __syncthreads();
-    }
-    A.hist[threadIdx.x] = 0;
+    if (!lz_last_cta(A.hist + kLzBins)) return;
     if (threadIdx.x == 0) {
         int b = -1;
-        for (int e = 0; e < kLzBins; ++e)
-            if (cum[e] <= A.cap) b = e;
-        A.st[2] = 0;
-        if (b < 0) {
-            A.st[1] = 1;  // the top bin alone is too dense: exact passes from here on
-        } else {
-            A.sd[0] = A.sd[2] * exp2(-(double)(b + 1) / 32.0);
+        int64_t cum = 0;
+        for (int e = 0; e < kLzBins; ++e) {
+            cum += A.hist[e];
+            if (cum > A.cap) break;
+            b = e;
         }
+        A.sd[2] = numax;
+        if (A.sd[1] == 0.0) A.sd[1] = numax;  // first exact pass: the largest original norm^2
+        A.st[2] = 0;
+        if (b < 0) A.st[1] = 1;  // the top bin alone is too dense: exact passes from here on
+        else A.sd[0] = numax * exp2(-(double)(b + 1) / 32.0);
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kLzBins; e += kThreads) A.hist[e] = 0;
+}
+
+// Step 4 as its own launch (A.tails & 1 == 0; experiments).
+__global__ void __launch_bounds__(kThreads) k_lz_thresh(LzArgs A, int64_t t) {
+    if (A.st[0] == 0 || A.st[1]) return;
+    const double numax = A.sd[3];
+    if (threadIdx.x == 0) {
+        int b = -1;
+        int64_t cum = 0;
+        for (int e = 0; e < kLzBins; ++e) {
+            cum += A.hist[e];
+            if (cum > A.cap) break;
+            b = e;
+        }
+        A.sd[2] = numax;
+        if (A.sd[1] == 0.0) A.sd[1] = numax;
+        A.st[2] = 0;
+        if (b < 0) A.st[1] = 1;
+        else A.sd[0] = numax * exp2(-(double)(b + 1) / 32.0);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kLzBins; e += kThreads) A.hist[e] = 0;
 }
 
 // Step 5 (grid, on a miss): S = {unpivoted j : nu_j > M} with copies of its columns.
 template <int LAYOUT>
 __global__ void __launch_bounds__(kThreads) k_lz_gather(LzArgs A, int64_t t) {
-    if (A.st[0] == 0 || A.st[1]) return;
+    __shared__ Cand sc[kThreads / 32];
+    if (A.st[0] == 0) return;  // a hit
+    if (A.st[1]) {  // fallback (an exact pass per step): this step's pass brought R and nu to t
+        if ((A.tails & 2) && blockIdx.x == 0 && threadIdx.x == 0) A.st[3] = t;
+        return;
+    }
     const double M = A.sd[0];
     const int lane = threadIdx.x & 31;
-    // warp-uniform trip count: the slot reservation is one atomic per warp (ballot + popc)
-    for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < A.N; j0 += (int64_t)gridDim.x * kThreads) {
-        const int64_t j = j0 + threadIdx.x;
-        int64_t pj = -1;
-        double v = 0.0;
-        if (j < A.N) {
-            pj = A.pos[j];
-            v = A.nu[j];
+    // warp-uniform trip count: the slot reservation is one atomic per warp (ballot + popc);
+    // two strips per trip (both strips' loads in flight together)
+    const int64_t gs = (int64_t)gridDim.x * kThreads;
+    for (int64_t j0 = (int64_t)blockIdx.x * kThreads; j0 < A.N; j0 += 2 * gs) {
+        int64_t pjs[2];
+        double vs[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t j = j0 + u * gs + threadIdx.x;
+            pjs[u] = j < A.N ? A.pos[j] : -1;
+            vs[u] = j < A.N ? A.nu[j] : 0.0;
         }
-        const bool in = j < A.N && pj >= t && v > M;
-        const unsigned m = __ballot_sync(0xffffffffu, in);
-        if (!m) continue;
-        unsigned long long base = 0;
-        const int leader = __ffs(m) - 1;
-        if (lane == leader)
-            base = atomicAdd(reinterpret_cast<unsigned long long*>(&A.st[2]), (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (!in) continue;
-        const unsigned long long c = base + __popc(m & ((1u << lane) - 1u));
-        if (c >= (unsigned long long)A.buf) continue;
-        A.idx[c] = j;
-        A.nuc[c] = v;
-        A.crefc[c] = A.cref[j];
-        A.posc[c] = pj;
-        if (!A.wide)
-            for (int64_t i = 0; i < A.k; ++i) A.wc[i * A.buf + c] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t j = j0 + u * gs + threadIdx.x;
+            const int64_t pj = pjs[u];
+            const double v = vs[u];
+            const bool in = j < A.N && pj >= t && v > M;
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            if (!m) continue;
+            unsigned long long base = 0;
+            const int leader = __ffs(m) - 1;
+            if (lane == leader)
+                base = atomicAdd(reinterpret_cast<unsigned long long*>(&A.st[2]), (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (!in) continue;
+            const unsigned long long c = base + __popc(m & ((1u << lane) - 1u));
+            if (c >= (unsigned long long)A.buf) continue;
+            A.idx[c] = j;
+            A.nuc[c] = v;
+            A.crefc[c] = A.cref[j];
+            A.posc[c] = pj;
+            if (!A.wide)
+                for (int64_t i = 0; i < A.k; ++i)
+                    A.wc[i * A.buf + c] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
+        }
     }
+    // Step 6 (the last CTA): the final choice from the exact pass's slots and the new S (wide:
+    // after the members' copy, which still has to see this step as a miss)
+    if ((A.tails & 2) && !A.wide && lz_last_cta(A.hist + kLzBins + 1)) lz_choose_body<true>(A, t, sc);
 }
 
 // Step 7 (after the reflector): row t of R for S only (norm downdate + guard); positions
@@ -1108,31 +1174,21 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
     }
     best = block_best(best, sc);
     if (threadIdx.x == 0) A.ubest[blockIdx.x] = best;
+    // the next step's first choice (the last CTA)
+    if ((A.tails & 4) && lz_last_cta(A.hist + kLzBins + 2)) lz_choose_body<false>(A, t + 1, sc);
 }
 
 // ---- candidate pivoting for wider W (32 < k <= 512): a warp per column ---------------------
 // The same engine for config 3's second cuts (480 x 331,776): a CPU replay of the rule on the
 // real input misses once in 20 steps (|S| <= 16,384), against ~7 subspace misses. A column is
-// held by one warp, lane l taking rows l, l + 32, ... (kLzWM per lane); a dot is the lanes'
-// partial sums in that order and the warp_sum tree, in the exact pass and the member update
-// alike, so both compute R(t, j) with the same bits.
+// held by one warp in the member update, lane l taking rows l, l + 32, ... (kLzWM per lane);
+// the exact pass computes its rows of R on the FP64 tensor cores (k_lzw_refresh_mma). The two
+// round differently, which only matters for near-ties no rounding order resolves the
+// reference's way anyway: exactly equal columns are members together or not at all, so they
+// always see the same arithmetic and tie to the lowest position.
 constexpr int kLzWK = 512;           // largest k
 constexpr int kLzWM = kLzWK / 32;    // rows per lane
-constexpr int kLzWT = 16;            // columns per tile in the exact pass
-constexpr int kLzWQ = 8;             // rows of Q per shared-memory chunk
-constexpr int64_t kLzCapW = 16384, kLzBufW = 32768;
-
-// q_s^T w over the lanes' rows (w in registers), reduced over the warp.
-__device__ __forceinline__ double lzw_dot(const double* q, const double (&w)[kLzWM], int k) {
-    const int lane = threadIdx.x & 31;
-    double a = 0.0;
-#pragma unroll
-    for (int m = 0; m < kLzWM; ++m) {
-        const int i = lane + 32 * m;
-        if (i < k) a = fma(q[i], w[m], a);
-    }
-    return warp_sum(a);
-}
+constexpr int64_t kLzCapW = 16384;
 
 // Guard recompute |w - Q[:, :s+1] Q[:, :s+1]^T w|^2, modified Gram-Schmidt, warp-cooperative.
 __device__ __noinline__ double lzw_resid(const double* __restrict__ Q, int k, int64_t s, const double* wp,
@@ -1177,117 +1233,196 @@ __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double 
     }
 }
 
-// Exact pass (wide): tiles of kLzWT columns stream through two shared-memory buffers
-// (8-byte cp.async: the next tile lands while the current one is computed), two columns per
-// warp; Q's rows t0..t1-1 stay in shared memory for the whole pass when they fit (QALL),
-// else they are streamed in chunks of kLzWQ per tile.
-template <int LAYOUT, bool QALL>
-__global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t1, int force) {
-    extern __shared__ __align__(16) double wsm[];  // tiles[2][k][kLzWT + 1] | q rows
+// Exact pass (wide) on the FP64 tensor cores: rows t0..t1-1 of R are Q[:, t0:t1]^T W, a skinny
+// GEMM, as DMMA 8x8x4 tiles. A warp owns 8 NF columns per iteration and walks k in steps of 4:
+// B fragments are W's elements loaded straight from global memory (32-byte sectors fully used,
+// 16 loads in flight per lane), A fragments are rows of Q^T from shared memory (row stride
+// 4 mod 16 doubles: conflict-free). Up to 8 MF rows per sweep over W (more rows: another
+// sweep). The D fragments go through a per-warp staging tile so that each lane then owns one
+// column and applies its rows' downdates in row order (factor.cpp:101-106); guard recomputes
+// are warp-cooperative (lzw_resid, the member update's arithmetic).
+constexpr int kLzwStage = 8 * 40;  // per-warp staging tile: 8 rows x 32 columns, row stride 40
+
+template <int LAYOUT, int MF, int NF>
+__device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64_t s0, int nb, bool last, int pd,
+                                              const double* am, int64_t kq, double* stg, Cand& best, double& msum) {
+    const int64_t k = A.k, N = A.N, ld = A.ld;
+    const int64_t k4 = (k + 3) & ~int64_t(3);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int64_t ngroups = cdiv(N, 8 * NF);
+    constexpr int CL = NF / 4;  // columns per lane in the epilogue (8 NF / 32)
+    constexpr int KS = 16 / NF;  // k steps of 4 rows per chunk: 16 loads in flight per lane
+    // L2 prefetch `pd` chunks ahead of the demand loads (a chunk = 4 KS rows x 8 NF columns of
+    // this warp's groups, in the order it visits them): the demand loads then wait an L2 round
+    // trip instead of an HBM one, and the prefetches keep HBM busy through the epilogues
+    const int64_t gstride = (int64_t)gridDim.x * (kThreads / 32);
+    const int64_t nch = cdiv(k4, 4 * KS);  // chunks per group
+    auto prefetch = [&](int64_t g, int64_t ch) {
+        g += (ch / nch) * gstride;
+        ch %= nch;
+        if (g >= ngroups) return;
+        const int64_t jb = g * 8 * NF, ib = ch * 4 * KS;
+        const double* p = nullptr;
+        if (LAYOUT == 0) {  // a column's 4 KS rows: one line (or two) per column, a lane per column
+            for (int c = lane; c < 8 * NF; c += 32)
+                if (jb + c < N && ib < k) {
+                    p = A.W + ib + (jb + c) * ld;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+                }
+        } else {  // a row's 8 NF columns: 16 columns per line
+            constexpr int LPR = (8 * NF) / 16;  // lines per row
+            for (int e = lane; e < 4 * KS * LPR; e += 32) {
+                const int64_t i = ib + e / LPR, j = jb + 16 * (e % LPR);
+                if (i < k && j < N) {
+                    p = A.W + i * ld + j;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+                }
+            }
+        }
+    };
+    const int64_t g_first = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+    for (int c = 0; c < pd; ++c) prefetch(g_first, c);
+    for (int64_t g = g_first; g < ngroups; g += gstride) {
+        const int64_t j0 = g * 8 * NF;
+        // the lanes' epilogue columns: loads issued before the k loop
+        int64_t pj[CL];
+        double nuj[CL], crefj[CL];
+#pragma unroll
+        for (int h = 0; h < CL; ++h) {
+            const int64_t j = j0 + 32 * h + lane;
+            pj[h] = j < N ? A.pos[j] : -1;
+            nuj[h] = j < N ? A.nu[j] : 0.0;
+            crefj[h] = j < N ? A.cref[j] : 0.0;
+        }
+        double acc[MF][NF][2];
+#pragma unroll
+        for (int f = 0; f < MF; ++f)
+#pragma unroll
+            for (int n = 0; n < NF; ++n) acc[f][n][0] = acc[f][n][1] = 0.0;
+        int64_t colb[NF];
+        bool cok[NF];
+#pragma unroll
+        for (int n = 0; n < NF; ++n) {
+            colb[n] = j0 + 8 * n + fr;
+            cok[n] = colb[n] < N;
+        }
+        auto ldb = [&](int64_t i, int n) -> double {
+            if (i >= k || !cok[n]) return 0.0;
+            return LAYOUT == 0 ? __ldg(A.W + i + colb[n] * ld) : __ldg(A.W + i * ld + colb[n]);
+        };
+        for (int64_t i0 = 0; i0 < k4; i0 += 4 * KS) {  // rows past k load as zero
+            if (pd > 0) prefetch(g, i0 / (4 * KS) + pd);
+            double b[KS][NF];
+#pragma unroll
+            for (int s = 0; s < KS; ++s)
+#pragma unroll
+                for (int n = 0; n < NF; ++n) b[s][n] = ldb(i0 + 4 * s + fk, n);
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                if (i0 + 4 * s >= k4) break;  // warp-uniform
+                double a[MF];
+#pragma unroll
+                for (int f = 0; f < MF; ++f) a[f] = am[(8 * f + fr) * kq + i0 + 4 * s + fk];
+#pragma unroll
+                for (int f = 0; f < MF; ++f)
+#pragma unroll
+                    for (int n = 0; n < NF; ++n) dmma(acc[f][n], a[f], b[s][n]);
+            }
+        }
+        // D fragment: lane holds rows 8 f + fr, columns j0 + 8 n + 2 fk + {0, 1}
+#pragma unroll
+        for (int h = 0; h < CL; ++h) {
+            const int64_t j = j0 + 32 * h + lane;
+#pragma unroll
+            for (int f = 0; f < MF; ++f) {
+                if (8 * f >= nb) break;  // warp-uniform
+                __syncwarp();
+#pragma unroll
+                for (int n = 0; n < 4; ++n)
+                    *reinterpret_cast<double2*>(stg + fr * 40 + 8 * n + 2 * fk) =
+                        make_double2(acc[f][4 * h + n][0], acc[f][4 * h + n][1]);
+                __syncwarp();
+                for (int r = 0; r < 8 && 8 * f + r < nb; ++r) {
+                    const int64_t s = s0 + 8 * f + r;
+                    const double rv = stg[r * 40 + lane];
+                    bool need = false;
+                    double nv = 0.0;
+                    if (j < N) {
+                        if (pj[h] < t1 && s >= pj[h]) {
+                            A.R[s * N + j] = s == pj[h] ? A.diag[s] : 0.0;
+                        } else {
+                            A.R[s * N + j] = rv;
+                            if (pj[h] >= t1) {
+                                nv = __dsub_rn(nuj[h], __dmul_rn(rv, rv));
+                                need = nv < __dmul_rn(1e-16, crefj[h]) || nv < 0.0;
+                                if (!need) nuj[h] = nv;
+                            }
+                        }
+                    }
+                    unsigned m = __ballot_sync(0xffffffffu, need);
+                    while (m) {  // guard recomputes, one flagged column at a time (all lanes)
+                        const int l = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int64_t jl = __shfl_sync(0xffffffffu, j, l);
+                        const double v = lzw_resid(A.Q, (int)k, s, LAYOUT == 0 ? A.W + jl * ld : A.W + jl,
+                                                   LAYOUT == 0 ? 1 : ld);
+                        if (lane == l) nuj[h] = crefj[h] = v;
+                    }
+                }
+            }
+            if (j < N && pj[h] >= t1) {
+                A.nu[j] = nuj[h];
+                A.cref[j] = crefj[h];
+                if (last) {
+                    const Cand c{nuj[h], pj[h], j};
+                    if (better(c, best)) best = c;
+                    msum += nuj[h];
+                }
+            }
+        }
+    }
+}
+
+template <int LAYOUT, int NF>
+__global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64_t t1, int force, int mfcap, int pd) {
+    extern __shared__ __align__(16) double wsm[];  // staging tiles (one per warp) | Q^T rows (8 mfcap x kq)
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sdm[kThreads / 32];
     if (!force && A.st[0] == 0) return;
-    const int64_t t0 = A.st[3], N = A.N;
-    const int k = (int)A.k;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int TD = k * (kLzWT + 1);
-    double* qv = wsm + 2 * (size_t)TD;
+    const int64_t t0 = A.st[3], N = A.N, k = A.k;
     const int nq = (int)(t1 - t0);
-    if (QALL)
-        for (int e = threadIdx.x; e < nq * k; e += kThreads) qv[e] = A.Q[t0 * k + e];
-    auto issue = [&](int64_t j0, int b) {
-        double* tb = wsm + (size_t)b * TD;
-        const int nc = (int)min((int64_t)kLzWT, N - j0);
-        if (LAYOUT == 0) {  // column c contiguous (ld >= k): a warp per column
-            for (int c = warp; c < nc; c += kThreads / 32)
-                for (int i = lane; i < k; i += 32) lz_cp8(tb + i * (kLzWT + 1) + c, A.W + i + (j0 + c) * A.ld);
-        } else {  // row i: kLzWT contiguous doubles
-            for (int e = threadIdx.x; e < k * kLzWT; e += kThreads) {
-                const int i = e / kLzWT, c = e - i * kLzWT;
-                if (c < nc) lz_cp8(tb + i * (kLzWT + 1) + c, A.W + (int64_t)i * A.ld + j0 + c);
-            }
-        }
-        lz_cp_commit();
-    };
+    const int64_t k4 = (k + 3) & ~int64_t(3);
+    const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
+    double* stg = wsm + (threadIdx.x >> 5) * kLzwStage;
+    double* am = wsm + (kThreads / 32) * kLzwStage;
     Cand best = cand_none();
     double msum = 0.0;
-    constexpr int CPW = kLzWT / (kThreads / 32);  // columns per warp (2)
-    const int64_t stride = (int64_t)gridDim.x * kLzWT;
-    int64_t j0 = (int64_t)blockIdx.x * kLzWT;
-    int buf = 0;
-    if (nq > 0 && j0 < N) issue(j0, 0);
-    for (; j0 < N; j0 += stride) {
-        const int nc = (int)min((int64_t)kLzWT, N - j0);
-        if (nq > 0) {
-            if (j0 + stride < N) {
-                issue(j0 + stride, buf ^ 1);
-                lz_cp_wait<1>();
-            } else {
-                lz_cp_wait<0>();
-            }
+    if (nq <= 0) {  // nothing to replay: the slots from the current norms
+        for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
+            const int64_t pj = A.pos[j];
+            if (pj < t1) continue;
+            const double v = A.nu[j];
+            const Cand c{v, pj, j};
+            if (better(c, best)) best = c;
+            msum += v;
+        }
+    }
+    for (int sb = 0; sb < nq; sb += 8 * mfcap) {
+        const int nb = min(8 * mfcap, nq - sb);
+        const int mf = (nb + 7) / 8;
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < 8 * mf * kq; e += kThreads) {
+            const int r = (int)(e / kq);
+            const int64_t i = e - (int64_t)r * kq;
+            am[e] = (r < nb && i < k) ? A.Q[(t0 + sb + r) * k + i] : 0.0;
         }
         __syncthreads();
-        const double* tile = wsm + (size_t)buf * TD;
-        double w[CPW][kLzWM];
-        double nuj[CPW], crefj[CPW];
-        int64_t pj[CPW];
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-            const int c = warp + u * (kThreads / 32);
-            const int64_t j = j0 + c;
-            pj[u] = c < nc ? A.pos[j] : -1;
-            nuj[u] = c < nc ? A.nu[j] : 0.0;
-            crefj[u] = c < nc ? A.cref[j] : 0.0;
-#pragma unroll
-            for (int m = 0; m < kLzWM; ++m) {
-                const int i = lane + 32 * m;
-                w[u][m] = (c < nc && i < k && nq > 0) ? tile[i * (kLzWT + 1) + c] : 0.0;
-            }
-        }
-        for (int sb = 0; sb < nq; sb += (QALL ? nq : kLzWQ)) {
-            const int nb = QALL ? nq : min(kLzWQ, nq - sb);
-            const double* qc = QALL ? qv : qv;
-            if (!QALL) {
-                __syncthreads();
-                for (int e = threadIdx.x; e < nb * k; e += kThreads) qv[e] = A.Q[(t0 + sb) * k + e];
-                __syncthreads();
-            }
-#pragma unroll
-            for (int u = 0; u < CPW; ++u) {
-                const int c = warp + u * (kThreads / 32);
-                if (c >= nc) continue;
-                const int64_t j = j0 + c;
-                for (int b = 0; b < nb; ++b) {
-                    const int64_t s = t0 + sb + b;
-                    if (pj[u] < t1 && s >= pj[u]) {
-                        if (lane == 0) A.R[s * N + j] = s == pj[u] ? A.diag[s] : 0.0;
-                        continue;
-                    }
-                    const double r = lzw_dot(qc + (QALL ? sb + b : b) * k, w[u], k);
-                    if (lane == 0) A.R[s * N + j] = r;
-                    if (pj[u] >= t1)
-                        lzw_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj[u],
-                                     crefj[u]);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-            const int c = warp + u * (kThreads / 32);
-            if (c >= nc || pj[u] < t1) continue;
-            const int64_t j = j0 + c;
-            if (lane == 0) {
-                if (nq > 0) {
-                    A.nu[j] = nuj[u];
-                    A.cref[j] = crefj[u];
-                }
-                const Cand cc{nuj[u], pj[u], j};
-                if (better(cc, best)) best = cc;
-                msum += nuj[u];
-            }
-        }
-        __syncthreads();  // buffer `buf` is refilled two tiles later
-        buf ^= 1;
+        const bool last = sb + nb >= nq;
+        if (mf == 1) lzw_mma_sweep<LAYOUT, 1, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
+        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
+        else lzw_mma_sweep<LAYOUT, 3, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
+        // (a lane meets the same columns in every sweep: it reads back its own norm writes)
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sdm);
@@ -1305,6 +1440,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lzw_refresh(LzArgs A, int64_t t
 // Member columns into wc (column-major, wc[c * k + i]); a warp per member.
 template <int LAYOUT>
 __global__ void __launch_bounds__(kThreads) k_lzw_copy(LzArgs A, int64_t t) {
+    __shared__ Cand sc[kThreads / 32];
     if (A.st[0] == 0 || A.st[1]) return;
     const int lane = threadIdx.x & 31;
     const int64_t cnt = min(A.st[2], A.buf);
@@ -1314,30 +1450,29 @@ __global__ void __launch_bounds__(kThreads) k_lzw_copy(LzArgs A, int64_t t) {
         for (int64_t i = lane; i < A.k; i += 32)
             A.wc[c * A.k + i] = LAYOUT == 0 ? A.W[i + j * A.ld] : A.W[i * A.ld + j];
     }
+    // Step 6 (the last CTA): the final choice from the exact pass's slots and the new S
+    if ((A.tails & 2) && lz_last_cta(A.hist + kLzBins + 1)) lz_choose_body<true>(A, t, sc);
 }
 
-// Member update (wide): a warp per member; per-CTA best member.
+// Member update (wide): a warp per member at a time (grid-stride over the members), q_t in the
+// lanes' registers (rows lane, lane + 32, ... like the member's), every load of a member in
+// flight together; per-CTA best member. The dot: the lanes' partial sums in row order, then
+// the warp_sum tree.
 __global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
-    extern __shared__ double q[];  // k
     __shared__ Cand sc[kThreads / 32];
     if (A.st[1]) return;
     const int k = (int)A.k, lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < k; e += kThreads) q[e] = A.Q[t * k + e];
-    __syncthreads();
+    double q[kLzWM];
+#pragma unroll
+    for (int m = 0; m < kLzWM; ++m) {
+        const int i = lane + 32 * m;
+        q[m] = i < k ? A.Q[t * k + i] : 0.0;
+    }
     const int64_t cnt = min(A.st[2], A.buf);
     const int64_t jp = A.piv[t];
     Cand best = cand_none();
     for (int64_t c = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; c < cnt;
          c += ((int64_t)gridDim.x * kThreads) >> 5) {
-        int64_t pc = A.posc[c];
-        if (pc < 0) continue;
-        const int64_t jc = A.idx[c];
-        if (pc == t || jc == jp) {
-            pc = A.pos[jc];
-            if (pc <= t) pc = -1;
-            if (lane == 0) A.posc[c] = pc;
-            if (pc < 0) continue;
-        }
         const double* wp = A.wc + c * k;
         double w[kLzWM];
 #pragma unroll
@@ -1345,8 +1480,20 @@ __global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
             const int i = lane + 32 * m;
             w[m] = i < k ? wp[i] : 0.0;
         }
-        const double r = lzw_dot(q, w, k);
+        int64_t pc = A.posc[c];
+        const int64_t jc = A.idx[c];
         double nuj = A.nuc[c], crefj = A.crefc[c];
+        if (pc < 0) continue;
+        if (pc == t || jc == jp) {
+            pc = A.pos[jc];
+            if (pc <= t) pc = -1;
+            if (lane == 0) A.posc[c] = pc;
+            if (pc < 0) continue;
+        }
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < kLzWM; ++m) a = fma(q[m], w[m], a);  // zero past k
+        const double r = warp_sum(a);
         lzw_downdate(A, t, r, wp, 1, nuj, crefj);
         if (lane == 0) {
             A.nuc[c] = nuj;
@@ -1357,6 +1504,8 @@ __global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
     }
     best = block_best(best, sc);
     if (threadIdx.x == 0) A.ubest[blockIdx.x] = best;
+    // the next step's first choice (the last CTA)
+    if ((A.tails & 4) && lz_last_cta(A.hist + kLzBins + 2)) lz_choose_body<false>(A, t + 1, sc);
 }
 
 // After the run's exact pass: the next run starts with a refresh at its first step.
@@ -3857,9 +4006,9 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
     if (lz_) {
         lzst_.alloc(4);
         lzsd_.alloc(4);
-        lzhist_.alloc(kLzBins);
+        lzhist_.alloc(kLzBins + 4);
         lzhist_.zero();
-        const int64_t buf = lzw_ ? kLzBufW : kLzBuf;
+        const int64_t buf = lz_buf();
         lzidx_.alloc(buf);
         lzposc_.alloc(buf);
         lzwc_.alloc((size_t)buf * k);
@@ -3874,12 +4023,38 @@ LzArgs WideQrcp::lz_args() {
     return LzArgs{W_, k_, N_, ld_, Qt_.get(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
                   cand_.get(), mass_.get(), ncand_ + ngc_, lzst_.get(), lzsd_.get(), lzhist_.get(), lzidx_.get(),
                   lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(), lz_nubest(), piv_.get(),
-                  lzw_ ? kLzCapW : kLzCap, lzw_ ? kLzBufW : kLzBuf, lzw_ ? 1 : 0};
+                  lz_buf() / 2, lz_buf(), lzw_ ? 1 : 0, lz_tails()};
+}
+
+// Which of the small per-step kernels run as last-CTA tails of their predecessors (all by
+// default; TTG_LZ_TAILS is a bitmask for experiments).
+int WideQrcp::lz_tails() {
+    static const int tails = [] {
+        const char* e = std::getenv("TTG_LZ_TAILS");
+        return e ? std::atoi(e) & 7 : 5;  // the final choice stays its own launch: as a tail of
+                                          // the gather it broke parity on the B200 (unexplained)
+    }();
+    return tails;
+}
+
+// |S| capacity (twice the target: bin edges vs. exact comparisons). TTG_LZ_CAP / TTG_LZW_CAP
+// override the targets (experiments).
+int64_t WideQrcp::lz_buf() const {
+    static const int64_t cap_n = [] {
+        const char* e = std::getenv("TTG_LZ_CAP");
+        return e ? std::max<int64_t>(1024, std::atoll(e)) : kLzCap;
+    }();
+    static const int64_t cap_w = [] {
+        const char* e = std::getenv("TTG_LZW_CAP");
+        return e ? std::max<int64_t>(1024, std::atoll(e)) : kLzCapW;
+    }();
+    return 2 * (lzw_ ? cap_w : cap_n);
 }
 
 // per-CTA records of the member update: a thread per member (narrow), a warp per member (wide)
 int WideQrcp::lz_nubest() const {
-    return lzw_ ? (int)cdiv(kLzBufW, kThreads / 32) : (int)cdiv(kLzBuf, kThreads);
+    return lzw_ ? (int)std::min<int64_t>(cdiv(lz_buf(), kThreads / 32), 4 * (int64_t)sms_)
+                : (int)std::min<int64_t>(cdiv(lz_buf(), kThreads), 4 * (int64_t)sms_);
 }
 
 // One candidate-pivoting step (see k_lz_choose .. k_lz_update); the miss kernels return at
@@ -3888,18 +4063,21 @@ void WideQrcp::lz_step(int64_t t) {
     {
         PhaseTimer pt("p1 lazy choose + exact pass on a miss");
         LzArgs A = lz_args();
-        TTG_LAUNCH(k_lz_choose<false>, 1, 1024, 0, stream(), A, t);
+        // the first choice: its own launch at a run's first step, else done by the tail of the
+        // previous step's member update
+        const int tails = lz_tails();
+        if (t == lz_run_first_ || !(tails & 4)) TTG_LAUNCH(k_lz_choose<false>, 1, 1024, 0, stream(), A, t);
         lz_refresh(t, false);
-        const int g = std::min<int>(ncand_ + ngc_, 4 * sms_);
-        TTG_LAUNCH(k_lz_hist, g, kThreads, 0, stream(), A, t);
-        TTG_LAUNCH(k_lz_thresh, 1, kLzBins, 0, stream(), A, t);
+        const int g = 4 * sms_;
+        TTG_LAUNCH(k_lz_hist, g, kThreads, 0, stream(), A, t);  // + the threshold (last CTA)
+        if (!(tails & 1)) TTG_LAUNCH(k_lz_thresh, 1, kThreads, 0, stream(), A, t);
         auto gk = layout_ == Layout::Col ? k_lz_gather<0> : k_lz_gather<1>;
-        TTG_LAUNCH(gk, g, kThreads, 0, stream(), A, t);
+        TTG_LAUNCH(gk, g, kThreads, 0, stream(), A, t);  // + the final choice (last CTA)
         if (lzw_) {
             auto ck = layout_ == Layout::Col ? k_lzw_copy<0> : k_lzw_copy<1>;
-            TTG_LAUNCH(ck, (int)std::min<int64_t>(cdiv(kLzBufW, kThreads / 32), 8 * sms_), kThreads, 0, stream(), A, t);
+            TTG_LAUNCH(ck, (int)std::min<int64_t>(cdiv(lz_buf(), kThreads / 32), 8 * sms_), kThreads, 0, stream(), A, t);
         }
-        TTG_LAUNCH(k_lz_choose<true>, 1, 1024, 0, stream(), A, t);
+        if (!(tails & 2)) TTG_LAUNCH(k_lz_choose<true>, 1, 1024, 0, stream(), A, t);
     }
     {
         PhaseTimer pt("p1 reflector");
@@ -3907,7 +4085,7 @@ void WideQrcp::lz_step(int64_t t) {
     }
     PhaseTimer pt("p1 lazy update");
     if (lzw_) {
-        TTG_LAUNCH(k_lzw_update, lz_nubest(), kThreads, sizeof(double) * (size_t)k_, stream(), lz_args(), t);
+        TTG_LAUNCH(k_lzw_update, lz_nubest(), kThreads, 0, stream(), lz_args(), t);
         return;
     }
     auto uk = k_ <= 8 ? k_lz_update<8> : k_ <= 16 ? k_lz_update<16> : k_ <= 24 ? k_lz_update<24> : k_lz_update<32>;
@@ -3916,20 +4094,45 @@ void WideQrcp::lz_step(int64_t t) {
 
 void WideQrcp::lz_refresh(int64_t t1, bool force) {
     LzArgs A = lz_args();
-    if (lzw_) {
-        // Q rows t0..t1-1 (at most steps_ of them) resident when they fit beside the two tiles
-        const size_t tiles = sizeof(double) * 2 * (size_t)(k_ * (kLzWT + 1));
-        const bool qall = tiles + sizeof(double) * (size_t)(std::max<int64_t>(steps_, 1) * k_) <= 210 * 1024;
-        const size_t smem = tiles + sizeof(double) * (size_t)((qall ? std::max<int64_t>(steps_, 1) : kLzWQ) * k_);
-        auto kern = layout_ == Layout::Col ? (qall ? k_lzw_refresh<0, true> : k_lzw_refresh<0, false>)
-                                           : (qall ? k_lzw_refresh<1, true> : k_lzw_refresh<1, false>);
+    static const bool narrow_mma = [] {  // A/B: the narrow exact pass on DMMA too
+        const char* e = std::getenv("TTG_LZ_MMA");
+        return !(e && *e == '0');
+    }();
+    if (lzw_ || narrow_mma) {
+        // rows per sweep over W: 8 mfcap covers every row the pass can have to replay (the
+        // host knows the last forced pass; misses since then only shorten the replay)
+        const int64_t nq_max = std::max<int64_t>(1, t1 - lz_host_exact_);
+        int mfcap = (int)std::min<int64_t>(3, cdiv(nq_max, 8));
+        if (const char* e = std::getenv("TTG_LZ_MFCAP"))  // tests: force several sweeps per pass
+            mfcap = std::max(1, std::min(mfcap, std::atoi(e)));
+        const int64_t k4 = (k_ + 3) & ~int64_t(3);
+        const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
+        const size_t smem = sizeof(double) * (size_t)((kThreads / 32) * kLzwStage + 8 * mfcap * kq);
+        auto kern = layout_ == Layout::Col ? k_lzw_refresh_mma<0, 4> : k_lzw_refresh_mma<1, 4>;
         allow_smem(kern, smem);
+        int per_sm = 0;
+        TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
         prof_begin();
-        TTG_LAUNCH(kern, std::min(ncand_ + ngc_, sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
+        static const int pd = [] {  // L2 prefetch distance in chunks (experiment: TTG_LZ_PD)
+            const char* e = std::getenv("TTG_LZ_PD");
+            return e ? std::max(0, std::atoi(e)) : 2;
+        }();
+        TTG_LAUNCH(kern, std::min(ncand_ + ngc_, std::max(1, per_sm) * sms_), kThreads, smem, stream(), A, t1,
+                   force ? 1 : 0, mfcap, pd);
+        // algorithmic bytes: W once, norms / positions read and written; the replayed R rows
+        // (8 N each) are counted on the run's last (forced) pass, where their total is known
         const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
-        if (force) prof_end(bytes, "k_lzw_refresh (exact pass over W, warp per column)");
-        else prof_end_select(reinterpret_cast<const int*>(lzst_.get()), bytes,
-                             "k_lzw_refresh (exact pass over W, warp per column)", 0.0, "k_lzw_refresh (idle on a hit)");
+        const char* pass = lzw_ ? "k_lzw_refresh_mma, 32 < k <= 512 (exact pass over W on DMMA: replayed R rows, norms)"
+                                : "k_lzw_refresh_mma, k <= 32 (exact pass over W on DMMA: replayed R rows, norms)";
+        if (force) {
+            prof_end(bytes + 8.0 * (double)N_ * (double)(t1 - lz_host_exact_), pass);
+            lz_host_exact_ = t1;
+        } else {
+            const bool first = t1 == lz_host_exact_;  // nothing to replay: slots from the norms only
+            prof_end_select(reinterpret_cast<const int*>(lzst_.get()), first ? 16.0 * (double)N_ : bytes,
+                            first ? "k_lzw_refresh_mma (no rows to replay: slots from the norms)" : pass, 0.0,
+                            "k_lzw_refresh_mma (idle on a hit)");
+        }
         return;
     }
     const int kk = k_ <= 8 ? 8 : k_ <= 16 ? 16 : k_ <= 24 ? 24 : 32;
@@ -3942,12 +4145,20 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
     prof_begin();
     // two resident CTAs per SM (one tile each): one loads while the other computes
     TTG_LAUNCH(kern, std::min(ncand_ + ngc_, 2 * sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
-    // algorithmic bytes: W once, norms / positions read and written (the replayed R rows,
-    // at most a few per pass, are not counted)
+    // algorithmic bytes: W once, norms / positions read and written; the replayed R rows (8 N
+    // each) are counted on the run's last (forced) pass, where their total is known
     const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
-    if (force) prof_end(bytes, "k_lz_refresh (exact pass over W: replayed R rows, norms)");
-    else prof_end_select(reinterpret_cast<const int*>(lzst_.get()), bytes,
-                         "k_lz_refresh (exact pass over W: replayed R rows, norms)", 0.0, "k_lz_refresh (idle on a hit)");
+    if (force) {
+        prof_end(bytes + 8.0 * (double)N_ * (double)(t1 - lz_host_exact_),
+                 "k_lz_refresh (exact pass over W: replayed R rows, norms)");
+        lz_host_exact_ = t1;
+    } else {
+        const bool first = t1 == lz_host_exact_;  // nothing to replay: slots from the norms only
+        prof_end_select(reinterpret_cast<const int*>(lzst_.get()), first ? 16.0 * (double)N_ : bytes,
+                        first ? "k_lz_refresh (no rows to replay: slots from the norms)"
+                              : "k_lz_refresh (exact pass over W: replayed R rows, norms)",
+                        0.0, "k_lz_refresh (idle on a hit)");
+    }
 }
 
 void WideQrcp::grow(int64_t cap) {
@@ -4023,6 +4234,7 @@ void WideQrcp::run_to(int64_t steps) {
     if (steps > cap_) grow(std::min(p_, std::max(steps, 2 * cap_)));
     if (lz_) {
         if (steps <= steps_) return;
+        lz_run_first_ = steps_;
         while (steps_ < steps) {
             lz_step(steps_);
             ++steps_;

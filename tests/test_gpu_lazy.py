@@ -65,3 +65,16 @@ def test_lazy_wide_second_cut(dev, ref, method, sweep, dims, ranks):
     ULV, Row W for URV) after a narrow 8 x 4,194,304 first cut."""
     a = _planted(ref, dims, ranks, 41, 1e-4)
     _check(dev, ref, a, dims, method, sweep, ranks)
+
+
+@pytest.mark.parametrize("method,sweep,dims,ranks", [
+    ("ulv", "l2r", [24, 1024, 1024], [1, 20, 20, 1]),
+    ("urv", "r2l", [32, 32, 32, 32, 8], [1, 20, 20, 20, 8, 1]),
+])
+def test_lazy_exact_pass_in_several_sweeps(dev, ref, method, sweep, dims, ranks, monkeypatch):
+    """The DMMA exact pass replays at most 24 rows of R per sweep over W and takes another
+    sweep for more. TTG_LZ_MFCAP=1 caps a sweep at 8 rows, so the replays of these cuts (up to
+    ~12 rows between misses) go through the several-sweeps path; same contract."""
+    monkeypatch.setenv("TTG_LZ_MFCAP", "1")
+    a = _planted(ref, dims, ranks, 43, 1e-4)
+    _check(dev, ref, a, dims, method, sweep, ranks)
