@@ -98,11 +98,7 @@ struct DeviceInput {
             static std::mutex mu;
             std::lock_guard<std::mutex> lk(mu);
             buf.alloc((size_t)n);
-            // in 16 MB pieces: another caller's small transfers (the host round trips of its
-            // decomposition) queue behind one piece, not behind the whole tensor
-            const size_t piece = (size_t)2 << 20;
-            for (size_t off = 0; off < (size_t)n; off += piece)
-                buf.upload(a + off, std::min(piece, (size_t)n - off), off);
+            buf.upload(a, (size_t)n);
             ttg::sync();
             ptr = buf.get();
         }

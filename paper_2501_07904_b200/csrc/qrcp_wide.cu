@@ -1233,29 +1233,30 @@ __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double 
     }
 }
 
-// Exact pass (wide) on the FP64 tensor cores: rows t0..t1-1 of R are Q[:, t0:t1]^T W, a skinny
-// GEMM, as DMMA 8x8x4 tiles. A warp owns 8 NF columns per iteration and walks k in steps of 4:
+// Exact pass on the FP64 tensor cores: rows t0..t1-1 of R are Q[:, t0:t1]^T W, a skinny GEMM,
+// as DMMA 8x8x4 tiles. A warp owns 32 columns per iteration and walks k in steps of 4:
 // B fragments are W's elements loaded straight from global memory (32-byte sectors fully used,
-// 16 loads in flight per lane), A fragments are rows of Q^T from shared memory (row stride
-// 4 mod 16 doubles: conflict-free). Up to 8 MF rows per sweep over W (more rows: another
-// sweep). The D fragments go through a per-warp staging tile so that each lane then owns one
-// column and applies its rows' downdates in row order (factor.cpp:101-106); guard recomputes
-// are warp-cooperative (lzw_resid, the member update's arithmetic).
-constexpr int kLzwStage = 8 * 40;  // per-warp staging tile: 8 rows x 32 columns, row stride 40
-
-template <int LAYOUT, int MF, int NF>
+// 16 loads in flight per lane, L2 prefetch two chunks ahead), A fragments are rows of Q^T from
+// shared memory (row stride 4 mod 16 doubles: conflict-free). Up to 8 MF rows per sweep over W
+// (more rows: another sweep). Epilogue in the fragment layout: each lane stores its two
+// adjacent columns of a row of R (16 bytes), the squares r^2 are summed per column over the
+// lanes' rows by a three-step butterfly that leaves each lane one column's total, and that
+// lane downdates the column's norm once: norms only fall, so the reference's per-row guard
+// (factor.cpp:101-106) can only fire in a sweep whose last row fires it; such a column (rare)
+// is redone row by row from the stored R rows, with warp-cooperative recomputes (lzw_resid).
+// Pivoted columns (at most t1 of them) get their rows >= their position fixed up afterwards.
+template <int LAYOUT, int MF>
 __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64_t s0, int nb, bool last, int pd,
-                                              const double* am, int64_t kq, double* stg, Cand& best, double& msum) {
+                                              const double* am, int64_t kq, Cand& best, double& msum) {
+    constexpr int NF = 4;
     const int64_t k = A.k, N = A.N, ld = A.ld;
     const int64_t k4 = (k + 3) & ~int64_t(3);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fk = lane & 3;
     const int64_t ngroups = cdiv(N, 8 * NF);
-    constexpr int CL = NF / 4;  // columns per lane in the epilogue (8 NF / 32)
     constexpr int KS = 16 / NF;  // k steps of 4 rows per chunk: 16 loads in flight per lane
-    // L2 prefetch `pd` chunks ahead of the demand loads (a chunk = 4 KS rows x 8 NF columns of
-    // this warp's groups, in the order it visits them): the demand loads then wait an L2 round
-    // trip instead of an HBM one, and the prefetches keep HBM busy through the epilogues
+    // L2 prefetch `pd` chunks ahead of the demand loads (a chunk = 4 KS rows x 32 columns of
+    // this warp's groups, in the order it visits them)
     const int64_t gstride = (int64_t)gridDim.x * (kThreads / 32);
     const int64_t nch = cdiv(k4, 4 * KS);  // chunks per group
     auto prefetch = [&](int64_t g, int64_t ch) {
@@ -1263,61 +1264,54 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
         ch %= nch;
         if (g >= ngroups) return;
         const int64_t jb = g * 8 * NF, ib = ch * 4 * KS;
-        const double* p = nullptr;
         if (LAYOUT == 0) {  // a column's 4 KS rows: one line (or two) per column, a lane per column
-            for (int c = lane; c < 8 * NF; c += 32)
-                if (jb + c < N && ib < k) {
-                    p = A.W + ib + (jb + c) * ld;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-                }
-        } else {  // a row's 8 NF columns: 16 columns per line
-            constexpr int LPR = (8 * NF) / 16;  // lines per row
-            for (int e = lane; e < 4 * KS * LPR; e += 32) {
-                const int64_t i = ib + e / LPR, j = jb + 16 * (e % LPR);
-                if (i < k && j < N) {
-                    p = A.W + i * ld + j;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-                }
+            if (jb + lane < N && ib < k) {
+                const double* p = A.W + ib + (jb + lane) * ld;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            }
+        } else {  // a row's 32 columns: two lines per row
+            const int64_t i = ib + (lane >> 1), j = jb + 16 * (lane & 1);
+            if (i < k && j < N) {
+                const double* p = A.W + i * ld + j;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
             }
         }
     };
     const int64_t g_first = (int64_t)blockIdx.x * (kThreads / 32) + warp;
     for (int c = 0; c < pd; ++c) prefetch(g_first, c);
+    const bool kfull = k4 == k;
     for (int64_t g = g_first; g < ngroups; g += gstride) {
         const int64_t j0 = g * 8 * NF;
-        // the lanes' epilogue columns: loads issued before the k loop
-        int64_t pj[CL];
-        double nuj[CL], crefj[CL];
-#pragma unroll
-        for (int h = 0; h < CL; ++h) {
-            const int64_t j = j0 + 32 * h + lane;
-            pj[h] = j < N ? A.pos[j] : -1;
-            nuj[h] = j < N ? A.nu[j] : 0.0;
-            crefj[h] = j < N ? A.cref[j] : 0.0;
-        }
+        // the lane's own column in the epilogue (the butterfly's outcome): fragment column
+        // 8 (fr >> 1) + 2 fk + (fr & 1); its state is loaded before the k loop
+        const int64_t jl = j0 + 8 * (fr >> 1) + 2 * fk + (fr & 1);
+        const bool jin = jl < N;
+        const int64_t pjl = jin ? A.pos[jl] : -1;
+        double nul = jin ? A.nu[jl] : 0.0;
+        double crefl = jin ? A.cref[jl] : 0.0;
         double acc[MF][NF][2];
 #pragma unroll
         for (int f = 0; f < MF; ++f)
 #pragma unroll
             for (int n = 0; n < NF; ++n) acc[f][n][0] = acc[f][n][1] = 0.0;
-        int64_t colb[NF];
-        bool cok[NF];
-#pragma unroll
-        for (int n = 0; n < NF; ++n) {
-            colb[n] = j0 + 8 * n + fr;
-            cok[n] = colb[n] < N;
-        }
-        auto ldb = [&](int64_t i, int n) -> double {
-            if (i >= k || !cok[n]) return 0.0;
-            return LAYOUT == 0 ? __ldg(A.W + i + colb[n] * ld) : __ldg(A.W + i * ld + colb[n]);
-        };
+        const bool gfull = j0 + 8 * NF <= N;
+        // element (i, j0 + 8 n + fr): Col at cbase + 8 n ld + i, Row at rbase + i ld + 8 n
+        const double* cbase = A.W + (j0 + fr) * ld + fk;
+        const double* rbase = A.W + fk * ld + j0 + fr;
         for (int64_t i0 = 0; i0 < k4; i0 += 4 * KS) {  // rows past k load as zero
             if (pd > 0) prefetch(g, i0 / (4 * KS) + pd);
             double b[KS][NF];
 #pragma unroll
-            for (int s = 0; s < KS; ++s)
+            for (int s = 0; s < KS; ++s) {
+                const int64_t i = i0 + 4 * s;  // this lane's row is i + fk
+                const bool rok = kfull ? i < k4 : i + fk < k;
 #pragma unroll
-                for (int n = 0; n < NF; ++n) b[s][n] = ldb(i0 + 4 * s + fk, n);
+                for (int n = 0; n < NF; ++n) {
+                    const bool ok = rok && (gfull || j0 + 8 * n + fr < N);
+                    const double* p = LAYOUT == 0 ? cbase + (int64_t)(8 * n) * ld + i : rbase + i * ld + 8 * n;
+                    b[s][n] = ok ? __ldg(p) : 0.0;
+                }
+            }
 #pragma unroll
             for (int s = 0; s < KS; ++s) {
                 if (i0 + 4 * s >= k4) break;  // warp-uniform
@@ -1331,62 +1325,93 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
             }
         }
         // D fragment: lane holds rows 8 f + fr, columns j0 + 8 n + 2 fk + {0, 1}
+        double sq[2 * NF];
 #pragma unroll
-        for (int h = 0; h < CL; ++h) {
-            const int64_t j = j0 + 32 * h + lane;
+        for (int v = 0; v < 2 * NF; ++v) sq[v] = 0.0;
 #pragma unroll
-            for (int f = 0; f < MF; ++f) {
-                if (8 * f >= nb) break;  // warp-uniform
-                __syncwarp();
+        for (int f = 0; f < MF; ++f) {
+            const int row = 8 * f + fr;
+            if (row < nb) {
+                double* rp = A.R + (s0 + row) * N + j0 + 2 * fk;
 #pragma unroll
-                for (int n = 0; n < 4; ++n)
-                    *reinterpret_cast<double2*>(stg + fr * 40 + 8 * n + 2 * fk) =
-                        make_double2(acc[f][4 * h + n][0], acc[f][4 * h + n][1]);
-                __syncwarp();
-                for (int r = 0; r < 8 && 8 * f + r < nb; ++r) {
-                    const int64_t s = s0 + 8 * f + r;
-                    const double rv = stg[r * 40 + lane];
-                    bool need = false;
-                    double nv = 0.0;
-                    if (j < N) {
-                        if (pj[h] < t1 && s >= pj[h]) {
-                            A.R[s * N + j] = s == pj[h] ? A.diag[s] : 0.0;
-                        } else {
-                            A.R[s * N + j] = rv;
-                            if (pj[h] >= t1) {
-                                nv = __dsub_rn(nuj[h], __dmul_rn(rv, rv));
-                                need = nv < __dmul_rn(1e-16, crefj[h]) || nv < 0.0;
-                                if (!need) nuj[h] = nv;
-                            }
-                        }
+                for (int n = 0; n < NF; ++n) {
+                    const double r0 = acc[f][n][0], r1 = acc[f][n][1];
+                    if (gfull && (N & 1) == 0) {
+                        *reinterpret_cast<double2*>(rp + 8 * n) = make_double2(r0, r1);
+                    } else {
+                        if (j0 + 8 * n + 2 * fk < N) rp[8 * n] = r0;
+                        if (j0 + 8 * n + 2 * fk + 1 < N) rp[8 * n + 1] = r1;
                     }
-                    unsigned m = __ballot_sync(0xffffffffu, need);
-                    while (m) {  // guard recomputes, one flagged column at a time (all lanes)
-                        const int l = __ffs(m) - 1;
-                        m &= m - 1;
-                        const int64_t jl = __shfl_sync(0xffffffffu, j, l);
-                        const double v = lzw_resid(A.Q, (int)k, s, LAYOUT == 0 ? A.W + jl * ld : A.W + jl,
-                                                   LAYOUT == 0 ? 1 : ld);
-                        if (lane == l) nuj[h] = crefj[h] = v;
-                    }
+                    sq[2 * n] = fma(r0, r0, sq[2 * n]);
+                    sq[2 * n + 1] = fma(r1, r1, sq[2 * n + 1]);
                 }
             }
-            if (j < N && pj[h] >= t1) {
-                A.nu[j] = nuj[h];
-                A.cref[j] = crefj[h];
-                if (last) {
-                    const Cand c{nuj[h], pj[h], j};
-                    if (better(c, best)) best = c;
-                    msum += nuj[h];
+        }
+        // per-column totals over the eight fr lanes: halve the value set at every step
+        double tot;
+        {
+            const bool b2 = (fr & 4) != 0, b1 = (fr & 2) != 0, b0 = (fr & 1) != 0;
+            double a4[4], a2[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double send = b2 ? sq[i] : sq[i + 4], keep = b2 ? sq[i + 4] : sq[i];
+                a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double send = b1 ? a4[i] : a4[i + 2], keep = b1 ? a4[i + 2] : a4[i];
+                a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            const double send = b0 ? a2[0] : a2[1], keep = b0 ? a2[1] : a2[0];
+            tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        const bool live = jin && pjl >= t1;       // unpivoted through this pass
+        const bool pivoted = jin && pjl < t1;     // rows >= its position are the triangle's
+        double nv = __dsub_rn(nul, tot);
+        bool redo = live && (nv < __dmul_rn(1e-16, crefl) || nv < 0.0);
+        if (live && !redo) nul = nv;
+        unsigned m = __ballot_sync(0xffffffffu, redo || pivoted);
+        if (m) {
+            __syncwarp();  // the R rows stored above are read back / overwritten by other lanes
+            if (pivoted)
+                for (int64_t s = max(pjl, s0); s < s0 + nb; ++s) A.R[s * N + jl] = s == pjl ? A.diag[s] : 0.0;
+            m = __ballot_sync(0xffffffffu, redo);
+            while (m) {  // row by row for a column whose guard fires (all lanes, one column at a time)
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                const int64_t jc = __shfl_sync(0xffffffffu, jl, l);
+                double nuc = __shfl_sync(0xffffffffu, nul, l), crc = __shfl_sync(0xffffffffu, crefl, l);
+                for (int64_t s = s0; s < s0 + nb; ++s) {
+                    const double r = A.R[s * N + jc];
+                    const double x = __dsub_rn(nuc, __dmul_rn(r, r));
+                    if (x < __dmul_rn(1e-16, crc) || x < 0.0) {
+                        nuc = lzw_resid(A.Q, (int)k, s, LAYOUT == 0 ? A.W + jc * ld : A.W + jc, LAYOUT == 0 ? 1 : ld);
+                        crc = nuc;
+                    } else {
+                        nuc = x;
+                    }
                 }
+                if (lane == l) {
+                    nul = nuc;
+                    crefl = crc;
+                }
+            }
+        }
+        if (live) {
+            A.nu[jl] = nul;
+            A.cref[jl] = crefl;
+            if (last) {
+                const Cand c{nul, pjl, jl};
+                if (better(c, best)) best = c;
+                msum += nul;
             }
         }
     }
 }
 
-template <int LAYOUT, int NF>
+template <int LAYOUT>
 __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64_t t1, int force, int mfcap, int pd) {
-    extern __shared__ __align__(16) double wsm[];  // staging tiles (one per warp) | Q^T rows (8 mfcap x kq)
+    extern __shared__ __align__(16) double am[];  // Q^T rows (8 mfcap x kq)
     __shared__ Cand sc[kThreads / 32];
     __shared__ double sdm[kThreads / 32];
     if (!force && A.st[0] == 0) return;
@@ -1394,8 +1419,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
     const int nq = (int)(t1 - t0);
     const int64_t k4 = (k + 3) & ~int64_t(3);
     const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
-    double* stg = wsm + (threadIdx.x >> 5) * kLzwStage;
-    double* am = wsm + (kThreads / 32) * kLzwStage;
     Cand best = cand_none();
     double msum = 0.0;
     if (nq <= 0) {  // nothing to replay: the slots from the current norms
@@ -1419,10 +1442,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
         }
         __syncthreads();
         const bool last = sb + nb >= nq;
-        if (mf == 1) lzw_mma_sweep<LAYOUT, 1, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
-        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
-        else lzw_mma_sweep<LAYOUT, 3, NF>(A, t1, t0 + sb, nb, last, pd, am, kq, stg, best, msum);
         // (a lane meets the same columns in every sweep: it reads back its own norm writes)
+        if (mf == 1) lzw_mma_sweep<LAYOUT, 1>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else lzw_mma_sweep<LAYOUT, 3>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sdm);
@@ -4031,8 +4054,7 @@ LzArgs WideQrcp::lz_args() {
 int WideQrcp::lz_tails() {
     static const int tails = [] {
         const char* e = std::getenv("TTG_LZ_TAILS");
-        return e ? std::atoi(e) & 7 : 5;  // the final choice stays its own launch: as a tail of
-                                          // the gather it broke parity on the B200 (unexplained)
+        return e ? std::atoi(e) & 7 : 7;
     }();
     return tails;
 }
@@ -4107,8 +4129,8 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
             mfcap = std::max(1, std::min(mfcap, std::atoi(e)));
         const int64_t k4 = (k_ + 3) & ~int64_t(3);
         const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
-        const size_t smem = sizeof(double) * (size_t)((kThreads / 32) * kLzwStage + 8 * mfcap * kq);
-        auto kern = layout_ == Layout::Col ? k_lzw_refresh_mma<0, 4> : k_lzw_refresh_mma<1, 4>;
+        const size_t smem = sizeof(double) * (size_t)(8 * mfcap * kq);
+        auto kern = layout_ == Layout::Col ? k_lzw_refresh_mma<0> : k_lzw_refresh_mma<1>;
         allow_smem(kern, smem);
         int per_sm = 0;
         TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
