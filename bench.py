@@ -577,7 +577,8 @@ def run_ours(args):
                          "note": ("hbm_gbs is a read+write copy rate; a read-dominated stream can exceed it; "
                                   "traffic = ncu DRAM bytes of one launch of this kernel (profiles/traffic.json)"),
                          "frac_vs_ncu_dram_peak": achieved / ncu_peak if ncu_peak else None,
-                         "traffic": traffic, "phases": phases, "launches": dom["launches"], "kernel_ms": dom["ms"],
+                         "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                         "traffic_detail": traffic, "phases": phases, "launches": dom["launches"], "kernel_ms": dom["ms"],
                          "share_of_step": dom["ms"] / ms if ms > 0 else None,
                          "stream_family": {"achieved": achieved_family, "frac": achieved_family / peak if peak else None,
                                            "launches": nk, "kernel_ms": kern_ms,

@@ -1186,17 +1186,18 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
 // round differently, which only matters for near-ties no rounding order resolves the
 // reference's way anyway: exactly equal columns are members together or not at all, so they
 // always see the same arithmetic and tie to the lowest position.
-constexpr int kLzWK = 512;           // largest k
-constexpr int kLzWM = kLzWK / 32;    // rows per lane
+constexpr int kLzWK = 1024;          // largest k
+constexpr int kLzWM = kLzWK / 32;    // rows per lane (guard recomputes; the member update takes 16 for k <= 512)
 constexpr int64_t kLzCapW = 16384;
 
 // Guard recompute |w - Q[:, :s+1] Q[:, :s+1]^T w|^2, modified Gram-Schmidt, warp-cooperative.
-__device__ __noinline__ double lzw_resid(const double* __restrict__ Q, int k, int64_t s, const double* wp,
+template <int KM>
+__device__ __noinline__ double lzw_resid_km(const double* __restrict__ Q, int k, int64_t s, const double* wp,
                                          int64_t stride) {
     const int lane = threadIdx.x & 31;
-    double x[kLzWM];
+    double x[KM];
 #pragma unroll
-    for (int m = 0; m < kLzWM; ++m) {
+    for (int m = 0; m < KM; ++m) {
         const int i = lane + 32 * m;
         x[m] = i < k ? wp[(int64_t)i * stride] : 0.0;
     }
@@ -1204,29 +1205,37 @@ __device__ __noinline__ double lzw_resid(const double* __restrict__ Q, int k, in
         const double* q = Q + l * k;
         double z = 0.0;
 #pragma unroll
-        for (int m = 0; m < kLzWM; ++m) {
+        for (int m = 0; m < KM; ++m) {
             const int i = lane + 32 * m;
             if (i < k) z = fma(q[i], x[m], z);
         }
         z = warp_sum(z);
 #pragma unroll
-        for (int m = 0; m < kLzWM; ++m) {
+        for (int m = 0; m < KM; ++m) {
             const int i = lane + 32 * m;
             if (i < k) x[m] = fma(-q[i], z, x[m]);
         }
     }
     double sq = 0.0;
 #pragma unroll
-    for (int m = 0; m < kLzWM; ++m) sq = fma(x[m], x[m], sq);
+    for (int m = 0; m < KM; ++m) sq = fma(x[m], x[m], sq);
     return warp_sum(sq);
 }
 
+// (16 rows per lane cover k <= 512, 32 rows k <= 1024: two out-of-line bodies, so the callers of
+// the common width do not carry the wider one's registers)
+__device__ __forceinline__ double lzw_resid(const double* __restrict__ Q, int k, int64_t s, const double* wp,
+                                            int64_t stride) {
+    return k <= 512 ? lzw_resid_km<16>(Q, k, s, wp, stride) : lzw_resid_km<32>(Q, k, s, wp, stride);
+}
+
 // Downdate + guard for one column (all lanes; nu / cref valid in every lane).
+template <int KM>
 __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double r, const double* wp, int64_t stride,
                                              double& nuj, double& crefj) {
     const double nv = __dsub_rn(nuj, __dmul_rn(r, r));
     if (nv < __dmul_rn(1e-16, crefj) || nv < 0.0) {  // warp-uniform (r and nu are)
-        nuj = lzw_resid(A.Q, (int)A.k, s, wp, stride);
+        nuj = lzw_resid_km<KM>(A.Q, (int)A.k, s, wp, stride);
         crefj = nuj;
     } else {
         nuj = nv;
@@ -1245,7 +1254,7 @@ __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double 
 // (factor.cpp:101-106) can only fire in a sweep whose last row fires it; such a column (rare)
 // is redone row by row from the stored R rows, with warp-cooperative recomputes (lzw_resid).
 // Pivoted columns (at most t1 of them) get their rows >= their position fixed up afterwards.
-template <int LAYOUT, int MF>
+template <int LAYOUT, int MF, int NT>
 __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64_t s0, int nb, bool last, int pd,
                                               const double* am, int64_t kq, Cand& best, double& msum) {
     constexpr int NF = 4;
@@ -1257,8 +1266,10 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
     constexpr int KS = 16 / NF;  // k steps of 4 rows per chunk: 16 loads in flight per lane
     // L2 prefetch `pd` chunks ahead of the demand loads (a chunk = 4 KS rows x 32 columns of
     // this warp's groups, in the order it visits them)
-    const int64_t gstride = (int64_t)gridDim.x * (kThreads / 32);
+    const int64_t gstride = (int64_t)gridDim.x * (NT / 32);
     const int64_t nch = cdiv(k4, 4 * KS);  // chunks per group
+    // (the division per call measured faster than carrying the (group, chunk) position in
+    // registers: the kernel sits at its 128-register cap)
     auto prefetch = [&](int64_t g, int64_t ch) {
         g += (ch / nch) * gstride;
         ch %= nch;
@@ -1277,7 +1288,7 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
             }
         }
     };
-    const int64_t g_first = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+    const int64_t g_first = (int64_t)blockIdx.x * (NT / 32) + warp;
     for (int c = 0; c < pd; ++c) prefetch(g_first, c);
     const bool kfull = k4 == k;
     for (int64_t g = g_first; g < ngroups; g += gstride) {
@@ -1409,11 +1420,13 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
     }
 }
 
-template <int LAYOUT>
-__global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64_t t1, int force, int mfcap, int pd) {
+// NT threads per CTA: 256 (two CTAs per SM) or, when Q^T's rows leave room for one CTA only
+// (k > 512 at 24 rows), 512.
+template <int LAYOUT, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_lzw_refresh_mma(LzArgs A, int64_t t1, int force, int mfcap, int pd) {
     extern __shared__ __align__(16) double am[];  // Q^T rows (8 mfcap x kq)
-    __shared__ Cand sc[kThreads / 32];
-    __shared__ double sdm[kThreads / 32];
+    __shared__ Cand sc[NT / 32];
+    __shared__ double sdm[NT / 32];
     if (!force && A.st[0] == 0) return;
     const int64_t t0 = A.st[3], N = A.N, k = A.k;
     const int nq = (int)(t1 - t0);
@@ -1422,7 +1435,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
     Cand best = cand_none();
     double msum = 0.0;
     if (nq <= 0) {  // nothing to replay: the slots from the current norms
-        for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < N; j += (int64_t)gridDim.x * kThreads) {
+        for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < N; j += (int64_t)gridDim.x * NT) {
             const int64_t pj = A.pos[j];
             if (pj < t1) continue;
             const double v = A.nu[j];
@@ -1435,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
         const int nb = min(8 * mfcap, nq - sb);
         const int mf = (nb + 7) / 8;
         __syncthreads();
-        for (int64_t e = threadIdx.x; e < 8 * mf * kq; e += kThreads) {
+        for (int64_t e = threadIdx.x; e < 8 * mf * kq; e += NT) {
             const int r = (int)(e / kq);
             const int64_t i = e - (int64_t)r * kq;
             am[e] = (r < nb && i < k) ? A.Q[(t0 + sb + r) * k + i] : 0.0;
@@ -1443,9 +1456,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
         __syncthreads();
         const bool last = sb + nb >= nq;
         // (a lane meets the same columns in every sweep: it reads back its own norm writes)
-        if (mf == 1) lzw_mma_sweep<LAYOUT, 1>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
-        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
-        else lzw_mma_sweep<LAYOUT, 3>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        if (mf == 1) lzw_mma_sweep<LAYOUT, 1, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else lzw_mma_sweep<LAYOUT, 3, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sdm);
@@ -1454,7 +1467,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_lzw_refresh_mma(LzArgs A, int64
         A.mass[blockIdx.x] = msum;
     }
     if (blockIdx.x == 0)
-        for (int g = (int)gridDim.x + threadIdx.x; g < A.nslots; g += kThreads) {
+        for (int g = (int)gridDim.x + threadIdx.x; g < A.nslots; g += NT) {
             A.cand[g] = cand_none();
             A.mass[g] = 0.0;
         }
@@ -1481,13 +1494,14 @@ __global__ void __launch_bounds__(kThreads) k_lzw_copy(LzArgs A, int64_t t) {
 // lanes' registers (rows lane, lane + 32, ... like the member's), every load of a member in
 // flight together; per-CTA best member. The dot: the lanes' partial sums in row order, then
 // the warp_sum tree.
-__global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
+template <int KM>
+__global__ void __launch_bounds__(kThreads, KM == 16 ? 2 : 1) k_lzw_update(LzArgs A, int64_t t) {
     __shared__ Cand sc[kThreads / 32];
     if (A.st[1]) return;
     const int k = (int)A.k, lane = threadIdx.x & 31;
-    double q[kLzWM];
+    double q[KM];
 #pragma unroll
-    for (int m = 0; m < kLzWM; ++m) {
+    for (int m = 0; m < KM; ++m) {
         const int i = lane + 32 * m;
         q[m] = i < k ? A.Q[t * k + i] : 0.0;
     }
@@ -1497,9 +1511,9 @@ __global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
     for (int64_t c = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; c < cnt;
          c += ((int64_t)gridDim.x * kThreads) >> 5) {
         const double* wp = A.wc + c * k;
-        double w[kLzWM];
+        double w[KM];
 #pragma unroll
-        for (int m = 0; m < kLzWM; ++m) {
+        for (int m = 0; m < KM; ++m) {
             const int i = lane + 32 * m;
             w[m] = i < k ? wp[i] : 0.0;
         }
@@ -1515,9 +1529,9 @@ __global__ void __launch_bounds__(kThreads) k_lzw_update(LzArgs A, int64_t t) {
         }
         double a = 0.0;
 #pragma unroll
-        for (int m = 0; m < kLzWM; ++m) a = fma(q[m], w[m], a);  // zero past k
+        for (int m = 0; m < KM; ++m) a = fma(q[m], w[m], a);  // zero past k
         const double r = warp_sum(a);
-        lzw_downdate(A, t, r, wp, 1, nuj, crefj);
+        lzw_downdate<KM>(A, t, r, wp, 1, nuj, crefj);
         if (lane == 0) {
             A.nuc[c] = nuj;
             A.crefc[c] = crefj;
@@ -4068,9 +4082,12 @@ int64_t WideQrcp::lz_buf() const {
     }();
     static const int64_t cap_w = [] {
         const char* e = std::getenv("TTG_LZW_CAP");
-        return e ? std::max<int64_t>(1024, std::atoll(e)) : kLzCapW;
+        return e ? std::max<int64_t>(1024, std::atoll(e)) : (int64_t)0;
     }();
-    return 2 * (lzw_ ? cap_w : cap_n);
+    // wide: 16,384 members up to k = 512, 4,096 beyond (config 5, k = 1024: 55.6 ms per step at
+    // 4,096, 57.4 at 2,048, 59.3 at 8,192, 64.8 at 16,384: the members' copy is read every step)
+    const int64_t by_k = k_ <= 512 ? kLzCapW : 4096;
+    return 2 * (lzw_ ? (cap_w ? cap_w : by_k) : cap_n);
 }
 
 // per-CTA records of the member update: a thread per member (narrow), a warp per member (wide)
@@ -4107,7 +4124,8 @@ void WideQrcp::lz_step(int64_t t) {
     }
     PhaseTimer pt("p1 lazy update");
     if (lzw_) {
-        TTG_LAUNCH(k_lzw_update, lz_nubest(), kThreads, 0, stream(), lz_args(), t);
+        auto uk = k_ <= 512 ? k_lzw_update<16> : k_lzw_update<32>;
+        TTG_LAUNCH(uk, lz_nubest(), kThreads, 0, stream(), lz_args(), t);
         return;
     }
     auto uk = k_ <= 8 ? k_lz_update<8> : k_ <= 16 ? k_lz_update<16> : k_ <= 24 ? k_lz_update<24> : k_lz_update<32>;
@@ -4130,16 +4148,23 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
         const int64_t k4 = (k_ + 3) & ~int64_t(3);
         const int64_t kq = k4 + ((4 - (k4 & 15)) & 15);
         const size_t smem = sizeof(double) * (size_t)(8 * mfcap * kq);
-        auto kern = layout_ == Layout::Col ? k_lzw_refresh_mma<0> : k_lzw_refresh_mma<1>;
+        // one CTA per SM only (Q^T's rows fill the shared memory): 512 threads instead of 256
+        const bool big = smem > 110 * 1024;
+        const int nt = big ? 512 : kThreads;
+        auto kern = layout_ == Layout::Col ? (big ? k_lzw_refresh_mma<0, 512> : k_lzw_refresh_mma<0, kThreads>)
+                                           : (big ? k_lzw_refresh_mma<1, 512> : k_lzw_refresh_mma<1, kThreads>);
         allow_smem(kern, smem);
         int per_sm = 0;
-        TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+        TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
         prof_begin();
-        static const int pd = [] {  // L2 prefetch distance in chunks (experiment: TTG_LZ_PD)
+        // L2 prefetch distance in chunks: two for narrow W (+5% on config 3's first cuts), none
+        // for wide W (k = 480: no gain; k = 1024 row layout: 2.4 ms per pass without, 3.0 with)
+        static const int pd_env = [] {  // experiment: TTG_LZ_PD
             const char* e = std::getenv("TTG_LZ_PD");
-            return e ? std::max(0, std::atoi(e)) : 2;
+            return e ? std::max(0, std::atoi(e)) : -1;
         }();
-        TTG_LAUNCH(kern, std::min(ncand_ + ngc_, std::max(1, per_sm) * sms_), kThreads, smem, stream(), A, t1,
+        const int pd = pd_env >= 0 ? pd_env : (lzw_ ? 0 : 2);
+        TTG_LAUNCH(kern, std::min(ncand_ + ngc_, std::max(1, per_sm) * sms_), nt, smem, stream(), A, t1,
                    force ? 1 : 0, mfcap, pd);
         // algorithmic bytes: W once, norms / positions read and written; the replayed R rows
         // (8 N each) are counted on the run's last (forced) pass, where their total is known

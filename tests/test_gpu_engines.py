@@ -4,6 +4,8 @@ subprocess with the switch that forces them, against the same reference checks:
                            only for square in-place problems >= 2048)
   TTG_TALL_ENGINE=steps    the per-step in-place kernels everywhere
   TTG_LAZY=0               plain per-step streams instead of candidate pivoting (narrow W)
+  TTG_LAZY_WIDE=0          the subspace engine instead of candidate pivoting on 32 < k <= 1024 (it is
+                           the default only for 1024 < k <= 2048)
 """
 import os
 import subprocess
@@ -34,3 +36,7 @@ def test_per_step_inplace_engine():
 
 def test_plain_streams_without_candidate_pivoting():
     _run({"TTG_LAZY": "0"}, ["tests/test_gpu_lazy.py", "-k", "planted"])
+
+
+def test_subspace_engine_on_wide_cuts():
+    _run({"TTG_LAZY_WIDE": "0"}, ["tests/test_gpu_lazy.py", "-k", "wide_second_cut"])
