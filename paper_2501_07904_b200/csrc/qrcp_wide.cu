@@ -1222,13 +1222,6 @@ __device__ __noinline__ double lzw_resid_km(const double* __restrict__ Q, int k,
     return warp_sum(sq);
 }
 
-// (16 rows per lane cover k <= 512, 32 rows k <= 1024: two out-of-line bodies, so the callers of
-// the common width do not carry the wider one's registers)
-__device__ __forceinline__ double lzw_resid(const double* __restrict__ Q, int k, int64_t s, const double* wp,
-                                            int64_t stride) {
-    return k <= 512 ? lzw_resid_km<16>(Q, k, s, wp, stride) : lzw_resid_km<32>(Q, k, s, wp, stride);
-}
-
 // Downdate + guard for one column (all lanes; nu / cref valid in every lane).
 template <int KM>
 __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double r, const double* wp, int64_t stride,
@@ -1254,7 +1247,7 @@ __device__ __forceinline__ void lzw_downdate(const LzArgs& A, int64_t s, double 
 // (factor.cpp:101-106) can only fire in a sweep whose last row fires it; such a column (rare)
 // is redone row by row from the stored R rows, with warp-cooperative recomputes (lzw_resid).
 // Pivoted columns (at most t1 of them) get their rows >= their position fixed up afterwards.
-template <int LAYOUT, int MF, int NT>
+template <int LAYOUT, int MF, int NT, int KM>
 __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64_t s0, int nb, bool last, int pd,
                                               const double* am, int64_t kq, Cand& best, double& msum) {
     constexpr int NF = 4;
@@ -1396,7 +1389,7 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
                     const double r = A.R[s * N + jc];
                     const double x = __dsub_rn(nuc, __dmul_rn(r, r));
                     if (x < __dmul_rn(1e-16, crc) || x < 0.0) {
-                        nuc = lzw_resid(A.Q, (int)k, s, LAYOUT == 0 ? A.W + jc * ld : A.W + jc, LAYOUT == 0 ? 1 : ld);
+                        nuc = lzw_resid_km<KM>(A.Q, (int)k, s, LAYOUT == 0 ? A.W + jc * ld : A.W + jc, LAYOUT == 0 ? 1 : ld);
                         crc = nuc;
                     } else {
                         nuc = x;
@@ -1421,8 +1414,9 @@ __device__ __forceinline__ void lzw_mma_sweep(const LzArgs& A, int64_t t1, int64
 }
 
 // NT threads per CTA: 256 (two CTAs per SM) or, when Q^T's rows leave room for one CTA only
-// (k > 512 at 24 rows), 512.
-template <int LAYOUT, int NT>
+// (k > 512 at 24 rows), 512. KM: rows per lane of the guard recompute (16: k <= 512, 32: k <= 1024;
+// the narrower body keeps the common widths' kernels free of the wider one's frame).
+template <int LAYOUT, int NT, int KM>
 __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_lzw_refresh_mma(LzArgs A, int64_t t1, int force, int mfcap, int pd) {
     extern __shared__ __align__(16) double am[];  // Q^T rows (8 mfcap x kq)
     __shared__ Cand sc[NT / 32];
@@ -1456,9 +1450,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_lzw_refresh_mma(LzArg
         __syncthreads();
         const bool last = sb + nb >= nq;
         // (a lane meets the same columns in every sweep: it reads back its own norm writes)
-        if (mf == 1) lzw_mma_sweep<LAYOUT, 1, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
-        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
-        else lzw_mma_sweep<LAYOUT, 3, NT>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        if (mf == 1) lzw_mma_sweep<LAYOUT, 1, NT, KM>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else if (mf == 2) lzw_mma_sweep<LAYOUT, 2, NT, KM>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
+        else lzw_mma_sweep<LAYOUT, 3, NT, KM>(A, t1, t0 + sb, nb, last, pd, am, kq, best, msum);
     }
     best = block_best(best, sc);
     msum = block_sum(msum, sdm);
@@ -4057,7 +4051,7 @@ WideQrcp::WideQrcp(const double* W, int64_t k, int64_t N, int64_t ld, Layout lay
 }
 
 LzArgs WideQrcp::lz_args() {
-    return LzArgs{W_, k_, N_, ld_, Qt_.get(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
+    return LzArgs{W_, k_, N_, ld_, qptr(), diag_.get(), pos_.get(), R_.get(), nu_.get(), cref_.get(),
                   cand_.get(), mass_.get(), ncand_ + ngc_, lzst_.get(), lzsd_.get(), lzhist_.get(), lzidx_.get(),
                   lzwc_.get(), lznuc_.get(), lzcrefc_.get(), lzposc_.get(), lzubest_.get(), lz_nubest(), piv_.get(),
                   lz_buf() / 2, lz_buf(), lzw_ ? 1 : 0, lz_tails()};
@@ -4099,6 +4093,9 @@ int WideQrcp::lz_nubest() const {
 // One candidate-pivoting step (see k_lz_choose .. k_lz_update); the miss kernels return at
 // once on a hit (device-side decision, no host synchronisation).
 void WideQrcp::lz_step(int64_t t) {
+    // explicit Q for 512 <= k <= 2048 like step(): the compact-WY reflector's chunked path costs
+    // several times the k x k rank-1 update there (config 5's 1024-row cut)
+    if (!explicit_ && !comm_ && k_ >= 512 && k_ <= 2048) to_explicit(t);
     {
         PhaseTimer pt("p1 lazy choose + exact pass on a miss");
         LzArgs A = lz_args();
@@ -4119,8 +4116,9 @@ void WideQrcp::lz_step(int64_t t) {
         if (!(tails & 2)) TTG_LAUNCH(k_lz_choose<true>, 1, 1024, 0, stream(), A, t);
     }
     {
-        PhaseTimer pt("p1 reflector");
-        reflect_step(t);
+        PhaseTimer pt(explicit_ ? "p1 explicit reflector" : "p1 reflector");
+        if (explicit_) explicit_step(t);
+        else reflect_step(t);
     }
     PhaseTimer pt("p1 lazy update");
     if (lzw_) {
@@ -4151,8 +4149,10 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
         // one CTA per SM only (Q^T's rows fill the shared memory): 512 threads instead of 256
         const bool big = smem > 110 * 1024;
         const int nt = big ? 512 : kThreads;
-        auto kern = layout_ == Layout::Col ? (big ? k_lzw_refresh_mma<0, 512> : k_lzw_refresh_mma<0, kThreads>)
-                                           : (big ? k_lzw_refresh_mma<1, 512> : k_lzw_refresh_mma<1, kThreads>);
+        const bool km32 = k_ > 512;
+        auto kern = layout_ == Layout::Col
+                        ? (big ? k_lzw_refresh_mma<0, 512, 32> : km32 ? k_lzw_refresh_mma<0, kThreads, 32> : k_lzw_refresh_mma<0, kThreads, 16>)
+                        : (big ? k_lzw_refresh_mma<1, 512, 32> : km32 ? k_lzw_refresh_mma<1, kThreads, 32> : k_lzw_refresh_mma<1, kThreads, 16>);
         allow_smem(kern, smem);
         int per_sm = 0;
         TTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
