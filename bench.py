@@ -254,6 +254,8 @@ def ncu_traffic(cfg: int, kernel: str = ""):
             break
     if t is None:
         t = d.get(str(cfg))
+        if t is not None and t.get("kernel") and kernel and not kernel.startswith(t["kernel"]):
+            t = None  # that capture is of another kernel
     # the DRAM peak ncu implies is a property of the part, not of the config
     if t is not None and "implied_dram_peak_gbs_ncu" not in t:
         for v in d.values():

@@ -853,147 +853,8 @@ __device__ __forceinline__ bool lz_last_cta(int* ticket) {
     return last != 0;
 }
 
-// Step 2 (grid, on a miss or forced): rows t0..t1-1 of R for every column, norms brought to
-// step t1-1, candidate slots and masses (as the stream kernels leave them). Tiles of 256
-// columns stream through two shared-memory buffers with 8-byte cp.async (the next tile lands
-// while the current one is computed): Row W as tile[i * 258 + c], Col W as tile[c * (KK + 1)
-// + i] (odd stride: conflict-free column reads). A thread per column takes its KK values
-// into registers and replays the rows from them (q_s broadcast from shared memory).
-__device__ __forceinline__ void lz_cp8(double* smem, const double* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void lz_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void lz_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <int LAYOUT, int KK>
-constexpr int lz_tile_doubles() { return LAYOUT == 0 ? kThreads * (KK + 1) : KK * (kThreads + 2); }
-
-template <int LAYOUT, int KK>
-__global__ void __launch_bounds__(kThreads, 2) k_lz_refresh(LzArgs A, int64_t t1, int force) {
-    __shared__ double qs[kLzK * kLzK];
-    __shared__ Cand sc[kThreads / 32];
-    __shared__ double sdm[kThreads / 32];
-    extern __shared__ __align__(16) double tiles[];  // two buffers
-    if (!force && A.st[0] == 0) return;
-    const int64_t t0 = A.st[3], k = A.k, N = A.N;
-    const int64_t nq = t1 - t0;
-    for (int64_t e = threadIdx.x; e < k * nq; e += kThreads) qs[e] = A.Q[t0 * k + e];
-    constexpr int TD = lz_tile_doubles<LAYOUT, KK>();
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    // issue the copies of the tile at j0 into buffer b (element e = tid + u * 256 of the
-    // tile's k x nc values)
-    auto issue = [&](int64_t j0, int b) {
-        double* tb = tiles + b * TD;
-        const int nc = (int)min((int64_t)kThreads, N - j0);
-        if (LAYOUT == 0) {  // contiguous k x nc block, column-major (ld == k): flat e -> (e / k, e % k)
-            const int kk = (int)k, tot = kk * nc;
-            const int dq = kThreads / kk, dr = kThreads - dq * kk;
-            int c = threadIdx.x / kk, i = threadIdx.x - c * kk;
-            const double* src = A.W + j0 * k;
-            for (int e = threadIdx.x; e < tot; e += kThreads) {
-                lz_cp8(tb + c * (KK + 1) + i, src + e);
-                c += dq;
-                i += dr;
-                if (i >= kk) {
-                    i -= kk;
-                    ++c;
-                }
-            }
-        } else if ((int)threadIdx.x < nc) {  // row i of the tile: 256 contiguous doubles of W
-            const double* src = A.W + j0 + threadIdx.x;
-            for (int64_t i = 0; i < k; ++i) lz_cp8(tb + i * (kThreads + 2) + threadIdx.x, src + i * A.ld);
-        }
-        lz_cp_commit();
-    };
-    Cand best = cand_none();
-    double msum = 0.0;
-    int64_t j0 = (int64_t)blockIdx.x * kThreads;
-    int buf = 0;
-    if (nq > 0 && j0 < N) issue(j0, 0);
-    for (; j0 < N; j0 += stride) {
-        const int64_t j = j0 + threadIdx.x;
-        double w[KK];
-        if (nq > 0) {
-            if (j0 + stride < N) {
-                issue(j0 + stride, buf ^ 1);
-                lz_cp_wait<1>();
-            } else {
-                lz_cp_wait<0>();
-            }
-            __syncthreads();
-            const double* tb = tiles + buf * TD;
-#pragma unroll
-            for (int i = 0; i < KK; ++i)
-                w[i] = (k == KK || i < k) ? (LAYOUT == 0 ? tb[threadIdx.x * (KK + 1) + i] : tb[i * (kThreads + 2) + threadIdx.x])
-                                          : 0.0;
-        }
-        if (j < N) {
-            const int64_t pj = A.pos[j];
-            double nuj = A.nu[j], crefj = A.cref[j];
-            auto row = [&](int64_t s, double r) {
-                if (pj < t1 && s >= pj) {
-                    A.R[s * N + j] = s == pj ? A.diag[s] : 0.0;
-                    return;
-                }
-                A.R[s * N + j] = r;
-                if (pj >= t1)
-                    lz_downdate(A, s, r, LAYOUT == 0 ? A.W + j * A.ld : A.W + j, LAYOUT == 0 ? 1 : A.ld, nuj, crefj);
-            };
-            // four rows' dots at a time (independent chains; each row's own chain is the one
-            // k_lz_update uses), then their downdates in row order
-            int64_t s = t0;
-            for (; s + 4 <= t1; s += 4) {
-                const double* q = qs + (s - t0) * k;
-                double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-#pragma unroll
-                for (int i = 0; i < KK; ++i) {
-                    if (k == KK || i < k) {
-                        r0 = fma(q[i], w[i], r0);
-                        r1 = fma(q[k + i], w[i], r1);
-                        r2 = fma(q[2 * k + i], w[i], r2);
-                        r3 = fma(q[3 * k + i], w[i], r3);
-                    }
-                }
-                row(s, r0);
-                row(s + 1, r1);
-                row(s + 2, r2);
-                row(s + 3, r3);
-            }
-            for (; s < t1; ++s) {
-                const double* q = qs + (s - t0) * k;
-                double r = 0.0;
-#pragma unroll
-                for (int i = 0; i < KK; ++i)
-                    if (k == KK || i < k) r = fma(q[i], w[i], r);
-                row(s, r);
-            }
-            if (pj >= t1) {
-                if (nq > 0) {
-                    A.nu[j] = nuj;
-                    A.cref[j] = crefj;
-                }
-                const Cand c{nuj, pj, j};
-                if (better(c, best)) best = c;
-                msum += nuj;
-            }
-        }
-        if (nq > 0) __syncthreads();  // buffer `buf` is refilled two tiles later
-        buf ^= 1;
-    }
-    best = block_best(best, sc);
-    msum = block_sum(msum, sdm);
-    if (threadIdx.x == 0) {
-        A.cand[blockIdx.x] = best;
-        A.mass[blockIdx.x] = msum;
-    }
-    if (blockIdx.x == 0)  // slots past the grid hold nothing
-        for (int g = (int)gridDim.x + threadIdx.x; g < A.nslots; g += kThreads) {
-            A.cand[g] = cand_none();
-            A.mass[g] = 0.0;
-        }
-}
+// Step 2 (grid, on a miss or forced): the exact pass, k_lzw_refresh_mma below (rows t0..t1-1
+// of R for every column, norms brought to step t1-1, candidate slots and masses).
 
 // Step 3 (grid, on a miss): histogram of the unpivoted norms in 1/32-octave bins below the
 // largest one.
@@ -4132,11 +3993,7 @@ void WideQrcp::lz_step(int64_t t) {
 
 void WideQrcp::lz_refresh(int64_t t1, bool force) {
     LzArgs A = lz_args();
-    static const bool narrow_mma = [] {  // A/B: the narrow exact pass on DMMA too
-        const char* e = std::getenv("TTG_LZ_MMA");
-        return !(e && *e == '0');
-    }();
-    if (lzw_ || narrow_mma) {
+    {
         // rows per sweep over W: 8 mfcap covers every row the pass can have to replay (the
         // host knows the last forced pass; misses since then only shorten the replay)
         const int64_t nq_max = std::max<int64_t>(1, t1 - lz_host_exact_);
@@ -4169,7 +4026,7 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
         // algorithmic bytes: W once, norms / positions read and written; the replayed R rows
         // (8 N each) are counted on the run's last (forced) pass, where their total is known
         const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
-        const char* pass = lzw_ ? "k_lzw_refresh_mma, 32 < k <= 512 (exact pass over W on DMMA: replayed R rows, norms)"
+        const char* pass = lzw_ ? "k_lzw_refresh_mma, 32 < k <= 1024 (exact pass over W on DMMA: replayed R rows, norms)"
                                 : "k_lzw_refresh_mma, k <= 32 (exact pass over W on DMMA: replayed R rows, norms)";
         if (force) {
             prof_end(bytes + 8.0 * (double)N_ * (double)(t1 - lz_host_exact_), pass);
@@ -4180,31 +4037,6 @@ void WideQrcp::lz_refresh(int64_t t1, bool force) {
                             first ? "k_lzw_refresh_mma (no rows to replay: slots from the norms)" : pass, 0.0,
                             "k_lzw_refresh_mma (idle on a hit)");
         }
-        return;
-    }
-    const int kk = k_ <= 8 ? 8 : k_ <= 16 ? 16 : k_ <= 24 ? 24 : 32;
-    const size_t smem = sizeof(double) * 2 *
-                        (size_t)(layout_ == Layout::Col ? kThreads * (kk + 1) : kk * (kThreads + 2));  // two tiles
-    auto kern = layout_ == Layout::Col
-                    ? (k_ <= 8 ? k_lz_refresh<0, 8> : k_ <= 16 ? k_lz_refresh<0, 16> : k_ <= 24 ? k_lz_refresh<0, 24> : k_lz_refresh<0, 32>)
-                    : (k_ <= 8 ? k_lz_refresh<1, 8> : k_ <= 16 ? k_lz_refresh<1, 16> : k_ <= 24 ? k_lz_refresh<1, 24> : k_lz_refresh<1, 32>);
-    allow_smem(kern, smem);
-    prof_begin();
-    // two resident CTAs per SM (one tile each): one loads while the other computes
-    TTG_LAUNCH(kern, std::min(ncand_ + ngc_, 2 * sms_), kThreads, smem, stream(), A, t1, force ? 1 : 0);
-    // algorithmic bytes: W once, norms / positions read and written; the replayed R rows (8 N
-    // each) are counted on the run's last (forced) pass, where their total is known
-    const double bytes = 8.0 * (double)N_ * (double)(k_ + 5);
-    if (force) {
-        prof_end(bytes + 8.0 * (double)N_ * (double)(t1 - lz_host_exact_),
-                 "k_lz_refresh (exact pass over W: replayed R rows, norms)");
-        lz_host_exact_ = t1;
-    } else {
-        const bool first = t1 == lz_host_exact_;  // nothing to replay: slots from the norms only
-        prof_end_select(reinterpret_cast<const int*>(lzst_.get()), first ? 16.0 * (double)N_ : bytes,
-                        first ? "k_lz_refresh (no rows to replay: slots from the norms)"
-                              : "k_lz_refresh (exact pass over W: replayed R rows, norms)",
-                        0.0, "k_lz_refresh (idle on a hit)");
     }
 }
 

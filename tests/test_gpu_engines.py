@@ -4,6 +4,8 @@ subprocess with the switch that forces them, against the same reference checks:
                            only for square in-place problems >= 2048)
   TTG_TALL_ENGINE=steps    the per-step in-place kernels everywhere
   TTG_LAZY=0               plain per-step streams instead of candidate pivoting (narrow W)
+  TTG_LZ_TAILS=0           the candidate engine's threshold / final choice / next first choice as
+                           launches of their own instead of last-CTA tails of their predecessors
   TTG_LAZY_WIDE=0          the subspace engine instead of candidate pivoting on 32 < k <= 1024 (it is
                            the default only for 1024 < k <= 2048)
 """
@@ -40,3 +42,7 @@ def test_plain_streams_without_candidate_pivoting():
 
 def test_subspace_engine_on_wide_cuts():
     _run({"TTG_LAZY_WIDE": "0"}, ["tests/test_gpu_lazy.py", "-k", "wide_second_cut"])
+
+
+def test_candidate_engine_without_last_cta_tails():
+    _run({"TTG_LZ_TAILS": "0"}, ["tests/test_gpu_lazy.py", "-k", "planted or wide_second_cut"])
