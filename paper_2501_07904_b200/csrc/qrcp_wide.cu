@@ -724,7 +724,8 @@ __global__ void k_set_identity(double* Qx, int64_t k) {
 // ---------------------------------------------------------------------------
 constexpr int kLzK = 32;            // largest k
 constexpr int kLzBins = 512;        // 1/32-octave bins below the largest norm
-constexpr int64_t kLzCap = 65536;   // target |S|
+constexpr int64_t kLzCap = 32768;   // target |S| (config 3, ms per step: 19.8 at 16,384 (more passes), 18.85 at
+                                    // 32,768, 19.2 at 65,536, 19.6 at 131,072)
 
 }  // namespace
 
@@ -1049,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads) k_lz_update(LzArgs A, int64_t t) {
 // always see the same arithmetic and tie to the lowest position.
 constexpr int kLzWK = 1024;          // largest k
 constexpr int kLzWM = kLzWK / 32;    // rows per lane (guard recomputes; the member update takes 16 for k <= 512)
-constexpr int64_t kLzCapW = 16384;
+constexpr int64_t kLzCapW = 4096;
 
 // Guard recompute |w - Q[:, :s+1] Q[:, :s+1]^T w|^2, modified Gram-Schmidt, warp-cooperative.
 template <int KM>
@@ -3939,9 +3940,10 @@ int64_t WideQrcp::lz_buf() const {
         const char* e = std::getenv("TTG_LZW_CAP");
         return e ? std::max<int64_t>(1024, std::atoll(e)) : (int64_t)0;
     }();
-    // wide: 16,384 members up to k = 512, 4,096 beyond (config 5, k = 1024: 55.6 ms per step at
-    // 4,096, 57.4 at 2,048, 59.3 at 8,192, 64.8 at 16,384: the members' copy is read every step)
-    const int64_t by_k = k_ <= 512 ? kLzCapW : 4096;
+    // wide: 4,096 members (the members' copy is read every step; config 3, k = 480: 18.75 ms per
+    // step at 4,096, 18.8 at 8,192, 19.2 at 16,384; config 5, k = 1024: 55.6 at 4,096, 57.4 at
+    // 2,048, 59.3 at 8,192, 64.8 at 16,384)
+    const int64_t by_k = kLzCapW;
     return 2 * (lzw_ ? (cap_w ? cap_w : by_k) : cap_n);
 }
 

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Final check of the head: all GPU tests, smoke, headline bench line (with the CPU baseline), config 5.
-O=gpurun_out/ab23
+O=gpurun_out/ab25
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.txt 2>&1
 echo "pytest exit $?" >> $O/pytest_gpu.txt
